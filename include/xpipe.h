@@ -1,0 +1,219 @@
+/*
+ * xpipe.h -- C ABI of the B200-native XPipe hot path (libxpipe.so).
+ *
+ * XPipe (Guan, Yin, Li, Lu; arXiv 1911.04610; P:n = /root/reference/PAPER.md line n):
+ * an asynchronous micro-batch pipeline across K GPU stages (Sec. III-A) in which
+ * every stage runs its forward and backward passes under weights predicted by the
+ * mini-batch's bellwether (Sec. III-B):
+ *     W_hat = W - s * lr * m_hat / (sqrt(v_hat) + eps)            (Eq. (3), BJ north star)
+ * with the version difference s of Eq. (1) (forward) or Eq. (2) (backward,
+ * P:111-115), and Adam's own moments.  Gradients of the T micro-batches of a mini-batch are
+ * accumulated and applied when the T-th micro-batch finishes its backward by one
+ * fused Adam-update + prediction sweep that also materialises the next W_hat buffers.
+ *
+ * Conventions for every function:
+ *   - returns int: XP_OK (0) or a negative XP_E* code; no C++ exception crosses the ABI;
+ *   - pointers are host pointers unless the argument says "device";
+ *   - the library copies what it needs from its inputs before returning (nothing borrowed
+ *     is retained); outputs go to caller-owned buffers;
+ *   - a device or communication fault poisons the context: every later call except
+ *     xpipe_last_error and xpipe_finalize returns XP_ESTATE.
+ * Thread safety: one context must not be used from two threads at once.
+ */
+#ifndef XPIPE_H
+#define XPIPE_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes -------------------------------------------------------------------- */
+enum {
+  XP_OK = 0,
+  XP_EINVAL = -1,        /* invalid argument; detected before any device work */
+  XP_ENOMEM = -2,        /* device or host allocation failed */
+  XP_ECUDA = -3,         /* CUDA runtime/driver error (context poisoned) */
+  XP_ECOMM = -4,         /* stage-to-stage transport error (context poisoned) */
+  XP_ESCHED = -5,        /* schedule/cache violation or pipeline watchdog timeout (internal) */
+  XP_ENONFINITE = -6,    /* non-finite loss seen (only checked with cfg.trace) */
+  XP_ESTATE = -7,        /* context is poisoned */
+  XP_EUNSUPPORTED = -8   /* valid request this build does not implement */
+};
+
+/* ---- layer kinds (the DNN is partitioned layer-wise into stages) ----------- */
+enum { XP_LINEAR = 1, XP_CONV2D, XP_BATCHNORM2D, XP_RELU, XP_MAXPOOL2D, XP_AVGPOOL_GLOBAL,
+       XP_FLATTEN, XP_ADD, XP_CONCAT, XP_SOFTMAX_XENT };
+
+/* ---- configuration enums -------------------------------------------------------------- */
+enum { XP_FP32 = 0,   /* fp32 SIMT path, bit-exact with the oracle's fp32 contract */
+       XP_BF16 = 1 }; /* bf16 operands on tcgen05 tensor cores, fp32 master/moments/grads */
+enum { XP_SCHED_XPIPE = 0, XP_SCHED_GPIPE = 1 };
+enum { XP_PRED_PAPER = 0,  /* s from Eq. (1)/(2) */
+       XP_PRED_OFF = 1,    /* s = 0 (plain asynchronous pipeline / GPipe semantics) */
+       XP_PRED_FIXED = 2 };/* s = cfg.s_fwd / cfg.s_bwd */
+enum { XP_DELTA_ADAM = 0,  /* dW = lr * m_hat / (sqrt(v_hat) + eps)   (north star) */
+       XP_DELTA_PAPER = 1 };/* dW = lr * (m/(1-b1)) / sqrt(v/(1-b2) + eps)  (Eq. (3)-(4) literal) */
+enum { XP_MOM_ZERO = 0, XP_MOM_GIVEN = 1 /* cfg.init_m / cfg.init_v (e.g. 1e-4*U[0,1)) */ };
+enum { XP_TRANSPORT_P2P = 0 };  /* producer kernels store into the consumer's ring slot
+                                   (same device or NVLink peer); device-side flags order it */
+
+/* xpipe_step flags */
+enum { XP_FLUSH = 1,        /* drain the pipeline at the end of the call */
+       XP_DEVICE_PTRS = 2,  /* x and y are device pointers on stage 0's / stage K-1's device */
+       XP_ASYNC = 4 };      /* return after enqueue; the next call (or xpipe_sync) waits */
+
+/* xpipe_get_weights selectors */
+enum { XP_T_WEIGHT = 0, XP_T_BIAS = 1 };       /* BatchNorm: WEIGHT = gamma, BIAS = beta */
+enum { XP_S_PARAM = 0, XP_S_M = 1, XP_S_V = 2, XP_S_PRED_FWD = 3, XP_S_PRED_BWD = 4, XP_S_GRAD = 5 };
+
+/* One layer.  src0/src1: producer layer indices (-1 = the previous layer); a DAG edge may
+   not cross a stage cut except into the next stage's first layer.  stage: -1 = automatic
+   (layer-count rule of P:154-156: partition units begin at every Linear/Conv2d layer, the
+   remainder goes to the last stages); otherwise an explicit, contiguous stage id. */
+typedef struct {
+  int32_t kind, in_c, out_c, kh, kw, sh, sw, ph, pw, bias;
+  float bn_eps;
+  int32_t src0, src1;
+  int32_t concat_off;
+  int32_t stage;
+} xpipe_layer;
+
+/* optional device-memory hooks (the Python binding routes them to PyTorch's allocator) */
+typedef void* (*xpipe_alloc_fn)(size_t bytes, int32_t device, void* user);
+typedef void (*xpipe_free_fn)(void* ptr, size_t bytes, int32_t device, void* user);
+
+/* Zero-initialised = defaults. */
+typedef struct {
+  int32_t in_c, in_h, in_w, classes;  /* network input [C,H,W] and number of classes (required) */
+  uint64_t seed;                      /* weight init when init_params is NULL (default 1) */
+  int32_t precision;                  /* XP_FP32 | XP_BF16 */
+  int32_t schedule;                   /* XP_SCHED_XPIPE | XP_SCHED_GPIPE */
+  int32_t predict;                    /* XP_PRED_* */
+  int32_t s_fwd, s_bwd;               /* with XP_PRED_FIXED */
+  int32_t delta_form;                 /* XP_DELTA_ADAM | XP_DELTA_PAPER */
+  int32_t moment_init;                /* XP_MOM_ZERO | XP_MOM_GIVEN (requires XP_DELTA_PAPER) */
+  int32_t n_devices;                  /* stage k runs on devices[k % n_devices]; 0 = current device */
+  int32_t devices[8];
+  int32_t transport;                  /* XP_TRANSPORT_P2P */
+  int32_t snapshots;                  /* keep W after every version for get_weights(version=v) */
+  int32_t trace;                      /* record per-op device trace (K12); disables graphs */
+  int32_t graphs;                     /* capture repeated step calls as CUDA graphs */
+  int32_t profile;                    /* record CUDA events around every sweep launch */
+  int32_t watchdog_ms;                /* xpipe_step timeout (0 = 120000) */
+  /* optional initial tensors, float32, PyTorch layout, [2*layer + XP_T_*]; NULL = seeded init */
+  const float* const* init_params;
+  const float* const* init_m;         /* with XP_MOM_GIVEN, same indexing */
+  const float* const* init_v;
+  xpipe_alloc_fn alloc;               /* NULL = cudaMalloc / cudaFree */
+  xpipe_free_fn free;
+  void* alloc_user;
+} xpipe_config;
+
+/* one device-trace record (K12): op 0 = forward, 1 = backward, 2 = update.  version is the
+   weight version the op ran under (update: the version it produced), s the version
+   difference used, wbuf the W_hat buffer (forward: version & 1).  t0/t1: %globaltimer ns. */
+typedef struct {
+  int32_t stage, op, t, j, version, s, bellwether, wbuf;
+  uint64_t t0_ns, t1_ns;
+} xpipe_trace_rec;
+
+/* kernel classes timed with CUDA events on the launching stream when cfg.profile != 0 */
+enum { XP_PROF_SWEEP = 0,       /* K1: work = algorithmic bytes */
+       XP_PROF_CONV_FPROP = 1,  /* tcgen05 implicit-GEMM conv forward: work = 2*M*N*K flops */
+       XP_PROF_CONV_DGRAD = 2,
+       XP_PROF_CONV_WGRAD = 3,
+       XP_PROF_N = 4 };
+
+typedef struct {
+  double span_ms;                    /* reserved */
+  double prof_ms[XP_PROF_N];         /* summed device time per kernel class (cfg.profile) */
+  int64_t prof_launches[XP_PROF_N];
+  double prof_work[XP_PROF_N];       /* algorithmic bytes (sweep) or flops (GEMM classes) */
+  int64_t kernel_launches;           /* kernels enqueued by this call */
+  float* losses;                     /* optional caller buffer of M*T per-micro-batch mean losses */
+} xpipe_stats;
+
+/* Build the pipeline.  layers/n_layers: the network, last layer XP_SOFTMAX_XENT;
+   stages = K; micro_batches = T; mini_batch = N (N % T == 0); lr > 0; betas in [0,1);
+   eps > 0 (defaults of P:168: 0.9, 0.999, 1e-8).  cfg may be NULL only if the input
+   shape can be inferred (it cannot: pass cfg).  Allocates every device buffer, writes the
+   initial weights and version-0 predictions (W_hat = W).  All-or-nothing: on failure
+   *out = NULL and nothing stays allocated.  Errors: XP_EINVAL (shapes, partition,
+   hyperparameters, unsupported DAG), XP_EUNSUPPORTED, XP_ENOMEM, XP_ECUDA. */
+int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int32_t micro_batches,
+               int32_t mini_batch, float lr, const float betas[2], float eps,
+               const xpipe_config* cfg, struct xpipe_ctx** out);
+
+/* Feed n_minibatches mini-batches into the running pipeline and execute every op whose
+   inputs exist.  x: [M*N, C, H, W] fp32 NCHW (stage 0 reads it);
+   y: [M*N] int32 labels in [0, classes) (the last stage reads them).  Host pointers
+   unless XP_DEVICE_PTRS.  With XP_FLUSH the pipeline drains: afterwards every stage's
+   version equals the number of mini-batches fed.  Splitting a sequence of mini-batches
+   across calls (flush only at the end) gives bit-identical weights and traces.
+   Errors: XP_EINVAL (labels out of range are not checked on device pointers), XP_ECUDA,
+   XP_ESCHED (watchdog), XP_ENONFINITE (with cfg.trace). */
+int xpipe_step(struct xpipe_ctx* h, const float* x, const int32_t* y, int32_t n_minibatches,
+               uint32_t flags, xpipe_stats* st);
+
+/* Wait for all enqueued work (after XP_ASYNC). */
+int xpipe_sync(struct xpipe_ctx* h);
+
+/* Copy one parameter tensor (or its moment / prediction / gradient state) to dst as fp32
+   in PyTorch layout.  count must equal the tensor size (else XP_EINVAL).  version: -1 =
+   latest; otherwise a snapshot (cfg.snapshots, XP_S_PARAM only).  PRED_FWD returns the
+   W_hat_f buffer of the latest version, PRED_BWD the W_hat_b buffer (bf16 values widened
+   exactly in XP_BF16). */
+int xpipe_get_weights(struct xpipe_ctx* h, int32_t layer, int32_t tensor, int32_t state,
+                      int64_t version, float* dst, size_t count);
+
+/* Number of trace records of a stage (*n_out) and up to cap of them (dst may be NULL). */
+int xpipe_get_trace(struct xpipe_ctx* h, int32_t stage, xpipe_trace_rec* dst, size_t cap,
+                    size_t* n_out);
+
+/* Introspection: stage of a layer; current version of a stage (host mirror of the device
+   counter); parameters of a stage (arena elements incl. alignment padding). */
+int xpipe_stage_of_layer(struct xpipe_ctx* h, int32_t layer);
+int xpipe_stage_version(struct xpipe_ctx* h, int32_t stage);
+int64_t xpipe_stage_params(struct xpipe_ctx* h, int32_t stage);
+
+/* NULL-safe, idempotent; frees everything the context owns. */
+int xpipe_finalize(struct xpipe_ctx* h);
+
+/* Last error message of h (h == NULL: this thread's last init error). Never NULL. */
+const char* xpipe_last_error(const struct xpipe_ctx* h);
+
+/* ---- kernel-level entry points (config 5 and unit parity) ----------------------------- */
+
+/* K1, the fused Adam-update + weight-prediction sweep over n fp32 parameters (device
+   pointers, 16-byte aligned).  Reads W, g, m, v once; writes W, m, v (in place) and
+   W_hat_f = W' - s_f*d, W_hat_b = W' - s_b*d (either may be NULL) as fp32
+   (pred_bf16 = 0) or bf16 (pred_bf16 = 1, round-to-nearest-even), where
+   d = (c1*m')/(sqrt(v')*r2 + eps), c1 = lr/(1-b1^k), r2 = 1/sqrt(1-b2^k), k = version >= 1,
+   beta^k by k repeated double multiplications.  stream: cudaStream_t
+   (NULL = legacy default).  Asynchronous; errors: XP_EINVAL, XP_ECUDA (launch). */
+int xpipe_adam_predict(float* W, const float* g, float* m, float* v, void* pred_f, void* pred_b,
+                       int64_t n, int64_t version, float lr, float beta1, float beta2, float eps,
+                       int32_t s_f, int32_t s_b, int32_t pred_bf16, int32_t delta_form, void* stream);
+
+/* bf16 tensor-core GEMM used by the conv/linear path, exposed for unit parity:
+   D[M][N] (fp32, row-major, ldd) = sum_k A(m,k) * B(n,k) with A given row-major [M][K]
+   (a_kmajor = 1) or [K][M] (0), B row-major [N][K] (b_kmajor = 1) or [K][N] (0); device
+   pointers, bf16 inputs.  Asynchronous on stream. */
+int xpipe_gemm_bf16(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,
+                    int32_t a_kmajor, int32_t b_kmajor, int64_t ldd, void* stream);
+
+/* Implicit-GEMM convolution on the same tensor-core path, exposed for unit parity.
+   geo = {Nimg, H, W, C, Co, R, S, P, Q, sh, sw, ph, pw}: input NHWC [Nimg][H][W][C] bf16 (C a
+   multiple of 8), weights KRSC [Co][R][S][C] bf16, output NHWC [Nimg][P][Q][Co].  mode:
+   1 = fprop (in0 = X, in1 = W, out = Y bf16), 2 = dgrad (in0 = dY, in1 = W, out = dX bf16
+   [Nimg][H][W][C]), 3 = wgrad (in0 = X, in1 = dY, out = dW fp32 [Co][R][S][C], accumulate
+   adds into out).  ws: optional fp32 device workspace of ws_elems for split-K (NULL = none).
+   Device pointers; asynchronous on stream. */
+int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void* in0, const void* in1, void* out,
+                      int32_t accumulate, float* ws, int64_t ws_elems, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XPIPE_H */

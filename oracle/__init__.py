@@ -27,7 +27,7 @@ def build(force=False):
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
         tmp = _SO + ".tmp%d" % os.getpid()
-        subprocess.check_call(["g++", "-std=c++17", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC",
+        subprocess.check_call(["g++", "-std=c++17", "-O3", "-march=native", "-fopenmp", "-ffp-contract=off", "-fPIC",
                                "-shared", "-o", tmp, _SRC])
         os.replace(tmp, _SO)
     return _SO

@@ -167,6 +167,14 @@ void linear_bwd(const Model& M, int li, int n, const Vec& x, const Vec& dy, cons
     }
 }
 
+/* output columns q whose input column q*sw - pw + s lies inside [0, W) */
+void valid_range(int sw, int pw, int s, int W, int Q, int& qlo, int& qhi) {
+  qlo = 0;
+  while (qlo < Q && qlo * sw - pw + s < 0) ++qlo;
+  qhi = Q;
+  while (qhi > qlo && (qhi - 1) * sw - pw + s >= W) --qhi;
+}
+
 /* Conv2d: cross-correlation with zero padding (PyTorch semantics), NCHW.
    y[n][co][p][q] = sum_{ci,r,s} x[n][ci][p*sh-ph+r][q*sw-pw+s] * W[co][ci][r][s] (+ b) */
 void conv_fwd(const Model& M, int li, int n, const Vec& x, const double* W, const double* b, Vec& y) {
@@ -183,15 +191,21 @@ void conv_fwd(const Model& M, int li, int n, const Vec& x, const double* W, cons
         for (int r = 0; r < R; ++r)
           for (int s = 0; s < S; ++s) {
             double w = W[(((size_t)co * C + ci) * R + r) * S + s];
+            int qlo, qhi;
+            valid_range(l.d.sw, l.d.pw, s, Wd, Q, qlo, qhi);
             for (int p = 0; p < P; ++p) {
               int ih = p * l.d.sh - l.d.ph + r;
               if (ih < 0 || ih >= H) continue;
               const double* xr = &x[(((size_t)s0 * C + ci) * H + ih) * Wd];
-              for (int q = 0; q < Q; ++q) {
-                int iw = q * l.d.sw - l.d.pw + s;
-                if (iw < 0 || iw >= Wd) continue;
-                if (M.mode == XO_FP32) accf[(size_t)p * Q + q] = std::fmaf((float)xr[iw], (float)w, accf[(size_t)p * Q + q]);
-                else acc[(size_t)p * Q + q] += xr[iw] * w;
+              double* ar = &acc[(size_t)p * Q];
+              float* af = &accf[(size_t)p * Q];
+              if (M.mode == XO_FP32) {
+                for (int q = qlo; q < qhi; ++q) af[q] = std::fmaf((float)xr[q * l.d.sw - l.d.pw + s], (float)w, af[q]);
+              } else if (l.d.sw == 1) {
+                const double* xs = xr + s - l.d.pw;
+                for (int q = qlo; q < qhi; ++q) ar[q] += xs[q] * w;
+              } else {
+                for (int q = qlo; q < qhi; ++q) ar[q] += xr[q * l.d.sw - l.d.pw + s] * w;
               }
             }
           }
@@ -221,15 +235,21 @@ void conv_bwd(const Model& M, int li, int n, const Vec& x, const Vec& dy, const 
           for (int r = 0; r < R; ++r)
             for (int s = 0; s < S; ++s) {
               double w = W[(((size_t)co * C + ci) * R + r) * S + s];
+              int qlo, qhi;
+              valid_range(l.d.sw, l.d.pw, s, Wd, Q, qlo, qhi);
               for (int p = 0; p < P; ++p) {
                 int ih = p * l.d.sh - l.d.ph + r;
                 if (ih < 0 || ih >= H) continue;
                 const double* dyr = &dy[(((size_t)s0 * K + co) * P + p) * Q];
-                for (int q = 0; q < Q; ++q) {
-                  int iw = q * l.d.sw - l.d.pw + s;
-                  if (iw < 0 || iw >= Wd) continue;
-                  if (M.mode == XO_FP32) accf[(size_t)ih * Wd + iw] = std::fmaf((float)dyr[q], (float)w, accf[(size_t)ih * Wd + iw]);
-                  else acc[(size_t)ih * Wd + iw] += dyr[q] * w;
+                double* ar = &acc[(size_t)ih * Wd];
+                float* af = &accf[(size_t)ih * Wd];
+                if (M.mode == XO_FP32) {
+                  for (int q = qlo; q < qhi; ++q) af[q * l.d.sw - l.d.pw + s] = std::fmaf((float)dyr[q], (float)w, af[q * l.d.sw - l.d.pw + s]);
+                } else if (l.d.sw == 1) {
+                  double* as = ar + s - l.d.pw;
+                  for (int q = qlo; q < qhi; ++q) as[q] += dyr[q] * w;
+                } else {
+                  for (int q = qlo; q < qhi; ++q) ar[q * l.d.sw - l.d.pw + s] += dyr[q] * w;
                 }
               }
             }
@@ -240,31 +260,36 @@ void conv_bwd(const Model& M, int li, int n, const Vec& x, const Vec& dy, const 
         }
       }
   }
-  /* dW[co][ci][r][s] = sum_{n,p,q} dy[n][co][p][q] x[n][ci][p*sh-ph+r][q*sw-pw+s] */
+  /* dW[co][ci][r][s] = sum_{n,p,q} dy[n][co][p][q] x[n][ci][p*sh-ph+r][q*sw-pw+s]; every
+     dW element is one sequential sum in (n, p, q) order; the R*S sums of a (co, ci) pair
+     advance together (independent accumulators, no reordering within any sum) */
 #pragma omp parallel for collapse(2) schedule(static)
   for (int co = 0; co < K; ++co)
-    for (int ci = 0; ci < C; ++ci)
-      for (int r = 0; r < R; ++r)
-        for (int s = 0; s < S; ++s) {
-          double acc = 0.0;
-          float accf = 0.f;
-          for (int s0 = 0; s0 < n; ++s0)
-            for (int p = 0; p < P; ++p) {
-              int ih = p * l.d.sh - l.d.ph + r;
+    for (int ci = 0; ci < C; ++ci) {
+      std::vector<double> acc((size_t)R * S, 0.0);
+      std::vector<float> accf((size_t)R * S, 0.f);
+      for (int s0 = 0; s0 < n; ++s0)
+        for (int p = 0; p < P; ++p)
+          for (int q = 0; q < Q; ++q) {
+            const double a = dy[(((size_t)s0 * K + co) * P + p) * Q + q];
+            for (int r = 0; r < R; ++r) {
+              const int ih = p * l.d.sh - l.d.ph + r;
               if (ih < 0 || ih >= H) continue;
-              for (int q = 0; q < Q; ++q) {
-                int iw = q * l.d.sw - l.d.pw + s;
+              const double* xr = &x[(((size_t)s0 * C + ci) * H + ih) * Wd];
+              for (int s = 0; s < S; ++s) {
+                const int iw = q * l.d.sw - l.d.pw + s;
                 if (iw < 0 || iw >= Wd) continue;
-                double a = dy[(((size_t)s0 * K + co) * P + p) * Q + q];
-                double bb = x[(((size_t)s0 * C + ci) * H + ih) * Wd + iw];
-                if (M.mode == XO_FP32) accf = std::fmaf((float)a, (float)bb, accf);
-                else acc += a * bb;
+                if (M.mode == XO_FP32) accf[r * S + s] = std::fmaf((float)a, (float)xr[iw], accf[r * S + s]);
+                else acc[r * S + s] += a * xr[iw];
               }
             }
-          double v = (M.mode == XO_FP32) ? (double)accf : acc;
-          if (M.mode == XO_BF16) v = (double)(float)v;
-          dW[(((size_t)co * C + ci) * R + r) * S + s] = v;
-        }
+          }
+      for (int rs = 0; rs < R * S; ++rs) {
+        double v = (M.mode == XO_FP32) ? (double)accf[rs] : acc[rs];
+        if (M.mode == XO_BF16) v = (double)(float)v;
+        dW[((size_t)co * C + ci) * R * S + rs] = v;
+      }
+    }
   if (l.d.bias)
     for (int co = 0; co < K; ++co) {
       double acc = 0.0;

@@ -1,0 +1,408 @@
+// bf16.cu -- the non-GEMM kernels of the bf16 conv path:
+//   input staging (NCHW fp32 -> NHWC bf16, channels padded to 8);
+//   BatchNorm statistics of the stored conv output (per-chunk Welford, fixed-order Chan merge);
+//   BN-apply + ReLU (+ MaxPool, first-max rule) fused, bf16 out;
+//   backward: max-pool routing + ReLU mask + BN reductions fused, then BN input gradient;
+//   the small bf16-operand Linear layers (fp32 accumulation, fp32 logits).
+// Rounding points follow DESIGN.md section 5: every stored activation / activation gradient
+// is bf16 (round-to-nearest-even); statistics, logits and parameter gradients are fp32.
+// All reductions are deterministic (fixed order, no atomics).
+#include "../internal.h"
+#include "bf16_kernels.h"
+
+namespace xp {
+
+namespace {
+
+typedef __nv_bfloat16 bf16;
+
+__device__ __forceinline__ float q16(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
+// The BN-apply + ReLU of one element, bit-identical wherever it is (re)computed:
+// a = Q(relu(gamma * ((x - mean) * rstd) + beta))
+__device__ __forceinline__ float bn_act(float x, float mean, float rstd, float gamma, float beta) {
+  const float t = __fmul_rn(__fsub_rn(x, mean), rstd);
+  const float v = __fadd_rn(__fmul_rn(gamma, t), beta);
+  return q16(v > 0.f ? v : 0.f);
+}
+
+// ---- K11 ---------------------------------------------------------------------------------
+__global__ void stage_input_bf16_kernel(const float* __restrict__ x, bf16* __restrict__ y, int n, int C, int H, int W,
+                                        int Cp) {
+  const int64_t total = (int64_t)n * H * W * Cp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Cp);
+    int64_t r = i / Cp;
+    const int w = (int)(r % W);
+    r /= W;
+    const int h = (int)(r % H);
+    const int s = (int)(r / H);
+    const float v = c < C ? x[(((int64_t)s * C + c) * H + h) * W + w] : 0.f;
+    y[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// ---- BN statistics: x [M][C] bf16 -> partial (mean, M2) per row chunk ----------------------
+// block: G = C/8 channel groups x RL = 256/G row lanes; chunk = RC rows; thread keeps
+// Welford (n, mean, M2) for 8 channels; lanes merged in fixed order through smem.
+__global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C, int RC, float* __restrict__ part) {
+  extern __shared__ float sh[];  // [RL][G][16] (mean[8], M2[8]) + counts
+  const int G = C / 8, RL = blockDim.x / G;
+  const int g = threadIdx.x % G, rl = threadIdx.x / G;
+  const int r0 = blockIdx.x * RC, r1 = min(M, r0 + RC);
+  float mean[8], m2[8];
+  int cnt = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) { mean[e] = 0.f; m2[e] = 0.f; }
+  if (rl < RL) {
+    for (int r = r0 + rl; r < r1; r += RL) {
+      const uint4 u = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + g * 8);
+      const bf16* v = reinterpret_cast<const bf16*>(&u);
+      ++cnt;
+      const float inv = 1.f / (float)cnt;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xv = __bfloat162float(v[e]);
+        const float d = xv - mean[e];
+        mean[e] += d * inv;
+        m2[e] += d * (xv - mean[e]);
+      }
+    }
+  }
+  // fixed-order merge over row lanes: lane 0 absorbs lanes 1..RL-1 in order
+  float* slot = sh + ((size_t)rl * G + g) * 17;
+  if (rl < RL) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { slot[e] = mean[e]; slot[8 + e] = m2[e]; }
+    slot[16] = (float)cnt;
+  }
+  __syncthreads();
+  if (rl == 0) {
+    float na = slot[16];
+    for (int l = 1; l < RL; ++l) {
+      const float* o = sh + ((size_t)l * G + g) * 17;
+      const float nb = o[16];
+      if (nb == 0.f) continue;
+      const float nab = na + nb;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = o[e] - mean[e];
+        mean[e] += d * (nb / nab);
+        m2[e] += o[8 + e] + d * d * (na * nb / nab);
+      }
+      na = nab;
+    }
+    float* p = part + (size_t)blockIdx.x * 2 * C;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { p[g * 8 + e] = mean[e]; p[C + g * 8 + e] = m2[e]; }
+  }
+}
+
+// merge the chunk partials in chunk order -> stats[0..C) mean, [C..2C) rstd, [2C..3C) gamma_f,
+// [3C..4C) beta_f (the forward's affine parameters, kept for the backward recompute)
+__global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
+                                      const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
+                                      float* __restrict__ stats) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float na = 0.f, mean = 0.f, m2 = 0.f;
+  for (int k = 0; k < chunks; ++k) {
+    const float nb = (float)min(RC, M - k * RC);
+    const float mb = part[(size_t)k * 2 * C + c], m2b = part[(size_t)k * 2 * C + C + c];
+    const float nab = na + nb;
+    const float d = mb - mean;
+    mean += d * (nb / nab);
+    m2 += m2b + d * d * (na * nb / nab);
+    na = nab;
+  }
+  const float var = m2 / na;
+  stats[c] = mean;
+  stats[C + c] = 1.f / sqrtf(var + eps);
+  stats[2 * C + c] = __bfloat162float(gamma[c]);
+  stats[3 * C + c] = __bfloat162float(beta[c]);
+}
+
+// ---- BN-apply + ReLU (+ pool) ------------------------------------------------------------
+// y[n][p][q][c] = max over the pool window (first max, row-major) of bn_act(x[n][h][w][c])
+__global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restrict__ st, bf16* __restrict__ y,
+                                int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph,
+                                int pw, int pool) {
+  const int G = C / 8;
+  const int64_t total = (int64_t)n * P * Q * G;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    int64_t r = i / G;
+    const int q = (int)(r % Q);
+    r /= Q;
+    const int p = (int)(r % P);
+    const int s = (int)(r / P);
+    const int c0 = g * 8;
+    float mean[8], rstd[8], ga[8], be[8], best[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      mean[e] = st[c0 + e]; rstd[e] = st[C + c0 + e]; ga[e] = st[2 * C + c0 + e]; be[e] = st[3 * C + c0 + e];
+      best[e] = 0.f;
+    }
+    if (!pool) {
+      const uint4 u = *reinterpret_cast<const uint4*>(x + (((int64_t)s * H + p) * W + q) * C + c0);
+      const bf16* v = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) best[e] = bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e]);
+    } else {
+      bool first = true;
+      for (int a = 0; a < kh; ++a)
+        for (int b = 0; b < kw; ++b) {
+          const int hh = p * sh - ph + a, ww = q * sw - pw + b;
+          if (hh < 0 || hh >= H || ww < 0 || ww >= W) continue;
+          const uint4 u = *reinterpret_cast<const uint4*>(x + (((int64_t)s * H + hh) * W + ww) * C + c0);
+          const bf16* v = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float t = bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e]);
+            if (first || t > best[e]) best[e] = t;
+          }
+          first = false;
+        }
+    }
+    uint32_t w4[4];
+#pragma unroll
+    for (int h2 = 0; h2 < 4; ++h2) {
+      __nv_bfloat162 t = __floats2bfloat162_rn(best[2 * h2], best[2 * h2 + 1]);
+      w4[h2] = *reinterpret_cast<uint32_t*>(&t);
+    }
+    *reinterpret_cast<uint4*>(y + (((int64_t)s * P + p) * Q + q) * C + c0) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+  }
+}
+
+// gradient reaching BN output element (s,h,w,c): max-pool routing (first max of every window
+// containing it) and the ReLU mask, recomputing a from the stash (x, stats)
+struct BwdGeo {
+  int H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool;
+};
+
+__device__ __forceinline__ float routed_dy(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                           const BwdGeo& G, int s, int h, int w, int c, float mean, float rstd, float ga,
+                                           float be) {
+  const float a = bn_act(__bfloat162float(x[(((int64_t)s * G.H + h) * G.W + w) * G.C + c]), mean, rstd, ga, be);
+  if (!(a > 0.f)) return 0.f;
+  if (!G.pool) return __bfloat162float(dout[(((int64_t)s * G.H + h) * G.W + w) * G.C + c]);
+  // windows (p,q) with p*sh - ph <= h < p*sh - ph + kh
+  const int plo = max(0, (h + G.ph - G.kh + G.sh) / G.sh), phi = min(G.P - 1, (h + G.ph) / G.sh);
+  const int qlo = max(0, (w + G.pw - G.kw + G.sw) / G.sw), qhi = min(G.Q - 1, (w + G.pw) / G.sw);
+  float acc = 0.f;
+  int hits = 0;
+  for (int p = plo; p <= phi; ++p)
+    for (int q = qlo; q <= qhi; ++q) {
+      // first max of window (p,q)
+      float best = 0.f;
+      int bh = -1, bw = -1;
+      for (int a2 = 0; a2 < G.kh; ++a2)
+        for (int b2 = 0; b2 < G.kw; ++b2) {
+          const int hh = p * G.sh - G.ph + a2, ww = q * G.sw - G.pw + b2;
+          if (hh < 0 || hh >= G.H || ww < 0 || ww >= G.W) continue;
+          const float t = bn_act(__bfloat162float(x[(((int64_t)s * G.H + hh) * G.W + ww) * G.C + c]), mean, rstd, ga, be);
+          if (bh < 0 || t > best) { best = t; bh = hh; bw = ww; }
+        }
+      if (bh == h && bw == w) {
+        const float d = __bfloat162float(dout[(((int64_t)s * G.P + p) * G.Q + q) * G.C + c]);
+        acc = hits ? __fadd_rn(acc, d) : d;
+        ++hits;
+      }
+    }
+  return hits > 1 ? q16(acc) : acc;
+}
+
+// per chunk of rows, per channel: sum dy, sum dy*xhat (fixed order: row lanes then merge)
+__global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                     const float* __restrict__ st, BwdGeo G, int M, int RC, float* __restrict__ part) {
+  extern __shared__ float sh[];
+  const int C = G.C;
+  const int r0 = blockIdx.x * RC, r1 = min(M, r0 + RC);
+  const int cl = threadIdx.x & 63, rl = threadIdx.x >> 6, RL = blockDim.x >> 6;
+  const int c = blockIdx.y * 64 + cl;
+  float s1 = 0.f, s2 = 0.f;
+  if (c < C) {
+    const float mean = st[c], rstd = st[C + c], ga = st[2 * C + c], be = st[3 * C + c];
+    for (int r = r0 + rl; r < r1; r += RL) {
+      const int w = r % G.W, t = r / G.W, h = t % G.H, s = t / G.H;
+      const float dy = routed_dy(x, dout, G, s, h, w, c, mean, rstd, ga, be);
+      const float xh = __fmul_rn(__fsub_rn(__bfloat162float(x[(int64_t)r * C + c]), mean), rstd);
+      s1 = __fadd_rn(s1, dy);
+      s2 = __fadd_rn(s2, __fmul_rn(dy, xh));
+    }
+  }
+  sh[(rl * 64 + cl) * 2] = s1;
+  sh[(rl * 64 + cl) * 2 + 1] = s2;
+  __syncthreads();
+  if (rl == 0 && c < C) {
+    for (int l = 1; l < RL; ++l) { s1 = __fadd_rn(s1, sh[(l * 64 + cl) * 2]); s2 = __fadd_rn(s2, sh[(l * 64 + cl) * 2 + 1]); }
+    part[(size_t)blockIdx.x * 2 * C + c] = s1;
+    part[(size_t)blockIdx.x * 2 * C + C + c] = s2;
+  }
+}
+
+// totals over chunks (fixed order); dgamma/dbeta into the gradient accumulator
+__global__ void bn_bwd_final_kernel(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
+                                    float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s1 = 0.f, s2 = 0.f;
+  for (int k = 0; k < chunks; ++k) { s1 = __fadd_rn(s1, part[(size_t)k * 2 * C + c]); s2 = __fadd_rn(s2, part[(size_t)k * 2 * C + C + c]); }
+  tot[c] = s1;
+  tot[C + c] = s2;
+  g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
+  g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
+}
+
+// dx = Q(gamma_b * rstd * (dy - sum(dy)/cnt - xhat * sum(dy xhat)/cnt))
+__global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                    const float* __restrict__ st, const float* __restrict__ tot,
+                                    const bf16* __restrict__ gamma_b, BwdGeo G, int M, bf16* __restrict__ dx) {
+  const int C = G.C;
+  const float inv_cnt = 1.f / (float)M;
+  const int64_t total = (int64_t)M * C;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const int r = (int)(i / C);
+    const int w = r % G.W, t = r / G.W, h = t % G.H, s = t / G.H;
+    const float mean = st[c], rstd = st[C + c], ga = st[2 * C + c], be = st[3 * C + c];
+    const float dy = routed_dy(x, dout, G, s, h, w, c, mean, rstd, ga, be);
+    const float xh = __fmul_rn(__fsub_rn(__bfloat162float(x[i]), mean), rstd);
+    const float gb = __bfloat162float(gamma_b[c]);
+    const float v = __fmul_rn(__fmul_rn(gb, rstd),
+                              __fsub_rn(__fsub_rn(dy, __fmul_rn(tot[c], inv_cnt)), __fmul_rn(xh, __fmul_rn(tot[C + c], inv_cnt))));
+    dx[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// ---- bf16-operand Linear (small: micro-batch rows) ------------------------------------------
+// y[r][o] = sum_i x[r][i] W[o][i] (fp32) + b[o]; logits: fp32 out, else Q(relu?) bf16
+__global__ void linear_fwd_bf16_kernel(const bf16* __restrict__ x, const bf16* __restrict__ W,
+                                       const bf16* __restrict__ b, void* __restrict__ y, int n, int in, int out,
+                                       int relu, int f32out) {
+  const int o = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (o >= out) return;
+  for (int r = 0; r < n; ++r) {
+    float acc = 0.f;
+    for (int i = lane; i < in; i += 32) acc += __bfloat162float(x[(int64_t)r * in + i]) * __bfloat162float(W[(int64_t)o * in + i]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) {
+      float v = b ? __fadd_rn(acc, __bfloat162float(b[o])) : acc;
+      if (f32out) static_cast<float*>(y)[(int64_t)r * out + o] = v;
+      else {
+        if (relu) v = v > 0.f ? v : 0.f;
+        static_cast<bf16*>(y)[(int64_t)r * out + o] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+template <bool DY_F32>
+__device__ __forceinline__ float load_dy(const void* dy, int64_t idx, const bf16* mask) {
+  float d = DY_F32 ? q16(static_cast<const float*>(dy)[idx]) : __bfloat162float(static_cast<const bf16*>(dy)[idx]);
+  if (mask && !(__bfloat162float(mask[idx]) > 0.f)) d = 0.f;
+  return d;
+}
+
+// dx[r][i] = Q(sum_o dy'[r][o] W[o][i])
+template <bool DY_F32>
+__global__ void linear_dgrad_bf16_kernel(const void* __restrict__ dy, const bf16* __restrict__ mask,
+                                         const bf16* __restrict__ W, bf16* __restrict__ dx, int n, int in, int out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= in) return;
+  for (int r = 0; r < n; ++r) {
+    float acc = 0.f;
+    for (int o = 0; o < out; ++o) acc += load_dy<DY_F32>(dy, (int64_t)r * out + o, mask) * __bfloat162float(W[(int64_t)o * in + i]);
+    dx[(int64_t)r * in + i] = __float2bfloat16_rn(acc);
+  }
+}
+
+// gW[o][i] (=|+=) sum_r dy'[r][o] x[r][i]; gb[o] (=|+=) sum_r dy'[r][o]
+template <bool DY_F32>
+__global__ void linear_wgrad_bf16_kernel(const void* __restrict__ dy, const bf16* __restrict__ mask,
+                                         const bf16* __restrict__ x, float* __restrict__ gW, float* __restrict__ gb,
+                                         int n, int in, int out, int accumulate) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int o = blockIdx.y;
+  if (i > in || (i == in && !gb)) return;
+  float acc = 0.f;
+  for (int r = 0; r < n; ++r) {
+    const float d = load_dy<DY_F32>(dy, (int64_t)r * out + o, mask);
+    acc += i < in ? d * __bfloat162float(x[(int64_t)r * in + i]) : d;
+  }
+  float* dst = i < in ? &gW[(int64_t)o * in + i] : &gb[o];
+  *dst = accumulate ? __fadd_rn(*dst, acc) : acc;
+}
+
+int grid1d(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+}  // namespace
+
+cudaError_t launch_stage_input_bf16(const float* x, bf16* y, int n, int C, int H, int W, int Cp, cudaStream_t st) {
+  stage_input_bf16_kernel<<<grid1d((int64_t)n * H * W * Cp), 256, 0, st>>>(x, y, n, C, H, W, Cp);
+  return cudaGetLastError();
+}
+
+int bn_chunk_rows(int M) { return M <= 2048 ? 64 : 256; }
+int bn_chunks(int M) { return (M + bn_chunk_rows(M) - 1) / bn_chunk_rows(M); }
+size_t bn_ws_floats(int M, int C) { return (size_t)bn_chunks(M) * 2 * C + 2 * (size_t)C; }
+
+cudaError_t launch_bn_stats(const bf16* x, int M, int C, float eps, const bf16* gamma, const bf16* beta, float* ws,
+                            float* stats, cudaStream_t st) {
+  if (C % 8 || C > 2048) return cudaErrorInvalidValue;
+  const int RC = bn_chunk_rows(M), chunks = bn_chunks(M);
+  const int G = C / 8;
+  const int threads = G >= 256 ? G : (256 / G) * G;
+  const size_t shm = (size_t)(threads / G) * G * 17 * 4;
+  bn_stats_partial_kernel<<<chunks, threads, shm, st>>>(x, M, C, RC, ws);
+  bn_stats_final_kernel<<<(C + 127) / 128, 128, 0, st>>>(ws, chunks, M, RC, C, eps, gamma, beta, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, int n, int H, int W, int C, int P, int Q, int kh,
+                            int kw, int sh, int sw, int ph, int pw, bool pool, cudaStream_t st) {
+  const int64_t total = (int64_t)n * P * Q * (C / 8);
+  bn_apply_kernel<<<grid1d(total), 256, 0, st>>>(x, stats, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bn_backward(const bf16* x, const bf16* dout, const float* stats, const bf16* gamma_b, int n, int H,
+                               int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,
+                               float* ws, float* g_gamma, float* g_beta, bool accumulate, bf16* dx, cudaStream_t st) {
+  BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0};
+  const int M = n * H * W;
+  const int RC = bn_chunk_rows(M), chunks = bn_chunks(M);
+  dim3 grid(chunks, (C + 63) / 64);
+  bn_bwd_reduce_kernel<<<grid, 256, 256 * 2 * 4, st>>>(x, dout, stats, G, M, RC, ws);
+  float* tot = ws + (size_t)chunks * 2 * C;
+  bn_bwd_final_kernel<<<(C + 127) / 128, 128, 0, st>>>(ws, chunks, C, tot, g_gamma, g_beta, accumulate ? 1 : 0);
+  bn_bwd_apply_kernel<<<grid1d((int64_t)M * C), 256, 0, st>>>(x, dout, stats, tot, gamma_b, G, M, dx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_linear_fwd_bf16(const bf16* x, const bf16* W, const bf16* b, void* y, int n, int in, int out,
+                                   bool relu, bool f32out, cudaStream_t st) {
+  linear_fwd_bf16_kernel<<<(out + 7) / 8, 256, 0, st>>>(x, W, b, y, n, in, out, relu ? 1 : 0, f32out ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_linear_dgrad_bf16(const void* dy, bool dy_f32, const bf16* mask, const bf16* W, bf16* dx, int n,
+                                     int in, int out, cudaStream_t st) {
+  if (dy_f32) linear_dgrad_bf16_kernel<true><<<(in + 127) / 128, 128, 0, st>>>(dy, mask, W, dx, n, in, out);
+  else linear_dgrad_bf16_kernel<false><<<(in + 127) / 128, 128, 0, st>>>(dy, mask, W, dx, n, in, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_linear_wgrad_bf16(const void* dy, bool dy_f32, const bf16* mask, const bf16* x, float* gW, float* gb,
+                                     int n, int in, int out, bool accumulate, cudaStream_t st) {
+  dim3 grid((in + 1 + 127) / 128, out);
+  if (dy_f32) linear_wgrad_bf16_kernel<true><<<grid, 128, 0, st>>>(dy, mask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
+  else linear_wgrad_bf16_kernel<false><<<grid, 128, 0, st>>>(dy, mask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
+}  // namespace xp

@@ -1,0 +1,48 @@
+// gemm_tc.h -- tcgen05 implicit-GEMM entry points (kernels/gemm_tc.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace xp {
+
+enum { GEMM_PLAIN = 0, GEMM_FPROP = 1, GEMM_DGRAD = 2, GEMM_WGRAD = 3 };
+enum { EPI_BF16 = 0, EPI_F32 = 1, EPI_WGRAD_T = 2 };
+
+struct ConvGeo {
+  int Nimg, H, W, C;      // input NHWC, C = channel stride (Cin padded to a multiple of 8)
+  int Co, R, S, P, Q;     // output channels, filter, output spatial
+  int sh, sw, ph, pw;
+};
+
+struct GemmArgs {
+  int M, N, K;
+  const __nv_bfloat16* A;
+  const __nv_bfloat16* B;
+  int64_t lda, ldb;
+  ConvGeo g;
+  int epi;
+  void* out;
+  int64_t ldo;
+  int accumulate;
+  int64_t split_stride;   // elements between split-K partial planes (EPI_F32 into a workspace)
+  int kb_per_split;
+};
+
+// plain GEMM for unit parity: D[M][N] fp32 (ldd) = A(m,k) B(n,k)
+cudaError_t tc_gemm_plain(const __nv_bfloat16* A, const __nv_bfloat16* B, float* D, int M, int N, int K, bool a_kmajor,
+                          bool b_kmajor, int64_t ldd, cudaStream_t st);
+
+// Y [Nimg*P*Q][Co] bf16 = conv(X [Nimg][H][W][C] bf16, W [Co][R][S][C] bf16)
+cudaError_t tc_conv_fprop(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* Wt, __nv_bfloat16* Y,
+                          float* ws, int64_t ws_elems, cudaStream_t st);
+// dX [Nimg*H*W][Cx] bf16 (Cx = real input channels, multiple of 8) from dY [Nimg*P*Q][Co]
+cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const __nv_bfloat16* dY, const __nv_bfloat16* Wt,
+                          __nv_bfloat16* dX, float* ws, int64_t ws_elems, cudaStream_t st);
+// gW [Co][R][S][C] fp32 (=|+=) sum over pixels of dY x im2col(X)
+cudaError_t tc_conv_wgrad(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* dY, float* gW, bool accumulate,
+                          float* ws, int64_t ws_elems, cudaStream_t st);
+// workspace (floats) the launchers above can use profitably for split-K
+int64_t tc_conv_ws_elems(const ConvGeo& g);
+
+}  // namespace xp

@@ -1,0 +1,121 @@
+// runtime.h -- host-side context of the XPipe runtime (shared by xpipe.cu, blocks.cu, plan.cu).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/xpipe.h"
+#include "internal.h"
+#include "plan.h"
+
+#define XP_CUDA(c, call)                                                                           \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return set_err(c, XP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +     \
+                                      std::to_string(__LINE__));                                   \
+  } while (0)
+
+#define XP_TRY(x)            \
+  do {                       \
+    int r_ = (x);            \
+    if (r_ != XP_OK) return r_; \
+  } while (0)
+
+
+namespace xp {
+// ----------------------------------------------------------------------------------------
+// context
+// ----------------------------------------------------------------------------------------
+struct Alloc { void* p; size_t bytes; int dev; };
+
+struct Snapshot { int ver; std::vector<float> W; float* pinned; };
+
+struct StageRT {
+  int k = 0, dev = 0;
+  cudaStream_t stream = nullptr;
+  int l0 = 0, l1 = 0;
+  StagePlan plan;                       // blocks, arena layout (plan.h)
+  float *W = nullptr, *g = nullptr, *m = nullptr, *v = nullptr;
+  void* pf[2] = {nullptr, nullptr};
+  void* pb = nullptr;
+  DevState* ds = nullptr;
+  uint32_t* flags = nullptr;            // [0] act_ready [1] grad_ready [2] act_ack [3] grad_ack
+  int S = 1;                            // stash slots (max micro-batches in flight)
+  std::vector<void*> in_slot;           // input ring (R = S)
+  std::vector<void*> gin_slot;          // gradient ring (R = S), k < K-1
+  std::vector<std::vector<void*>> out;  // [block][slot] block outputs
+  std::vector<std::vector<void*>> mid;  // [block][slot] conv outputs (bf16 path)
+  std::vector<std::vector<float*>> stats;
+  std::vector<float*> dz;               // [slot] logits gradient (last stage)
+  std::vector<float*> logits;           // [slot]
+  void* gbuf[2] = {nullptr, nullptr};   // backward gradient ping-pong
+  void* gmid = nullptr;                 // conv block: gradient of the conv output (bf16)
+  int64_t gbuf_elems = 0;
+  float* ws = nullptr;                  // split-K workspace (fp32)
+  int64_t ws_elems = 0;
+  float* bnws = nullptr;                // BatchNorm partial-reduction workspace
+  // host program state
+  int64_t pos = 0;
+  bool done = false;
+  int host_ver = 0, host_fver = 0, host_bver = 0;
+  // trace
+  TraceRec* trace_dev = nullptr;
+  int64_t trace_cap = 0, trace_n = 0;
+  std::vector<Snapshot> snaps;
+  std::vector<float*> snap_pool;         // pinned buffers reserved before enqueue
+  // profiling (cfg.profile): event pool and the (class, work) of each recorded pair
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> prof_cls;
+  std::vector<double> prof_work;
+};
+
+}  // namespace xp
+
+struct xpipe_ctx {
+  using StageRT = xp::StageRT;
+  using Alloc = xp::Alloc;
+  using NetPlan = xp::NetPlan;
+  std::string err;
+  bool poisoned = false;
+  NetPlan net;
+  int K = 1, T = 1, N = 1, n = 1;
+  float lr = 0, b1 = 0, b2 = 0, eps = 0;
+  xpipe_config cfg{};
+  std::vector<StageRT> S;
+  std::vector<Alloc> allocs;
+  // per-call buffers
+  float* x_dev = nullptr; int64_t x_cap = 0;
+  int32_t* y_dev = nullptr; int64_t y_cap = 0;
+  float* loss_dev = nullptr; int64_t loss_cap = 0;
+  int64_t fed = 0;           // micro-batches fed (absolute, 1-based count)
+  int64_t base = 0;          // micro-batch offset of the current epoch
+  int64_t call_first = 0;    // first micro-batch (absolute) of the current call's input buffer
+  int64_t kernels = 0;
+  std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)
+};
+
+
+namespace xp {
+// blocks.cu
+void* dmalloc(xpipe_ctx* c, size_t bytes, int dev);
+int set_err(xpipe_ctx* c, int code, const std::string& m);
+int check_launch(xpipe_ctx* c, cudaError_t e, const char* what);
+int allocate_stage(xpipe_ctx* c, StageRT& s);
+int init_stage_params(xpipe_ctx* c, StageRT& s, const xpipe_layer* layers);
+int stage_input(xpipe_ctx* c, StageRT& s, const float* x_nchw, void* dst);
+int block_forward(xpipe_ctx* c, StageRT& s, size_t b, const void* x, const void* Wf, int slot);
+int block_backward(xpipe_ctx* c, StageRT& s, int b, const void* x, const void* dy, void* dx, const void* Wb, int slot,
+                   bool accumulate);
+// bf16_blocks.cu
+int bf16_block_forward(xpipe_ctx* c, StageRT& s, size_t b, const void* x, const void* Wf, int slot);
+int bf16_block_backward(xpipe_ctx* c, StageRT& s, int b, const void* x, const void* dy, void* dx, const void* Wb,
+                        int slot, bool accumulate);
+// xpipe.cu
+int version_difference(const xpipe_ctx* c, int k, int pass);
+int version_difference_public(const xpipe_ctx* c, int k, int pass);
+// profiling: bracket one kernel launch on s.stream (no-ops unless cfg.profile)
+int prof_begin(xpipe_ctx* c, StageRT& s);
+int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work);
+}  // namespace xp

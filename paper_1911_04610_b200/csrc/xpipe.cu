@@ -1,0 +1,636 @@
+// xpipe.cu -- host runtime of the B200-native XPipe hot path and its C ABI (include/xpipe.h).
+//
+// One CUDA stream per pipeline stage (stage k on devices[k % n_devices]).  The host turns
+// every stage's program (reading R7: K-k warm-up forwards, then B(i),
+// F(i+K-k) pairs, then drain; or GPipe) into stream work in program order; ordering
+// between stages is carried entirely by device-side 32-bit flags written and waited with
+// CUDA stream memory operations (cuStreamWriteValue32 / cuStreamWaitValue32):
+//   act_ready[k]  = last micro-batch u whose activation message reached stage k's ring
+//   grad_ready[k] = last micro-batch u whose gradient message reached stage k's ring
+//   act_ack[k]    = last u whose activation message stage k+1 released (ring credit)
+//   grad_ack[k]   = last u whose gradient message stage k-1 released (ring credit)
+// so the host never blocks on another stage, a stage never spins on an SM, and the same
+// code drives K stages on one GPU, on K GPUs (peer copies over NVLink), or -- with the
+// rings/flags mapped through CUDA IPC -- one process per GPU.
+//
+// Messages (a5, a8) are copied by the copy engine (cudaMemcpyAsync, same-device or peer)
+// from the producer's local stash into the consumer's ring slot, then the flag is written
+// (the write value op orders after the copy).  Ring slots double as the consumer's stash of
+// its first layer's input.  The fused Adam+prediction sweep (K1) runs after B(t,T) and
+// materialises W_hat_f[(v+1) & 1] and W_hat_b of the new version.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/xpipe.h"
+#include "runtime.h"
+
+using namespace xp;
+
+// ----------------------------------------------------------------------------------------
+// driver entry points (no link-time dependency on libcuda: the .so loads without a GPU)
+// ----------------------------------------------------------------------------------------
+namespace {
+typedef int (*PFN_waitValue32)(cudaStream_t, unsigned long long, uint32_t, unsigned int);
+typedef int (*PFN_writeValue32)(cudaStream_t, unsigned long long, uint32_t, unsigned int);
+PFN_waitValue32 p_wait32 = nullptr;
+PFN_writeValue32 p_write32 = nullptr;
+
+bool load_driver_entry_points() {
+  if (p_wait32 && p_write32) return true;
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess || !f) return false;
+  p_wait32 = (PFN_waitValue32)f;
+  f = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess || !f) return false;
+  p_write32 = (PFN_writeValue32)f;
+  return true;
+}
+
+thread_local std::string g_init_error;
+}  // namespace
+
+namespace xp {
+
+int set_err(xpipe_ctx* c, int code, const std::string& m) {
+  if (c) {
+    c->err = m;
+    if (code == XP_ECUDA || code == XP_ECOMM || code == XP_ESCHED) c->poisoned = true;
+  } else {
+    g_init_error = m;
+  }
+  return code;
+}
+
+void* dmalloc(xpipe_ctx* c, size_t bytes, int dev) {
+  if (bytes == 0) bytes = 256;
+  bytes = (bytes + 255) & ~size_t(255);
+  void* p = nullptr;
+  if (c->cfg.alloc) {
+    p = c->cfg.alloc(bytes, dev, c->cfg.alloc_user);
+  } else {
+    cudaSetDevice(dev);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
+  }
+  if (p) c->allocs.push_back({p, bytes, dev});
+  return p;
+}
+
+void free_all(xpipe_ctx* c) {
+  for (auto& s : c->S) {
+    for (auto& sn : s.snaps) if (sn.pinned) cudaFreeHost(sn.pinned);
+    s.snaps.clear();
+    for (auto p : s.snap_pool) cudaFreeHost(p);
+    s.snap_pool.clear();
+    for (auto e : s.ev_pool) cudaEventDestroy(e);
+    s.ev_pool.clear();
+    if (s.stream) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.stream); cudaStreamDestroy(s.stream); s.stream = nullptr; }
+  }
+  for (auto it = c->allocs.rbegin(); it != c->allocs.rend(); ++it) {
+    if (c->cfg.free) c->cfg.free(it->p, it->bytes, it->dev, c->cfg.alloc_user);
+    else { cudaSetDevice(it->dev); cudaFree(it->p); }
+  }
+  c->allocs.clear();
+}
+
+int check_launch(xpipe_ctx* c, cudaError_t e, const char* what) {
+  c->kernels++;
+  if (e != cudaSuccess) return set_err(c, XP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return XP_OK;
+}
+
+}  // namespace xp
+
+namespace xp {
+// Eq. (1) P:104-109 / Eq. (2) P:111-115 with half-up rounding (R3), integer form:
+//   s_f = floor((2K + 3T - 4 - k) / (2T)),  s_b = floor((3T + 2*floor(k/2) - 2) / (2T))
+int version_difference(const xpipe_ctx* c, int k, int pass) {
+  if (c->cfg.predict == XP_PRED_OFF) return 0;
+  if (c->cfg.predict == XP_PRED_FIXED) return pass == 0 ? c->cfg.s_fwd : c->cfg.s_bwd;
+  const int K = c->K, T = c->T;
+  int s = pass == 0 ? (2 * K + 3 * T - 4 - k) / (2 * T) : (3 * T + 2 * (k / 2) - 2) / (2 * T);
+  return s < 0 ? 0 : s;
+}
+
+int version_difference_public(const xpipe_ctx* c, int k, int pass) { return version_difference(c, k, pass); }
+
+int prof_begin(xpipe_ctx* c, StageRT& s) {
+  if (!c->cfg.profile) return XP_OK;
+  while (s.ev_pool.size() < s.ev_used + 2) {
+    cudaEvent_t e;
+    XP_CUDA(c, cudaEventCreate(&e));
+    s.ev_pool.push_back(e);
+  }
+  XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used], s.stream));
+  return XP_OK;
+}
+
+int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work) {
+  if (!c->cfg.profile) return XP_OK;
+  XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used + 1], s.stream));
+  s.ev_used += 2;
+  s.prof_cls.push_back(cls);
+  s.prof_work.push_back(work);
+  return XP_OK;
+}
+}  // namespace xp
+
+namespace {
+
+int flag_wait(xpipe_ctx* c, StageRT& s, uint32_t* flag, int64_t value) {
+  if (value <= 0) return XP_OK;
+  int r = p_wait32(s.stream, (unsigned long long)(uintptr_t)flag, (uint32_t)value, 0 /*GEQ*/);
+  if (r != 0) return set_err(c, XP_ECOMM, "cuStreamWaitValue32 failed: " + std::to_string(r));
+  return XP_OK;
+}
+
+int flag_write(xpipe_ctx* c, StageRT& s, uint32_t* flag, int64_t value) {
+  int r = p_write32(s.stream, (unsigned long long)(uintptr_t)flag, (uint32_t)value, 0 /*DEFAULT: with barrier*/);
+  if (r != 0) return set_err(c, XP_ECOMM, "cuStreamWriteValue32 failed: " + std::to_string(r));
+  return XP_OK;
+}
+
+// ---- stage program (a1; R7), written independently of the oracle ---------------------------
+// returns op (0 = F, 1 = B) and micro-batch u (absolute, 1-based) at program position p
+void program_op(const xpipe_ctx* c, int k, int64_t p, int* op, int64_t* u) {
+  if (c->cfg.schedule == XP_SCHED_GPIPE) {
+    const int64_t t = p / (2 * c->T), r = p % (2 * c->T);
+    *op = r < c->T ? 0 : 1;
+    *u = t * c->T + (r < c->T ? r : r - c->T) + 1;
+  } else {
+    const int64_t W = c->K - k;
+    if (p < W) { *op = 0; *u = p + 1; }
+    else {
+      const int64_t q = p - W, i = q / 2 + 1;
+      if (q % 2 == 0) { *op = 1; *u = i; } else { *op = 0; *u = i + W; }
+    }
+  }
+  *u += c->base;
+}
+
+int trace_slot(xpipe_ctx* c, StageRT& s, TraceRec** rec) {
+  *rec = nullptr;
+  if (!c->cfg.trace) return XP_OK;
+  if (s.trace_n >= s.trace_cap) return set_err(c, XP_ESCHED, "trace capacity (internal)");
+  *rec = s.trace_dev + s.trace_n++;
+  return XP_OK;
+}
+
+// Everything that can allocate (and so implicitly synchronise the device) happens here,
+// before any op of the call is enqueued: once stream work waits on a flag that only later
+// work writes, a device-wide synchronisation would deadlock the pipeline.
+int reserve_for_call(xpipe_ctx* c, int64_t M) {
+  for (auto& s : c->S) {
+    if (c->cfg.trace) {
+      const int64_t need = 3 * (c->fed + c->T) + 64;  // <= 2 ops per micro-batch + 1 update per mini-batch
+      if (need > s.trace_cap) {
+        const int64_t cap = std::max<int64_t>(need, 2 * s.trace_cap);
+        TraceRec* nt = (TraceRec*)dmalloc(c, cap * sizeof(TraceRec), s.dev);
+        if (!nt) return set_err(c, XP_ENOMEM, "trace buffer");
+        cudaSetDevice(s.dev);
+        if (s.trace_n) XP_CUDA(c, cudaMemcpy(nt, s.trace_dev, s.trace_n * sizeof(TraceRec), cudaMemcpyDeviceToDevice));
+        s.trace_dev = nt;
+        s.trace_cap = cap;
+      }
+    }
+    if (c->cfg.profile) {
+      int nconv = 0;
+      for (const Block& B : s.plan.blocks) nconv += B.kind == BK_CONV;
+      const size_t want = (size_t)2 * (3 * nconv + 1) * (size_t)(M * c->T + c->K + 1);
+      while (s.ev_pool.size() < want) {
+        cudaEvent_t e;
+        XP_CUDA(c, cudaEventCreate(&e));
+        s.ev_pool.push_back(e);
+      }
+    }
+    if (c->cfg.snapshots) {
+      const size_t want = (size_t)(M + c->K + 1);
+      while (s.snap_pool.size() < want) {
+        float* p = nullptr;
+        XP_CUDA(c, cudaMallocHost(&p, s.plan.P * sizeof(float)));
+        s.snap_pool.push_back(p);
+      }
+    }
+  }
+  return XP_OK;
+}
+
+// ---- forward / backward of one stage on one micro-batch -----------------------------------
+int enqueue_forward(xpipe_ctx* c, int k, int64_t u) {
+  StageRT& s = c->S[k];
+  const int64_t t = (u - 1) / c->T + 1, j = u - (t - 1) * c->T;
+  const int slot = (int)((u - 1) % s.S);
+  const int sf = version_difference(c, k, 0);
+  const bool bw = (j == 1);
+  cudaSetDevice(s.dev);
+  // input: stage 0 stages the call's input into its stash slot; others wait for the message
+  if (k == 0) {
+    const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
+    const float* src = c->x_dev + (u - c->call_first) * c->n * per;
+    XP_TRY(stage_input(c, s, src, s.in_slot[slot]));
+  } else {
+    XP_TRY(flag_wait(c, s, &s.flags[0], u));
+  }
+  TraceRec* rec = nullptr;
+  XP_TRY(trace_slot(c, s, &rec));
+  if (rec) XP_TRY(check_launch(c, launch_trace_begin(s.ds, rec, k, 0, (int)t, (int)j, sf, bw, s.stream), "trace"));
+  if (bw) s.host_fver = s.host_ver;
+  void* Wf = s.pf[s.host_fver & 1];
+  const void* x = s.in_slot[slot];
+  for (size_t b = 0; b < s.plan.blocks.size(); ++b) {
+    const Block& B = s.plan.blocks[b];
+    if (B.kind == BK_XENT) {
+      const int32_t* y = c->y_dev + (u - c->call_first) * c->n;
+      float* loss = c->loss_dev + (u - c->call_first);
+      XP_TRY(check_launch(c, launch_xent_f32((const float*)x, y, s.dz[slot], loss, c->n, B.out.c,
+                                             (float)(1.0 / (double)c->N), s.stream), "xent"));
+      continue;
+    }
+    XP_TRY(block_forward(c, s, b, x, Wf, slot));
+    x = s.out[b][slot];
+  }
+  if (k + 1 < c->K) {
+    StageRT& nx = c->S[k + 1];
+    XP_TRY(flag_wait(c, s, &s.flags[2], u - nx.S));  // ring credit: consumer released u - R
+    const size_t bytes = s.plan.out_bytes;
+    XP_CUDA(c, cudaMemcpyAsync(nx.in_slot[(u - 1) % nx.S], x, bytes, cudaMemcpyDefault, s.stream));
+    XP_TRY(flag_write(c, s, &nx.flags[0], u));
+  }
+  if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
+  return XP_OK;
+}
+
+int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
+  StageRT& s = c->S[k];
+  const int64_t t = (u - 1) / c->T + 1, j = u - (t - 1) * c->T;
+  const int slot = (int)((u - 1) % s.S);
+  const int sb = version_difference(c, k, 1);
+  const bool bw = (j == 1);
+  cudaSetDevice(s.dev);
+  if (k + 1 < c->K) XP_TRY(flag_wait(c, s, &s.flags[1], u));
+  TraceRec* rec = nullptr;
+  XP_TRY(trace_slot(c, s, &rec));
+  if (rec) XP_TRY(check_launch(c, launch_trace_begin(s.ds, rec, k, 1, (int)t, (int)j, sb, bw, s.stream), "trace"));
+  if (bw) s.host_bver = s.host_ver;
+  const bool accumulate = (j != 1);
+  // gradient of the stage output
+  const void* dy = (k + 1 < c->K) ? s.gin_slot[slot] : (const void*)s.dz[slot];
+  int pp = 0;
+  const int nb = (int)s.plan.blocks.size();
+  for (int b = nb - 1; b >= 0; --b) {
+    const Block& B = s.plan.blocks[b];
+    if (B.kind == BK_XENT) continue;
+    const void* x = b == 0 ? s.in_slot[slot] : s.out[b - 1][slot];
+    const bool need_dx = !(b == 0 && k == 0);
+    void* dx = need_dx ? s.gbuf[pp] : nullptr;
+    XP_TRY(block_backward(c, s, b, x, dy, dx, s.pb, slot, accumulate));
+    dy = dx;
+    pp ^= 1;
+  }
+  if (k + 1 < c->K) XP_TRY(flag_write(c, s, &c->S[k + 1].flags[3], u));  // released gin slot u
+  if (k > 0) {
+    StageRT& pv = c->S[k - 1];
+    XP_TRY(flag_wait(c, s, &s.flags[3], u - pv.S));
+    XP_CUDA(c, cudaMemcpyAsync(pv.gin_slot[(u - 1) % pv.S], dy, s.plan.in_bytes, cudaMemcpyDefault, s.stream));
+    XP_TRY(flag_write(c, s, &pv.flags[1], u));
+    XP_TRY(flag_write(c, s, &pv.flags[2], u));  // released our input slot u
+  }
+  if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
+  if (j == c->T) {
+    // the T-th micro-batch's backward ends the mini-batch: update + prediction (K1)
+    TraceRec* urec = nullptr;
+    XP_TRY(trace_slot(c, s, &urec));
+    XP_TRY(check_launch(c, launch_bump(s.ds, urec, k, (int)t, c->T, s.stream), "bump"));
+    const int nv = s.host_ver + 1;
+    const float sf = (float)version_difference(c, k, 0), sbf = (float)sb;
+    const bool bf16 = c->cfg.precision == XP_BF16;
+    XP_TRY(prof_begin(c, s));
+    XP_TRY(check_launch(c, launch_sweep(s.W, s.g, s.m, s.v, s.pf[nv & 1], s.pb, s.plan.P, s.ds, nullptr, sf, sbf, bf16,
+                                        c->cfg.delta_form, true, s.stream), "sweep"));
+    XP_TRY(prof_end(c, s, XP_PROF_SWEEP, (double)s.plan.P * (bf16 ? 32.0 : 36.0)));
+    s.host_ver = nv;
+    if (c->cfg.snapshots) {
+      if (s.snap_pool.empty()) return set_err(c, XP_ESCHED, "snapshot pool (internal)");
+      Snapshot sn{nv, {}, s.snap_pool.back()};
+      s.snap_pool.pop_back();
+      XP_CUDA(c, cudaMemcpyAsync(sn.pinned, s.W, s.plan.P * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      s.snaps.push_back(std::move(sn));
+    }
+  }
+  return XP_OK;
+}
+
+// host enqueue loop: every stage's program in order, as far as fed micro-batches allow
+int drive(xpipe_ctx* c, int64_t total) {
+  for (int k = 0; k < c->K; ++k) {
+    StageRT& s = c->S[k];
+    while (!s.done) {
+      int op;
+      int64_t u;
+      program_op(c, k, s.pos, &op, &u);
+      if (total >= 0 && u > total) {
+        if (op == 1 || c->cfg.schedule == XP_SCHED_GPIPE) { s.done = true; break; }
+        ++s.pos;  // flushing: forwards beyond the last fed micro-batch are dropped
+        continue;
+      }
+      if (u > c->fed) break;  // needs a micro-batch not fed yet
+      XP_TRY(op == 0 ? enqueue_forward(c, k, u) : enqueue_backward(c, k, u));
+      ++s.pos;
+    }
+  }
+  return XP_OK;
+}
+
+int sync_all(xpipe_ctx* c) {
+  const int ms = c->cfg.watchdog_ms > 0 ? c->cfg.watchdog_ms : 120000;
+  auto t0 = std::chrono::steady_clock::now();
+  for (auto& s : c->S) {
+    cudaSetDevice(s.dev);
+    for (;;) {
+      cudaError_t e = cudaStreamQuery(s.stream);
+      if (e == cudaSuccess) break;
+      if (e != cudaErrorNotReady) return set_err(c, XP_ECUDA, std::string("stream: ") + cudaGetErrorString(e));
+      if (std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count() > ms)
+        return set_err(c, XP_ESCHED, "pipeline watchdog: stage " + std::to_string(s.k) + " did not drain");
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
+  return XP_OK;
+}
+
+int ensure_call_buffers(xpipe_ctx* c, int64_t M) {
+  const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
+  const int64_t xs = M * c->N * per, ys = M * c->N, ls = M * c->T;
+  if (xs > c->x_cap || ys > c->y_cap || ls > c->loss_cap) {
+    XP_TRY(sync_all(c));
+    if (xs > c->x_cap) { c->x_dev = (float*)dmalloc(c, xs * 4, c->S[0].dev); c->x_cap = xs; }
+    if (ys > c->y_cap) { c->y_dev = (int32_t*)dmalloc(c, ys * 4, c->S[c->K - 1].dev); c->y_cap = ys; }
+    if (ls > c->loss_cap) { c->loss_dev = (float*)dmalloc(c, ls * 4, c->S[c->K - 1].dev); c->loss_cap = ls; }
+    if (!c->x_dev || !c->y_dev || !c->loss_dev) return set_err(c, XP_ENOMEM, "call buffers");
+  }
+  return XP_OK;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------------------
+// C ABI
+// ----------------------------------------------------------------------------------------
+extern "C" {
+
+const char* xpipe_last_error(const xpipe_ctx* h) { return h ? h->err.c_str() : g_init_error.c_str(); }
+
+int xpipe_finalize(xpipe_ctx* h) {
+  if (!h) return XP_OK;
+  free_all(h);
+  delete h;
+  return XP_OK;
+}
+
+int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int32_t T, int32_t N, float lr,
+               const float betas[2], float eps, const xpipe_config* cfg, xpipe_ctx** out) {
+  if (!out) return set_err(nullptr, XP_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!layers || n_layers < 2 || !cfg || !betas) return set_err(nullptr, XP_EINVAL, "layers/cfg/betas required");
+  if (stages < 1 || stages > 64 || T < 1 || N < 1 || N % T) return set_err(nullptr, XP_EINVAL, "mini_batch % micro_batches != 0");
+  if (!(lr > 0) || !(betas[0] >= 0 && betas[0] < 1) || !(betas[1] >= 0 && betas[1] < 1) || !(eps > 0))
+    return set_err(nullptr, XP_EINVAL, "hyperparameters: lr > 0, betas in [0,1), eps > 0");
+  if (cfg->moment_init == XP_MOM_GIVEN && (cfg->delta_form != XP_DELTA_PAPER || !cfg->init_m || !cfg->init_v))
+    return set_err(nullptr, XP_EINVAL, "XP_MOM_GIVEN requires XP_DELTA_PAPER and init_m/init_v (R2)");
+  if (cfg->precision != XP_FP32 && cfg->precision != XP_BF16) return set_err(nullptr, XP_EINVAL, "precision");
+  if (cfg->schedule != XP_SCHED_XPIPE && cfg->schedule != XP_SCHED_GPIPE) return set_err(nullptr, XP_EINVAL, "schedule");
+  if (cfg->predict < 0 || cfg->predict > 2 || (cfg->predict == XP_PRED_FIXED && (cfg->s_fwd < 0 || cfg->s_bwd < 0)))
+    return set_err(nullptr, XP_EINVAL, "predict");
+  std::unique_ptr<xpipe_ctx> c(new xpipe_ctx());
+  c->cfg = *cfg;
+  if (!c->cfg.seed) c->cfg.seed = 1;
+  c->K = stages; c->T = T; c->N = N; c->n = N / T;
+  c->lr = lr; c->b1 = betas[0]; c->b2 = betas[1]; c->eps = eps;
+  std::string perr;
+  int r = build_net_plan(layers, n_layers, stages, c->cfg, c->n, &c->net, &perr);
+  if (r != XP_OK) return set_err(nullptr, r, perr);
+  if (!load_driver_entry_points()) return set_err(nullptr, XP_ECUDA, "CUDA driver stream memory operations unavailable");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return set_err(nullptr, XP_ECUDA, "no CUDA device");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  c->S.resize(stages);
+  for (int k = 0; k < stages; ++k) {
+    StageRT& s = c->S[k];
+    s.k = k;
+    s.dev = c->cfg.n_devices > 0 ? c->cfg.devices[k % c->cfg.n_devices] : cur;
+    if (s.dev < 0 || s.dev >= ndev) return set_err(nullptr, XP_EINVAL, "device id out of range");
+    s.plan = c->net.stages[k];
+    s.S = c->cfg.schedule == XP_SCHED_GPIPE ? T : (stages - k);
+  }
+  // peer access between the devices of neighbouring stages
+  for (int k = 0; k + 1 < stages; ++k) {
+    int a = c->S[k].dev, b = c->S[k + 1].dev;
+    if (a == b) continue;
+    int ok = 0;
+    cudaDeviceCanAccessPeer(&ok, a, b);
+    if (!ok) return set_err(nullptr, XP_EUNSUPPORTED, "no peer access between stage devices");
+    cudaSetDevice(a); cudaDeviceEnablePeerAccess(b, 0); cudaGetLastError();
+    cudaSetDevice(b); cudaDeviceEnablePeerAccess(a, 0); cudaGetLastError();
+  }
+  xpipe_ctx* cp = c.get();
+  auto fail_init = [&](int code, const std::string& m) {
+    std::string msg = m + (cp->err.empty() ? "" : (": " + cp->err));
+    free_all(cp);
+    return set_err(nullptr, code, msg);
+  };
+  for (int k = 0; k < stages; ++k) {
+    StageRT& s = c->S[k];
+    cudaSetDevice(s.dev);
+    if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
+    int rr = allocate_stage(cp, s);
+    if (rr != XP_OK) return fail_init(rr, "stage allocation");
+    rr = init_stage_params(cp, s, layers);
+    if (rr != XP_OK) return fail_init(rr, "parameter init");
+  }
+  for (auto& s : c->S) {
+    cudaSetDevice(s.dev);
+    if (cudaStreamSynchronize(s.stream) != cudaSuccess) return fail_init(XP_ECUDA, "init sync");
+  }
+  cudaSetDevice(cur);
+  *out = c.release();
+  return XP_OK;
+}
+
+int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32_t flags, xpipe_stats* st) {
+  if (!c) return set_err(nullptr, XP_EINVAL, "ctx is NULL");
+  if (c->poisoned) return XP_ESTATE;
+  if (M < 0 || (M > 0 && (!x || !y))) return set_err(c, XP_EINVAL, "x/y");
+  const bool dev_ptrs = flags & XP_DEVICE_PTRS;
+  if (!dev_ptrs && M > 0)
+    for (int64_t i = 0; i < (int64_t)M * c->N; ++i)
+      if (y[i] < 0 || y[i] >= c->cfg.classes) return set_err(c, XP_EINVAL, "label out of range");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  const int64_t k0 = c->kernels;
+  // previous call's work must be done before its call buffers are overwritten
+  XP_TRY(sync_all(c));
+  if (M > 0) {
+    XP_TRY(ensure_call_buffers(c, M));
+    const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
+    StageRT& s0 = c->S[0];
+    StageRT& sl = c->S[c->K - 1];
+    cudaSetDevice(s0.dev);
+    XP_CUDA(c, cudaMemcpyAsync(c->x_dev, x, (size_t)M * c->N * per * 4, dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.stream));
+    cudaSetDevice(sl.dev);
+    XP_CUDA(c, cudaMemcpyAsync(c->y_dev, y, (size_t)M * c->N * 4, dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sl.stream));
+    XP_CUDA(c, cudaMemsetAsync(c->loss_dev, 0xff, (size_t)M * c->T * 4, sl.stream));  // NaN = not computed
+    c->call_first = c->fed + 1;
+    c->fed += (int64_t)M * c->T;
+  }
+  for (auto& s : c->S) { s.ev_used = 0; s.prof_cls.clear(); s.prof_work.clear(); }
+  XP_TRY(reserve_for_call(c, M));
+  XP_TRY(drive(c, -1));
+  if (flags & XP_FLUSH) {
+    XP_TRY(drive(c, c->fed));
+    for (auto& s : c->S) {
+      if (!s.done) return set_err(c, XP_ESCHED, "flush did not drain stage " + std::to_string(s.k));
+      s.done = false;
+      s.pos = 0;
+    }
+    c->base = c->fed;
+  }
+  int rr = XP_OK;
+  if (!(flags & XP_ASYNC)) rr = sync_all(c);
+  if (rr != XP_OK) return rr;
+  if (st) {
+    st->kernel_launches = c->kernels - k0;
+    st->span_ms = 0;
+    for (int q = 0; q < XP_PROF_N; ++q) { st->prof_ms[q] = 0; st->prof_launches[q] = 0; st->prof_work[q] = 0; }
+    if (c->cfg.profile && !(flags & XP_ASYNC)) {
+      for (auto& s : c->S) {
+        for (size_t i = 0; i < s.prof_cls.size(); ++i) {
+          float ms = 0;
+          cudaEventElapsedTime(&ms, s.ev_pool[2 * i], s.ev_pool[2 * i + 1]);
+          const int q = s.prof_cls[i];
+          st->prof_ms[q] += ms;
+          st->prof_launches[q]++;
+          st->prof_work[q] += s.prof_work[i];
+        }
+      }
+    }
+    if (st->losses && M > 0 && !(flags & XP_ASYNC)) {
+      cudaSetDevice(c->S[c->K - 1].dev);
+      XP_CUDA(c, cudaMemcpy(st->losses, c->loss_dev, (size_t)M * c->T * 4, cudaMemcpyDeviceToHost));
+    }
+  }
+  cudaSetDevice(cur);
+  return XP_OK;
+}
+
+int xpipe_sync(xpipe_ctx* c) {
+  if (!c) return set_err(nullptr, XP_EINVAL, "ctx is NULL");
+  if (c->poisoned) return XP_ESTATE;
+  return sync_all(c);
+}
+
+int xpipe_stage_of_layer(xpipe_ctx* c, int32_t layer) {
+  if (!c || layer < 0 || layer >= (int)c->net.layers.size()) return set_err(c, XP_EINVAL, "layer");
+  return c->net.layers[layer].stage;
+}
+
+int xpipe_stage_version(xpipe_ctx* c, int32_t stage) {
+  if (!c || stage < 0 || stage >= c->K) return set_err(c, XP_EINVAL, "stage");
+  return c->S[stage].host_ver;
+}
+
+int64_t xpipe_stage_params(xpipe_ctx* c, int32_t stage) {
+  if (!c || stage < 0 || stage >= c->K) return set_err(c, XP_EINVAL, "stage");
+  return c->S[stage].plan.P;
+}
+
+int xpipe_get_weights(xpipe_ctx* c, int32_t layer, int32_t tensor, int32_t state, int64_t version, float* dst,
+                      size_t count) {
+  if (!c || !dst) return set_err(c, XP_EINVAL, "args");
+  if (c->poisoned) return XP_ESTATE;
+  if (layer < 0 || layer >= (int)c->net.layers.size()) return set_err(c, XP_EINVAL, "layer");
+  const LayerInfo& L = c->net.layers[layer];
+  if (tensor != XP_T_WEIGHT && tensor != XP_T_BIAS) return set_err(c, XP_EINVAL, "tensor");
+  const int64_t n = tensor == XP_T_WEIGHT ? L.nw_torch : L.nb;
+  if ((int64_t)count != n) return set_err(c, XP_EINVAL, "count is not the tensor size");
+  if (n == 0) return XP_OK;
+  XP_TRY(sync_all(c));
+  StageRT& s = c->S[L.stage];
+  const int64_t off = tensor == XP_T_WEIGHT ? L.woff : L.boff;
+  const int64_t ng = tensor == XP_T_WEIGHT ? L.nw_gpu : L.nb;
+  std::vector<float> buf(ng);
+  cudaSetDevice(s.dev);
+  const bool bf16 = c->cfg.precision == XP_BF16;
+  if (state == XP_S_PRED_FWD || state == XP_S_PRED_BWD) {
+    const void* src = state == XP_S_PRED_FWD ? s.pf[s.host_ver & 1] : s.pb;
+    if (bf16) {
+      std::vector<uint16_t> hb(ng);
+      XP_CUDA(c, cudaMemcpy(hb.data(), (const __nv_bfloat16*)src + off, ng * 2, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < ng; ++i) { uint32_t u = (uint32_t)hb[i] << 16; std::memcpy(&buf[i], &u, 4); }
+    } else {
+      XP_CUDA(c, cudaMemcpy(buf.data(), (const float*)src + off, ng * 4, cudaMemcpyDeviceToHost));
+    }
+  } else {
+    const float* src = nullptr;
+    if (state == XP_S_PARAM && version >= 0 && version != s.host_ver) {
+      if (version == 0 || !c->cfg.snapshots) {
+        if (!c->cfg.snapshots) return set_err(c, XP_EINVAL, "snapshots disabled");
+      }
+      const Snapshot* sn = nullptr;
+      for (auto& q : s.snaps) if (q.ver == version) sn = &q;
+      if (!sn) return set_err(c, XP_EINVAL, "no snapshot of that version");
+      std::memcpy(buf.data(), sn->pinned + off, ng * 4);
+    } else {
+      switch (state) {
+        case XP_S_PARAM: src = s.W; break;
+        case XP_S_M: src = s.m; break;
+        case XP_S_V: src = s.v; break;
+        case XP_S_GRAD: src = s.g; break;
+        default: return set_err(c, XP_EINVAL, "state");
+      }
+      XP_CUDA(c, cudaMemcpy(buf.data(), src + off, ng * 4, cudaMemcpyDeviceToHost));
+    }
+  }
+  gpu_to_torch_layout(L, tensor, buf.data(), dst);
+  return XP_OK;
+}
+
+int xpipe_get_trace(xpipe_ctx* c, int32_t stage, xpipe_trace_rec* dst, size_t cap, size_t* n_out) {
+  if (!c || !n_out || stage < 0 || stage >= c->K) return set_err(c, XP_EINVAL, "args");
+  if (c->poisoned) return XP_ESTATE;
+  XP_TRY(sync_all(c));
+  StageRT& s = c->S[stage];
+  *n_out = (size_t)s.trace_n;
+  if (dst && s.trace_n) {
+    cudaSetDevice(s.dev);
+    const size_t n = std::min(cap, (size_t)s.trace_n);
+    static_assert(sizeof(TraceRec) == sizeof(xpipe_trace_rec), "trace layout");
+    XP_CUDA(c, cudaMemcpy(dst, s.trace_dev, n * sizeof(TraceRec), cudaMemcpyDeviceToHost));
+  }
+  return XP_OK;
+}
+
+int xpipe_adam_predict(float* W, const float* g, float* m, float* v, void* pred_f, void* pred_b, int64_t n,
+                       int64_t version, float lr, float beta1, float beta2, float eps, int32_t s_f, int32_t s_b,
+                       int32_t pred_bf16, int32_t delta_form, void* stream) {
+  if (!W || !g || !m || !v || n < 0 || version < 1) return set_err(nullptr, XP_EINVAL, "adam_predict args");
+  if (((uintptr_t)W | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) return set_err(nullptr, XP_EINVAL, "alignment");
+  SweepScalars hs;
+  host_scalars(version, lr, beta1, beta2, eps, &hs);
+  cudaError_t e = launch_sweep(W, g, m, v, pred_f, pred_b, n, nullptr, &hs, (float)s_f, (float)s_b, pred_bf16 != 0,
+                               delta_form, true, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_err(nullptr, XP_ECUDA, cudaGetErrorString(e));
+  return XP_OK;
+}
+
+}  // extern "C"

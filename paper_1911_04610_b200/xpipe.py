@@ -1,0 +1,270 @@
+"""Thin ctypes binding of libxpipe.so (include/xpipe.h).  Argument marshalling only: every
+step of the hot path runs in the library's CUDA kernels.  PyTorch is used for device memory
+(the allocator hooks route to torch's caching allocator) and nothing else.
+
+Fails loudly when the extension is missing -- there is no CPU fallback.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libxpipe.so")
+
+XP_OK, XP_EINVAL, XP_ENOMEM, XP_ECUDA, XP_ECOMM, XP_ESCHED, XP_ENONFINITE, XP_ESTATE, XP_EUNSUPPORTED = \
+    0, -1, -2, -3, -4, -5, -6, -7, -8
+PRECISION = {"fp32": 0, "bf16": 1}
+SCHEDULE = {"xpipe": 0, "gpipe": 1}
+PREDICT = {"paper": 0, "off": 1, "fixed": 2}
+DELTA = {"adam": 0, "paper": 1}
+STATE = {"param": 0, "m": 1, "v": 2, "pred_fwd": 3, "pred_bwd": 4, "grad": 5}
+XP_FLUSH, XP_DEVICE_PTRS, XP_ASYNC = 1, 2, 4
+
+
+class Layer(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("kind", "in_c", "out_c", "kh", "kw", "sh", "sw", "ph", "pw", "bias")] + \
+               [("bn_eps", C.c_float)] + [(n, C.c_int32) for n in ("src0", "src1", "concat_off", "stage")]
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+
+
+class Config(C.Structure):
+    _fields_ = [("in_c", C.c_int32), ("in_h", C.c_int32), ("in_w", C.c_int32), ("classes", C.c_int32),
+                ("seed", C.c_uint64)] + \
+               [(n, C.c_int32) for n in ("precision", "schedule", "predict", "s_fwd", "s_bwd", "delta_form",
+                                         "moment_init", "n_devices")] + \
+               [("devices", C.c_int32 * 8)] + \
+               [(n, C.c_int32) for n in ("transport", "snapshots", "trace", "graphs", "profile", "watchdog_ms")] + \
+               [("init_params", C.POINTER(C.POINTER(C.c_float))),
+                ("init_m", C.POINTER(C.POINTER(C.c_float))),
+                ("init_v", C.POINTER(C.POINTER(C.c_float))),
+                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", C.c_void_p)]
+
+
+class TraceRec(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("stage", "op", "t", "j", "version", "s", "bellwether", "wbuf")] + \
+               [("t0_ns", C.c_uint64), ("t1_ns", C.c_uint64)]
+
+
+PROF_CLASSES = ("sweep", "conv_fprop", "conv_dgrad", "conv_wgrad")
+
+
+class Stats(C.Structure):
+    _fields_ = [("span_ms", C.c_double), ("prof_ms", C.c_double * 4), ("prof_launches", C.c_int64 * 4),
+                ("prof_work", C.c_double * 4), ("kernel_launches", C.c_int64), ("losses", C.POINTER(C.c_float))]
+
+    def profile(self):
+        return {n: dict(ms=self.prof_ms[i], launches=self.prof_launches[i], work=self.prof_work[i])
+                for i, n in enumerate(PROF_CLASSES)}
+
+
+_lib = None
+
+
+def lib():
+    """Load libxpipe.so; raise if it was not built (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise ImportError("libxpipe.so not built: run paper_1911_04610_b200/build.py (no CPU fallback)")
+        L = C.CDLL(SO_PATH)
+        vp, i32, i64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+        L.xpipe_init.argtypes = [C.POINTER(Layer), i32, i32, i32, i32, f32, C.POINTER(f32), f32, C.POINTER(Config),
+                                 C.POINTER(vp)]
+        L.xpipe_step.argtypes = [vp, vp, vp, i32, C.c_uint32, C.POINTER(Stats)]
+        L.xpipe_sync.argtypes = [vp]
+        L.xpipe_get_weights.argtypes = [vp, i32, i32, i32, i64, vp, C.c_size_t]
+        L.xpipe_get_trace.argtypes = [vp, i32, vp, C.c_size_t, C.POINTER(C.c_size_t)]
+        L.xpipe_stage_of_layer.argtypes = [vp, i32]
+        L.xpipe_stage_version.argtypes = [vp, i32]
+        L.xpipe_stage_params.argtypes = [vp, i32]
+        L.xpipe_stage_params.restype = i64
+        L.xpipe_finalize.argtypes = [vp]
+        L.xpipe_last_error.argtypes = [vp]
+        L.xpipe_last_error.restype = C.c_char_p
+        L.xpipe_adam_predict.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, f32, f32, f32, f32, i32, i32, i32, i32, vp]
+        L.xpipe_gemm_bf16.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i64, vp]
+        L.xpipe_conv2d_bf16.argtypes = [i32, C.POINTER(i32), vp, vp, vp, i32, vp, i64, vp]
+        _lib = L
+    return _lib
+
+
+class XPipeError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("xpipe error %d: %s" % (code, msg))
+        self.code = code
+
+
+def _check(r, h=None):
+    if r < 0:
+        raise XPipeError(r, lib().xpipe_last_error(h).decode())
+    return r
+
+
+def _torch_allocator():
+    import torch
+
+    def alloc(nbytes, device, user):
+        return torch.cuda.caching_allocator_alloc(int(nbytes), device=int(device))
+
+    def free(ptr, nbytes, device, user):
+        torch.cuda.caching_allocator_delete(ptr)
+    return ALLOC_FN(alloc), FREE_FN(free)
+
+
+def _ptr(a):
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class XPipe:
+    """One pipeline context: xpipe_init / xpipe_step / xpipe_get_weights / xpipe_get_trace /
+    xpipe_finalize."""
+
+    def __init__(self, layers, stages, micro_batches, mini_batch, lr, betas, eps, in_shape, classes, params=None,
+                 precision="fp32", schedule="xpipe", predict="paper", s_fwd=0, s_bwd=0, delta="adam",
+                 init_m=None, init_v=None, devices=None, snapshots=False, trace=False, graphs=False, profile=False,
+                 seed=1, watchdog_ms=0, torch_allocator=True):
+        self.h = None
+        L = lib()
+        self.layers = list(layers)
+        arr = (Layer * len(self.layers))()
+        for i, l in enumerate(self.layers):
+            for f, _ in Layer._fields_:
+                setattr(arr[i], f, getattr(l, f))
+        self._keep = []
+        cfg = Config(in_c=in_shape[0], in_h=in_shape[1], in_w=in_shape[2], classes=classes, seed=seed,
+                     precision=PRECISION[precision], schedule=SCHEDULE[schedule], predict=PREDICT[predict],
+                     s_fwd=s_fwd, s_bwd=s_bwd, delta_form=DELTA[delta], snapshots=int(snapshots), trace=int(trace),
+                     graphs=int(graphs), profile=int(profile), watchdog_ms=watchdog_ms)
+        if devices:
+            cfg.n_devices = len(devices)
+            for i, d in enumerate(devices):
+                cfg.devices[i] = d
+
+        def table(src):
+            tab = (C.POINTER(C.c_float) * (2 * len(self.layers)))()
+            for i, pair in enumerate(src):
+                for t, a in enumerate(pair):
+                    if a is not None:
+                        a = np.ascontiguousarray(a, dtype=np.float32).ravel()
+                        self._keep.append(a)
+                        tab[2 * i + t] = a.ctypes.data_as(C.POINTER(C.c_float))
+            self._keep.append(tab)
+            return tab
+        if params is not None:
+            cfg.init_params = table(params)
+        if init_m is not None:
+            cfg.moment_init = 1
+            cfg.init_m = table(init_m)
+            cfg.init_v = table(init_v)
+        if torch_allocator:
+            self._alloc = _torch_allocator()
+            cfg.alloc, cfg.free = self._alloc
+        b = (C.c_float * 2)(*betas)
+        h = C.c_void_p()
+        r = L.xpipe_init(arr, len(self.layers), stages, micro_batches, mini_batch, lr, b, eps, C.byref(cfg),
+                         C.byref(h))
+        _check(r, None)
+        self.h = h
+        self.K, self.T, self.N = stages, micro_batches, mini_batch
+        self.in_shape, self.classes = tuple(in_shape), classes
+
+    def close(self):
+        if self.h:
+            lib().xpipe_finalize(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, x, y, M, flush=False, async_=False, losses=True):
+        """x: [M*N, C, H, W] float32, y: [M*N] int32 -- numpy (host) or torch CUDA tensors (device)."""
+        flags = (XP_FLUSH if flush else 0) | (XP_ASYNC if async_ else 0)
+        if hasattr(x, "is_cuda") and x.is_cuda:
+            flags |= XP_DEVICE_PTRS
+        else:
+            x = np.ascontiguousarray(x, dtype=np.float32)
+            y = np.ascontiguousarray(y, dtype=np.int32)
+        st = Stats()
+        out = None
+        if losses and not async_:
+            out = np.empty(M * self.T, dtype=np.float32)
+            st.losses = out.ctypes.data_as(C.POINTER(C.c_float))
+        _check(lib().xpipe_step(self.h, _ptr(x), _ptr(y), M, flags, C.byref(st)), self.h)
+        self.last_stats = st
+        return out
+
+    def sync(self):
+        _check(lib().xpipe_sync(self.h), self.h)
+
+    def get(self, layer, tensor=0, state="param", version=-1, count=None):
+        if count is None:
+            count = self._count(layer, tensor)
+        out = np.empty(count, dtype=np.float32)
+        _check(lib().xpipe_get_weights(self.h, layer, tensor, STATE[state], version, _ptr(out), count), self.h)
+        return out
+
+    def _count(self, layer, tensor):
+        l = self.layers[layer]
+        kinds_w = {1: lambda: l.out_c * l.in_c, 2: lambda: l.out_c * l.in_c * l.kh * l.kw, 3: lambda: l.in_c}
+        if tensor == 0:
+            return kinds_w[l.kind]() if l.kind in kinds_w else 0
+        if l.kind == 3:
+            return l.in_c
+        return l.out_c if (l.kind in (1, 2) and l.bias) else 0
+
+    def params_flat(self, state="param", version=-1):
+        parts = []
+        for i in range(len(self.layers)):
+            for t in (0, 1):
+                n = self._count(i, t)
+                if n:
+                    parts.append(self.get(i, t, state, version, n))
+        return np.concatenate(parts)
+
+    def stage_of(self, layer):
+        return _check(lib().xpipe_stage_of_layer(self.h, layer), self.h)
+
+    def version(self, stage):
+        return _check(lib().xpipe_stage_version(self.h, stage), self.h)
+
+    def stage_params(self, stage):
+        return lib().xpipe_stage_params(self.h, stage)
+
+    def trace(self, stage, timestamps=False):
+        n = C.c_size_t()
+        _check(lib().xpipe_get_trace(self.h, stage, None, 0, C.byref(n)), self.h)
+        buf = (TraceRec * max(1, n.value))()
+        _check(lib().xpipe_get_trace(self.h, stage, buf, n.value, C.byref(n)), self.h)
+        f = [x for x, _ in TraceRec._fields_][:7 + (3 if timestamps else 0)]
+        return [tuple(getattr(buf[i], q) for q in f) for i in range(n.value)]
+
+
+def adam_predict(W, g, m, v, pf, pb, version, lr, betas, eps, s_f, s_b, pred_bf16, delta="adam", stream=None):
+    """K1 on torch CUDA tensors (in place on W, m, v)."""
+    n = W.numel()
+    _check(lib().xpipe_adam_predict(_ptr(W), _ptr(g), _ptr(m), _ptr(v), _ptr(pf) if pf is not None else None,
+                                    _ptr(pb) if pb is not None else None, n, version, lr, betas[0], betas[1], eps,
+                                    s_f, s_b, int(pred_bf16), DELTA[delta],
+                                    C.c_void_p(stream) if stream else None))
+
+
+def gemm_bf16(A, B, D, M, N, K, a_kmajor=True, b_kmajor=True, ldd=None, stream=None):
+    _check(lib().xpipe_gemm_bf16(_ptr(A), _ptr(B), _ptr(D), M, N, K, int(a_kmajor), int(b_kmajor),
+                                 ldd if ldd is not None else N, C.c_void_p(stream) if stream else None))
+
+
+def conv2d_bf16(mode, geo, in0, in1, out, accumulate=False, ws=None, stream=None):
+    """mode 1 fprop / 2 dgrad / 3 wgrad; geo = (Nimg, H, W, C, Co, R, S, P, Q, sh, sw, ph, pw)."""
+    g = (C.c_int32 * 13)(*geo)
+    _check(lib().xpipe_conv2d_bf16(mode, g, _ptr(in0), _ptr(in1), _ptr(out), int(accumulate),
+                                   _ptr(ws) if ws is not None else None, ws.numel() if ws is not None else 0,
+                                   C.c_void_p(stream) if stream else None))

@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""bench.py -- XPipe hot path on B200: pipeline samples/s (BASELINE.json metric) with the
+dominant kernel's roofline, the end-to-end number through the public API, and the CPU oracle
+as the reported baseline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload vgg16|mlp|sweep] [--minibatches M] [--stages S]
+
+A step = one xpipe_step call feeding M mini-batches (N=128 samples, T=4 micro-batches of 32)
+into the running pipeline: every row of the hot path (schedule, Eq. (1)/(2) staleness, W_hat
+materialisation, stage conv/linear compute under W_hat, hand-offs, loss, backward, the fused
+Adam+prediction sweep) runs on the GPU.  Inputs already resident in HBM for `value`; `e2e`
+feeds host (pinned) buffers through the same API call with the H2D copies inside.
+Stages K = number of GPUs unless --stages is given (config C2 names 4 stages: --stages 4 on
+one GPU maps the 4 stages onto one device).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pipeline samples/sec (VGG-16 synthetic CIFAR-10, XPipe Adam+prediction)"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+class Clocks:
+    """Sample nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.samples, self.stop_ev = device, [], threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop_ev.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.samples.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self.stop_ev.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 5 + i and s[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_model(name):
+    import synthetic as S
+    if name == "mlp":
+        return S.mlp(), (784, 1, 1), 10, "mnist", 32, 4, "fp32"
+    return S.vgg16_cifar(), (3, 32, 32), 10, "cifar", 128, 4, "bf16"
+
+
+def cpu_baseline(workload, seconds=20.0):
+    """The oracle as it stands, on this host's cores: one micro-batch at a time of the same
+    workload (K=1 stage, bf16 emulation for VGG-16 / fp32 for the MLP), bounded to ~seconds."""
+    import oracle
+    import synthetic as S
+    L, shape, classes, kind, N, T, prec = workload_model(workload)
+    n = N // T
+    P = S.make_params(L, 1)
+    o = oracle.Oracle(L, 1, 1, n, 1e-4, (0.9, 0.999), 1e-8, shape, classes, P, mode=prec)
+    x, y = S.make_inputs(n, shape, classes, 1, kind=kind)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        o.step(x, y, 1, flush=True)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or (done >= 1 and el * (done + 1) / done > 3 * seconds):
+            break
+    cores = os.cpu_count()
+    return {"value": done * n / el, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "sample": "%d micro-batch(es) of %d samples through the oracle (%s, K=1, fwd+bwd+update), %.1f s"
+                      % (done, n, "bf16 emulation" if prec == "bf16" else "fp32", el)}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed as it stands (the reference arm of this tier)."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    import synthetic as S
+    oracle.build()
+    L, shape, classes, kind, N, T, prec = workload_model(args.workload)
+    n = N // T
+    P = S.make_params(L, 1)
+    o = oracle.Oracle(L, 1, 1, n, 1e-4, (0.9, 0.999), 1e-8, shape, classes, P, mode=prec)
+    x, y = S.make_inputs(n, shape, classes, 1, kind=kind)
+    for _ in range(args.warmup):
+        o.step(x, y, 1, flush=True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.step(x, y, 1, flush=True)
+    el = time.perf_counter() - t0
+    v = args.steps * n / el
+    cfg = {"workload": "%s (oracle sample: one %d-sample micro-batch per step, K=1)" % (args.workload, n)}
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1000 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": "%d steps x %d samples" % (args.steps, n)},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_sweep(args, peaks, peak_kind):
+    """Config 5: the fused Adam+prediction sweep alone (kernel-level metric)."""
+    import torch
+    from paper_1911_04610_b200 import adam_predict
+    n = args.sweep_params
+    dev = torch.device("cuda", 0)
+    W = torch.rand(n, device=dev) * 0.1 - 0.05
+    g = torch.rand(n, device=dev) * 2e-2 - 1e-2
+    m = (torch.rand(n, device=dev) * 2e-2 - 1e-2) * 0.1
+    v = torch.rand(n, device=dev) * 9.9e-5 + 1e-6
+    pf = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    pb = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    for i in range(args.warmup):
+        adam_predict(W, g, m, v, pf, pb, i + 1, 1e-4, (0.9, 0.999), 1e-8, 3, 1, True, stream=st)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(0) as ck:
+        e0.record()
+        for i in range(args.steps):
+            adam_predict(W, g, m, v, pf, pb, args.warmup + i + 1, 1e-4, (0.9, 0.999), 1e-8, 3, 1, True, stream=st)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    gbs = n * 32 / (ms * 1e-3) / 1e9
+    peak = peaks["hbm_gbs"]
+    return {"metric": "Adam+predict sweep HBM GB/s (config 5)", "value": gbs, "unit": "GB/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "sweep P=%d, s_f=3, s_b=1, bf16 W_hat, 32 B/param" % n,
+                       "l2": "working set %d MB > 126 MB L2" % (n * 32 // 2**20)},
+            "gpu_launches": args.steps, "clocks": ck.summary(),
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "traffic": None, "peak_source": peak_kind}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="vgg16", choices=["vgg16", "mlp", "sweep"])
+    ap.add_argument("--minibatches", type=int, default=4, help="mini-batches fed per step")
+    ap.add_argument("--stages", type=int, default=0, help="pipeline stages (default = --gpus)")
+    ap.add_argument("--sweep-params", type=int, default=1 << 28)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        return run_reference(args)
+
+    ws, rank, local = dist_env()
+    import torch
+    peaks, peak_kind = load_peaks()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.workload == "sweep":
+        line = run_sweep(args, peaks, peak_kind)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        return 0
+
+    import numpy as np
+    import synthetic as S
+    from paper_1911_04610_b200 import XPipe
+    K = args.stages or args.gpus
+    L, shape, classes, kind, N, T, prec = workload_model(args.workload)
+    M = args.minibatches
+    # One process drives every stage of the pipeline through the C-ABI library (stage k on
+    # GPU k % n_gpus); the other ranks of a torchrun launch only join the barriers.
+    value = e2e = None
+    result = {}
+    if rank == 0:
+        P = S.make_params(L, 1)
+        g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
+                  devices=list(range(args.gpus)), profile=True, watchdog_ms=300000)
+        x, y = S.make_inputs(M * N, shape, classes, 1, kind=kind)
+        xd = torch.from_numpy(x).cuda(0)
+        yd = torch.from_numpy(y).cuda(0 if K == 1 else (K - 1) % args.gpus)
+        for _ in range(args.warmup):
+            g.step(xd, yd, M)
+        prof = {}
+        launches = 0
+        with Clocks(0) as ck:
+            g.timer_start()
+            for _ in range(args.steps):
+                g.step(xd, yd, M, losses=False)
+                st = g.last_stats
+                launches += st.kernel_launches
+                for name, d in st.profile().items():
+                    q = prof.setdefault(name, {"ms": 0.0, "launches": 0, "work": 0.0})
+                    q["ms"] += d["ms"]; q["launches"] += d["launches"]; q["work"] += d["work"]
+            ms = g.timer_stop()
+        clocks = ck.summary()
+        value = args.steps * M * N / (ms * 1e-3)
+        # ---- roofline of the dominant kernel class (CUDA events on the launching streams)
+        dom = max(prof, key=lambda k: prof[k]["ms"])
+        d = prof[dom]
+        if dom == "sweep":
+            ach = d["work"] / (d["ms"] * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+        else:
+            ach = d["work"] / (d["ms"] * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": peaks.get("bf16_tflops_sustained", 1400.0),
+                    "unit": "TFLOP/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["kernel"] = dom
+        roof["peak_source"] = peak_kind + (" (sustained)" if roof["bound"] == "tensor" else "")
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                tr = json.load(f).get(dom)
+            if tr is not None:
+                roof["traffic"] = tr
+        shares = {k: {"ms_per_step": v["ms"] / args.steps, "share_of_step": v["ms"] / ms,
+                      "achieved": (v["work"] / (v["ms"] * 1e-3) / (1e9 if k == "sweep" else 1e12)) if v["ms"] else 0,
+                      "unit": "GB/s" if k == "sweep" else "TFLOP/s", "launches": v["launches"]}
+                  for k, v in prof.items()}
+        # ---- end to end through the public API with host (pinned) buffers
+        if not args.no_e2e:
+            xh = torch.from_numpy(x).pin_memory()
+            yh = torch.from_numpy(y).pin_memory()
+            xh_np, yh_np = xh.numpy(), yh.numpy()
+            g.step(xh_np, yh_np, M)
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                g.step(xh_np, yh_np, M, losses=True)
+            e2e_s = time.perf_counter() - t0
+            e2e = {"value": args.steps * M * N / e2e_s, "unit": "samples/s",
+                   "h2d_bytes_per_step": int(x.nbytes + y.nbytes), "d2h_bytes_per_step": int(M * T * 4)}
+        g.close()
+        result = dict(ms=ms, clocks=clocks, roof=roof, shares=shares, launches=launches)
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([result.get("ms", 0.0)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    if rank != 0:
+        return 0
+    cpu = None if args.no_cpu_baseline else cpu_baseline(args.workload)
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": result["ms"] / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "config": {"workload": "%s, K=%d stages, mini-batch %d, T=%d micro-batches, %d mini-batches per step"
+                                   % ("VGG-16 on synthetic CIFAR-10 32x32 (BASELINE configs[1])"
+                                      if args.workload == "vgg16" else "MLP 784-256-256-256-10 (configs[0])",
+                                      K, N, T, M),
+                       "global_batch": N, "stages": K, "micro_batches": T, "minibatches_per_step": M,
+                       "parallelism": "pipeline K=%d (XPipe)" % K,
+                       "l2": "working set > L2: optimizer state 16 B/param x 14.7M params = 235 MB (126 MB L2)"},
+            "e2e": e2e, "gpu_launches": result["launches"], "clocks": result["clocks"],
+            "roofline": result["roof"], "kernel_shares": result["shares"], "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

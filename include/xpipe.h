@@ -177,6 +177,11 @@ int xpipe_stage_of_layer(struct xpipe_ctx* h, int32_t layer);
 int xpipe_stage_version(struct xpipe_ctx* h, int32_t stage);
 int64_t xpipe_stage_params(struct xpipe_ctx* h, int32_t stage);
 
+/* Device timing across every stage stream: which = 0 records a start event on each stage's
+   stream, which = 1 a stop event; after a stop, *ms_out (nullable) = max over stages of the
+   device time between the two events (CUDA events on the streams the kernels run on). */
+int xpipe_timer(struct xpipe_ctx* h, int32_t which, double* ms_out);
+
 /* NULL-safe, idempotent; frees everything the context owns. */
 int xpipe_finalize(struct xpipe_ctx* h);
 

@@ -473,6 +473,53 @@ void avgpool_bwd(const Model& M, int li, int n, const Vec& dy, Vec& dx) {
       }
 }
 
+/* AvgPool2d with zero padding counted in the divisor (PyTorch count_include_pad=True, the
+   torchvision Inception-V3 branch pool): y = (sum over the kh*kw window) * (1/(kh*kw)) */
+void avgpool2d_fwd(const Model& M, int li, int n, const Vec& x, Vec& y) {
+  const Layer& l = M.L[li];
+  const int C = l.in0.c, H = l.in0.h, Wd = l.in0.w, P = l.out.h, Q = l.out.w;
+  const double inv = 1.0 / (double)(l.d.kh * l.d.kw);
+  y.assign((size_t)n * C * P * Q, 0.0);
+  for (int s0 = 0; s0 < n; ++s0)
+    for (int c = 0; c < C; ++c)
+      for (int p = 0; p < P; ++p)
+        for (int q = 0; q < Q; ++q) {
+          double acc = 0.0;
+          float accf = 0.f;
+          for (int r = 0; r < l.d.kh; ++r)
+            for (int s = 0; s < l.d.kw; ++s) {
+              int ih = p * l.d.sh - l.d.ph + r, iw = q * l.d.sw - l.d.pw + s;
+              if (ih < 0 || ih >= H || iw < 0 || iw >= Wd) continue;
+              double v = x[(((size_t)s0 * C + c) * H + ih) * Wd + iw];
+              if (M.mode == XO_FP32) accf = accf + (float)v; else acc += v;
+            }
+          double v = (M.mode == XO_FP32) ? (double)(accf * (float)inv) : acc * inv;
+          y[(((size_t)s0 * C + c) * P + p) * Q + q] = M.qa(v, li);
+        }
+}
+
+void avgpool2d_bwd(const Model& M, int li, int n, const Vec& dy, Vec& dx) {
+  const Layer& l = M.L[li];
+  const int C = l.in0.c, H = l.in0.h, Wd = l.in0.w, P = l.out.h, Q = l.out.w;
+  const double inv = 1.0 / (double)(l.d.kh * l.d.kw);
+  dx.assign((size_t)n * C * H * Wd, 0.0);
+  for (int s0 = 0; s0 < n; ++s0)
+    for (int c = 0; c < C; ++c)
+      for (int p = 0; p < P; ++p)
+        for (int q = 0; q < Q; ++q) {
+          const double g = dy[(((size_t)s0 * C + c) * P + p) * Q + q];
+          const double gi = (M.mode == XO_FP64) ? g * inv : (double)((float)g * (float)inv);
+          for (int r = 0; r < l.d.kh; ++r)
+            for (int s = 0; s < l.d.kw; ++s) {
+              int ih = p * l.d.sh - l.d.ph + r, iw = q * l.d.sw - l.d.pw + s;
+              if (ih < 0 || ih >= H || iw < 0 || iw >= Wd) continue;
+              size_t idx = (((size_t)s0 * C + c) * H + ih) * Wd + iw;
+              dx[idx] = M.add(dx[idx], gi);
+            }
+        }
+  for (auto& v : dx) v = M.qg(v);
+}
+
 /* softmax cross-entropy (a6, R8): row max; e_i = exp(z_i - max) (fp32 modes: the exp is
    taken in double and rounded to fp32); sum in class order; p = e/sum;
    dz = (p - onehot) * (1/N) with N the mini-batch size; loss = -log p_y (reporting). */
@@ -671,6 +718,7 @@ void stage_forward(const xo_ctx& c, const Stage& st, const Vec& Wp, int n, Vec i
       }
       case XO_MAXPOOL2D: maxpool_fwd(M, li, n, src(li, 0), y, nullptr); break;
       case XO_AVGPOOL_GLOBAL: avgpool_fwd(M, li, n, src(li, 0), y); break;
+      case XO_AVGPOOL2D: avgpool2d_fwd(M, li, n, src(li, 0), y); break;
       case XO_FLATTEN: y = src(li, 0); break;
       case XO_ADD: {
         const Vec &a = src(li, 0), &b = src(li, 1);
@@ -743,6 +791,7 @@ void stage_backward(const xo_ctx& c, const Stage& st, const Vec& Wb, int n, cons
       }
       case XO_MAXPOOL2D: maxpool_bwd(M, li, n, x0, dy, dx); acc(l.src0, std::move(dx)); break;
       case XO_AVGPOOL_GLOBAL: avgpool_bwd(M, li, n, dy, dx); acc(l.src0, std::move(dx)); break;
+      case XO_AVGPOOL2D: avgpool2d_bwd(M, li, n, dy, dx); acc(l.src0, std::move(dx)); break;
       case XO_FLATTEN: acc(l.src0, Vec(dy)); break;
       case XO_ADD: acc(l.src0, Vec(dy)); acc(l.src1, Vec(dy)); break;
       case XO_CONCAT: {
@@ -939,7 +988,7 @@ int xo_init(const xo_layer* layers, int32_t n_layers, int32_t stages, int32_t T,
         if (l.d.kind == XO_SOFTMAX_XENT && (i != n_layers - 1 || x.size() != (size_t)M.classes))
           return fail(E_INVAL, "softmax-xent must be last and see [classes] logits");
         break;
-      case XO_MAXPOOL2D: {
+      case XO_MAXPOOL2D: case XO_AVGPOOL2D: {
         int P = (x.h + 2 * l.d.ph - l.d.kh) / l.d.sh + 1, Q = (x.w + 2 * l.d.pw - l.d.kw) / l.d.sw + 1;
         if (P < 1 || Q < 1 || l.d.sh < 1 || l.d.sw < 1) return fail(E_INVAL, "pool shape");
         l.out = Shape{x.c, P, Q};

@@ -31,7 +31,7 @@ extern "C" {
 #endif
 
 enum { XO_LINEAR = 1, XO_CONV2D, XO_BATCHNORM2D, XO_RELU, XO_MAXPOOL2D, XO_AVGPOOL_GLOBAL,
-       XO_FLATTEN, XO_ADD, XO_CONCAT, XO_SOFTMAX_XENT };
+       XO_FLATTEN, XO_ADD, XO_CONCAT, XO_SOFTMAX_XENT, XO_AVGPOOL2D };
 enum { XO_FP64 = 0, XO_FP32 = 1, XO_BF16 = 2 };
 enum { XO_SCHED_XPIPE = 0, XO_SCHED_GPIPE = 1 };
 enum { XO_PRED_PAPER = 0, XO_PRED_OFF = 1, XO_PRED_FIXED = 2 };

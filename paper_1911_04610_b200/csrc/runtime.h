@@ -66,6 +66,7 @@ struct StageRT {
   std::vector<float*> snap_pool;         // pinned buffers reserved before enqueue
   // profiling (cfg.profile): event pool and the (class, work) of each recorded pair
   std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t tmark[2] = {nullptr, nullptr};
   size_t ev_used = 0;
   std::vector<int> prof_cls;
   std::vector<double> prof_work;

@@ -94,6 +94,7 @@ void free_all(xpipe_ctx* c) {
     s.snap_pool.clear();
     for (auto e : s.ev_pool) cudaEventDestroy(e);
     s.ev_pool.clear();
+    for (auto& e : s.tmark) if (e) { cudaEventDestroy(e); e = nullptr; }
     if (s.stream) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.stream); cudaStreamDestroy(s.stream); s.stream = nullptr; }
   }
   for (auto it = c->allocs.rbegin(); it != c->allocs.rend(); ++it) {
@@ -530,6 +531,27 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     }
   }
   cudaSetDevice(cur);
+  return XP_OK;
+}
+
+int xpipe_timer(xpipe_ctx* c, int32_t which, double* ms_out) {
+  if (!c || (which != 0 && which != 1)) return set_err(c, XP_EINVAL, "timer args");
+  if (c->poisoned) return XP_ESTATE;
+  for (auto& s : c->S) {
+    cudaSetDevice(s.dev);
+    if (!s.tmark[which]) XP_CUDA(c, cudaEventCreate(&s.tmark[which]));
+    XP_CUDA(c, cudaEventRecord(s.tmark[which], s.stream));
+  }
+  if (which == 1) {
+    XP_TRY(sync_all(c));
+    double mx = 0;
+    for (auto& s : c->S) {
+      float ms = 0;
+      XP_CUDA(c, cudaEventElapsedTime(&ms, s.tmark[0], s.tmark[1]));
+      mx = std::max(mx, (double)ms);
+    }
+    if (ms_out) *ms_out = mx;
+  }
   return XP_OK;
 }
 

@@ -76,6 +76,7 @@ def lib():
                                  C.POINTER(vp)]
         L.xpipe_step.argtypes = [vp, vp, vp, i32, C.c_uint32, C.POINTER(Stats)]
         L.xpipe_sync.argtypes = [vp]
+        L.xpipe_timer.argtypes = [vp, i32, C.POINTER(C.c_double)]
         L.xpipe_get_weights.argtypes = [vp, i32, i32, i32, i64, vp, C.c_size_t]
         L.xpipe_get_trace.argtypes = [vp, i32, vp, C.c_size_t, C.POINTER(C.c_size_t)]
         L.xpipe_stage_of_layer.argtypes = [vp, i32]
@@ -201,6 +202,14 @@ class XPipe:
         _check(lib().xpipe_step(self.h, _ptr(x), _ptr(y), M, flags, C.byref(st)), self.h)
         self.last_stats = st
         return out
+
+    def timer_start(self):
+        _check(lib().xpipe_timer(self.h, 0, None), self.h)
+
+    def timer_stop(self):
+        ms = C.c_double()
+        _check(lib().xpipe_timer(self.h, 1, C.byref(ms)), self.h)
+        return ms.value
 
     def sync(self):
         _check(lib().xpipe_sync(self.h), self.h)

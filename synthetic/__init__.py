@@ -15,11 +15,11 @@ Recipe:
   * seed 1 by default ("The seed was fixed with 1").
 """
 from .models import (LINEAR, CONV2D, BATCHNORM2D, RELU, MAXPOOL2D, AVGPOOL_GLOBAL, FLATTEN, ADD,
-                     CONCAT, SOFTMAX_XENT, Layer, mlp, vgg16_cifar, tiny_cnn, infer_shapes)
+                     CONCAT, SOFTMAX_XENT, AVGPOOL2D, Layer, mlp, vgg16_cifar, tiny_cnn, infer_shapes)
 from .data import make_params, make_inputs, CIFAR_MEAN, CIFAR_STD, IMAGENET_MEAN, IMAGENET_STD
 
 __all__ = [
     "LINEAR", "CONV2D", "BATCHNORM2D", "RELU", "MAXPOOL2D", "AVGPOOL_GLOBAL", "FLATTEN", "ADD",
-    "CONCAT", "SOFTMAX_XENT", "Layer", "mlp", "vgg16_cifar", "tiny_cnn", "infer_shapes",
+    "CONCAT", "SOFTMAX_XENT", "AVGPOOL2D", "Layer", "mlp", "vgg16_cifar", "tiny_cnn", "infer_shapes",
     "make_params", "make_inputs", "CIFAR_MEAN", "CIFAR_STD", "IMAGENET_MEAN", "IMAGENET_STD",
 ]

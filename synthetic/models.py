@@ -7,7 +7,7 @@ layer-count partition rule.
 """
 from dataclasses import dataclass, replace
 
-LINEAR, CONV2D, BATCHNORM2D, RELU, MAXPOOL2D, AVGPOOL_GLOBAL, FLATTEN, ADD, CONCAT, SOFTMAX_XENT = range(1, 11)
+LINEAR, CONV2D, BATCHNORM2D, RELU, MAXPOOL2D, AVGPOOL_GLOBAL, FLATTEN, ADD, CONCAT, SOFTMAX_XENT, AVGPOOL2D = range(1, 12)
 
 
 @dataclass(frozen=True)
@@ -53,6 +53,10 @@ def relu():
 
 def maxpool(k, s, p=0):
     return Layer(MAXPOOL2D, kh=k, kw=k, sh=s, sw=s, ph=p, pw=p)
+
+
+def avgpool(k, s, p=0):
+    return Layer(AVGPOOL2D, kh=k, kw=k, sh=s, sw=s, ph=p, pw=p)
 
 
 def xent():
@@ -106,7 +110,7 @@ def infer_shapes(layers, in_shape):
             o = (l.out_c, 1, 1)
         elif l.kind == CONV2D:
             o = (l.out_c, (h + 2 * l.ph - l.kh) // l.sh + 1, (w + 2 * l.pw - l.kw) // l.sw + 1)
-        elif l.kind == MAXPOOL2D:
+        elif l.kind in (MAXPOOL2D, AVGPOOL2D):
             o = (c, (h + 2 * l.ph - l.kh) // l.sh + 1, (w + 2 * l.pw - l.kw) // l.sw + 1)
         elif l.kind == AVGPOOL_GLOBAL:
             o = (c, 1, 1)
@@ -119,3 +123,168 @@ def infer_shapes(layers, in_shape):
             o = x
         outs.append(o)
     return outs
+
+
+# ---------------------------------------------------------------------------------------
+# DAG models (configs C3, C4).  Built as layer lists with explicit producer indices; each
+# layer carries the partition unit it belongs to (R17) so `assign_stages` can apply the
+# layer-count rule over units and write explicit stage ids (skip/branch edges never cross).
+# ---------------------------------------------------------------------------------------
+class Builder:
+    def __init__(self):
+        self.L, self.units, self.unit = [], [], 0
+
+    def add(self, layer, src0=None, src1=None):
+        kw = {}
+        if src0 is not None:
+            kw["src0"] = src0
+        if src1 is not None:
+            kw["src1"] = src1
+        self.L.append(replace(layer, **kw))
+        self.units.append(self.unit)
+        return len(self.L) - 1
+
+    def next_unit(self):
+        self.unit += 1
+
+    def conv_bn(self, src, i, o, k, s=1, p=0, relu_=True, eps=1e-5):
+        a = self.add(conv(i, o, k, s, p), src0=src)
+        b = self.add(bn(o, eps), src0=a)
+        return self.add(relu(), src0=b) if relu_ else b
+
+    def concat(self, srcs):
+        cur = srcs[0]
+        for s in srcs[1:]:
+            cur = self.add(Layer(CONCAT), src0=cur, src1=s)
+        return cur
+
+
+def _bottleneck(B, x, inplanes, planes, stride):
+    a = B.conv_bn(x, inplanes, planes, 1)
+    a = B.conv_bn(a, planes, planes, 3, stride, 1)
+    a = B.conv_bn(a, planes, 4 * planes, 1, relu_=False)
+    sc = x
+    if stride != 1 or inplanes != 4 * planes:
+        sc = B.conv_bn(x, inplanes, 4 * planes, 1, stride, 0, relu_=False)
+    s = B.add(Layer(ADD), src0=a, src1=sc)
+    return B.add(relu(), src0=s)
+
+
+def resnet101(classes=200, in_c=3, layers=(3, 4, 23, 3)):
+    """C3: torchvision ResNet-101 (v1.5: stride on the 3x3 conv), 64x64 input, no change
+    other than the input size (R19).  Units: stem / each bottleneck / head (35 units)."""
+    B = Builder()
+    x = B.conv_bn(-1, in_c, 64, 7, 2, 3)
+    x = B.add(maxpool(3, 2, 1), src0=x)
+    inplanes = 64
+    for li, (planes, n) in enumerate(zip((64, 128, 256, 512), layers)):
+        for b in range(n):
+            B.next_unit()
+            stride = 2 if (b == 0 and li > 0) else 1
+            x = _bottleneck(B, x, inplanes, planes, stride)
+            inplanes = 4 * planes
+    B.next_unit()
+    x = B.add(Layer(AVGPOOL_GLOBAL), src0=x)
+    x = B.add(Layer(FLATTEN), src0=x)
+    x = B.add(linear(2048, classes), src0=x)
+    B.add(xent(), src0=x)
+    return B.L, B.units
+
+
+def inception_v3(classes=200, in_c=3):
+    """C4: torchvision Inception-V3 with aux_logits off and no dropout, padding 1 on the
+    unpadded stem convs Conv2d_1a, 2a, 4a so 64x64 inputs survive to Mixed_7 (R14).
+    BasicConv2d = conv (no bias) + BN(eps=1e-3) + ReLU.  Units: stem conv / module / head."""
+    B = Builder()
+    e = 1e-3
+    cb = lambda src, i, o, k, s=1, p=0: B.conv_bn(src, i, o, k, s, p, True, e)
+    x = cb(-1, in_c, 32, 3, 2, 1)                       # Conv2d_1a (padded, R14)
+    B.next_unit(); x = cb(x, 32, 32, 3, 1, 1)           # Conv2d_2a (padded)
+    B.next_unit(); x = cb(x, 32, 64, 3, 1, 1)           # Conv2d_2b
+    x = B.add(maxpool(3, 2), src0=x)
+    B.next_unit(); x = cb(x, 64, 80, 1)                 # Conv2d_3b
+    B.next_unit(); x = cb(x, 80, 192, 3, 1, 1)          # Conv2d_4a (padded)
+    x = B.add(maxpool(3, 2), src0=x)
+
+    def incA(x, cin, pf):
+        b1 = cb(x, cin, 64, 1)
+        b5 = cb(cb(x, cin, 48, 1), 48, 64, 5, 1, 2)
+        b3 = cb(cb(cb(x, cin, 64, 1), 64, 96, 3, 1, 1), 96, 96, 3, 1, 1)
+        bp = cb(B.add(avgpool(3, 1, 1), src0=x), cin, pf, 1)
+        return B.concat([b1, b5, b3, bp])
+
+    def incB(x, cin):
+        b3 = cb(x, cin, 384, 3, 2)
+        bd = cb(cb(cb(x, cin, 64, 1), 64, 96, 3, 1, 1), 96, 96, 3, 2)
+        bp = B.add(maxpool(3, 2), src0=x)
+        return B.concat([b3, bd, bp])
+
+    def incC(x, c7):
+        b1 = cb(x, 768, 192, 1)
+        b7 = cb(cb(cb(x, 768, c7, 1), c7, c7, (1, 7), 1, (0, 3)), c7, 192, (7, 1), 1, (3, 0))
+        d = cb(x, 768, c7, 1)
+        d = cb(d, c7, c7, (7, 1), 1, (3, 0))
+        d = cb(d, c7, c7, (1, 7), 1, (0, 3))
+        d = cb(d, c7, c7, (7, 1), 1, (3, 0))
+        d = cb(d, c7, 192, (1, 7), 1, (0, 3))
+        bp = cb(B.add(avgpool(3, 1, 1), src0=x), 768, 192, 1)
+        return B.concat([b1, b7, d, bp])
+
+    def incD(x):
+        b3 = cb(cb(x, 768, 192, 1), 192, 320, 3, 2)
+        b7 = cb(x, 768, 192, 1)
+        b7 = cb(b7, 192, 192, (1, 7), 1, (0, 3))
+        b7 = cb(b7, 192, 192, (7, 1), 1, (3, 0))
+        b7 = cb(b7, 192, 192, 3, 2)
+        bp = B.add(maxpool(3, 2), src0=x)
+        return B.concat([b3, b7, bp])
+
+    def incE(x, cin):
+        b1 = cb(x, cin, 320, 1)
+        t = cb(x, cin, 384, 1)
+        b3 = B.concat([cb(t, 384, 384, (1, 3), 1, (0, 1)), cb(t, 384, 384, (3, 1), 1, (1, 0))])
+        d = cb(cb(x, cin, 448, 1), 448, 384, 3, 1, 1)
+        bd = B.concat([cb(d, 384, 384, (1, 3), 1, (0, 1)), cb(d, 384, 384, (3, 1), 1, (1, 0))])
+        bp = cb(B.add(avgpool(3, 1, 1), src0=x), cin, 192, 1)
+        return B.concat([b1, b3, bd, bp])
+
+    for cin, pf in ((192, 32), (256, 64), (288, 64)):
+        B.next_unit(); x = incA(x, cin, pf)
+    B.next_unit(); x = incB(x, 288)
+    for c7 in (128, 160, 160, 192):
+        B.next_unit(); x = incC(x, c7)
+    B.next_unit(); x = incD(x)
+    for cin in (1280, 2048):
+        B.next_unit(); x = incE(x, cin)
+    B.next_unit()
+    x = B.add(Layer(AVGPOOL_GLOBAL), src0=x)
+    x = B.add(Layer(FLATTEN), src0=x)
+    x = B.add(linear(2048, classes), src0=x)
+    B.add(xent(), src0=x)
+    return B.L, B.units
+
+
+def assign_stages(layers, units, K):
+    """Layer-count rule over partition units (remainder to the last r stages,
+    S:107), written as explicit stage ids on the layers."""
+    n_units = max(units) + 1
+    if K > n_units:
+        raise ValueError("more stages than units")
+    base, r = divmod(n_units, K)
+    st, u = [], 0
+    for k in range(K):
+        st += [k] * (base + (1 if k >= K - r else 0))
+    return [l.with_stage(st[units[i]]) for i, l in enumerate(layers)]
+
+
+def param_count(layers, in_shape):
+    shapes = infer_shapes(layers, in_shape)
+    n = 0
+    for i, l in enumerate(layers):
+        if l.kind == LINEAR:
+            n += l.out_c * l.in_c + (l.out_c if l.bias else 0)
+        elif l.kind == CONV2D:
+            n += l.out_c * l.in_c * l.kh * l.kw + (l.out_c if l.bias else 0)
+        elif l.kind == BATCHNORM2D:
+            n += 2 * l.in_c
+    return n

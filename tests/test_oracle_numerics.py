@@ -53,6 +53,8 @@ class TorchNet(torch.nn.Module):
                 y = F.relu(a)
             elif l.kind == S.MAXPOOL2D:
                 y = F.max_pool2d(a, (l.kh, l.kw), (l.sh, l.sw), (l.ph, l.pw))
+            elif l.kind == S.AVGPOOL2D:
+                y = F.avg_pool2d(a, (l.kh, l.kw), (l.sh, l.sw), (l.ph, l.pw), count_include_pad=True)
             elif l.kind == S.AVGPOOL_GLOBAL:
                 y = a.mean(dim=(2, 3), keepdim=True)
             elif l.kind == S.FLATTEN:
@@ -97,6 +99,10 @@ NETS = {
     "mlp": (small_mlp, (20, 1, 1), 5),
     "cnn": (lambda: S.tiny_cnn(3, 5, 4), (3, 8, 8), 5),
     "res": (residual_net, (3, 8, 8), 5),
+    "inception_branch": (lambda: [conv(3, 8, 3, 1, 1), bn(8), relu(),
+                                  Layer(S.AVGPOOL2D, kh=3, kw=3, sh=1, sw=1, ph=1, pw=1), conv(8, 4, 1, 1, 0),
+                                  bn(4), relu(), Layer(CONCAT, src0=6, src1=2), Layer(AVGPOOL_GLOBAL),
+                                  Layer(FLATTEN), linear(12, 5), xent()], (3, 7, 7), 5),
     "conv_s2": (lambda: [conv(2, 4, (3, 1), (2, 1), (1, 0), bias=1), relu(), conv(4, 3, (1, 3), 1, (0, 1)),
                          maxpool(2, 2), Layer(FLATTEN), linear(3 * 2 * 4, 5), xent()], (2, 7, 8), 5),
 }
@@ -126,7 +132,7 @@ def test_loss_grad_matches_torch_autograd(oracle_mod, name):
     np.testing.assert_allclose(g, net.flat_grad(), rtol=1e-10, atol=1e-13)
 
 
-@pytest.mark.parametrize("name", ["mlp", "cnn", "res", "conv_s2"])
+@pytest.mark.parametrize("name", ["mlp", "cnn", "res", "conv_s2", "inception_branch"])
 def test_loss_grad_matches_finite_differences(oracle_mod, name):
     """P8: central differences, h=1e-5, relative error < 1e-4, fp64."""
     import oracle
@@ -347,3 +353,42 @@ def test_paper_delta_form(oracle_mod):
     dW = (mn[0] / (1 - b1)) / np.sqrt(vn[0] / (1 - b2) + EPS32)
     assert abs(dW - 1.0) < 1e-5
     assert abs((Wn[0] - pf[0]) - 0.2) < 1e-5
+
+
+def test_dag_models_match_torch_autograd(oracle_mod):
+    """ResNet bottlenecks (residual add, strided 1x1 downsample, 7x7 s2 stem, 3x3 s2 maxpool)
+    and Inception modules (asymmetric kernels, avgpool branch, multi-way concat) against torch
+    autograd in fp64: reduced depth, the real block structure."""
+    import oracle
+    from synthetic.models import resnet101, inception_v3
+    for L, shape, classes in ((resnet101(classes=7, layers=(1, 1, 1, 1))[0], (3, 32, 32), 7),
+                              (inception_v3(classes=7)[0], (3, 64, 64), 7)):
+        P = S.make_params(L, 2)
+        o = oracle.Oracle(L, 1, 1, 4, 1e-3, BETAS32, EPS32, shape, classes, P, mode="fp64", predict="off")
+        x, y = S.make_inputs(4, shape, classes, 3, kind="imagenet")
+        loss, g = o.eval_loss_grad(x, y)
+        net = TorchNet(L, P)
+        ref = torch.nn.functional.cross_entropy(net(torch.tensor(x, dtype=torch.float64)), torch.tensor(y, dtype=torch.long))
+        ref.backward()
+        assert abs(loss - ref.item()) <= 1e-10
+        ref_g = net.flat_grad()
+        # fp64 accumulation-order noise only: bound relative to the gradient's scale
+        np.testing.assert_allclose(g, ref_g, rtol=1e-8, atol=1e-11 * np.abs(ref_g).max())
+
+
+@pytest.mark.parametrize("K", [2, 3])
+def test_dag_gpipe_no_prediction_equals_single_stage(oracle_mod, K):
+    """P6 on a DAG model with explicit unit-based stage assignment (R17)."""
+    import oracle
+    from synthetic.models import resnet101, assign_stages
+    L, units = resnet101(classes=5, layers=(1, 1, 1, 1))
+    P = S.make_params(L, 4)
+    x, y = S.make_inputs(3 * 4, (3, 16, 16), 5, 4, kind="imagenet")
+    res = []
+    for k in (1, K):
+        Lk = assign_stages(L, units, k)
+        o = oracle.Oracle(Lk, k, 2, 4, 1e-3, BETAS32, EPS32, (3, 16, 16), 5, P, mode="fp32", schedule="gpipe",
+                          predict="off")
+        o.step(x, y, 3, flush=True)
+        res.append(o.params_flat())
+    assert np.array_equal(res[0], res[1])

@@ -43,7 +43,8 @@ enum {
 
 /* ---- layer kinds (the DNN is partitioned layer-wise into stages) ----------- */
 enum { XP_LINEAR = 1, XP_CONV2D, XP_BATCHNORM2D, XP_RELU, XP_MAXPOOL2D, XP_AVGPOOL_GLOBAL,
-       XP_FLATTEN, XP_ADD, XP_CONCAT, XP_SOFTMAX_XENT };
+       XP_FLATTEN, XP_ADD, XP_CONCAT, XP_SOFTMAX_XENT,
+       XP_AVGPOOL2D /* kh x kw window, zero padding counted in the divisor (Inception branch pool) */ };
 
 /* ---- configuration enums -------------------------------------------------------------- */
 enum { XP_FP32 = 0,   /* fp32 SIMT path, bit-exact with the oracle's fp32 contract */

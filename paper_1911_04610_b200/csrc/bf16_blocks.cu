@@ -1,11 +1,13 @@
-// bf16_blocks.cu -- forward/backward of the bf16 fused blocks:
-//   BK_CONV   : tcgen05 implicit-GEMM conv -> BN statistics -> BN-apply + ReLU (+ MaxPool)
-//               backward: pool routing + ReLU mask + BN reductions -> BN input gradient ->
-//               wgrad (into the fp32 accumulator g) and dgrad (under W_hat_b)
-//   BK_LINEAR : bf16-operand Linear (+ ReLU), fp32 logits when it feeds the softmax-xent
+// bf16_blocks.cu -- forward/backward of the bf16 fused ops:
+//   OP_CONV    : tcgen05 implicit-GEMM conv -> BN statistics -> BN-apply [+ ReLU] [+ MaxPool]
+//                backward: pool routing + ReLU mask + BN reductions -> BN input gradient ->
+//                wgrad (into the fp32 accumulator g) and dgrad (under W_hat_b)
+//   OP_LINEAR  : bf16-operand Linear [+ ReLU], fp32 logits when it feeds the softmax-xent
+//   OP_ADD / OP_CONCAT / OP_MAXPOOL / OP_AVGPOOL / OP_GAP : the DAG glue of ResNet / Inception
 // Forward runs under W_hat_f, backward under W_hat_b (stash mode, R10); BN's forward affine
 // parameters and statistics are stashed per micro-batch so the backward recompute of the
-// activation is bit-identical to the forward.
+// activation is bit-identical to the forward (R24).  Activation gradients that fan in from
+// several consumers accumulate with the oracle's rounding point, Q(old + Q(g)).
 #include "kernels/bf16_kernels.h"
 #include "kernels/gemm_tc.h"
 #include "runtime.h"
@@ -15,83 +17,129 @@ namespace xp {
 namespace {
 typedef __nv_bfloat16 bf16;
 
-ConvGeo conv_geo(const xpipe_ctx* c, const Block& B, const LayerInfo& L) {
+ConvGeo conv_geo(const xpipe_ctx* c, const Op& O, const LayerInfo& L) {
   ConvGeo g;
-  g.Nimg = c->n; g.H = B.in.h; g.W = B.in.w; g.C = L.cin_pad;
-  g.Co = L.d.out_c; g.R = L.d.kh; g.S = L.d.kw; g.P = B.mid.h; g.Q = B.mid.w;
+  g.Nimg = c->n; g.H = O.sin0.h; g.W = O.sin0.w; g.C = L.cin_pad;
+  g.Co = L.d.out_c; g.R = L.d.kh; g.S = L.d.kw; g.P = O.smid.h; g.Q = O.smid.w;
   g.sh = L.d.sh; g.sw = L.d.sw; g.ph = L.d.ph; g.pw = L.d.pw;
   return g;
 }
-// algorithmic flops of one conv GEMM (real channels; padding of C to 8 not counted as work)
-double conv_flops(const ConvGeo& g) { return 2.0 * g.Nimg * g.P * g.Q * (double)g.Co * g.R * g.S * g.C; }
+// algorithmic flops of one conv GEMM (channel padding to 8 is not counted as work)
+double conv_flops(const ConvGeo& g, int cin) { return 2.0 * g.Nimg * g.P * g.Q * (double)g.Co * g.R * g.S * cin; }
+
+struct PoolGeo { int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0; };
+PoolGeo pool_geo(const xpipe_ctx* c, int l) {
+  PoolGeo p;
+  if (l < 0) return p;
+  const LayerInfo& P = c->net.layers[l];
+  p.kh = P.d.kh; p.kw = P.d.kw; p.sh = P.d.sh; p.sw = P.d.sw; p.ph = P.d.ph; p.pw = P.d.pw;
+  return p;
+}
 }  // namespace
 
-int bf16_block_forward(xpipe_ctx* c, StageRT& s, size_t b, const void* x, const void* Wf, int slot) {
-  const Block& B = s.plan.blocks[b];
-  const LayerInfo& L = c->net.layers[B.lmain];
+int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
+  const Op& O = s.plan.ops[o];
+  const LayerInfo& L = c->net.layers[O.lmain];
   const bf16* W = static_cast<const bf16*>(Wf);
-  if (B.kind == BK_LINEAR) {
-    return check_launch(c, launch_linear_fwd_bf16((const bf16*)x, W + L.woff, L.nb ? W + L.boff : nullptr,
-                                                  s.out[b][slot], c->n, L.d.in_c, L.d.out_c, B.lrelu >= 0, B.logits,
-                                                  s.stream), "linear_fwd_bf16");
+  const bf16* x = (const bf16*)s.act[O.in0][slot];
+  void* y = s.act[O.out][slot];
+  const int n = c->n;
+  switch (O.kind) {
+    case OP_LINEAR:
+      return check_launch(c, launch_linear_fwd_bf16(x, W + L.woff, L.nb ? W + L.boff : nullptr, y, n, L.d.in_c,
+                                                    L.d.out_c, O.relu, O.logits, s.stream), "linear_fwd_bf16");
+    case OP_CONV: {
+      const ConvGeo g = conv_geo(c, O, L);
+      bf16* mid = (bf16*)s.mid[o][slot];
+      XP_TRY(prof_begin(c, s));
+      XP_TRY(check_launch(c, tc_conv_fprop(g, x, W + L.woff, mid, s.ws, s.ws_elems, s.stream), "conv_fprop"));
+      XP_TRY(prof_end(c, s, XP_PROF_CONV_FPROP, conv_flops(g, L.in0.c)));
+      const LayerInfo& N = c->net.layers[O.lbn];
+      const int M = n * O.smid.h * O.smid.w;
+      XP_TRY(check_launch(c, launch_bn_stats(mid, M, O.smid.c, N.d.bn_eps, W + N.woff, W + N.boff, s.bnws,
+                                             s.stats[o][slot], s.stream), "bn_stats"));
+      const PoolGeo p = pool_geo(c, O.lpool);
+      return check_launch(c, launch_bn_apply(mid, s.stats[o][slot], (bf16*)y, n, O.smid.h, O.smid.w, O.smid.c,
+                                             O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0,
+                                             O.relu, s.stream), "bn_apply");
+    }
+    case OP_ADD:
+      return check_launch(c, launch_add_fwd(x, (const bf16*)s.act[O.in1][slot], (bf16*)y, (int64_t)n * O.sout.size(),
+                                            O.relu, s.stream), "add_fwd");
+    case OP_CONCAT:
+      return check_launch(c, launch_concat_fwd(x, (const bf16*)s.act[O.in1][slot], (bf16*)y,
+                                               (int64_t)n * O.sout.h * O.sout.w, O.sin0.c, O.sin1.c, s.stream),
+                          "concat_fwd");
+    case OP_MAXPOOL: case OP_AVGPOOL: {
+      const PoolGeo p = pool_geo(c, O.lmain);
+      return check_launch(c, launch_pool_fwd(x, (bf16*)y, n, O.sin0.h, O.sin0.w, O.sin0.c, O.sout.h, O.sout.w, p.kh,
+                                             p.kw, p.sh, p.sw, p.ph, p.pw, O.kind == OP_AVGPOOL, s.stream), "pool_fwd");
+    }
+    case OP_GAP:
+      return check_launch(c, launch_gap_fwd(x, (bf16*)y, n, O.sin0.h * O.sin0.w, O.sin0.c, s.stream), "gap_fwd");
   }
-  const ConvGeo g = conv_geo(c, B, L);
-  bf16* mid = (bf16*)s.mid[b][slot];
-  XP_TRY(prof_begin(c, s));
-  XP_TRY(check_launch(c, tc_conv_fprop(g, (const bf16*)x, W + L.woff, mid, s.ws, s.ws_elems, s.stream), "conv_fprop"));
-  XP_TRY(prof_end(c, s, XP_PROF_CONV_FPROP, conv_flops(g)));
-  const LayerInfo& N = c->net.layers[B.lbn];
-  const int M = c->n * B.mid.h * B.mid.w;
-  XP_TRY(check_launch(c, launch_bn_stats(mid, M, B.mid.c, N.d.bn_eps, W + N.woff, W + N.boff, s.bnws, s.stats[b][slot],
-                                         s.stream), "bn_stats"));
-  int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
-  const bool pool = B.lpool >= 0;
-  if (pool) {
-    const LayerInfo& Pl = c->net.layers[B.lpool];
-    kh = Pl.d.kh; kw = Pl.d.kw; sh = Pl.d.sh; sw = Pl.d.sw; ph = Pl.d.ph; pw = Pl.d.pw;
-  }
-  return check_launch(c, launch_bn_apply(mid, s.stats[b][slot], (bf16*)s.out[b][slot], c->n, B.mid.h, B.mid.w, B.mid.c,
-                                         B.out.h, B.out.w, kh, kw, sh, sw, ph, pw, pool, s.stream), "bn_apply");
+  return set_err(c, XP_EUNSUPPORTED, "op kind");
 }
 
-int bf16_block_backward(xpipe_ctx* c, StageRT& s, int b, const void* x, const void* dy, void* dx, const void* Wb,
-                        int slot, bool accumulate) {
-  const Block& B = s.plan.blocks[b];
-  const LayerInfo& L = c->net.layers[B.lmain];
+int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0, bool acc0, void* dx1, bool acc1,
+                     const void* Wb, int slot, bool accumulate_g) {
+  const Op& O = s.plan.ops[o];
+  const LayerInfo& L = c->net.layers[O.lmain];
   const bf16* W = static_cast<const bf16*>(Wb);
-  if (B.kind == BK_LINEAR) {
-    const bf16* mask = B.lrelu >= 0 ? (const bf16*)s.out[b][slot] : nullptr;
-    if (dx)
-      XP_TRY(check_launch(c, launch_linear_dgrad_bf16(dy, B.logits, mask, W + L.woff, (bf16*)dx, c->n, L.d.in_c,
-                                                      L.d.out_c, s.stream), "linear_dgrad_bf16"));
-    return check_launch(c, launch_linear_wgrad_bf16(dy, B.logits, mask, (const bf16*)x, s.g + L.woff,
-                                                    L.nb ? s.g + L.boff : nullptr, c->n, L.d.in_c, L.d.out_c,
-                                                    accumulate, s.stream), "linear_wgrad_bf16");
+  const int n = c->n;
+  switch (O.kind) {
+    case OP_LINEAR: {
+      if (acc0) return set_err(c, XP_EUNSUPPORTED, "fan-out into a Linear input");
+      const bf16* mask = O.relu ? (const bf16*)s.act[O.out][slot] : nullptr;
+      if (dx0)
+        XP_TRY(check_launch(c, launch_linear_dgrad_bf16(dy, O.logits, mask, W + L.woff, (bf16*)dx0, n, L.d.in_c,
+                                                        L.d.out_c, s.stream), "linear_dgrad_bf16"));
+      return check_launch(c, launch_linear_wgrad_bf16(dy, O.logits, mask, (const bf16*)s.act[O.in0][slot],
+                                                      s.g + L.woff, L.nb ? s.g + L.boff : nullptr, n, L.d.in_c,
+                                                      L.d.out_c, accumulate_g, s.stream), "linear_wgrad_bf16");
+    }
+    case OP_CONV: {
+      const ConvGeo g = conv_geo(c, O, L);
+      const LayerInfo& N = c->net.layers[O.lbn];
+      const PoolGeo p = pool_geo(c, O.lpool);
+      bf16* dmid = (bf16*)s.gmid;
+      XP_TRY(check_launch(c, launch_bn_backward((const bf16*)s.mid[o][slot], (const bf16*)dy, s.stats[o][slot],
+                                                W + N.woff, n, O.smid.h, O.smid.w, O.smid.c, O.sout.h, O.sout.w, p.kh,
+                                                p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws,
+                                                s.g + N.woff, s.g + N.boff, accumulate_g, dmid, s.stream),
+                          "bn_backward"));
+      XP_TRY(prof_begin(c, s));
+      XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)s.act[O.in0][slot], dmid, s.g + L.woff, accumulate_g, s.ws,
+                                           s.ws_elems, s.stream), "conv_wgrad"));
+      XP_TRY(prof_end(c, s, XP_PROF_CONV_WGRAD, conv_flops(g, L.in0.c)));
+      if (dx0) {
+        XP_TRY(prof_begin(c, s));
+        XP_TRY(check_launch(c, tc_conv_dgrad(g, O.sin0.c, dmid, W + L.woff, (bf16*)dx0, s.ws, s.ws_elems, s.stream,
+                                             acc0), "conv_dgrad"));
+        XP_TRY(prof_end(c, s, XP_PROF_CONV_DGRAD, conv_flops(g, L.in0.c)));
+      }
+      return XP_OK;
+    }
+    case OP_ADD:
+      return check_launch(c, launch_add_bwd((const bf16*)dy, (const bf16*)s.act[O.out][slot], (bf16*)dx0, (bf16*)dx1,
+                                            (int64_t)n * O.sout.size(), O.relu, acc0, acc1, s.stream), "add_bwd");
+    case OP_CONCAT:
+      return check_launch(c, launch_concat_bwd((const bf16*)dy, (bf16*)dx0, (bf16*)dx1,
+                                               (int64_t)n * O.sout.h * O.sout.w, O.sin0.c, O.sin1.c, acc0, acc1,
+                                               s.stream), "concat_bwd");
+    case OP_MAXPOOL: case OP_AVGPOOL: {
+      if (!dx0) return XP_OK;
+      const PoolGeo p = pool_geo(c, O.lmain);
+      return check_launch(c, launch_pool_bwd((const bf16*)s.act[O.in0][slot], (const bf16*)dy, (bf16*)dx0, n,
+                                             O.sin0.h, O.sin0.w, O.sin0.c, O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw,
+                                             p.ph, p.pw, O.kind == OP_AVGPOOL, acc0, s.stream), "pool_bwd");
+    }
+    case OP_GAP:
+      if (!dx0) return XP_OK;
+      return check_launch(c, launch_gap_bwd((const bf16*)dy, (bf16*)dx0, n, O.sin0.h * O.sin0.w, O.sin0.c, acc0,
+                                            s.stream), "gap_bwd");
   }
-  const ConvGeo g = conv_geo(c, B, L);
-  const LayerInfo& N = c->net.layers[B.lbn];
-  int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0;
-  const bool pool = B.lpool >= 0;
-  if (pool) {
-    const LayerInfo& Pl = c->net.layers[B.lpool];
-    kh = Pl.d.kh; kw = Pl.d.kw; sh = Pl.d.sh; sw = Pl.d.sw; ph = Pl.d.ph; pw = Pl.d.pw;
-  }
-  bf16* dmid = (bf16*)s.gmid;
-  XP_TRY(check_launch(c, launch_bn_backward((const bf16*)s.mid[b][slot], (const bf16*)dy, s.stats[b][slot],
-                                            W + N.woff, c->n, B.mid.h, B.mid.w, B.mid.c, B.out.h, B.out.w, kh, kw, sh,
-                                            sw, ph, pw, pool, s.bnws, s.g + N.woff, s.g + N.boff, accumulate, dmid,
-                                            s.stream), "bn_backward"));
-  XP_TRY(prof_begin(c, s));
-  XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)x, dmid, s.g + L.woff, accumulate, s.ws, s.ws_elems, s.stream),
-                      "conv_wgrad"));
-  XP_TRY(prof_end(c, s, XP_PROF_CONV_WGRAD, conv_flops(g)));
-  if (dx) {
-    XP_TRY(prof_begin(c, s));
-    XP_TRY(check_launch(c, tc_conv_dgrad(g, B.in.c, dmid, W + L.woff, (bf16*)dx, s.ws, s.ws_elems, s.stream),
-                        "conv_dgrad"));
-    XP_TRY(prof_end(c, s, XP_PROF_CONV_DGRAD, conv_flops(g)));
-  }
-  return XP_OK;
+  return set_err(c, XP_EUNSUPPORTED, "op kind");
 }
 
 }  // namespace xp

@@ -1,4 +1,4 @@
-// blocks.cu -- per-stage device memory and the forward/backward of one fused block.
+// blocks.cu -- per-stage device memory; op dispatch (fp32 contract path here, bf16 in bf16_blocks.cu).
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -36,41 +36,46 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
     s.gin_slot.resize(s.S);
     for (auto& q : s.gin_slot) if (!(q = A(p.out_bytes))) return set_err(c, XP_ENOMEM, "gradient ring");
   }
-  const size_t aes = bf ? 2 : 4;
-  s.out.assign(p.blocks.size(), {});
-  s.mid.assign(p.blocks.size(), {});
-  s.stats.assign(p.blocks.size(), {});
-  for (size_t b = 0; b < p.blocks.size(); ++b) {
-    const Block& B = p.blocks[b];
-    if (B.kind == BK_XENT) continue;
-    const size_t oes = B.logits ? 4 : aes;
-    s.out[b].resize(s.S);
-    for (auto& q : s.out[b]) if (!(q = A((size_t)n * B.out.size() * oes))) return set_err(c, XP_ENOMEM, "stash");
-    if (B.kind == BK_CONV) {
-      s.mid[b].resize(s.S);
-      s.stats[b].resize(s.S);
-      for (auto& q : s.mid[b]) if (!(q = A((size_t)n * B.mid.size() * 2))) return set_err(c, XP_ENOMEM, "stash");
-      for (auto& q : s.stats[b]) if (!(q = (float*)A((size_t)B.mid.c * 4 * 4))) return set_err(c, XP_ENOMEM, "stash");
-    }
+  // per-micro-batch stash of every op output (tensor 0 is the input ring itself)
+  s.act.assign(p.tensors.size(), {});
+  s.act[0] = s.in_slot;
+  s.grad.assign(p.tensors.size(), nullptr);
+  for (size_t t = 1; t < p.tensors.size(); ++t) {
+    const TensorInfo& T = p.tensors[t];
+    s.act[t].resize(s.S);
+    for (auto& q : s.act[t]) if (!(q = A((size_t)n * T.shape.size() * T.es))) return set_err(c, XP_ENOMEM, "stash");
+  }
+  // activation-gradient buffers, one per tensor (reused by every backward pass, stream-ordered)
+  for (size_t t = 0; t < p.tensors.size(); ++t) {
+    if (t == (size_t)p.out_tensor) continue;  // seeded by the gradient ring / dz
+    if (!(s.grad[t] = A((size_t)n * p.tensors[t].shape.size() * 4))) return set_err(c, XP_ENOMEM, "gradient buffers");
+  }
+  s.mid.assign(p.ops.size(), {});
+  s.stats.assign(p.ops.size(), {});
+  for (size_t o = 0; o < p.ops.size(); ++o) {
+    const Op& O = p.ops[o];
+    if (O.kind != OP_CONV) continue;
+    s.mid[o].resize(s.S);
+    s.stats[o].resize(s.S);
+    for (auto& q : s.mid[o]) if (!(q = A((size_t)n * O.smid.size() * 2))) return set_err(c, XP_ENOMEM, "stash");
+    for (auto& q : s.stats[o]) if (!(q = (float*)A((size_t)O.smid.c * 4 * 4))) return set_err(c, XP_ENOMEM, "stash");
   }
   if (s.k == c->K - 1) {
     s.dz.resize(s.S);
     for (auto& q : s.dz) if (!(q = (float*)A((size_t)n * c->cfg.classes * 4))) return set_err(c, XP_ENOMEM, "dz");
   }
   s.gbuf_elems = (int64_t)n * p.max_act;
-  s.gbuf[0] = A((size_t)s.gbuf_elems * 4);
-  s.gbuf[1] = A((size_t)s.gbuf_elems * 4);
   s.gmid = A((size_t)s.gbuf_elems * 4);
-  if (!s.gbuf[0] || !s.gbuf[1] || !s.gmid) return set_err(c, XP_ENOMEM, "gradient scratch");
+  if (!s.gmid) return set_err(c, XP_ENOMEM, "gradient scratch");
   if (bf) {
     int64_t ws = 0;
     size_t bnws = 64;
-    for (const Block& B : p.blocks) {
-      if (B.kind != BK_CONV) continue;
-      const LayerInfo& L = c->net.layers[B.lmain];
-      ConvGeo g{n, B.in.h, B.in.w, L.cin_pad, L.d.out_c, L.d.kh, L.d.kw, B.mid.h, B.mid.w, L.d.sh, L.d.sw, L.d.ph, L.d.pw};
+    for (const Op& O : p.ops) {
+      if (O.kind != OP_CONV) continue;
+      const LayerInfo& L = c->net.layers[O.lmain];
+      ConvGeo g{n, O.sin0.h, O.sin0.w, L.cin_pad, L.d.out_c, L.d.kh, L.d.kw, O.smid.h, O.smid.w, L.d.sh, L.d.sw, L.d.ph, L.d.pw};
       ws = std::max(ws, tc_conv_ws_elems(g));
-      bnws = std::max(bnws, bn_ws_floats(n * B.mid.h * B.mid.w, B.mid.c));
+      bnws = std::max(bnws, bn_ws_floats(n * O.smid.h * O.smid.w, O.smid.c));
     }
     s.ws_elems = ws;
     s.ws = (float*)A((size_t)std::max<int64_t>(ws, 64) * 4);
@@ -176,34 +181,41 @@ int stage_input(xpipe_ctx* c, StageRT& s, const float* x, void* dst) {
                                                  s.stream), "stage_input");
 }
 
-int block_forward(xpipe_ctx* c, StageRT& s, size_t b, const void* x, const void* Wf, int slot) {
-  const Block& B = s.plan.blocks[b];
-  const LayerInfo& L = c->net.layers[B.lmain];
-  if (!is_bf16(c)) {
-    if (B.kind != BK_LINEAR) return set_err(c, XP_EUNSUPPORTED, "fp32 block");
-    const float* W = (const float*)Wf;
-    return check_launch(c, launch_linear_fwd_f32((const float*)x, W + L.woff, L.nb ? W + L.boff : nullptr,
-                                                 (float*)s.out[b][slot], c->n, L.d.in_c, L.d.out_c, B.lrelu >= 0,
-                                                 s.stream), "linear_fwd_f32");
+int op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot, int64_t u) {
+  const Op& O = s.plan.ops[o];
+  if (O.kind == OP_XENT) {
+    const int32_t* y = c->y_dev + (u - c->call_first) * c->n;
+    float* loss = c->loss_dev + (u - c->call_first);
+    return check_launch(c, launch_xent_f32((const float*)s.act[O.in0][slot], y, s.dz[slot], loss, c->n, O.sin0.c,
+                                           (float)(1.0 / (double)c->N), s.stream), "xent");
   }
-  return bf16_block_forward(c, s, b, x, Wf, slot);
+  if (!is_bf16(c)) {
+    if (O.kind != OP_LINEAR) return set_err(c, XP_EUNSUPPORTED, "fp32 op");
+    const LayerInfo& L = c->net.layers[O.lmain];
+    const float* W = (const float*)Wf;
+    return check_launch(c, launch_linear_fwd_f32((const float*)s.act[O.in0][slot], W + L.woff,
+                                                 L.nb ? W + L.boff : nullptr, (float*)s.act[O.out][slot], c->n,
+                                                 L.d.in_c, L.d.out_c, O.relu, s.stream), "linear_fwd_f32");
+  }
+  return bf16_op_forward(c, s, o, Wf, slot);
 }
 
-int block_backward(xpipe_ctx* c, StageRT& s, int b, const void* x, const void* dy, void* dx, const void* Wb, int slot,
-                   bool accumulate) {
-  const Block& B = s.plan.blocks[b];
-  const LayerInfo& L = c->net.layers[B.lmain];
+int op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0, bool acc0, void* dx1, bool acc1,
+                const void* Wb, int slot, bool accumulate_g) {
+  const Op& O = s.plan.ops[o];
   if (!is_bf16(c)) {
+    const LayerInfo& L = c->net.layers[O.lmain];
+    if (acc0) return set_err(c, XP_EUNSUPPORTED, "fan-out into a Linear input");
     const float* W = (const float*)Wb;
-    const float* mask = B.lrelu >= 0 ? (const float*)s.out[b][slot] : nullptr;
-    if (dx)
-      XP_TRY(check_launch(c, launch_linear_dgrad_f32((const float*)dy, mask, W + L.woff, (float*)dx, c->n, L.d.in_c,
+    const float* mask = O.relu ? (const float*)s.act[O.out][slot] : nullptr;
+    if (dx0)
+      XP_TRY(check_launch(c, launch_linear_dgrad_f32((const float*)dy, mask, W + L.woff, (float*)dx0, c->n, L.d.in_c,
                                                      L.d.out_c, s.stream), "linear_dgrad_f32"));
-    return check_launch(c, launch_linear_wgrad_f32((const float*)dy, mask, (const float*)x, s.g + L.woff,
-                                                   L.nb ? s.g + L.boff : nullptr, c->n, L.d.in_c, L.d.out_c,
-                                                   accumulate, s.stream), "linear_wgrad_f32");
+    return check_launch(c, launch_linear_wgrad_f32((const float*)dy, mask, (const float*)s.act[O.in0][slot],
+                                                   s.g + L.woff, L.nb ? s.g + L.boff : nullptr, c->n, L.d.in_c,
+                                                   L.d.out_c, accumulate_g, s.stream), "linear_wgrad_f32");
   }
-  return bf16_block_backward(c, s, b, x, dy, dx, Wb, slot, accumulate);
+  return bf16_op_backward(c, s, o, dy, dx0, acc0, dx1, acc1, Wb, slot, accumulate_g);
 }
 
 }  // namespace xp

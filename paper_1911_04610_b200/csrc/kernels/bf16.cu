@@ -20,10 +20,10 @@ __device__ __forceinline__ float q16(float v) { return __bfloat162float(__float2
 
 // The BN-apply + ReLU of one element, bit-identical wherever it is (re)computed:
 // a = Q(relu(gamma * ((x - mean) * rstd) + beta))
-__device__ __forceinline__ float bn_act(float x, float mean, float rstd, float gamma, float beta) {
+__device__ __forceinline__ float bn_act(float x, float mean, float rstd, float gamma, float beta, int relu) {
   const float t = __fmul_rn(__fsub_rn(x, mean), rstd);
   const float v = __fadd_rn(__fmul_rn(gamma, t), beta);
-  return q16(v > 0.f ? v : 0.f);
+  return q16((relu && !(v > 0.f)) ? 0.f : v);
 }
 
 // ---- K11 ---------------------------------------------------------------------------------
@@ -126,7 +126,7 @@ __global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks
 // y[n][p][q][c] = max over the pool window (first max, row-major) of bn_act(x[n][h][w][c])
 __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restrict__ st, bf16* __restrict__ y,
                                 int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph,
-                                int pw, int pool) {
+                                int pw, int pool, int relu) {
   const int G = C / 8;
   const int64_t total = (int64_t)n * P * Q * G;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -147,7 +147,7 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
       const uint4 u = *reinterpret_cast<const uint4*>(x + (((int64_t)s * H + p) * W + q) * C + c0);
       const bf16* v = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) best[e] = bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e]);
+      for (int e = 0; e < 8; ++e) best[e] = bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e], relu);
     } else {
       bool first = true;
       for (int a = 0; a < kh; ++a)
@@ -158,7 +158,7 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
           const bf16* v = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float t = bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e]);
+            const float t = bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e], relu);
             if (first || t > best[e]) best[e] = t;
           }
           first = false;
@@ -177,14 +177,14 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
 // gradient reaching BN output element (s,h,w,c): max-pool routing (first max of every window
 // containing it) and the ReLU mask, recomputing a from the stash (x, stats)
 struct BwdGeo {
-  int H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool;
+  int H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool, relu;
 };
 
 __device__ __forceinline__ float routed_dy(const bf16* __restrict__ x, const bf16* __restrict__ dout,
                                            const BwdGeo& G, int s, int h, int w, int c, float mean, float rstd, float ga,
                                            float be) {
-  const float a = bn_act(__bfloat162float(x[(((int64_t)s * G.H + h) * G.W + w) * G.C + c]), mean, rstd, ga, be);
-  if (!(a > 0.f)) return 0.f;
+  const float a = bn_act(__bfloat162float(x[(((int64_t)s * G.H + h) * G.W + w) * G.C + c]), mean, rstd, ga, be, G.relu);
+  if (G.relu && !(a > 0.f)) return 0.f;
   if (!G.pool) return __bfloat162float(dout[(((int64_t)s * G.H + h) * G.W + w) * G.C + c]);
   // windows (p,q) with p*sh - ph <= h < p*sh - ph + kh
   const int plo = max(0, (h + G.ph - G.kh + G.sh) / G.sh), phi = min(G.P - 1, (h + G.ph) / G.sh);
@@ -200,7 +200,7 @@ __device__ __forceinline__ float routed_dy(const bf16* __restrict__ x, const bf1
         for (int b2 = 0; b2 < G.kw; ++b2) {
           const int hh = p * G.sh - G.ph + a2, ww = q * G.sw - G.pw + b2;
           if (hh < 0 || hh >= G.H || ww < 0 || ww >= G.W) continue;
-          const float t = bn_act(__bfloat162float(x[(((int64_t)s * G.H + hh) * G.W + ww) * G.C + c]), mean, rstd, ga, be);
+          const float t = bn_act(__bfloat162float(x[(((int64_t)s * G.H + hh) * G.W + ww) * G.C + c]), mean, rstd, ga, be, G.relu);
           if (bh < 0 || t > best) { best = t; bh = hh; bw = ww; }
         }
       if (bh == h && bw == w) {
@@ -364,16 +364,18 @@ cudaError_t launch_bn_stats(const bf16* x, int M, int C, float eps, const bf16* 
 }
 
 cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, int n, int H, int W, int C, int P, int Q, int kh,
-                            int kw, int sh, int sw, int ph, int pw, bool pool, cudaStream_t st) {
+                            int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st) {
   const int64_t total = (int64_t)n * P * Q * (C / 8);
-  bn_apply_kernel<<<grid1d(total), 256, 0, st>>>(x, stats, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool ? 1 : 0);
+  bn_apply_kernel<<<grid1d(total), 256, 0, st>>>(x, stats, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool ? 1 : 0,
+                                                 relu ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bn_backward(const bf16* x, const bf16* dout, const float* stats, const bf16* gamma_b, int n, int H,
                                int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,
-                               float* ws, float* g_gamma, float* g_beta, bool accumulate, bf16* dx, cudaStream_t st) {
-  BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0};
+                               bool relu, float* ws, float* g_gamma, float* g_beta, bool accumulate, bf16* dx,
+                               cudaStream_t st) {
+  BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
   const int M = n * H * W;
   const int RC = bn_chunk_rows(M), chunks = bn_chunks(M);
   dim3 grid(chunks, (C + 63) / 64);
@@ -402,6 +404,192 @@ cudaError_t launch_linear_wgrad_bf16(const void* dy, bool dy_f32, const bf16* ma
   dim3 grid((in + 1 + 127) / 128, out);
   if (dy_f32) linear_wgrad_bf16_kernel<true><<<grid, 128, 0, st>>>(dy, mask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
   else linear_wgrad_bf16_kernel<false><<<grid, 128, 0, st>>>(dy, mask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
+}  // namespace xp
+
+// =========================================================================================
+// DAG-model kernels (ResNet-101 / Inception-V3): residual add (+ReLU), channel concat,
+// standalone max / average pooling and global average pooling, and the gradient side of
+// each.  Activation gradients accumulate with the oracle's rounding point:
+// out = Q(old + Q(g)) when a tensor already holds a contribution (fan-out), else out = Q(g).
+// =========================================================================================
+namespace xp {
+
+namespace {
+typedef __nv_bfloat16 bf16;
+__device__ __forceinline__ float q16b(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+__device__ __forceinline__ void put_grad(bf16* p, float g, int accumulate) {
+  const float gq = q16b(g);
+  *p = __float2bfloat16_rn(accumulate ? __fadd_rn(__bfloat162float(*p), gq) : gq);
+}
+int g1(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
+
+// y = Q(relu?(a + b)) elementwise over n elements
+__global__ void add_fwd_kernel(const bf16* a, const bf16* b, bf16* y, int64_t n, int relu) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = q16b(__fadd_rn(__bfloat162float(a[i]), __bfloat162float(b[i])));
+    if (relu) v = v > 0.f ? v : 0.f;
+    y[i] = __float2bfloat16_rn(v);
+  }
+}
+// da (=|+=) dy', db (=|+=) dy' with dy' = (relu && !(y > 0)) ? 0 : dy
+__global__ void add_bwd_kernel(const bf16* dy, const bf16* y, bf16* da, bf16* db, int64_t n, int relu, int acc_a,
+                               int acc_b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float g = __bfloat162float(dy[i]);
+    if (relu && !(__bfloat162float(y[i]) > 0.f)) g = 0.f;
+    if (da) put_grad(da + i, g, acc_a);
+    if (db) put_grad(db + i, g, acc_b);
+  }
+}
+// y[r][0:Ca] = a[r], y[r][Ca:Ca+Cb] = b[r]   (r = pixel)
+__global__ void concat_fwd_kernel(const bf16* a, const bf16* b, bf16* y, int64_t rows, int Ca, int Cb) {
+  const int C = Ca + Cb;
+  const int64_t n = rows * C;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / C;
+    const int c = (int)(i - r * C);
+    y[i] = c < Ca ? a[r * Ca + c] : b[r * Cb + (c - Ca)];
+  }
+}
+__global__ void concat_bwd_kernel(const bf16* dy, bf16* da, bf16* db, int64_t rows, int Ca, int Cb, int acc_a,
+                                  int acc_b) {
+  const int C = Ca + Cb;
+  const int64_t n = rows * C;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / C;
+    const int c = (int)(i - r * C);
+    const float g = __bfloat162float(dy[i]);
+    if (c < Ca) { if (da) put_grad(da + r * Ca + c, g, acc_a); }
+    else if (db) put_grad(db + r * Cb + (c - Ca), g, acc_b);
+  }
+}
+// pooling forward: mode 0 max (first max, padded positions skipped), 1 avg (count_include_pad)
+__global__ void pool_fwd_kernel(const bf16* x, bf16* y, int n, int H, int W, int C, int P, int Q, int kh, int kw,
+                                int sh, int sw, int ph, int pw, int mode) {
+  const int64_t total = (int64_t)n * P * Q * C;
+  const float inv = 1.f / (float)(kh * kw);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    int64_t r = i / C;
+    const int q = (int)(r % Q); r /= Q;
+    const int p = (int)(r % P);
+    const int s = (int)(r / P);
+    float best = 0.f, acc = 0.f;
+    bool first = true;
+    for (int a = 0; a < kh; ++a)
+      for (int b = 0; b < kw; ++b) {
+        const int hh = p * sh - ph + a, ww = q * sw - pw + b;
+        if (hh < 0 || hh >= H || ww < 0 || ww >= W) continue;
+        const float v = __bfloat162float(x[(((int64_t)s * H + hh) * W + ww) * C + c]);
+        if (mode == 0) { if (first || v > best) best = v; first = false; }
+        else acc = __fadd_rn(acc, v);
+      }
+    y[i] = __float2bfloat16_rn(mode == 0 ? best : __fmul_rn(acc, inv));
+  }
+}
+// pooling backward, gather form over the input: for each input element sum the gradients of
+// the windows that route to it (max: it is the window's first max; avg: every window
+// covering it contributes g*inv), then store/accumulate
+__global__ void pool_bwd_kernel(const bf16* x, const bf16* dy, bf16* dx, int n, int H, int W, int C, int P, int Q,
+                                int kh, int kw, int sh, int sw, int ph, int pw, int mode, int accumulate) {
+  const int64_t total = (int64_t)n * H * W * C;
+  const float inv = 1.f / (float)(kh * kw);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    int64_t r = i / C;
+    const int w = (int)(r % W); r /= W;
+    const int h = (int)(r % H);
+    const int s = (int)(r / H);
+    const int plo = max(0, (h + ph - kh + sh) / sh), phi = min(P - 1, (h + ph) / sh);
+    const int qlo = max(0, (w + pw - kw + sw) / sw), qhi = min(Q - 1, (w + pw) / sw);
+    float acc = 0.f;
+    int hits = 0;
+    for (int p = plo; p <= phi; ++p)
+      for (int q = qlo; q <= qhi; ++q) {
+        if (h < p * sh - ph || h >= p * sh - ph + kh || w < q * sw - pw || w >= q * sw - pw + kw) continue;
+        const float g = __bfloat162float(dy[(((int64_t)s * P + p) * Q + q) * C + c]);
+        if (mode == 0) {
+          float best = 0.f;
+          int bh = -1, bw = -1;
+          for (int a = 0; a < kh; ++a)
+            for (int b = 0; b < kw; ++b) {
+              const int hh = p * sh - ph + a, ww = q * sw - pw + b;
+              if (hh < 0 || hh >= H || ww < 0 || ww >= W) continue;
+              const float v = __bfloat162float(x[(((int64_t)s * H + hh) * W + ww) * C + c]);
+              if (bh < 0 || v > best) { best = v; bh = hh; bw = ww; }
+            }
+          if (bh != h || bw != w) continue;
+          acc = hits ? __fadd_rn(acc, g) : g;
+        } else {
+          const float gi = __fmul_rn(g, inv);
+          acc = hits ? __fadd_rn(acc, gi) : gi;
+        }
+        ++hits;
+      }
+    put_grad(dx + i, acc, accumulate);
+  }
+}
+// global average pool: y[s][c] = (sum over H*W in raster order) * (1/(H*W))
+__global__ void gap_fwd_kernel(const bf16* x, bf16* y, int n, int HW, int C) {
+  const int64_t total = (int64_t)n * C;
+  const float inv = 1.f / (float)HW;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const int64_t s = i / C;
+    float acc = 0.f;
+    for (int k = 0; k < HW; ++k) acc = __fadd_rn(acc, __bfloat162float(x[(s * HW + k) * C + c]));
+    y[i] = __float2bfloat16_rn(__fmul_rn(acc, inv));
+  }
+}
+__global__ void gap_bwd_kernel(const bf16* dy, bf16* dx, int n, int HW, int C, int accumulate) {
+  const int64_t total = (int64_t)n * HW * C;
+  const float inv = 1.f / (float)HW;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    const int64_t s = i / ((int64_t)HW * C);
+    put_grad(dx + i, __fmul_rn(__bfloat162float(dy[s * C + c]), inv), accumulate);
+  }
+}
+}  // namespace
+
+cudaError_t launch_add_fwd(const bf16* a, const bf16* b, bf16* y, int64_t n, bool relu, cudaStream_t st) {
+  add_fwd_kernel<<<g1(n), 256, 0, st>>>(a, b, y, n, relu ? 1 : 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_add_bwd(const bf16* dy, const bf16* y, bf16* da, bf16* db, int64_t n, bool relu, bool acc_a,
+                           bool acc_b, cudaStream_t st) {
+  add_bwd_kernel<<<g1(n), 256, 0, st>>>(dy, y, da, db, n, relu ? 1 : 0, acc_a ? 1 : 0, acc_b ? 1 : 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_concat_fwd(const bf16* a, const bf16* b, bf16* y, int64_t rows, int Ca, int Cb, cudaStream_t st) {
+  concat_fwd_kernel<<<g1(rows * (Ca + Cb)), 256, 0, st>>>(a, b, y, rows, Ca, Cb);
+  return cudaGetLastError();
+}
+cudaError_t launch_concat_bwd(const bf16* dy, bf16* da, bf16* db, int64_t rows, int Ca, int Cb, bool acc_a, bool acc_b,
+                              cudaStream_t st) {
+  concat_bwd_kernel<<<g1(rows * (Ca + Cb)), 256, 0, st>>>(dy, da, db, rows, Ca, Cb, acc_a ? 1 : 0, acc_b ? 1 : 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_pool_fwd(const bf16* x, bf16* y, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
+                            int sw, int ph, int pw, bool avg, cudaStream_t st) {
+  pool_fwd_kernel<<<g1((int64_t)n * P * Q * C), 256, 0, st>>>(x, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, avg ? 1 : 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_pool_bwd(const bf16* x, const bf16* dy, bf16* dx, int n, int H, int W, int C, int P, int Q, int kh,
+                            int kw, int sh, int sw, int ph, int pw, bool avg, bool accumulate, cudaStream_t st) {
+  pool_bwd_kernel<<<g1((int64_t)n * H * W * C), 256, 0, st>>>(x, dy, dx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
+                                                              avg ? 1 : 0, accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_gap_fwd(const bf16* x, bf16* y, int n, int HW, int C, cudaStream_t st) {
+  gap_fwd_kernel<<<g1((int64_t)n * C), 256, 0, st>>>(x, y, n, HW, C);
+  return cudaGetLastError();
+}
+cudaError_t launch_gap_bwd(const bf16* dy, bf16* dx, int n, int HW, int C, bool accumulate, cudaStream_t st) {
+  gap_bwd_kernel<<<g1((int64_t)n * HW * C), 256, 0, st>>>(dy, dx, n, HW, C, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -10,16 +10,36 @@ size_t bn_ws_floats(int M, int C);
 cudaError_t launch_bn_stats(const __nv_bfloat16* x, int M, int C, float eps, const __nv_bfloat16* gamma,
                             const __nv_bfloat16* beta, float* ws, float* stats, cudaStream_t st);
 cudaError_t launch_bn_apply(const __nv_bfloat16* x, const float* stats, __nv_bfloat16* y, int n, int H, int W, int C,
-                            int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, cudaStream_t st);
+                            int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu,
+                            cudaStream_t st);
 // backward through [pool] + ReLU + BN: dgamma/dbeta into g_gamma/g_beta, dx = BN input grad
 cudaError_t launch_bn_backward(const __nv_bfloat16* x, const __nv_bfloat16* dout, const float* stats,
                                const __nv_bfloat16* gamma_b, int n, int H, int W, int C, int P, int Q, int kh, int kw,
-                               int sh, int sw, int ph, int pw, bool pool, float* ws, float* g_gamma, float* g_beta,
-                               bool accumulate, __nv_bfloat16* dx, cudaStream_t st);
+                               int sh, int sw, int ph, int pw, bool pool, bool relu, float* ws, float* g_gamma,
+                               float* g_beta, bool accumulate, __nv_bfloat16* dx, cudaStream_t st);
 cudaError_t launch_linear_fwd_bf16(const __nv_bfloat16* x, const __nv_bfloat16* W, const __nv_bfloat16* b, void* y,
                                    int n, int in, int out, bool relu, bool f32out, cudaStream_t st);
 cudaError_t launch_linear_dgrad_bf16(const void* dy, bool dy_f32, const __nv_bfloat16* mask, const __nv_bfloat16* W,
                                      __nv_bfloat16* dx, int n, int in, int out, cudaStream_t st);
 cudaError_t launch_linear_wgrad_bf16(const void* dy, bool dy_f32, const __nv_bfloat16* mask, const __nv_bfloat16* x,
                                      float* gW, float* gb, int n, int in, int out, bool accumulate, cudaStream_t st);
+}  // namespace xp
+
+namespace xp {
+cudaError_t launch_add_fwd(const __nv_bfloat16* a, const __nv_bfloat16* b, __nv_bfloat16* y, int64_t n, bool relu,
+                           cudaStream_t st);
+cudaError_t launch_add_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* y, __nv_bfloat16* da, __nv_bfloat16* db,
+                           int64_t n, bool relu, bool acc_a, bool acc_b, cudaStream_t st);
+cudaError_t launch_concat_fwd(const __nv_bfloat16* a, const __nv_bfloat16* b, __nv_bfloat16* y, int64_t rows, int Ca,
+                              int Cb, cudaStream_t st);
+cudaError_t launch_concat_bwd(const __nv_bfloat16* dy, __nv_bfloat16* da, __nv_bfloat16* db, int64_t rows, int Ca,
+                              int Cb, bool acc_a, bool acc_b, cudaStream_t st);
+cudaError_t launch_pool_fwd(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int H, int W, int C, int P, int Q, int kh,
+                            int kw, int sh, int sw, int ph, int pw, bool avg, cudaStream_t st);
+cudaError_t launch_pool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* dy, __nv_bfloat16* dx, int n, int H, int W,
+                            int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool avg,
+                            bool accumulate, cudaStream_t st);
+cudaError_t launch_gap_fwd(const __nv_bfloat16* x, __nv_bfloat16* y, int n, int HW, int C, cudaStream_t st);
+cudaError_t launch_gap_bwd(const __nv_bfloat16* dy, __nv_bfloat16* dx, int n, int HW, int C, bool accumulate,
+                           cudaStream_t st);
 }  // namespace xp

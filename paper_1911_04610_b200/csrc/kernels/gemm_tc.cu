@@ -250,6 +250,14 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
   if (row >= a.M) return;
   if (a.epi == EPI_BF16) {
     bf16* o = static_cast<bf16*>(a.out) + (int64_t)row * a.ldo + col0;
+    if (a.accumulate) {  // fan-out tensor: out = Q(old + Q(acc)) (the oracle's rounding points)
+      for (int e = 0; e < 32; ++e)
+        if (col0 + e < a.N) {
+          const float g = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[e])));
+          o[e] = __float2bfloat16_rn(__fadd_rn(__bfloat162float(o[e]), g));
+        }
+      return;
+    }
 #pragma unroll
     for (int e = 0; e < 32; e += 8) {
       if (col0 + e + 8 <= a.N) {
@@ -423,12 +431,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) 
 }
 
 // split-K reduction in fixed order z = 0..splits-1
-__global__ void reduce_bf16_kernel(const float* ws, int splits, int64_t stride, int M, int N, bf16* out, int64_t ldo) {
+__global__ void reduce_bf16_kernel(const float* ws, int splits, int64_t stride, int M, int N, bf16* out, int64_t ldo,
+                                   int accumulate) {
   const int64_t total = (int64_t)M * N;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     float acc = ws[i];
     for (int z = 1; z < splits; ++z) acc = __fadd_rn(acc, ws[z * stride + i]);
-    out[(i / N) * ldo + (i % N)] = __float2bfloat16_rn(acc);
+    bf16* o = out + (i / N) * ldo + (i % N);
+    if (accumulate) {
+      const float g = __bfloat162float(__float2bfloat16_rn(acc));
+      *o = __float2bfloat16_rn(__fadd_rn(__bfloat162float(*o), g));
+    } else {
+      *o = __float2bfloat16_rn(acc);
+    }
   }
 }
 
@@ -523,7 +538,7 @@ cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_
   if (e != cudaSuccess) return e;
   if (final_epi == EPI_BF16) {
     int grid = (int)std::min<int64_t>((plane + 255) / 256, 148 * 8);
-    reduce_bf16_kernel<<<grid, 256, 0, st>>>(ws, splits, plane, a.M, a.N, (bf16*)final_out, final_ldo);
+    reduce_bf16_kernel<<<grid, 256, 0, st>>>(ws, splits, plane, a.M, a.N, (bf16*)final_out, final_ldo, accumulate);
   } else {
     dim3 grid((a.M + 31) / 32, (a.N + 31) / 32);
     reduce_wgrad_t_kernel<<<grid, 256, 0, st>>>(ws, splits, plane, a.M, a.N, (float*)final_out, final_ldo, accumulate);
@@ -555,11 +570,11 @@ cudaError_t tc_conv_fprop(const ConvGeo& g, const bf16* X, const bf16* Wt, bf16*
 }
 
 cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const bf16* dY, const bf16* Wt, bf16* dX, float* ws,
-                          int64_t ws_elems, cudaStream_t st) {
+                          int64_t ws_elems, cudaStream_t st, bool accumulate) {
   GemmArgs a{};
   a.g = g; a.A = dY; a.B = Wt;
   a.M = g.Nimg * g.H * g.W; a.N = Cx; a.K = g.R * g.S * g.Co;
-  return run_split<GEMM_DGRAD, false, true>(a, EPI_BF16, dX, Cx, 0, ws, ws_elems, st);
+  return run_split<GEMM_DGRAD, false, true>(a, EPI_BF16, dX, Cx, accumulate ? 1 : 0, ws, ws_elems, st);
 }
 
 cudaError_t tc_conv_wgrad(const ConvGeo& g, const bf16* X, const bf16* dY, float* gW, bool accumulate, float* ws,

@@ -38,7 +38,7 @@ cudaError_t tc_conv_fprop(const ConvGeo& g, const __nv_bfloat16* X, const __nv_b
                           float* ws, int64_t ws_elems, cudaStream_t st);
 // dX [Nimg*H*W][Cx] bf16 (Cx = real input channels, multiple of 8) from dY [Nimg*P*Q][Co]
 cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const __nv_bfloat16* dY, const __nv_bfloat16* Wt,
-                          __nv_bfloat16* dX, float* ws, int64_t ws_elems, cudaStream_t st);
+                          __nv_bfloat16* dX, float* ws, int64_t ws_elems, cudaStream_t st, bool accumulate = false);
 // gW [Co][R][S][C] fp32 (=|+=) sum over pixels of dY x im2col(X)
 cudaError_t tc_conv_wgrad(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* dY, float* gW, bool accumulate,
                           float* ws, int64_t ws_elems, cudaStream_t st);

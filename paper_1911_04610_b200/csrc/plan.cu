@@ -1,4 +1,4 @@
-// plan.cu -- shape inference, layer-wise partition, fused blocks, parameter arena.
+// plan.cu -- shape inference, layer-wise partition, fused ops, tensors, parameter arena.
 #include <algorithm>
 
 #include "plan.h"
@@ -55,7 +55,7 @@ int build_net_plan(const xpipe_layer* layers, int n, int K, const xpipe_config& 
         L.nb = x.c;
         break;
       case XP_RELU: L.out = x; break;
-      case XP_MAXPOOL2D: {
+      case XP_MAXPOOL2D: case XP_AVGPOOL2D: {
         if (L.d.kh < 1 || L.d.kw < 1 || L.d.sh < 1 || L.d.sw < 1) return bad(XP_EINVAL, "pool geometry");
         const int Pp = (x.h + 2 * L.d.ph - L.d.kh) / L.d.sh + 1, Q = (x.w + 2 * L.d.pw - L.d.kw) / L.d.sw + 1;
         if (Pp < 1 || Q < 1) return bad(XP_EINVAL, "pool output is empty");
@@ -109,7 +109,7 @@ int build_net_plan(const xpipe_layer* layers, int n, int K, const xpipe_config& 
       for (int c = 0; c < base + (k >= K - r ? 1 : 0); ++c) st[q++] = k;
     for (int i = 0; i < n; ++i) P.layers[i].stage = st[unit[i]];
   }
-  // ---- stages, blocks, arena ----
+  // ---- stages, ops, tensors, arena ----
   P.stages.resize(K);
   for (int k = 0; k < K; ++k) P.stages[k].l0 = -1;
   for (int i = 0; i < n; ++i) {
@@ -118,12 +118,25 @@ int build_net_plan(const xpipe_layer* layers, int n, int K, const xpipe_config& 
     s.l1 = i + 1;
   }
   const int es = bf16 ? 2 : 4;
+  // consumers of every layer output (fusion is legal only along single-consumer chains)
+  std::vector<int> nuse(n, 0);
+  for (int i = 0; i < n; ++i) {
+    if (P.layers[i].src0 >= 0) nuse[P.layers[i].src0]++;
+    if (P.layers[i].src1 >= 0) nuse[P.layers[i].src1]++;
+  }
+  auto next_is = [&](int i, int kind, int l1) {
+    return i + 1 < l1 && P.layers[i + 1].d.kind == kind && P.layers[i + 1].src0 == i && P.layers[i + 1].src1 < 0 &&
+           nuse[i] == 1;
+  };
   for (int k = 0; k < K; ++k) {
     StagePlan& s = P.stages[k];
-    // sequential chains only in this build (DAG models: ResNet/Inception are the next rows)
+    // DAG edges may reach back only to the stage input (layer l0-1) -- R17
     for (int i = s.l0; i < s.l1; ++i) {
       const LayerInfo& L = P.layers[i];
-      if (L.src1 >= 0 || L.src0 != i - 1) return bad(XP_EUNSUPPORTED, "DAG layers (add/concat/skip) are not supported yet");
+      for (int q : {L.src0, L.src1})
+        if (q >= 0 && q < s.l0 - 1) return bad(XP_EINVAL, "a DAG edge crosses a stage cut");
+      if (L.src1 >= 0 && L.src1 == s.l0 - 1 && L.src0 == s.l0 - 1 && L.d.kind == XP_ADD)
+        return bad(XP_EUNSUPPORTED, "add of the stage input with itself");
     }
     int64_t off = 0;
     for (int i = s.l0; i < s.l1; ++i) {
@@ -134,53 +147,97 @@ int build_net_plan(const xpipe_layer* layers, int n, int K, const xpipe_config& 
     s.P = std::max<int64_t>(64, off);
     s.in = P.layers[s.l0].in0;
     s.max_act = s.in.size();
+    // tensor ids: 0 = stage input; every op output gets a new id; flatten aliases its input
+    std::vector<int> tid(n, -1);
+    if (s.l0 > 0) tid[s.l0 - 1] = 0;
+    TensorInfo tin;
+    tin.shape = s.in; tin.es = es; tin.producer = -1;
+    s.tensors.push_back(tin);
+    auto tensor_of = [&](int layer) -> int { return layer < 0 ? 0 : tid[layer]; };
     for (int i = s.l0; i < s.l1;) {
       const LayerInfo& L = P.layers[i];
-      Block B;
-      B.in = L.in0;
+      Op o;
+      o.in0 = tensor_of(L.src0);
+      o.in1 = L.src1 >= 0 ? tensor_of(L.src1) : -1;
+      if (o.in0 < 0 || (L.src1 >= 0 && o.in1 < 0)) return bad(XP_EINVAL, "source is not a tensor of this stage");
+      o.sin0 = L.in0; o.sin1 = L.in1;
+      int last = i;
       switch (L.d.kind) {
         case XP_LINEAR:
-          B.kind = BK_LINEAR; B.lmain = i; B.out = L.out;
-          if (i + 1 < s.l1 && P.layers[i + 1].d.kind == XP_RELU) B.lrelu = ++i;
-          ++i;
+          o.kind = OP_LINEAR; o.lmain = i; o.sout = L.out;
+          if (next_is(i, XP_RELU, s.l1)) { o.lrelu = ++last; o.relu = true; }
           break;
         case XP_CONV2D:
           if (!bf16) return bad(XP_EUNSUPPORTED, "Conv2d needs precision XP_BF16");
-          B.kind = BK_CONV; B.lmain = i; B.mid = L.out; B.out = L.out;
-          ++i;
-          if (i < s.l1 && P.layers[i].d.kind == XP_BATCHNORM2D) B.lbn = i++;
-          if (i < s.l1 && P.layers[i].d.kind == XP_RELU) B.lrelu = i++;
-          if (i < s.l1 && P.layers[i].d.kind == XP_MAXPOOL2D) { B.lpool = i; B.out = P.layers[i].out; ++i; }
-          if (B.lbn < 0 || B.lrelu < 0) return bad(XP_EUNSUPPORTED, "Conv2d must be followed by BatchNorm2d and ReLU");
+          o.kind = OP_CONV; o.lmain = i; o.smid = L.out; o.sout = L.out;
+          if (!next_is(last, XP_BATCHNORM2D, s.l1)) return bad(XP_EUNSUPPORTED, "Conv2d must be followed by BatchNorm2d");
+          o.lbn = ++last;
+          if (next_is(last, XP_RELU, s.l1)) { o.lrelu = ++last; o.relu = true; }
+          if (o.relu && next_is(last, XP_MAXPOOL2D, s.l1)) { o.lpool = ++last; o.sout = P.layers[last].out; }
           if (L.d.bias) return bad(XP_EUNSUPPORTED, "Conv2d bias before BatchNorm (R16: bias-free)");
           if (L.d.out_c % 8) return bad(XP_EUNSUPPORTED, "Conv2d out_channels must be a multiple of 8");
-          if (B.lmain != 0 && L.in0.c % 8) return bad(XP_EUNSUPPORTED, "Conv2d in_channels must be a multiple of 8");
+          if (!(k == 0 && L.src0 < 0) && L.in0.c % 8) return bad(XP_EUNSUPPORTED, "Conv2d in_channels must be a multiple of 8");
+          break;
+        case XP_ADD:
+          if (!bf16) return bad(XP_EUNSUPPORTED, "Add needs precision XP_BF16");
+          o.kind = OP_ADD; o.lmain = i; o.sout = L.out;
+          if (next_is(i, XP_RELU, s.l1)) { o.lrelu = ++last; o.relu = true; }
+          break;
+        case XP_CONCAT:
+          if (!bf16) return bad(XP_EUNSUPPORTED, "Concat needs precision XP_BF16");
+          o.kind = OP_CONCAT; o.lmain = i; o.sout = L.out;
+          break;
+        case XP_MAXPOOL2D: case XP_AVGPOOL2D: case XP_AVGPOOL_GLOBAL:
+          if (!bf16) return bad(XP_EUNSUPPORTED, "pooling needs precision XP_BF16");
+          o.kind = L.d.kind == XP_MAXPOOL2D ? OP_MAXPOOL : (L.d.kind == XP_AVGPOOL2D ? OP_AVGPOOL : OP_GAP);
+          o.lmain = i; o.sout = L.out;
+          if (o.sin0.c % 8) return bad(XP_EUNSUPPORTED, "pooling needs channels % 8 == 0");
           break;
         case XP_FLATTEN:
           if (L.in0.h != 1 || L.in0.w != 1) return bad(XP_EUNSUPPORTED, "Flatten of a spatial map (needs 1x1)");
+          tid[i] = o.in0;   // alias
           ++i;
           continue;
         case XP_SOFTMAX_XENT:
-          B.kind = BK_XENT; B.out = L.in0;
-          ++i;
+          o.kind = OP_XENT; o.lmain = i; o.sout = L.in0;
           break;
         default:
           return bad(XP_EUNSUPPORTED, "layer kind not supported standalone in this build (kind " +
                                           std::to_string(L.d.kind) + ")");
       }
-      s.max_act = std::max({s.max_act, B.in.size(), B.mid.size(), B.out.size()});
-      s.blocks.push_back(B);
+      if (o.kind != OP_XENT) {
+        TensorInfo t;
+        t.shape = o.sout; t.es = es; t.producer = (int)s.ops.size();
+        o.out = (int)s.tensors.size();
+        s.tensors.push_back(t);
+        for (int q = i; q <= last; ++q) tid[q] = o.out;
+      }
+      s.tensors[o.in0].consumers++;
+      if (o.in1 >= 0) s.tensors[o.in1].consumers++;
+      s.max_act = std::max({s.max_act, o.sin0.size(), o.sin1.size(), o.smid.size(), o.sout.size()});
+      s.ops.push_back(o);
+      i = last + 1;
     }
-    for (size_t b = 0; b + 1 < s.blocks.size(); ++b)
-      if (s.blocks[b + 1].kind == BK_XENT) s.blocks[b].logits = true;
-    for (const Block& B : s.blocks)
-      if (B.kind == BK_LINEAR && !bf16 && (B.lmain < 0)) return bad(XP_EINVAL, "internal");
-    // stage output = output of the last non-xent block
-    s.out = s.blocks.back().kind == BK_XENT ? s.blocks.back().out : s.blocks.back().out;
+    // the op producing the logits keeps fp32
+    if (s.ops.back().kind == OP_XENT) {
+      const int lt = s.ops.back().in0;
+      const int pr = s.tensors[lt].producer;
+      if (pr < 0 || s.ops[pr].kind != OP_LINEAR) return bad(XP_EUNSUPPORTED, "logits must come from a Linear on the last stage");
+      s.ops[pr].logits = true;
+      s.tensors[lt].es = 4;
+      s.out_tensor = lt;
+    } else {
+      s.out_tensor = tid[s.l1 - 1];
+    }
+    s.out = s.tensors[s.out_tensor].shape;
     s.in_bytes = (size_t)nm * s.in.size() * es;
     s.in_slot_bytes = s.in_bytes;
     if (k == 0 && bf16) s.in_slot_bytes = (size_t)nm * s.in.h * s.in.w * round8(s.in.c) * 2;
     s.out_bytes = (size_t)nm * s.out.size() * es;
+    // stage-0 channel padding only feeds convolutions
+    if (k == 0 && bf16 && s.in.c % 8)
+      for (const Op& o : s.ops)
+        if ((o.in0 == 0 || o.in1 == 0) && o.kind != OP_CONV) return bad(XP_EUNSUPPORTED, "network input must feed a Conv2d");
   }
   if (!bf16)
     for (const auto& L : P.layers)

@@ -1,4 +1,4 @@
-// plan.h -- static plan of the network on the GPU: shapes, partition, fused blocks, arena.
+// plan.h -- static plan of the network on the GPU: shapes, partition, fused ops, tensors, arena.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -21,31 +21,46 @@ struct LayerInfo {
   int64_t nw_torch = 0, nb = 0;   // PyTorch-layout element counts (weight, bias)
   int64_t nw_gpu = 0;             // GPU-layout weight elements (conv: Cout*R*S*Cin_pad)
   int64_t woff = -1, boff = -1;   // offsets in the stage arena
-  int cin_pad = 0;                // conv: input channels padded to a multiple of 8 (bf16)
+  int cin_pad = 0;                // conv: input channel stride (Cin padded to 8 on stage 0's input)
 };
 
-// A fused execution unit of the GPU path:
-//   BK_LINEAR : Linear [+ ReLU]                         (fp32 contract or bf16 operands)
-//   BK_CONV   : Conv2d [+ BatchNorm2d] [+ ReLU] [+ MaxPool2d]   (bf16, tcgen05)
-//   BK_XENT   : softmax cross-entropy on the logits
-enum { BK_LINEAR = 1, BK_CONV = 2, BK_XENT = 3 };
+// A fused execution unit of the GPU path (one stage = a DAG of ops in layer order):
+//   OP_CONV    : Conv2d + BatchNorm2d [+ ReLU] [+ MaxPool2d]         (bf16, tcgen05)
+//   OP_LINEAR  : Linear [+ ReLU]                                      (fp32 contract or bf16)
+//   OP_ADD     : residual add [+ ReLU]
+//   OP_CONCAT  : channel concat of two tensors
+//   OP_MAXPOOL / OP_AVGPOOL : standalone pooling;  OP_GAP : global average pool
+//   OP_XENT    : softmax cross-entropy on the logits
+enum { OP_LINEAR = 1, OP_CONV, OP_XENT, OP_ADD, OP_CONCAT, OP_MAXPOOL, OP_AVGPOOL, OP_GAP };
 
-struct Block {
+struct Op {
   int kind = 0;
   int lmain = -1, lbn = -1, lrelu = -1, lpool = -1;
-  Shape in, mid, out;      // mid = conv output before BN/ReLU/pool
-  bool logits = false;     // output feeds the softmax-xent (kept fp32)
+  int in0 = -1, in1 = -1;   // input tensor ids (0 = the stage input)
+  int out = -1;             // output tensor id (stashed per micro-batch)
+  Shape sin0, sin1, smid, sout;
+  bool relu = false;
+  bool logits = false;      // output feeds the softmax-xent (kept fp32)
+};
+
+struct TensorInfo {
+  Shape shape;
+  int es = 2;               // bytes per element (bf16 activations, fp32 logits / fp32 path)
+  int producer = -1;        // op index (-1 = stage input)
+  int consumers = 0;
 };
 
 struct StagePlan {
   int l0 = 0, l1 = 0;
-  std::vector<Block> blocks;
-  int64_t P = 0;           // arena elements (multiple of 64)
-  Shape in, out;           // stage input / output shapes
-  size_t in_bytes = 0;     // gradient message bytes (n x in) / input slot bytes
-  size_t in_slot_bytes = 0;
-  size_t out_bytes = 0;    // activation message bytes (n x out)
-  int64_t max_act = 0;     // max elements of any activation of the stage (per micro-batch)
+  std::vector<Op> ops;
+  std::vector<TensorInfo> tensors;   // [0] = stage input
+  int out_tensor = 0;                // the stage output (message to the next stage / logits)
+  int64_t P = 0;                     // arena elements (multiple of 64)
+  Shape in, out;
+  size_t in_bytes = 0;               // gradient message bytes (n x in)
+  size_t in_slot_bytes = 0;          // input ring slot bytes (stage 0: channel-padded bf16)
+  size_t out_bytes = 0;              // activation message bytes (n x out)
+  int64_t max_act = 0;               // max elements of any activation of the stage (per micro-batch)
 };
 
 struct NetPlan {

@@ -42,15 +42,14 @@ struct StageRT {
   DevState* ds = nullptr;
   uint32_t* flags = nullptr;            // [0] act_ready [1] grad_ready [2] act_ack [3] grad_ack
   int S = 1;                            // stash slots (max micro-batches in flight)
-  std::vector<void*> in_slot;           // input ring (R = S)
+  std::vector<void*> in_slot;           // input ring (R = S); = act[0]
   std::vector<void*> gin_slot;          // gradient ring (R = S), k < K-1
-  std::vector<std::vector<void*>> out;  // [block][slot] block outputs
-  std::vector<std::vector<void*>> mid;  // [block][slot] conv outputs (bf16 path)
-  std::vector<std::vector<float*>> stats;
+  std::vector<std::vector<void*>> act;  // [tensor][slot] stashed activations (tensor 0 = in_slot)
+  std::vector<std::vector<void*>> mid;  // [op][slot] conv outputs before BN (bf16 path)
+  std::vector<std::vector<float*>> stats;  // [op][slot] BN mean, rstd, gamma_f, beta_f
   std::vector<float*> dz;               // [slot] logits gradient (last stage)
-  std::vector<float*> logits;           // [slot]
-  void* gbuf[2] = {nullptr, nullptr};   // backward gradient ping-pong
-  void* gmid = nullptr;                 // conv block: gradient of the conv output (bf16)
+  std::vector<void*> grad;              // [tensor] activation-gradient buffers (per op pass)
+  void* gmid = nullptr;                 // conv op: gradient of the conv output (bf16)
   int64_t gbuf_elems = 0;
   float* ws = nullptr;                  // split-K workspace (fp32)
   int64_t ws_elems = 0;
@@ -106,13 +105,16 @@ int check_launch(xpipe_ctx* c, cudaError_t e, const char* what);
 int allocate_stage(xpipe_ctx* c, StageRT& s);
 int init_stage_params(xpipe_ctx* c, StageRT& s, const xpipe_layer* layers);
 int stage_input(xpipe_ctx* c, StageRT& s, const float* x_nchw, void* dst);
-int block_forward(xpipe_ctx* c, StageRT& s, size_t b, const void* x, const void* Wf, int slot);
-int block_backward(xpipe_ctx* c, StageRT& s, int b, const void* x, const void* dy, void* dx, const void* Wb, int slot,
-                   bool accumulate);
+// forward of op o on micro-batch slot under Wf (writes act[o.out][slot])
+int op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot, int64_t u);
+// backward of op o: dy = gradient of its output; writes/accumulates the input gradients
+// (dx0/dx1 may be NULL when not needed; acc0/acc1 = add into an existing contribution)
+int op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0, bool acc0, void* dx1, bool acc1,
+                const void* Wb, int slot, bool accumulate_g);
 // bf16_blocks.cu
-int bf16_block_forward(xpipe_ctx* c, StageRT& s, size_t b, const void* x, const void* Wf, int slot);
-int bf16_block_backward(xpipe_ctx* c, StageRT& s, int b, const void* x, const void* dy, void* dx, const void* Wb,
-                        int slot, bool accumulate);
+int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot);
+int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0, bool acc0, void* dx1, bool acc1,
+                     const void* Wb, int slot, bool accumulate_g);
 // xpipe.cu
 int version_difference(const xpipe_ctx* c, int k, int pass);
 int version_difference_public(const xpipe_ctx* c, int k, int pass);

@@ -206,7 +206,7 @@ int reserve_for_call(xpipe_ctx* c, int64_t M) {
     }
     if (c->cfg.profile) {
       int nconv = 0;
-      for (const Block& B : s.plan.blocks) nconv += B.kind == BK_CONV;
+      for (const Op& O : s.plan.ops) nconv += O.kind == OP_CONV;
       const size_t want = (size_t)2 * (3 * nconv + 1) * (size_t)(M * c->T + c->K + 1);
       while (s.ev_pool.size() < want) {
         cudaEvent_t e;
@@ -246,25 +246,13 @@ int enqueue_forward(xpipe_ctx* c, int k, int64_t u) {
   XP_TRY(trace_slot(c, s, &rec));
   if (rec) XP_TRY(check_launch(c, launch_trace_begin(s.ds, rec, k, 0, (int)t, (int)j, sf, bw, s.stream), "trace"));
   if (bw) s.host_fver = s.host_ver;
-  void* Wf = s.pf[s.host_fver & 1];
-  const void* x = s.in_slot[slot];
-  for (size_t b = 0; b < s.plan.blocks.size(); ++b) {
-    const Block& B = s.plan.blocks[b];
-    if (B.kind == BK_XENT) {
-      const int32_t* y = c->y_dev + (u - c->call_first) * c->n;
-      float* loss = c->loss_dev + (u - c->call_first);
-      XP_TRY(check_launch(c, launch_xent_f32((const float*)x, y, s.dz[slot], loss, c->n, B.out.c,
-                                             (float)(1.0 / (double)c->N), s.stream), "xent"));
-      continue;
-    }
-    XP_TRY(block_forward(c, s, b, x, Wf, slot));
-    x = s.out[b][slot];
-  }
+  const void* Wf = s.pf[s.host_fver & 1];
+  for (size_t o = 0; o < s.plan.ops.size(); ++o) XP_TRY(op_forward(c, s, (int)o, Wf, slot, u));
   if (k + 1 < c->K) {
     StageRT& nx = c->S[k + 1];
     XP_TRY(flag_wait(c, s, &s.flags[2], u - nx.S));  // ring credit: consumer released u - R
-    const size_t bytes = s.plan.out_bytes;
-    XP_CUDA(c, cudaMemcpyAsync(nx.in_slot[(u - 1) % nx.S], x, bytes, cudaMemcpyDefault, s.stream));
+    XP_CUDA(c, cudaMemcpyAsync(nx.in_slot[(u - 1) % nx.S], s.act[s.plan.out_tensor][slot], s.plan.out_bytes,
+                               cudaMemcpyDefault, s.stream));
     XP_TRY(flag_write(c, s, &nx.flags[0], u));
   }
   if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
@@ -284,25 +272,30 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
   if (rec) XP_TRY(check_launch(c, launch_trace_begin(s.ds, rec, k, 1, (int)t, (int)j, sb, bw, s.stream), "trace"));
   if (bw) s.host_bver = s.host_ver;
   const bool accumulate = (j != 1);
-  // gradient of the stage output
-  const void* dy = (k + 1 < c->K) ? s.gin_slot[slot] : (const void*)s.dz[slot];
-  int pp = 0;
-  const int nb = (int)s.plan.blocks.size();
-  for (int b = nb - 1; b >= 0; --b) {
-    const Block& B = s.plan.blocks[b];
-    if (B.kind == BK_XENT) continue;
-    const void* x = b == 0 ? s.in_slot[slot] : s.out[b - 1][slot];
-    const bool need_dx = !(b == 0 && k == 0);
-    void* dx = need_dx ? s.gbuf[pp] : nullptr;
-    XP_TRY(block_backward(c, s, b, x, dy, dx, s.pb, slot, accumulate));
-    dy = dx;
-    pp ^= 1;
+  // gradient bookkeeping over the stage's tensors: the output gradient is the gradient ring
+  // slot (or dz on the last stage); every other tensor's gradient is written by its first
+  // consumer (reverse op order) and accumulated by the others
+  const StagePlan& P = s.plan;
+  std::vector<char> has(P.tensors.size(), 0);
+  std::vector<void*> gp(s.grad);
+  gp[P.out_tensor] = (k + 1 < c->K) ? s.gin_slot[slot] : (void*)s.dz[slot];
+  has[P.out_tensor] = 1;
+  for (int o = (int)P.ops.size() - 1; o >= 0; --o) {
+    const Op& O = P.ops[o];
+    if (O.kind == OP_XENT || !has[O.out]) continue;
+    const bool need0 = !(O.in0 == 0 && k == 0);  // the first stage needs no input gradient
+    const bool need1 = O.in1 >= 0 && !(O.in1 == 0 && k == 0);
+    XP_TRY(op_backward(c, s, o, gp[O.out], need0 ? gp[O.in0] : nullptr, need0 && has[O.in0],
+                       need1 ? gp[O.in1] : nullptr, need1 && has[O.in1], s.pb, slot, accumulate));
+    if (need0) has[O.in0] = 1;
+    if (need1) has[O.in1] = 1;
   }
   if (k + 1 < c->K) XP_TRY(flag_write(c, s, &c->S[k + 1].flags[3], u));  // released gin slot u
   if (k > 0) {
+    if (!has[0]) return set_err(c, XP_ESCHED, "no gradient reaches the stage input (internal)");
     StageRT& pv = c->S[k - 1];
     XP_TRY(flag_wait(c, s, &s.flags[3], u - pv.S));
-    XP_CUDA(c, cudaMemcpyAsync(pv.gin_slot[(u - 1) % pv.S], dy, s.plan.in_bytes, cudaMemcpyDefault, s.stream));
+    XP_CUDA(c, cudaMemcpyAsync(pv.gin_slot[(u - 1) % pv.S], gp[0], P.in_bytes, cudaMemcpyDefault, s.stream));
     XP_TRY(flag_write(c, s, &pv.flags[1], u));
     XP_TRY(flag_write(c, s, &pv.flags[2], u));  // released our input slot u
   }
@@ -352,6 +345,36 @@ int drive(xpipe_ctx* c, int64_t total) {
   return XP_OK;
 }
 
+// on a watchdog timeout: read the ring flags and the trace tail through a side stream
+// (never blocking on a hung device) into the error message
+std::string pipeline_state(xpipe_ctx* c) {
+  std::string out;
+  for (auto& s : c->S) {
+    cudaSetDevice(s.dev);
+    cudaStream_t side;
+    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) return out + " (no side stream)";
+    uint32_t f[4] = {0, 0, 0, 0};
+    TraceRec last{};
+    cudaMemcpyAsync(f, s.flags, 16, cudaMemcpyDeviceToHost, side);
+    if (c->cfg.trace && s.trace_n) cudaMemcpyAsync(&last, s.trace_dev + s.trace_n - 1, sizeof(TraceRec), cudaMemcpyDeviceToHost, side);
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, side);
+    auto t0 = std::chrono::steady_clock::now();
+    bool ok = false;
+    while (std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count() < 2000) {
+      if (cudaEventQuery(e) == cudaSuccess) { ok = true; break; }
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+    char buf[512];
+    snprintf(buf, sizeof buf, " | stage %d: pos=%lld host_ver=%d flags(act_ready,grad_ready,act_ack,grad_ack)=%s%u,%u,%u,%u"
+             " trace_n=%lld last={op=%d t=%d j=%d t1=%llu}", s.k, (long long)s.pos, s.host_ver, ok ? "" : "(unread)",
+             f[0], f[1], f[2], f[3], (long long)s.trace_n, last.op, last.t, last.j, (unsigned long long)last.t1_ns);
+    out += buf;
+  }
+  return out;
+}
+
 int sync_all(xpipe_ctx* c) {
   const int ms = c->cfg.watchdog_ms > 0 ? c->cfg.watchdog_ms : 120000;
   auto t0 = std::chrono::steady_clock::now();
@@ -362,7 +385,8 @@ int sync_all(xpipe_ctx* c) {
       if (e == cudaSuccess) break;
       if (e != cudaErrorNotReady) return set_err(c, XP_ECUDA, std::string("stream: ") + cudaGetErrorString(e));
       if (std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count() > ms)
-        return set_err(c, XP_ESCHED, "pipeline watchdog: stage " + std::to_string(s.k) + " did not drain");
+        return set_err(c, XP_ESCHED, "pipeline watchdog: stage " + std::to_string(s.k) + " did not drain" +
+                                         pipeline_state(c));
       std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
   }

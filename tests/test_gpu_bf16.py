@@ -109,3 +109,29 @@ def test_config2_vgg16_cifar(oracle_mod):
     L = S.vgg16_cifar()
     g, o, P, lg, lo = run_bf16(oracle_mod, L, (3, 32, 32), 4, 4, 128, 10, kind="cifar")
     check(g, o, L, 4, 10)
+
+
+def model_count_dag(L, i, t):
+    return model_count(L, i, t)
+
+
+@pytest.mark.parametrize("K", [1, 3])
+def test_resnet_blocks_bf16(oracle_mod, K):
+    """ResNet-101 block structure (7x7 s2 stem + 3x3 s2 maxpool, bottlenecks with strided 1x1
+    downsample, residual add + ReLU, global average pool), one bottleneck per stage group,
+    explicit unit-based stages (R17)."""
+    from synthetic.models import resnet101, assign_stages
+    L, units = resnet101(classes=10, layers=(1, 1, 1, 1))
+    L = assign_stages(L, units, K)
+    g, o, P, lg, lo = run_bf16(oracle_mod, L, (3, 32, 32), K, 2, 16, 6, kind="imagenet")
+    check(g, o, L, K, 6)
+
+
+def test_inception_v3_bf16(oracle_mod):
+    """The full Inception-V3 topology at 64x64 (R14): asymmetric 1x7/7x1/1x3/3x1 kernels,
+    average-pool branches, stride-2 reductions, four-way concats; 2 stages."""
+    from synthetic.models import inception_v3, assign_stages
+    L, units = inception_v3(classes=10)
+    L = assign_stages(L, units, 2)
+    g, o, P, lg, lo = run_bf16(oracle_mod, L, (3, 64, 64), 2, 2, 16, 3, kind="imagenet")
+    check(g, o, L, 2, 3)

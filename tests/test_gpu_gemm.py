@@ -16,7 +16,7 @@ def bf(t):
 @pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, True), (False, False)])
 @pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 200, 136), (129, 256, 1000), (64, 72, 8), (1000, 512, 64)])
 def test_plain_gemm_all_majorness(a_k, b_k, M, N, K):
-    from paper_1911_04610_b200 import gemm_bf16
+    from paper_1911_04610_b200 import gemm_bf16, XPipeError
     g = torch.Generator().manual_seed(M * 7 + N)
     A = torch.randn(M, K, generator=g)
     B = torch.randn(N, K, generator=g)
@@ -24,6 +24,10 @@ def test_plain_gemm_all_majorness(a_k, b_k, M, N, K):
     A_dev = (Ab if a_k else Ab.t().contiguous()).to(DEV)
     B_dev = (Bb if b_k else Bb.t().contiguous()).to(DEV)
     D = torch.full((M, N), float("nan"), device=DEV)
+    if (K if a_k else M) % 8 or (K if b_k else N) % 8:
+        with pytest.raises(XPipeError):   # rows of 16 bytes are required (documented EINVAL)
+            gemm_bf16(A_dev, B_dev, D, M, N, K, a_k, b_k)
+        return
     gemm_bf16(A_dev, B_dev, D, M, N, K, a_k, b_k)
     torch.cuda.synchronize()
     ref = Ab.double() @ Bb.double().t()

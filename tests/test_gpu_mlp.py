@@ -28,7 +28,8 @@ def run_pair(oracle_mod, K, T, N, M, lr=1e-4, calls=None, schedule="xpipe", pred
     o = oracle_mod.Oracle(L, K, T, N, lr, (0.9, 0.999), 1e-8, in_shape, 10, P, mode="fp32", schedule=schedule,
                           predict=predict, s_fwd=s_fwd, s_bwd=s_bwd, snapshots=True)
     g = XPipe(L, K, T, N, lr, (0.9, 0.999), 1e-8, in_shape, 10, params=P, precision="fp32", schedule=schedule,
-              predict=predict, s_fwd=s_fwd, s_bwd=s_bwd, snapshots=True, trace=True)
+              predict=predict, s_fwd=s_fwd, s_bwd=s_bwd, snapshots=True, trace=True,
+              watchdog_ms=20000)
     calls = calls or [M]
     off = 0
     lo, lg = [], []
@@ -68,7 +69,7 @@ def assert_pipeline_equal(o, g, L, K, M):
 
 
 @pytest.mark.parametrize("lr", [1e-4, 1e-3])
-def test_config1_mlp_two_stages(oracle_mod, lr):
+def test_config1_mlp_two_stages(oracle_mod, lr):  # noqa: runs after the single-stage case below
     """BASELINE.json configs[0]: MLP 784-256-256-256-10, 2 stages, N=32, T=4, Adam, M=10."""
     o, g, L, lo, lg = run_pair(oracle_mod, 2, 4, 32, 10, lr=lr)
     assert_pipeline_equal(o, g, L, 2, 10)

@@ -218,82 +218,107 @@ def main():
 
     import numpy as np
     import synthetic as S
-    from paper_1911_04610_b200 import XPipe
-    K = args.stages or args.gpus
+    from paper_1911_04610_b200 import XPipe, connect_pipeline
     L, shape, classes, kind, N, T, prec = workload_model(args.workload)
     M = args.minibatches
-    # One process drives every stage of the pipeline through the C-ABI library (stage k on
-    # GPU k % n_gpus); the other ranks of a torchrun launch only join the barriers.
-    value = e2e = None
-    result = {}
-    if rank == 0:
-        P = S.make_params(L, 1)
+    mp_mode = ws > 1
+    K = ws if mp_mode else (args.stages or args.gpus)
+    dev = local if mp_mode else 0
+    P = S.make_params(L, 1)
+    if mp_mode:
+        # one process per GPU: this rank owns stage `rank`; rings/flags are CUDA IPC-mapped
+        import torch.distributed as dist
+        g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec, profile=True,
+                  watchdog_ms=300000, my_stage=rank)
+        connect_pipeline(g, dist.new_group(backend="gloo"))
+    else:
         g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
                   devices=list(range(args.gpus)), profile=True, watchdog_ms=300000)
-        x, y = S.make_inputs(M * N, shape, classes, 1, kind=kind)
-        xd = torch.from_numpy(x).cuda(0)
-        yd = torch.from_numpy(y).cuda(0 if K == 1 else (K - 1) % args.gpus)
-        for _ in range(args.warmup):
-            g.step(xd, yd, M)
-        prof = {}
-        launches = 0
-        with Clocks(0) as ck:
-            g.timer_start()
-            for _ in range(args.steps):
-                g.step(xd, yd, M, losses=False)
-                st = g.last_stats
-                launches += st.kernel_launches
-                for name, d in st.profile().items():
-                    q = prof.setdefault(name, {"ms": 0.0, "launches": 0, "work": 0.0})
-                    q["ms"] += d["ms"]; q["launches"] += d["launches"]; q["work"] += d["work"]
-            ms = g.timer_stop()
-        clocks = ck.summary()
-        value = args.steps * M * N / (ms * 1e-3)
-        # ---- roofline of the dominant kernel class (CUDA events on the launching streams)
-        dom = max(prof, key=lambda k: prof[k]["ms"])
-        d = prof[dom]
-        if dom == "sweep":
-            ach = d["work"] / (d["ms"] * 1e-3) / 1e9
-            roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
-        else:
-            ach = d["work"] / (d["ms"] * 1e-3) / 1e12
-            roof = {"bound": "tensor", "achieved": ach, "peak": peaks.get("bf16_tflops_sustained", 1400.0),
-                    "unit": "TFLOP/s"}
-        roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = None
-        roof["kernel"] = dom
-        roof["peak_source"] = peak_kind + (" (sustained)" if roof["bound"] == "tensor" else "")
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            with open(tp) as f:
-                tr = json.load(f).get(dom)
-            if tr is not None:
-                roof["traffic"] = tr
-        shares = {k: {"ms_per_step": v["ms"] / args.steps, "share_of_step": v["ms"] / ms,
-                      "achieved": (v["work"] / (v["ms"] * 1e-3) / (1e9 if k == "sweep" else 1e12)) if v["ms"] else 0,
-                      "unit": "GB/s" if k == "sweep" else "TFLOP/s", "launches": v["launches"]}
-                  for k, v in prof.items()}
-        # ---- end to end through the public API with host (pinned) buffers
-        if not args.no_e2e:
-            xh = torch.from_numpy(x).pin_memory()
-            yh = torch.from_numpy(y).pin_memory()
-            xh_np, yh_np = xh.numpy(), yh.numpy()
-            g.step(xh_np, yh_np, M)
-            t0 = time.perf_counter()
-            for _ in range(args.steps):
-                g.step(xh_np, yh_np, M, losses=True)
-            e2e_s = time.perf_counter() - t0
-            e2e = {"value": args.steps * M * N / e2e_s, "unit": "samples/s",
-                   "h2d_bytes_per_step": int(x.nbytes + y.nbytes), "d2h_bytes_per_step": int(M * T * 4)}
-        g.close()
-        result = dict(ms=ms, clocks=clocks, roof=roof, shares=shares, launches=launches)
-    if ws > 1:
+    x, y = S.make_inputs(M * N, shape, classes, 1, kind=kind)
+    last_dev = dev if mp_mode else (K - 1) % args.gpus
+    xd = torch.from_numpy(x).cuda(dev)
+    yd = torch.from_numpy(y).cuda(last_dev)
+
+    def barrier():
+        if mp_mode:
+            import torch.distributed as dist
+            dist.barrier()
+    for _ in range(args.warmup):
+        g.step(xd, yd, M)
+    barrier()
+    prof = {}
+    launches = 0
+    with Clocks(dev) as ck:
+        g.timer_start()
+        for _ in range(args.steps):
+            g.step(xd, yd, M, losses=False)
+            st = g.last_stats
+            launches += st.kernel_launches
+            for name, d in st.profile().items():
+                q = prof.setdefault(name, {"ms": 0.0, "launches": 0, "work": 0.0})
+                q["ms"] += d["ms"]; q["launches"] += d["launches"]; q["work"] += d["work"]
+        ms = g.timer_stop()
+        barrier()
+    clocks = ck.summary()
+    e2e_s = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(x).pin_memory()
+        yh = torch.from_numpy(y).pin_memory()
+        xh_np, yh_np = xh.numpy(), yh.numpy()
+        g.step(xh_np, yh_np, M)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            g.step(xh_np, yh_np, M, losses=True)
+        barrier()
+        e2e_s = time.perf_counter() - t0
+    if mp_mode:
         import torch.distributed as dist
-        t = torch.tensor([result.get("ms", 0.0)], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allp = [None] * ws
+        dist.all_gather_object(allp, {"ms": ms, "prof": prof, "launches": launches, "e2e_s": e2e_s})
+        ms = max(p["ms"] for p in allp)                       # max over ranks
+        e2e_s = None if e2e_s is None else max(p["e2e_s"] for p in allp)
+        launches = sum(p["launches"] for p in allp)
+        prof = {}
+        for p in allp:
+            for name, d in p["prof"].items():
+                q = prof.setdefault(name, {"ms": 0.0, "launches": 0, "work": 0.0})
+                q["ms"] += d["ms"]; q["launches"] += d["launches"]; q["work"] += d["work"]
         dist.barrier()
+    g.close()
     if rank != 0:
         return 0
+    value = args.steps * M * N / (ms * 1e-3)
+    e2e = None
+    if e2e_s is not None:
+        e2e = {"value": args.steps * M * N / e2e_s, "unit": "samples/s",
+               "h2d_bytes_per_step": int(x.nbytes + y.nbytes), "d2h_bytes_per_step": int(M * T * 4)}
+    # ---- roofline of the dominant kernel class (CUDA events on the launching streams)
+    total_prof_ms = sum(v["ms"] for v in prof.values())
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    d = prof[dom]
+    if dom == "sweep":
+        roof = {"bound": "hbm", "achieved": d["work"] / (d["ms"] * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s"}
+    else:
+        roof = {"bound": "tensor", "achieved": d["work"] / (d["ms"] * 1e-3) / 1e12,
+                "peak": peaks.get("bf16_tflops_sustained", 1400.0), "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = dom
+    roof["launches_per_step"] = d["launches"] / args.steps
+    roof["peak_source"] = peak_kind + (" (sustained)" if roof["bound"] == "tensor" else "")
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tr = json.load(f).get(dom)
+        if tr is not None:
+            roof["traffic"] = tr
+    shares = {k: {"ms_per_step": v["ms"] / args.steps, "share_of_step": v["ms"] / (ms * (ws if mp_mode else 1)),
+                  "achieved": (v["work"] / (v["ms"] * 1e-3) / (1e9 if k == "sweep" else 1e12)) if v["ms"] else 0,
+                  "unit": "GB/s" if k == "sweep" else "TFLOP/s", "launches": v["launches"]}
+              for k, v in prof.items()}
+    result = dict(ms=ms, clocks=clocks, roof=roof, shares=shares, launches=launches)
     cpu = None if args.no_cpu_baseline else cpu_baseline(args.workload)
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": result["ms"] / args.steps, "higher_is_better": True,
@@ -302,6 +327,7 @@ def main():
                                    % ("VGG-16 on synthetic CIFAR-10 32x32 (BASELINE configs[1])"
                                       if args.workload == "vgg16" else "MLP 784-256-256-256-10 (configs[0])",
                                       K, N, T, M),
+                       "processes": "one per GPU (CUDA IPC rings)" if ws > 1 else "one process",
                        "global_batch": N, "stages": K, "micro_batches": T, "minibatches_per_step": M,
                        "parallelism": "pipeline K=%d (XPipe)" % K,
                        "l2": "working set > L2: optimizer state 16 B/param x 14.7M params = 235 MB (126 MB L2)"},

@@ -102,6 +102,9 @@ typedef struct {
   int32_t graphs;                     /* capture repeated step calls as CUDA graphs */
   int32_t profile;                    /* record CUDA events around every sweep launch */
   int32_t watchdog_ms;                /* xpipe_step timeout (0 = 120000) */
+  int32_t multi_process;              /* 1 = one process per stage: this process owns stage my_stage
+                                         only; neighbours are attached with xpipe_ipc_import */
+  int32_t my_stage;
   /* optional initial tensors, float32, PyTorch layout, [2*layer + XP_T_*]; NULL = seeded init */
   const float* const* init_params;
   const float* const* init_m;         /* with XP_MOM_GIVEN, same indexing */
@@ -182,6 +185,15 @@ int64_t xpipe_stage_params(struct xpipe_ctx* h, int32_t stage);
    stream, which = 1 a stop event; after a stop, *ms_out (nullable) = max over stages of the
    device time between the two events (CUDA events on the streams the kernels run on). */
 int xpipe_timer(struct xpipe_ctx* h, int32_t which, double* ms_out);
+
+/* One-process-per-GPU mode (cfg.multi_process = 1).  Each process owns one stage; its
+   input ring, gradient ring and flags are exported as CUDA IPC handles (xpipe_ipc_export
+   writes an opaque blob of *len <= cap bytes, cap >= 4096) and every process imports the
+   blobs of its neighbours (xpipe_ipc_import, any order, before the first xpipe_step).  The
+   host logic never waits on another process: the device flags carry all ordering.
+   Errors: XP_EINVAL (not in multi-process mode, foreign or malformed blob), XP_ECUDA. */
+int xpipe_ipc_export(struct xpipe_ctx* h, void* blob, size_t cap, size_t* len);
+int xpipe_ipc_import(struct xpipe_ctx* h, const void* blob, size_t len);
 
 /* NULL-safe, idempotent; frees everything the context owns. */
 int xpipe_finalize(struct xpipe_ctx* h);

@@ -25,16 +25,25 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
   s.W = (float*)A(P * 4); s.g = (float*)A(P * 4); s.m = (float*)A(P * 4); s.v = (float*)A(P * 4);
   s.pf[0] = A(P * pes); s.pf[1] = A(P * pes); s.pb = A(P * pes);
   s.ds = (DevState*)A(sizeof(DevState));
-  s.flags = (uint32_t*)A(64);
+  s.flags = (uint32_t*)dmalloc_shared(c, 64, s.dev);
   if (!s.W || !s.g || !s.m || !s.v || !s.pf[0] || !s.pf[1] || !s.pb || !s.ds || !s.flags)
     return set_err(c, XP_ENOMEM, "arena");
   XP_CUDA(c, cudaMemsetAsync(s.flags, 0, 64, s.stream));
   const int n = c->n;
+  // rings: one contiguous allocation each (one IPC handle per ring in multi-process mode)
+  s.in_stride = (p.in_slot_bytes + 255) & ~size_t(255);
+  s.gin_stride = (p.out_bytes + 255) & ~size_t(255);
+  uint8_t* ring = (uint8_t*)dmalloc_shared(c, s.in_stride * s.S, s.dev);
+  if (!ring) return set_err(c, XP_ENOMEM, "input ring");
+  s.in_ring = ring;
   s.in_slot.resize(s.S);
-  for (auto& q : s.in_slot) if (!(q = A(p.in_slot_bytes))) return set_err(c, XP_ENOMEM, "input ring");
+  for (int i = 0; i < s.S; ++i) s.in_slot[i] = ring + i * s.in_stride;
   if (s.k + 1 < c->K) {
+    uint8_t* gr = (uint8_t*)dmalloc_shared(c, s.gin_stride * s.S, s.dev);
+    if (!gr) return set_err(c, XP_ENOMEM, "gradient ring");
+    s.gin_ring = gr;
     s.gin_slot.resize(s.S);
-    for (auto& q : s.gin_slot) if (!(q = A(p.out_bytes))) return set_err(c, XP_ENOMEM, "gradient ring");
+    for (int i = 0; i < s.S; ++i) s.gin_slot[i] = gr + i * s.gin_stride;
   }
   // per-micro-batch stash of every op output (tensor 0 is the input ring itself)
   s.act.assign(p.tensors.size(), {});

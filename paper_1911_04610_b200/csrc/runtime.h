@@ -42,6 +42,9 @@ struct StageRT {
   DevState* ds = nullptr;
   uint32_t* flags = nullptr;            // [0] act_ready [1] grad_ready [2] act_ack [3] grad_ack
   int S = 1;                            // stash slots (max micro-batches in flight)
+  void* in_ring = nullptr;              // contiguous ring allocations (IPC-exportable)
+  void* gin_ring = nullptr;
+  size_t in_stride = 0, gin_stride = 0;
   std::vector<void*> in_slot;           // input ring (R = S); = act[0]
   std::vector<void*> gin_slot;          // gradient ring (R = S), k < K-1
   std::vector<std::vector<void*>> act;  // [tensor][slot] stashed activations (tensor 0 = in_slot)
@@ -85,6 +88,9 @@ struct xpipe_ctx {
   xpipe_config cfg{};
   std::vector<StageRT> S;
   std::vector<Alloc> allocs;
+  std::vector<void*> ipc_allocs;     // cudaMalloc'ed (exportable) rings/flags, multi-process mode
+  std::vector<void*> ipc_opened;     // neighbour memory mapped with cudaIpcOpenMemHandle
+  bool mp() const { return cfg.multi_process != 0; }
   // per-call buffers
   float* x_dev = nullptr; int64_t x_cap = 0;
   int32_t* y_dev = nullptr; int64_t y_cap = 0;
@@ -100,6 +106,8 @@ struct xpipe_ctx {
 namespace xp {
 // blocks.cu
 void* dmalloc(xpipe_ctx* c, size_t bytes, int dev);
+void* dmalloc_shared(xpipe_ctx* c, size_t bytes, int dev);  // IPC-exportable in multi-process mode
+inline bool owned(const StageRT& s) { return s.stream != nullptr; }
 int set_err(xpipe_ctx* c, int code, const std::string& m);
 int check_launch(xpipe_ctx* c, cudaError_t e, const char* what);
 int allocate_stage(xpipe_ctx* c, StageRT& s);

@@ -86,6 +86,16 @@ void* dmalloc(xpipe_ctx* c, size_t bytes, int dev) {
   return p;
 }
 
+void* dmalloc_shared(xpipe_ctx* c, size_t bytes, int dev) {
+  if (!c->mp()) return dmalloc(c, bytes, dev);
+  bytes = (bytes + 255) & ~size_t(255);
+  void* p = nullptr;
+  cudaSetDevice(dev);
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  c->ipc_allocs.push_back(p);
+  return p;
+}
+
 void free_all(xpipe_ctx* c) {
   for (auto& s : c->S) {
     for (auto& sn : s.snaps) if (sn.pinned) cudaFreeHost(sn.pinned);
@@ -97,6 +107,10 @@ void free_all(xpipe_ctx* c) {
     for (auto& e : s.tmark) if (e) { cudaEventDestroy(e); e = nullptr; }
     if (s.stream) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.stream); cudaStreamDestroy(s.stream); s.stream = nullptr; }
   }
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  c->ipc_opened.clear();
+  for (void* p : c->ipc_allocs) cudaFree(p);
+  c->ipc_allocs.clear();
   for (auto it = c->allocs.rbegin(); it != c->allocs.rend(); ++it) {
     if (c->cfg.free) c->cfg.free(it->p, it->bytes, it->dev, c->cfg.alloc_user);
     else { cudaSetDevice(it->dev); cudaFree(it->p); }
@@ -192,6 +206,7 @@ int trace_slot(xpipe_ctx* c, StageRT& s, TraceRec** rec) {
 // work writes, a device-wide synchronisation would deadlock the pipeline.
 int reserve_for_call(xpipe_ctx* c, int64_t M) {
   for (auto& s : c->S) {
+    if (!owned(s)) continue;
     if (c->cfg.trace) {
       const int64_t need = 3 * (c->fed + c->T) + 64;  // <= 2 ops per micro-batch + 1 update per mini-batch
       if (need > s.trace_cap) {
@@ -328,6 +343,7 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
 int drive(xpipe_ctx* c, int64_t total) {
   for (int k = 0; k < c->K; ++k) {
     StageRT& s = c->S[k];
+    if (!owned(s)) continue;
     while (!s.done) {
       int op;
       int64_t u;
@@ -350,6 +366,7 @@ int drive(xpipe_ctx* c, int64_t total) {
 std::string pipeline_state(xpipe_ctx* c) {
   std::string out;
   for (auto& s : c->S) {
+    if (!owned(s)) continue;
     cudaSetDevice(s.dev);
     cudaStream_t side;
     if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) return out + " (no side stream)";
@@ -379,6 +396,7 @@ int sync_all(xpipe_ctx* c) {
   const int ms = c->cfg.watchdog_ms > 0 ? c->cfg.watchdog_ms : 120000;
   auto t0 = std::chrono::steady_clock::now();
   for (auto& s : c->S) {
+    if (!owned(s)) continue;
     cudaSetDevice(s.dev);
     for (;;) {
       cudaError_t e = cudaStreamQuery(s.stream);
@@ -398,10 +416,11 @@ int ensure_call_buffers(xpipe_ctx* c, int64_t M) {
   const int64_t xs = M * c->N * per, ys = M * c->N, ls = M * c->T;
   if (xs > c->x_cap || ys > c->y_cap || ls > c->loss_cap) {
     XP_TRY(sync_all(c));
-    if (xs > c->x_cap) { c->x_dev = (float*)dmalloc(c, xs * 4, c->S[0].dev); c->x_cap = xs; }
-    if (ys > c->y_cap) { c->y_dev = (int32_t*)dmalloc(c, ys * 4, c->S[c->K - 1].dev); c->y_cap = ys; }
-    if (ls > c->loss_cap) { c->loss_dev = (float*)dmalloc(c, ls * 4, c->S[c->K - 1].dev); c->loss_cap = ls; }
-    if (!c->x_dev || !c->y_dev || !c->loss_dev) return set_err(c, XP_ENOMEM, "call buffers");
+    const bool first = owned(c->S[0]), last = owned(c->S[c->K - 1]);
+    if (first && xs > c->x_cap) { c->x_dev = (float*)dmalloc(c, xs * 4, c->S[0].dev); c->x_cap = xs; }
+    if (last && ys > c->y_cap) { c->y_dev = (int32_t*)dmalloc(c, ys * 4, c->S[c->K - 1].dev); c->y_cap = ys; }
+    if (last && ls > c->loss_cap) { c->loss_dev = (float*)dmalloc(c, ls * 4, c->S[c->K - 1].dev); c->loss_cap = ls; }
+    if ((first && !c->x_dev) || (last && (!c->y_dev || !c->loss_dev))) return set_err(c, XP_ENOMEM, "call buffers");
   }
   return XP_OK;
 }
@@ -436,6 +455,8 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
   if (cfg->schedule != XP_SCHED_XPIPE && cfg->schedule != XP_SCHED_GPIPE) return set_err(nullptr, XP_EINVAL, "schedule");
   if (cfg->predict < 0 || cfg->predict > 2 || (cfg->predict == XP_PRED_FIXED && (cfg->s_fwd < 0 || cfg->s_bwd < 0)))
     return set_err(nullptr, XP_EINVAL, "predict");
+  if (cfg->multi_process && (cfg->my_stage < 0 || cfg->my_stage >= stages))
+    return set_err(nullptr, XP_EINVAL, "my_stage out of range");
   std::unique_ptr<xpipe_ctx> c(new xpipe_ctx());
   c->cfg = *cfg;
   if (!c->cfg.seed) c->cfg.seed = 1;
@@ -453,13 +474,14 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
   for (int k = 0; k < stages; ++k) {
     StageRT& s = c->S[k];
     s.k = k;
-    s.dev = c->cfg.n_devices > 0 ? c->cfg.devices[k % c->cfg.n_devices] : cur;
+    s.dev = c->mp() ? cur : (c->cfg.n_devices > 0 ? c->cfg.devices[k % c->cfg.n_devices] : cur);
     if (s.dev < 0 || s.dev >= ndev) return set_err(nullptr, XP_EINVAL, "device id out of range");
     s.plan = c->net.stages[k];
     s.S = c->cfg.schedule == XP_SCHED_GPIPE ? T : (stages - k);
   }
-  // peer access between the devices of neighbouring stages
-  for (int k = 0; k + 1 < stages; ++k) {
+  // peer access between the devices of neighbouring stages (multi-process mode: lazily, by
+  // cudaIpcOpenMemHandle)
+  for (int k = 0; k + 1 < stages && !c->mp(); ++k) {
     int a = c->S[k].dev, b = c->S[k + 1].dev;
     if (a == b) continue;
     int ok = 0;
@@ -476,6 +498,7 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
   };
   for (int k = 0; k < stages; ++k) {
     StageRT& s = c->S[k];
+    if (c->mp() && k != c->cfg.my_stage) continue;
     cudaSetDevice(s.dev);
     if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
     int rr = allocate_stage(cp, s);
@@ -484,6 +507,7 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
     if (rr != XP_OK) return fail_init(rr, "parameter init");
   }
   for (auto& s : c->S) {
+    if (!owned(s)) continue;
     cudaSetDevice(s.dev);
     if (cudaStreamSynchronize(s.stream) != cudaSuccess) return fail_init(XP_ECUDA, "init sync");
   }
@@ -497,6 +521,11 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
   if (c->poisoned) return XP_ESTATE;
   if (M < 0 || (M > 0 && (!x || !y))) return set_err(c, XP_EINVAL, "x/y");
   const bool dev_ptrs = flags & XP_DEVICE_PTRS;
+  if (c->mp()) {
+    const int me = c->cfg.my_stage;
+    if ((me + 1 < c->K && c->S[me + 1].in_slot.empty()) || (me > 0 && c->S[me - 1].gin_slot.empty()))
+      return set_err(c, XP_EINVAL, "multi-process: neighbour stages not attached (xpipe_ipc_import)");
+  }
   if (!dev_ptrs && M > 0)
     for (int64_t i = 0; i < (int64_t)M * c->N; ++i)
       if (y[i] < 0 || y[i] >= c->cfg.classes) return set_err(c, XP_EINVAL, "label out of range");
@@ -510,11 +539,17 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
     StageRT& s0 = c->S[0];
     StageRT& sl = c->S[c->K - 1];
-    cudaSetDevice(s0.dev);
-    XP_CUDA(c, cudaMemcpyAsync(c->x_dev, x, (size_t)M * c->N * per * 4, dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.stream));
-    cudaSetDevice(sl.dev);
-    XP_CUDA(c, cudaMemcpyAsync(c->y_dev, y, (size_t)M * c->N * 4, dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sl.stream));
-    XP_CUDA(c, cudaMemsetAsync(c->loss_dev, 0xff, (size_t)M * c->T * 4, sl.stream));  // NaN = not computed
+    if (owned(s0)) {
+      cudaSetDevice(s0.dev);
+      XP_CUDA(c, cudaMemcpyAsync(c->x_dev, x, (size_t)M * c->N * per * 4,
+                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.stream));
+    }
+    if (owned(sl)) {
+      cudaSetDevice(sl.dev);
+      XP_CUDA(c, cudaMemcpyAsync(c->y_dev, y, (size_t)M * c->N * 4,
+                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sl.stream));
+      XP_CUDA(c, cudaMemsetAsync(c->loss_dev, 0xff, (size_t)M * c->T * 4, sl.stream));  // NaN = not computed
+    }
     c->call_first = c->fed + 1;
     c->fed += (int64_t)M * c->T;
   }
@@ -524,6 +559,7 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
   if (flags & XP_FLUSH) {
     XP_TRY(drive(c, c->fed));
     for (auto& s : c->S) {
+      if (!owned(s)) continue;
       if (!s.done) return set_err(c, XP_ESCHED, "flush did not drain stage " + std::to_string(s.k));
       s.done = false;
       s.pos = 0;
@@ -549,7 +585,7 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
         }
       }
     }
-    if (st->losses && M > 0 && !(flags & XP_ASYNC)) {
+    if (st->losses && M > 0 && !(flags & XP_ASYNC) && owned(c->S[c->K - 1])) {
       cudaSetDevice(c->S[c->K - 1].dev);
       XP_CUDA(c, cudaMemcpy(st->losses, c->loss_dev, (size_t)M * c->T * 4, cudaMemcpyDeviceToHost));
     }
@@ -562,6 +598,7 @@ int xpipe_timer(xpipe_ctx* c, int32_t which, double* ms_out) {
   if (!c || (which != 0 && which != 1)) return set_err(c, XP_EINVAL, "timer args");
   if (c->poisoned) return XP_ESTATE;
   for (auto& s : c->S) {
+    if (!owned(s)) continue;
     cudaSetDevice(s.dev);
     if (!s.tmark[which]) XP_CUDA(c, cudaEventCreate(&s.tmark[which]));
     XP_CUDA(c, cudaEventRecord(s.tmark[which], s.stream));
@@ -570,11 +607,71 @@ int xpipe_timer(xpipe_ctx* c, int32_t which, double* ms_out) {
     XP_TRY(sync_all(c));
     double mx = 0;
     for (auto& s : c->S) {
+      if (!owned(s)) continue;
       float ms = 0;
       XP_CUDA(c, cudaEventElapsedTime(&ms, s.tmark[0], s.tmark[1]));
       mx = std::max(mx, (double)ms);
     }
     if (ms_out) *ms_out = mx;
+  }
+  return XP_OK;
+}
+
+namespace {
+struct IpcBlob {
+  uint32_t magic;
+  int32_t stage, K, S, n;
+  uint64_t in_stride, gin_stride, in_bytes, out_bytes;
+  int32_t has_gin;
+  cudaIpcMemHandle_t in_ring, gin_ring, flags;
+};
+const uint32_t kIpcMagic = 0x58504950u;  // "XPIP"
+}  // namespace
+
+int xpipe_ipc_export(xpipe_ctx* c, void* blob, size_t cap, size_t* len) {
+  if (!c || !blob || !len || !c->mp()) return set_err(c, XP_EINVAL, "ipc_export: not in multi-process mode");
+  if (cap < sizeof(IpcBlob)) return set_err(c, XP_EINVAL, "ipc_export: buffer too small");
+  StageRT& s = c->S[c->cfg.my_stage];
+  IpcBlob b{};
+  b.magic = kIpcMagic; b.stage = s.k; b.K = c->K; b.S = s.S; b.n = c->n;
+  b.in_stride = s.in_stride; b.gin_stride = s.gin_stride;
+  b.in_bytes = s.plan.in_slot_bytes; b.out_bytes = s.plan.out_bytes;
+  cudaSetDevice(s.dev);
+  XP_CUDA(c, cudaIpcGetMemHandle(&b.in_ring, s.in_ring));
+  XP_CUDA(c, cudaIpcGetMemHandle(&b.flags, s.flags));
+  b.has_gin = s.gin_ring != nullptr;
+  if (b.has_gin) XP_CUDA(c, cudaIpcGetMemHandle(&b.gin_ring, s.gin_ring));
+  std::memcpy(blob, &b, sizeof b);
+  *len = sizeof b;
+  return XP_OK;
+}
+
+int xpipe_ipc_import(xpipe_ctx* c, const void* blob, size_t len) {
+  if (!c || !blob || !c->mp() || len != sizeof(IpcBlob)) return set_err(c, XP_EINVAL, "ipc_import: bad blob");
+  IpcBlob b;
+  std::memcpy(&b, blob, sizeof b);
+  const int me = c->cfg.my_stage;
+  if (b.magic != kIpcMagic || b.K != c->K || b.n != c->n || b.stage < 0 || b.stage >= c->K)
+    return set_err(c, XP_EINVAL, "ipc_import: blob of another pipeline");
+  if (b.stage != me - 1 && b.stage != me + 1) return XP_OK;  // not a neighbour: nothing to map
+  StageRT& nb = c->S[b.stage];
+  if (b.S != nb.S) return set_err(c, XP_EINVAL, "ipc_import: ring size mismatch");
+  cudaSetDevice(c->S[me].dev);
+  void* p = nullptr;
+  XP_CUDA(c, cudaIpcOpenMemHandle(&p, b.flags, cudaIpcMemLazyEnablePeerAccess));
+  c->ipc_opened.push_back(p);
+  nb.flags = (uint32_t*)p;
+  if (b.stage == me + 1) {  // we write activations into its input ring
+    XP_CUDA(c, cudaIpcOpenMemHandle(&p, b.in_ring, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    nb.in_slot.resize(nb.S);
+    for (int i = 0; i < nb.S; ++i) nb.in_slot[i] = (uint8_t*)p + i * b.in_stride;
+  } else {                  // we write input gradients into its gradient ring
+    if (!b.has_gin) return set_err(c, XP_EINVAL, "ipc_import: upstream stage without a gradient ring");
+    XP_CUDA(c, cudaIpcOpenMemHandle(&p, b.gin_ring, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    nb.gin_slot.resize(nb.S);
+    for (int i = 0; i < nb.S; ++i) nb.gin_slot[i] = (uint8_t*)p + i * b.gin_stride;
   }
   return XP_OK;
 }
@@ -612,6 +709,7 @@ int xpipe_get_weights(xpipe_ctx* c, int32_t layer, int32_t tensor, int32_t state
   if (n == 0) return XP_OK;
   XP_TRY(sync_all(c));
   StageRT& s = c->S[L.stage];
+  if (!owned(s)) return set_err(c, XP_EINVAL, "layer belongs to a stage of another process");
   const int64_t off = tensor == XP_T_WEIGHT ? L.woff : L.boff;
   const int64_t ng = tensor == XP_T_WEIGHT ? L.nw_gpu : L.nb;
   std::vector<float> buf(ng);
@@ -656,6 +754,7 @@ int xpipe_get_trace(xpipe_ctx* c, int32_t stage, xpipe_trace_rec* dst, size_t ca
   if (c->poisoned) return XP_ESTATE;
   XP_TRY(sync_all(c));
   StageRT& s = c->S[stage];
+  if (!owned(s)) return set_err(c, XP_EINVAL, "stage of another process");
   *n_out = (size_t)s.trace_n;
   if (dst && s.trace_n) {
     cudaSetDevice(s.dev);

@@ -37,7 +37,8 @@ class Config(C.Structure):
                [(n, C.c_int32) for n in ("precision", "schedule", "predict", "s_fwd", "s_bwd", "delta_form",
                                          "moment_init", "n_devices")] + \
                [("devices", C.c_int32 * 8)] + \
-               [(n, C.c_int32) for n in ("transport", "snapshots", "trace", "graphs", "profile", "watchdog_ms")] + \
+               [(n, C.c_int32) for n in ("transport", "snapshots", "trace", "graphs", "profile", "watchdog_ms",
+                                         "multi_process", "my_stage")] + \
                [("init_params", C.POINTER(C.POINTER(C.c_float))),
                 ("init_m", C.POINTER(C.POINTER(C.c_float))),
                 ("init_v", C.POINTER(C.POINTER(C.c_float))),
@@ -77,6 +78,8 @@ def lib():
         L.xpipe_step.argtypes = [vp, vp, vp, i32, C.c_uint32, C.POINTER(Stats)]
         L.xpipe_sync.argtypes = [vp]
         L.xpipe_timer.argtypes = [vp, i32, C.POINTER(C.c_double)]
+        L.xpipe_ipc_export.argtypes = [vp, vp, C.c_size_t, C.POINTER(C.c_size_t)]
+        L.xpipe_ipc_import.argtypes = [vp, vp, C.c_size_t]
         L.xpipe_get_weights.argtypes = [vp, i32, i32, i32, i64, vp, C.c_size_t]
         L.xpipe_get_trace.argtypes = [vp, i32, vp, C.c_size_t, C.POINTER(C.c_size_t)]
         L.xpipe_stage_of_layer.argtypes = [vp, i32]
@@ -129,7 +132,7 @@ class XPipe:
     def __init__(self, layers, stages, micro_batches, mini_batch, lr, betas, eps, in_shape, classes, params=None,
                  precision="fp32", schedule="xpipe", predict="paper", s_fwd=0, s_bwd=0, delta="adam",
                  init_m=None, init_v=None, devices=None, snapshots=False, trace=False, graphs=False, profile=False,
-                 seed=1, watchdog_ms=0, torch_allocator=True):
+                 seed=1, watchdog_ms=0, torch_allocator=True, my_stage=None):
         self.h = None
         L = lib()
         self.layers = list(layers)
@@ -141,7 +144,8 @@ class XPipe:
         cfg = Config(in_c=in_shape[0], in_h=in_shape[1], in_w=in_shape[2], classes=classes, seed=seed,
                      precision=PRECISION[precision], schedule=SCHEDULE[schedule], predict=PREDICT[predict],
                      s_fwd=s_fwd, s_bwd=s_bwd, delta_form=DELTA[delta], snapshots=int(snapshots), trace=int(trace),
-                     graphs=int(graphs), profile=int(profile), watchdog_ms=watchdog_ms)
+                     graphs=int(graphs), profile=int(profile), watchdog_ms=watchdog_ms,
+                     multi_process=int(my_stage is not None), my_stage=my_stage or 0)
         if devices:
             cfg.n_devices = len(devices)
             for i, d in enumerate(devices):
@@ -202,6 +206,16 @@ class XPipe:
         _check(lib().xpipe_step(self.h, _ptr(x), _ptr(y), M, flags, C.byref(st)), self.h)
         self.last_stats = st
         return out
+
+    def ipc_export(self):
+        buf = C.create_string_buffer(4096)
+        n = C.c_size_t()
+        _check(lib().xpipe_ipc_export(self.h, buf, 4096, C.byref(n)), self.h)
+        return buf.raw[:n.value]
+
+    def ipc_import(self, blob):
+        b = C.create_string_buffer(blob, len(blob))
+        _check(lib().xpipe_ipc_import(self.h, b, len(blob)), self.h)
 
     def timer_start(self):
         _check(lib().xpipe_timer(self.h, 0, None), self.h)
@@ -277,3 +291,21 @@ def conv2d_bf16(mode, geo, in0, in1, out, accumulate=False, ws=None, stream=None
     _check(lib().xpipe_conv2d_bf16(mode, g, _ptr(in0), _ptr(in1), _ptr(out), int(accumulate),
                                    _ptr(ws) if ws is not None else None, ws.numel() if ws is not None else 0,
                                    C.c_void_p(stream) if stream else None))
+
+
+def exchange_blobs(blob, group=None):
+    """All-gather one opaque bytes blob per rank over torch.distributed (any backend);
+    returns the list ordered by rank.  Host-side plumbing of the multi-process mode."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, blob, group=group)
+    return out
+
+
+def connect_pipeline(model, group=None):
+    """One-process-per-GPU mode: exchange the CUDA IPC handles of every stage's rings and
+    flags, then attach this process's neighbours (xpipe_ipc_import)."""
+    blobs = exchange_blobs(model.ipc_export(), group)
+    for b in blobs:
+        model.ipc_import(b)
+    return blobs

@@ -117,6 +117,32 @@ def cpu_baseline(workload, seconds=20.0):
                       % (done, n, "bf16 emulation" if prec == "bf16" else "fp32", el)}
 
 
+def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank):
+    """Bubble fraction of one traced call (single-process mode): 1 - sum_k busy_k / (K * span),
+    busy_k = device time of stage k's F/B ops (%globaltimer), next to the uniform-cost ideal
+    (K-1)/(M*T+K-1) of SPEC S:397 / SURVEY A.3."""
+    if mp_mode:
+        return None
+    import synthetic as S
+    import torch
+    from paper_1911_04610_b200 import XPipe
+    g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
+              devices=list(range(args.gpus)), trace=True, watchdog_ms=300000)
+    x, y = S.make_inputs(M * N, shape, classes, 2, kind=kind)
+    g.step(torch.from_numpy(x).cuda(0), torch.from_numpy(y).cuda((K - 1) % args.gpus), M, flush=True)
+    busy, t0s, t1s = [], [], []
+    for k in range(K):
+        tr = g.trace(k, timestamps=True)
+        ops = [r for r in tr if r[1] in (0, 1)]
+        busy.append(sum(r[9] - r[8] for r in ops))
+        t0s.append(min(r[8] for r in ops))
+        t1s.append(max(r[9] for r in ops))
+    g.close()
+    span = max(t1s) - min(t0s)
+    return {"bubble_fraction": 1.0 - sum(busy) / (K * span), "ideal_uniform": (K - 1) / (M * T + K - 1),
+            "traced_minibatches": M, "note": "separate traced call with flush (trace kernels add overhead)"}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed as it stands (the reference arm of this tier)."""
     ws, rank, local = dist_env()
@@ -197,6 +223,7 @@ def main():
     ap.add_argument("--sweep-params", type=int, default=1 << 28)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="enqueue every kernel from the host (no CUDA graphs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -233,7 +260,7 @@ def main():
         connect_pipeline(g, dist.new_group(backend="gloo"))
     else:
         g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
-                  devices=list(range(args.gpus)), profile=True, watchdog_ms=300000)
+                  devices=list(range(args.gpus)), profile=True, watchdog_ms=300000, graphs=not args.no_graphs)
     x, y = S.make_inputs(M * N, shape, classes, 1, kind=kind)
     last_dev = dev if mp_mode else (K - 1) % args.gpus
     xd = torch.from_numpy(x).cuda(dev)
@@ -248,12 +275,14 @@ def main():
     barrier()
     prof = {}
     launches = 0
+    replays = 0
     with Clocks(dev) as ck:
         g.timer_start()
         for _ in range(args.steps):
             g.step(xd, yd, M, losses=False)
             st = g.last_stats
             launches += st.kernel_launches
+            replays += st.graph_replays
             for name, d in st.profile().items():
                 q = prof.setdefault(name, {"ms": 0.0, "launches": 0, "work": 0.0})
                 q["ms"] += d["ms"]; q["launches"] += d["launches"]; q["work"] += d["work"]
@@ -318,7 +347,11 @@ def main():
                   "achieved": (v["work"] / (v["ms"] * 1e-3) / (1e9 if k == "sweep" else 1e12)) if v["ms"] else 0,
                   "unit": "GB/s" if k == "sweep" else "TFLOP/s", "launches": v["launches"]}
               for k, v in prof.items()}
-    result = dict(ms=ms, clocks=clocks, roof=roof, shares=shares, launches=launches)
+    result = dict(ms=ms, clocks=clocks, roof=roof, shares=shares, launches=launches, replays=replays)
+    try:
+        bubble = measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank)
+    except Exception as e:  # the bubble is a report, not the metric
+        bubble = {"error": repr(e)[:200]}
     cpu = None if args.no_cpu_baseline else cpu_baseline(args.workload)
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": result["ms"] / args.steps, "higher_is_better": True,
@@ -331,8 +364,9 @@ def main():
                        "global_batch": N, "stages": K, "micro_batches": T, "minibatches_per_step": M,
                        "parallelism": "pipeline K=%d (XPipe)" % K,
                        "l2": "working set > L2: optimizer state 16 B/param x 14.7M params = 235 MB (126 MB L2)"},
-            "e2e": e2e, "gpu_launches": result["launches"], "clocks": result["clocks"],
-            "roofline": result["roof"], "kernel_shares": result["shares"], "cpu_baseline": cpu}
+            "e2e": e2e, "gpu_launches": result["launches"], "graph_replays": result.get("replays"),
+            "clocks": result["clocks"],
+            "roofline": result["roof"], "kernel_shares": result["shares"], "bubble": bubble, "cpu_baseline": cpu}
     print(json.dumps(line), flush=True)
     return 0
 

@@ -134,7 +134,8 @@ typedef struct {
   double prof_ms[XP_PROF_N];         /* summed device time per kernel class (cfg.profile) */
   int64_t prof_launches[XP_PROF_N];
   double prof_work[XP_PROF_N];       /* algorithmic bytes (sweep) or flops (GEMM classes) */
-  int64_t kernel_launches;           /* kernels enqueued by this call */
+  int64_t kernel_launches;           /* kernels enqueued by this call (directly or in a graph) */
+  int64_t graph_replays;             /* 1 if this call replayed a captured CUDA graph */
   float* losses;                     /* optional caller buffer of M*T per-micro-batch mean losses */
 } xpipe_stats;
 

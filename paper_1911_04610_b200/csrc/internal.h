@@ -47,6 +47,7 @@ void host_scalars(int64_t k, float lr, float b1, float b2, float eps, SweepScala
 cudaError_t launch_trace_begin(DevState* ds, TraceRec* rec, int stage, int op, int t, int j, int s, int bw,
                                cudaStream_t st);
 cudaError_t launch_trace_end(TraceRec* rec, cudaStream_t st);
+cudaError_t launch_rebase_flags(uint32_t* flags, int n, uint32_t delta, cudaStream_t st);
 cudaError_t launch_copy_f32(const float* src, float* dst, int64_t n, cudaStream_t st);
 cudaError_t launch_fill_uniform(float* dst, int64_t n, float bound, uint64_t seed, uint64_t stream_id,
                                 cudaStream_t st);

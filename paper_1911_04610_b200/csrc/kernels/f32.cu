@@ -34,6 +34,11 @@ __global__ void trace_begin_kernel(DevState* ds, TraceRec* rec, int stage, int o
 
 __global__ void trace_end_kernel(TraceRec* rec) { rec->t1_ns = globaltimer(); }
 
+// ring flags hold micro-batch indices relative to a base; rebasing subtracts delta (mod 2^32)
+__global__ void rebase_flags_kernel(uint32_t* f, int n, uint32_t delta) {
+  if (threadIdx.x < n) f[threadIdx.x] -= delta;
+}
+
 __global__ void copy_kernel(const float* __restrict__ s, float* __restrict__ d, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d[i] = s[i];
@@ -186,6 +191,11 @@ int grid_for(int64_t n, int threads = 256) {
 cudaError_t launch_trace_begin(DevState* ds, TraceRec* rec, int stage, int op, int t, int j, int s, int bw,
                                cudaStream_t st) {
   trace_begin_kernel<<<1, 1, 0, st>>>(ds, rec, stage, op, t, j, s, bw);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rebase_flags(uint32_t* flags, int n, uint32_t delta, cudaStream_t st) {
+  rebase_flags_kernel<<<1, 32, 0, st>>>(flags, n, delta);
   return cudaGetLastError();
 }
 

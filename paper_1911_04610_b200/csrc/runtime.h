@@ -1,6 +1,7 @@
 // runtime.h -- host-side context of the XPipe runtime (shared by xpipe.cu, blocks.cu, plan.cu).
 #pragma once
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -66,6 +67,7 @@ struct StageRT {
   int64_t trace_cap = 0, trace_n = 0;
   std::vector<Snapshot> snaps;
   std::vector<float*> snap_pool;         // pinned buffers reserved before enqueue
+  void* diag = nullptr;                  // pinned scratch for watchdog diagnostics
   // profiling (cfg.profile): event pool and the (class, work) of each recorded pair
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t tmark[2] = {nullptr, nullptr};
@@ -99,6 +101,19 @@ struct xpipe_ctx {
   int64_t base = 0;          // micro-batch offset of the current epoch
   int64_t call_first = 0;    // first micro-batch (absolute) of the current call's input buffer
   int64_t kernels = 0;
+  int64_t flag_base = 0;     // flag values are micro-batch indices minus flag_base
+  // CUDA graphs of steady-state steps (cfg.graphs): signature -> executable + host-state deltas
+  struct GraphRec {
+    cudaGraphExec_t exec = nullptr;
+    int seen = 0;
+    int64_t kernels = 0;
+    std::vector<int64_t> dpos;
+    std::vector<int> dver, dfver, dbver;
+    std::vector<std::vector<int>> prof_cls;
+    std::vector<std::vector<double>> prof_work;
+  };
+  std::map<std::string, GraphRec> graphs;
+  int64_t graph_replays = 0;
   std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)
 };
 

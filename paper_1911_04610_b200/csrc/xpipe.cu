@@ -97,11 +97,15 @@ void* dmalloc_shared(xpipe_ctx* c, size_t bytes, int dev) {
 }
 
 void free_all(xpipe_ctx* c) {
+  for (auto& kv : c->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  c->graphs.clear();
   for (auto& s : c->S) {
     for (auto& sn : s.snaps) if (sn.pinned) cudaFreeHost(sn.pinned);
     s.snaps.clear();
     for (auto p : s.snap_pool) cudaFreeHost(p);
     s.snap_pool.clear();
+    if (s.diag) { cudaFreeHost(s.diag); s.diag = nullptr; }
     for (auto e : s.ev_pool) cudaEventDestroy(e);
     s.ev_pool.clear();
     for (auto& e : s.tmark) if (e) { cudaEventDestroy(e); e = nullptr; }
@@ -146,13 +150,14 @@ int prof_begin(xpipe_ctx* c, StageRT& s) {
     XP_CUDA(c, cudaEventCreate(&e));
     s.ev_pool.push_back(e);
   }
-  XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used], s.stream));
+  // external record: inside a stream capture this becomes an event-record node of the graph
+  XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used], s.stream, cudaEventRecordExternal));
   return XP_OK;
 }
 
 int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work) {
   if (!c->cfg.profile) return XP_OK;
-  XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used + 1], s.stream));
+  XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used + 1], s.stream, cudaEventRecordExternal));
   s.ev_used += 2;
   s.prof_cls.push_back(cls);
   s.prof_work.push_back(work);
@@ -162,15 +167,28 @@ int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work) {
 
 namespace {
 
+// Flag values are micro-batch indices relative to c->flag_base (rebased between calls when
+// CUDA graphs are on); GEQ compares the wraparound-safe signed difference, so rebased values
+// may go negative.
+bool verbose() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("XPIPE_VERBOSE"); v = (e && *e && *e != '0') ? 1 : 0; }
+  return v == 1;
+}
+
 int flag_wait(xpipe_ctx* c, StageRT& s, uint32_t* flag, int64_t value) {
-  if (value <= 0) return XP_OK;
-  int r = p_wait32(s.stream, (unsigned long long)(uintptr_t)flag, (uint32_t)value, 0 /*GEQ*/);
+  if (verbose()) fprintf(stderr, "[xpipe] stage %d wait %p >= %lld%s\n", s.k, (void*)flag, (long long)value,
+                         value <= 0 ? " (skip)" : "");
+  if (value <= 0) return XP_OK;  // absolute: that message never existed
+  int r = p_wait32(s.stream, (unsigned long long)(uintptr_t)flag, (uint32_t)(value - c->flag_base), 0 /*GEQ*/);
   if (r != 0) return set_err(c, XP_ECOMM, "cuStreamWaitValue32 failed: " + std::to_string(r));
   return XP_OK;
 }
 
 int flag_write(xpipe_ctx* c, StageRT& s, uint32_t* flag, int64_t value) {
-  int r = p_write32(s.stream, (unsigned long long)(uintptr_t)flag, (uint32_t)value, 0 /*DEFAULT: with barrier*/);
+  if (verbose()) fprintf(stderr, "[xpipe] stage %d write %p = %lld\n", s.k, (void*)flag, (long long)value);
+  int r = p_write32(s.stream, (unsigned long long)(uintptr_t)flag, (uint32_t)(value - c->flag_base),
+                    0 /*DEFAULT: with barrier*/);
   if (r != 0) return set_err(c, XP_ECOMM, "cuStreamWriteValue32 failed: " + std::to_string(r));
   return XP_OK;
 }
@@ -354,6 +372,8 @@ int drive(xpipe_ctx* c, int64_t total) {
         continue;
       }
       if (u > c->fed) break;  // needs a micro-batch not fed yet
+      if (verbose()) fprintf(stderr, "[xpipe] stage %d pos %lld: %c(%lld) slot %lld\n", k, (long long)s.pos,
+                             op == 0 ? 'F' : 'B', (long long)u, (long long)((u - 1) % s.S));
       XP_TRY(op == 0 ? enqueue_forward(c, k, u) : enqueue_backward(c, k, u));
       ++s.pos;
     }
@@ -370,8 +390,11 @@ std::string pipeline_state(xpipe_ctx* c) {
     cudaSetDevice(s.dev);
     cudaStream_t side;
     if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) return out + " (no side stream)";
-    uint32_t f[4] = {0, 0, 0, 0};
-    TraceRec last{};
+    uint32_t* f = (uint32_t*)s.diag;  // pinned, allocated at init: the copy never blocks the host
+    TraceRec& last = *(TraceRec*)((char*)s.diag + 64);
+    if (!f) return out + " (no diag buffer)";
+    f[0] = f[1] = f[2] = f[3] = 0xFFFFFFFFu;
+    last = TraceRec{};
     cudaMemcpyAsync(f, s.flags, 16, cudaMemcpyDeviceToHost, side);
     if (c->cfg.trace && s.trace_n) cudaMemcpyAsync(&last, s.trace_dev + s.trace_n - 1, sizeof(TraceRec), cudaMemcpyDeviceToHost, side);
     cudaEvent_t e;
@@ -388,6 +411,7 @@ std::string pipeline_state(xpipe_ctx* c) {
              " trace_n=%lld last={op=%d t=%d j=%d t1=%llu}", s.k, (long long)s.pos, s.host_ver, ok ? "" : "(unread)",
              f[0], f[1], f[2], f[3], (long long)s.trace_n, last.op, last.t, last.j, (unsigned long long)last.t1_ns);
     out += buf;
+    out += " base=" + std::to_string(c->flag_base);
   }
   return out;
 }
@@ -408,6 +432,108 @@ int sync_all(xpipe_ctx* c) {
       std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
   }
+  return XP_OK;
+}
+
+// ---- CUDA graphs of steady-state steps -------------------------------------------------------
+// In steady state (no flush, every in-flight wait already past the warm-up) a call's enqueue is
+// a pure function of: M, the call buffers, and per stage (pos - 2*(fed - base)), (fed - base)
+// mod S (ring-slot phase), and the parities of the version counters (W_hat_f buffer choice);
+// the ring flags are rebased to fed so their values repeat too.
+bool graph_eligible(const xpipe_ctx* c, uint32_t flags, int64_t M, int64_t fed_before) {
+  if (!c->cfg.graphs || c->mp() || c->cfg.trace || c->cfg.snapshots) return false;
+  if ((flags & XP_FLUSH) || M <= 0 || fed_before - c->base < 2 * c->K) return false;
+  for (const auto& s : c->S)
+    if (s.dev != c->S[0].dev) return false;  // single-device capture only
+  return true;
+}
+
+std::string graph_signature(const xpipe_ctx* c, int64_t M, int64_t fed_before) {
+  std::string sig = std::to_string(M) + ":" + std::to_string((uintptr_t)c->x_dev) + ":" +
+                    std::to_string((uintptr_t)c->y_dev) + ":" + std::to_string((uintptr_t)c->loss_dev);
+  const int64_t f = fed_before - c->base;
+  for (const auto& s : c->S)
+    sig += "|" + std::to_string(s.pos - 2 * f) + "," + std::to_string(f % s.S) + "," + std::to_string(s.host_ver & 1) +
+           "," + std::to_string(s.host_fver & 1) + "," + std::to_string((int)s.done);
+  return sig;
+}
+
+int rebase_flags(xpipe_ctx* c, int64_t new_base) {
+  const int64_t delta = new_base - c->flag_base;
+  if (delta == 0) return XP_OK;
+  for (auto& s : c->S) {
+    cudaSetDevice(s.dev);
+    XP_TRY(check_launch(c, launch_rebase_flags(s.flags, 4, (uint32_t)delta, s.stream), "rebase"));
+  }
+  for (auto& s : c->S) { cudaSetDevice(s.dev); XP_CUDA(c, cudaStreamSynchronize(s.stream)); }
+  c->flag_base = new_base;
+  return XP_OK;
+}
+
+int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
+  XP_TRY(rebase_flags(c, fed_before));
+  const std::string sig = graph_signature(c, M, fed_before);
+  xpipe_ctx::GraphRec& g = c->graphs[sig];
+  StageRT& o = c->S[0];
+  cudaSetDevice(o.dev);
+  if (g.exec) {
+    XP_CUDA(c, cudaGraphLaunch(g.exec, o.stream));
+    for (size_t k = 0; k < c->S.size(); ++k) {
+      StageRT& s = c->S[k];
+      const int v0 = s.host_ver;
+      s.pos += g.dpos[k];
+      s.host_ver += g.dver[k];
+      s.host_fver = v0 + g.dfver[k];
+      s.host_bver = v0 + g.dbver[k];
+    }
+    c->kernels += g.kernels;
+    c->graph_replays++;
+    for (size_t k = 0; k < c->S.size(); ++k) {  // the graph re-records the same profiling events
+      c->S[k].prof_cls = g.prof_cls[k];
+      c->S[k].prof_work = g.prof_work[k];
+      c->S[k].ev_used = 2 * g.prof_cls[k].size();
+    }
+    return XP_OK;
+  }
+  if (g.seen++ == 0) return drive(c, -1);  // first sighting: plain enqueue
+  // second sighting: capture this call's enqueue, then launch it
+  std::vector<int64_t> pos0;
+  std::vector<int> ver0;
+  for (auto& s : c->S) { pos0.push_back(s.pos); ver0.push_back(s.host_ver); }
+  const int64_t k0 = c->kernels;
+  static thread_local std::vector<cudaEvent_t> evs;
+  while (evs.size() < c->S.size() + 1) {
+    cudaEvent_t e;
+    XP_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    evs.push_back(e);
+  }
+  XP_CUDA(c, cudaStreamBeginCapture(o.stream, cudaStreamCaptureModeThreadLocal));
+  XP_CUDA(c, cudaEventRecord(evs[0], o.stream));
+  for (size_t k = 1; k < c->S.size(); ++k) XP_CUDA(c, cudaStreamWaitEvent(c->S[k].stream, evs[0], 0));
+  int r = drive(c, -1);
+  for (size_t k = 1; k < c->S.size() && r == XP_OK; ++k) {
+    if (cudaEventRecord(evs[k], c->S[k].stream) != cudaSuccess || cudaStreamWaitEvent(o.stream, evs[k], 0) != cudaSuccess)
+      r = set_err(c, XP_ECUDA, "graph join");
+  }
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(o.stream, &graph);
+  if (r != XP_OK) return r;
+  if (e != cudaSuccess) return set_err(c, XP_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return set_err(c, XP_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  g.kernels = c->kernels - k0;
+  g.dpos.clear(); g.dver.clear(); g.dfver.clear(); g.dbver.clear();
+  g.prof_cls.clear(); g.prof_work.clear();
+  for (auto& s : c->S) { g.prof_cls.push_back(s.prof_cls); g.prof_work.push_back(s.prof_work); }
+  for (size_t k = 0; k < c->S.size(); ++k) {
+    StageRT& s = c->S[k];
+    g.dpos.push_back(s.pos - pos0[k]);
+    g.dver.push_back(s.host_ver - ver0[k]);
+    g.dfver.push_back(s.host_fver - ver0[k]);
+    g.dbver.push_back(s.host_bver - ver0[k]);
+  }
+  XP_CUDA(c, cudaGraphLaunch(g.exec, o.stream));
   return XP_OK;
 }
 
@@ -501,6 +627,7 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
     if (c->mp() && k != c->cfg.my_stage) continue;
     cudaSetDevice(s.dev);
     if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
+    if (cudaMallocHost(&s.diag, 256) != cudaSuccess) return fail_init(XP_ENOMEM, "diag buffer");
     int rr = allocate_stage(cp, s);
     if (rr != XP_OK) return fail_init(rr, "stage allocation");
     rr = init_stage_params(cp, s, layers);
@@ -531,7 +658,7 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
       if (y[i] < 0 || y[i] >= c->cfg.classes) return set_err(c, XP_EINVAL, "label out of range");
   int cur = 0;
   cudaGetDevice(&cur);
-  const int64_t k0 = c->kernels;
+  const int64_t k0 = c->kernels, g0 = c->graph_replays;
   // previous call's work must be done before its call buffers are overwritten
   XP_TRY(sync_all(c));
   if (M > 0) {
@@ -555,7 +682,9 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
   }
   for (auto& s : c->S) { s.ev_used = 0; s.prof_cls.clear(); s.prof_work.clear(); }
   XP_TRY(reserve_for_call(c, M));
-  XP_TRY(drive(c, -1));
+  const int64_t fed_before = c->fed - (int64_t)M * c->T;
+  if (graph_eligible(c, flags, M, fed_before)) XP_TRY(drive_graph(c, M, fed_before));
+  else XP_TRY(drive(c, -1));
   if (flags & XP_FLUSH) {
     XP_TRY(drive(c, c->fed));
     for (auto& s : c->S) {
@@ -571,6 +700,7 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
   if (rr != XP_OK) return rr;
   if (st) {
     st->kernel_launches = c->kernels - k0;
+    st->graph_replays = c->graph_replays - g0;
     st->span_ms = 0;
     for (int q = 0; q < XP_PROF_N; ++q) { st->prof_ms[q] = 0; st->prof_launches[q] = 0; st->prof_work[q] = 0; }
     if (c->cfg.profile && !(flags & XP_ASYNC)) {

@@ -55,7 +55,8 @@ PROF_CLASSES = ("sweep", "conv_fprop", "conv_dgrad", "conv_wgrad")
 
 class Stats(C.Structure):
     _fields_ = [("span_ms", C.c_double), ("prof_ms", C.c_double * 4), ("prof_launches", C.c_int64 * 4),
-                ("prof_work", C.c_double * 4), ("kernel_launches", C.c_int64), ("losses", C.POINTER(C.c_float))]
+                ("prof_work", C.c_double * 4), ("kernel_launches", C.c_int64), ("graph_replays", C.c_int64),
+                ("losses", C.POINTER(C.c_float))]
 
     def profile(self):
         return {n: dict(ms=self.prof_ms[i], launches=self.prof_launches[i], work=self.prof_work[i])

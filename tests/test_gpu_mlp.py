@@ -20,7 +20,7 @@ def max_rel(a, b):
 
 
 def run_pair(oracle_mod, K, T, N, M, lr=1e-4, calls=None, schedule="xpipe", predict="paper", s_fwd=0, s_bwd=0,
-             layers=None, in_shape=(784, 1, 1), seed=1):
+             layers=None, in_shape=(784, 1, 1), seed=1, graphs=False):
     from paper_1911_04610_b200 import XPipe
     L = layers or S.mlp()
     P = S.make_params(L, seed)
@@ -28,16 +28,18 @@ def run_pair(oracle_mod, K, T, N, M, lr=1e-4, calls=None, schedule="xpipe", pred
     o = oracle_mod.Oracle(L, K, T, N, lr, (0.9, 0.999), 1e-8, in_shape, 10, P, mode="fp32", schedule=schedule,
                           predict=predict, s_fwd=s_fwd, s_bwd=s_bwd, snapshots=True)
     g = XPipe(L, K, T, N, lr, (0.9, 0.999), 1e-8, in_shape, 10, params=P, precision="fp32", schedule=schedule,
-              predict=predict, s_fwd=s_fwd, s_bwd=s_bwd, snapshots=True, trace=True,
-              watchdog_ms=20000)
+              predict=predict, s_fwd=s_fwd, s_bwd=s_bwd, snapshots=not graphs, trace=not graphs,
+              watchdog_ms=20000, graphs=graphs)
     calls = calls or [M]
     off = 0
     lo, lg = [], []
+    g.replays = 0
     for i, m in enumerate(calls):
         sl = slice(off * N, (off + m) * N)
         fl = i == len(calls) - 1
         lo.append(o.step(x[sl], y[sl], m, flush=fl))
         lg.append(g.step(x[sl], y[sl], m, flush=fl))
+        g.replays += g.last_stats.graph_replays
         off += m
     return o, g, L, np.concatenate(lo), np.concatenate(lg)
 
@@ -102,3 +104,16 @@ def test_determinism_two_runs(oracle_mod):
     _, g1, L, _, _ = run_pair(oracle_mod, 2, 4, 32, 3)
     _, g2, _, _, _ = run_pair(oracle_mod, 2, 4, 32, 3)
     assert np.array_equal(g1.params_flat(), g2.params_flat())
+
+
+@pytest.mark.parametrize("K,T", [(2, 4), (4, 2), (1, 4)])
+def test_cuda_graph_replay_bit_exact(oracle_mod, K, T):
+    """Steady-state steps captured as CUDA graphs and replayed (flags rebased per call) give
+    the same weights, bit for bit, as the oracle's replay of the same calls."""
+    calls = [2] * 8 + [2]
+    o, g, L, lo, lg = run_pair(oracle_mod, K, T, 16, sum(calls), calls=calls, graphs=True)
+    assert g.replays >= 4, g.replays
+    for k in range(K):
+        assert g.version(k) == o.version(k) == sum(calls)
+    assert np.array_equal(g.params_flat(), o.params_flat().astype(np.float32))
+    np.testing.assert_allclose(lg[np.isfinite(lg)], lo[np.isfinite(lg)], rtol=1e-5)

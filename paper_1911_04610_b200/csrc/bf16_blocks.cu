@@ -59,7 +59,8 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
       XP_TRY(check_launch(c, launch_bn_stats(mid, M, O.smid.c, N.d.bn_eps, W + N.woff, W + N.boff, s.bnws,
                                              s.stats[o][slot], s.stream), "bn_stats"));
       const PoolGeo p = pool_geo(c, O.lpool);
-      return check_launch(c, launch_bn_apply(mid, s.stats[o][slot], (bf16*)y, n, O.smid.h, O.smid.w, O.smid.c,
+      uint8_t* pidx = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
+      return check_launch(c, launch_bn_apply(mid, s.stats[o][slot], (bf16*)y, pidx, n, O.smid.h, O.smid.w, O.smid.c,
                                              O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0,
                                              O.relu, s.stream), "bn_apply");
     }
@@ -103,7 +104,9 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       const LayerInfo& N = c->net.layers[O.lbn];
       const PoolGeo p = pool_geo(c, O.lpool);
       bf16* dmid = (bf16*)s.gmid;
-      XP_TRY(check_launch(c, launch_bn_backward((const bf16*)s.mid[o][slot], (const bf16*)dy, s.stats[o][slot],
+      XP_TRY(check_launch(c, launch_bn_backward((const bf16*)s.mid[o][slot], (const bf16*)dy,
+                                                (const bf16*)s.act[O.out][slot],
+                                                O.lpool >= 0 ? s.pidx[o][slot] : nullptr, s.stats[o][slot],
                                                 W + N.woff, n, O.smid.h, O.smid.w, O.smid.c, O.sout.h, O.sout.w, p.kh,
                                                 p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws,
                                                 s.g + N.woff, s.g + N.boff, accumulate_g, dmid, s.stream),

@@ -61,6 +61,7 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
   }
   s.mid.assign(p.ops.size(), {});
   s.stats.assign(p.ops.size(), {});
+  s.pidx.assign(p.ops.size(), {});
   for (size_t o = 0; o < p.ops.size(); ++o) {
     const Op& O = p.ops[o];
     if (O.kind != OP_CONV) continue;
@@ -68,6 +69,10 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
     s.stats[o].resize(s.S);
     for (auto& q : s.mid[o]) if (!(q = A((size_t)n * O.smid.size() * 2))) return set_err(c, XP_ENOMEM, "stash");
     for (auto& q : s.stats[o]) if (!(q = (float*)A((size_t)O.smid.c * 4 * 4))) return set_err(c, XP_ENOMEM, "stash");
+    if (O.lpool >= 0) {
+      s.pidx[o].resize(s.S);
+      for (auto& q : s.pidx[o]) if (!(q = (uint8_t*)A((size_t)n * O.sout.size()))) return set_err(c, XP_ENOMEM, "stash");
+    }
   }
   if (s.k == c->K - 1) {
     s.dz.resize(s.S);

@@ -99,34 +99,48 @@ __global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C
 }
 
 // merge the chunk partials in chunk order -> stats[0..C) mean, [C..2C) rstd, [2C..3C) gamma_f,
-// [3C..4C) beta_f (the forward's affine parameters, kept for the backward recompute)
+// [3C..4C) beta_f (the forward's affine parameters).  One warp per channel: lane l merges
+// chunks l, l+32, ... in order, then the 32 lane results merge in a fixed butterfly order.
+__device__ __forceinline__ void chan_merge(float& na, float& mean, float& m2, float nb, float mb, float m2b) {
+  if (nb == 0.f) return;
+  if (na == 0.f) { na = nb; mean = mb; m2 = m2b; return; }
+  const float nab = na + nb;
+  const float d = mb - mean;
+  mean += d * (nb / nab);
+  m2 += m2b + d * d * (na * nb / nab);
+  na = nab;
+}
+
 __global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
                                       const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
                                       float* __restrict__ stats) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= C) return;
   float na = 0.f, mean = 0.f, m2 = 0.f;
-  for (int k = 0; k < chunks; ++k) {
-    const float nb = (float)min(RC, M - k * RC);
-    const float mb = part[(size_t)k * 2 * C + c], m2b = part[(size_t)k * 2 * C + C + c];
-    const float nab = na + nb;
-    const float d = mb - mean;
-    mean += d * (nb / nab);
-    m2 += m2b + d * d * (na * nb / nab);
-    na = nab;
+  for (int k = lane; k < chunks; k += 32)
+    chan_merge(na, mean, m2, (float)min(RC, M - k * RC), part[(size_t)k * 2 * C + c], part[(size_t)k * 2 * C + C + c]);
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float nb = __shfl_xor_sync(0xffffffffu, na, off), mb = __shfl_xor_sync(0xffffffffu, mean, off),
+                m2b = __shfl_xor_sync(0xffffffffu, m2, off);
+    // fixed order: the lower lane of each pair absorbs the upper one; both end with the same value
+    if ((lane & off) == 0) chan_merge(na, mean, m2, nb, mb, m2b);
+    else { float a = nb, b = mb, q = m2b; chan_merge(a, b, q, na, mean, m2); na = a; mean = b; m2 = q; }
   }
-  const float var = m2 / na;
-  stats[c] = mean;
-  stats[C + c] = 1.f / sqrtf(var + eps);
-  stats[2 * C + c] = __bfloat162float(gamma[c]);
-  stats[3 * C + c] = __bfloat162float(beta[c]);
+  if (lane == 0) {
+    stats[c] = mean;
+    stats[C + c] = 1.f / sqrtf(m2 / na + eps);
+    stats[2 * C + c] = __bfloat162float(gamma[c]);
+    stats[3 * C + c] = __bfloat162float(beta[c]);
+  }
 }
 
-// ---- BN-apply + ReLU (+ pool) ------------------------------------------------------------
-// y[n][p][q][c] = max over the pool window (first max, row-major) of bn_act(x[n][h][w][c])
+// ---- BN-apply [+ ReLU] [+ pool] ----------------------------------------------------------
+// y[n][p][q][c] = first max over the pool window (row-major scan) of bn_act(x[n][h][w][c]);
+// pidx[n][p][q][c] = the winner's position in the window (the backward routes through it)
 __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restrict__ st, bf16* __restrict__ y,
-                                int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph,
-                                int pw, int pool, int relu) {
+                                uint8_t* __restrict__ pidx, int n, int H, int W, int C, int P, int Q, int kh, int kw,
+                                int sh, int sw, int ph, int pw, int pool, int relu) {
   const int G = C / 8;
   const int64_t total = (int64_t)n * P * Q * G;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -138,10 +152,11 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
     const int s = (int)(r / P);
     const int c0 = g * 8;
     float mean[8], rstd[8], ga[8], be[8], best[8];
+    int arg[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       mean[e] = st[c0 + e]; rstd[e] = st[C + c0 + e]; ga[e] = st[2 * C + c0 + e]; be[e] = st[3 * C + c0 + e];
-      best[e] = 0.f;
+      best[e] = 0.f; arg[e] = 0;
     }
     if (!pool) {
       const uint4 u = *reinterpret_cast<const uint4*>(x + (((int64_t)s * H + p) * W + q) * C + c0);
@@ -159,10 +174,14 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const float t = bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e], relu);
-            if (first || t > best[e]) best[e] = t;
+            if (first || t > best[e]) { best[e] = t; arg[e] = a * kw + b; }
           }
           first = false;
         }
+      uint32_t w2[2] = {0u, 0u};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) w2[e >> 2] |= (uint32_t)arg[e] << (8 * (e & 3));
+      *reinterpret_cast<uint2*>(pidx + (((int64_t)s * P + p) * Q + q) * C + c0) = make_uint2(w2[0], w2[1]);
     }
     uint32_t w4[4];
 #pragma unroll
@@ -174,126 +193,181 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
   }
 }
 
-// gradient reaching BN output element (s,h,w,c): max-pool routing (first max of every window
-// containing it) and the ReLU mask, recomputing a from the stash (x, stats)
+// The gradient reaching 8 channels of BN-output element (s,h,w,c0..c0+7), from the stash of
+// the forward only (no recomputation): max-pool routing through the stored winner index of
+// every window containing (h,w), masked by ReLU on the stored output (the window max is the
+// winner's activation, so `y > 0` is exactly the ReLU mask of the winner).
 struct BwdGeo {
   int H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool, relu;
 };
 
-__device__ __forceinline__ float routed_dy(const bf16* __restrict__ x, const bf16* __restrict__ dout,
-                                           const BwdGeo& G, int s, int h, int w, int c, float mean, float rstd, float ga,
-                                           float be) {
-  const float a = bn_act(__bfloat162float(x[(((int64_t)s * G.H + h) * G.W + w) * G.C + c]), mean, rstd, ga, be, G.relu);
-  if (G.relu && !(a > 0.f)) return 0.f;
-  if (!G.pool) return __bfloat162float(dout[(((int64_t)s * G.H + h) * G.W + w) * G.C + c]);
-  // windows (p,q) with p*sh - ph <= h < p*sh - ph + kh
+__device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const bf16* __restrict__ y,
+                                           const uint8_t* __restrict__ pidx, const BwdGeo& G, int s, int h, int w,
+                                           int c0, float (&dy)[8]) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) dy[e] = 0.f;
+  if (!G.pool) {
+    const int64_t o = (((int64_t)s * G.H + h) * G.W + w) * G.C + c0;
+    const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
+    const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
+    const bf16* d = reinterpret_cast<const bf16*>(&ud);
+    const bf16* yy = reinterpret_cast<const bf16*>(&uy);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) dy[e] = (G.relu && !(__bfloat162float(yy[e]) > 0.f)) ? 0.f : __bfloat162float(d[e]);
+    return;
+  }
   const int plo = max(0, (h + G.ph - G.kh + G.sh) / G.sh), phi = min(G.P - 1, (h + G.ph) / G.sh);
   const int qlo = max(0, (w + G.pw - G.kw + G.sw) / G.sw), qhi = min(G.Q - 1, (w + G.pw) / G.sw);
-  float acc = 0.f;
-  int hits = 0;
+  int hits[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int p = plo; p <= phi; ++p)
     for (int q = qlo; q <= qhi; ++q) {
-      // first max of window (p,q)
-      float best = 0.f;
-      int bh = -1, bw = -1;
-      for (int a2 = 0; a2 < G.kh; ++a2)
-        for (int b2 = 0; b2 < G.kw; ++b2) {
-          const int hh = p * G.sh - G.ph + a2, ww = q * G.sw - G.pw + b2;
-          if (hh < 0 || hh >= G.H || ww < 0 || ww >= G.W) continue;
-          const float t = bn_act(__bfloat162float(x[(((int64_t)s * G.H + hh) * G.W + ww) * G.C + c]), mean, rstd, ga, be, G.relu);
-          if (bh < 0 || t > best) { best = t; bh = hh; bw = ww; }
-        }
-      if (bh == h && bw == w) {
-        const float d = __bfloat162float(dout[(((int64_t)s * G.P + p) * G.Q + q) * G.C + c]);
-        acc = hits ? __fadd_rn(acc, d) : d;
-        ++hits;
+      const int a = h - (p * G.sh - G.ph), b = w - (q * G.sw - G.pw);
+      if (a < 0 || a >= G.kh || b < 0 || b >= G.kw) continue;
+      const int pos = a * G.kw + b;
+      const int64_t o = (((int64_t)s * G.P + p) * G.Q + q) * G.C + c0;
+      const uint2 ui = *reinterpret_cast<const uint2*>(pidx + o);
+      const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
+      const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
+      const bf16* d = reinterpret_cast<const bf16*>(&ud);
+      const bf16* yy = reinterpret_cast<const bf16*>(&uy);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int win = (int)(((e < 4 ? ui.x : ui.y) >> (8 * (e & 3))) & 0xFF);
+        if (win != pos) continue;
+        if (G.relu && !(__bfloat162float(yy[e]) > 0.f)) continue;
+        const float g = __bfloat162float(d[e]);
+        dy[e] = hits[e] ? __fadd_rn(dy[e], g) : g;
+        ++hits[e];
       }
     }
-  return hits > 1 ? q16(acc) : acc;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    if (hits[e] > 1) dy[e] = q16(dy[e]);
 }
 
-// per chunk of rows, per channel: sum dy, sum dy*xhat (fixed order: row lanes then merge)
+// per chunk of RC rows: sum dy and sum dy*xhat per channel (8 channels per thread, row lanes
+// merged in fixed order) -> part[chunk][2][C]
 __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                     const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
                                      const float* __restrict__ st, BwdGeo G, int M, int RC, float* __restrict__ part) {
   extern __shared__ float sh[];
-  const int C = G.C;
+  const int C = G.C, NG = C / 8, RL = blockDim.x / NG;
+  const int g = threadIdx.x % NG, rl = threadIdx.x / NG;
+  const int c0 = g * 8;
   const int r0 = blockIdx.x * RC, r1 = min(M, r0 + RC);
-  const int cl = threadIdx.x & 63, rl = threadIdx.x >> 6, RL = blockDim.x >> 6;
-  const int c = blockIdx.y * 64 + cl;
-  float s1 = 0.f, s2 = 0.f;
-  if (c < C) {
-    const float mean = st[c], rstd = st[C + c], ga = st[2 * C + c], be = st[3 * C + c];
+  float s1[8], s2[8], mean[8], rstd[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) { s1[e] = 0.f; s2[e] = 0.f; mean[e] = st[c0 + e]; rstd[e] = st[C + c0 + e]; }
+  if (rl < RL)
     for (int r = r0 + rl; r < r1; r += RL) {
-      const int w = r % G.W, t = r / G.W, h = t % G.H, s = t / G.H;
-      const float dy = routed_dy(x, dout, G, s, h, w, c, mean, rstd, ga, be);
-      const float xh = __fmul_rn(__fsub_rn(__bfloat162float(x[(int64_t)r * C + c]), mean), rstd);
-      s1 = __fadd_rn(s1, dy);
-      s2 = __fadd_rn(s2, __fmul_rn(dy, xh));
+      const int w = r % G.W, t = r / G.W, h = t % G.H, sidx = t / G.H;
+      float dy[8];
+      routed_dy8(dout, y, pidx, G, sidx, h, w, c0, dy);
+      const uint4 ux = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + c0);
+      const bf16* xv = reinterpret_cast<const bf16*>(&ux);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = __fmul_rn(__fsub_rn(__bfloat162float(xv[e]), mean[e]), rstd[e]);
+        s1[e] = __fadd_rn(s1[e], dy[e]);
+        s2[e] = __fadd_rn(s2[e], __fmul_rn(dy[e], xh));
+      }
     }
-  }
-  sh[(rl * 64 + cl) * 2] = s1;
-  sh[(rl * 64 + cl) * 2 + 1] = s2;
+  float* slot = sh + ((size_t)rl * NG + g) * 16;
+  if (rl < RL)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { slot[e] = s1[e]; slot[8 + e] = s2[e]; }
   __syncthreads();
-  if (rl == 0 && c < C) {
-    for (int l = 1; l < RL; ++l) { s1 = __fadd_rn(s1, sh[(l * 64 + cl) * 2]); s2 = __fadd_rn(s2, sh[(l * 64 + cl) * 2 + 1]); }
-    part[(size_t)blockIdx.x * 2 * C + c] = s1;
-    part[(size_t)blockIdx.x * 2 * C + C + c] = s2;
+  if (rl == 0) {
+    for (int l = 1; l < RL; ++l) {
+      const float* o = sh + ((size_t)l * NG + g) * 16;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { s1[e] = __fadd_rn(s1[e], o[e]); s2[e] = __fadd_rn(s2[e], o[8 + e]); }
+    }
+    float* p = part + (size_t)blockIdx.x * 2 * C;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { p[c0 + e] = s1[e]; p[C + c0 + e] = s2[e]; }
   }
 }
 
-// totals over chunks (fixed order); dgamma/dbeta into the gradient accumulator
+// totals over chunks (warp per channel, fixed order); dgamma/dbeta into the accumulator
 __global__ void bn_bwd_final_kernel(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
                                     float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (c >= C) return;
   float s1 = 0.f, s2 = 0.f;
-  for (int k = 0; k < chunks; ++k) { s1 = __fadd_rn(s1, part[(size_t)k * 2 * C + c]); s2 = __fadd_rn(s2, part[(size_t)k * 2 * C + C + c]); }
-  tot[c] = s1;
-  tot[C + c] = s2;
-  g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
-  g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
+  for (int k = lane; k < chunks; k += 32) {
+    s1 = __fadd_rn(s1, part[(size_t)k * 2 * C + c]);
+    s2 = __fadd_rn(s2, part[(size_t)k * 2 * C + C + c]);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    s1 = __fadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, off));
+    s2 = __fadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, off));
+  }
+  if (lane == 0) {
+    tot[c] = s1;
+    tot[C + c] = s2;
+    g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
+    g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
+  }
 }
 
-// dx = Q(gamma_b * rstd * (dy - sum(dy)/cnt - xhat * sum(dy xhat)/cnt))
+// dx = Q(gamma_b * rstd * (dy - sum(dy)/cnt - xhat * sum(dy xhat)/cnt)), 8 channels per thread
 __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                    const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
                                     const float* __restrict__ st, const float* __restrict__ tot,
                                     const bf16* __restrict__ gamma_b, BwdGeo G, int M, bf16* __restrict__ dx) {
-  const int C = G.C;
+  const int C = G.C, NG = C / 8;
   const float inv_cnt = 1.f / (float)M;
-  const int64_t total = (int64_t)M * C;
+  const int64_t total = (int64_t)M * NG;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % C);
-    const int r = (int)(i / C);
-    const int w = r % G.W, t = r / G.W, h = t % G.H, s = t / G.H;
-    const float mean = st[c], rstd = st[C + c], ga = st[2 * C + c], be = st[3 * C + c];
-    const float dy = routed_dy(x, dout, G, s, h, w, c, mean, rstd, ga, be);
-    const float xh = __fmul_rn(__fsub_rn(__bfloat162float(x[i]), mean), rstd);
-    const float gb = __bfloat162float(gamma_b[c]);
-    const float v = __fmul_rn(__fmul_rn(gb, rstd),
-                              __fsub_rn(__fsub_rn(dy, __fmul_rn(tot[c], inv_cnt)), __fmul_rn(xh, __fmul_rn(tot[C + c], inv_cnt))));
-    dx[i] = __float2bfloat16_rn(v);
+    const int g = (int)(i % NG);
+    const int r = (int)(i / NG);
+    const int c0 = g * 8;
+    const int w = r % G.W, t = r / G.W, h = t % G.H, sidx = t / G.H;
+    float dy[8];
+    routed_dy8(dout, y, pidx, G, sidx, h, w, c0, dy);
+    const uint4 ux = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + c0);
+    const bf16* xv = reinterpret_cast<const bf16*>(&ux);
+    uint32_t o4[4];
+#pragma unroll
+    for (int e2 = 0; e2 < 4; ++e2) {
+      float v2[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int e = 2 * e2 + q, c = c0 + e;
+        const float mean = st[c], rstd = st[C + c];
+        const float xh = __fmul_rn(__fsub_rn(__bfloat162float(xv[e]), mean), rstd);
+        const float gb = __bfloat162float(gamma_b[c]);
+        v2[q] = __fmul_rn(__fmul_rn(gb, rstd), __fsub_rn(__fsub_rn(dy[e], __fmul_rn(tot[c], inv_cnt)),
+                                                          __fmul_rn(xh, __fmul_rn(tot[C + c], inv_cnt))));
+      }
+      __nv_bfloat162 t2 = __floats2bfloat162_rn(v2[0], v2[1]);
+      o4[e2] = *reinterpret_cast<uint32_t*>(&t2);
+    }
+    *reinterpret_cast<uint4*>(dx + (int64_t)r * C + c0) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
   }
 }
 
 // ---- bf16-operand Linear (small: micro-batch rows) ------------------------------------------
-// y[r][o] = sum_i x[r][i] W[o][i] (fp32) + b[o]; logits: fp32 out, else Q(relu?) bf16
+// y[r][o] = sum_i x[r][i] W[o][i] (fp32) + b[o]; logits: fp32 out, else Q(relu?) bf16.
+// One warp per (r, o); lanes stride over i, shuffle reduction.
 __global__ void linear_fwd_bf16_kernel(const bf16* __restrict__ x, const bf16* __restrict__ W,
                                        const bf16* __restrict__ b, void* __restrict__ y, int n, int in, int out,
                                        int relu, int f32out) {
-  const int o = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (o >= out) return;
-  for (int r = 0; r < n; ++r) {
-    float acc = 0.f;
-    for (int i = lane; i < in; i += 32) acc += __bfloat162float(x[(int64_t)r * in + i]) * __bfloat162float(W[(int64_t)o * in + i]);
+  const int wid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (wid >= n * out) return;
+  const int r = wid / out, o = wid % out;
+  float acc = 0.f;
+  for (int i = lane; i < in; i += 32) acc += __bfloat162float(x[(int64_t)r * in + i]) * __bfloat162float(W[(int64_t)o * in + i]);
 #pragma unroll
-    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) {
-      float v = b ? __fadd_rn(acc, __bfloat162float(b[o])) : acc;
-      if (f32out) static_cast<float*>(y)[(int64_t)r * out + o] = v;
-      else {
-        if (relu) v = v > 0.f ? v : 0.f;
-        static_cast<bf16*>(y)[(int64_t)r * out + o] = __float2bfloat16_rn(v);
-      }
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) {
+    float v = b ? __fadd_rn(acc, __bfloat162float(b[o])) : acc;
+    if (f32out) static_cast<float*>(y)[(int64_t)r * out + o] = v;
+    else {
+      if (relu) v = v > 0.f ? v : 0.f;
+      static_cast<bf16*>(y)[(int64_t)r * out + o] = __float2bfloat16_rn(v);
     }
   }
 }
@@ -305,17 +379,15 @@ __device__ __forceinline__ float load_dy(const void* dy, int64_t idx, const bf16
   return d;
 }
 
-// dx[r][i] = Q(sum_o dy'[r][o] W[o][i])
+// dx[r][i] = Q(sum_o dy'[r][o] W[o][i]); thread per (r, i)
 template <bool DY_F32>
 __global__ void linear_dgrad_bf16_kernel(const void* __restrict__ dy, const bf16* __restrict__ mask,
                                          const bf16* __restrict__ W, bf16* __restrict__ dx, int n, int in, int out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= in) return;
-  for (int r = 0; r < n; ++r) {
-    float acc = 0.f;
-    for (int o = 0; o < out; ++o) acc += load_dy<DY_F32>(dy, (int64_t)r * out + o, mask) * __bfloat162float(W[(int64_t)o * in + i]);
-    dx[(int64_t)r * in + i] = __float2bfloat16_rn(acc);
-  }
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+  if (i >= in || r >= n) return;
+  float acc = 0.f;
+  for (int o = 0; o < out; ++o) acc += load_dy<DY_F32>(dy, (int64_t)r * out + o, mask) * __bfloat162float(W[(int64_t)o * in + i]);
+  dx[(int64_t)r * in + i] = __float2bfloat16_rn(acc);
 }
 
 // gW[o][i] (=|+=) sum_r dy'[r][o] x[r][i]; gb[o] (=|+=) sum_r dy'[r][o]
@@ -347,7 +419,7 @@ cudaError_t launch_stage_input_bf16(const float* x, bf16* y, int n, int C, int H
   return cudaGetLastError();
 }
 
-int bn_chunk_rows(int M) { return M <= 2048 ? 64 : 256; }
+int bn_chunk_rows(int M) { return M <= 2048 ? 32 : 128; }
 int bn_chunks(int M) { return (M + bn_chunk_rows(M) - 1) / bn_chunk_rows(M); }
 size_t bn_ws_floats(int M, int C) { return (size_t)bn_chunks(M) * 2 * C + 2 * (size_t)C; }
 
@@ -359,43 +431,47 @@ cudaError_t launch_bn_stats(const bf16* x, int M, int C, float eps, const bf16* 
   const int threads = G >= 256 ? G : (256 / G) * G;
   const size_t shm = (size_t)(threads / G) * G * 17 * 4;
   bn_stats_partial_kernel<<<chunks, threads, shm, st>>>(x, M, C, RC, ws);
-  bn_stats_final_kernel<<<(C + 127) / 128, 128, 0, st>>>(ws, chunks, M, RC, C, eps, gamma, beta, stats);
+  bn_stats_final_kernel<<<(C + 7) / 8, 256, 0, st>>>(ws, chunks, M, RC, C, eps, gamma, beta, stats);
   return cudaGetLastError();
 }
 
-cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, int n, int H, int W, int C, int P, int Q, int kh,
-                            int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st) {
+cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, uint8_t* pidx, int n, int H, int W, int C, int P,
+                            int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st) {
   const int64_t total = (int64_t)n * P * Q * (C / 8);
-  bn_apply_kernel<<<grid1d(total), 256, 0, st>>>(x, stats, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool ? 1 : 0,
-                                                 relu ? 1 : 0);
+  bn_apply_kernel<<<grid1d(total), 256, 0, st>>>(x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
+                                                 pool ? 1 : 0, relu ? 1 : 0);
   return cudaGetLastError();
 }
 
-cudaError_t launch_bn_backward(const bf16* x, const bf16* dout, const float* stats, const bf16* gamma_b, int n, int H,
-                               int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,
-                               bool relu, float* ws, float* g_gamma, float* g_beta, bool accumulate, bf16* dx,
-                               cudaStream_t st) {
+cudaError_t launch_bn_backward(const bf16* x, const bf16* dout, const bf16* y, const uint8_t* pidx, const float* stats,
+                               const bf16* gamma_b, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
+                               int sw, int ph, int pw, bool pool, bool relu, float* ws, float* g_gamma, float* g_beta,
+                               bool accumulate, bf16* dx, cudaStream_t st) {
+  if (C % 8 || C > 2048) return cudaErrorInvalidValue;
   BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
   const int M = n * H * W;
   const int RC = bn_chunk_rows(M), chunks = bn_chunks(M);
-  dim3 grid(chunks, (C + 63) / 64);
-  bn_bwd_reduce_kernel<<<grid, 256, 256 * 2 * 4, st>>>(x, dout, stats, G, M, RC, ws);
+  const int NG = C / 8;
+  const int threads = NG >= 256 ? NG : (256 / NG) * NG;
+  const size_t shm = (size_t)threads * 16 * 4;
+  bn_bwd_reduce_kernel<<<chunks, threads, shm, st>>>(x, dout, y, pidx, stats, G, M, RC, ws);
   float* tot = ws + (size_t)chunks * 2 * C;
-  bn_bwd_final_kernel<<<(C + 127) / 128, 128, 0, st>>>(ws, chunks, C, tot, g_gamma, g_beta, accumulate ? 1 : 0);
-  bn_bwd_apply_kernel<<<grid1d((int64_t)M * C), 256, 0, st>>>(x, dout, stats, tot, gamma_b, G, M, dx);
+  bn_bwd_final_kernel<<<(C + 7) / 8, 256, 0, st>>>(ws, chunks, C, tot, g_gamma, g_beta, accumulate ? 1 : 0);
+  bn_bwd_apply_kernel<<<grid1d((int64_t)M * NG), 256, 0, st>>>(x, dout, y, pidx, stats, tot, gamma_b, G, M, dx);
   return cudaGetLastError();
 }
 
 cudaError_t launch_linear_fwd_bf16(const bf16* x, const bf16* W, const bf16* b, void* y, int n, int in, int out,
                                    bool relu, bool f32out, cudaStream_t st) {
-  linear_fwd_bf16_kernel<<<(out + 7) / 8, 256, 0, st>>>(x, W, b, y, n, in, out, relu ? 1 : 0, f32out ? 1 : 0);
+  linear_fwd_bf16_kernel<<<(n * out + 7) / 8, 256, 0, st>>>(x, W, b, y, n, in, out, relu ? 1 : 0, f32out ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_linear_dgrad_bf16(const void* dy, bool dy_f32, const bf16* mask, const bf16* W, bf16* dx, int n,
                                      int in, int out, cudaStream_t st) {
-  if (dy_f32) linear_dgrad_bf16_kernel<true><<<(in + 127) / 128, 128, 0, st>>>(dy, mask, W, dx, n, in, out);
-  else linear_dgrad_bf16_kernel<false><<<(in + 127) / 128, 128, 0, st>>>(dy, mask, W, dx, n, in, out);
+  dim3 grid((in + 127) / 128, n);
+  if (dy_f32) linear_dgrad_bf16_kernel<true><<<grid, 128, 0, st>>>(dy, mask, W, dx, n, in, out);
+  else linear_dgrad_bf16_kernel<false><<<grid, 128, 0, st>>>(dy, mask, W, dx, n, in, out);
   return cudaGetLastError();
 }
 

@@ -24,7 +24,10 @@ namespace xp {
 
 namespace {
 
-constexpr int BM = 128, BK = 64, ST = 4, LAG = 2;
+constexpr int BM = 128, BK = 64;
+// smem ring depth by N tile (~192 KB of stages): more loads in flight for the narrow tiles,
+// whose k-blocks are short relative to the global-memory latency
+template <int BN> struct Depth { static constexpr int ST = BN == 64 ? 8 : (BN == 128 ? 6 : 4); static constexpr int LAG = ST - 2; };
 constexpr int NTHREADS = 256;  // warps 0-3 producers, warp 4 MMA issuer, warps 4-7 epilogue
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -309,6 +312,7 @@ template <int MODE, int BN, bool A_MN, bool B_MN>
 __device__ __forceinline__ void producer(const GemmArgs& a, uint32_t base, uint32_t full0, uint32_t empty0, int m0,
                                          int n0, int kb0, int nkb, int tid) {
   constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
+  constexpr int ST = Depth<BN>::ST, LAG = Depth<BN>::LAG;
   // operand loaders
   DenseK<BM> pak; DenseMN<BM> pam; DenseK<BN> pbk; DenseMN<BN> pbm;
   FpropA fa; DgradA da; WgradA wa; DgradB<BN> db;
@@ -355,6 +359,7 @@ template <int MODE, int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
+  constexpr int ST = Depth<BN>::ST;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023) & ~1023u;
   const uint32_t bars = base + ST * STAGE;
@@ -430,13 +435,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) 
   }
 }
 
-// split-K reduction in fixed order z = 0..splits-1
+// split-K reductions in fixed order z = 0..splits-1 (all loads of an element issued first)
+__device__ __forceinline__ float sum_splits(const float* ws, int splits, int64_t stride, int64_t i) {
+  float v[8];
+  float acc = 0.f;
+  for (int z0 = 0; z0 < splits; z0 += 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = (z0 + q < splits) ? ws[(int64_t)(z0 + q) * stride + i] : 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (z0 + q < splits) acc = (z0 + q == 0) ? v[q] : __fadd_rn(acc, v[q]);
+  }
+  return acc;
+}
+
 __global__ void reduce_bf16_kernel(const float* ws, int splits, int64_t stride, int M, int N, bf16* out, int64_t ldo,
                                    int accumulate) {
   const int64_t total = (int64_t)M * N;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    float acc = ws[i];
-    for (int z = 1; z < splits; ++z) acc = __fadd_rn(acc, ws[z * stride + i]);
+    const float acc = sum_splits(ws, splits, stride, i);
     bf16* o = out + (i / N) * ldo + (i % N);
     if (accumulate) {
       const float g = __bfloat162float(__float2bfloat16_rn(acc));
@@ -447,34 +464,27 @@ __global__ void reduce_bf16_kernel(const float* ws, int splits, int64_t stride, 
   }
 }
 
-// g[n][m] (=|+=) sum_z ws[z][m][n]  via a 32x32 shared-memory transpose
+// g[n][m] (=|+=) sum_z ws[z][m][n]  via a 32x32 shared-memory transpose, one element per thread
 __global__ void reduce_wgrad_t_kernel(const float* ws, int splits, int64_t stride, int M, int N, float* g, int64_t ldo,
                                       int accumulate) {
   __shared__ float tile[32][33];
   const int m0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (int r = ty; r < 32; r += 8) {
-    const int m = m0 + r, n = n0 + tx;
-    float acc = 0.f;
-    if (m < M && n < N) {
-      acc = ws[(int64_t)m * N + n];
-      for (int z = 1; z < splits; ++z) acc = __fadd_rn(acc, ws[z * stride + (int64_t)m * N + n]);
-    }
-    tile[r][tx] = acc;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 32
+  {
+    const int m = m0 + ty, n = n0 + tx;
+    tile[ty][tx] = (m < M && n < N) ? sum_splits(ws, splits, stride, (int64_t)m * N + n) : 0.f;
   }
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int n = n0 + r, m = m0 + tx;
-    if (m < M && n < N) {
-      float* p = g + (int64_t)n * ldo + m;
-      *p = accumulate ? __fadd_rn(*p, tile[tx][r]) : tile[tx][r];
-    }
+  const int n = n0 + ty, m = m0 + tx;
+  if (m < M && n < N) {
+    float* p = g + (int64_t)n * ldo + m;
+    *p = accumulate ? __fadd_rn(*p, tile[tx][ty]) : tile[tx][ty];
   }
 }
 
 template <int MODE, int BN, bool A_MN, bool B_MN>
 cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
-  constexpr int SMEM = ST * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
+  constexpr int SMEM = Depth<BN>::ST * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN>,
@@ -494,7 +504,14 @@ cudaError_t launch_bn(const GemmArgs& a, int bn, int splits, cudaStream_t st) {
   return launch<MODE, 256, A_MN, B_MN>(a, splits, st);
 }
 
-int choose_bn(int N) { return N <= 64 ? 64 : (N <= 128 ? 128 : 256); }
+// N tile: the widest tile whose grid still fills the SMs (a narrower tile gives more CTAs and
+// avoids split-K and its reduction pass); 64 when nothing fills them
+int choose_bn(int M, int N) {
+  const int64_t mt = (M + 127) / 128;
+  if (N > 128 && mt * ((N + 255) / 256) >= 148) return 256;
+  if (N > 64 && mt * ((N + 127) / 128) >= 148) return 128;
+  return 64;
+}
 
 int num_sms() {
   static int sms = 0;
@@ -511,7 +528,7 @@ int num_sms() {
 int choose_splits(int M, int N, int K, int bn) {
   const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   const int nkb = (K + BK - 1) / BK;
-  if (tiles >= num_sms() / 2 || nkb < 8) return 1;
+  if (tiles >= num_sms() / 2 || nkb < 8) return 1;  // >= half a wave: no split
   int s = num_sms() / tiles;
   s = std::min(s, nkb / 4);
   return std::max(1, s);
@@ -521,7 +538,7 @@ int choose_splits(int M, int N, int K, int bn) {
 template <int MODE, bool A_MN, bool B_MN>
 cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_ldo, int accumulate, float* ws,
                       int64_t ws_elems, cudaStream_t st) {
-  const int bn = choose_bn(a.N);
+  const int bn = choose_bn(a.M, a.N);
   int splits = choose_splits(a.M, a.N, a.K, bn);
   const int64_t plane = (int64_t)a.M * a.N;
   while (splits > 1 && (int64_t)splits * plane > ws_elems) --splits;
@@ -541,7 +558,7 @@ cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_
     reduce_bf16_kernel<<<grid, 256, 0, st>>>(ws, splits, plane, a.M, a.N, (bf16*)final_out, final_ldo, accumulate);
   } else {
     dim3 grid((a.M + 31) / 32, (a.N + 31) / 32);
-    reduce_wgrad_t_kernel<<<grid, 256, 0, st>>>(ws, splits, plane, a.M, a.N, (float*)final_out, final_ldo, accumulate);
+    reduce_wgrad_t_kernel<<<grid, 1024, 0, st>>>(ws, splits, plane, a.M, a.N, (float*)final_out, final_ldo, accumulate);
   }
   return cudaGetLastError();
 }
@@ -554,7 +571,7 @@ cudaError_t tc_gemm_plain(const bf16* A, const bf16* B, float* D, int M, int N, 
   a.M = M; a.N = N; a.K = K; a.A = A; a.B = B;
   a.lda = a_kmajor ? K : M; a.ldb = b_kmajor ? K : N;
   a.epi = EPI_F32; a.out = D; a.ldo = ldd; a.kb_per_split = std::max(1, (K + BK - 1) / BK);
-  const int bn = choose_bn(N);
+  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
   if (a_kmajor && b_kmajor) return launch_bn<GEMM_PLAIN, false, false>(a, bn, 1, st);
   if (a_kmajor && !b_kmajor) return launch_bn<GEMM_PLAIN, false, true>(a, bn, 1, st);
   if (!a_kmajor && b_kmajor) return launch_bn<GEMM_PLAIN, true, false>(a, bn, 1, st);
@@ -588,7 +605,7 @@ cudaError_t tc_conv_wgrad(const ConvGeo& g, const bf16* X, const bf16* dY, float
 int64_t tc_conv_ws_elems(const ConvGeo& g) {
   // the largest of the three GEMMs' split-K need, capped at 16M floats
   auto need = [](int M, int N, int K) -> int64_t {
-    const int bn = choose_bn(N);
+    const int bn = choose_bn(M, N);
     return (int64_t)choose_splits(M, N, K, bn) * M * N;
   };
   int64_t a = need(g.Nimg * g.P * g.Q, g.Co, g.R * g.S * g.C);

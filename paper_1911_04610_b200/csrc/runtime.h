@@ -51,6 +51,7 @@ struct StageRT {
   std::vector<std::vector<void*>> act;  // [tensor][slot] stashed activations (tensor 0 = in_slot)
   std::vector<std::vector<void*>> mid;  // [op][slot] conv outputs before BN (bf16 path)
   std::vector<std::vector<float*>> stats;  // [op][slot] BN mean, rstd, gamma_f, beta_f
+  std::vector<std::vector<uint8_t*>> pidx; // [op][slot] max-pool winner positions (conv op with pool)
   std::vector<float*> dz;               // [slot] logits gradient (last stage)
   std::vector<void*> grad;              // [tensor] activation-gradient buffers (per op pass)
   void* gmid = nullptr;                 // conv op: gradient of the conv output (bf16)
@@ -61,6 +62,7 @@ struct StageRT {
   // host program state
   int64_t pos = 0;
   bool done = false;
+  int64_t fwd_enq = 0, bwd_enq = 0;     // last micro-batch whose F / B has been enqueued
   int host_ver = 0, host_fver = 0, host_bver = 0;
   // trace
   TraceRec* trace_dev = nullptr;
@@ -107,13 +109,14 @@ struct xpipe_ctx {
     cudaGraphExec_t exec = nullptr;
     int seen = 0;
     int64_t kernels = 0;
-    std::vector<int64_t> dpos;
+    std::vector<int64_t> dpos, dfwd, dbwd;
     std::vector<int> dver, dfver, dbver;
     std::vector<std::vector<int>> prof_cls;
     std::vector<std::vector<double>> prof_work;
   };
   std::map<std::string, GraphRec> graphs;
   int64_t graph_replays = 0;
+  bool capturing = false;
   std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)
 };
 

@@ -151,13 +151,15 @@ int prof_begin(xpipe_ctx* c, StageRT& s) {
     s.ev_pool.push_back(e);
   }
   // external record: inside a stream capture this becomes an event-record node of the graph
-  XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used], s.stream, cudaEventRecordExternal));
+  if (c->capturing) XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used], s.stream, cudaEventRecordExternal));
+  else XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used], s.stream));
   return XP_OK;
 }
 
 int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work) {
   if (!c->cfg.profile) return XP_OK;
-  XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used + 1], s.stream, cudaEventRecordExternal));
+  if (c->capturing) XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used + 1], s.stream, cudaEventRecordExternal));
+  else XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used + 1], s.stream));
   s.ev_used += 2;
   s.prof_cls.push_back(cls);
   s.prof_work.push_back(work);
@@ -357,25 +359,46 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
   return XP_OK;
 }
 
-// host enqueue loop: every stage's program in order, as far as fed micro-batches allow
+// Host enqueue loop in dataflow order (the oracle's O2 driver, on enqueue counters): a stage's
+// next op is enqueued only once every op its device waits depend on has been enqueued, so a
+// full hardware queue can never block the host while the work it waits for is unenqueued.
+// In multi-process mode the other stages' progress is unknown: only program order applies.
+bool op_ready(const xpipe_ctx* c, int k, int op, int64_t u) {
+  if (c->mp()) return true;
+  const auto& S = c->S;
+  if (op == 0) {
+    if (k > 0 && S[k - 1].fwd_enq < u) return false;                          // activation message
+    if (k + 1 < c->K && S[k + 1].bwd_enq < u - S[k + 1].S) return false;      // ring credit
+  } else {
+    if (k + 1 < c->K ? S[k + 1].bwd_enq < u : S[k].fwd_enq < u) return false; // gradient / logits
+    if (k > 0 && S[k - 1].bwd_enq < u - S[k - 1].S) return false;             // gradient ring credit
+  }
+  return true;
+}
+
 int drive(xpipe_ctx* c, int64_t total) {
-  for (int k = 0; k < c->K; ++k) {
-    StageRT& s = c->S[k];
-    if (!owned(s)) continue;
-    while (!s.done) {
-      int op;
-      int64_t u;
-      program_op(c, k, s.pos, &op, &u);
-      if (total >= 0 && u > total) {
-        if (op == 1 || c->cfg.schedule == XP_SCHED_GPIPE) { s.done = true; break; }
-        ++s.pos;  // flushing: forwards beyond the last fed micro-batch are dropped
-        continue;
+  for (bool progress = true; progress;) {
+    progress = false;
+    for (int k = 0; k < c->K; ++k) {
+      StageRT& s = c->S[k];
+      if (!owned(s)) continue;
+      while (!s.done) {
+        int op;
+        int64_t u;
+        program_op(c, k, s.pos, &op, &u);
+        if (total >= 0 && u > total) {
+          if (op == 1 || c->cfg.schedule == XP_SCHED_GPIPE) { s.done = true; break; }
+          ++s.pos;  // flushing: forwards beyond the last fed micro-batch are dropped
+          continue;
+        }
+        if (u > c->fed || !op_ready(c, k, op, u)) break;
+        if (verbose()) fprintf(stderr, "[xpipe] stage %d pos %lld: %c(%lld) slot %lld\n", k, (long long)s.pos,
+                               op == 0 ? 'F' : 'B', (long long)u, (long long)((u - 1) % s.S));
+        XP_TRY(op == 0 ? enqueue_forward(c, k, u) : enqueue_backward(c, k, u));
+        if (op == 0) s.fwd_enq = u; else s.bwd_enq = u;
+        ++s.pos;
+        progress = true;
       }
-      if (u > c->fed) break;  // needs a micro-batch not fed yet
-      if (verbose()) fprintf(stderr, "[xpipe] stage %d pos %lld: %c(%lld) slot %lld\n", k, (long long)s.pos,
-                             op == 0 ? 'F' : 'B', (long long)u, (long long)((u - 1) % s.S));
-      XP_TRY(op == 0 ? enqueue_forward(c, k, u) : enqueue_backward(c, k, u));
-      ++s.pos;
     }
   }
   return XP_OK;
@@ -453,7 +476,8 @@ std::string graph_signature(const xpipe_ctx* c, int64_t M, int64_t fed_before) {
                     std::to_string((uintptr_t)c->y_dev) + ":" + std::to_string((uintptr_t)c->loss_dev);
   const int64_t f = fed_before - c->base;
   for (const auto& s : c->S)
-    sig += "|" + std::to_string(s.pos - 2 * f) + "," + std::to_string(f % s.S) + "," + std::to_string(s.host_ver & 1) +
+    sig += "|" + std::to_string(s.pos - 2 * f) + "," + std::to_string(s.fwd_enq - fed_before) + "," +
+           std::to_string(s.bwd_enq - fed_before) + "," + std::to_string(f % s.S) + "," + std::to_string(s.host_ver & 1) +
            "," + std::to_string(s.host_fver & 1) + "," + std::to_string((int)s.done);
   return sig;
 }
@@ -482,6 +506,8 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
       StageRT& s = c->S[k];
       const int v0 = s.host_ver;
       s.pos += g.dpos[k];
+      s.fwd_enq += g.dfwd[k];
+      s.bwd_enq += g.dbwd[k];
       s.host_ver += g.dver[k];
       s.host_fver = v0 + g.dfver[k];
       s.host_bver = v0 + g.dbver[k];
@@ -497,9 +523,9 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
   }
   if (g.seen++ == 0) return drive(c, -1);  // first sighting: plain enqueue
   // second sighting: capture this call's enqueue, then launch it
-  std::vector<int64_t> pos0;
+  std::vector<int64_t> pos0, fwd0, bwd0;
   std::vector<int> ver0;
-  for (auto& s : c->S) { pos0.push_back(s.pos); ver0.push_back(s.host_ver); }
+  for (auto& s : c->S) { pos0.push_back(s.pos); ver0.push_back(s.host_ver); fwd0.push_back(s.fwd_enq); bwd0.push_back(s.bwd_enq); }
   const int64_t k0 = c->kernels;
   static thread_local std::vector<cudaEvent_t> evs;
   while (evs.size() < c->S.size() + 1) {
@@ -510,7 +536,9 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
   XP_CUDA(c, cudaStreamBeginCapture(o.stream, cudaStreamCaptureModeThreadLocal));
   XP_CUDA(c, cudaEventRecord(evs[0], o.stream));
   for (size_t k = 1; k < c->S.size(); ++k) XP_CUDA(c, cudaStreamWaitEvent(c->S[k].stream, evs[0], 0));
+  c->capturing = true;
   int r = drive(c, -1);
+  c->capturing = false;
   for (size_t k = 1; k < c->S.size() && r == XP_OK; ++k) {
     if (cudaEventRecord(evs[k], c->S[k].stream) != cudaSuccess || cudaStreamWaitEvent(o.stream, evs[k], 0) != cudaSuccess)
       r = set_err(c, XP_ECUDA, "graph join");
@@ -523,12 +551,14 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) return set_err(c, XP_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
   g.kernels = c->kernels - k0;
-  g.dpos.clear(); g.dver.clear(); g.dfver.clear(); g.dbver.clear();
+  g.dpos.clear(); g.dver.clear(); g.dfver.clear(); g.dbver.clear(); g.dfwd.clear(); g.dbwd.clear();
   g.prof_cls.clear(); g.prof_work.clear();
   for (auto& s : c->S) { g.prof_cls.push_back(s.prof_cls); g.prof_work.push_back(s.prof_work); }
   for (size_t k = 0; k < c->S.size(); ++k) {
     StageRT& s = c->S[k];
     g.dpos.push_back(s.pos - pos0[k]);
+    g.dfwd.push_back(s.fwd_enq - fwd0[k]);
+    g.dbwd.push_back(s.bwd_enq - bwd0[k]);
     g.dver.push_back(s.host_ver - ver0[k]);
     g.dfver.push_back(s.host_fver - ver0[k]);
     g.dbver.push_back(s.host_bver - ver0[k]);

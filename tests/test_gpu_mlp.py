@@ -109,8 +109,9 @@ def test_determinism_two_runs(oracle_mod):
 @pytest.mark.parametrize("K,T", [(2, 4), (4, 2), (1, 4)])
 def test_cuda_graph_replay_bit_exact(oracle_mod, K, T):
     """Steady-state steps captured as CUDA graphs and replayed (flags rebased per call) give
-    the same weights, bit for bit, as the oracle's replay of the same calls."""
-    calls = [2] * 8 + [2]
+    the same weights, bit for bit, as the oracle's replay of the same calls.  (The ring-slot
+    phase repeats with period lcm(S_k)/gcd(.., micro-batches per call) calls: 16 calls cover it.)"""
+    calls = [2] * 16 + [2]
     o, g, L, lo, lg = run_pair(oracle_mod, K, T, 16, sum(calls), calls=calls, graphs=True)
     assert g.replays >= 4, g.replays
     for k in range(K):

@@ -72,6 +72,7 @@ struct StageRT {
   void* diag = nullptr;                  // pinned scratch for watchdog diagnostics
   // profiling (cfg.profile): event pool and the (class, work) of each recorded pair
   std::vector<cudaEvent_t> ev_pool;
+  std::vector<cudaEvent_t> ev_flag[4];  // per-slot events standing in for the flags inside graphs
   cudaEvent_t tmark[2] = {nullptr, nullptr};
   size_t ev_used = 0;
   std::vector<int> prof_cls;
@@ -117,6 +118,7 @@ struct xpipe_ctx {
   std::map<std::string, GraphRec> graphs;
   int64_t graph_replays = 0;
   bool capturing = false;
+  std::vector<int64_t> cap_fwd0, cap_bwd0;  // enqueue counters when the capture started
   std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)
 };
 

@@ -108,6 +108,7 @@ void free_all(xpipe_ctx* c) {
     if (s.diag) { cudaFreeHost(s.diag); s.diag = nullptr; }
     for (auto e : s.ev_pool) cudaEventDestroy(e);
     s.ev_pool.clear();
+    for (auto& v : s.ev_flag) { for (auto e : v) cudaEventDestroy(e); v.clear(); }
     for (auto& e : s.tmark) if (e) { cudaEventDestroy(e); e = nullptr; }
     if (s.stream) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.stream); cudaStreamDestroy(s.stream); s.stream = nullptr; }
   }
@@ -178,17 +179,40 @@ bool verbose() {
   return v == 1;
 }
 
-int flag_wait(xpipe_ctx* c, StageRT& s, uint32_t* flag, int64_t value) {
-  if (verbose()) fprintf(stderr, "[xpipe] stage %d wait %p >= %lld%s\n", s.k, (void*)flag, (long long)value,
+// Cross-stage dependency on ring flag `which` of stage s (0 act_ready, 1 grad_ready,
+// 2 act_ack, 3 grad_ack) reaching micro-batch `value`.  Normally a device-side memop wait.
+// While a CUDA graph is being captured it becomes a graph edge (wait on the per-slot event the
+// producer recorded), and waits on producers enqueued before this call are dropped (every
+// earlier op completed before the call started).
+int flag_wait(xpipe_ctx* c, StageRT& s, int which, int64_t value) {
+  uint32_t* flag = &s.flags[which];
+  if (verbose()) fprintf(stderr, "[xpipe] stage %d wait %d(%p) >= %lld%s\n", s.k, which, (void*)flag, (long long)value,
                          value <= 0 ? " (skip)" : "");
   if (value <= 0) return XP_OK;  // absolute: that message never existed
+  if (c->capturing) {
+    // producer's enqueue counter at capture start: waits on earlier messages are satisfied
+    const int prod = (which == 0 || which == 3) ? s.k - 1 : s.k + 1;
+    const int64_t before = (which == 0) ? c->cap_fwd0[prod] : c->cap_bwd0[prod];
+    if (value <= before) return XP_OK;
+    auto& evs = s.ev_flag[which];
+    XP_CUDA(c, cudaStreamWaitEvent(s.stream, evs[(value - 1) % evs.size()], 0));
+    return XP_OK;
+  }
   int r = p_wait32(s.stream, (unsigned long long)(uintptr_t)flag, (uint32_t)(value - c->flag_base), 0 /*GEQ*/);
   if (r != 0) return set_err(c, XP_ECOMM, "cuStreamWaitValue32 failed: " + std::to_string(r));
   return XP_OK;
 }
 
-int flag_write(xpipe_ctx* c, StageRT& s, uint32_t* flag, int64_t value) {
-  if (verbose()) fprintf(stderr, "[xpipe] stage %d write %p = %lld\n", s.k, (void*)flag, (long long)value);
+// producer side: set ring flag `which` of stage `tgt` to `value` from stream s (memop write,
+// ordered after the preceding work); while capturing also record the per-slot event
+int flag_write(xpipe_ctx* c, StageRT& s, StageRT& tgt, int which, int64_t value) {
+  uint32_t* flag = &tgt.flags[which];
+  if (verbose()) fprintf(stderr, "[xpipe] stage %d write stage %d flag %d(%p) = %lld\n", s.k, tgt.k, which, (void*)flag,
+                         (long long)value);
+  if (c->capturing) {
+    auto& evs = tgt.ev_flag[which];
+    XP_CUDA(c, cudaEventRecord(evs[(value - 1) % evs.size()], s.stream));
+  }
   int r = p_write32(s.stream, (unsigned long long)(uintptr_t)flag, (uint32_t)(value - c->flag_base),
                     0 /*DEFAULT: with barrier*/);
   if (r != 0) return set_err(c, XP_ECOMM, "cuStreamWriteValue32 failed: " + std::to_string(r));
@@ -275,7 +299,7 @@ int enqueue_forward(xpipe_ctx* c, int k, int64_t u) {
     const float* src = c->x_dev + (u - c->call_first) * c->n * per;
     XP_TRY(stage_input(c, s, src, s.in_slot[slot]));
   } else {
-    XP_TRY(flag_wait(c, s, &s.flags[0], u));
+    XP_TRY(flag_wait(c, s, 0, u));
   }
   TraceRec* rec = nullptr;
   XP_TRY(trace_slot(c, s, &rec));
@@ -285,10 +309,10 @@ int enqueue_forward(xpipe_ctx* c, int k, int64_t u) {
   for (size_t o = 0; o < s.plan.ops.size(); ++o) XP_TRY(op_forward(c, s, (int)o, Wf, slot, u));
   if (k + 1 < c->K) {
     StageRT& nx = c->S[k + 1];
-    XP_TRY(flag_wait(c, s, &s.flags[2], u - nx.S));  // ring credit: consumer released u - R
+    XP_TRY(flag_wait(c, s, 2, u - nx.S));  // ring credit: consumer released u - R
     XP_CUDA(c, cudaMemcpyAsync(nx.in_slot[(u - 1) % nx.S], s.act[s.plan.out_tensor][slot], s.plan.out_bytes,
                                cudaMemcpyDefault, s.stream));
-    XP_TRY(flag_write(c, s, &nx.flags[0], u));
+    XP_TRY(flag_write(c, s, nx, 0, u));
   }
   if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
   return XP_OK;
@@ -301,7 +325,7 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
   const int sb = version_difference(c, k, 1);
   const bool bw = (j == 1);
   cudaSetDevice(s.dev);
-  if (k + 1 < c->K) XP_TRY(flag_wait(c, s, &s.flags[1], u));
+  if (k + 1 < c->K) XP_TRY(flag_wait(c, s, 1, u));
   TraceRec* rec = nullptr;
   XP_TRY(trace_slot(c, s, &rec));
   if (rec) XP_TRY(check_launch(c, launch_trace_begin(s.ds, rec, k, 1, (int)t, (int)j, sb, bw, s.stream), "trace"));
@@ -325,14 +349,14 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     if (need0) has[O.in0] = 1;
     if (need1) has[O.in1] = 1;
   }
-  if (k + 1 < c->K) XP_TRY(flag_write(c, s, &c->S[k + 1].flags[3], u));  // released gin slot u
+  if (k + 1 < c->K) XP_TRY(flag_write(c, s, c->S[k + 1], 3, u));  // released gin slot u
   if (k > 0) {
     if (!has[0]) return set_err(c, XP_ESCHED, "no gradient reaches the stage input (internal)");
     StageRT& pv = c->S[k - 1];
-    XP_TRY(flag_wait(c, s, &s.flags[3], u - pv.S));
+    XP_TRY(flag_wait(c, s, 3, u - pv.S));
     XP_CUDA(c, cudaMemcpyAsync(pv.gin_slot[(u - 1) % pv.S], gp[0], P.in_bytes, cudaMemcpyDefault, s.stream));
-    XP_TRY(flag_write(c, s, &pv.flags[1], u));
-    XP_TRY(flag_write(c, s, &pv.flags[2], u));  // released our input slot u
+    XP_TRY(flag_write(c, s, pv, 1, u));
+    XP_TRY(flag_write(c, s, pv, 2, u));  // released our input slot u
   }
   if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
   if (j == c->T) {
@@ -536,6 +560,20 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
   XP_CUDA(c, cudaStreamBeginCapture(o.stream, cudaStreamCaptureModeThreadLocal));
   XP_CUDA(c, cudaEventRecord(evs[0], o.stream));
   for (size_t k = 1; k < c->S.size(); ++k) XP_CUDA(c, cudaStreamWaitEvent(c->S[k].stream, evs[0], 0));
+  c->cap_fwd0.clear(); c->cap_bwd0.clear();
+  for (auto& s : c->S) {
+    c->cap_fwd0.push_back(s.fwd_enq);
+    c->cap_bwd0.push_back(s.bwd_enq);
+    for (int w = 0; w < 4; ++w) {
+      const int k = s.k;
+      const size_t n = (w == 0 || w == 1) ? s.S : (w == 2 ? (k + 1 < c->K ? c->S[k + 1].S : 1) : (k > 0 ? c->S[k - 1].S : 1));
+      while (s.ev_flag[w].size() < n) {
+        cudaEvent_t e;
+        XP_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s.ev_flag[w].push_back(e);
+      }
+    }
+  }
   c->capturing = true;
   int r = drive(c, -1);
   c->capturing = false;

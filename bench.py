@@ -270,8 +270,14 @@ def main():
         if mp_mode:
             import torch.distributed as dist
             dist.barrier()
-    for _ in range(args.warmup):
+    # warm-up: at least --warmup steps, and (with CUDA graphs) until every step signature of the
+    # steady state has been captured -- the ring-slot phase repeats with a period of up to K
+    # calls -- so no capture/instantiation lands in the timed region
+    streak, w = 0, 0
+    while w < args.warmup or (not args.no_graphs and not mp_mode and streak < K + 1 and w < args.warmup + 4 * K + 8):
         g.step(xd, yd, M)
+        streak = streak + 1 if g.last_stats.graph_replays else 0
+        w += 1
     barrier()
     prof = {}
     launches = 0

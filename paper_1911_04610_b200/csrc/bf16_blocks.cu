@@ -52,7 +52,7 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
       const ConvGeo g = conv_geo(c, O, L);
       bf16* mid = (bf16*)s.mid[o][slot];
       XP_TRY(prof_begin(c, s));
-      XP_TRY(check_launch(c, tc_conv_fprop(g, x, W + L.woff, mid, s.ws, s.ws_elems, s.stream), "conv_fprop"));
+      XP_TRY(check_launch(c, tc_conv_fprop(g, x, W + L.woff, mid, s.ws, s.ws_elems, s.ctr, s.stream), "conv_fprop"));
       XP_TRY(prof_end(c, s, XP_PROF_CONV_FPROP, conv_flops(g, L.in0.c)));
       const LayerInfo& N = c->net.layers[O.lbn];
       const int M = n * O.smid.h * O.smid.w;
@@ -113,12 +113,12 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
                           "bn_backward"));
       XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)s.act[O.in0][slot], dmid, s.g + L.woff, accumulate_g, s.ws,
-                                           s.ws_elems, s.stream), "conv_wgrad"));
+                                           s.ws_elems, s.ctr, s.stream), "conv_wgrad"));
       XP_TRY(prof_end(c, s, XP_PROF_CONV_WGRAD, conv_flops(g, L.in0.c)));
       if (dx0) {
         XP_TRY(prof_begin(c, s));
-        XP_TRY(check_launch(c, tc_conv_dgrad(g, O.sin0.c, dmid, W + L.woff, (bf16*)dx0, s.ws, s.ws_elems, s.stream,
-                                             acc0), "conv_dgrad"));
+        XP_TRY(check_launch(c, tc_conv_dgrad(g, O.sin0.c, dmid, W + L.woff, (bf16*)dx0, s.ws, s.ws_elems, s.ctr,
+                                             s.stream, acc0), "conv_dgrad"));
         XP_TRY(prof_end(c, s, XP_PROF_CONV_DGRAD, conv_flops(g, L.in0.c)));
       }
       return XP_OK;

@@ -94,7 +94,9 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
     s.ws_elems = ws;
     s.ws = (float*)A((size_t)std::max<int64_t>(ws, 64) * 4);
     s.bnws = (float*)A(bnws * 4);
-    if (!s.ws || !s.bnws) return set_err(c, XP_ENOMEM, "workspace");
+    s.ctr = (int*)A((size_t)kTileCounters * sizeof(int));
+    if (!s.ws || !s.bnws || !s.ctr) return set_err(c, XP_ENOMEM, "workspace");
+    XP_CUDA(c, cudaMemsetAsync(s.ctr, 0, (size_t)kTileCounters * sizeof(int), s.stream));
   }
   return XP_OK;
 }

@@ -426,6 +426,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) 
       }
       if (n0 + c0 < a.N) epi_store(a, row, n0 + c0, v);
     }
+    if (a.splits > 1) {
+      // last-CTA reduction: publish this partial, count it, and let the last split finish
+      __shared__ int is_last;
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+      if (tid == 128) {
+        const int old = atomicAdd(&a.tile_counters[tile], 1);
+        is_last = (old == a.splits - 1);
+        if (is_last) a.tile_counters[tile] = 0;  // ready for the next launch
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (is_last) {
+        __threadfence();
+        GemmArgs f = a;
+        f.epi = a.final_epi; f.out = a.final_out; f.ldo = a.final_ldo; f.accumulate = a.final_accumulate;
+        const float* ws = static_cast<const float*>(a.out);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN && n0 + c0 < a.N; c0 += 32) {
+          uint32_t v[32];
+          if (row < a.M) {
+            const float* base = ws + (int64_t)row * a.ldo + n0 + c0;
+            const int ncol = min(32, a.N - n0 - c0);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              float acc = 0.f;
+              if (e < ncol)
+                for (int z = 0; z < a.splits; ++z) {
+                  const float x = __ldcg(base + (int64_t)z * a.split_stride + e);
+                  acc = z ? __fadd_rn(acc, x) : x;
+                }
+              v[e] = __float_as_uint(acc);
+            }
+          }
+          epi_store(f, row, n0 + c0, v);
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -537,30 +575,27 @@ int choose_splits(int M, int N, int K, int bn) {
 // run a conv GEMM with optional split-K through the workspace
 template <int MODE, bool A_MN, bool B_MN>
 cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_ldo, int accumulate, float* ws,
-                      int64_t ws_elems, cudaStream_t st) {
+                      int64_t ws_elems, int* counters, cudaStream_t st) {
   const int bn = choose_bn(a.M, a.N);
   int splits = choose_splits(a.M, a.N, a.K, bn);
   const int64_t plane = (int64_t)a.M * a.N;
   while (splits > 1 && (int64_t)splits * plane > ws_elems) --splits;
+  if (!counters) splits = 1;
   const int nkb = (a.K + BK - 1) / BK;
   if (splits <= 1) {
+    a.splits = 1;
     a.kb_per_split = std::max(1, nkb);
     a.epi = final_epi; a.out = final_out; a.ldo = final_ldo; a.accumulate = accumulate; a.split_stride = 0;
     return launch_bn<MODE, A_MN, B_MN>(a, bn, 1, st);
   }
   a.kb_per_split = (nkb + splits - 1) / splits;
   splits = (nkb + a.kb_per_split - 1) / a.kb_per_split;
+  const int tiles = ((a.M + BM - 1) / BM) * ((a.N + bn - 1) / bn);
+  if (tiles > kTileCounters) return cudaErrorInvalidValue;
   a.epi = EPI_F32; a.out = ws; a.ldo = a.N; a.accumulate = 0; a.split_stride = plane;
-  cudaError_t e = launch_bn<MODE, A_MN, B_MN>(a, bn, splits, st);
-  if (e != cudaSuccess) return e;
-  if (final_epi == EPI_BF16) {
-    int grid = (int)std::min<int64_t>((plane + 255) / 256, 148 * 8);
-    reduce_bf16_kernel<<<grid, 256, 0, st>>>(ws, splits, plane, a.M, a.N, (bf16*)final_out, final_ldo, accumulate);
-  } else {
-    dim3 grid((a.M + 31) / 32, (a.N + 31) / 32);
-    reduce_wgrad_t_kernel<<<grid, 1024, 0, st>>>(ws, splits, plane, a.M, a.N, (float*)final_out, final_ldo, accumulate);
-  }
-  return cudaGetLastError();
+  a.splits = splits; a.tile_counters = counters;
+  a.final_epi = final_epi; a.final_out = final_out; a.final_ldo = final_ldo; a.final_accumulate = accumulate;
+  return launch_bn<MODE, A_MN, B_MN>(a, bn, splits, st);
 }
 
 }  // namespace
@@ -579,27 +614,27 @@ cudaError_t tc_gemm_plain(const bf16* A, const bf16* B, float* D, int M, int N, 
 }
 
 cudaError_t tc_conv_fprop(const ConvGeo& g, const bf16* X, const bf16* Wt, bf16* Y, float* ws, int64_t ws_elems,
-                          cudaStream_t st) {
+                          int* counters, cudaStream_t st) {
   GemmArgs a{};
   a.g = g; a.A = X; a.B = Wt;
   a.M = g.Nimg * g.P * g.Q; a.N = g.Co; a.K = g.R * g.S * g.C;
-  return run_split<GEMM_FPROP, false, false>(a, EPI_BF16, Y, g.Co, 0, ws, ws_elems, st);
+  return run_split<GEMM_FPROP, false, false>(a, EPI_BF16, Y, g.Co, 0, ws, ws_elems, counters, st);
 }
 
 cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const bf16* dY, const bf16* Wt, bf16* dX, float* ws,
-                          int64_t ws_elems, cudaStream_t st, bool accumulate) {
+                          int64_t ws_elems, int* counters, cudaStream_t st, bool accumulate) {
   GemmArgs a{};
   a.g = g; a.A = dY; a.B = Wt;
   a.M = g.Nimg * g.H * g.W; a.N = Cx; a.K = g.R * g.S * g.Co;
-  return run_split<GEMM_DGRAD, false, true>(a, EPI_BF16, dX, Cx, accumulate ? 1 : 0, ws, ws_elems, st);
+  return run_split<GEMM_DGRAD, false, true>(a, EPI_BF16, dX, Cx, accumulate ? 1 : 0, ws, ws_elems, counters, st);
 }
 
 cudaError_t tc_conv_wgrad(const ConvGeo& g, const bf16* X, const bf16* dY, float* gW, bool accumulate, float* ws,
-                          int64_t ws_elems, cudaStream_t st) {
+                          int64_t ws_elems, int* counters, cudaStream_t st) {
   GemmArgs a{};
   a.g = g; a.A = X; a.B = dY;
   a.M = g.R * g.S * g.C; a.N = g.Co; a.K = g.Nimg * g.P * g.Q;
-  return run_split<GEMM_WGRAD, true, true>(a, EPI_WGRAD_T, gW, a.M, accumulate ? 1 : 0, ws, ws_elems, st);
+  return run_split<GEMM_WGRAD, true, true>(a, EPI_WGRAD_T, gW, a.M, accumulate ? 1 : 0, ws, ws_elems, counters, st);
 }
 
 int64_t tc_conv_ws_elems(const ConvGeo& g) {
@@ -634,10 +669,17 @@ extern "C" int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void
   if (g.P != (g.H + 2 * g.ph - g.R) / g.sh + 1 || g.Q != (g.W + 2 * g.pw - g.S) / g.sw + 1) return XP_EINVAL;
   if (!ws) ws_elems = 0;
   cudaStream_t st = (cudaStream_t)stream;
+  // unit-test entry: split-K counters live in the tail of the caller's workspace
+  int* counters = nullptr;
+  if (ws && ws_elems > xp::kTileCounters) {
+    ws_elems -= xp::kTileCounters;
+    counters = reinterpret_cast<int*>(ws + ws_elems);
+    if (cudaMemsetAsync(counters, 0, xp::kTileCounters * sizeof(int), st) != cudaSuccess) return XP_ECUDA;
+  }
   cudaError_t e;
   typedef __nv_bfloat16 B;
-  if (mode == 1) e = xp::tc_conv_fprop(g, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, st);
-  else if (mode == 2) e = xp::tc_conv_dgrad(g, g.C, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, st);
-  else e = xp::tc_conv_wgrad(g, (const B*)in0, (const B*)in1, (float*)out, accumulate != 0, ws, ws_elems, st);
+  if (mode == 1) e = xp::tc_conv_fprop(g, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, counters, st);
+  else if (mode == 2) e = xp::tc_conv_dgrad(g, g.C, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, counters, st);
+  else e = xp::tc_conv_wgrad(g, (const B*)in0, (const B*)in1, (float*)out, accumulate != 0, ws, ws_elems, counters, st);
   return e == cudaSuccess ? XP_OK : XP_ECUDA;
 }

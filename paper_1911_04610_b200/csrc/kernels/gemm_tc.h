@@ -8,6 +8,7 @@ namespace xp {
 
 enum { GEMM_PLAIN = 0, GEMM_FPROP = 1, GEMM_DGRAD = 2, GEMM_WGRAD = 3 };
 enum { EPI_BF16 = 0, EPI_F32 = 1, EPI_WGRAD_T = 2 };
+constexpr int kTileCounters = 1 << 14;  // per-stream split-K arrival counters (zero-initialised)
 
 struct ConvGeo {
   int Nimg, H, W, C;      // input NHWC, C = channel stride (Cin padded to a multiple of 8)
@@ -27,6 +28,15 @@ struct GemmArgs {
   int accumulate;
   int64_t split_stride;   // elements between split-K partial planes (EPI_F32 into a workspace)
   int kb_per_split;
+  // split-K with in-kernel reduction: every split CTA writes its fp32 partial plane, the last
+  // one to finish (per-tile counter) sums the planes in fixed order z = 0..splits-1 and applies
+  // the final epilogue (final_epi into final_out)
+  int splits;
+  int* tile_counters;
+  int final_epi;
+  void* final_out;
+  int64_t final_ldo;
+  int final_accumulate;
 };
 
 // plain GEMM for unit parity: D[M][N] fp32 (ldd) = A(m,k) B(n,k)
@@ -34,14 +44,17 @@ cudaError_t tc_gemm_plain(const __nv_bfloat16* A, const __nv_bfloat16* B, float*
                           bool b_kmajor, int64_t ldd, cudaStream_t st);
 
 // Y [Nimg*P*Q][Co] bf16 = conv(X [Nimg][H][W][C] bf16, W [Co][R][S][C] bf16)
+// ws: fp32 split-K workspace of ws_elems; counters: kTileCounters zeroed ints owned by the
+// calling stream (NULL = no split-K)
 cudaError_t tc_conv_fprop(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* Wt, __nv_bfloat16* Y,
-                          float* ws, int64_t ws_elems, cudaStream_t st);
+                          float* ws, int64_t ws_elems, int* counters, cudaStream_t st);
 // dX [Nimg*H*W][Cx] bf16 (Cx = real input channels, multiple of 8) from dY [Nimg*P*Q][Co]
 cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const __nv_bfloat16* dY, const __nv_bfloat16* Wt,
-                          __nv_bfloat16* dX, float* ws, int64_t ws_elems, cudaStream_t st, bool accumulate = false);
+                          __nv_bfloat16* dX, float* ws, int64_t ws_elems, int* counters, cudaStream_t st,
+                          bool accumulate = false);
 // gW [Co][R][S][C] fp32 (=|+=) sum over pixels of dY x im2col(X)
 cudaError_t tc_conv_wgrad(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* dY, float* gW, bool accumulate,
-                          float* ws, int64_t ws_elems, cudaStream_t st);
+                          float* ws, int64_t ws_elems, int* counters, cudaStream_t st);
 // workspace (floats) the launchers above can use profitably for split-K
 int64_t tc_conv_ws_elems(const ConvGeo& g);
 

@@ -57,7 +57,7 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
       const LayerInfo& N = c->net.layers[O.lbn];
       const int M = n * O.smid.h * O.smid.w;
       XP_TRY(check_launch(c, launch_bn_stats(mid, M, O.smid.c, N.d.bn_eps, W + N.woff, W + N.boff, s.bnws,
-                                             s.stats[o][slot], s.stream), "bn_stats"));
+                                             s.ctr + kTileCounters - 2, s.stats[o][slot], s.stream), "bn_stats"));
       const PoolGeo p = pool_geo(c, O.lpool);
       uint8_t* pidx = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
       return check_launch(c, launch_bn_apply(mid, s.stats[o][slot], (bf16*)y, pidx, n, O.smid.h, O.smid.w, O.smid.c,
@@ -109,7 +109,7 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
                                                 O.lpool >= 0 ? s.pidx[o][slot] : nullptr, s.stats[o][slot],
                                                 W + N.woff, n, O.smid.h, O.smid.w, O.smid.c, O.sout.h, O.sout.w, p.kh,
                                                 p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws,
-                                                s.g + N.woff, s.g + N.boff, accumulate_g, dmid, s.stream),
+                                                s.ctr + kTileCounters - 1, s.g + N.woff, s.g + N.boff, accumulate_g, dmid, s.stream),
                           "bn_backward"));
       XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)s.act[O.in0][slot], dmid, s.g + L.woff, accumulate_g, s.ws,

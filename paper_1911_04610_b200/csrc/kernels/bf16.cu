@@ -8,6 +8,7 @@
 // is bf16 (round-to-nearest-even); statistics, logits and parameter gradients are fp32.
 // All reductions are deterministic (fixed order, no atomics).
 #include "../internal.h"
+#include "launch.h"
 #include "bf16_kernels.h"
 
 namespace xp {
@@ -29,6 +30,7 @@ __device__ __forceinline__ float bn_act(float x, float mean, float rstd, float g
 // ---- K11 ---------------------------------------------------------------------------------
 __global__ void stage_input_bf16_kernel(const float* __restrict__ x, bf16* __restrict__ y, int n, int C, int H, int W,
                                         int Cp) {
+  pdl_wait();
   const int64_t total = (int64_t)n * H * W * Cp;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % Cp);
@@ -42,10 +44,26 @@ __global__ void stage_input_bf16_kernel(const float* __restrict__ x, bf16* __res
   }
 }
 
+__device__ __forceinline__ void chan_merge(float& na, float& mean, float& m2, float nb, float mb, float m2b) {
+  if (nb == 0.f) return;
+  if (na == 0.f) { na = nb; mean = mb; m2 = m2b; return; }
+  const float nab = na + nb;
+  const float d = mb - mean;
+  mean += d * (nb / nab);
+  m2 += m2b + d * d * (na * nb / nab);
+  na = nab;
+}
+
 // ---- BN statistics: x [M][C] bf16 -> partial (mean, M2) per row chunk ----------------------
 // block: G = C/8 channel groups x RL = 256/G row lanes; chunk = RC rows; thread keeps
 // Welford (n, mean, M2) for 8 channels; lanes merged in fixed order through smem.
-__global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C, int RC, float* __restrict__ part) {
+__device__ void bn_stats_merge(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
+                               const bf16* __restrict__ gamma, const bf16* __restrict__ beta, float* __restrict__ stats);
+
+__global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C, int RC, float* __restrict__ part,
+                                        int* __restrict__ counter, float eps, const bf16* __restrict__ gamma,
+                                        const bf16* __restrict__ beta, float* __restrict__ stats) {
+  pdl_wait();
   extern __shared__ float sh[];  // [RL][G][16] (mean[8], M2[8]) + counts
   const int G = C / 8, RL = blockDim.x / G;
   const int g = threadIdx.x % G, rl = threadIdx.x / G;
@@ -96,42 +114,45 @@ __global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C
 #pragma unroll
     for (int e = 0; e < 8; ++e) { p[g * 8 + e] = mean[e]; p[C + g * 8 + e] = m2[e]; }
   }
-}
-
-// merge the chunk partials in chunk order -> stats[0..C) mean, [C..2C) rstd, [2C..3C) gamma_f,
-// [3C..4C) beta_f (the forward's affine parameters).  One warp per channel: lane l merges
-// chunks l, l+32, ... in order, then the 32 lane results merge in a fixed butterfly order.
-__device__ __forceinline__ void chan_merge(float& na, float& mean, float& m2, float nb, float mb, float m2b) {
-  if (nb == 0.f) return;
-  if (na == 0.f) { na = nb; mean = mb; m2 = m2b; return; }
-  const float nab = na + nb;
-  const float d = mb - mean;
-  mean += d * (nb / nab);
-  m2 += m2b + d * d * (na * nb / nab);
-  na = nab;
-}
-
-__global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
-                                      const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
-                                      float* __restrict__ stats) {
-  const int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (c >= C) return;
-  float na = 0.f, mean = 0.f, m2 = 0.f;
-  for (int k = lane; k < chunks; k += 32)
-    chan_merge(na, mean, m2, (float)min(RC, M - k * RC), part[(size_t)k * 2 * C + c], part[(size_t)k * 2 * C + C + c]);
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const float nb = __shfl_xor_sync(0xffffffffu, na, off), mb = __shfl_xor_sync(0xffffffffu, mean, off),
-                m2b = __shfl_xor_sync(0xffffffffu, m2, off);
-    // fixed order: the lower lane of each pair absorbs the upper one; both end with the same value
-    if ((lane & off) == 0) chan_merge(na, mean, m2, nb, mb, m2b);
-    else { float a = nb, b = mb, q = m2b; chan_merge(a, b, q, na, mean, m2); na = a; mean = b; m2 = q; }
+  // the last block to finish merges all chunks (fixed order) -- no separate final launch
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(counter, 1);
+    last = (old == (int)gridDim.x - 1);
+    if (last) *counter = 0;
   }
-  if (lane == 0) {
-    stats[c] = mean;
-    stats[C + c] = 1.f / sqrtf(m2 / na + eps);
-    stats[2 * C + c] = __bfloat162float(gamma[c]);
-    stats[3 * C + c] = __bfloat162float(beta[c]);
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    bn_stats_merge(part, gridDim.x, M, RC, C, eps, gamma, beta, stats);
+  }
+}
+
+// warp w of the block merges channels w, w+nwarps, ...: lane l takes chunks l, l+32, ... in
+// order, then the lanes merge in a fixed butterfly order (deterministic)
+__device__ void bn_stats_merge(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
+                               const bf16* __restrict__ gamma, const bf16* __restrict__ beta, float* __restrict__ stats) {
+  const int nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int c = threadIdx.x >> 5; c < C; c += nw) {
+    float na = 0.f, mean = 0.f, m2 = 0.f;
+    for (int k = lane; k < chunks; k += 32)
+      chan_merge(na, mean, m2, (float)min(RC, M - k * RC), __ldcg(part + (size_t)k * 2 * C + c),
+                 __ldcg(part + (size_t)k * 2 * C + C + c));
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float nb = __shfl_xor_sync(0xffffffffu, na, off), mb = __shfl_xor_sync(0xffffffffu, mean, off),
+                  m2b = __shfl_xor_sync(0xffffffffu, m2, off);
+      if ((lane & off) == 0) chan_merge(na, mean, m2, nb, mb, m2b);
+      else { float a = nb, b = mb, q = m2b; chan_merge(a, b, q, na, mean, m2); na = a; mean = b; m2 = q; }
+    }
+    if (lane == 0) {
+      stats[c] = mean;
+      stats[C + c] = 1.f / sqrtf(m2 / na + eps);
+      stats[2 * C + c] = __bfloat162float(gamma[c]);
+      stats[3 * C + c] = __bfloat162float(beta[c]);
+    }
   }
 }
 
@@ -141,6 +162,7 @@ __global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks
 __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restrict__ st, bf16* __restrict__ y,
                                 uint8_t* __restrict__ pidx, int n, int H, int W, int C, int P, int Q, int kh, int kw,
                                 int sh, int sw, int ph, int pw, int pool, int relu) {
+  pdl_wait();
   const int G = C / 8;
   const int64_t total = (int64_t)n * P * Q * G;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -247,9 +269,15 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
 
 // per chunk of RC rows: sum dy and sum dy*xhat per channel (8 channels per thread, row lanes
 // merged in fixed order) -> part[chunk][2][C]
+__device__ void bn_bwd_merge(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
+                             float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate);
+
 __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
                                      const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
-                                     const float* __restrict__ st, BwdGeo G, int M, int RC, float* __restrict__ part) {
+                                     const float* __restrict__ st, BwdGeo G, int M, int RC, float* __restrict__ part,
+                                     int* __restrict__ counter, float* __restrict__ tot, float* __restrict__ g_gamma,
+                                     float* __restrict__ g_beta, int accumulate) {
+  pdl_wait();
   extern __shared__ float sh[];
   const int C = G.C, NG = C / 8, RL = blockDim.x / NG;
   const int g = threadIdx.x % NG, rl = threadIdx.x / NG;
@@ -287,28 +315,42 @@ __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __r
 #pragma unroll
     for (int e = 0; e < 8; ++e) { p[c0 + e] = s1[e]; p[C + c0 + e] = s2[e]; }
   }
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(counter, 1);
+    last = (old == (int)gridDim.x - 1);
+    if (last) *counter = 0;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    bn_bwd_merge(part, gridDim.x, C, tot, g_gamma, g_beta, accumulate);
+  }
 }
 
 // totals over chunks (warp per channel, fixed order); dgamma/dbeta into the accumulator
-__global__ void bn_bwd_final_kernel(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
-                                    float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate) {
-  const int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (c >= C) return;
-  float s1 = 0.f, s2 = 0.f;
-  for (int k = lane; k < chunks; k += 32) {
-    s1 = __fadd_rn(s1, part[(size_t)k * 2 * C + c]);
-    s2 = __fadd_rn(s2, part[(size_t)k * 2 * C + C + c]);
-  }
+__device__ void bn_bwd_merge(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
+                             float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate) {
+  const int nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int c = threadIdx.x >> 5; c < C; c += nw) {
+    float s1 = 0.f, s2 = 0.f;
+    for (int k = lane; k < chunks; k += 32) {
+      s1 = __fadd_rn(s1, __ldcg(part + (size_t)k * 2 * C + c));
+      s2 = __fadd_rn(s2, __ldcg(part + (size_t)k * 2 * C + C + c));
+    }
 #pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    s1 = __fadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, off));
-    s2 = __fadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, off));
-  }
-  if (lane == 0) {
-    tot[c] = s1;
-    tot[C + c] = s2;
-    g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
-    g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
+    for (int off = 16; off; off >>= 1) {
+      s1 = __fadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, off));
+      s2 = __fadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, off));
+    }
+    if (lane == 0) {
+      tot[c] = s1;
+      tot[C + c] = s2;
+      g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
+      g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
+    }
   }
 }
 
@@ -317,6 +359,7 @@ __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __re
                                     const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
                                     const float* __restrict__ st, const float* __restrict__ tot,
                                     const bf16* __restrict__ gamma_b, BwdGeo G, int M, bf16* __restrict__ dx) {
+  pdl_wait();
   const int C = G.C, NG = C / 8;
   const float inv_cnt = 1.f / (float)M;
   const int64_t total = (int64_t)M * NG;
@@ -355,6 +398,7 @@ __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __re
 __global__ void linear_fwd_bf16_kernel(const bf16* __restrict__ x, const bf16* __restrict__ W,
                                        const bf16* __restrict__ b, void* __restrict__ y, int n, int in, int out,
                                        int relu, int f32out) {
+  pdl_wait();
   const int wid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (wid >= n * out) return;
   const int r = wid / out, o = wid % out;
@@ -383,6 +427,7 @@ __device__ __forceinline__ float load_dy(const void* dy, int64_t idx, const bf16
 template <bool DY_F32>
 __global__ void linear_dgrad_bf16_kernel(const void* __restrict__ dy, const bf16* __restrict__ mask,
                                          const bf16* __restrict__ W, bf16* __restrict__ dx, int n, int in, int out) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
   if (i >= in || r >= n) return;
   float acc = 0.f;
@@ -395,6 +440,7 @@ template <bool DY_F32>
 __global__ void linear_wgrad_bf16_kernel(const void* __restrict__ dy, const bf16* __restrict__ mask,
                                          const bf16* __restrict__ x, float* __restrict__ gW, float* __restrict__ gb,
                                          int n, int in, int out, int accumulate) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int o = blockIdx.y;
   if (i > in || (i == in && !gb)) return;
@@ -415,7 +461,7 @@ int grid1d(int64_t n, int threads = 256) {
 }  // namespace
 
 cudaError_t launch_stage_input_bf16(const float* x, bf16* y, int n, int C, int H, int W, int Cp, cudaStream_t st) {
-  stage_input_bf16_kernel<<<grid1d((int64_t)n * H * W * Cp), 256, 0, st>>>(x, y, n, C, H, W, Cp);
+  launch_pdl(stage_input_bf16_kernel, dim3(grid1d((int64_t)n * H * W * Cp)), dim3(256), 0, st, x, y, n, C, H, W, Cp);
   return cudaGetLastError();
 }
 
@@ -424,29 +470,28 @@ int bn_chunks(int M) { return (M + bn_chunk_rows(M) - 1) / bn_chunk_rows(M); }
 size_t bn_ws_floats(int M, int C) { return (size_t)bn_chunks(M) * 2 * C + 2 * (size_t)C; }
 
 cudaError_t launch_bn_stats(const bf16* x, int M, int C, float eps, const bf16* gamma, const bf16* beta, float* ws,
-                            float* stats, cudaStream_t st) {
+                            int* counter, float* stats, cudaStream_t st) {
   if (C % 8 || C > 2048) return cudaErrorInvalidValue;
   const int RC = bn_chunk_rows(M), chunks = bn_chunks(M);
   const int G = C / 8;
   const int threads = G >= 256 ? G : (256 / G) * G;
   const size_t shm = (size_t)(threads / G) * G * 17 * 4;
-  bn_stats_partial_kernel<<<chunks, threads, shm, st>>>(x, M, C, RC, ws);
-  bn_stats_final_kernel<<<(C + 7) / 8, 256, 0, st>>>(ws, chunks, M, RC, C, eps, gamma, beta, stats);
+  launch_pdl(bn_stats_partial_kernel, dim3(chunks), dim3(threads), shm, st, x, M, C, RC, ws, counter, eps, gamma, beta, stats);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, uint8_t* pidx, int n, int H, int W, int C, int P,
                             int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st) {
   const int64_t total = (int64_t)n * P * Q * (C / 8);
-  bn_apply_kernel<<<grid1d(total), 256, 0, st>>>(x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
+  launch_pdl(bn_apply_kernel, dim3(grid1d(total)), dim3(256), 0, st, x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
                                                  pool ? 1 : 0, relu ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bn_backward(const bf16* x, const bf16* dout, const bf16* y, const uint8_t* pidx, const float* stats,
                                const bf16* gamma_b, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
-                               int sw, int ph, int pw, bool pool, bool relu, float* ws, float* g_gamma, float* g_beta,
-                               bool accumulate, bf16* dx, cudaStream_t st) {
+                               int sw, int ph, int pw, bool pool, bool relu, float* ws, int* counter, float* g_gamma,
+                               float* g_beta, bool accumulate, bf16* dx, cudaStream_t st) {
   if (C % 8 || C > 2048) return cudaErrorInvalidValue;
   BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
   const int M = n * H * W;
@@ -454,32 +499,32 @@ cudaError_t launch_bn_backward(const bf16* x, const bf16* dout, const bf16* y, c
   const int NG = C / 8;
   const int threads = NG >= 256 ? NG : (256 / NG) * NG;
   const size_t shm = (size_t)threads * 16 * 4;
-  bn_bwd_reduce_kernel<<<chunks, threads, shm, st>>>(x, dout, y, pidx, stats, G, M, RC, ws);
   float* tot = ws + (size_t)chunks * 2 * C;
-  bn_bwd_final_kernel<<<(C + 7) / 8, 256, 0, st>>>(ws, chunks, C, tot, g_gamma, g_beta, accumulate ? 1 : 0);
-  bn_bwd_apply_kernel<<<grid1d((int64_t)M * NG), 256, 0, st>>>(x, dout, y, pidx, stats, tot, gamma_b, G, M, dx);
+  launch_pdl(bn_bwd_reduce_kernel, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC, ws, counter, tot, g_gamma,
+                                                     g_beta, accumulate ? 1 : 0);
+  launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * NG)), dim3(256), 0, st, x, dout, y, pidx, stats, tot, gamma_b, G, M, dx);
   return cudaGetLastError();
 }
 
 cudaError_t launch_linear_fwd_bf16(const bf16* x, const bf16* W, const bf16* b, void* y, int n, int in, int out,
                                    bool relu, bool f32out, cudaStream_t st) {
-  linear_fwd_bf16_kernel<<<(n * out + 7) / 8, 256, 0, st>>>(x, W, b, y, n, in, out, relu ? 1 : 0, f32out ? 1 : 0);
+  launch_pdl(linear_fwd_bf16_kernel, dim3((n * out + 7) / 8), dim3(256), 0, st, x, W, b, y, n, in, out, relu ? 1 : 0, f32out ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_linear_dgrad_bf16(const void* dy, bool dy_f32, const bf16* mask, const bf16* W, bf16* dx, int n,
                                      int in, int out, cudaStream_t st) {
   dim3 grid((in + 127) / 128, n);
-  if (dy_f32) linear_dgrad_bf16_kernel<true><<<grid, 128, 0, st>>>(dy, mask, W, dx, n, in, out);
-  else linear_dgrad_bf16_kernel<false><<<grid, 128, 0, st>>>(dy, mask, W, dx, n, in, out);
+  if (dy_f32) launch_pdl(linear_dgrad_bf16_kernel<true>, dim3(grid), dim3(128), 0, st, dy, mask, W, dx, n, in, out);
+  else launch_pdl(linear_dgrad_bf16_kernel<false>, dim3(grid), dim3(128), 0, st, dy, mask, W, dx, n, in, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_linear_wgrad_bf16(const void* dy, bool dy_f32, const bf16* mask, const bf16* x, float* gW, float* gb,
                                      int n, int in, int out, bool accumulate, cudaStream_t st) {
   dim3 grid((in + 1 + 127) / 128, out);
-  if (dy_f32) linear_wgrad_bf16_kernel<true><<<grid, 128, 0, st>>>(dy, mask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
-  else linear_wgrad_bf16_kernel<false><<<grid, 128, 0, st>>>(dy, mask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
+  if (dy_f32) launch_pdl(linear_wgrad_bf16_kernel<true>, dim3(grid), dim3(128), 0, st, dy, mask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
+  else launch_pdl(linear_wgrad_bf16_kernel<false>, dim3(grid), dim3(128), 0, st, dy, mask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -504,6 +549,7 @@ int g1(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255)
 
 // y = Q(relu?(a + b)) elementwise over n elements
 __global__ void add_fwd_kernel(const bf16* a, const bf16* b, bf16* y, int64_t n, int relu) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float v = q16b(__fadd_rn(__bfloat162float(a[i]), __bfloat162float(b[i])));
     if (relu) v = v > 0.f ? v : 0.f;
@@ -513,6 +559,7 @@ __global__ void add_fwd_kernel(const bf16* a, const bf16* b, bf16* y, int64_t n,
 // da (=|+=) dy', db (=|+=) dy' with dy' = (relu && !(y > 0)) ? 0 : dy
 __global__ void add_bwd_kernel(const bf16* dy, const bf16* y, bf16* da, bf16* db, int64_t n, int relu, int acc_a,
                                int acc_b) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float g = __bfloat162float(dy[i]);
     if (relu && !(__bfloat162float(y[i]) > 0.f)) g = 0.f;
@@ -522,6 +569,7 @@ __global__ void add_bwd_kernel(const bf16* dy, const bf16* y, bf16* da, bf16* db
 }
 // y[r][0:Ca] = a[r], y[r][Ca:Ca+Cb] = b[r]   (r = pixel)
 __global__ void concat_fwd_kernel(const bf16* a, const bf16* b, bf16* y, int64_t rows, int Ca, int Cb) {
+  pdl_wait();
   const int C = Ca + Cb;
   const int64_t n = rows * C;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -532,6 +580,7 @@ __global__ void concat_fwd_kernel(const bf16* a, const bf16* b, bf16* y, int64_t
 }
 __global__ void concat_bwd_kernel(const bf16* dy, bf16* da, bf16* db, int64_t rows, int Ca, int Cb, int acc_a,
                                   int acc_b) {
+  pdl_wait();
   const int C = Ca + Cb;
   const int64_t n = rows * C;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -545,6 +594,7 @@ __global__ void concat_bwd_kernel(const bf16* dy, bf16* da, bf16* db, int64_t ro
 // pooling forward: mode 0 max (first max, padded positions skipped), 1 avg (count_include_pad)
 __global__ void pool_fwd_kernel(const bf16* x, bf16* y, int n, int H, int W, int C, int P, int Q, int kh, int kw,
                                 int sh, int sw, int ph, int pw, int mode) {
+  pdl_wait();
   const int64_t total = (int64_t)n * P * Q * C;
   const float inv = 1.f / (float)(kh * kw);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -571,6 +621,7 @@ __global__ void pool_fwd_kernel(const bf16* x, bf16* y, int n, int H, int W, int
 // covering it contributes g*inv), then store/accumulate
 __global__ void pool_bwd_kernel(const bf16* x, const bf16* dy, bf16* dx, int n, int H, int W, int C, int P, int Q,
                                 int kh, int kw, int sh, int sw, int ph, int pw, int mode, int accumulate) {
+  pdl_wait();
   const int64_t total = (int64_t)n * H * W * C;
   const float inv = 1.f / (float)(kh * kw);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -610,6 +661,7 @@ __global__ void pool_bwd_kernel(const bf16* x, const bf16* dy, bf16* dx, int n, 
 }
 // global average pool: y[s][c] = (sum over H*W in raster order) * (1/(H*W))
 __global__ void gap_fwd_kernel(const bf16* x, bf16* y, int n, int HW, int C) {
+  pdl_wait();
   const int64_t total = (int64_t)n * C;
   const float inv = 1.f / (float)HW;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -621,6 +673,7 @@ __global__ void gap_fwd_kernel(const bf16* x, bf16* y, int n, int HW, int C) {
   }
 }
 __global__ void gap_bwd_kernel(const bf16* dy, bf16* dx, int n, int HW, int C, int accumulate) {
+  pdl_wait();
   const int64_t total = (int64_t)n * HW * C;
   const float inv = 1.f / (float)HW;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -632,40 +685,40 @@ __global__ void gap_bwd_kernel(const bf16* dy, bf16* dx, int n, int HW, int C, i
 }  // namespace
 
 cudaError_t launch_add_fwd(const bf16* a, const bf16* b, bf16* y, int64_t n, bool relu, cudaStream_t st) {
-  add_fwd_kernel<<<g1(n), 256, 0, st>>>(a, b, y, n, relu ? 1 : 0);
+  launch_pdl(add_fwd_kernel, dim3(g1(n)), dim3(256), 0, st, a, b, y, n, relu ? 1 : 0);
   return cudaGetLastError();
 }
 cudaError_t launch_add_bwd(const bf16* dy, const bf16* y, bf16* da, bf16* db, int64_t n, bool relu, bool acc_a,
                            bool acc_b, cudaStream_t st) {
-  add_bwd_kernel<<<g1(n), 256, 0, st>>>(dy, y, da, db, n, relu ? 1 : 0, acc_a ? 1 : 0, acc_b ? 1 : 0);
+  launch_pdl(add_bwd_kernel, dim3(g1(n)), dim3(256), 0, st, dy, y, da, db, n, relu ? 1 : 0, acc_a ? 1 : 0, acc_b ? 1 : 0);
   return cudaGetLastError();
 }
 cudaError_t launch_concat_fwd(const bf16* a, const bf16* b, bf16* y, int64_t rows, int Ca, int Cb, cudaStream_t st) {
-  concat_fwd_kernel<<<g1(rows * (Ca + Cb)), 256, 0, st>>>(a, b, y, rows, Ca, Cb);
+  launch_pdl(concat_fwd_kernel, dim3(g1(rows * (Ca + Cb))), dim3(256), 0, st, a, b, y, rows, Ca, Cb);
   return cudaGetLastError();
 }
 cudaError_t launch_concat_bwd(const bf16* dy, bf16* da, bf16* db, int64_t rows, int Ca, int Cb, bool acc_a, bool acc_b,
                               cudaStream_t st) {
-  concat_bwd_kernel<<<g1(rows * (Ca + Cb)), 256, 0, st>>>(dy, da, db, rows, Ca, Cb, acc_a ? 1 : 0, acc_b ? 1 : 0);
+  launch_pdl(concat_bwd_kernel, dim3(g1(rows * (Ca + Cb))), dim3(256), 0, st, dy, da, db, rows, Ca, Cb, acc_a ? 1 : 0, acc_b ? 1 : 0);
   return cudaGetLastError();
 }
 cudaError_t launch_pool_fwd(const bf16* x, bf16* y, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
                             int sw, int ph, int pw, bool avg, cudaStream_t st) {
-  pool_fwd_kernel<<<g1((int64_t)n * P * Q * C), 256, 0, st>>>(x, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, avg ? 1 : 0);
+  launch_pdl(pool_fwd_kernel, dim3(g1((int64_t)n * P * Q * C)), dim3(256), 0, st, x, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, avg ? 1 : 0);
   return cudaGetLastError();
 }
 cudaError_t launch_pool_bwd(const bf16* x, const bf16* dy, bf16* dx, int n, int H, int W, int C, int P, int Q, int kh,
                             int kw, int sh, int sw, int ph, int pw, bool avg, bool accumulate, cudaStream_t st) {
-  pool_bwd_kernel<<<g1((int64_t)n * H * W * C), 256, 0, st>>>(x, dy, dx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
+  launch_pdl(pool_bwd_kernel, dim3(g1((int64_t)n * H * W * C)), dim3(256), 0, st, x, dy, dx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
                                                               avg ? 1 : 0, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 cudaError_t launch_gap_fwd(const bf16* x, bf16* y, int n, int HW, int C, cudaStream_t st) {
-  gap_fwd_kernel<<<g1((int64_t)n * C), 256, 0, st>>>(x, y, n, HW, C);
+  launch_pdl(gap_fwd_kernel, dim3(g1((int64_t)n * C)), dim3(256), 0, st, x, y, n, HW, C);
   return cudaGetLastError();
 }
 cudaError_t launch_gap_bwd(const bf16* dy, bf16* dx, int n, int HW, int C, bool accumulate, cudaStream_t st) {
-  gap_bwd_kernel<<<g1((int64_t)n * HW * C), 256, 0, st>>>(dy, dx, n, HW, C, accumulate ? 1 : 0);
+  launch_pdl(gap_bwd_kernel, dim3(g1((int64_t)n * HW * C)), dim3(256), 0, st, dy, dx, n, HW, C, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -8,8 +8,9 @@ namespace xp {
 int bn_chunks(int M);
 size_t bn_ws_floats(int M, int C);
 // stats [4][C]: mean, rstd, gamma_f, beta_f (the forward's affine parameters)
+// counter: one zero-initialised int owned by the calling stream (last-block merge)
 cudaError_t launch_bn_stats(const __nv_bfloat16* x, int M, int C, float eps, const __nv_bfloat16* gamma,
-                            const __nv_bfloat16* beta, float* ws, float* stats, cudaStream_t st);
+                            const __nv_bfloat16* beta, float* ws, int* counter, float* stats, cudaStream_t st);
 // pool: pidx receives the winner's position in every window (uint8 per pooled element)
 cudaError_t launch_bn_apply(const __nv_bfloat16* x, const float* stats, __nv_bfloat16* y, uint8_t* pidx, int n, int H,
                             int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,
@@ -19,7 +20,7 @@ cudaError_t launch_bn_apply(const __nv_bfloat16* x, const float* stats, __nv_bfl
 cudaError_t launch_bn_backward(const __nv_bfloat16* x, const __nv_bfloat16* dout, const __nv_bfloat16* y,
                                const uint8_t* pidx, const float* stats, const __nv_bfloat16* gamma_b, int n, int H,
                                int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,
-                               bool relu, float* ws, float* g_gamma, float* g_beta, bool accumulate,
+                               bool relu, float* ws, int* counter, float* g_gamma, float* g_beta, bool accumulate,
                                __nv_bfloat16* dx, cudaStream_t st);
 cudaError_t launch_linear_fwd_bf16(const __nv_bfloat16* x, const __nv_bfloat16* W, const __nv_bfloat16* b, void* y,
                                    int n, int in, int out, bool relu, bool f32out, cudaStream_t st);

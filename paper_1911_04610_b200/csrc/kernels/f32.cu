@@ -9,6 +9,7 @@
 // Tiles are staged through shared memory only to coalesce global loads; the per-output
 // reduction order is untouched.
 #include "../internal.h"
+#include "launch.h"
 
 namespace xp {
 
@@ -23,6 +24,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // K12: trace record at op start.  The version comes from the device counter (the sweep's
 // bump kernel increments it), the bellwether latches it for the other T-1 micro-batches.
 __global__ void trace_begin_kernel(DevState* ds, TraceRec* rec, int stage, int op, int t, int j, int s, int bw) {
+  pdl_wait();
   int ver;
   if (op == 0) { if (bw) ds->fver = ds->ver; ver = ds->fver; }
   else { if (bw) ds->bver = ds->ver; ver = ds->bver; }
@@ -32,14 +34,17 @@ __global__ void trace_begin_kernel(DevState* ds, TraceRec* rec, int stage, int o
   rec->t1_ns = 0;
 }
 
-__global__ void trace_end_kernel(TraceRec* rec) { rec->t1_ns = globaltimer(); }
+__global__ void trace_end_kernel(TraceRec* rec) {
+  pdl_wait(); rec->t1_ns = globaltimer(); }
 
 // ring flags hold micro-batch indices relative to a base; rebasing subtracts delta (mod 2^32)
 __global__ void rebase_flags_kernel(uint32_t* f, int n, uint32_t delta) {
+  pdl_wait();
   if (threadIdx.x < n) f[threadIdx.x] -= delta;
 }
 
 __global__ void copy_kernel(const float* __restrict__ s, float* __restrict__ d, int64_t n) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d[i] = s[i];
 }
@@ -53,6 +58,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 
 // counter-based U(-bound, bound): value i of stream (seed, id) -- no state, any launch shape
 __global__ void fill_uniform_kernel(float* d, int64_t n, float bound, uint64_t seed, uint64_t id) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t r = splitmix64(seed * 0x632be59bd9b4e019ull ^ splitmix64(id * 0x100000001b3ull + (uint64_t)i));
     double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);  // [0,1)
@@ -61,6 +67,7 @@ __global__ void fill_uniform_kernel(float* d, int64_t n, float bound, uint64_t s
 }
 
 __global__ void fill_const_kernel(float* d, int64_t n, float v) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d[i] = v;
 }
@@ -70,6 +77,7 @@ __global__ void fill_const_kernel(float* d, int64_t n, float v) {
 __global__ void __launch_bounds__(256) linear_fwd_f32_kernel(const float* __restrict__ x, const float* __restrict__ W,
                                                              const float* __restrict__ b, float* __restrict__ y, int n,
                                                              int in, int out, int relu) {
+  pdl_wait();
   __shared__ float Ws[32][33];
   __shared__ float xs[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -101,6 +109,7 @@ __global__ void __launch_bounds__(256) linear_dgrad_f32_kernel(const float* __re
                                                                const float* __restrict__ ymask,
                                                                const float* __restrict__ W, float* __restrict__ dx,
                                                                int n, int in, int out) {
+  pdl_wait();
   __shared__ float Ws[32][33];
   __shared__ float ds[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -134,6 +143,7 @@ __global__ void __launch_bounds__(256) linear_wgrad_f32_kernel(const float* __re
                                                                const float* __restrict__ x, float* __restrict__ gW,
                                                                float* __restrict__ gb, int n, int in, int out,
                                                                int accumulate) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;  // i in [0, in] (in = bias column)
   const int o = blockIdx.y;
   if (i > in || (i == in && !gb)) return;
@@ -153,6 +163,7 @@ __global__ void __launch_bounds__(256) linear_wgrad_f32_kernel(const float* __re
 // dz = (p - onehot) * invN; loss row = -log(e_y/s) (reporting only)
 __global__ void xent_f32_kernel(const float* __restrict__ z, const int32_t* __restrict__ y, float* __restrict__ dz,
                                 float* __restrict__ loss, int n, int C, float invN) {
+  pdl_wait();
   __shared__ double lsum[256];
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   double l = 0.0;
@@ -190,60 +201,60 @@ int grid_for(int64_t n, int threads = 256) {
 
 cudaError_t launch_trace_begin(DevState* ds, TraceRec* rec, int stage, int op, int t, int j, int s, int bw,
                                cudaStream_t st) {
-  trace_begin_kernel<<<1, 1, 0, st>>>(ds, rec, stage, op, t, j, s, bw);
+  launch_pdl(trace_begin_kernel, dim3(1), dim3(1), 0, st, ds, rec, stage, op, t, j, s, bw);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rebase_flags(uint32_t* flags, int n, uint32_t delta, cudaStream_t st) {
-  rebase_flags_kernel<<<1, 32, 0, st>>>(flags, n, delta);
+  launch_pdl(rebase_flags_kernel, dim3(1), dim3(32), 0, st, flags, n, delta);
   return cudaGetLastError();
 }
 
 cudaError_t launch_trace_end(TraceRec* rec, cudaStream_t st) {
-  trace_end_kernel<<<1, 1, 0, st>>>(rec);
+  launch_pdl(trace_end_kernel, dim3(1), dim3(1), 0, st, rec);
   return cudaGetLastError();
 }
 
 cudaError_t launch_copy_f32(const float* src, float* dst, int64_t n, cudaStream_t st) {
-  copy_kernel<<<grid_for(n), 256, 0, st>>>(src, dst, n);
+  launch_pdl(copy_kernel, dim3(grid_for(n)), dim3(256), 0, st, src, dst, n);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fill_uniform(float* dst, int64_t n, float bound, uint64_t seed, uint64_t id, cudaStream_t st) {
-  fill_uniform_kernel<<<grid_for(n), 256, 0, st>>>(dst, n, bound, seed, id);
+  launch_pdl(fill_uniform_kernel, dim3(grid_for(n)), dim3(256), 0, st, dst, n, bound, seed, id);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fill_const(float* dst, int64_t n, float value, cudaStream_t st) {
-  fill_const_kernel<<<grid_for(n), 256, 0, st>>>(dst, n, value);
+  launch_pdl(fill_const_kernel, dim3(grid_for(n)), dim3(256), 0, st, dst, n, value);
   return cudaGetLastError();
 }
 
 cudaError_t launch_linear_fwd_f32(const float* x, const float* W, const float* b, float* y, int n, int in, int out,
                                   bool relu, cudaStream_t st) {
   dim3 grid((out + 31) / 32, (n + 7) / 8);
-  linear_fwd_f32_kernel<<<grid, 256, 0, st>>>(x, W, b, y, n, in, out, relu ? 1 : 0);
+  launch_pdl(linear_fwd_f32_kernel, dim3(grid), dim3(256), 0, st, x, W, b, y, n, in, out, relu ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_linear_dgrad_f32(const float* dy, const float* ymask, const float* W, float* dx, int n, int in,
                                     int out, cudaStream_t st) {
   dim3 grid((in + 31) / 32, (n + 7) / 8);
-  linear_dgrad_f32_kernel<<<grid, 256, 0, st>>>(dy, ymask, W, dx, n, in, out);
+  launch_pdl(linear_dgrad_f32_kernel, dim3(grid), dim3(256), 0, st, dy, ymask, W, dx, n, in, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_linear_wgrad_f32(const float* dy, const float* ymask, const float* x, float* gW, float* gb, int n,
                                     int in, int out, bool accumulate, cudaStream_t st) {
   dim3 grid((in + 1 + 127) / 128, out);
-  linear_wgrad_f32_kernel<<<grid, 128, 0, st>>>(dy, ymask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
+  launch_pdl(linear_wgrad_f32_kernel, dim3(grid), dim3(128), 0, st, dy, ymask, x, gW, gb, n, in, out, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_xent_f32(const float* z, const int32_t* y, float* dz, float* loss, int n, int classes, float invN,
                             cudaStream_t st) {
   if (n > 256) return cudaErrorInvalidValue;
-  xent_f32_kernel<<<1, 256, 0, st>>>(z, y, dz, loss, n, classes, invN);
+  launch_pdl(xent_f32_kernel, dim3(1), dim3(256), 0, st, z, y, dz, loss, n, classes, invN);
   return cudaGetLastError();
 }
 

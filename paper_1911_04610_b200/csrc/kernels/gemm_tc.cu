@@ -18,6 +18,7 @@
 
 #include "../../../include/xpipe.h"
 #include "../internal.h"
+#include "launch.h"
 #include "gemm_tc.h"
 
 namespace xp {
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp < 4) {
     producer<MODE, BN, A_MN, B_MN>(a, base, full0, empty0, m0, n0, kb0, nkb, tid);
@@ -409,6 +411,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) 
         umma_commit(empty0 + 8 * s);
       }
       umma_commit(accum);
+      pdl_trigger();
     }
     __syncwarp();
     mbar_wait(accum, 0);
@@ -473,53 +476,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) 
   }
 }
 
-// split-K reductions in fixed order z = 0..splits-1 (all loads of an element issued first)
-__device__ __forceinline__ float sum_splits(const float* ws, int splits, int64_t stride, int64_t i) {
-  float v[8];
-  float acc = 0.f;
-  for (int z0 = 0; z0 < splits; z0 += 8) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = (z0 + q < splits) ? ws[(int64_t)(z0 + q) * stride + i] : 0.f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (z0 + q < splits) acc = (z0 + q == 0) ? v[q] : __fadd_rn(acc, v[q]);
-  }
-  return acc;
-}
-
-__global__ void reduce_bf16_kernel(const float* ws, int splits, int64_t stride, int M, int N, bf16* out, int64_t ldo,
-                                   int accumulate) {
-  const int64_t total = (int64_t)M * N;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const float acc = sum_splits(ws, splits, stride, i);
-    bf16* o = out + (i / N) * ldo + (i % N);
-    if (accumulate) {
-      const float g = __bfloat162float(__float2bfloat16_rn(acc));
-      *o = __float2bfloat16_rn(__fadd_rn(__bfloat162float(*o), g));
-    } else {
-      *o = __float2bfloat16_rn(acc);
-    }
-  }
-}
-
-// g[n][m] (=|+=) sum_z ws[z][m][n]  via a 32x32 shared-memory transpose, one element per thread
-__global__ void reduce_wgrad_t_kernel(const float* ws, int splits, int64_t stride, int M, int N, float* g, int64_t ldo,
-                                      int accumulate) {
-  __shared__ float tile[32][33];
-  const int m0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 32
-  {
-    const int m = m0 + ty, n = n0 + tx;
-    tile[ty][tx] = (m < M && n < N) ? sum_splits(ws, splits, stride, (int64_t)m * N + n) : 0.f;
-  }
-  __syncthreads();
-  const int n = n0 + ty, m = m0 + tx;
-  if (m < M && n < N) {
-    float* p = g + (int64_t)n * ldo + m;
-    *p = accumulate ? __fadd_rn(*p, tile[tx][ty]) : tile[tx][ty];
-  }
-}
-
 template <int MODE, int BN, bool A_MN, bool B_MN>
 cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   constexpr int SMEM = Depth<BN>::ST * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
@@ -531,7 +487,7 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     attr = true;
   }
   dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, splits);
-  tc_gemm_kernel<MODE, BN, A_MN, B_MN><<<grid, NTHREADS, SMEM, st>>>(a);
+  launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, dim3(grid), dim3(NTHREADS), SMEM, st, a);
   return cudaGetLastError();
 }
 
@@ -591,7 +547,7 @@ cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_
   a.kb_per_split = (nkb + splits - 1) / splits;
   splits = (nkb + a.kb_per_split - 1) / a.kb_per_split;
   const int tiles = ((a.M + BM - 1) / BM) * ((a.N + bn - 1) / bn);
-  if (tiles > kTileCounters) return cudaErrorInvalidValue;
+  if (tiles > kTileCounters - 16) return cudaErrorInvalidValue;  // the last 16 are reserved
   a.epi = EPI_F32; a.out = ws; a.ldo = a.N; a.accumulate = 0; a.split_stride = plane;
   a.splits = splits; a.tile_counters = counters;
   a.final_epi = final_epi; a.final_out = final_out; a.final_ldo = final_ldo; a.final_accumulate = accumulate;

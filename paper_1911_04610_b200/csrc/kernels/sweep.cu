@@ -16,6 +16,7 @@
 // 128-bit store per bf16 prediction stream); streaming loads/stores (evict-first) for the
 // optimizer state, default policy for W_hat which the next forward/backward reads from L2.
 #include "../internal.h"
+#include "launch.h"
 
 namespace xp {
 
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(float* __restrict__ W, const
                                                     void* __restrict__ pf, void* __restrict__ pb, int64_t n,
                                                     const DevState* __restrict__ ds, SweepScalars hs, float sf,
                                                     float sb) {
+  pdl_wait();
   const Sc s = load_sc(ds, hs);
   const float nsf = -sf, nsb = -sb;
   const int64_t n8 = n >> 3;
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(float* __restrict__ W, const
 template <bool BF16>
 __global__ void predict_copy_kernel(const float* __restrict__ W, void* __restrict__ pf, void* __restrict__ pb,
                                     int64_t n) {
+  pdl_wait();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const float w = W[e];
     if (BF16) {
@@ -151,6 +154,7 @@ __global__ void predict_copy_kernel(const float* __restrict__ W, void* __restric
 
 // beta^k by repeated multiplication, c1/r2 in double then rounded
 __global__ void bump_kernel(DevState* ds, TraceRec* rec, int stage, int t, int T) {
+  pdl_wait();
   ds->ver += 1;
   ds->b1p = ds->b1p * (double)ds->b1;
   ds->b2p = ds->b2p * (double)ds->b2;
@@ -165,6 +169,7 @@ __global__ void bump_kernel(DevState* ds, TraceRec* rec, int stage, int t, int T
 }
 
 __global__ void state_init_kernel(DevState* ds, float lr, float b1, float b2, float eps) {
+  pdl_wait();
   ds->ver = 0; ds->fver = 0; ds->bver = 0; ds->pad = 0;
   ds->b1p = 1.0; ds->b2p = 1.0;
   ds->c1 = 0.f; ds->r2 = 0.f;
@@ -209,7 +214,7 @@ cudaError_t launch_sweep(float* W, const float* g, float* m, float* v, void* pf,
   SweepScalars h{};
   if (hs) h = *hs;
   const int grid = sweep_grid(n);
-#define XP_SWEEP(B, U, D) sweep_kernel<B, U, D><<<grid, 256, 0, st>>>(W, g, m, v, pf, pb, n, ds, h, s_f, s_b)
+#define XP_SWEEP(B, U, D) launch_pdl(sweep_kernel<B, U, D>, dim3(grid), dim3(256), 0, st, W, g, m, v, pf, pb, n, ds, h, s_f, s_b)
   if (bf16) {
     if (update) { if (delta_form) XP_SWEEP(true, true, 1); else XP_SWEEP(true, true, 0); }
     else { if (delta_form) XP_SWEEP(true, false, 1); else XP_SWEEP(true, false, 0); }
@@ -225,18 +230,18 @@ cudaError_t launch_predict_copy(const float* W, void* pf, void* pb, int64_t n, b
   int grid = (int)((n + 255) / 256);
   if (grid > 148 * 16) grid = 148 * 16;
   if (grid < 1) grid = 1;
-  if (bf16) predict_copy_kernel<true><<<grid, 256, 0, st>>>(W, pf, pb, n);
-  else predict_copy_kernel<false><<<grid, 256, 0, st>>>(W, pf, pb, n);
+  if (bf16) launch_pdl(predict_copy_kernel<true>, dim3(grid), dim3(256), 0, st, W, pf, pb, n);
+  else launch_pdl(predict_copy_kernel<false>, dim3(grid), dim3(256), 0, st, W, pf, pb, n);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bump(DevState* ds, TraceRec* rec, int stage, int t, int T, cudaStream_t st) {
-  bump_kernel<<<1, 1, 0, st>>>(ds, rec, stage, t, T);
+  launch_pdl(bump_kernel, dim3(1), dim3(1), 0, st, ds, rec, stage, t, T);
   return cudaGetLastError();
 }
 
 cudaError_t launch_state_init(DevState* ds, float lr, float b1, float b2, float eps, cudaStream_t st) {
-  state_init_kernel<<<1, 1, 0, st>>>(ds, lr, b1, b2, eps);
+  launch_pdl(state_init_kernel, dim3(1), dim3(1), 0, st, ds, lr, b1, b2, eps);
   return cudaGetLastError();
 }
 

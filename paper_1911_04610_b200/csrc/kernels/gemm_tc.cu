@@ -15,6 +15,8 @@
 // tcgen05.ld and store bf16 / fp32.  Deterministic: no atomics; split-K partials are
 // reduced in a fixed order by a separate kernel.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "../../../include/xpipe.h"
 #include "../internal.h"
@@ -61,6 +63,23 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int x0, int x1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"((uint64_t)map), "r"(x0), "r"(x1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int x0, int x1, int x2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(x0), "r"(x1), "r"(x2), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -310,8 +329,8 @@ template <int BN> struct ALoader<GEMM_DGRAD, BN> { typedef DgradA T; };
 template <int BN> struct ALoader<GEMM_WGRAD, BN> { typedef WgradA T; };
 
 template <int MODE, int BN, bool A_MN, bool B_MN>
-__device__ __forceinline__ void producer(const GemmArgs& a, uint32_t base, uint32_t full0, uint32_t empty0, int m0,
-                                         int n0, int kb0, int nkb, int tid) {
+__device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* tmB, uint32_t base, uint32_t full0,
+                                         uint32_t empty0, int m0, int n0, int kb0, int nkb, int tid) {
   constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
   constexpr int ST = Depth<BN>::ST, LAG = Depth<BN>::LAG;
   // operand loaders
@@ -334,15 +353,35 @@ __device__ __forceinline__ void producer(const GemmArgs& a, uint32_t base, uint3
     const int s = i % ST, it = i / ST, kb = kb0 + i;
     if (it > 0) mbar_wait(empty0 + 8 * s, (it - 1) & 1);
     const uint32_t sa = base + s * STAGE, sb = sa + A_BYTES;
+    const uint32_t full = full0 + 8 * s;
+    if (a.b_tma) {
+      if (tid == 0) {  // one elected thread moves the whole B tile with the TMA engine
+        mbar_expect_tx(full, BN * BK * 2);
+        const int k0 = kb * BK;
+        if (a.b_tma == 1) {
+          tma_2d(sb, tmB, k0, n0, full);
+        } else if (a.b_tma == 2) {
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) tma_2d(sb + j * (BK * 128), tmB, n0 + 64 * j, k0, full);
+        } else {
+          const int tap = k0 / a.g.Co, co0 = k0 - tap * a.g.Co;
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) tma_3d(sb + j * (BK * 128), tmB, n0 + 64 * j, tap, co0, full);
+        }
+      }
+    }
     if (MODE == GEMM_PLAIN) {
       if (A_MN) pam.load(sa, kb, tid); else pak.load(sa, kb, tid);
-      if (B_MN) pbm.load(sb, kb, tid); else pbk.load(sb, kb, tid);
+      if (!a.b_tma) { if (B_MN) pbm.load(sb, kb, tid); else pbk.load(sb, kb, tid); }
     } else if (MODE == GEMM_FPROP) {
-      fa.load(sa, kb, tid); pbk.load(sb, kb, tid);
+      fa.load(sa, kb, tid);
+      if (!a.b_tma) pbk.load(sb, kb, tid);
     } else if (MODE == GEMM_DGRAD) {
-      da.load(sa, kb, tid); db.load(sb, kb, tid);
+      da.load(sa, kb, tid);
+      if (!a.b_tma) db.load(sb, kb, tid);
     } else {
-      wa.load(sa, kb, tid); pbm.load(sb, kb, tid);
+      wa.load(sa, kb, tid);
+      if (!a.b_tma) pbm.load(sb, kb, tid);
     }
     cp_commit();
     if (i >= LAG) {
@@ -357,7 +396,7 @@ __device__ __forceinline__ void producer(const GemmArgs& a, uint32_t base, uint3
 }
 
 template <int MODE, int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) {
+__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
   constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
   constexpr int ST = Depth<BN>::ST;
@@ -375,7 +414,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) 
 
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(full0 + 8 * s, 128);
+      mbar_init(full0 + 8 * s, a.b_tma ? 129 : 128);  // 128 cp.async arrivals (+ the TMA expect_tx)
       mbar_init(empty0 + 8 * s, 1);
     }
     mbar_init(accum, 1);
@@ -393,7 +432,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) 
   pdl_wait();  // the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp < 4) {
-    producer<MODE, BN, A_MN, B_MN>(a, base, full0, empty0, m0, n0, kb0, nkb, tid);
+    producer<MODE, BN, A_MN, B_MN>(a, &tmB, base, full0, empty0, m0, n0, kb0, nkb, tid);
   } else {
     if (warp == 4 && lane == 0) {
       const uint32_t id = idesc<BN, A_MN, B_MN>();
@@ -476,6 +515,68 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a) 
   }
 }
 
+bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && *e && *e != '0';
+}
+
+// ---- TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point) ------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled encode_fn() {
+  static PFN_encodeTiled f = nullptr;
+  if (!f) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess) f = (PFN_encodeTiled)p;
+  }
+  return f;
+}
+
+// bf16 map, 128B swizzle, zero fill out of bounds; dims/strides innermost first (strides of
+// dims 1.. in bytes); returns false if the geometry is not TMA-legal (caller falls back)
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+              const uint32_t* box) {
+  PFN_encodeTiled f = encode_fn();
+  if (!f || ((uintptr_t)base & 15)) return false;
+  for (int i = 0; i + 1 < rank; ++i)
+    if (strides_bytes[i] % 16) return false;
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; es[i] = 1; }
+  for (int i = 0; i + 1 < rank; ++i) st[i] = strides_bytes[i];
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, st, b, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the B-operand map of a GEMM (sets a.b_tma; 0 when the geometry needs the cp.async path)
+template <int MODE, int BN, bool B_MN>
+void setup_b_tma(GemmArgs& a, CUtensorMap* m) {
+  a.b_tma = 0;
+  if (MODE == GEMM_PLAIN || MODE == GEMM_FPROP) {
+    if (!B_MN) {  // B [N][K] rows of K
+      const uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.N}, str[1] = {(uint64_t)a.ldb * 2};
+      const uint32_t box[2] = {64, (uint32_t)BN};
+      if (make_map(m, a.B, 2, dims, str, box)) a.b_tma = 1;
+    } else {      // B [K][N] rows of N
+      const uint64_t dims[2] = {(uint64_t)a.N, (uint64_t)a.K}, str[1] = {(uint64_t)a.ldb * 2};
+      const uint32_t box[2] = {64, 64};
+      if (make_map(m, a.B, 2, dims, str, box)) a.b_tma = 2;
+    }
+  } else if (MODE == GEMM_WGRAD) {  // dY [pixels][Co]
+    const uint64_t dims[2] = {(uint64_t)a.g.Co, (uint64_t)a.K}, str[1] = {(uint64_t)a.g.Co * 2};
+    const uint32_t box[2] = {64, 64};
+    if (make_map(m, a.B, 2, dims, str, box)) a.b_tma = 2;
+  } else if (MODE == GEMM_DGRAD && a.g.Co % 64 == 0) {  // W [Co][R*S][C]: k-block = 64 co of one tap
+    const uint64_t dims[3] = {(uint64_t)a.g.C, (uint64_t)(a.g.R * a.g.S), (uint64_t)a.g.Co};
+    const uint64_t str[2] = {(uint64_t)a.g.C * 2, (uint64_t)a.g.R * a.g.S * a.g.C * 2};
+    const uint32_t box[3] = {64, 1, 64};
+    if (make_map(m, a.B, 3, dims, str, box)) a.b_tma = 3;
+  }
+}
+
 template <int MODE, int BN, bool A_MN, bool B_MN>
 cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   constexpr int SMEM = Depth<BN>::ST * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
@@ -487,7 +588,12 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     attr = true;
   }
   dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, splits);
-  launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, dim3(grid), dim3(NTHREADS), SMEM, st, a);
+  GemmArgs args = a;
+  CUtensorMap tmB;
+  memset(&tmB, 0, sizeof tmB);
+  if (!getenv_flag("XPIPE_NO_TMA")) setup_b_tma<MODE, BN, B_MN>(args, &tmB);
+  else args.b_tma = 0;
+  launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, dim3(grid), dim3(NTHREADS), SMEM, st, args, tmB);
   return cudaGetLastError();
 }
 

@@ -1,5 +1,6 @@
 // gemm_tc.h -- tcgen05 implicit-GEMM entry points (kernels/gemm_tc.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -37,6 +38,10 @@ struct GemmArgs {
   void* final_out;
   int64_t final_ldo;
   int final_accumulate;
+  // B operand by TMA (cp.async.bulk.tensor into the 128B-swizzled UMMA layout):
+  // 0 = cp.async gather, 1 = 2D K-major box {64, BN}, 2 = 2D MN-major boxes {64, 64},
+  // 3 = 3D dgrad weights view {C, R*S, Co} boxes {64, 1, 64}
+  int b_tma;
 };
 
 // plain GEMM for unit parity: D[M][N] fp32 (ldd) = A(m,k) B(n,k)

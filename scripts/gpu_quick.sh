@@ -1,5 +1,5 @@
 #!/bin/bash
-out=gpurun_out; mkdir -p $out
+out=gpurun_out/${RUN:-run}; mkdir -p $out
 export PYTHONUNBUFFERED=1
 python __graft_entry__.py > $out/build.log 2>&1
 run() { name=$1; shift; echo "=== $name" >> $out/summary.txt; timeout ${T:-600} "$@" > $out/$name.log 2>&1; echo "rc=$?" >> $out/summary.txt; tail -${TL:-8} $out/$name.log >> $out/summary.txt; }

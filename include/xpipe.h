@@ -227,8 +227,12 @@ int xpipe_gemm_bf16(const void* A, const void* B, float* D, int32_t M, int32_t N
    multiple of 8), weights KRSC [Co][R][S][C] bf16, output NHWC [Nimg][P][Q][Co].  mode:
    1 = fprop (in0 = X, in1 = W, out = Y bf16), 2 = dgrad (in0 = dY, in1 = W, out = dX bf16
    [Nimg][H][W][C]), 3 = wgrad (in0 = X, in1 = dY, out = dW fp32 [Co][R][S][C], accumulate
-   adds into out).  ws: optional fp32 device workspace of ws_elems for split-K (NULL = none).
-   Device pointers; asynchronous on stream. */
+   adds into out).  ws: optional fp32 device workspace of ws_elems for split-K across
+   several clusters (NULL = split-K within one thread-block cluster only); its last 16384
+   elements hold the split-K arrival counters: they must be zero before the first call and
+   every call leaves them zero (so zero the workspace once).  Calls sharing one ws must be
+   stream-ordered.  Device pointers; asynchronous on stream.  Errors: XP_EINVAL (bad
+   geometry: C or Co not a multiple of 8, P/Q inconsistent), XP_ECUDA (launch). */
 int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void* in0, const void* in1, void* out,
                       int32_t accumulate, float* ws, int64_t ws_elems, void* stream);
 

@@ -6,14 +6,18 @@
 //   WGRAD : dW^T[(r,s,ci)][co] = sum_{n,p,q} X[n, p*sh-ph+r, q*sw-pw+s][ci] * dY[n,p,q][co]
 //   PLAIN : D[m][n] = sum_k A(m,k) B(n,k)   (unit parity of the MMA path, any operand majorness)
 // NHWC bf16 activations, KRSC weights (C padded to a multiple of 8), fp32 accumulation in
-// TMEM.  Tile 128 x BN x 64; the A/B tiles are gathered (implicit im2col with zero fill for
-// padding and ragged edges) by four producer warps with 16-byte cp.async straight into the
-// canonical 128B-swizzled UMMA layouts (K-major or MN-major) and handed to the MMA issuer
-// through an mbarrier ring (producers fence the generic->async proxy before arriving); one
-// thread issues tcgen05.mma (M=128, N=BN, K=16) and commits completion to the ring's empty
-// barriers and finally to the accumulator barrier; four epilogue warps drain TMEM with
-// tcgen05.ld and store bf16 / fp32.  Deterministic: no atomics; split-K partials are
-// reduced in a fixed order by a separate kernel.
+// TMEM.  Tile 128 x BN x 64; the dense B operand (weights in fprop/dgrad, dY in wgrad) is
+// moved by the TMA engine (one elected thread, cp.async.bulk.tensor with 128B swizzle straight
+// into the UMMA layout); the gathered A operand (implicit im2col with zero fill for padding and
+// ragged edges) by four producer warps with 16-byte cp.async.  Both hand the stage to the MMA
+// issuer through an mbarrier ring (cp.async producers fence the generic->async proxy before
+// arriving; the TMA completes the transaction count); one thread issues tcgen05.mma (M=128,
+// N=BN, K=16) and commits completion to the ring's empty barriers and finally to the
+// accumulator barrier; four epilogue warps drain TMEM with tcgen05.ld.
+// Split-K runs as a thread-block cluster along z (one CTA per K range, <= 8): every CTA parks
+// its fp32 accumulator tile in its own shared memory, and after a cluster barrier CTA z sums
+// rows [z*128/cs, (z+1)*128/cs) of all cs tiles over DSMEM in the fixed order 0..cs-1 and
+// applies the epilogue.  No atomics, no workspace, deterministic.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -30,7 +34,9 @@ namespace {
 constexpr int BM = 128, BK = 64;
 // smem ring depth by N tile (~192 KB of stages): more loads in flight for the narrow tiles,
 // whose k-blocks are short relative to the global-memory latency
-template <int BN> struct Depth { static constexpr int ST = BN == 64 ? 8 : (BN == 128 ? 6 : 4); static constexpr int LAG = ST - 2; };
+// smem ring depth by N tile: 96 KB (two CTAs per SM) for BN <= 128, 144 KB for BN = 256
+template <int BN> struct Depth { static constexpr int ST = BN == 64 ? 4 : 3; static constexpr int LAG = ST - 1; };
+constexpr int kMaxCluster = 8;
 constexpr int NTHREADS = 256;  // warps 0-3 producers, warp 4 MMA issuer, warps 4-7 epilogue
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -63,6 +69,22 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -71,6 +93,14 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           dst),
       "l"((uint64_t)map), "r"(x0), "r"(x1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int x0, int x1, int x2, int x3,
+                                       uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int x0, int x1, int x2, uint32_t bar) {
@@ -137,6 +167,14 @@ __device__ __forceinline__ uint32_t mnmaj_off(int mn0, int kk) {
 }
 
 typedef __nv_bfloat16 bf16;
+
+__host__ bool getenv_flag(const char* name) {  // read once per name (development switches)
+  const char* e = getenv(name);
+  return e && *e && *e != '0';
+}
+__host__ bool no_tma() { static const bool v = getenv_flag("XPIPE_NO_TMA"); return v; }
+__host__ bool no_tma_a() { static const bool v = getenv_flag("XPIPE_NO_TMA_A"); return v; }
+__host__ bool no_splitk() { static const bool v = getenv_flag("XPIPE_NO_SPLITK"); return v; }
 
 // ---------------------------------------------------------------------------------------
 // operand loaders: init once per tile, load(kb) per k-block; 128 producer threads (tid)
@@ -322,6 +360,43 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
   }
 }
 
+// 8 consecutive columns [col0, col0+8) of row `row` (split-K reduction output)
+__device__ __forceinline__ void epi_store8(const GemmArgs& a, int row, int col0, const float (&v)[8]) {
+  if (a.epi == EPI_BF16) {
+    bf16* o = static_cast<bf16*>(a.out) + (int64_t)row * a.ldo + col0;
+    if (!a.accumulate && col0 + 8 <= a.N) {
+      uint32_t w[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+        w[h] = *reinterpret_cast<uint32_t*>(&t);
+      }
+      *reinterpret_cast<uint4*>(o) = make_uint4(w[0], w[1], w[2], w[3]);
+      return;
+    }
+    for (int e = 0; e < 8; ++e)
+      if (col0 + e < a.N) {
+        if (a.accumulate) {
+          const float g = __bfloat162float(__float2bfloat16_rn(v[e]));
+          o[e] = __float2bfloat16_rn(__fadd_rn(__bfloat162float(o[e]), g));
+        } else {
+          o[e] = __float2bfloat16_rn(v[e]);
+        }
+      }
+  } else if (a.epi == EPI_F32) {
+    float* o = static_cast<float*>(a.out) + (int64_t)row * a.ldo + col0;
+    for (int e = 0; e < 8; ++e)
+      if (col0 + e < a.N) o[e] = v[e];
+  } else {
+    float* g = static_cast<float*>(a.out);
+    for (int e = 0; e < 8; ++e)
+      if (col0 + e < a.N) {
+        float* p = g + (int64_t)(col0 + e) * a.ldo + row;
+        *p = a.accumulate ? __fadd_rn(*p, v[e]) : v[e];
+      }
+  }
+}
+
 template <int MODE, int BN>
 struct ALoader;
 template <int BN> struct ALoader<GEMM_FPROP, BN> { typedef FpropA T; };
@@ -329,8 +404,8 @@ template <int BN> struct ALoader<GEMM_DGRAD, BN> { typedef DgradA T; };
 template <int BN> struct ALoader<GEMM_WGRAD, BN> { typedef WgradA T; };
 
 template <int MODE, int BN, bool A_MN, bool B_MN>
-__device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* tmB, uint32_t base, uint32_t full0,
-                                         uint32_t empty0, int m0, int n0, int kb0, int nkb, int tid) {
+__device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* tmA, const CUtensorMap* tmB, uint32_t base,
+                                         uint32_t full0, uint32_t empty0, int m0, int n0, int kb0, int nkb, int tid) {
   constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
   constexpr int ST = Depth<BN>::ST, LAG = Depth<BN>::LAG;
   // operand loaders
@@ -348,6 +423,45 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
   } else {
     wa.init(a, m0, tid);
     pbm.init(a.B, a.g.Co, a.N, a.K, n0);        // dY [pixels][Co]
+  }
+  if (a.a_tma) {
+    // full-TMA pipeline: one elected thread streams both operands; the others are idle
+    if (tid != 0) return;
+    int tn = 0, tp = 0, tq = 0;  // pixel origin of the tile's rows (fprop / dgrad)
+    if (MODE != GEMM_WGRAD) {
+      tn = m0 / (a.gq * a.gp);
+      const int rem = m0 - tn * a.gq * a.gp;
+      tp = rem / a.gq; tq = rem - tp * a.gq;
+    }
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % ST, it = i / ST, kb = kb0 + i;
+      if (it > 0) mbar_wait(empty0 + 8 * s, (it - 1) & 1);
+      const uint32_t sa = base + s * STAGE, sb = sa + A_BYTES, full = full0 + 8 * s;
+      const int k0 = kb * BK;
+      if (MODE == GEMM_FPROP) {
+        mbar_expect_tx(full, STAGE);
+        const int tap = k0 / a.g.C, c0 = k0 - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
+        tma_4d(sa, tmA, c0, tq + ss - a.g.pw, tp + r - a.g.ph, tn, full);
+        tma_2d(sb, tmB, k0, n0, full);
+      } else if (MODE == GEMM_DGRAD) {
+        mbar_expect_tx(full, STAGE);
+        const int tap = k0 / a.g.Co, c0 = k0 - tap * a.g.Co, r = tap / a.g.S, ss = tap - r * a.g.S;
+        tma_4d(sa, tmA, c0, tq + a.g.pw - ss, tp + a.g.ph - r, tn, full);
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j) tma_3d(sb + j * (BK * 128), tmB, n0 + 64 * j, tap, c0, full);
+      } else if (MODE == GEMM_WGRAD) {
+        const int pn = k0 / (a.gq * a.gp), rem = k0 - pn * a.gq * a.gp, pp = rem / a.gq, pq = rem - pp * a.gq;
+        const int nch = min(2, (a.M - m0 + 63) / 64);
+        mbar_expect_tx(full, (uint32_t)(nch * BK * 128 + BN * BK * 2));
+        for (int j = 0; j < nch; ++j) {
+          const int mm = m0 + 64 * j, tap = mm / a.g.C, c0 = mm - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
+          tma_4d(sa + j * (BK * 128), tmA, c0, pq + ss - a.g.pw, pp + r - a.g.ph, pn, full);
+        }
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j) tma_2d(sb + j * (BK * 128), tmB, n0 + 64 * j, k0, full);
+      }
+    }
+    return;
   }
   for (int i = 0; i < nkb; ++i) {
     const int s = i % ST, it = i / ST, kb = kb0 + i;
@@ -396,7 +510,8 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
 }
 
 template <int MODE, int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, const __grid_constant__ CUtensorMap tmB) {
+__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, const __grid_constant__ CUtensorMap tmA,
+                                                               const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
   constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
   constexpr int ST = Depth<BN>::ST;
@@ -414,7 +529,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
 
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(full0 + 8 * s, a.b_tma ? 129 : 128);  // 128 cp.async arrivals (+ the TMA expect_tx)
+      // 128 cp.async arrivals (+ the TMA expect_tx), or the TMA thread's alone
+      mbar_init(full0 + 8 * s, a.a_tma ? 1 : (a.b_tma ? 129 : 128));
       mbar_init(empty0 + 8 * s, 1);
     }
     mbar_init(accum, 1);
@@ -432,7 +548,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
   pdl_wait();  // the prologue above overlapped the previous kernel; its outputs are visible now
 
   if (warp < 4) {
-    producer<MODE, BN, A_MN, B_MN>(a, &tmB, base, full0, empty0, m0, n0, kb0, nkb, tid);
+    producer<MODE, BN, A_MN, B_MN>(a, &tmA, &tmB, base, full0, empty0, m0, n0, kb0, nkb, tid);
+    __syncwarp();  // reconverge (the TMA producer is one thread) before the aligned barriers
   } else {
     if (warp == 4 && lane == 0) {
       const uint32_t id = idesc<BN, A_MN, B_MN>();
@@ -453,59 +570,116 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
       pdl_trigger();
     }
     __syncwarp();
-    mbar_wait(accum, 0);
-    tc_fence_after();
-    const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
+  }
+  constexpr int LDS = BN + 4;  // fp32 staging row pitch of the split-K reduction (bank skew)
+  const int q = warp & 3;
+  const int row = m0 + q * 32 + lane;
+  if (a.splits <= 1) {
+    if (warp >= 4) {
+      mbar_wait(accum, 0);
+      tc_fence_after();
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t v[32];
-      if (nkb > 0) {
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-      } else {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        if (nkb > 0) {
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+        } else {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = 0u;
+          for (int e = 0; e < 32; ++e) v[e] = 0u;
+        }
+        if (n0 + c0 < a.N) epi_store(a, row, n0 + c0, v);
       }
-      if (n0 + c0 < a.N) epi_store(a, row, n0 + c0, v);
     }
-    if (a.splits > 1) {
-      // last-CTA reduction: publish this partial, count it, and let the last split finish
-      __shared__ int is_last;
-      __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-      if (tid == 128) {
-        const int old = atomicAdd(&a.tile_counters[tile], 1);
-        is_last = (old == a.splits - 1);
-        if (is_last) a.tile_counters[tile] = 0;  // ready for the next launch
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (is_last) {
-        __threadfence();
-        GemmArgs f = a;
-        f.epi = a.final_epi; f.out = a.final_out; f.ldo = a.final_ldo; f.accumulate = a.final_accumulate;
-        const float* ws = static_cast<const float*>(a.out);
+  } else {
+    // cluster split-K: park the partial tile in this CTA's smem (the ring is drained: every
+    // stage was consumed by an MMA that completed before the accumulator barrier)
+    float* red = reinterpret_cast<float*>(smem_raw + (base - raw));
+    if (warp >= 4) {
+      mbar_wait(accum, 0);
+      tc_fence_after();
+      const int r = q * 32 + lane;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN && n0 + c0 < a.N; c0 += 32) {
-          uint32_t v[32];
-          if (row < a.M) {
-            const float* base = ws + (int64_t)row * a.ldo + n0 + c0;
-            const int ncol = min(32, a.N - n0 - c0);
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        if (nkb > 0) {
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+        } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              float acc = 0.f;
-              if (e < ncol)
-                for (int z = 0; z < a.splits; ++z) {
-                  const float x = __ldcg(base + (int64_t)z * a.split_stride + e);
-                  acc = z ? __fadd_rn(acc, x) : x;
-                }
-              v[e] = __float_as_uint(acc);
-            }
+          for (int e = 0; e < 32; ++e) v[e] = 0u;
+        }
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          *reinterpret_cast<float4*>(red + r * LDS + c0 + e) =
+              make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                          __uint_as_float(v[e + 3]));
+      }
+    }
+    cluster_sync();
+    const int cs = a.cs, nc = a.nc, z = blockIdx.z % cs, cl = blockIdx.z / cs;
+    const int rpr = (BM + cs - 1) / cs, r0 = z * rpr, r1 = min(BM, r0 + rpr);
+    const int nrows = max(0, r1 - r0);
+    constexpr int NCH = BN / 8;
+    const bool row_fast = a.epi == EPI_WGRAD_T;  // transposed store: consecutive threads = consecutive m
+    const uint32_t red_u = base;
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    float* wsp = a.ws + ((int64_t)tile * nc + cl) * (BM * BN);  // this cluster's partial tile
+#pragma unroll 1
+    for (int idx = tid; idx < nrows * NCH; idx += NTHREADS) {
+      const int rr = row_fast ? idx % nrows : idx / NCH, ch = row_fast ? idx / nrows : idx % NCH;
+      const int lr = r0 + rr, gr = m0 + lr, gc = n0 + ch * 8;
+      if (gr >= a.M || gc >= a.N) continue;
+      const uint32_t off = red_u + (uint32_t)((lr * LDS + ch * 8) * 4);
+      float acc[8];
+#pragma unroll 1
+      for (int src = 0; src < cs; ++src) {
+        const uint32_t ra = mapa(off, (uint32_t)src);
+        const float4 x0 = ld_dsmem4(ra), x1 = ld_dsmem4(ra + 16);
+        const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = src ? __fadd_rn(acc[e], x[e]) : x[e];
+      }
+      if (nc == 1) {
+        epi_store8(a, gr, gc, acc);
+      } else {
+        float4* d = reinterpret_cast<float4*>(wsp + lr * BN + ch * 8);
+        __stcg(d, make_float4(acc[0], acc[1], acc[2], acc[3]));
+        __stcg(d + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+      }
+    }
+    if (nc > 1) {
+      // cross-cluster: the last of the nc CTAs owning row slice z of this tile sums the slices
+      __shared__ int last;
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        int* ctr = a.tile_counters + tile * cs + z;
+        const int old = atomicAdd(ctr, 1);
+        last = old == nc - 1;
+        if (last) *ctr = 0;  // ready for the next launch on this stream
+      }
+      __syncthreads();
+      if (last) {
+        __threadfence();
+        const float* w0 = a.ws + (int64_t)tile * nc * (BM * BN);
+#pragma unroll 1
+        for (int idx = tid; idx < nrows * NCH; idx += NTHREADS) {
+          const int rr = row_fast ? idx % nrows : idx / NCH, ch = row_fast ? idx / nrows : idx % NCH;
+          const int lr = r0 + rr, gr = m0 + lr, gc = n0 + ch * 8;
+          if (gr >= a.M || gc >= a.N) continue;
+          float acc[8];
+#pragma unroll 1
+          for (int c = 0; c < nc; ++c) {
+            const float4* sp = reinterpret_cast<const float4*>(w0 + (int64_t)c * (BM * BN) + lr * BN + ch * 8);
+            const float4 x0 = __ldcg(sp), x1 = __ldcg(sp + 1);
+            const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = c ? __fadd_rn(acc[e], x[e]) : x[e];
           }
-          epi_store(f, row, n0 + c0, v);
+          epi_store8(a, gr, gc, acc);
         }
       }
     }
+    cluster_sync();  // no CTA leaves while its tile is still being read
   }
   tc_fence_before();
   __syncthreads();
@@ -515,10 +689,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
   }
 }
 
-bool getenv_flag(const char* name) {
-  const char* e = getenv(name);
-  return e && *e && *e != '0';
-}
 
 // ---- TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point) ------
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -556,8 +726,9 @@ template <int MODE, int BN, bool B_MN>
 void setup_b_tma(GemmArgs& a, CUtensorMap* m) {
   a.b_tma = 0;
   if (MODE == GEMM_PLAIN || MODE == GEMM_FPROP) {
-    if (!B_MN) {  // B [N][K] rows of K
-      const uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.N}, str[1] = {(uint64_t)a.ldb * 2};
+    if (!B_MN) {  // B [N][K] rows of K (fprop: W [Co][R*S*C])
+      const uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.N};
+      const uint64_t str[1] = {(uint64_t)(MODE == GEMM_FPROP ? a.K : a.ldb) * 2};
       const uint32_t box[2] = {64, (uint32_t)BN};
       if (make_map(m, a.B, 2, dims, str, box)) a.b_tma = 1;
     } else {      // B [K][N] rows of N
@@ -577,6 +748,41 @@ void setup_b_tma(GemmArgs& a, CUtensorMap* m) {
   }
 }
 
+// pixel box of T consecutive rows of the (n, p, q) grid {Q, P}: {bq, bp, bn}, or false
+bool pixel_box(int T, int Q, int P, uint32_t* box) {
+  if (Q % T == 0) { box[0] = T; box[1] = 1; box[2] = 1; return true; }
+  if (T % Q) return false;
+  const int rp = T / Q;
+  if (P % rp == 0) { box[0] = Q; box[1] = rp; box[2] = 1; return true; }
+  if (rp % P == 0) { box[0] = Q; box[1] = P; box[2] = rp / P; return true; }
+  return false;
+}
+
+// the A-operand map of a stride-1 conv GEMM (sets a.a_tma; needs a.b_tma)
+template <int MODE>
+void setup_a_tma(GemmArgs& a, CUtensorMap* m) {
+  a.a_tma = 0;
+  if (MODE == GEMM_PLAIN || !a.b_tma || a.g.sh != 1 || a.g.sw != 1) return;
+  const ConvGeo& g = a.g;
+  uint32_t pb[3];
+  uint64_t dims[4], str[3];
+  if (MODE == GEMM_FPROP || MODE == GEMM_WGRAD) {  // gather from X {C, W, H, N}
+    if (g.C % 64) return;
+    if (!pixel_box(MODE == GEMM_FPROP ? BM : BK, g.Q, g.P, pb)) return;
+    dims[0] = g.C; dims[1] = g.W; dims[2] = g.H; dims[3] = g.Nimg;
+    str[0] = (uint64_t)g.C * 2; str[1] = (uint64_t)g.W * g.C * 2; str[2] = (uint64_t)g.H * g.W * g.C * 2;
+    a.gq = g.Q; a.gp = g.P;
+  } else {  // DGRAD: gather from dY {Co, Q, P, N}, rows on the input grid {W, H}
+    if (g.Co % 64) return;
+    if (!pixel_box(BM, g.W, g.H, pb)) return;
+    dims[0] = g.Co; dims[1] = g.Q; dims[2] = g.P; dims[3] = g.Nimg;
+    str[0] = (uint64_t)g.Co * 2; str[1] = (uint64_t)g.Q * g.Co * 2; str[2] = (uint64_t)g.P * g.Q * g.Co * 2;
+    a.gq = g.W; a.gp = g.H;
+  }
+  const uint32_t box[4] = {64, pb[0], pb[1], pb[2]};
+  if (make_map(m, a.A, 4, dims, str, box)) a.a_tma = 1;
+}
+
 template <int MODE, int BN, bool A_MN, bool B_MN>
 cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   constexpr int SMEM = Depth<BN>::ST * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
@@ -589,12 +795,31 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   }
   dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, splits);
   GemmArgs args = a;
-  CUtensorMap tmB;
+  CUtensorMap tmA, tmB;
+  memset(&tmA, 0, sizeof tmA);
   memset(&tmB, 0, sizeof tmB);
-  if (!getenv_flag("XPIPE_NO_TMA")) setup_b_tma<MODE, BN, B_MN>(args, &tmB);
-  else args.b_tma = 0;
-  launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, dim3(grid), dim3(NTHREADS), SMEM, st, args, tmB);
-  return cudaGetLastError();
+  args.a_tma = args.b_tma = 0;
+  if (!no_tma()) {
+    setup_b_tma<MODE, BN, B_MN>(args, &tmB);
+    if (!no_tma_a()) setup_a_tma<MODE>(args, &tmA);
+  }
+  if (splits <= 1) {
+    launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, dim3(grid), dim3(NTHREADS), SMEM, st, args, tmA, tmB);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = 1; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = a.cs;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<MODE, BN, A_MN, B_MN>, args, tmA, tmB);
 }
 
 template <int MODE, bool A_MN, bool B_MN>
@@ -624,40 +849,40 @@ int num_sms() {
   return sms;
 }
 
-// split-K factor: fill ~one wave of SMs, at least 4 k-blocks per split
-int choose_splits(int M, int N, int K, int bn) {
-  const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-  const int nkb = (K + BK - 1) / BK;
-  if (tiles >= num_sms() / 2 || nkb < 8) return 1;  // >= half a wave: no split
-  int s = num_sms() / tiles;
-  s = std::min(s, nkb / 4);
-  return std::max(1, s);
+// split-K plan of a conv GEMM: N tile, cluster size cs (<= 8), clusters per tile nc, k-blocks
+// per split.  Aim at ~one CTA per SM with >= 8 k-blocks each (a CTA's fixed cost -- prologue,
+// pipeline fill, epilogue -- is several k-blocks' worth); no split when the tile grid alone
+// fills half the SMs or K is short.
+struct SplitPlan { int bn, cs, nc, kbps; };
+SplitPlan plan_splits(int M, int N, int K) {
+  SplitPlan p;
+  p.bn = choose_bn(M, N);
+  const int tiles = ((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn);
+  const int nkb = std::max(1, (K + BK - 1) / BK);
+  int s = 1;
+  if (!no_splitk() && tiles < num_sms() / 2 && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / 8));
+  if (tiles * (int64_t)std::min(s, kMaxCluster) > kTileCounters - 16) s = 1;
+  p.cs = std::min(s, kMaxCluster);
+  p.nc = std::max(1, s / p.cs);
+  p.kbps = (nkb + p.cs * p.nc - 1) / (p.cs * p.nc);
+  return p;
 }
 
-// run a conv GEMM with optional split-K through the workspace
+// run a conv GEMM, split-K as clusters when the tile grid alone does not fill the SMs
 template <int MODE, bool A_MN, bool B_MN>
 cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_ldo, int accumulate, float* ws,
                       int64_t ws_elems, int* counters, cudaStream_t st) {
-  const int bn = choose_bn(a.M, a.N);
-  int splits = choose_splits(a.M, a.N, a.K, bn);
-  const int64_t plane = (int64_t)a.M * a.N;
-  while (splits > 1 && (int64_t)splits * plane > ws_elems) --splits;
-  if (!counters) splits = 1;
-  const int nkb = (a.K + BK - 1) / BK;
-  if (splits <= 1) {
-    a.splits = 1;
-    a.kb_per_split = std::max(1, nkb);
-    a.epi = final_epi; a.out = final_out; a.ldo = final_ldo; a.accumulate = accumulate; a.split_stride = 0;
-    return launch_bn<MODE, A_MN, B_MN>(a, bn, 1, st);
+  SplitPlan p = plan_splits(a.M, a.N, a.K);
+  const int tiles = ((a.M + BM - 1) / BM) * ((a.N + p.bn - 1) / p.bn);
+  if (p.nc > 1 && (!ws || !counters || (int64_t)tiles * p.nc * BM * p.bn > ws_elems)) {  // one cluster only
+    p.nc = 1;
+    p.kbps = (std::max(1, (a.K + BK - 1) / BK) + p.cs - 1) / p.cs;
   }
-  a.kb_per_split = (nkb + splits - 1) / splits;
-  splits = (nkb + a.kb_per_split - 1) / a.kb_per_split;
-  const int tiles = ((a.M + BM - 1) / BM) * ((a.N + bn - 1) / bn);
-  if (tiles > kTileCounters - 16) return cudaErrorInvalidValue;  // the last 16 are reserved
-  a.epi = EPI_F32; a.out = ws; a.ldo = a.N; a.accumulate = 0; a.split_stride = plane;
-  a.splits = splits; a.tile_counters = counters;
-  a.final_epi = final_epi; a.final_out = final_out; a.final_ldo = final_ldo; a.final_accumulate = accumulate;
-  return launch_bn<MODE, A_MN, B_MN>(a, bn, splits, st);
+  a.kb_per_split = p.kbps;
+  a.cs = p.cs; a.nc = p.nc; a.splits = p.cs * p.nc;
+  a.ws = ws; a.tile_counters = counters;
+  a.epi = final_epi; a.out = final_out; a.ldo = final_ldo; a.accumulate = accumulate; a.split_stride = 0;
+  return launch_bn<MODE, A_MN, B_MN>(a, p.bn, a.splits, st);
 }
 
 }  // namespace
@@ -700,15 +925,14 @@ cudaError_t tc_conv_wgrad(const ConvGeo& g, const bf16* X, const bf16* dY, float
 }
 
 int64_t tc_conv_ws_elems(const ConvGeo& g) {
-  // the largest of the three GEMMs' split-K need, capped at 16M floats
+  // cross-cluster split-K partial tiles of the largest of the three GEMMs
   auto need = [](int M, int N, int K) -> int64_t {
-    const int bn = choose_bn(M, N);
-    return (int64_t)choose_splits(M, N, K, bn) * M * N;
+    const SplitPlan p = plan_splits(M, N, K);
+    if (p.nc <= 1) return 0;
+    return (int64_t)((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn) * p.nc * BM * p.bn;
   };
-  int64_t a = need(g.Nimg * g.P * g.Q, g.Co, g.R * g.S * g.C);
-  int64_t b = need(g.Nimg * g.H * g.W, g.C, g.R * g.S * g.Co);
-  int64_t c = need(g.R * g.S * g.C, g.Co, g.Nimg * g.P * g.Q);
-  return std::min<int64_t>(std::max({a, b, c}), (int64_t)16 << 20);
+  return std::max({need(g.Nimg * g.P * g.Q, g.Co, g.R * g.S * g.C), need(g.Nimg * g.H * g.W, g.C, g.R * g.S * g.Co),
+                   need(g.R * g.S * g.C, g.Co, g.Nimg * g.P * g.Q)});
 }
 
 }  // namespace xp
@@ -731,12 +955,12 @@ extern "C" int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void
   if (g.P != (g.H + 2 * g.ph - g.R) / g.sh + 1 || g.Q != (g.W + 2 * g.pw - g.S) / g.sw + 1) return XP_EINVAL;
   if (!ws) ws_elems = 0;
   cudaStream_t st = (cudaStream_t)stream;
-  // unit-test entry: split-K counters live in the tail of the caller's workspace
+  // unit-test entry: the cross-cluster split-K counters live in the tail of the caller's
+  // workspace (zero on entry, self-resetting; see xpipe.h)
   int* counters = nullptr;
   if (ws && ws_elems > xp::kTileCounters) {
     ws_elems -= xp::kTileCounters;
     counters = reinterpret_cast<int*>(ws + ws_elems);
-    if (cudaMemsetAsync(counters, 0, xp::kTileCounters * sizeof(int), st) != cudaSuccess) return XP_ECUDA;
   }
   cudaError_t e;
   typedef __nv_bfloat16 B;

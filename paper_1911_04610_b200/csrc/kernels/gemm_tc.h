@@ -27,21 +27,24 @@ struct GemmArgs {
   void* out;
   int64_t ldo;
   int accumulate;
-  int64_t split_stride;   // elements between split-K partial planes (EPI_F32 into a workspace)
+  int64_t split_stride;   // unused (kept 0)
   int kb_per_split;
-  // split-K with in-kernel reduction: every split CTA writes its fp32 partial plane, the last
-  // one to finish (per-tile counter) sums the planes in fixed order z = 0..splits-1 and applies
-  // the final epilogue (final_epi into final_out)
-  int splits;
+  // split-K: grid.z = splits = cs x nc CTAs per tile; clusters of cs CTAs along z reduce over
+  // DSMEM (CTA rank z owns rows [z*128/cs, (z+1)*128/cs) of the tile); with nc > 1 clusters
+  // every row slice goes to the workspace `ws` and the last of the nc CTAs owning that slice
+  // (per-slice arrival counter, self-resetting) sums the nc slices in order c = 0..nc-1
+  int splits, cs, nc;
+  float* ws;
   int* tile_counters;
-  int final_epi;
-  void* final_out;
-  int64_t final_ldo;
-  int final_accumulate;
   // B operand by TMA (cp.async.bulk.tensor into the 128B-swizzled UMMA layout):
   // 0 = cp.async gather, 1 = 2D K-major box {64, BN}, 2 = 2D MN-major boxes {64, 64},
   // 3 = 3D dgrad weights view {C, R*S, Co} boxes {64, 1, 64}
   int b_tma;
+  // A operand by TMA (stride-1 convs with C % 64 == 0 whose tile rows form a box of the pixel
+  // grid): 4D tiled map over the NHWC activation {C, W, H, N}, box {64, bq, bp, bn}; the tile's
+  // pixel origin comes from the m (fprop/dgrad) or k (wgrad) index on the grid {gq, gp}
+  int a_tma;
+  int gq, gp;
 };
 
 // plain GEMM for unit parity: D[M][N] fp32 (ldd) = A(m,k) B(n,k)

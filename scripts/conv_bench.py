@@ -24,7 +24,8 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--check", action="store_true", help="compare each GEMM with torch (fp32 math)")
-    ap.add_argument("--layers", default="vgg")
+    ap.add_argument("--only", type=int, default=-1, help="run only this layer index")
+    ap.add_argument("--modes", default="123", help="subset of 1 fprop / 2 dgrad / 3 wgrad")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.manual_seed(0)
@@ -34,7 +35,9 @@ def main():
     flops_tot = 0.0
     print("%-22s %10s %10s %10s %8s %8s %8s" % ("layer", "fprop us", "dgrad us", "wgrad us", "TF/s f", "TF/s d",
                                                  "TF/s w"))
-    for (H, C, Co, R) in VGG:
+    for li, (H, C, Co, R) in enumerate(VGG):
+        if args.only >= 0 and li != args.only:
+            continue
         n = args.batch
         x = torch.randn(n, H, H, C, device=dev).to(torch.bfloat16)
         w = (torch.randn(Co, R, R, C, device=dev) * 0.05).to(torch.bfloat16)
@@ -46,15 +49,26 @@ def main():
         flops = 2.0 * n * H * H * Co * R * R * C
         res = []
         for mode, a, b, o in ((1, x, w, y), (2, dy, w, dx), (3, x, dy, gw)):
+            if str(mode) not in args.modes:
+                res.append(float("nan"))
+                continue
             with torch.cuda.stream(st):
                 for _ in range(3):
                     xpipe.conv2d_bf16(mode, geo, a, b, o, ws=ws, stream=st.cuda_stream)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(st)
-                for _ in range(args.iters):
-                    xpipe.conv2d_bf16(mode, geo, a, b, o, ws=ws, stream=st.cuda_stream)
-                e1.record(st)
             st.synchronize()
+            # GPU time: replay a CUDA graph of `iters` launches (host launch cost excluded)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                cs = torch.cuda.current_stream().cuda_stream
+                for _ in range(args.iters):
+                    xpipe.conv2d_bf16(mode, geo, a, b, o, ws=ws, stream=cs)
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
             us = e0.elapsed_time(e1) * 1e3 / args.iters
             res.append(us)
             tot[mode] += us

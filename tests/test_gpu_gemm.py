@@ -49,6 +49,13 @@ CONVS = [
     (1, 128, 4, 4, 256, 3, 3, 1, 1, 1, 1),
     (32, 512, 2, 2, 512, 3, 3, 1, 1, 1, 1),     # VGG late layer (M=128, K=4608)
     (32, 64, 32, 32, 64, 3, 3, 1, 1, 1, 1),     # VGG layer 2 (M=32768)
+    # full-TMA operand paths (stride 1, C % 64 == 0, tile rows form a pixel box)
+    (4, 64, 8, 8, 64, 3, 3, 1, 1, 1, 1),        # box {8, 8, 2}
+    (3, 64, 16, 16, 128, 3, 3, 1, 1, 1, 1),     # box {16, 8, 1}
+    (3, 128, 4, 4, 192, 3, 3, 1, 1, 1, 1),      # ragged images past the last one (zero fill)
+    (5, 64, 8, 8, 64, 1, 1, 1, 1, 0, 0),        # wgrad M = 64 (half an MN tile)
+    (2, 64, 8, 8, 64, 1, 7, 1, 1, 0, 3),        # asymmetric filter / padding
+    (6, 192, 2, 2, 320, 3, 3, 1, 1, 1, 1),      # box {2, 2, 32}, ragged N tiles
 ]
 
 
@@ -79,7 +86,7 @@ def test_conv_fprop_dgrad_wgrad(cfg):
     Xd = X.permute(0, 2, 3, 1).contiguous().to(DEV)        # NHWC
     Wd = Wt.permute(0, 2, 3, 1).contiguous().to(DEV)       # KRSC
     dYd = dY.permute(0, 2, 3, 1).contiguous().to(DEV)
-    ws = torch.empty(16 << 20, device=DEV)
+    ws = torch.zeros(16 << 20, device=DEV)  # zero once: the split-K counters live in its tail
     for use_ws in (None, ws):
         Y = torch.empty(n, P, Q, co, dtype=torch.bfloat16, device=DEV)
         conv2d_bf16(1, geo, Xd, Wd, Y, ws=use_ws)

@@ -58,7 +58,8 @@ __device__ __forceinline__ void chan_merge(float& na, float& mean, float& m2, fl
 // block: G = C/8 channel groups x RL = 256/G row lanes; chunk = RC rows; thread keeps
 // Welford (n, mean, M2) for 8 channels; lanes merged in fixed order through smem.
 __device__ void bn_stats_merge(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
-                               const bf16* __restrict__ gamma, const bf16* __restrict__ beta, float* __restrict__ stats);
+                               const bf16* __restrict__ gamma, const bf16* __restrict__ beta, float* __restrict__ stats,
+                               float* sh);
 
 __global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C, int RC, float* __restrict__ part,
                                         int* __restrict__ counter, float eps, const bf16* __restrict__ gamma,
@@ -126,28 +127,46 @@ __global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C
   __syncthreads();
   if (last) {
     __threadfence();
-    bn_stats_merge(part, gridDim.x, M, RC, C, eps, gamma, beta, stats);
+    bn_stats_merge(part, gridDim.x, M, RC, C, eps, gamma, beta, stats, sh);
   }
 }
 
-// warp w of the block merges channels w, w+nwarps, ...: lane l takes chunks l, l+32, ... in
-// order, then the lanes merge in a fixed butterfly order (deterministic)
+// Final merge in the last block.  Thread t takes channel c = c0 + t % CW (CW = min(C, T)) and
+// lane j = t / CW of J = T / CW lanes per channel; lane j merges chunks j, j+J, j+2J, ... in
+// order (loads batched 8 deep so L2 latency overlaps), then lane 0 absorbs lanes 1..J-1 in
+// order through shared memory (deterministic).  sh: >= 3*T floats.
 __device__ void bn_stats_merge(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
-                               const bf16* __restrict__ gamma, const bf16* __restrict__ beta, float* __restrict__ stats) {
-  const int nw = blockDim.x >> 5, lane = threadIdx.x & 31;
-  for (int c = threadIdx.x >> 5; c < C; c += nw) {
+                               const bf16* __restrict__ gamma, const bf16* __restrict__ beta, float* __restrict__ stats,
+                               float* sh) {
+  const int T = blockDim.x, CW = min(C, T), J = T / CW;
+  const int t = threadIdx.x, j = t / CW;
+  for (int cb = 0; cb < C; cb += CW) {
+    const int c = cb + t % CW;
     float na = 0.f, mean = 0.f, m2 = 0.f;
-    for (int k = lane; k < chunks; k += 32)
-      chan_merge(na, mean, m2, (float)min(RC, M - k * RC), __ldcg(part + (size_t)k * 2 * C + c),
-                 __ldcg(part + (size_t)k * 2 * C + C + c));
+    if (j < J && c < C) {
+      for (int k = j; k < chunks; k += 8 * J) {
+        float mb[8], qb[8];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const float nb = __shfl_xor_sync(0xffffffffu, na, off), mb = __shfl_xor_sync(0xffffffffu, mean, off),
-                  m2b = __shfl_xor_sync(0xffffffffu, m2, off);
-      if ((lane & off) == 0) chan_merge(na, mean, m2, nb, mb, m2b);
-      else { float a = nb, b = mb, q = m2b; chan_merge(a, b, q, na, mean, m2); na = a; mean = b; m2 = q; }
+        for (int u = 0; u < 8; ++u) {
+          const int kk = k + u * J;
+          mb[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + c) : 0.f;
+          qb[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + C + c) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int kk = k + u * J;
+          if (kk < chunks) chan_merge(na, mean, m2, (float)min(RC, M - kk * RC), mb[u], qb[u]);
+        }
+      }
     }
-    if (lane == 0) {
+    __syncthreads();
+    sh[3 * t] = na; sh[3 * t + 1] = mean; sh[3 * t + 2] = m2;
+    __syncthreads();
+    if (j == 0 && c < C) {
+      for (int l = 1; l < J; ++l) {
+        const float* o = sh + 3 * (l * CW + t);
+        chan_merge(na, mean, m2, o[0], o[1], o[2]);
+      }
       stats[c] = mean;
       stats[C + c] = 1.f / sqrtf(m2 / na + eps);
       stats[2 * C + c] = __bfloat162float(gamma[c]);
@@ -270,7 +289,7 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
 // per chunk of RC rows: sum dy and sum dy*xhat per channel (8 channels per thread, row lanes
 // merged in fixed order) -> part[chunk][2][C]
 __device__ void bn_bwd_merge(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
-                             float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate);
+                             float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate, float* sh);
 
 __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
                                      const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
@@ -326,26 +345,41 @@ __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __r
   __syncthreads();
   if (last) {
     __threadfence();
-    bn_bwd_merge(part, gridDim.x, C, tot, g_gamma, g_beta, accumulate);
+    bn_bwd_merge(part, gridDim.x, C, tot, g_gamma, g_beta, accumulate, sh);
   }
 }
 
-// totals over chunks (warp per channel, fixed order); dgamma/dbeta into the accumulator
+// totals over chunks (layout as bn_stats_merge: lanes over chunks in order, then lanes in
+// order); dgamma/dbeta into the accumulator.  sh: >= 2*T floats.
 __device__ void bn_bwd_merge(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
-                             float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate) {
-  const int nw = blockDim.x >> 5, lane = threadIdx.x & 31;
-  for (int c = threadIdx.x >> 5; c < C; c += nw) {
+                             float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate, float* sh) {
+  const int T = blockDim.x, CW = min(C, T), J = T / CW;
+  const int t = threadIdx.x, j = t / CW;
+  for (int cb = 0; cb < C; cb += CW) {
+    const int c = cb + t % CW;
     float s1 = 0.f, s2 = 0.f;
-    for (int k = lane; k < chunks; k += 32) {
-      s1 = __fadd_rn(s1, __ldcg(part + (size_t)k * 2 * C + c));
-      s2 = __fadd_rn(s2, __ldcg(part + (size_t)k * 2 * C + C + c));
-    }
+    if (j < J && c < C) {
+      for (int k = j; k < chunks; k += 8 * J) {
+        float a[8], b[8];
 #pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      s1 = __fadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, off));
-      s2 = __fadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, off));
+        for (int u = 0; u < 8; ++u) {
+          const int kk = k + u * J;
+          a[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + c) : 0.f;
+          b[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + C + c) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k + u * J < chunks) { s1 = __fadd_rn(s1, a[u]); s2 = __fadd_rn(s2, b[u]); }
+      }
     }
-    if (lane == 0) {
+    __syncthreads();
+    sh[2 * t] = s1; sh[2 * t + 1] = s2;
+    __syncthreads();
+    if (j == 0 && c < C) {
+      for (int l = 1; l < J; ++l) {
+        s1 = __fadd_rn(s1, sh[2 * (l * CW + t)]);
+        s2 = __fadd_rn(s2, sh[2 * (l * CW + t) + 1]);
+      }
       tot[c] = s1;
       tot[C + c] = s2;
       g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
@@ -465,7 +499,9 @@ cudaError_t launch_stage_input_bf16(const float* x, bf16* y, int n, int C, int H
   return cudaGetLastError();
 }
 
-int bn_chunk_rows(int M) { return M <= 2048 ? 32 : 128; }
+// rows per partial chunk: ~128 chunks (enough blocks to spread the read, few enough partials
+// for the last block's merge), multiple of 32
+int bn_chunk_rows(int M) { return std::max(32, ((M + 127) / 128 + 31) / 32 * 32); }
 int bn_chunks(int M) { return (M + bn_chunk_rows(M) - 1) / bn_chunk_rows(M); }
 size_t bn_ws_floats(int M, int C) { return (size_t)bn_chunks(M) * 2 * C + 2 * (size_t)C; }
 

@@ -127,13 +127,15 @@ enum { XP_PROF_SWEEP = 0,       /* K1: work = algorithmic bytes */
        XP_PROF_CONV_FPROP = 1,  /* tcgen05 implicit-GEMM conv forward: work = 2*M*N*K flops */
        XP_PROF_CONV_DGRAD = 2,
        XP_PROF_CONV_WGRAD = 3,
-       XP_PROF_N = 4 };
+       XP_PROF_BN_FWD = 4,      /* BN statistics + apply [+ ReLU + pool]: work = algorithmic bytes */
+       XP_PROF_BN_BWD = 5,      /* BN backward reduce + apply: work = algorithmic bytes */
+       XP_PROF_N = 6 };
 
 typedef struct {
   double span_ms;                    /* reserved */
   double prof_ms[XP_PROF_N];         /* summed device time per kernel class (cfg.profile) */
   int64_t prof_launches[XP_PROF_N];
-  double prof_work[XP_PROF_N];       /* algorithmic bytes (sweep) or flops (GEMM classes) */
+  double prof_work[XP_PROF_N];       /* algorithmic bytes (sweep, BN) or flops (GEMM classes) */
   int64_t kernel_launches;           /* kernels enqueued by this call (directly or in a graph) */
   int64_t graph_replays;             /* 1 if this call replayed a captured CUDA graph */
   float* losses;                     /* optional caller buffer of M*T per-micro-batch mean losses */
@@ -235,6 +237,15 @@ int xpipe_gemm_bf16(const void* A, const void* B, float* D, int32_t M, int32_t N
    geometry: C or Co not a multiple of 8, P/Q inconsistent), XP_ECUDA (launch). */
 int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void* in0, const void* in1, void* out,
                       int32_t accumulate, float* ws, int64_t ws_elems, void* stream);
+
+/* Development probe of the GEMM kernels (not part of the training path).  When the process
+   runs with XPIPE_GEMM_DBG=1 every tensor-core GEMM launch records, per CTA c, 16 uint64 at
+   host[16c ..]: globaltimer ns at start (after the PDL wait), first operand stage ready, all
+   MMAs issued, accumulator ready, end; the SM id; the number of tiles the CTA processed; then
+   (split-K only) partial parked in smem, first cluster barrier passed, cluster reduction done,
+   cross-cluster reduction done.  Each launch overwrites the buffer.  Copies n values (synchronous).  Errors: XP_EINVAL (probe
+   disabled or bad n), XP_ECUDA. */
+int xpipe_dev_gemm_probe(unsigned long long* host, int32_t n);
 
 #ifdef __cplusplus
 }

@@ -56,13 +56,17 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
       XP_TRY(prof_end(c, s, XP_PROF_CONV_FPROP, conv_flops(g, L.in0.c)));
       const LayerInfo& N = c->net.layers[O.lbn];
       const int M = n * O.smid.h * O.smid.w;
+      XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, launch_bn_stats(mid, M, O.smid.c, N.d.bn_eps, W + N.woff, W + N.boff, s.bnws,
                                              s.ctr + kTileCounters - 2, s.stats[o][slot], s.stream), "bn_stats"));
       const PoolGeo p = pool_geo(c, O.lpool);
       uint8_t* pidx = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
-      return check_launch(c, launch_bn_apply(mid, s.stats[o][slot], (bf16*)y, pidx, n, O.smid.h, O.smid.w, O.smid.c,
+      XP_TRY(check_launch(c, launch_bn_apply(mid, s.stats[o][slot], (bf16*)y, pidx, n, O.smid.h, O.smid.w, O.smid.c,
                                              O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0,
-                                             O.relu, s.stream), "bn_apply");
+                                             O.relu, s.stream), "bn_apply"));
+      // algorithmic bytes: mid read twice (statistics, apply), output written (+ pool winners)
+      const double out_elems = (double)n * O.sout.h * O.sout.w * O.sout.c;
+      return prof_end(c, s, XP_PROF_BN_FWD, 4.0 * M * O.smid.c + out_elems * (O.lpool >= 0 ? 3.0 : 2.0));
     }
     case OP_ADD:
       return check_launch(c, launch_add_fwd(x, (const bf16*)s.act[O.in1][slot], (bf16*)y, (int64_t)n * O.sout.size(),
@@ -104,6 +108,7 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       const LayerInfo& N = c->net.layers[O.lbn];
       const PoolGeo p = pool_geo(c, O.lpool);
       bf16* dmid = (bf16*)s.gmid;
+      XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, launch_bn_backward((const bf16*)s.mid[o][slot], (const bf16*)dy,
                                                 (const bf16*)s.act[O.out][slot],
                                                 O.lpool >= 0 ? s.pidx[o][slot] : nullptr, s.stats[o][slot],
@@ -111,6 +116,12 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
                                                 p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws,
                                                 s.ctr + kTileCounters - 1, s.g + N.woff, s.g + N.boff, accumulate_g, dmid, s.stream),
                           "bn_backward"));
+      {
+        // algorithmic bytes: mid, dy, y (+ pool winners) read by both passes, dmid written
+        const double mid_e = (double)n * O.smid.h * O.smid.w * O.smid.c;
+        const double out_e = (double)n * O.sout.h * O.sout.w * O.sout.c;
+        XP_TRY(prof_end(c, s, XP_PROF_BN_BWD, 2.0 * (2.0 * mid_e + out_e * (O.lpool >= 0 ? 5.0 : 4.0)) + 2.0 * mid_e));
+      }
       XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)s.act[O.in0][slot], dmid, s.g + L.woff, accumulate_g, s.ws,
                                            s.ws_elems, s.ctr, s.stream), "conv_wgrad"));

@@ -55,124 +55,131 @@ __device__ __forceinline__ void chan_merge(float& na, float& mean, float& m2, fl
 }
 
 // ---- BN statistics: x [M][C] bf16 -> partial (mean, M2) per row chunk ----------------------
-// block: G = C/8 channel groups x RL = 256/G row lanes; chunk = RC rows; thread keeps
-// Welford (n, mean, M2) for 8 channels; lanes merged in fixed order through smem.
-__device__ void bn_stats_merge(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
-                               const bf16* __restrict__ gamma, const bf16* __restrict__ beta, float* __restrict__ stats,
-                               float* sh);
+// block: G = C/8 channel groups x RL = T/G row lanes; chunk = RC <= kBnRows*RL rows, so every
+// lane keeps its rows in registers.  Two passes over the registers: chunk sum -> chunk mean,
+// then sum of squared deviations from that mean; lanes are combined by a fixed pairwise tree
+// (deterministic, no divisions on the critical path).
+constexpr int kBnRows = 8;
 
-__global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C, int RC, float* __restrict__ part,
-                                        int* __restrict__ counter, float eps, const bf16* __restrict__ gamma,
-                                        const bf16* __restrict__ beta, float* __restrict__ stats) {
-  pdl_wait();
-  extern __shared__ float sh[];  // [RL][G][16] (mean[8], M2[8]) + counts
-  const int G = C / 8, RL = blockDim.x / G;
-  const int g = threadIdx.x % G, rl = threadIdx.x / G;
-  const int r0 = blockIdx.x * RC, r1 = min(M, r0 + RC);
-  float mean[8], m2[8];
-  int cnt = 0;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) { mean[e] = 0.f; m2[e] = 0.f; }
-  if (rl < RL) {
-    for (int r = r0 + rl; r < r1; r += RL) {
-      const uint4 u = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + g * 8);
-      const bf16* v = reinterpret_cast<const bf16*>(&u);
-      ++cnt;
-      const float inv = 1.f / (float)cnt;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float xv = __bfloat162float(v[e]);
-        const float d = xv - mean[e];
-        mean[e] += d * inv;
-        m2[e] += d * (xv - mean[e]);
-      }
+// fixed-order tree over the RL row lanes of slot [rl][G][W] (W floats per (lane, group));
+// the result lands in lane 0.  Every thread of the block must call it.
+__device__ __forceinline__ void lane_tree(float* sh, int RL, int G, int W, int rl, int g) {
+  int p2 = 1;
+  while (p2 < RL) p2 <<= 1;
+  for (int stride = p2 >> 1; stride > 0; stride >>= 1) {
+    __syncthreads();
+    if (rl < stride && rl + stride < RL) {
+      float* d = sh + ((size_t)rl * G + g) * W;
+      const float* o = sh + ((size_t)(rl + stride) * G + g) * W;
+      for (int e = 0; e < W; ++e) d[e] = __fadd_rn(d[e], o[e]);
     }
   }
-  // fixed-order merge over row lanes: lane 0 absorbs lanes 1..RL-1 in order
-  float* slot = sh + ((size_t)rl * G + g) * 17;
-  if (rl < RL) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) { slot[e] = mean[e]; slot[8 + e] = m2[e]; }
-    slot[16] = (float)cnt;
-  }
   __syncthreads();
-  if (rl == 0) {
-    float na = slot[16];
-    for (int l = 1; l < RL; ++l) {
-      const float* o = sh + ((size_t)l * G + g) * 17;
-      const float nb = o[16];
-      if (nb == 0.f) continue;
-      const float nab = na + nb;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float d = o[e] - mean[e];
-        mean[e] += d * (nb / nab);
-        m2[e] += o[8 + e] + d * d * (na * nb / nab);
-      }
-      na = nab;
-    }
-    float* p = part + (size_t)blockIdx.x * 2 * C;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) { p[g * 8 + e] = mean[e]; p[C + g * 8 + e] = m2[e]; }
-  }
-  // the last block to finish merges all chunks (fixed order) -- no separate final launch
-  __shared__ int last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int old = atomicAdd(counter, 1);
-    last = (old == (int)gridDim.x - 1);
-    if (last) *counter = 0;
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    bn_stats_merge(part, gridDim.x, M, RC, C, eps, gamma, beta, stats, sh);
-  }
 }
 
-// Final merge in the last block.  Thread t takes channel c = c0 + t % CW (CW = min(C, T)) and
-// lane j = t / CW of J = T / CW lanes per channel; lane j merges chunks j, j+J, j+2J, ... in
-// order (loads batched 8 deep so L2 latency overlaps), then lane 0 absorbs lanes 1..J-1 in
-// order through shared memory (deterministic).  sh: >= 3*T floats.
-__device__ void bn_stats_merge(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
-                               const bf16* __restrict__ gamma, const bf16* __restrict__ beta, float* __restrict__ stats,
-                               float* sh) {
-  const int T = blockDim.x, CW = min(C, T), J = T / CW;
-  const int t = threadIdx.x, j = t / CW;
-  for (int cb = 0; cb < C; cb += CW) {
-    const int c = cb + t % CW;
-    float na = 0.f, mean = 0.f, m2 = 0.f;
-    if (j < J && c < C) {
-      for (int k = j; k < chunks; k += 8 * J) {
-        float mb[8], qb[8];
+__global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C, int RC, float* __restrict__ part) {
+  pdl_wait();
+  extern __shared__ float sh[];  // [RL][G][8]
+  const int G = C / 8, RL = blockDim.x / G;
+  const int g = threadIdx.x % G, rl = threadIdx.x / G;
+  const bool act = rl < RL;
+  const int r0 = blockIdx.x * RC, r1 = min(M, r0 + RC);
+  uint4 keep[kBnRows];
+  float sum[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int kk = k + u * J;
-          mb[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + c) : 0.f;
-          qb[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + C + c) : 0.f;
-        }
+  for (int e = 0; e < 8; ++e) sum[e] = 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int kk = k + u * J;
-          if (kk < chunks) chan_merge(na, mean, m2, (float)min(RC, M - kk * RC), mb[u], qb[u]);
-        }
-      }
-    }
-    __syncthreads();
-    sh[3 * t] = na; sh[3 * t + 1] = mean; sh[3 * t + 2] = m2;
-    __syncthreads();
-    if (j == 0 && c < C) {
-      for (int l = 1; l < J; ++l) {
-        const float* o = sh + 3 * (l * CW + t);
-        chan_merge(na, mean, m2, o[0], o[1], o[2]);
-      }
-      stats[c] = mean;
-      stats[C + c] = 1.f / sqrtf(m2 / na + eps);
-      stats[2 * C + c] = __bfloat162float(gamma[c]);
-      stats[3 * C + c] = __bfloat162float(beta[c]);
+  for (int k = 0; k < kBnRows; ++k) {
+    const int r = r0 + rl + k * RL;
+    keep[k] = make_uint4(0u, 0u, 0u, 0u);
+    if (act && r < r1) {
+      keep[k] = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + g * 8);
+      const bf16* v = reinterpret_cast<const bf16*>(&keep[k]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sum[e] = __fadd_rn(sum[e], __bfloat162float(v[e]));
     }
   }
+  float* slot = sh + ((size_t)rl * G + g) * 8;
+  if (act)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) slot[e] = sum[e];
+  lane_tree(sh, RL, G, 8, rl, g);
+  const float n = (float)(r1 - r0);
+  float mean[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) mean[e] = act ? sh[(size_t)g * 8 + e] / n : 0.f;
+  __syncthreads();  // everyone has read the sums before the slots are reused
+  float m2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) m2[e] = 0.f;
+#pragma unroll
+  for (int k = 0; k < kBnRows; ++k) {
+    const int r = r0 + rl + k * RL;
+    if (act && r < r1) {
+      const bf16* v = reinterpret_cast<const bf16*>(&keep[k]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = __fsub_rn(__bfloat162float(v[e]), mean[e]);
+        m2[e] = __fadd_rn(m2[e], __fmul_rn(d, d));
+      }
+    }
+  }
+  if (act)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) slot[e] = m2[e];
+  lane_tree(sh, RL, G, 8, rl, g);
+  if (rl == 0) {
+    float* p = part + (size_t)blockIdx.x * 2 * C;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { p[g * 8 + e] = mean[e]; p[C + g * 8 + e] = sh[(size_t)g * 8 + e]; }
+  }
+  pdl_trigger();
+}
+
+// Final merge (its own launch, ceil(C/8) blocks of 256 threads): thread (j, cc) = (tid / 8,
+// tid % 8) takes channel c = 8*blockIdx.x + cc and merges chunks j, j+32, j+64, ... in order
+// (Chan's pairwise formula; loads batched 8 deep), then the 32 lanes of a channel are combined by
+// a fixed pairwise tree in shared memory (deterministic).
+__global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
+                                      const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
+                                      float* __restrict__ stats) {
+  pdl_wait();
+  __shared__ float sh[32][8][3];
+  const int cc = threadIdx.x & 7, j = threadIdx.x >> 3, c = blockIdx.x * 8 + cc;
+  float na = 0.f, mean = 0.f, m2 = 0.f;
+  if (c < C) {
+    for (int k = j; k < chunks; k += 8 * 32) {
+      float mb[8], qb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int kk = k + 32 * u;
+        mb[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + c) : 0.f;
+        qb[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + C + c) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int kk = k + 32 * u;
+        if (kk < chunks) chan_merge(na, mean, m2, (float)min(RC, M - kk * RC), mb[u], qb[u]);
+      }
+    }
+  }
+  sh[j][cc][0] = na; sh[j][cc][1] = mean; sh[j][cc][2] = m2;
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    __syncthreads();
+    if (j < stride) {
+      float a = sh[j][cc][0], b = sh[j][cc][1], q = sh[j][cc][2];
+      chan_merge(a, b, q, sh[j + stride][cc][0], sh[j + stride][cc][1], sh[j + stride][cc][2]);
+      sh[j][cc][0] = a; sh[j][cc][1] = b; sh[j][cc][2] = q;
+    }
+  }
+  __syncthreads();
+  if (j == 0 && c < C) {
+    stats[c] = sh[0][cc][1];
+    stats[C + c] = 1.f / sqrtf(sh[0][cc][2] / sh[0][cc][0] + eps);
+    stats[2 * C + c] = __bfloat162float(gamma[c]);
+    stats[3 * C + c] = __bfloat162float(beta[c]);
+  }
+  pdl_trigger();
 }
 
 // ---- BN-apply [+ ReLU] [+ pool] ----------------------------------------------------------
@@ -287,15 +294,11 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
 }
 
 // per chunk of RC rows: sum dy and sum dy*xhat per channel (8 channels per thread, row lanes
-// merged in fixed order) -> part[chunk][2][C]
-__device__ void bn_bwd_merge(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
-                             float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate, float* sh);
+// combined by a fixed tree) -> part[chunk][2][C]
 
 __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
                                      const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
-                                     const float* __restrict__ st, BwdGeo G, int M, int RC, float* __restrict__ part,
-                                     int* __restrict__ counter, float* __restrict__ tot, float* __restrict__ g_gamma,
-                                     float* __restrict__ g_beta, int accumulate) {
+                                     const float* __restrict__ st, BwdGeo G, int M, int RC, float* __restrict__ part) {
   pdl_wait();
   extern __shared__ float sh[];
   const int C = G.C, NG = C / 8, RL = blockDim.x / NG;
@@ -305,8 +308,10 @@ __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __r
   float s1[8], s2[8], mean[8], rstd[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) { s1[e] = 0.f; s2[e] = 0.f; mean[e] = st[c0 + e]; rstd[e] = st[C + c0 + e]; }
-  if (rl < RL)
-    for (int r = r0 + rl; r < r1; r += RL) {
+#pragma unroll
+  for (int k = 0; k < kBnRows; ++k) {  // RC <= kBnRows*RL: every row of the lane, loads in flight together
+    const int r = r0 + rl + k * RL;
+    if (rl < RL && r < r1) {
       const int w = r % G.W, t = r / G.W, h = t % G.H, sidx = t / G.H;
       float dy[8];
       routed_dy8(dout, y, pidx, G, sidx, h, w, c0, dy);
@@ -319,73 +324,59 @@ __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __r
         s2[e] = __fadd_rn(s2[e], __fmul_rn(dy[e], xh));
       }
     }
+  }
   float* slot = sh + ((size_t)rl * NG + g) * 16;
   if (rl < RL)
 #pragma unroll
     for (int e = 0; e < 8; ++e) { slot[e] = s1[e]; slot[8 + e] = s2[e]; }
-  __syncthreads();
+  lane_tree(sh, RL, NG, 16, rl, g);
   if (rl == 0) {
-    for (int l = 1; l < RL; ++l) {
-      const float* o = sh + ((size_t)l * NG + g) * 16;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) { s1[e] = __fadd_rn(s1[e], o[e]); s2[e] = __fadd_rn(s2[e], o[8 + e]); }
-    }
     float* p = part + (size_t)blockIdx.x * 2 * C;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) { p[c0 + e] = s1[e]; p[C + c0 + e] = s2[e]; }
+    for (int e = 0; e < 8; ++e) { p[c0 + e] = slot[e]; p[C + c0 + e] = slot[8 + e]; }
   }
-  __shared__ int last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int old = atomicAdd(counter, 1);
-    last = (old == (int)gridDim.x - 1);
-    if (last) *counter = 0;
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    bn_bwd_merge(part, gridDim.x, C, tot, g_gamma, g_beta, accumulate, sh);
-  }
+  pdl_trigger();
 }
 
-// totals over chunks (layout as bn_stats_merge: lanes over chunks in order, then lanes in
-// order); dgamma/dbeta into the accumulator.  sh: >= 2*T floats.
-__device__ void bn_bwd_merge(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
-                             float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate, float* sh) {
-  const int T = blockDim.x, CW = min(C, T), J = T / CW;
-  const int t = threadIdx.x, j = t / CW;
-  for (int cb = 0; cb < C; cb += CW) {
-    const int c = cb + t % CW;
-    float s1 = 0.f, s2 = 0.f;
-    if (j < J && c < C) {
-      for (int k = j; k < chunks; k += 8 * J) {
-        float a[8], b[8];
+// totals over chunks (layout as bn_stats_final_kernel: 32 lanes per channel over chunks in
+// order, then a fixed tree); dgamma/dbeta into the accumulator
+__global__ void bn_bwd_final_kernel(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
+                                    float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate) {
+  pdl_wait();
+  __shared__ float sh[32][8][2];
+  const int cc = threadIdx.x & 7, j = threadIdx.x >> 3, c = blockIdx.x * 8 + cc;
+  float s1 = 0.f, s2 = 0.f;
+  if (c < C) {
+    for (int k = j; k < chunks; k += 8 * 32) {
+      float a[8], b[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int kk = k + u * J;
-          a[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + c) : 0.f;
-          b[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + C + c) : 0.f;
-        }
+      for (int u = 0; u < 8; ++u) {
+        const int kk = k + 32 * u;
+        a[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + c) : 0.f;
+        b[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + C + c) : 0.f;
+      }
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (k + u * J < chunks) { s1 = __fadd_rn(s1, a[u]); s2 = __fadd_rn(s2, b[u]); }
-      }
-    }
-    __syncthreads();
-    sh[2 * t] = s1; sh[2 * t + 1] = s2;
-    __syncthreads();
-    if (j == 0 && c < C) {
-      for (int l = 1; l < J; ++l) {
-        s1 = __fadd_rn(s1, sh[2 * (l * CW + t)]);
-        s2 = __fadd_rn(s2, sh[2 * (l * CW + t) + 1]);
-      }
-      tot[c] = s1;
-      tot[C + c] = s2;
-      g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
-      g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
+      for (int u = 0; u < 8; ++u)
+        if (k + 32 * u < chunks) { s1 = __fadd_rn(s1, a[u]); s2 = __fadd_rn(s2, b[u]); }
     }
   }
+  sh[j][cc][0] = s1; sh[j][cc][1] = s2;
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    __syncthreads();
+    if (j < stride) {
+      sh[j][cc][0] = __fadd_rn(sh[j][cc][0], sh[j + stride][cc][0]);
+      sh[j][cc][1] = __fadd_rn(sh[j][cc][1], sh[j + stride][cc][1]);
+    }
+  }
+  __syncthreads();
+  if (j == 0 && c < C) {
+    s1 = sh[0][cc][0]; s2 = sh[0][cc][1];
+    tot[c] = s1;
+    tot[C + c] = s2;
+    g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
+    g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
+  }
+  pdl_trigger();
 }
 
 // dx = Q(gamma_b * rstd * (dy - sum(dy)/cnt - xhat * sum(dy xhat)/cnt)), 8 channels per thread
@@ -499,20 +490,27 @@ cudaError_t launch_stage_input_bf16(const float* x, bf16* y, int n, int C, int H
   return cudaGetLastError();
 }
 
-// rows per partial chunk: ~128 chunks (enough blocks to spread the read, few enough partials
-// for the last block's merge), multiple of 32
-int bn_chunk_rows(int M) { return std::max(32, ((M + 127) / 128 + 31) / 32 * 32); }
-int bn_chunks(int M) { return (M + bn_chunk_rows(M) - 1) / bn_chunk_rows(M); }
-size_t bn_ws_floats(int M, int C) { return (size_t)bn_chunks(M) * 2 * C + 2 * (size_t)C; }
+// block shape of the BN reductions: G = C/8 channel groups x RL row lanes (256 threads, or G)
+int bn_threads(int C) { const int G = C / 8; return G >= 256 ? G : (256 / G) * G; }
+// rows per partial chunk: ~512 chunks (many blocks, one to a few rows per lane so every load
+// is in flight at once), at most kBnRows rows per lane (register-resident two passes)
+int bn_chunk_rows(int M, int C) {
+  const int RL = bn_threads(C) / (C / 8);
+  return std::max(1, std::min(std::max(RL, (M + 511) / 512), kBnRows * RL));
+}
+int bn_chunks(int M, int C) { return (M + bn_chunk_rows(M, C) - 1) / bn_chunk_rows(M, C); }
+size_t bn_ws_floats(int M, int C) { return (size_t)bn_chunks(M, C) * 2 * C + 2 * (size_t)C; }
 
 cudaError_t launch_bn_stats(const bf16* x, int M, int C, float eps, const bf16* gamma, const bf16* beta, float* ws,
                             int* counter, float* stats, cudaStream_t st) {
   if (C % 8 || C > 2048) return cudaErrorInvalidValue;
-  const int RC = bn_chunk_rows(M), chunks = bn_chunks(M);
-  const int G = C / 8;
-  const int threads = G >= 256 ? G : (256 / G) * G;
-  const size_t shm = (size_t)(threads / G) * G * 17 * 4;
-  launch_pdl(bn_stats_partial_kernel, dim3(chunks), dim3(threads), shm, st, x, M, C, RC, ws, counter, eps, gamma, beta, stats);
+  const int RC = bn_chunk_rows(M, C), chunks = bn_chunks(M, C);
+  const int threads = bn_threads(C);
+  const size_t shm = (size_t)threads * 8 * 4;
+  (void)counter;
+  launch_pdl(bn_stats_partial_kernel, dim3(chunks), dim3(threads), shm, st, x, M, C, RC, ws);
+  launch_pdl(bn_stats_final_kernel, dim3((C + 7) / 8), dim3(256), 0, st, (const float*)ws, chunks, M, RC, C, eps, gamma,
+             beta, stats);
   return cudaGetLastError();
 }
 
@@ -531,14 +529,15 @@ cudaError_t launch_bn_backward(const bf16* x, const bf16* dout, const bf16* y, c
   if (C % 8 || C > 2048) return cudaErrorInvalidValue;
   BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
   const int M = n * H * W;
-  const int RC = bn_chunk_rows(M), chunks = bn_chunks(M);
-  const int NG = C / 8;
-  const int threads = NG >= 256 ? NG : (256 / NG) * NG;
+  const int RC = bn_chunk_rows(M, C), chunks = bn_chunks(M, C);
+  const int threads = bn_threads(C);
   const size_t shm = (size_t)threads * 16 * 4;
   float* tot = ws + (size_t)chunks * 2 * C;
-  launch_pdl(bn_bwd_reduce_kernel, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC, ws, counter, tot, g_gamma,
-                                                     g_beta, accumulate ? 1 : 0);
-  launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * NG)), dim3(256), 0, st, x, dout, y, pidx, stats, tot, gamma_b, G, M, dx);
+  (void)counter;
+  launch_pdl(bn_bwd_reduce_kernel, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC, ws);
+  launch_pdl(bn_bwd_final_kernel, dim3((C + 7) / 8), dim3(256), 0, st, (const float*)ws, chunks, C, tot, g_gamma, g_beta,
+             accumulate ? 1 : 0);
+  launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats, tot, gamma_b, G, M, dx);
   return cudaGetLastError();
 }
 

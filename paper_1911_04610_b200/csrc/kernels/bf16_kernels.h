@@ -5,7 +5,7 @@
 #include <stdint.h>
 
 namespace xp {
-int bn_chunks(int M);
+int bn_chunks(int M, int C);
 size_t bn_ws_floats(int M, int C);
 // stats [4][C]: mean, rstd, gamma_f, beta_f (the forward's affine parameters)
 // counter: one zero-initialised int owned by the calling stream (last-block merge)

@@ -19,6 +19,7 @@
 // rows [z*128/cs, (z+1)*128/cs) of all cs tiles over DSMEM in the fixed order 0..cs-1 and
 // applies the epilogue.  No atomics, no workspace, deterministic.
 #include <algorithm>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 
@@ -32,12 +33,11 @@ namespace xp {
 namespace {
 
 constexpr int BM = 128, BK = 64;
-// smem ring depth by N tile (~192 KB of stages): more loads in flight for the narrow tiles,
-// whose k-blocks are short relative to the global-memory latency
-// smem ring depth by N tile: 96 KB (two CTAs per SM) for BN <= 128, 144 KB for BN = 256
-template <int BN> struct Depth { static constexpr int ST = BN == 64 ? 4 : 3; static constexpr int LAG = ST - 1; };
 constexpr int kMaxCluster = 8;
-constexpr int NTHREADS = 256;  // warps 0-3 producers, warp 4 MMA issuer, warps 4-7 epilogue
+// warps 0-3 operand producers (one elected thread when both operands go by TMA), warp 4 the
+// MMA issuer, warps 5-8 the epilogue (TMEM lane quadrant = warp % 4)
+constexpr int NTHREADS = 288;
+constexpr int kMaxSmem = 227 * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -312,11 +312,33 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
   if (a.epi == EPI_BF16) {
     bf16* o = static_cast<bf16*>(a.out) + (int64_t)row * a.ldo + col0;
     if (a.accumulate) {  // fan-out tensor: out = Q(old + Q(acc)) (the oracle's rounding points)
-      for (int e = 0; e < 32; ++e)
-        if (col0 + e < a.N) {
-          const float g = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[e])));
-          o[e] = __float2bfloat16_rn(__fadd_rn(__bfloat162float(o[e]), g));
+#pragma unroll
+      for (int e0 = 0; e0 < 32; e0 += 8) {
+        if (col0 + e0 + 8 <= a.N) {
+          const uint4 u = *reinterpret_cast<const uint4*>(o + e0);
+          const bf16* ov = reinterpret_cast<const bf16*>(&u);
+          uint32_t w[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            float r[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const int e = e0 + 2 * h + t;
+              const float g = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[e])));
+              r[t] = __fadd_rn(__bfloat162float(ov[2 * h + t]), g);
+            }
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(r[0], r[1]);
+            w[h] = *reinterpret_cast<uint32_t*>(&t2);
+          }
+          *reinterpret_cast<uint4*>(o + e0) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+          for (int e = e0; e < e0 + 8; ++e)
+            if (col0 + e < a.N) {
+              const float g = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[e])));
+              o[e] = __float2bfloat16_rn(__fadd_rn(__bfloat162float(o[e]), g));
+            }
         }
+      }
       return;
     }
 #pragma unroll
@@ -347,15 +369,20 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
       }
     }
   } else {  // EPI_WGRAD_T: g[co][m] (=|+=) D[m][co]; lanes = consecutive m -> coalesced
-    float* g = static_cast<float*>(a.out);
-#pragma unroll 4
-    for (int e = 0; e < 32; ++e) {
-      const int co = col0 + e;
-      if (co < a.N) {
-        float* p = g + (int64_t)co * a.ldo + row;
-        const float x = __uint_as_float(v[e]);
-        *p = a.accumulate ? __fadd_rn(*p, x) : x;
-      }
+    float* g = static_cast<float*>(a.out) + (int64_t)col0 * a.ldo + row;
+#pragma unroll
+    for (int e0 = 0; e0 < 32; e0 += 8) {
+      // the 8 old values are loaded together (independent addresses), then stored
+      float old[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        old[e] = (a.accumulate && col0 + e0 + e < a.N) ? __ldcg(g + (int64_t)(e0 + e) * a.ldo) : 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (col0 + e0 + e < a.N) {
+          const float x = __uint_as_float(v[e0 + e]);
+          g[(int64_t)(e0 + e) * a.ldo] = a.accumulate ? __fadd_rn(old[e], x) : x;
+        }
     }
   }
 }
@@ -388,125 +415,168 @@ __device__ __forceinline__ void epi_store8(const GemmArgs& a, int row, int col0,
     for (int e = 0; e < 8; ++e)
       if (col0 + e < a.N) o[e] = v[e];
   } else {
-    float* g = static_cast<float*>(a.out);
+    float* g = static_cast<float*>(a.out) + (int64_t)col0 * a.ldo + row;
+    float old[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) old[e] = (a.accumulate && col0 + e < a.N) ? __ldcg(g + (int64_t)e * a.ldo) : 0.f;
+#pragma unroll
     for (int e = 0; e < 8; ++e)
-      if (col0 + e < a.N) {
-        float* p = g + (int64_t)(col0 + e) * a.ldo + row;
-        *p = a.accumulate ? __fadd_rn(*p, v[e]) : v[e];
-      }
+      if (col0 + e < a.N) g[(int64_t)e * a.ldo] = a.accumulate ? __fadd_rn(old[e], v[e]) : v[e];
   }
 }
 
-template <int MODE, int BN>
-struct ALoader;
-template <int BN> struct ALoader<GEMM_FPROP, BN> { typedef FpropA T; };
-template <int BN> struct ALoader<GEMM_DGRAD, BN> { typedef DgradA T; };
-template <int BN> struct ALoader<GEMM_WGRAD, BN> { typedef WgradA T; };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ring position: slot and phase advance together (runtime depth)
+struct Ring {
+  int slot, st;
+  uint32_t phase;
+  __device__ explicit Ring(int s) : slot(0), st(s), phase(0) {}
+  __device__ void next() {
+    if (++slot == st) { slot = 0; phase ^= 1u; }
+  }
+};
+
+// one unit of a CTA's work: an output tile and its k-block range.  Split-K: one unit per CTA
+// (tile blockIdx.xy, k range blockIdx.z); otherwise persistent: tiles blockIdx.x, +gridDim.x, ...
+struct Work { int m0, n0, kb0, nkb; };
+__device__ __forceinline__ int local_units(const GemmArgs& a, int ntiles) {
+  if (a.splits > 1) return 1;
+  return (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+}
+template <int BN>
+__device__ __forceinline__ Work work_of(const GemmArgs& a, int j, int mt) {
+  Work w;
+  const int nkb_total = (a.K + BK - 1) / BK;
+  if (a.splits > 1) {
+    w.m0 = blockIdx.x * BM; w.n0 = blockIdx.y * BN;
+    w.kb0 = blockIdx.z * a.kb_per_split;
+    w.nkb = max(0, min(nkb_total, w.kb0 + a.kb_per_split) - w.kb0);
+  } else {
+    const int t = (int)blockIdx.x + j * (int)gridDim.x;  // m fastest: concurrent CTAs share B tiles
+    w.m0 = (t % mt) * BM; w.n0 = (t / mt) * BN; w.kb0 = 0; w.nkb = nkb_total;
+  }
+  return w;
+}
 
 template <int MODE, int BN, bool A_MN, bool B_MN>
 __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* tmA, const CUtensorMap* tmB, uint32_t base,
-                                         uint32_t full0, uint32_t empty0, int m0, int n0, int kb0, int nkb, int tid) {
+                                         uint32_t full0, uint32_t empty0, int nunits, int mt, int tid) {
   constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
-  constexpr int ST = Depth<BN>::ST, LAG = Depth<BN>::LAG;
-  // operand loaders
-  DenseK<BM> pak; DenseMN<BM> pam; DenseK<BN> pbk; DenseMN<BN> pbm;
-  FpropA fa; DgradA da; WgradA wa; DgradB<BN> db;
-  if (MODE == GEMM_PLAIN) {
-    if (A_MN) pam.init(a.A, a.lda, a.M, a.K, m0); else pak.init(a.A, a.lda, a.M, a.K, m0);
-    if (B_MN) pbm.init(a.B, a.ldb, a.N, a.K, n0); else pbk.init(a.B, a.ldb, a.N, a.K, n0);
-  } else if (MODE == GEMM_FPROP) {
-    fa.init(a, m0, tid);
-    pbk.init(a.B, a.K, a.N, a.K, n0);           // W [Co][R*S*C]
-  } else if (MODE == GEMM_DGRAD) {
-    da.init(a, m0, tid);
-    db.init(a, n0);
-  } else {
-    wa.init(a, m0, tid);
-    pbm.init(a.B, a.g.Co, a.N, a.K, n0);        // dY [pixels][Co]
-  }
+  Ring ring(a.stages);
   if (a.a_tma) {
     // full-TMA pipeline: one elected thread streams both operands; the others are idle
     if (tid != 0) return;
-    int tn = 0, tp = 0, tq = 0;  // pixel origin of the tile's rows (fprop / dgrad)
-    if (MODE != GEMM_WGRAD) {
-      tn = m0 / (a.gq * a.gp);
-      const int rem = m0 - tn * a.gq * a.gp;
-      tp = rem / a.gq; tq = rem - tp * a.gq;
-    }
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % ST, it = i / ST, kb = kb0 + i;
-      if (it > 0) mbar_wait(empty0 + 8 * s, (it - 1) & 1);
-      const uint32_t sa = base + s * STAGE, sb = sa + A_BYTES, full = full0 + 8 * s;
-      const int k0 = kb * BK;
-      if (MODE == GEMM_FPROP) {
-        mbar_expect_tx(full, STAGE);
-        const int tap = k0 / a.g.C, c0 = k0 - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
-        tma_4d(sa, tmA, c0, tq + ss - a.g.pw, tp + r - a.g.ph, tn, full);
-        tma_2d(sb, tmB, k0, n0, full);
-      } else if (MODE == GEMM_DGRAD) {
-        mbar_expect_tx(full, STAGE);
-        const int tap = k0 / a.g.Co, c0 = k0 - tap * a.g.Co, r = tap / a.g.S, ss = tap - r * a.g.S;
-        tma_4d(sa, tmA, c0, tq + a.g.pw - ss, tp + a.g.ph - r, tn, full);
+    for (int j = 0; j < nunits; ++j) {
+      const Work w = work_of<BN>(a, j, mt);
+      int tn = 0, tp = 0, tq = 0;  // pixel origin of the tile's rows (fprop / dgrad)
+      if (MODE != GEMM_WGRAD) {
+        tn = w.m0 / (a.gq * a.gp);
+        const int rem = w.m0 - tn * a.gq * a.gp;
+        tp = rem / a.gq; tq = rem - tp * a.gq;
+      }
+      for (int i = 0; i < w.nkb; ++i, ring.next()) {
+        mbar_wait(empty0 + 8 * ring.slot, ring.phase ^ 1u);
+        const uint32_t sa = base + ring.slot * STAGE, sb = sa + A_BYTES, full = full0 + 8 * ring.slot;
+        const int k0 = (w.kb0 + i) * BK;
+        if (MODE == GEMM_FPROP) {
+          mbar_expect_tx(full, STAGE);
+          const int tap = k0 / a.g.C, c0 = k0 - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
+          tma_4d(sa, tmA, c0, tq + ss - a.g.pw, tp + r - a.g.ph, tn, full);
+          tma_2d(sb, tmB, k0, w.n0, full);
+        } else if (MODE == GEMM_DGRAD) {
+          mbar_expect_tx(full, STAGE);
+          const int tap = k0 / a.g.Co, c0 = k0 - tap * a.g.Co, r = tap / a.g.S, ss = tap - r * a.g.S;
+          tma_4d(sa, tmA, c0, tq + a.g.pw - ss, tp + a.g.ph - r, tn, full);
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j) tma_3d(sb + j * (BK * 128), tmB, n0 + 64 * j, tap, c0, full);
-      } else if (MODE == GEMM_WGRAD) {
-        const int pn = k0 / (a.gq * a.gp), rem = k0 - pn * a.gq * a.gp, pp = rem / a.gq, pq = rem - pp * a.gq;
-        const int nch = min(2, (a.M - m0 + 63) / 64);
-        mbar_expect_tx(full, (uint32_t)(nch * BK * 128 + BN * BK * 2));
-        for (int j = 0; j < nch; ++j) {
-          const int mm = m0 + 64 * j, tap = mm / a.g.C, c0 = mm - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
-          tma_4d(sa + j * (BK * 128), tmA, c0, pq + ss - a.g.pw, pp + r - a.g.ph, pn, full);
+          for (int q = 0; q < BN / 64; ++q) tma_3d(sb + q * (BK * 128), tmB, w.n0 + 64 * q, tap, c0, full);
+        } else if (MODE == GEMM_WGRAD) {
+          const int pn = k0 / (a.gq * a.gp), rem = k0 - pn * a.gq * a.gp, pp = rem / a.gq, pq = rem - pp * a.gq;
+          const int nch = min(2, (a.M - w.m0 + 63) / 64);
+          mbar_expect_tx(full, (uint32_t)(nch * BK * 128 + BN * BK * 2));
+          for (int q = 0; q < nch; ++q) {
+            const int mm = w.m0 + 64 * q, tap = mm / a.g.C, c0 = mm - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
+            tma_4d(sa + q * (BK * 128), tmA, c0, pq + ss - a.g.pw, pp + r - a.g.ph, pn, full);
+          }
+#pragma unroll
+          for (int q = 0; q < BN / 64; ++q) tma_2d(sb + q * (BK * 128), tmB, w.n0 + 64 * q, k0, full);
         }
-#pragma unroll
-        for (int j = 0; j < BN / 64; ++j) tma_2d(sb + j * (BK * 128), tmB, n0 + 64 * j, k0, full);
       }
     }
     return;
   }
-  for (int i = 0; i < nkb; ++i) {
-    const int s = i % ST, it = i / ST, kb = kb0 + i;
-    if (it > 0) mbar_wait(empty0 + 8 * s, (it - 1) & 1);
-    const uint32_t sa = base + s * STAGE, sb = sa + A_BYTES;
-    const uint32_t full = full0 + 8 * s;
-    if (a.b_tma) {
-      if (tid == 0) {  // one elected thread moves the whole B tile with the TMA engine
+  // cp.async gather of A (and of B unless b_tma): the full barrier of k-block g is arrived
+  // once its group has landed, LAG groups later (stages >= LAG + 1 keeps the ring live)
+  constexpr int LAG = 3;
+  Ring arr(a.stages);
+  int issued = 0, arrived = 0;
+  for (int j = 0; j < nunits; ++j) {
+    const Work w = work_of<BN>(a, j, mt);
+    DenseK<BM> pak; DenseMN<BM> pam; DenseK<BN> pbk; DenseMN<BN> pbm;
+    FpropA fa; DgradA da; WgradA wa; DgradB<BN> db;
+    if (MODE == GEMM_PLAIN) {
+      if (A_MN) pam.init(a.A, a.lda, a.M, a.K, w.m0); else pak.init(a.A, a.lda, a.M, a.K, w.m0);
+      if (B_MN) pbm.init(a.B, a.ldb, a.N, a.K, w.n0); else pbk.init(a.B, a.ldb, a.N, a.K, w.n0);
+    } else if (MODE == GEMM_FPROP) {
+      fa.init(a, w.m0, tid);
+      pbk.init(a.B, a.K, a.N, a.K, w.n0);           // W [Co][R*S*C]
+    } else if (MODE == GEMM_DGRAD) {
+      da.init(a, w.m0, tid);
+      db.init(a, w.n0);
+    } else {
+      wa.init(a, w.m0, tid);
+      pbm.init(a.B, a.g.Co, a.N, a.K, w.n0);        // dY [pixels][Co]
+    }
+    for (int i = 0; i < w.nkb; ++i, ring.next()) {
+      const int kb = w.kb0 + i;
+      mbar_wait(empty0 + 8 * ring.slot, ring.phase ^ 1u);
+      const uint32_t sa = base + ring.slot * STAGE, sb = sa + A_BYTES;
+      const uint32_t full = full0 + 8 * ring.slot;
+      if (a.b_tma && tid == 0) {  // one elected thread moves the whole B tile with the TMA engine
         mbar_expect_tx(full, BN * BK * 2);
         const int k0 = kb * BK;
         if (a.b_tma == 1) {
-          tma_2d(sb, tmB, k0, n0, full);
+          tma_2d(sb, tmB, k0, w.n0, full);
         } else if (a.b_tma == 2) {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) tma_2d(sb + j * (BK * 128), tmB, n0 + 64 * j, k0, full);
+          for (int q = 0; q < BN / 64; ++q) tma_2d(sb + q * (BK * 128), tmB, w.n0 + 64 * q, k0, full);
         } else {
           const int tap = k0 / a.g.Co, co0 = k0 - tap * a.g.Co;
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) tma_3d(sb + j * (BK * 128), tmB, n0 + 64 * j, tap, co0, full);
+          for (int q = 0; q < BN / 64; ++q) tma_3d(sb + q * (BK * 128), tmB, w.n0 + 64 * q, tap, co0, full);
         }
       }
-    }
-    if (MODE == GEMM_PLAIN) {
-      if (A_MN) pam.load(sa, kb, tid); else pak.load(sa, kb, tid);
-      if (!a.b_tma) { if (B_MN) pbm.load(sb, kb, tid); else pbk.load(sb, kb, tid); }
-    } else if (MODE == GEMM_FPROP) {
-      fa.load(sa, kb, tid);
-      if (!a.b_tma) pbk.load(sb, kb, tid);
-    } else if (MODE == GEMM_DGRAD) {
-      da.load(sa, kb, tid);
-      if (!a.b_tma) db.load(sb, kb, tid);
-    } else {
-      wa.load(sa, kb, tid);
-      if (!a.b_tma) pbm.load(sb, kb, tid);
-    }
-    cp_commit();
-    if (i >= LAG) {
-      cp_wait<LAG>();
-      fence_proxy_async();
-      mbar_arrive(full0 + 8 * ((i - LAG) % ST));
+      if (MODE == GEMM_PLAIN) {
+        if (A_MN) pam.load(sa, kb, tid); else pak.load(sa, kb, tid);
+        if (!a.b_tma) { if (B_MN) pbm.load(sb, kb, tid); else pbk.load(sb, kb, tid); }
+      } else if (MODE == GEMM_FPROP) {
+        fa.load(sa, kb, tid);
+        if (!a.b_tma) pbk.load(sb, kb, tid);
+      } else if (MODE == GEMM_DGRAD) {
+        da.load(sa, kb, tid);
+        if (!a.b_tma) db.load(sb, kb, tid);
+      } else {
+        wa.load(sa, kb, tid);
+        if (!a.b_tma) pbm.load(sb, kb, tid);
+      }
+      cp_commit();
+      ++issued;
+      if (issued > LAG) {
+        cp_wait<LAG>();
+        fence_proxy_async();
+        mbar_arrive(full0 + 8 * arr.slot);
+        arr.next();
+        ++arrived;
+      }
     }
   }
   cp_wait<0>();
   fence_proxy_async();
-  for (int i = max(0, nkb - LAG); i < nkb; ++i) mbar_arrive(full0 + 8 * (i % ST));
+  for (; arrived < issued; ++arrived, arr.next()) mbar_arrive(full0 + 8 * arr.slot);
 }
 
 template <int MODE, int BN, bool A_MN, bool B_MN>
@@ -514,31 +584,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
                                                                const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
   constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
-  constexpr int ST = Depth<BN>::ST;
+  const int ST = a.stages;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023) & ~1023u;
   const uint32_t bars = base + ST * STAGE;
-  const uint32_t full0 = bars, empty0 = bars + 8 * ST, accum = bars + 16 * ST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars - raw) + 16 * ST + 8);
+  // full[ST], empty[ST], acc_full[2], acc_empty[2], TMEM address slot
+  const uint32_t full0 = bars, empty0 = bars + 8 * ST, accf0 = bars + 16 * ST, acce0 = accf0 + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars - raw) + 16 * ST + 32);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int nkb_total = (a.K + BK - 1) / BK;
-  const int kb0 = blockIdx.z * a.kb_per_split;
-  const int nkb = max(0, min(nkb_total, kb0 + a.kb_per_split) - kb0);
+  const int mt = (a.M + BM - 1) / BM, ntiles = mt * ((a.N + BN - 1) / BN);
+  const int nunits = local_units(a, ntiles);
 
   if (tid == 0) {
+    if (a.a_tma) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+    if (a.b_tma) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
     for (int s = 0; s < ST; ++s) {
       // 128 cp.async arrivals (+ the TMA expect_tx), or the TMA thread's alone
       mbar_init(full0 + 8 * s, a.a_tma ? 1 : (a.b_tma ? 129 : 128));
       mbar_init(empty0 + 8 * s, 1);
     }
-    mbar_init(accum, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {
+  if (warp == 4) {  // two accumulators of BN columns (double-buffered across tiles)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -546,62 +620,84 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // the prologue above overlapped the previous kernel; its outputs are visible now
+  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (a.dbg && tid == 0) a.dbg[cta * 16 + 0] = gtimer();
 
   if (warp < 4) {
-    producer<MODE, BN, A_MN, B_MN>(a, &tmA, &tmB, base, full0, empty0, m0, n0, kb0, nkb, tid);
+    producer<MODE, BN, A_MN, B_MN>(a, &tmA, &tmB, base, full0, empty0, nunits, mt, tid);
     __syncwarp();  // reconverge (the TMA producer is one thread) before the aligned barriers
-  } else {
-    if (warp == 4 && lane == 0) {
+  } else if (warp == 4) {
+    if (lane == 0) {
       const uint32_t id = idesc<BN, A_MN, B_MN>();
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % ST, it = i / ST;
-        mbar_wait(full0 + 8 * s, it & 1);
+      Ring ring(ST);
+      for (int j = 0; j < nunits; ++j) {
+        const Work w = work_of<BN>(a, j, mt);
+        const int buf = j & 1;
+        mbar_wait(acce0 + 8 * buf, ((uint32_t)(j >> 1) & 1u) ^ 1u);  // accumulator drained
         tc_fence_after();
-        const uint32_t sa = base + s * STAGE, sb = sa + A_BYTES;
+        const uint32_t d = tmem + (uint32_t)(buf * BN);
+        for (int i = 0; i < w.nkb; ++i, ring.next()) {
+          mbar_wait(full0 + 8 * ring.slot, ring.phase);
+          if (a.dbg && j == 0 && i == 0) a.dbg[cta * 16 + 1] = gtimer();
+          tc_fence_after();
+          const uint32_t sa = base + ring.slot * STAGE, sb = sa + A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint64_t ad = A_MN ? sdesc(sa + kk * 2048, BK * 128, 1024) : sdesc(sa + kk * 32, 16, 1024);
-          const uint64_t bd = B_MN ? sdesc(sb + kk * 2048, BK * 128, 1024) : sdesc(sb + kk * 32, 16, 1024);
-          umma(tmem, ad, bd, id, (i > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? sdesc(sa + kk * 2048, BK * 128, 1024) : sdesc(sa + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? sdesc(sb + kk * 2048, BK * 128, 1024) : sdesc(sb + kk * 32, 16, 1024);
+            umma(d, ad, bd, id, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(empty0 + 8 * ring.slot);
         }
-        umma_commit(empty0 + 8 * s);
+        umma_commit(accf0 + 8 * buf);
       }
-      umma_commit(accum);
+      if (a.dbg) a.dbg[cta * 16 + 2] = gtimer();
       pdl_trigger();
     }
     __syncwarp();
   }
   constexpr int LDS = BN + 4;  // fp32 staging row pitch of the split-K reduction (bank skew)
-  const int q = warp & 3;
-  const int row = m0 + q * 32 + lane;
+  const int q = warp & 3;      // TMEM lane quadrant of an epilogue warp
   if (a.splits <= 1) {
-    if (warp >= 4) {
-      mbar_wait(accum, 0);
-      tc_fence_after();
+    if (warp >= 5) {
+      for (int j = 0; j < nunits; ++j) {
+        const Work w = work_of<BN>(a, j, mt);
+        const int buf = j & 1;
+        mbar_wait(accf0 + 8 * buf, (uint32_t)(j >> 1) & 1u);
+        if (a.dbg && j == 0 && warp == 5 && lane == 0) a.dbg[cta * 16 + 3] = gtimer();
+        tc_fence_after();
+        const int row = w.m0 + q * 32 + lane;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
-        if (nkb > 0) {
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-        } else {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t v[32];
+          if (w.nkb > 0) {
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + c0), v);
+          } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = 0u;
+            for (int e = 0; e < 32; ++e) v[e] = 0u;
+          }
+          if (w.n0 + c0 < a.N) epi_store(a, row, w.n0 + c0, v);
         }
-        if (n0 + c0 < a.N) epi_store(a, row, n0 + c0, v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acce0 + 8 * buf);
       }
     }
   } else {
-    // cluster split-K: park the partial tile in this CTA's smem (the ring is drained: every
-    // stage was consumed by an MMA that completed before the accumulator barrier)
+    // cluster split-K (one unit per CTA): park the partial tile in this CTA's smem (the ring is
+    // drained: every stage was consumed by an MMA that completed before the accumulator barrier)
+    const Work w = work_of<BN>(a, 0, mt);
+    const int m0 = w.m0, n0 = w.n0;
     float* red = reinterpret_cast<float*>(smem_raw + (base - raw));
-    if (warp >= 4) {
-      mbar_wait(accum, 0);
+    if (warp >= 5) {
+      mbar_wait(accf0, 0);
+      if (a.dbg && warp == 5 && lane == 0) a.dbg[cta * 16 + 3] = gtimer();
       tc_fence_after();
       const int r = q * 32 + lane;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
-        if (nkb > 0) {
+        if (w.nkb > 0) {
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
         } else {
 #pragma unroll
@@ -614,7 +710,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
                           __uint_as_float(v[e + 3]));
       }
     }
+    if (a.dbg && warp == 5 && lane == 0) a.dbg[cta * 16 + 7] = gtimer();
     cluster_sync();
+    if (a.dbg && tid == 0) a.dbg[cta * 16 + 8] = gtimer();
     const int cs = a.cs, nc = a.nc, z = blockIdx.z % cs, cl = blockIdx.z / cs;
     const int rpr = (BM + cs - 1) / cs, r0 = z * rpr, r1 = min(BM, r0 + rpr);
     const int nrows = max(0, r1 - r0);
@@ -629,15 +727,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
       const int lr = r0 + rr, gr = m0 + lr, gc = n0 + ch * 8;
       if (gr >= a.M || gc >= a.N) continue;
       const uint32_t off = red_u + (uint32_t)((lr * LDS + ch * 8) * 4);
-      float acc[8];
-#pragma unroll 1
-      for (int src = 0; src < cs; ++src) {
-        const uint32_t ra = mapa(off, (uint32_t)src);
-        const float4 x0 = ld_dsmem4(ra), x1 = ld_dsmem4(ra + 16);
-        const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+      // all cs remote loads in flight together, then the fixed-order sum src = 0..cs-1
+      float4 xs[2 * kMaxCluster];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = src ? __fadd_rn(acc[e], x[e]) : x[e];
-      }
+      for (int src = 0; src < kMaxCluster; ++src)
+        if (src < cs) {
+          const uint32_t ra = mapa(off, (uint32_t)src);
+          xs[2 * src] = ld_dsmem4(ra);
+          xs[2 * src + 1] = ld_dsmem4(ra + 16);
+        }
+      float acc[8];
+#pragma unroll
+      for (int src = 0; src < kMaxCluster; ++src)
+        if (src < cs) {
+          const float x[8] = {xs[2 * src].x, xs[2 * src].y, xs[2 * src].z, xs[2 * src].w,
+                              xs[2 * src + 1].x, xs[2 * src + 1].y, xs[2 * src + 1].z, xs[2 * src + 1].w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = src ? __fadd_rn(acc[e], x[e]) : x[e];
+        }
       if (nc == 1) {
         epi_store8(a, gr, gc, acc);
       } else {
@@ -646,6 +753,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
         __stcg(d + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
       }
     }
+    if (a.dbg && tid == 0) a.dbg[cta * 16 + 9] = gtimer();
     if (nc > 1) {
       // cross-cluster: the last of the nc CTAs owning row slice z of this tile sums the slices
       __shared__ int last;
@@ -668,27 +776,70 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
           if (gr >= a.M || gc >= a.N) continue;
           float acc[8];
 #pragma unroll 1
-          for (int c = 0; c < nc; ++c) {
-            const float4* sp = reinterpret_cast<const float4*>(w0 + (int64_t)c * (BM * BN) + lr * BN + ch * 8);
-            const float4 x0 = __ldcg(sp), x1 = __ldcg(sp + 1);
-            const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          for (int c0 = 0; c0 < nc; c0 += 8) {  // 8 cluster partials in flight, summed in order
+            float4 xs[16];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] = c ? __fadd_rn(acc[e], x[e]) : x[e];
+            for (int u = 0; u < 8; ++u)
+              if (c0 + u < nc) {
+                const float4* sp = reinterpret_cast<const float4*>(w0 + (int64_t)(c0 + u) * (BM * BN) + lr * BN + ch * 8);
+                xs[2 * u] = __ldcg(sp);
+                xs[2 * u + 1] = __ldcg(sp + 1);
+              }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (c0 + u < nc) {
+                const float x[8] = {xs[2 * u].x, xs[2 * u].y, xs[2 * u].z, xs[2 * u].w,
+                                    xs[2 * u + 1].x, xs[2 * u + 1].y, xs[2 * u + 1].z, xs[2 * u + 1].w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] = (c0 + u) ? __fadd_rn(acc[e], x[e]) : x[e];
+              }
           }
           epi_store8(a, gr, gc, acc);
         }
       }
     }
+    if (a.dbg && tid == 0) a.dbg[cta * 16 + 10] = gtimer();
     cluster_sync();  // no CTA leaves while its tile is still being read
   }
   tc_fence_before();
   __syncthreads();
+  if (a.dbg && tid == 0) {
+    a.dbg[cta * 16 + 4] = gtimer();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.dbg[cta * 16 + 5] = smid;
+    a.dbg[cta * 16 + 6] = nunits;
+  }
   if (warp == 4) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// development timing probe: XPIPE_GEMM_DBG=1 makes every GEMM launch record per-CTA
+// globaltimer stamps (start, first stage ready, MMAs issued, accumulator ready, end, smid,
+// units) into one device buffer (each launch overwrites it); xpipe_dev_gemm_probe reads it
+unsigned long long* gemm_dbg_buffer() {
+  static unsigned long long* buf = nullptr;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    if (getenv_flag("XPIPE_GEMM_DBG") && cudaMalloc(&buf, sizeof(unsigned long long) * 16 * 65536) != cudaSuccess)
+      buf = nullptr;
+  }
+  return buf;
+}
 
 // ---- TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point) ------
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -783,18 +934,33 @@ void setup_a_tma(GemmArgs& a, CUtensorMap* m) {
   if (make_map(m, a.A, 4, dims, str, box)) a.a_tma = 1;
 }
 
+// Launch geometry.  No split: a persistent grid of min(tiles, SMs) CTAs, one per SM with the
+// deepest ring that fits (<= 8 stages) and two TMEM accumulators, so each CTA streams its tiles
+// back to back and drains tile j while computing tile j+1.  Split-K: one CTA per (tile, split),
+// clusters of cs along z, 4 stages.
 template <int MODE, int BN, bool A_MN, bool B_MN>
 cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
-  constexpr int SMEM = Depth<BN>::ST * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
+  constexpr int STAGE = BM * BK * 2 + BN * BK * 2;
+  constexpr int DEEP = std::min(8, (kMaxSmem - 2048) / STAGE);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, DEEP * STAGE + 1024 + 256);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN, splits);
+  const int mt = (a.M + BM - 1) / BM, nt = (a.N + BN - 1) / BN;
   GemmArgs args = a;
+  dim3 grid;
+  if (splits <= 1) {
+    grid = dim3(std::max(1, std::min(mt * nt, num_sms())), 1, 1);
+    args.stages = DEEP;
+  } else {
+    grid = dim3(mt, nt, splits);
+    args.stages = std::min(DEEP, 4);  // small CTAs: clusters of up to 8 place easily (2 per SM)
+  }
+  const int SMEM = args.stages * STAGE + 1024 + 256;
+  args.dbg = gemm_dbg_buffer();
   CUtensorMap tmA, tmB;
   memset(&tmA, 0, sizeof tmA);
   memset(&tmB, 0, sizeof tmB);
@@ -804,11 +970,10 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     if (!no_tma_a()) setup_a_tma<MODE>(args, &tmA);
   }
   if (splits <= 1) {
-    launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, dim3(grid), dim3(NTHREADS), SMEM, st, args, tmA, tmB);
+    launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
   cfg.blockDim = dim3(NTHREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = st;
@@ -816,9 +981,33 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = 1; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = a.cs;
+  at[1].val.clusterDim.x = 1; at[1].val.clusterDim.y = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  // keep the whole split grid co-resident: clusters of cs CTAs must fit a GPC, so shrink the
+  // cross-cluster factor, then the cluster size, until the grid fits the active-cluster limit
+  static std::map<int, int> maxc_cache;  // cluster size -> max co-resident clusters
+  auto max_clusters = [&](int cs) {
+    auto it = maxc_cache.find(cs);
+    if (it != maxc_cache.end()) return it->second;
+    at[1].val.clusterDim.z = cs;
+    cfg.gridDim = dim3(mt, nt, cs);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<MODE, BN, A_MN, B_MN>, &cfg) != cudaSuccess || n <= 0)
+      n = 1 << 20;  // unknown: do not constrain
+    cudaGetLastError();
+    maxc_cache[cs] = n;
+    return n;
+  };
+  const int nkb = std::max(1, (a.K + BK - 1) / BK);
+  while ((int64_t)mt * nt * args.nc > max_clusters(args.cs) && (args.nc > 1 || args.cs > 2)) {
+    if (args.nc > 1) --args.nc;
+    else args.cs /= 2;
+  }
+  args.splits = args.cs * args.nc;
+  args.kb_per_split = (nkb + args.splits - 1) / args.splits;
+  at[1].val.clusterDim.z = args.cs;
+  cfg.gridDim = dim3(mt, nt, args.splits);
   return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<MODE, BN, A_MN, B_MN>, args, tmA, tmB);
 }
 
@@ -838,17 +1027,6 @@ int choose_bn(int M, int N) {
   return 64;
 }
 
-int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
-
 // split-K plan of a conv GEMM: N tile, cluster size cs (<= 8), clusters per tile nc, k-blocks
 // per split.  Aim at ~one CTA per SM with >= 8 k-blocks each (a CTA's fixed cost -- prologue,
 // pipeline fill, epilogue -- is several k-blocks' worth); no split when the tile grid alone
@@ -862,8 +1040,8 @@ SplitPlan plan_splits(int M, int N, int K) {
   int s = 1;
   if (!no_splitk() && tiles < num_sms() / 2 && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / 8));
   if (tiles * (int64_t)std::min(s, kMaxCluster) > kTileCounters - 16) s = 1;
-  p.cs = std::min(s, kMaxCluster);
-  p.nc = std::max(1, s / p.cs);
+  p.cs = std::min(s, kMaxCluster);  // cluster size
+  p.nc = std::max(1, s / p.cs);      // clusters per tile
   p.kbps = (nkb + p.cs * p.nc - 1) / (p.cs * p.nc);
   return p;
 }
@@ -936,6 +1114,12 @@ int64_t tc_conv_ws_elems(const ConvGeo& g) {
 }
 
 }  // namespace xp
+
+extern "C" int xpipe_dev_gemm_probe(unsigned long long* host, int32_t n) {
+  unsigned long long* b = xp::gemm_dbg_buffer();
+  if (!b || !host || n < 0 || n > 16 * 65536) return XP_EINVAL;
+  return cudaMemcpy(host, b, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) == cudaSuccess ? XP_OK : XP_ECUDA;
+}
 
 extern "C" int xpipe_gemm_bf16(const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,
                                int32_t a_kmajor, int32_t b_kmajor, int64_t ldd, void* stream) {

@@ -45,6 +45,8 @@ struct GemmArgs {
   // pixel origin comes from the m (fprop/dgrad) or k (wgrad) index on the grid {gq, gp}
   int a_tma;
   int gq, gp;
+  int stages;  // smem ring depth (set by the launcher)
+  unsigned long long* dbg;  // development timing probe (XPIPE_GEMM_DBG), else null
 };
 
 // plain GEMM for unit parity: D[M][N] fp32 (ldd) = A(m,k) B(n,k)

@@ -50,12 +50,13 @@ class TraceRec(C.Structure):
                [("t0_ns", C.c_uint64), ("t1_ns", C.c_uint64)]
 
 
-PROF_CLASSES = ("sweep", "conv_fprop", "conv_dgrad", "conv_wgrad")
+PROF_CLASSES = ("sweep", "conv_fprop", "conv_dgrad", "conv_wgrad", "bn_fwd", "bn_bwd")
+BYTE_CLASSES = ("sweep", "bn_fwd", "bn_bwd")  # work in bytes (else flops)
 
 
 class Stats(C.Structure):
-    _fields_ = [("span_ms", C.c_double), ("prof_ms", C.c_double * 4), ("prof_launches", C.c_int64 * 4),
-                ("prof_work", C.c_double * 4), ("kernel_launches", C.c_int64), ("graph_replays", C.c_int64),
+    _fields_ = [("span_ms", C.c_double), ("prof_ms", C.c_double * 6), ("prof_launches", C.c_int64 * 6),
+                ("prof_work", C.c_double * 6), ("kernel_launches", C.c_int64), ("graph_replays", C.c_int64),
                 ("losses", C.POINTER(C.c_float))]
 
     def profile(self):

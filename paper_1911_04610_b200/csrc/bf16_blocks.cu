@@ -107,7 +107,12 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       const ConvGeo g = conv_geo(c, O, L);
       const LayerInfo& N = c->net.layers[O.lbn];
       const PoolGeo p = pool_geo(c, O.lpool);
-      bf16* dmid = (bf16*)s.gmid;
+      // gradient buffer: alternate between two so the side-stream wgrad of this op can overlap
+      // the next op's BN backward; before reuse, wait for the wgrad two ops back
+      const int b = s.gsel;
+      s.gsel ^= 1;
+      bf16* dmid = (bf16*)(b ? s.gmid1 : s.gmid);
+      if (s.gdone_valid[b]) XP_CUDA(c, cudaStreamWaitEvent(s.stream, s.ev_gdone[b], 0));
       XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, launch_bn_backward((const bf16*)s.mid[o][slot], (const bf16*)dy,
                                                 (const bf16*)s.act[O.out][slot],
@@ -122,10 +127,16 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
         const double out_e = (double)n * O.sout.h * O.sout.w * O.sout.c;
         XP_TRY(prof_end(c, s, XP_PROF_BN_BWD, 2.0 * (2.0 * mid_e + out_e * (O.lpool >= 0 ? 5.0 : 4.0)) + 2.0 * mid_e));
       }
-      XP_TRY(prof_begin(c, s));
-      XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)s.act[O.in0][slot], dmid, s.g + L.woff, accumulate_g, s.ws,
-                                           s.ws_elems, s.ctr, s.stream), "conv_wgrad"));
-      XP_TRY(prof_end(c, s, XP_PROF_CONV_WGRAD, conv_flops(g, L.in0.c)));
+      // fork: the weight gradient (accumulated into g, read only by the update) on the side stream
+      XP_CUDA(c, cudaEventRecord(s.ev_fork, s.stream));
+      XP_CUDA(c, cudaStreamWaitEvent(s.side, s.ev_fork, 0));
+      XP_TRY(prof_begin(c, s, s.side));
+      XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)s.act[O.in0][slot], dmid, s.g + L.woff, accumulate_g,
+                                           s.ws_side, s.ws_elems, s.ctr_side, s.side), "conv_wgrad"));
+      XP_TRY(prof_end(c, s, XP_PROF_CONV_WGRAD, conv_flops(g, L.in0.c), s.side));
+      XP_CUDA(c, cudaEventRecord(s.ev_gdone[b], s.side));
+      s.gdone_valid[b] = true;
+      s.side_used = true;
       if (dx0) {
         XP_TRY(prof_begin(c, s));
         XP_TRY(check_launch(c, tc_conv_dgrad(g, O.sin0.c, dmid, W + L.woff, (bf16*)dx0, s.ws, s.ws_elems, s.ctr,

@@ -80,7 +80,8 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
   }
   s.gbuf_elems = (int64_t)n * p.max_act;
   s.gmid = A((size_t)s.gbuf_elems * 4);
-  if (!s.gmid) return set_err(c, XP_ENOMEM, "gradient scratch");
+  s.gmid1 = A((size_t)s.gbuf_elems * 4);
+  if (!s.gmid || !s.gmid1) return set_err(c, XP_ENOMEM, "gradient scratch");
   if (bf) {
     int64_t ws = 0;
     size_t bnws = 64;
@@ -95,8 +96,11 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
     s.ws = (float*)A((size_t)std::max<int64_t>(ws, 64) * 4);
     s.bnws = (float*)A(bnws * 4);
     s.ctr = (int*)A((size_t)kTileCounters * sizeof(int));
-    if (!s.ws || !s.bnws || !s.ctr) return set_err(c, XP_ENOMEM, "workspace");
+    s.ws_side = (float*)A((size_t)std::max<int64_t>(ws, 64) * 4);
+    s.ctr_side = (int*)A((size_t)kTileCounters * sizeof(int));
+    if (!s.ws || !s.bnws || !s.ctr || !s.ws_side || !s.ctr_side) return set_err(c, XP_ENOMEM, "workspace");
     XP_CUDA(c, cudaMemsetAsync(s.ctr, 0, (size_t)kTileCounters * sizeof(int), s.stream));
+    XP_CUDA(c, cudaMemsetAsync(s.ctr_side, 0, (size_t)kTileCounters * sizeof(int), s.stream));
   }
   return XP_OK;
 }

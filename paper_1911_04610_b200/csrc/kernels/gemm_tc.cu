@@ -174,6 +174,7 @@ __host__ bool getenv_flag(const char* name) {  // read once per name (developmen
 }
 __host__ bool no_tma() { static const bool v = getenv_flag("XPIPE_NO_TMA"); return v; }
 __host__ bool no_tma_a() { static const bool v = getenv_flag("XPIPE_NO_TMA_A"); return v; }
+__host__ bool no_l2red() { static const bool v = getenv_flag("XPIPE_NO_L2RED"); return v; }
 __host__ bool no_splitk() { static const bool v = getenv_flag("XPIPE_NO_SPLITK"); return v; }
 
 // ---------------------------------------------------------------------------------------
@@ -689,6 +690,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
     const Work w = work_of<BN>(a, 0, mt);
     const int m0 = w.m0, n0 = w.n0;
     float* red = reinterpret_cast<float*>(smem_raw + (base - raw));
+    const int tile_id = blockIdx.y * gridDim.x + blockIdx.x;
     if (warp >= 5) {
       mbar_wait(accf0, 0);
       if (a.dbg && warp == 5 && lane == 0) a.dbg[cta * 16 + 3] = gtimer();
@@ -703,11 +705,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = 0u;
         }
+        if (a.l2red) {  // through L2: this split's plane of the workspace, row-major [128][BN]
+          float4* d = reinterpret_cast<float4*>(a.ws + ((int64_t)tile_id * a.splits + blockIdx.z) * (BM * BN) +
+                                                r * BN + c0);
 #pragma unroll
-        for (int e = 0; e < 32; e += 4)
-          *reinterpret_cast<float4*>(red + r * LDS + c0 + e) =
-              make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
-                          __uint_as_float(v[e + 3]));
+          for (int e = 0; e < 32; e += 4)
+            __stcg(d + e / 4, make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                                          __uint_as_float(v[e + 3])));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(red + r * LDS + c0 + e) =
+                make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                            __uint_as_float(v[e + 3]));
+        }
       }
     }
     if (a.dbg && warp == 5 && lane == 0) a.dbg[cta * 16 + 7] = gtimer();
@@ -720,22 +731,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
     const bool row_fast = a.epi == EPI_WGRAD_T;  // transposed store: consecutive threads = consecutive m
     const uint32_t red_u = base;
     const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-    float* wsp = a.ws + ((int64_t)tile * nc + cl) * (BM * BN);  // this cluster's partial tile
+    float* wsp = a.ws_x + ((int64_t)tile * nc + cl) * (BM * BN);  // this cluster's partial tile
 #pragma unroll 1
     for (int idx = tid; idx < nrows * NCH; idx += NTHREADS) {
       const int rr = row_fast ? idx % nrows : idx / NCH, ch = row_fast ? idx / nrows : idx % NCH;
       const int lr = r0 + rr, gr = m0 + lr, gc = n0 + ch * 8;
       if (gr >= a.M || gc >= a.N) continue;
       const uint32_t off = red_u + (uint32_t)((lr * LDS + ch * 8) * 4);
-      // all cs remote loads in flight together, then the fixed-order sum src = 0..cs-1
+      // all cs partial loads in flight together, then the fixed-order sum src = 0..cs-1
       float4 xs[2 * kMaxCluster];
+      if (a.l2red) {
+        const float* p0 = a.ws + ((int64_t)tile * a.splits + cl * cs) * (BM * BN) + lr * BN + ch * 8;
 #pragma unroll
-      for (int src = 0; src < kMaxCluster; ++src)
-        if (src < cs) {
-          const uint32_t ra = mapa(off, (uint32_t)src);
-          xs[2 * src] = ld_dsmem4(ra);
-          xs[2 * src + 1] = ld_dsmem4(ra + 16);
-        }
+        for (int src = 0; src < kMaxCluster; ++src)
+          if (src < cs) {
+            const float4* sp = reinterpret_cast<const float4*>(p0 + (int64_t)src * (BM * BN));
+            xs[2 * src] = __ldcg(sp);
+            xs[2 * src + 1] = __ldcg(sp + 1);
+          }
+      } else {
+#pragma unroll
+        for (int src = 0; src < kMaxCluster; ++src)
+          if (src < cs) {
+            const uint32_t ra = mapa(off, (uint32_t)src);
+            xs[2 * src] = ld_dsmem4(ra);
+            xs[2 * src + 1] = ld_dsmem4(ra + 16);
+          }
+      }
       float acc[8];
 #pragma unroll
       for (int src = 0; src < kMaxCluster; ++src)
@@ -768,7 +790,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
       __syncthreads();
       if (last) {
         __threadfence();
-        const float* w0 = a.ws + (int64_t)tile * nc * (BM * BN);
+        const float* w0 = a.ws_x + (int64_t)tile * nc * (BM * BN);
 #pragma unroll 1
         for (int idx = tid; idx < nrows * NCH; idx += NTHREADS) {
           const int rr = row_fast ? idx % nrows : idx / NCH, ch = row_fast ? idx / nrows : idx % NCH;
@@ -799,7 +821,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, 
       }
     }
     if (a.dbg && tid == 0) a.dbg[cta * 16 + 10] = gtimer();
-    cluster_sync();  // no CTA leaves while its tile is still being read
+    if (!a.l2red) cluster_sync();  // no CTA leaves while its smem tile is still being read
   }
   tc_fence_before();
   __syncthreads();
@@ -1004,7 +1026,14 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     if (args.nc > 1) --args.nc;
     else args.cs /= 2;
   }
+  // workspace: [tile][split] partial planes (L2 reduction) then [tile][cluster] slices (nc > 1)
+  const int64_t plane = (int64_t)BM * BN, tiles = (int64_t)mt * nt;
+  const int64_t ws = args.ws ? args.ws_elems : 0;
+  if (args.nc > 1 && (!args.tile_counters || tiles * args.nc * plane > ws)) args.nc = 1;
+  const int64_t xarea = args.nc > 1 ? tiles * args.nc * plane : 0;
   args.splits = args.cs * args.nc;
+  args.l2red = (!no_l2red() && xarea + tiles * args.splits * plane <= ws) ? 1 : 0;
+  args.ws_x = args.ws ? args.ws + (args.l2red ? tiles * args.splits * plane : 0) : nullptr;
   args.kb_per_split = (nkb + args.splits - 1) / args.splits;
   at[1].val.clusterDim.z = args.cs;
   cfg.gridDim = dim3(mt, nt, args.splits);
@@ -1051,14 +1080,9 @@ template <int MODE, bool A_MN, bool B_MN>
 cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_ldo, int accumulate, float* ws,
                       int64_t ws_elems, int* counters, cudaStream_t st) {
   SplitPlan p = plan_splits(a.M, a.N, a.K);
-  const int tiles = ((a.M + BM - 1) / BM) * ((a.N + p.bn - 1) / p.bn);
-  if (p.nc > 1 && (!ws || !counters || (int64_t)tiles * p.nc * BM * p.bn > ws_elems)) {  // one cluster only
-    p.nc = 1;
-    p.kbps = (std::max(1, (a.K + BK - 1) / BK) + p.cs - 1) / p.cs;
-  }
   a.kb_per_split = p.kbps;
   a.cs = p.cs; a.nc = p.nc; a.splits = p.cs * p.nc;
-  a.ws = ws; a.tile_counters = counters;
+  a.ws = ws; a.ws_elems = ws ? ws_elems : 0; a.tile_counters = counters;
   a.epi = final_epi; a.out = final_out; a.ldo = final_ldo; a.accumulate = accumulate; a.split_stride = 0;
   return launch_bn<MODE, A_MN, B_MN>(a, p.bn, a.splits, st);
 }
@@ -1103,11 +1127,12 @@ cudaError_t tc_conv_wgrad(const ConvGeo& g, const bf16* X, const bf16* dY, float
 }
 
 int64_t tc_conv_ws_elems(const ConvGeo& g) {
-  // cross-cluster split-K partial tiles of the largest of the three GEMMs
+  // split-K partial planes + cross-cluster slices of the largest of the three GEMMs
   auto need = [](int M, int N, int K) -> int64_t {
     const SplitPlan p = plan_splits(M, N, K);
-    if (p.nc <= 1) return 0;
-    return (int64_t)((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn) * p.nc * BM * p.bn;
+    if (p.cs * p.nc <= 1) return 0;
+    const int64_t tiles = (int64_t)((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn);
+    return tiles * (p.cs * p.nc + (p.nc > 1 ? p.nc : 0)) * BM * p.bn;
   };
   return std::max({need(g.Nimg * g.P * g.Q, g.Co, g.R * g.S * g.C), need(g.Nimg * g.H * g.W, g.C, g.R * g.S * g.Co),
                    need(g.R * g.S * g.C, g.Co, g.Nimg * g.P * g.Q)});

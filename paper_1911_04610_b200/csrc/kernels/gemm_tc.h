@@ -34,7 +34,10 @@ struct GemmArgs {
   // every row slice goes to the workspace `ws` and the last of the nc CTAs owning that slice
   // (per-slice arrival counter, self-resetting) sums the nc slices in order c = 0..nc-1
   int splits, cs, nc;
-  float* ws;
+  float* ws;              // caller workspace (ws_elems floats)
+  int64_t ws_elems;
+  int l2red;              // 1: partial tiles go through ws (L2) [tile][split], else through DSMEM
+  float* ws_x;            // cross-cluster partial slices [tile][cluster] (nc > 1)
   int* tile_counters;
   // B operand by TMA (cp.async.bulk.tensor into the 128B-swizzled UMMA layout):
   // 0 = cp.async gather, 1 = 2D K-major box {64, BN}, 2 = 2D MN-major boxes {64, 64},

@@ -54,7 +54,19 @@ struct StageRT {
   std::vector<std::vector<uint8_t*>> pidx; // [op][slot] max-pool winner positions (conv op with pool)
   std::vector<float*> dz;               // [slot] logits gradient (last stage)
   std::vector<void*> grad;              // [tensor] activation-gradient buffers (per op pass)
-  void* gmid = nullptr;                 // conv op: gradient of the conv output (bf16)
+  void* gmid = nullptr;                 // conv op: gradient of the conv output (bf16), buffer 0
+  void* gmid1 = nullptr;                //   buffer 1 (consecutive conv ops alternate; see side)
+  // weight gradients run on a side stream, off the critical path of the backward chain
+  // (bn-backward -> dgrad -> next op): forked after the op's BN backward, joined at the end of
+  // the micro-batch's backward; conv op i waits for the wgrad of op i-2 before reusing its
+  // gradient buffer.  The side stream has its own split-K workspace and counters.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_gdone[2] = {nullptr, nullptr};
+  bool gdone_valid[2] = {false, false};
+  int gsel = 0;
+  bool side_used = false;
+  float* ws_side = nullptr;
+  int* ctr_side = nullptr;
   int64_t gbuf_elems = 0;
   float* ws = nullptr;                  // split-K workspace (fp32)
   int64_t ws_elems = 0;
@@ -148,6 +160,6 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
 int version_difference(const xpipe_ctx* c, int k, int pass);
 int version_difference_public(const xpipe_ctx* c, int k, int pass);
 // profiling: bracket one kernel launch on s.stream (no-ops unless cfg.profile)
-int prof_begin(xpipe_ctx* c, StageRT& s);
-int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work);
+int prof_begin(xpipe_ctx* c, StageRT& s, cudaStream_t st = nullptr);  // st: default the stage stream
+int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work, cudaStream_t st = nullptr);
 }  // namespace xp

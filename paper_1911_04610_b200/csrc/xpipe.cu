@@ -110,6 +110,9 @@ void free_all(xpipe_ctx* c) {
     s.ev_pool.clear();
     for (auto& v : s.ev_flag) { for (auto e : v) cudaEventDestroy(e); v.clear(); }
     for (auto& e : s.tmark) if (e) { cudaEventDestroy(e); e = nullptr; }
+    if (s.side) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.side); cudaStreamDestroy(s.side); s.side = nullptr; }
+    for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1]})
+      if (*e) { cudaEventDestroy(*e); *e = nullptr; }
     if (s.stream) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.stream); cudaStreamDestroy(s.stream); s.stream = nullptr; }
   }
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -144,23 +147,25 @@ int version_difference(const xpipe_ctx* c, int k, int pass) {
 
 int version_difference_public(const xpipe_ctx* c, int k, int pass) { return version_difference(c, k, pass); }
 
-int prof_begin(xpipe_ctx* c, StageRT& s) {
+int prof_begin(xpipe_ctx* c, StageRT& s, cudaStream_t st) {
   if (!c->cfg.profile) return XP_OK;
+  if (!st) st = s.stream;
   while (s.ev_pool.size() < s.ev_used + 2) {
     cudaEvent_t e;
     XP_CUDA(c, cudaEventCreate(&e));
     s.ev_pool.push_back(e);
   }
   // external record: inside a stream capture this becomes an event-record node of the graph
-  if (c->capturing) XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used], s.stream, cudaEventRecordExternal));
-  else XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used], s.stream));
+  if (c->capturing) XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used], st, cudaEventRecordExternal));
+  else XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used], st));
   return XP_OK;
 }
 
-int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work) {
+int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work, cudaStream_t st) {
   if (!c->cfg.profile) return XP_OK;
-  if (c->capturing) XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used + 1], s.stream, cudaEventRecordExternal));
-  else XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used + 1], s.stream));
+  if (!st) st = s.stream;
+  if (c->capturing) XP_CUDA(c, cudaEventRecordWithFlags(s.ev_pool[s.ev_used + 1], st, cudaEventRecordExternal));
+  else XP_CUDA(c, cudaEventRecord(s.ev_pool[s.ev_used + 1], st));
   s.ev_used += 2;
   s.prof_cls.push_back(cls);
   s.prof_work.push_back(work);
@@ -331,6 +336,8 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
   if (rec) XP_TRY(check_launch(c, launch_trace_begin(s.ds, rec, k, 1, (int)t, (int)j, sb, bw, s.stream), "trace"));
   if (bw) s.host_bver = s.host_ver;
   const bool accumulate = (j != 1);
+  s.gsel = 0;
+  s.gdone_valid[0] = s.gdone_valid[1] = false;
   // gradient bookkeeping over the stage's tensors: the output gradient is the gradient ring
   // slot (or dz on the last stage); every other tensor's gradient is written by its first
   // consumer (reverse op order) and accumulated by the others
@@ -357,6 +364,11 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     XP_CUDA(c, cudaMemcpyAsync(pv.gin_slot[(u - 1) % pv.S], gp[0], P.in_bytes, cudaMemcpyDefault, s.stream));
     XP_TRY(flag_write(c, s, pv, 1, u));
     XP_TRY(flag_write(c, s, pv, 2, u));  // released our input slot u
+  }
+  if (s.side_used) {  // join the weight-gradient side stream (the update reads g)
+    XP_CUDA(c, cudaEventRecord(s.ev_join, s.side));
+    XP_CUDA(c, cudaStreamWaitEvent(s.stream, s.ev_join, 0));
+    s.side_used = false;
   }
   if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
   if (j == c->T) {
@@ -695,6 +707,9 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
     if (c->mp() && k != c->cfg.my_stage) continue;
     cudaSetDevice(s.dev);
     if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
+    if (cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
+    for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1]})
+      if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail_init(XP_ECUDA, "event");
     if (cudaMallocHost(&s.diag, 256) != cudaSuccess) return fail_init(XP_ENOMEM, "diag buffer");
     int rr = allocate_stage(cp, s);
     if (rr != XP_OK) return fail_init(rr, "stage allocation");

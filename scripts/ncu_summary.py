@@ -71,7 +71,9 @@ def full(rep, out_md, traffic_key=None):
         d = dict(zip(hdr, row))
         item = {"kernel": short(d.get("Kernel Name", "?"))}
         for k in hdr:
-            if k in WANT or "tensor" in k and "pct" in k:
+            if k in WANT or ("tensor" in k and "pct" in k and ".avg." in k):
+                if k not in WANT and d[k].strip() in ("0", "0.000000", ""):
+                    continue  # drop the all-zero tensor sub-pipe rows (noise)
                 item[k] = d[k] + " " + units[hdr.index(k)]
         res.append(item)
     lines = ["# ncu --set full summary: %s" % os.path.basename(rep), ""]

@@ -175,11 +175,12 @@ def run_reference(args):
     return 0
 
 
-def run_sweep(args, peaks, peak_kind):
+def run_sweep(args, peaks, peak_kind, n=None, steps=None):
     """Config 5: the fused Adam+prediction sweep alone (kernel-level metric)."""
     import torch
     from paper_1911_04610_b200 import adam_predict
-    n = args.sweep_params
+    n = n or args.sweep_params
+    steps = steps or args.steps
     dev = torch.device("cuda", 0)
     W = torch.rand(n, device=dev) * 0.1 - 0.05
     g = torch.rand(n, device=dev) * 2e-2 - 1e-2
@@ -194,21 +195,36 @@ def run_sweep(args, peaks, peak_kind):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(0) as ck:
         e0.record()
-        for i in range(args.steps):
+        for i in range(steps):
             adam_predict(W, g, m, v, pf, pb, args.warmup + i + 1, 1e-4, (0.9, 0.999), 1e-8, 3, 1, True, stream=st)
         e1.record()
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = e0.elapsed_time(e1) / steps
+    del W, g, m, v, pf, pb
+    torch.cuda.empty_cache()
     gbs = n * 32 / (ms * 1e-3) / 1e9
     peak = peaks["hbm_gbs"]
     return {"metric": "Adam+predict sweep HBM GB/s (config 5)", "value": gbs, "unit": "GB/s", "n_gpus": 1,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "sweep P=%d, s_f=3, s_b=1, bf16 W_hat, 32 B/param" % n,
                        "l2": "working set %d MB > 126 MB L2" % (n * 32 // 2**20)},
-            "gpu_launches": args.steps, "clocks": ck.summary(),
+            "gpu_launches": steps, "clocks": ck.summary(),
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                         "traffic": None, "peak_source": peak_kind}}
+                         "traffic": sweep_traffic(n), "peak_source": peak_kind}}
+
+
+def sweep_traffic(n):
+    """DRAM bytes per launch from the committed ncu --set full capture of the sweep, scaled to P
+    (the capture's P is recorded beside it), or None."""
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(tp):
+        return None
+    with open(tp) as f:
+        d = json.load(f)
+    if "sweep" not in d:
+        return None
+    return d["sweep"] * n / d.get("sweep_params", 1 << 28)
 
 
 def main():
@@ -225,6 +241,7 @@ def main():
     ap.add_argument("--sweep-params", type=int, default=1 << 28)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the embedded config-5 sweep measurement")
     ap.add_argument("--no-graphs", action="store_true", help="enqueue every kernel from the host (no CUDA graphs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -370,7 +387,11 @@ def main():
     roof["traffic"] = None
     roof["kernel"] = dom
     roof["launches_per_step"] = d["launches"] / args.steps
+    roof["work_per_launch"] = d["work"] / d["launches"]
     roof["peak_source"] = peak_kind + (" (sustained)" if roof["bound"] == "tensor" else "")
+    roof["note"] = ("live launch durations with all K stage streams running concurrently on the GPU "
+                    "(each launch shares the SMs with the other stages' kernels); share_norm is comparable "
+                    "with the serialised ncu launch list")
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
@@ -378,6 +399,7 @@ def main():
         if tr is not None:
             roof["traffic"] = tr
     shares = {k: {"ms_per_step": v["ms"] / args.steps, "share_of_step": v["ms"] / (prof_step_ms * args.steps * (ws if mp_mode else 1)),
+                  "share_norm": v["ms"] / total_prof_ms,
                   "achieved": (v["work"] / (v["ms"] * 1e-3) / (1e9 if k in BYTE_CLASSES else 1e12)) if v["ms"] else 0,
                   "unit": "GB/s" if k in BYTE_CLASSES else "TFLOP/s", "launches": v["launches"]}
               for k, v in prof.items()}
@@ -387,6 +409,12 @@ def main():
     except Exception as e:  # the bubble is a report, not the metric
         bubble = {"error": repr(e)[:200]}
     cpu = None if args.no_cpu_baseline else cpu_baseline(args.workload)
+    sweep = None
+    if not args.no_sweep and not mp_mode:
+        # the BASELINE metric's second half: the fused Adam+prediction sweep alone (config 5)
+        sl = run_sweep(args, peaks, peak_kind, n=1 << 27, steps=20)
+        sweep = {k: sl[k] for k in ("value", "unit", "ms_per_step", "roofline")}
+        sweep["config"] = sl["config"]["workload"]
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": result["ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
@@ -400,7 +428,8 @@ def main():
                        "l2": "working set > L2: optimizer state 16 B/param x 14.7M params = 235 MB (126 MB L2)"},
             "e2e": e2e, "gpu_launches": result["launches"], "graph_replays": result.get("replays"),
             "clocks": result["clocks"],
-            "roofline": result["roof"], "kernel_shares": result["shares"], "bubble": bubble, "cpu_baseline": cpu}
+            "roofline": result["roof"], "kernel_shares": result["shares"], "bubble": bubble, "cpu_baseline": cpu,
+            "adam_predict": sweep}
     print(json.dumps(line), flush=True)
     return 0
 

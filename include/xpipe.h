@@ -127,9 +127,11 @@ enum { XP_PROF_SWEEP = 0,       /* K1: work = algorithmic bytes */
        XP_PROF_CONV_FPROP = 1,  /* tcgen05 implicit-GEMM conv forward: work = 2*M*N*K flops */
        XP_PROF_CONV_DGRAD = 2,
        XP_PROF_CONV_WGRAD = 3,
-       XP_PROF_BN_FWD = 4,      /* BN statistics + apply [+ ReLU + pool]: work = algorithmic bytes */
-       XP_PROF_BN_BWD = 5,      /* BN backward reduce + apply: work = algorithmic bytes */
-       XP_PROF_N = 6 };
+       XP_PROF_BN_STATS = 4,    /* BN statistics (partial chunks + fixed-order merge): work = algorithmic bytes */
+       XP_PROF_BN_APPLY = 5,    /* BN apply [+ ReLU + max-pool]: work = algorithmic bytes */
+       XP_PROF_BN_BWD_REDUCE = 6, /* BN backward reductions (sum dy, sum dy*xhat) + merge: bytes */
+       XP_PROF_BN_BWD_APPLY = 7,  /* BN input gradient: bytes */
+       XP_PROF_N = 8 };
 
 typedef struct {
   double span_ms;                    /* reserved */

@@ -44,7 +44,7 @@ def _compile(src, extra):
     hdr_t = max(os.path.getmtime(h) for h in headers())
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t):
         return obj
-    flags = list(COMMON) + list(extra)
+    flags = list(COMMON) + list(extra) + os.environ.get("XPIPE_NVCC_EXTRA", "").split()
     if os.path.basename(src) in STRICT:
         flags.append("--fmad=false")
     cmd = [NVCC] + flags + ["-c", src, "-o", obj + ".tmp"]

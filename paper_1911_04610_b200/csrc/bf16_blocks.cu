@@ -59,14 +59,17 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
       XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, launch_bn_stats(mid, M, O.smid.c, N.d.bn_eps, W + N.woff, W + N.boff, s.bnws,
                                              s.ctr + kTileCounters - 2, s.stats[o][slot], s.stream), "bn_stats"));
+      // algorithmic bytes: the conv output read once (register-resident two passes)
+      XP_TRY(prof_end(c, s, XP_PROF_BN_STATS, 2.0 * M * O.smid.c));
       const PoolGeo p = pool_geo(c, O.lpool);
       uint8_t* pidx = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
+      XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, launch_bn_apply(mid, s.stats[o][slot], (bf16*)y, pidx, n, O.smid.h, O.smid.w, O.smid.c,
                                              O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0,
                                              O.relu, s.stream), "bn_apply"));
-      // algorithmic bytes: mid read twice (statistics, apply), output written (+ pool winners)
+      // algorithmic bytes: conv output read, output written (+ 1 B pool winner per output)
       const double out_elems = (double)n * O.sout.h * O.sout.w * O.sout.c;
-      return prof_end(c, s, XP_PROF_BN_FWD, 4.0 * M * O.smid.c + out_elems * (O.lpool >= 0 ? 3.0 : 2.0));
+      return prof_end(c, s, XP_PROF_BN_APPLY, 2.0 * M * O.smid.c + out_elems * (O.lpool >= 0 ? 3.0 : 2.0));
     }
     case OP_ADD:
       return check_launch(c, launch_add_fwd(x, (const bf16*)s.act[O.in1][slot], (bf16*)y, (int64_t)n * O.sout.size(),
@@ -113,20 +116,26 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       s.gsel ^= 1;
       bf16* dmid = (bf16*)(b ? s.gmid1 : s.gmid);
       if (s.gdone_valid[b]) XP_CUDA(c, cudaStreamWaitEvent(s.stream, s.ev_gdone[b], 0));
+      const bf16* xmid = (const bf16*)s.mid[o][slot];
+      const bf16* yout = (const bf16*)s.act[O.out][slot];
+      const uint8_t* pw8 = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
+      // algorithmic bytes per pass: the conv output, plus dout and y (+ pool winners) at the
+      // output resolution; the apply pass also writes dmid
+      const double mid_e = (double)n * O.smid.h * O.smid.w * O.smid.c;
+      const double out_e = (double)n * O.sout.h * O.sout.w * O.sout.c;
+      const double pass_bytes = 2.0 * mid_e + out_e * (O.lpool >= 0 ? 5.0 : 4.0);
       XP_TRY(prof_begin(c, s));
-      XP_TRY(check_launch(c, launch_bn_backward((const bf16*)s.mid[o][slot], (const bf16*)dy,
-                                                (const bf16*)s.act[O.out][slot],
-                                                O.lpool >= 0 ? s.pidx[o][slot] : nullptr, s.stats[o][slot],
-                                                W + N.woff, n, O.smid.h, O.smid.w, O.smid.c, O.sout.h, O.sout.w, p.kh,
-                                                p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws,
-                                                s.ctr + kTileCounters - 1, s.g + N.woff, s.g + N.boff, accumulate_g, dmid, s.stream),
-                          "bn_backward"));
-      {
-        // algorithmic bytes: mid, dy, y (+ pool winners) read by both passes, dmid written
-        const double mid_e = (double)n * O.smid.h * O.smid.w * O.smid.c;
-        const double out_e = (double)n * O.sout.h * O.sout.w * O.sout.c;
-        XP_TRY(prof_end(c, s, XP_PROF_BN_BWD, 2.0 * (2.0 * mid_e + out_e * (O.lpool >= 0 ? 5.0 : 4.0)) + 2.0 * mid_e));
-      }
+      XP_TRY(check_launch(c, launch_bn_bwd_reduce(xmid, (const bf16*)dy, yout, pw8, s.stats[o][slot], n, O.smid.h,
+                                                  O.smid.w, O.smid.c, O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw, p.ph,
+                                                  p.pw, O.lpool >= 0, O.relu, s.bnws, s.g + N.woff, s.g + N.boff,
+                                                  accumulate_g, s.stream), "bn_bwd_reduce"));
+      XP_TRY(prof_end(c, s, XP_PROF_BN_BWD_REDUCE, pass_bytes));
+      XP_TRY(prof_begin(c, s));
+      XP_TRY(check_launch(c, launch_bn_bwd_apply(xmid, (const bf16*)dy, yout, pw8, s.stats[o][slot], W + N.woff, n,
+                                                 O.smid.h, O.smid.w, O.smid.c, O.sout.h, O.sout.w, p.kh, p.kw, p.sh,
+                                                 p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws, dmid, s.stream),
+                          "bn_bwd_apply"));
+      XP_TRY(prof_end(c, s, XP_PROF_BN_BWD_APPLY, pass_bytes + 2.0 * mid_e));
       // fork: the weight gradient (accumulated into g, read only by the update) on the side stream
       XP_CUDA(c, cudaEventRecord(s.ev_fork, s.stream));
       XP_CUDA(c, cudaStreamWaitEvent(s.side, s.ev_fork, 0));

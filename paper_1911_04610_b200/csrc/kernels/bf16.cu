@@ -522,10 +522,10 @@ cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, uint8_t*
   return cudaGetLastError();
 }
 
-cudaError_t launch_bn_backward(const bf16* x, const bf16* dout, const bf16* y, const uint8_t* pidx, const float* stats,
-                               const bf16* gamma_b, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
-                               int sw, int ph, int pw, bool pool, bool relu, float* ws, int* counter, float* g_gamma,
-                               float* g_beta, bool accumulate, bf16* dx, cudaStream_t st) {
+cudaError_t launch_bn_bwd_reduce(const bf16* x, const bf16* dout, const bf16* y, const uint8_t* pidx,
+                                 const float* stats, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
+                                 int sw, int ph, int pw, bool pool, bool relu, float* ws, float* g_gamma, float* g_beta,
+                                 bool accumulate, cudaStream_t st) {
   if (C % 8 || C > 2048) return cudaErrorInvalidValue;
   BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
   const int M = n * H * W;
@@ -533,11 +533,22 @@ cudaError_t launch_bn_backward(const bf16* x, const bf16* dout, const bf16* y, c
   const int threads = bn_threads(C);
   const size_t shm = (size_t)threads * 16 * 4;
   float* tot = ws + (size_t)chunks * 2 * C;
-  (void)counter;
   launch_pdl(bn_bwd_reduce_kernel, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC, ws);
   launch_pdl(bn_bwd_final_kernel, dim3((C + 7) / 8), dim3(256), 0, st, (const float*)ws, chunks, C, tot, g_gamma, g_beta,
              accumulate ? 1 : 0);
-  launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats, tot, gamma_b, G, M, dx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bn_bwd_apply(const bf16* x, const bf16* dout, const bf16* y, const uint8_t* pidx, const float* stats,
+                                const bf16* gamma_b, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
+                                int sw, int ph, int pw, bool pool, bool relu, const float* ws, bf16* dx,
+                                cudaStream_t st) {
+  if (C % 8 || C > 2048) return cudaErrorInvalidValue;
+  BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
+  const int M = n * H * W;
+  const float* tot = ws + (size_t)bn_chunks(M, C) * 2 * C;
+  launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats, tot,
+             gamma_b, G, M, dx);
   return cudaGetLastError();
 }
 

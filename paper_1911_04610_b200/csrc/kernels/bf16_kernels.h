@@ -17,11 +17,17 @@ cudaError_t launch_bn_apply(const __nv_bfloat16* x, const float* stats, __nv_bfl
                             bool relu, cudaStream_t st);
 // backward through [pool] + ReLU + BN: dgamma/dbeta into g_gamma/g_beta, dx = BN input grad
 // routes dout through the stored forward output y (ReLU mask) and pool winners pidx
-cudaError_t launch_bn_backward(const __nv_bfloat16* x, const __nv_bfloat16* dout, const __nv_bfloat16* y,
-                               const uint8_t* pidx, const float* stats, const __nv_bfloat16* gamma_b, int n, int H,
-                               int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,
-                               bool relu, float* ws, int* counter, float* g_gamma, float* g_beta, bool accumulate,
-                               __nv_bfloat16* dx, cudaStream_t st);
+// backward through [pool] + ReLU + BN, in two launches: the reductions (sum dy, sum dy*xhat per
+// channel; dgamma/dbeta into g_gamma/g_beta, totals kept in ws) and the BN input gradient dx.
+// Both route dout through the stored forward output y (ReLU mask) and pool winners pidx.
+cudaError_t launch_bn_bwd_reduce(const __nv_bfloat16* x, const __nv_bfloat16* dout, const __nv_bfloat16* y,
+                                 const uint8_t* pidx, const float* stats, int n, int H, int W, int C, int P, int Q,
+                                 int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, float* ws,
+                                 float* g_gamma, float* g_beta, bool accumulate, cudaStream_t st);
+cudaError_t launch_bn_bwd_apply(const __nv_bfloat16* x, const __nv_bfloat16* dout, const __nv_bfloat16* y,
+                                const uint8_t* pidx, const float* stats, const __nv_bfloat16* gamma_b, int n, int H,
+                                int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,
+                                bool relu, const float* ws, __nv_bfloat16* dx, cudaStream_t st);
 cudaError_t launch_linear_fwd_bf16(const __nv_bfloat16* x, const __nv_bfloat16* W, const __nv_bfloat16* b, void* y,
                                    int n, int in, int out, bool relu, bool f32out, cudaStream_t st);
 cudaError_t launch_linear_dgrad_bf16(const void* dy, bool dy_f32, const __nv_bfloat16* mask, const __nv_bfloat16* W,

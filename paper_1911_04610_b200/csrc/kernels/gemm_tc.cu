@@ -37,6 +37,12 @@ constexpr int kMaxCluster = 8;
 // warps 0-3 operand producers (one elected thread when both operands go by TMA), warp 4 the
 // MMA issuer, warps 5-8 the epilogue (TMEM lane quadrant = warp % 4)
 constexpr int NTHREADS = 288;
+#ifndef XP_GEMM_MAXREG
+// register cap sized for two co-resident CTAs per SM (2 x 288 threads x 112 <= 64K registers;
+// ptxas spills nothing at 112, whereas __launch_bounds__(288, 2) picks 96 and spills): two GEMM
+// CTAs (e.g. of two pipeline stages' streams) hide each other's fixed latency
+#define XP_GEMM_MAXREG 112
+#endif
 constexpr int kMaxSmem = 227 * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -144,14 +150,17 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
+      // load and wait in ONE asm statement: the destination registers are undefined until
+      // tcgen05.wait::ld, so the compiler must not be able to spill/move them in between
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
       "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
         "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
         "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      : "r"(taddr)
+      : "memory");
 }
 
 // smem byte offset of 16B chunk `chunk` of row `row` in a K-major SW128 tile (128 B rows,
@@ -176,6 +185,14 @@ __host__ bool no_tma() { static const bool v = getenv_flag("XPIPE_NO_TMA"); retu
 __host__ bool no_tma_a() { static const bool v = getenv_flag("XPIPE_NO_TMA_A"); return v; }
 __host__ bool no_l2red() { static const bool v = getenv_flag("XPIPE_NO_L2RED"); return v; }
 __host__ bool no_splitk() { static const bool v = getenv_flag("XPIPE_NO_SPLITK"); return v; }
+__host__ int getenv_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+// development knobs: split-K ring depth and the minimum k-blocks per split
+__host__ int split_stages() { static const int v = getenv_int("XPIPE_SPLIT_STAGES", 4); return v; }
+__host__ int persist_stages() { static const int v = getenv_int("XPIPE_PERSIST_STAGES", 4); return v; }
+__host__ int split_min_kb() { static const int v = getenv_int("XPIPE_SPLIT_MIN_KB", 8); return v; }
 
 // ---------------------------------------------------------------------------------------
 // operand loaders: init once per tile, load(kb) per k-block; 128 producer threads (tid)
@@ -581,7 +598,7 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
 }
 
 template <int MODE, int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const GemmArgs a, const __grid_constant__ CUtensorMap tmA,
+__global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, const __grid_constant__ CUtensorMap tmA,
                                                                const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
   constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
@@ -956,9 +973,12 @@ void setup_a_tma(GemmArgs& a, CUtensorMap* m) {
   if (make_map(m, a.A, 4, dims, str, box)) a.a_tma = 1;
 }
 
-// Launch geometry.  No split: a persistent grid of min(tiles, SMs) CTAs, one per SM with the
-// deepest ring that fits (<= 8 stages) and two TMEM accumulators, so each CTA streams its tiles
-// back to back and drains tile j while computing tile j+1.  Split-K: one CTA per (tile, split),
+// Launch geometry.  No split: a persistent grid of min(tiles, SMs) CTAs with a 4-stage ring and
+// two TMEM accumulators, so each CTA streams its tiles back to back and drains tile j while
+// computing tile j+1.  4 stages (96 KB at BN=64) and a register budget for two CTAs per SM let a
+// GEMM of another pipeline stage's stream share the SM: a deeper ring measured no faster (the
+// main loop is bound by L2->SM bandwidth, not latency) and one CTA per SM left the SM idle
+// through each GEMM's fixed prologue/epilogue (VGG-16 K=4 on one GPU: +31 % samples/s).  Split-K: one CTA per (tile, split),
 // clusters of cs along z, 4 stages.
 template <int MODE, int BN, bool A_MN, bool B_MN>
 cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
@@ -976,10 +996,10 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   dim3 grid;
   if (splits <= 1) {
     grid = dim3(std::max(1, std::min(mt * nt, num_sms())), 1, 1);
-    args.stages = DEEP;
+    args.stages = std::max(4, std::min(DEEP, persist_stages()));  // >= LAG+1 (cp.async ring)
   } else {
     grid = dim3(mt, nt, splits);
-    args.stages = std::min(DEEP, 4);  // small CTAs: clusters of up to 8 place easily (2 per SM)
+    args.stages = std::max(4, std::min(DEEP, split_stages()));  // small CTAs: clusters of up to 8 place easily
   }
   const int SMEM = args.stages * STAGE + 1024 + 256;
   args.dbg = gemm_dbg_buffer();
@@ -1067,7 +1087,7 @@ SplitPlan plan_splits(int M, int N, int K) {
   const int tiles = ((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn);
   const int nkb = std::max(1, (K + BK - 1) / BK);
   int s = 1;
-  if (!no_splitk() && tiles < num_sms() / 2 && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / 8));
+  if (!no_splitk() && tiles < num_sms() / 2 && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / split_min_kb()));
   if (tiles * (int64_t)std::min(s, kMaxCluster) > kTileCounters - 16) s = 1;
   p.cs = std::min(s, kMaxCluster);  // cluster size
   p.nc = std::max(1, s / p.cs);      // clusters per tile

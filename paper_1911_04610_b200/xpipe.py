@@ -50,13 +50,14 @@ class TraceRec(C.Structure):
                [("t0_ns", C.c_uint64), ("t1_ns", C.c_uint64)]
 
 
-PROF_CLASSES = ("sweep", "conv_fprop", "conv_dgrad", "conv_wgrad", "bn_fwd", "bn_bwd")
-BYTE_CLASSES = ("sweep", "bn_fwd", "bn_bwd")  # work in bytes (else flops)
+PROF_CLASSES = ("sweep", "conv_fprop", "conv_dgrad", "conv_wgrad", "bn_stats", "bn_apply", "bn_bwd_reduce",
+                "bn_bwd_apply")
+BYTE_CLASSES = ("sweep", "bn_stats", "bn_apply", "bn_bwd_reduce", "bn_bwd_apply")  # work in bytes (else flops)
 
 
 class Stats(C.Structure):
-    _fields_ = [("span_ms", C.c_double), ("prof_ms", C.c_double * 6), ("prof_launches", C.c_int64 * 6),
-                ("prof_work", C.c_double * 6), ("kernel_launches", C.c_int64), ("graph_replays", C.c_int64),
+    _fields_ = [("span_ms", C.c_double), ("prof_ms", C.c_double * 8), ("prof_launches", C.c_int64 * 8),
+                ("prof_work", C.c_double * 8), ("kernel_launches", C.c_int64), ("graph_replays", C.c_int64),
                 ("losses", C.POINTER(C.c_float))]
 
     def profile(self):
@@ -273,9 +274,26 @@ class XPipe:
         return [tuple(getattr(buf[i], q) for q in f) for i in range(n.value)]
 
 
+def _want(name, t, dtypes, n=None):
+    """Marshalling check (the C ABI sees only pointers): element type, contiguity, size."""
+    if t is None:
+        return
+    dt = str(getattr(t, "dtype", ""))
+    if not any(dt.endswith(d) for d in dtypes):
+        raise TypeError("%s: dtype %s, expected %s" % (name, dt, "/".join(dtypes)))
+    if hasattr(t, "is_contiguous") and not t.is_contiguous():
+        raise ValueError("%s must be contiguous" % name)
+    if n is not None and t.numel() < n:
+        raise ValueError("%s has %d elements, needs %d" % (name, t.numel(), n))
+
+
 def adam_predict(W, g, m, v, pf, pb, version, lr, betas, eps, s_f, s_b, pred_bf16, delta="adam", stream=None):
     """K1 on torch CUDA tensors (in place on W, m, v)."""
     n = W.numel()
+    for nm, t in (("W", W), ("g", g), ("m", m), ("v", v)):
+        _want(nm, t, ("float32",), n)
+    for nm, t in (("pf", pf), ("pb", pb)):
+        _want(nm, t, ("bfloat16",) if pred_bf16 else ("float32",), n)
     _check(lib().xpipe_adam_predict(_ptr(W), _ptr(g), _ptr(m), _ptr(v), _ptr(pf) if pf is not None else None,
                                     _ptr(pb) if pb is not None else None, n, version, lr, betas[0], betas[1], eps,
                                     s_f, s_b, int(pred_bf16), DELTA[delta],
@@ -283,12 +301,19 @@ def adam_predict(W, g, m, v, pf, pb, version, lr, betas, eps, s_f, s_b, pred_bf1
 
 
 def gemm_bf16(A, B, D, M, N, K, a_kmajor=True, b_kmajor=True, ldd=None, stream=None):
+    _want("A", A, ("bfloat16",), M * K)
+    _want("B", B, ("bfloat16",), N * K)
+    _want("D", D, ("float32",))
     _check(lib().xpipe_gemm_bf16(_ptr(A), _ptr(B), _ptr(D), M, N, K, int(a_kmajor), int(b_kmajor),
                                  ldd if ldd is not None else N, C.c_void_p(stream) if stream else None))
 
 
 def conv2d_bf16(mode, geo, in0, in1, out, accumulate=False, ws=None, stream=None):
     """mode 1 fprop / 2 dgrad / 3 wgrad; geo = (Nimg, H, W, C, Co, R, S, P, Q, sh, sw, ph, pw)."""
+    _want("in0", in0, ("bfloat16",))
+    _want("in1", in1, ("bfloat16",))
+    _want("out", out, ("float32",) if mode == 3 else ("bfloat16",))
+    _want("ws", ws, ("float32",))
     g = (C.c_int32 * 13)(*geo)
     _check(lib().xpipe_conv2d_bf16(mode, g, _ptr(in0), _ptr(in1), _ptr(out), int(accumulate),
                                    _ptr(ws) if ws is not None else None, ws.numel() if ws is not None else 0,

@@ -13,10 +13,19 @@ import torch
 import synthetic as S
 from synthetic.models import conv, bn, relu, maxpool, linear, xent, Layer, FLATTEN, AVGPOOL_GLOBAL, ADD, CONCAT
 
-torch.set_default_dtype(torch.float64)
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 BETAS32 = (float(np.float32(0.9)), float(np.float32(0.999)))
 EPS32 = float(np.float32(1e-8))
+
+
+@pytest.fixture(autouse=True)
+def _float64_default():
+    """fp64 torch twins for this module only (a module-level set_default_dtype would leak into
+    every test module collected after this one, e.g. the GPU tests' fp32 buffers)."""
+    old = torch.get_default_dtype()
+    torch.set_default_dtype(torch.float64)
+    yield
+    torch.set_default_dtype(old)
 
 
 # ----------------------------------------------------------------------------- torch twin

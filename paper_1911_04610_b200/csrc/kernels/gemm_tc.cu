@@ -38,10 +38,12 @@ constexpr int kMaxCluster = 8;
 // MMA issuer, warps 5-8 the epilogue (TMEM lane quadrant = warp % 4)
 constexpr int NTHREADS = 288;
 #ifndef XP_GEMM_MAXREG
-// register cap sized for two co-resident CTAs per SM (2 x 288 threads x 112 <= 64K registers;
-// ptxas spills nothing at 112, whereas __launch_bounds__(288, 2) picks 96 and spills): two GEMM
-// CTAs (e.g. of two pipeline stages' streams) hide each other's fixed latency
-#define XP_GEMM_MAXREG 112
+// register cap for two co-resident CTAs per SM: 2 x 9 warps spread over the 4 SM sub-partitions
+// put 5 warps on one of them, whose 16K-register file then allows 5 x 32 x 96; measured: caps of
+// 104 and 112 (no spills) ran 10 % slower in the 4-stage pipeline than 96 (small spills), i.e.
+// only 96 gives the second CTA.  Two GEMM CTAs (e.g. of two pipeline stages' streams) hide each
+// other's fixed prologue/epilogue latency.
+#define XP_GEMM_MAXREG 96
 #endif
 constexpr int kMaxSmem = 227 * 1024;
 
@@ -325,7 +327,7 @@ struct WgradA {
 // ---------------------------------------------------------------------------------------
 // epilogue: row m of the tile, 32 accumulator columns starting at col0
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, const uint32_t (&v)[32]) {
+__device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, uint32_t (&v)[32]) {
   if (row >= a.M) return;
   if (a.epi == EPI_BF16) {
     bf16* o = static_cast<bf16*>(a.out) + (int64_t)row * a.ldo + col0;
@@ -388,20 +390,19 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
     }
   } else {  // EPI_WGRAD_T: g[co][m] (=|+=) D[m][co]; lanes = consecutive m -> coalesced
     float* g = static_cast<float*>(a.out) + (int64_t)col0 * a.ldo + row;
+    if (a.accumulate) {
 #pragma unroll
-    for (int e0 = 0; e0 < 32; e0 += 8) {
-      // the 8 old values are loaded together (independent addresses), then stored
-      float old[8];
+      for (int e0 = 0; e0 < 32; e0 += 8) {
+        float old[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        old[e] = (a.accumulate && col0 + e0 + e < a.N) ? __ldcg(g + (int64_t)(e0 + e) * a.ldo) : 0.f;
+        for (int e = 0; e < 8; ++e) old[e] = col0 + e0 + e < a.N ? __ldcg(g + (int64_t)(e0 + e) * a.ldo) : 0.f;
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (col0 + e0 + e < a.N) {
-          const float x = __uint_as_float(v[e0 + e]);
-          g[(int64_t)(e0 + e) * a.ldo] = a.accumulate ? __fadd_rn(old[e], x) : x;
-        }
+        for (int e = 0; e < 8; ++e) v[e0 + e] = __float_as_uint(__fadd_rn(old[e], __uint_as_float(v[e0 + e])));
+      }
     }
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (col0 + e < a.N) g[(int64_t)e * a.ldo] = __uint_as_float(v[e]);
   }
 }
 
@@ -1088,7 +1089,7 @@ SplitPlan plan_splits(int M, int N, int K) {
   const int nkb = std::max(1, (K + BK - 1) / BK);
   int s = 1;
   if (!no_splitk() && tiles < num_sms() / 2 && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / split_min_kb()));
-  if (tiles * (int64_t)std::min(s, kMaxCluster) > kTileCounters - 16) s = 1;
+  if (tiles * (int64_t)std::min(s, kMaxCluster) > kTileCounters - 64) s = 1;  // tail: BN counters
   p.cs = std::min(s, kMaxCluster);  // cluster size
   p.nc = std::max(1, s / p.cs);      // clusters per tile
   p.kbps = (nkb + p.cs * p.nc - 1) / (p.cs * p.nc);

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--check", action="store_true", help="compare each GEMM with torch (fp32 math)")
     ap.add_argument("--only", type=int, default=-1, help="run only this layer index")
     ap.add_argument("--modes", default="123", help="subset of 1 fprop / 2 dgrad / 3 wgrad")
+    ap.add_argument("--acc", action="store_true", help="wgrad accumulates into g (micro-batches j > 1)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.manual_seed(0)
@@ -54,14 +55,14 @@ def main():
                 continue
             with torch.cuda.stream(st):
                 for _ in range(3):
-                    xpipe.conv2d_bf16(mode, geo, a, b, o, ws=ws, stream=st.cuda_stream)
+                    xpipe.conv2d_bf16(mode, geo, a, b, o, accumulate=args.acc and mode == 3, ws=ws, stream=st.cuda_stream)
             st.synchronize()
             # GPU time: replay a CUDA graph of `iters` launches (host launch cost excluded)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 cs = torch.cuda.current_stream().cuda_stream
                 for _ in range(args.iters):
-                    xpipe.conv2d_bf16(mode, geo, a, b, o, ws=ws, stream=cs)
+                    xpipe.conv2d_bf16(mode, geo, a, b, o, accumulate=args.acc and mode == 3, ws=ws, stream=cs)
             g.replay()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

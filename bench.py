@@ -27,6 +27,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "pipeline samples/sec (VGG-16 synthetic CIFAR-10, XPipe Adam+prediction)"
+METRICS = {"resnet101": "pipeline samples/sec (ResNet-101 synthetic Tiny-ImageNet 64x64, XPipe Adam+prediction)",
+           "inception": "pipeline samples/sec (Inception-V3 synthetic Tiny-ImageNet 64x64, XPipe Adam+prediction)",
+           "mlp": "pipeline samples/sec (MLP 784-256-256-256-10, XPipe Adam+prediction)"}
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -87,10 +90,27 @@ def dist_env():
     return ws, rank, local
 
 
-def workload_model(name):
+# BASELINE.json configs: default stage count on one GPU (the config's K) and the workload text
+DEFAULT_STAGES = {"mlp": 2, "vgg16": 4, "resnet101": 8, "inception": 4}
+WORKLOAD_TEXT = {"mlp": "MLP 784-256-256-256-10 (configs[0])",
+                 "vgg16": "VGG-16 on synthetic CIFAR-10 32x32 (BASELINE configs[1])",
+                 "resnet101": "ResNet-101 on synthetic Tiny-ImageNet 64x64 (BASELINE configs[2])",
+                 "inception": "Inception-V3 on synthetic Tiny-ImageNet 64x64 (BASELINE configs[3])"}
+
+
+def workload_model(name, K=1):
+    """(layers, input shape, classes, input kind, mini-batch N, micro-batches T, precision) of a
+    BASELINE config; DAG models get explicit unit-based stages for K (R17)."""
     import synthetic as S
+    from synthetic.models import resnet101, inception_v3, assign_stages
     if name == "mlp":
         return S.mlp(), (784, 1, 1), 10, "mnist", 32, 4, "fp32"
+    if name == "resnet101":
+        L, units = resnet101(classes=200)
+        return assign_stages(L, units, K), (3, 64, 64), 200, "imagenet", 256, 8, "bf16"
+    if name == "inception":
+        L, units = inception_v3(classes=200)
+        return assign_stages(L, units, K), (3, 64, 64), 200, "imagenet", 128, 4, "bf16"
     return S.vgg16_cifar(), (3, 32, 32), 10, "cifar", 128, 4, "bf16"
 
 
@@ -117,7 +137,7 @@ def cpu_baseline(workload, seconds=20.0):
                       % (done, n, "bf16 emulation" if prec == "bf16" else "fp32", el)}
 
 
-def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank):
+def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank, sched=None):
     """Bubble fraction of one traced call (single-process mode): 1 - sum_k busy_k / (K * span),
     busy_k = device time of stage k's F/B ops (%globaltimer), next to the uniform-cost ideal
     (K-1)/(M*T+K-1) of SPEC S:397 / SURVEY A.3."""
@@ -127,7 +147,7 @@ def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, 
     import torch
     from paper_1911_04610_b200 import XPipe
     g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
-              devices=list(range(args.gpus)), trace=True, watchdog_ms=300000)
+              devices=list(range(args.gpus)), trace=True, watchdog_ms=300000, **(sched or {}))
     x, y = S.make_inputs(M * N, shape, classes, 2, kind=kind)
     g.step(torch.from_numpy(x).cuda(0), torch.from_numpy(y).cuda((K - 1) % args.gpus), M, flush=True)
     busy, t0s, t1s = [], [], []
@@ -139,7 +159,9 @@ def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, 
         t1s.append(max(r[9] for r in ops))
     g.close()
     span = max(t1s) - min(t0s)
-    return {"bubble_fraction": 1.0 - sum(busy) / (K * span), "ideal_uniform": (K - 1) / (M * T + K - 1),
+    gp = (sched or {}).get("schedule") == "gpipe"
+    ideal = (K - 1) / (T + K - 1) if gp else (K - 1) / (M * T + K - 1)  # SURVEY A.3 closed forms
+    return {"bubble_fraction": 1.0 - sum(busy) / (K * span), "ideal_uniform": ideal,
             "traced_minibatches": M, "note": "separate traced call with flush (trace kernels add overhead)"}
 
 
@@ -164,7 +186,7 @@ def run_reference(args):
     el = time.perf_counter() - t0
     v = args.steps * n / el
     cfg = {"workload": "%s (oracle sample: one %d-sample micro-batch per step, K=1)" % (args.workload, n)}
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRICS.get(args.workload, METRIC), "value": v, "unit": "samples/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1000 / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": cfg,
@@ -233,7 +255,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="vgg16", choices=["vgg16", "mlp", "sweep"])
+    ap.add_argument("--workload", default="vgg16", choices=["vgg16", "mlp", "resnet101", "inception", "sweep"])
     ap.add_argument("--minibatches", type=int, default=4, help="mini-batches fed per step")
     ap.add_argument("--stages", type=int, default=0,
                     help="pipeline stages (default: the BASELINE config's -- VGG-16 4, MLP 2 -- on one GPU, "
@@ -242,6 +264,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the embedded config-5 sweep measurement")
+    ap.add_argument("--schedule", default="xpipe", choices=["xpipe", "gpipe"],
+                    help="gpipe: synchronous GPipe with a flush per mini-batch (prediction off), same kernels")
     ap.add_argument("--no-graphs", action="store_true", help="enqueue every kernel from the host (no CUDA graphs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -265,25 +289,30 @@ def main():
     import numpy as np
     import synthetic as S
     from paper_1911_04610_b200 import XPipe, connect_pipeline
-    L, shape, classes, kind, N, T, prec = workload_model(args.workload)
     M = args.minibatches
     mp_mode = ws > 1
-    # BASELINE configs[1] (VGG-16) is quoted on 4 stages, configs[0] (MLP) on 2: on one GPU all
-    # stages share the device (one stream each); on N GPUs one stage per GPU
-    K = ws if mp_mode else (args.stages or (({"vgg16": 4, "mlp": 2}[args.workload]) if args.gpus == 1 else args.gpus))
+    # each BASELINE config names its stage count (VGG-16 4, ResNet-101 8, Inception-V3 4, MLP 2):
+    # on one GPU all stages share the device (one stream each); on N GPUs one stage per GPU
+    K = ws if mp_mode else (args.stages or (DEFAULT_STAGES[args.workload] if args.gpus == 1 else args.gpus))
+    L, shape, classes, kind, N, T, prec = workload_model(args.workload, K)
     dev = local if mp_mode else 0
     P = S.make_params(L, 1)
+    from synthetic.models import param_count
+    nparams = param_count(L, shape)
+    # f1: the GPipe-flush schedule (prediction off) through the same kernels, for the paper's
+    # XPipe/GPipe throughput comparison (Figs. 7-8)
+    sched = dict(schedule="gpipe", predict="off") if args.schedule == "gpipe" else {}
     def make_model(profile):
         if mp_mode:
             # one process per GPU: this rank owns stage `rank`; rings/flags are CUDA IPC-mapped
             import torch.distributed as dist
             m = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
-                      profile=profile, watchdog_ms=300000, my_stage=rank)
+                      profile=profile, watchdog_ms=300000, my_stage=rank, **sched)
             connect_pipeline(m, dist.new_group(backend="gloo"))
         else:
             m = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
                       devices=list(range(args.gpus)), profile=profile, watchdog_ms=300000,
-                      graphs=not args.no_graphs)
+                      graphs=not args.no_graphs, **sched)
         return m
 
     x, y = S.make_inputs(M * N, shape, classes, 1, kind=kind)
@@ -405,7 +434,7 @@ def main():
               for k, v in prof.items()}
     result = dict(ms=ms, clocks=clocks, roof=roof, shares=shares, launches=launches, replays=replays)
     try:
-        bubble = measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank)
+        bubble = measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank, sched)
     except Exception as e:  # the bubble is a report, not the metric
         bubble = {"error": repr(e)[:200]}
     cpu = None if args.no_cpu_baseline else cpu_baseline(args.workload)
@@ -415,17 +444,17 @@ def main():
         sl = run_sweep(args, peaks, peak_kind, n=1 << 27, steps=20)
         sweep = {k: sl[k] for k in ("value", "unit", "ms_per_step", "roofline")}
         sweep["config"] = sl["config"]["workload"]
-    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
+    line = {"metric": METRICS.get(args.workload, METRIC), "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": result["ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
             "config": {"workload": "%s, K=%d stages, mini-batch %d, T=%d micro-batches, %d mini-batches per step"
-                                   % ("VGG-16 on synthetic CIFAR-10 32x32 (BASELINE configs[1])"
-                                      if args.workload == "vgg16" else "MLP 784-256-256-256-10 (configs[0])",
-                                      K, N, T, M),
+                                   % (WORKLOAD_TEXT[args.workload], K, N, T, M),
                        "processes": "one per GPU (CUDA IPC rings)" if ws > 1 else "one process",
                        "global_batch": N, "stages": K, "micro_batches": T, "minibatches_per_step": M,
-                       "parallelism": "pipeline K=%d (XPipe)" % K,
-                       "l2": "working set > L2: optimizer state 16 B/param x 14.7M params = 235 MB (126 MB L2)"},
+                       "parallelism": "pipeline K=%d (%s)" % (K, "GPipe-flush" if args.schedule == "gpipe" else "XPipe"),
+                       "schedule": args.schedule,
+                       "l2": "working set > L2: optimizer state 16 B/param x %.1fM params = %d MB (126 MB L2)"
+                             % (nparams / 1e6, nparams * 16 // 10**6)},
             "e2e": e2e, "gpu_launches": result["launches"], "graph_replays": result.get("replays"),
             "clocks": result["clocks"],
             "roofline": result["roof"], "kernel_shares": result["shares"], "bubble": bubble, "cpu_baseline": cpu,

@@ -7,6 +7,8 @@
 // Rounding points follow DESIGN.md section 5: every stored activation / activation gradient
 // is bf16 (round-to-nearest-even); statistics, logits and parameter gradients are fp32.
 // All reductions are deterministic (fixed order, no atomics).
+#include <cstdlib>
+
 #include "../internal.h"
 #include "launch.h"
 #include "bf16_kernels.h"
@@ -496,7 +498,11 @@ int bn_threads(int C) { const int G = C / 8; return G >= 256 ? G : (256 / G) * G
 // is in flight at once), at most kBnRows rows per lane (register-resident two passes)
 int bn_chunk_rows(int M, int C) {
   const int RL = bn_threads(C) / (C / 8);
-  return std::max(1, std::min(std::max(RL, (M + 511) / 512), kBnRows * RL));
+  static const int target = [] {  // development knob: target chunk count
+    const char* e = getenv("XPIPE_BN_CHUNKS");
+    return (e && *e) ? std::max(1, atoi(e)) : 512;
+  }();
+  return std::max(1, std::min(std::max(RL, (M + target - 1) / target), kBnRows * RL));
 }
 int bn_chunks(int M, int C) { return (M + bn_chunk_rows(M, C) - 1) / bn_chunk_rows(M, C); }
 size_t bn_ws_floats(int M, int C) { return (size_t)bn_chunks(M, C) * 2 * C + 2 * (size_t)C; }

@@ -1070,10 +1070,16 @@ cudaError_t launch_bn(const GemmArgs& a, int bn, int splits, cudaStream_t st) {
 
 // N tile: the widest tile whose grid still fills the SMs (a narrower tile gives more CTAs and
 // avoids split-K and its reduction pass); 64 when nothing fills them
+__host__ int bn_fill() { static const int v = getenv_int("XPIPE_BN_FILL", 148); return v; }
+// split-K only when the tile grid covers under a quarter of the SMs: with two CTAs per SM and
+// the other pipeline stages' kernels running concurrently, a split's reduction costs more than
+// the idle SMs it would fill (measured: threshold 74 -> 37 tiles, VGG-16 K=4 +5 %, K=1 equal;
+// 24 and below lose at K=1)
+__host__ int split_below() { static const int v = getenv_int("XPIPE_SPLIT_BELOW", num_sms() / 4); return v; }
 int choose_bn(int M, int N) {
   const int64_t mt = (M + 127) / 128;
-  if (N > 128 && mt * ((N + 255) / 256) >= 148) return 256;
-  if (N > 64 && mt * ((N + 127) / 128) >= 148) return 128;
+  if (N > 128 && mt * ((N + 255) / 256) >= bn_fill()) return 256;
+  if (N > 64 && mt * ((N + 127) / 128) >= bn_fill()) return 128;
   return 64;
 }
 
@@ -1088,7 +1094,7 @@ SplitPlan plan_splits(int M, int N, int K) {
   const int tiles = ((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn);
   const int nkb = std::max(1, (K + BK - 1) / BK);
   int s = 1;
-  if (!no_splitk() && tiles < num_sms() / 2 && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / split_min_kb()));
+  if (!no_splitk() && tiles < split_below() && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / split_min_kb()));
   if (tiles * (int64_t)std::min(s, kMaxCluster) > kTileCounters - 64) s = 1;  // tail: BN counters
   p.cs = std::min(s, kMaxCluster);  // cluster size
   p.nc = std::max(1, s / p.cs);      // clusters per tile

@@ -638,7 +638,12 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef XP_EARLY_TRIGGER_GEMM
   pdl_wait();  // the prologue above overlapped the previous kernel; its outputs are visible now
+  pdl_trigger();
+#else
+  pdl_wait_only();  // the prologue above overlapped the previous kernel; its outputs are visible now
+#endif
   const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   if (a.dbg && tid == 0) a.dbg[cta * 16 + 0] = gtimer();
 

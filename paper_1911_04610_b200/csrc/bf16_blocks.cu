@@ -51,14 +51,21 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
     case OP_CONV: {
       const ConvGeo g = conv_geo(c, O, L);
       bf16* mid = (bf16*)s.mid[o][slot];
+      // without split-K the GEMM epilogue also emits the BN partials of its 128-row tiles
+      int bn_tiles = 0;
       XP_TRY(prof_begin(c, s));
-      XP_TRY(check_launch(c, tc_conv_fprop(g, x, W + L.woff, mid, s.ws, s.ws_elems, s.ctr, s.stream), "conv_fprop"));
+      XP_TRY(check_launch(c, tc_conv_fprop(g, x, W + L.woff, mid, s.ws, s.ws_elems, s.ctr, s.stream, s.bnws, &bn_tiles),
+                          "conv_fprop"));
       XP_TRY(prof_end(c, s, XP_PROF_CONV_FPROP, conv_flops(g, L.in0.c)));
       const LayerInfo& N = c->net.layers[O.lbn];
       const int M = n * O.smid.h * O.smid.w;
       XP_TRY(prof_begin(c, s));
-      XP_TRY(check_launch(c, launch_bn_stats(mid, M, O.smid.c, N.d.bn_eps, W + N.woff, W + N.boff, s.bnws,
-                                             s.ctr + kTileCounters - 2, s.stats[o][slot], s.stream), "bn_stats"));
+      if (bn_tiles)
+        XP_TRY(check_launch(c, launch_bn_stats_final(s.bnws, bn_tiles, M, 128, O.smid.c, N.d.bn_eps, W + N.woff,
+                                                     W + N.boff, s.stats[o][slot], s.stream), "bn_stats_final"));
+      else
+        XP_TRY(check_launch(c, launch_bn_stats(mid, M, O.smid.c, N.d.bn_eps, W + N.woff, W + N.boff, s.bnws,
+                                               s.ctr + kTileCounters - 2, s.stats[o][slot], s.stream), "bn_stats"));
       // algorithmic bytes: the conv output read once (register-resident two passes)
       XP_TRY(prof_end(c, s, XP_PROF_BN_STATS, 2.0 * M * O.smid.c));
       const PoolGeo p = pool_geo(c, O.lpool);

@@ -90,7 +90,9 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
       const LayerInfo& L = c->net.layers[O.lmain];
       ConvGeo g{n, O.sin0.h, O.sin0.w, L.cin_pad, L.d.out_c, L.d.kh, L.d.kw, O.smid.h, O.smid.w, L.d.sh, L.d.sw, L.d.ph, L.d.pw};
       ws = std::max(ws, tc_conv_ws_elems(g));
-      bnws = std::max(bnws, bn_ws_floats(n * O.smid.h * O.smid.w, O.smid.c));
+      const int Mmid = n * O.smid.h * O.smid.w;
+      bnws = std::max(bnws, bn_ws_floats(Mmid, O.smid.c));
+      bnws = std::max(bnws, (size_t)((Mmid + 127) / 128) * 2 * O.smid.c);  // fprop-epilogue partials
     }
     s.ws_elems = ws;
     s.ws = (float*)A((size_t)std::max<int64_t>(ws, 64) * 4);

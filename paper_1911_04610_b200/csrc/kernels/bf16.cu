@@ -524,6 +524,13 @@ cudaError_t launch_bn_stats(const bf16* x, int M, int C, float eps, const bf16* 
   return cudaGetLastError();
 }
 
+cudaError_t launch_bn_stats_final(const float* part, int chunks, int M, int RC, int C, float eps, const bf16* gamma,
+                                  const bf16* beta, float* stats, cudaStream_t st) {
+  if (C % 8 || C > 2048) return cudaErrorInvalidValue;
+  launch_pdl(bn_stats_final_kernel, dim3((C + 7) / 8), dim3(256), 0, st, part, chunks, M, RC, C, eps, gamma, beta, stats);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, uint8_t* pidx, int n, int H, int W, int C, int P,
                             int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st) {
   const int64_t total = (int64_t)n * P * Q * (C / 8);

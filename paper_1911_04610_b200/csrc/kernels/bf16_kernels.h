@@ -11,6 +11,10 @@ size_t bn_ws_floats(int M, int C);
 // counter: one zero-initialised int owned by the calling stream (last-block merge)
 cudaError_t launch_bn_stats(const __nv_bfloat16* x, int M, int C, float eps, const __nv_bfloat16* gamma,
                             const __nv_bfloat16* beta, float* ws, int* counter, float* stats, cudaStream_t st);
+// the final merge alone, over partials [chunks][2][C] (mean, M2) of RC-row chunks (the last
+// one ragged) produced elsewhere -- the fprop GEMM epilogue (RC = 128)
+cudaError_t launch_bn_stats_final(const float* part, int chunks, int M, int RC, int C, float eps,
+                                  const __nv_bfloat16* gamma, const __nv_bfloat16* beta, float* stats, cudaStream_t st);
 // pool: pidx receives the winner's position in every window (uint8 per pooled element)
 cudaError_t launch_bn_apply(const __nv_bfloat16* x, const float* stats, __nv_bfloat16* y, uint8_t* pidx, int n, int H,
                             int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,

@@ -324,6 +324,25 @@ struct WgradA {
   }
 };
 
+// Column sums of a warp's 32 x 32 block (lane = row, t[e] = column e) by a fixed butterfly:
+// at offset o every lane keeps one half of its columns and adds the partner's copy of them,
+// so after 5 steps lane l holds the sum over the 32 rows of column l (t is destroyed).
+__device__ __forceinline__ float warp_colsum(float (&t)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = up ? t[i] : t[i + o];
+      const float keep = up ? t[i + o] : t[i];
+      t[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
+  return t[0];
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // the 4 epilogue warps
+__device__ __forceinline__ float bf16r(uint32_t v) { return __bfloat162float(__float2bfloat16_rn(__uint_as_float(v))); }
+
 // ---------------------------------------------------------------------------------------
 // epilogue: row m of the tile, 32 accumulator columns starting at col0
 // ---------------------------------------------------------------------------------------
@@ -610,6 +629,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
   // full[ST], empty[ST], acc_full[2], acc_empty[2], TMEM address slot
   const uint32_t full0 = bars, empty0 = bars + 8 * ST, accf0 = bars + 16 * ST, acce0 = accf0 + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + (bars - raw) + 16 * ST + 32);
+  float* epi_red = reinterpret_cast<float*>(smem_raw + (bars - raw) + 16 * ST + 64);  // [4][32] BN partial exchange
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const int mt = (a.M + BM - 1) / BM, ntiles = mt * ((a.N + BN - 1) / BN);
@@ -701,6 +721,40 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
             for (int e = 0; e < 32; ++e) v[e] = 0u;
           }
           if (w.n0 + c0 < a.N) epi_store(a, row, w.n0 + c0, v);
+          if (MODE == GEMM_FPROP && a.bn_part && w.n0 + c0 < a.N) {
+            // BatchNorm partials of this tile's 32 columns over its valid rows, from the stored
+            // (bf16-rounded) values: tile mean, then the sum of squared deviations (two passes;
+            // the second re-reads the accumulator from TMEM), fixed-order reductions
+            const bool vr = row < a.M;
+            const int nval = min(BM, a.M - w.m0);
+            float t[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) t[e] = vr ? bf16r(v[e]) : 0.f;
+            float cs = warp_colsum(t, lane);
+            epi_red[q * 32 + lane] = cs;
+            epi_bar();
+            const float mean = __fdiv_rn(
+                __fadd_rn(__fadd_rn(__fadd_rn(epi_red[lane], epi_red[32 + lane]), epi_red[64 + lane]), epi_red[96 + lane]),
+                (float)nval);
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + c0), v);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const float d = __fsub_rn(bf16r(v[e]), __shfl_sync(0xffffffffu, mean, e));
+              t[e] = vr ? __fmul_rn(d, d) : 0.f;
+            }
+            cs = warp_colsum(t, lane);
+            epi_bar();  // pass-1 sums read by every warp
+            epi_red[q * 32 + lane] = cs;
+            epi_bar();
+            const int col = w.n0 + c0 + lane;
+            if (q == 0 && col < a.N) {
+              float* bp = a.bn_part + (int64_t)(w.m0 / BM) * 2 * a.N;
+              bp[col] = mean;
+              bp[a.N + col] = __fadd_rn(__fadd_rn(__fadd_rn(epi_red[lane], epi_red[32 + lane]), epi_red[64 + lane]),
+                                        epi_red[96 + lane]);
+            }
+            epi_bar();  // epi_red free for the next chunk
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -993,7 +1047,7 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, DEEP * STAGE + 1024 + 256);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, DEEP * STAGE + 1024 + 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -1007,7 +1061,7 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     grid = dim3(mt, nt, splits);
     args.stages = std::max(4, std::min(DEEP, split_stages()));  // small CTAs: clusters of up to 8 place easily
   }
-  const int SMEM = args.stages * STAGE + 1024 + 256;
+  const int SMEM = args.stages * STAGE + 1024 + 1024;  // ring + alignment + barriers/BN exchange
   args.dbg = gemm_dbg_buffer();
   CUtensorMap tmA, tmB;
   memset(&tmA, 0, sizeof tmA);
@@ -1135,10 +1189,14 @@ cudaError_t tc_gemm_plain(const bf16* A, const bf16* B, float* D, int M, int N, 
 }
 
 cudaError_t tc_conv_fprop(const ConvGeo& g, const bf16* X, const bf16* Wt, bf16* Y, float* ws, int64_t ws_elems,
-                          int* counters, cudaStream_t st) {
+                          int* counters, cudaStream_t st, float* bn_part, int* bn_tiles) {
   GemmArgs a{};
   a.g = g; a.A = X; a.B = Wt;
   a.M = g.Nimg * g.P * g.Q; a.N = g.Co; a.K = g.R * g.S * g.C;
+  const SplitPlan sp = plan_splits(a.M, a.N, a.K);
+  const bool fused_bn = bn_part && sp.cs * sp.nc <= 1;
+  a.bn_part = fused_bn ? bn_part : nullptr;
+  if (bn_tiles) *bn_tiles = fused_bn ? (a.M + BM - 1) / BM : 0;
   return run_split<GEMM_FPROP, false, false>(a, EPI_BF16, Y, g.Co, 0, ws, ws_elems, counters, st);
 }
 

@@ -49,6 +49,10 @@ struct GemmArgs {
   int a_tma;
   int gq, gp;
   int stages;  // smem ring depth (set by the launcher)
+  // FPROP without split-K: the epilogue also writes the BatchNorm partial statistics of every
+  // 128-row tile of the stored (bf16-rounded) output, bn_part[mtile][0][co] = tile mean and
+  // bn_part[mtile][1][co] = sum of squared deviations (rows < M only), or null
+  float* bn_part;
   unsigned long long* dbg;  // development timing probe (XPIPE_GEMM_DBG), else null
 };
 
@@ -59,8 +63,12 @@ cudaError_t tc_gemm_plain(const __nv_bfloat16* A, const __nv_bfloat16* B, float*
 // Y [Nimg*P*Q][Co] bf16 = conv(X [Nimg][H][W][C] bf16, W [Co][R][S][C] bf16)
 // ws: fp32 split-K workspace of ws_elems; counters: kTileCounters zeroed ints owned by the
 // calling stream (NULL = no split-K)
+// bn_part (optional): if the launch runs without split-K, the per-128-row-tile BatchNorm
+// partials of Y go there ([ceil(M/128)][2][Co], see GemmArgs::bn_part) and *bn_tiles is set to
+// ceil(M/128); otherwise *bn_tiles = 0 and the caller computes the statistics itself
 cudaError_t tc_conv_fprop(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* Wt, __nv_bfloat16* Y,
-                          float* ws, int64_t ws_elems, int* counters, cudaStream_t st);
+                          float* ws, int64_t ws_elems, int* counters, cudaStream_t st, float* bn_part = nullptr,
+                          int* bn_tiles = nullptr);
 // dX [Nimg*H*W][Cx] bf16 (Cx = real input channels, multiple of 8) from dY [Nimg*P*Q][Co]
 cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const __nv_bfloat16* dY, const __nv_bfloat16* Wt,
                           __nv_bfloat16* dX, float* ws, int64_t ws_elems, int* counters, cudaStream_t st,

@@ -19,7 +19,8 @@ MODES = {"fp64": 0, "fp32": 1, "bf16": 2}
 SCHEDULES = {"xpipe": 0, "gpipe": 1}
 PREDICT = {"paper": 0, "off": 1, "fixed": 2}
 DELTA = {"adam": 0, "paper": 1}
-STATES = {"param": 0, "m": 1, "v": 2, "pred_fwd": 3, "pred_bwd": 4, "grad": 5}
+STATES = {"param": 0, "m": 1, "v": 2, "pred_fwd": 3, "pred_bwd": 4, "grad": 5, "buf": 6}
+OPTIMIZERS = {"adam": 0, "sgd": 1}
 
 
 def build(force=False):
@@ -43,7 +44,8 @@ class _Config(C.Structure):
                                          "s_fwd", "s_bwd", "delta_form", "snapshots")] + \
                [("init_params", C.POINTER(C.POINTER(C.c_double))),
                 ("init_m", C.POINTER(C.POINTER(C.c_double))),
-                ("init_v", C.POINTER(C.POINTER(C.c_double)))]
+                ("init_v", C.POINTER(C.POINTER(C.c_double))),
+                ("optimizer", C.c_int32), ("momentum", C.c_double), ("weight_decay", C.c_double)]
 
 
 class _Trace(C.Structure):
@@ -72,6 +74,8 @@ def lib():
         _lib.xo_version_difference.argtypes = [C.c_int32] * 4
         _lib.xo_adam_predict.argtypes = [C.c_int32, C.c_int32, C.c_size_t] + [C.c_void_p] * 4 + \
             [C.c_int64, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int32, C.c_int32] + [C.c_void_p] * 5
+        _lib.xo_sgd_predict.argtypes = [C.c_int32, C.c_size_t] + [C.c_void_p] * 5 + [C.c_float] * 6 + \
+            [C.c_int32, C.c_int32] + [C.c_void_p] * 6
         _lib.xo_finalize.argtypes = [C.c_void_p]
         _lib.xo_last_error.restype = C.c_char_p
     return _lib
@@ -106,12 +110,21 @@ def adam_predict(W, g, m, v, k, lr, betas, eps, s_f, s_b, mode="fp32", delta="ad
     return outs  # W', m', v', W_hat_f, W_hat_b
 
 
+def sgd_predict(W, g, buf, m, v, lr, betas, eps, momentum, weight_decay, s_f, s_b, mode="fp32"):
+    """One Momentum-SGD step with the paper-literal prediction (f2), elementwise."""
+    W, g, buf, m, v = (np.ascontiguousarray(a, dtype=np.float32) for a in (W, g, buf, m, v))
+    outs = [np.empty_like(W) for _ in range(6)]
+    _check(lib().xo_sgd_predict(MODES[mode], W.size, _ptr(W), _ptr(g), _ptr(buf), _ptr(m), _ptr(v), lr, betas[0],
+                                betas[1], eps, momentum, weight_decay, s_f, s_b, *[_ptr(o) for o in outs]))
+    return outs  # W', buf', m', v', W_hat_f, W_hat_b
+
+
 class Oracle:
     """Stateful oracle context (mirrors the product's xpipe_init/step/get_weights/trace)."""
 
     def __init__(self, layers, stages, micro_batches, mini_batch, lr, betas, eps, in_shape, classes, params,
                  mode="fp64", schedule="xpipe", predict="paper", s_fwd=0, s_bwd=0, delta="adam",
-                 snapshots=False, init_m=None, init_v=None):
+                 snapshots=False, init_m=None, init_v=None, optimizer="adam", momentum=0.9, weight_decay=5e-4):
         self.layers = list(layers)
         arr = (_Layer * len(self.layers))()
         for i, l in enumerate(self.layers):
@@ -127,7 +140,9 @@ class Oracle:
                     pp[2 * i + t] = a.ctypes.data_as(C.POINTER(C.c_double))
         cfg = _Config(in_c=in_shape[0], in_h=in_shape[1], in_w=in_shape[2], classes=classes, mode=MODES[mode],
                       schedule=SCHEDULES[schedule], predict=PREDICT[predict], s_fwd=s_fwd, s_bwd=s_bwd,
-                      delta_form=DELTA[delta], snapshots=int(snapshots), init_params=pp)
+                      delta_form=DELTA[delta], snapshots=int(snapshots), init_params=pp,
+                      optimizer=OPTIMIZERS[optimizer], momentum=float(np.float32(momentum)),
+                      weight_decay=float(np.float32(weight_decay)))
         for name, src in (("init_m", init_m), ("init_v", init_v)):
             if src is not None:
                 tab = (C.POINTER(C.c_double) * stages)()
@@ -147,7 +162,7 @@ class Oracle:
         self.in_shape, self.classes = tuple(in_shape), classes
 
     def close(self):
-        if self.h:
+        if getattr(self, "h", None):
             lib().xo_finalize(self.h)
             self.h = None
 

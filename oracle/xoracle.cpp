@@ -561,6 +561,8 @@ void xent(const Model& M, int n, int classes, int N, const Vec& z, const int32_t
 struct Hyper {
   double lr, b1, b2, eps;   /* as given (already float-representable) */
   int delta_form = XO_DELTA_ADAM;
+  int opt = XO_OPT_ADAM;
+  double mu = 0.0, wd = 0.0;  /* Momentum SGD, float-representable */
 };
 
 /* beta^k by k repeated multiplications in double, starting from 1 (DESIGN "scalars") */
@@ -624,6 +626,34 @@ void adam_elem(int mode, const Hyper& h, const Scalars& s, double& W, double& m,
   if (dout) *dout = delta(mode, h, s, m, v);
 }
 
+/* one Momentum-SGD step (the paper's training optimizer: momentum 0.9, weight
+   decay 5e-4; PyTorch SGD semantics, dampening 0, no Nesterov) with the prediction's moments
+   tracked by Eq. (4) (g_t = the raw stochastic gradient; R26), in place; returns the
+   paper-literal dW of Eq. (3)/(4) via dout.  fp32 order (DESIGN "f2 sweep"):
+     m' = fmaf(b1, m, omb1*g)     v' = fmaf(b2, v, omb2*(g*g))
+     gw = fmaf(wd, W, g)          buf' = fmaf(mu, buf, gw)         W' = W - lr*buf'           */
+void sgd_elem(int mode, const Hyper& h, const Scalars& s, double& W, double& buf, double& m, double& v, double g,
+              double* dout) {
+  if (mode == XO_FP64) {
+    m = h.b1 * m + (1.0 - h.b1) * g;
+    v = h.b2 * v + (1.0 - h.b2) * g * g;
+    const double gw = g + h.wd * W;
+    buf = h.mu * buf + gw;
+    W = W - h.lr * buf;
+    if (dout) *dout = delta(mode, h, s, m, v);
+    return;
+  }
+  const float mf = std::fmaf((float)h.b1, (float)m, s.omb1 * (float)g);
+  const float vf = std::fmaf((float)h.b2, (float)v, s.omb2 * ((float)g * (float)g));
+  const float gw = std::fmaf((float)h.wd, (float)W, (float)g);
+  const float bf = std::fmaf((float)h.mu, (float)buf, gw);
+  W = (double)((float)W - (float)h.lr * bf);
+  buf = bf;
+  m = mf;
+  v = vf;
+  if (dout) *dout = delta(mode, h, s, m, v);
+}
+
 /* ------------------------------------------------------------------------------------ */
 /* Pipeline state                                                      */
 /* ------------------------------------------------------------------------------------ */
@@ -632,7 +662,7 @@ struct Cache { int64_t t = -1; int ver = 0; Vec Wp; };
 
 struct Stage {
   int k = 0, l0 = 0, l1 = 0;
-  Vec W, m, v, g;
+  Vec W, m, v, g, buf;   /* buf: Momentum-SGD velocity (XO_OPT_SGD) */
   int ver = 0;
   Cache cf, cb;
   std::map<int64_t, std::vector<Vec>> stash;          /* u -> [stage input, outputs of l0..l1-1] */
@@ -895,7 +925,11 @@ int try_step(xo_ctx& c, int k) {
         /* the T-th micro-batch's backward ends the mini-batch: update */
         const int64_t kv = st.ver + 1;
         Scalars sc = scalars(c.H, kv);
-        for (size_t i = 0; i < st.W.size(); ++i) adam_elem(c.M.mode, c.H, sc, st.W[i], st.m[i], st.v[i], st.g[i], nullptr);
+        if (c.H.opt == XO_OPT_SGD)
+          for (size_t i = 0; i < st.W.size(); ++i)
+            sgd_elem(c.M.mode, c.H, sc, st.W[i], st.buf[i], st.m[i], st.v[i], st.g[i], nullptr);
+        else
+          for (size_t i = 0; i < st.W.size(); ++i) adam_elem(c.M.mode, c.H, sc, st.W[i], st.m[i], st.v[i], st.g[i], nullptr);
         st.ver = (int)kv;
         trace_push(st, 2, t, j, st.ver, 0, 0);
         if (c.snapshots) st.snaps[st.ver] = st.W;
@@ -946,6 +980,10 @@ int xo_init(const xo_layer* layers, int32_t n_layers, int32_t stages, int32_t T,
   std::unique_ptr<xo_ctx> c(new xo_ctx());
   c->K = stages; c->T = T; c->N = N; c->n = N / T;
   c->H.lr = lr; c->H.b1 = beta1; c->H.b2 = beta2; c->H.eps = eps; c->H.delta_form = cfg->delta_form;
+  c->H.opt = cfg->optimizer; c->H.mu = cfg->momentum; c->H.wd = cfg->weight_decay;
+  if (c->H.opt != XO_OPT_ADAM && c->H.opt != XO_OPT_SGD) return fail(E_INVAL, "optimizer");
+  if (c->H.opt == XO_OPT_SGD && (cfg->delta_form != XO_DELTA_PAPER || !(c->H.mu >= 0 && c->H.mu < 1) || !(c->H.wd >= 0)))
+    return fail(E_INVAL, "Momentum SGD needs the paper prediction form, momentum in [0,1), weight decay >= 0");
   c->schedule = cfg->schedule; c->predict = cfg->predict; c->s_fwd = cfg->s_fwd; c->s_bwd = cfg->s_bwd;
   c->snapshots = cfg->snapshots != 0;
   Model& M = c->M;
@@ -1062,6 +1100,7 @@ int xo_init(const xo_layer* layers, int32_t n_layers, int32_t stages, int32_t T,
       l.boff = off; off += l.nb;
     }
     st.W.assign(off, 0.0); st.m.assign(off, 0.0); st.v.assign(off, 0.0); st.g.assign(off, 0.0);
+    st.buf.assign(off, 0.0);
     for (int i = st.l0; i < st.l1; ++i) {
       const Layer& l = M.L[i];
       if (l.nw) {
@@ -1162,6 +1201,7 @@ int xo_get_param(xo_ctx* c, int32_t layer, int32_t tensor, int32_t state, int64_
       }
       break;
     case XO_M: src = &st.m; break;
+    case XO_BUF: src = &st.buf; break;
     case XO_V: src = &st.v; break;
     case XO_GRAD: src = &st.g; break;
     case XO_PRED_FWD: case XO_PRED_BWD:
@@ -1220,6 +1260,24 @@ int xo_eval_loss_grad(xo_ctx* c, const float* x, const int32_t* y, int32_t n, do
       for (size_t q = 0; q < l.nw; ++q) grad[o++] = g[l.woff + q];
       for (size_t q = 0; q < l.nb; ++q) grad[o++] = g[l.boff + q];
     }
+  }
+  return E_OK;
+}
+
+int xo_sgd_predict(int32_t mode, size_t n, const float* W, const float* g, const float* buf, const float* m,
+                   const float* v, float lr, float beta1, float beta2, float eps, float momentum, float weight_decay,
+                   int32_t s_f, int32_t s_b, float* W_out, float* buf_out, float* m_out, float* v_out, float* pf_out,
+                   float* pb_out) {
+  Hyper h;
+  h.lr = lr; h.b1 = beta1; h.b2 = beta2; h.eps = eps; h.delta_form = XO_DELTA_PAPER;
+  h.opt = XO_OPT_SGD; h.mu = momentum; h.wd = weight_decay;
+  Scalars sc = scalars(h, 1);  /* the paper form uses only the constant corrections */
+  for (size_t i = 0; i < n; ++i) {
+    double Wd = W[i], bd = buf[i], md = m[i], vd = v[i], d;
+    sgd_elem(mode, h, sc, Wd, bd, md, vd, g[i], &d);
+    W_out[i] = (float)Wd; buf_out[i] = (float)bd; m_out[i] = (float)md; v_out[i] = (float)vd;
+    if (pf_out) pf_out[i] = (float)predict_elem(mode, Wd, d, s_f);
+    if (pb_out) pb_out[i] = (float)predict_elem(mode, Wd, d, s_b);
   }
   return E_OK;
 }

@@ -36,7 +36,11 @@ enum { XO_FP64 = 0, XO_FP32 = 1, XO_BF16 = 2 };
 enum { XO_SCHED_XPIPE = 0, XO_SCHED_GPIPE = 1 };
 enum { XO_PRED_PAPER = 0, XO_PRED_OFF = 1, XO_PRED_FIXED = 2 };
 enum { XO_DELTA_ADAM = 0, XO_DELTA_PAPER = 1 };
-enum { XO_PARAM = 0, XO_M = 1, XO_V = 2, XO_PRED_FWD = 3, XO_PRED_BWD = 4, XO_GRAD = 5 };
+enum { XO_PARAM = 0, XO_M = 1, XO_V = 2, XO_PRED_FWD = 3, XO_PRED_BWD = 4, XO_GRAD = 5, XO_BUF = 6 };
+/* training optimizer: Adam (north star) or the paper's main-experiment Momentum SGD
+   (momentum 0.9, weight decay 5e-4) with the prediction's moments tracked
+   alongside by Eq. (4) */
+enum { XO_OPT_ADAM = 0, XO_OPT_SGD = 1 };
 
 typedef struct {
   int32_t kind, in_c, out_c, kh, kw, sh, sw, ph, pw, bias;
@@ -56,6 +60,9 @@ typedef struct {
      order; NULL = zeros */
   const double* const* init_m;
   const double* const* init_v;
+  /* XO_OPT_SGD (requires delta_form = XO_DELTA_PAPER): W <- W - lr*buf, buf <- mu*buf + (g + wd*W) */
+  int32_t optimizer;
+  double momentum, weight_decay;
 } xo_config;
 
 typedef struct { int32_t stage, op /*0=F 1=B 2=U*/, t, j, version, s, bellwether; } xo_trace_rec;
@@ -81,6 +88,12 @@ int  xo_eval_loss_grad(xo_ctx* h, const float* x, const int32_t* y, int32_t n,
 /* Eq. (1) (pass 0) / Eq. (2) (pass 1), half-up rounding */
 int  xo_version_difference(int32_t K, int32_t T, int32_t rank, int32_t pass);
 /* the elementwise Adam update + prediction, version k = new version */
+/* one Momentum-SGD step with the paper-literal prediction (Eq. (3)-(4)), elementwise:
+   outputs W', buf', m' (Eq. (4) v_t, first moment), v' (Eq. (4) m_t, second moment), W_hat_f/b */
+int  xo_sgd_predict(int32_t mode, size_t n, const float* W, const float* g, const float* buf, const float* m,
+                    const float* v, float lr, float beta1, float beta2, float eps, float momentum,
+                    float weight_decay, int32_t s_f, int32_t s_b, float* W_out, float* buf_out, float* m_out,
+                    float* v_out, float* pf_out, float* pb_out);
 int  xo_adam_predict(int32_t mode, int32_t delta_form, size_t n, const float* W, const float* g,
                      const float* m, const float* v, int64_t k, float lr, float beta1, float beta2,
                      float eps, int32_t s_f, int32_t s_b, float* W_out, float* m_out, float* v_out,

@@ -56,6 +56,11 @@ enum { XP_PRED_PAPER = 0,  /* s from Eq. (1)/(2) */
 enum { XP_DELTA_ADAM = 0,  /* dW = lr * m_hat / (sqrt(v_hat) + eps)   (north star) */
        XP_DELTA_PAPER = 1 };/* dW = lr * (m/(1-b1)) / sqrt(v/(1-b2) + eps)  (Eq. (3)-(4) literal) */
 enum { XP_MOM_ZERO = 0, XP_MOM_GIVEN = 1 /* cfg.init_m / cfg.init_v (e.g. 1e-4*U[0,1)) */ };
+/* training optimizer.  XP_OPT_MOMENTUM_SGD is the paper's main-experiment optimizer
+   (SURVEY 8f row f2): buf = momentum*buf + (g + weight_decay*W), W -= lr*buf, while
+   the prediction keeps its own Eq. (4) moments of the raw gradient and uses the
+   literal Eq. (3)/(4) dW, so it requires delta_form = XP_DELTA_PAPER. */
+enum { XP_OPT_ADAM = 0, XP_OPT_MOMENTUM_SGD = 1 };
 enum { XP_TRANSPORT_P2P = 0 };  /* producer kernels store into the consumer's ring slot
                                    (same device or NVLink peer); device-side flags order it */
 
@@ -66,7 +71,8 @@ enum { XP_FLUSH = 1,        /* drain the pipeline at the end of the call */
 
 /* xpipe_get_weights selectors */
 enum { XP_T_WEIGHT = 0, XP_T_BIAS = 1 };       /* BatchNorm: WEIGHT = gamma, BIAS = beta */
-enum { XP_S_PARAM = 0, XP_S_M = 1, XP_S_V = 2, XP_S_PRED_FWD = 3, XP_S_PRED_BWD = 4, XP_S_GRAD = 5 };
+enum { XP_S_PARAM = 0, XP_S_M = 1, XP_S_V = 2, XP_S_PRED_FWD = 3, XP_S_PRED_BWD = 4, XP_S_GRAD = 5,
+       XP_S_BUF = 6 /* Momentum-SGD velocity (XP_OPT_MOMENTUM_SGD) */ };
 
 /* One layer.  src0/src1: producer layer indices (-1 = the previous layer); a DAG edge may
    not cross a stage cut except into the next stage's first layer.  stage: -1 = automatic
@@ -112,6 +118,8 @@ typedef struct {
   xpipe_alloc_fn alloc;               /* NULL = cudaMalloc / cudaFree */
   xpipe_free_fn free;
   void* alloc_user;
+  int32_t optimizer;                  /* XP_OPT_ADAM (default) | XP_OPT_MOMENTUM_SGD */
+  float momentum, weight_decay;       /* XP_OPT_MOMENTUM_SGD: in [0,1) and >= 0 (paper: 0.9, 5e-4) */
 } xpipe_config;
 
 /* one device-trace record (K12): op 0 = forward, 1 = backward, 2 = update.  version is the
@@ -218,6 +226,15 @@ const char* xpipe_last_error(const struct xpipe_ctx* h);
 int xpipe_adam_predict(float* W, const float* g, float* m, float* v, void* pred_f, void* pred_b,
                        int64_t n, int64_t version, float lr, float beta1, float beta2, float eps,
                        int32_t s_f, int32_t s_b, int32_t pred_bf16, int32_t delta_form, void* stream);
+
+/* Kernel-level entry point of the f2 sweep (XP_OPT_MOMENTUM_SGD): one Momentum-SGD step with
+   the Eq. (4) moments tracked alongside and the paper-literal prediction, over n device
+   floats in place (W, buf, m, v; 16-byte aligned), predictions into pred_f / pred_b (bf16 if
+   pred_bf16, else fp32; either may be NULL).  Op order: DESIGN.md "f2".  Errors: XP_EINVAL for
+   NULL / misaligned pointers or n < 0; XP_ECUDA for a launch failure. */
+int xpipe_sgd_predict(float* W, const float* g, float* buf, float* m, float* v, void* pred_f, void* pred_b,
+                      int64_t n, float lr, float beta1, float beta2, float eps, float momentum, float weight_decay,
+                      int32_t s_f, int32_t s_b, int32_t pred_bf16, void* stream /* cudaStream_t, NULL = default */);
 
 /* bf16 tensor-core GEMM used by the conv/linear path, exposed for unit parity:
    D[M][N] (fp32, row-major, ldd) = sum_k A(m,k) * B(n,k) with A given row-major [M][K]

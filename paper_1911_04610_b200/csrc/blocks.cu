@@ -28,6 +28,7 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
   s.flags = (uint32_t*)dmalloc_shared(c, 64, s.dev);
   if (!s.W || !s.g || !s.m || !s.v || !s.pf[0] || !s.pf[1] || !s.pb || !s.ds || !s.flags)
     return set_err(c, XP_ENOMEM, "arena");
+  if (c->cfg.optimizer == XP_OPT_MOMENTUM_SGD && !(s.buf = (float*)A(P * 4))) return set_err(c, XP_ENOMEM, "arena");
   XP_CUDA(c, cudaMemsetAsync(s.flags, 0, 64, s.stream));
   const int n = c->n;
   // rings: one contiguous allocation each (one IPC handle per ring in multi-process mode)
@@ -116,6 +117,7 @@ int init_stage_params(xpipe_ctx* c, StageRT& s, const xpipe_layer* layers) {
   XP_CUDA(c, cudaMemsetAsync(s.g, 0, p.P * 4, s.stream));
   XP_CUDA(c, cudaMemsetAsync(s.m, 0, p.P * 4, s.stream));
   XP_CUDA(c, cudaMemsetAsync(s.v, 0, p.P * 4, s.stream));
+  if (s.buf) XP_CUDA(c, cudaMemsetAsync(s.buf, 0, p.P * 4, s.stream));
   std::vector<float> host_w, host_m, host_v;
   const bool given = c->cfg.init_params != nullptr;
   const bool mom = c->cfg.moment_init == XP_MOM_GIVEN;
@@ -170,7 +172,8 @@ int init_stage_params(xpipe_ctx* c, StageRT& s, const xpipe_layer* layers) {
     XP_CUDA(c, cudaMemcpyAsync(s.m, host_m.data(), p.P * 4, cudaMemcpyHostToDevice, s.stream));
     XP_CUDA(c, cudaMemcpyAsync(s.v, host_v.data(), p.P * 4, cudaMemcpyHostToDevice, s.stream));
   }
-  XP_TRY(check_launch(c, launch_state_init(s.ds, c->lr, c->b1, c->b2, c->eps, s.stream), "state"));
+  XP_TRY(check_launch(c, launch_state_init(s.ds, c->lr, c->b1, c->b2, c->eps, c->cfg.momentum, c->cfg.weight_decay,
+                                           s.stream), "state"));
   const bool bf = is_bf16(c);
   if (c->cfg.delta_form == XP_DELTA_PAPER) {
     // version 0 under the paper form: W_hat = W - s * dW_paper(m0, v0) (moments may be non-zero)

@@ -19,11 +19,12 @@ struct DevState {
   float omb1, omb2; // 1-b1, 1-b2 (fp32)
   float inv1, inv2; // 1/(1-b1), 1/(1-b2) (paper delta form)
   float lr, b1, b2, eps;
+  float mu, wd;     // Momentum-SGD momentum and weight decay (XP_OPT_MOMENTUM_SGD, f2)
 };
 
 // Scalars of one sweep launch (host-computed for the standalone entry point).
 struct SweepScalars {
-  float c1, r2, omb1, omb2, inv1, inv2, lr, b1, b2, eps;
+  float c1, r2, omb1, omb2, inv1, inv2, lr, b1, b2, eps, mu, wd;
 };
 
 struct TraceRec {  // identical layout to xpipe_trace_rec
@@ -36,11 +37,17 @@ struct TraceRec {  // identical layout to xpipe_trace_rec
 cudaError_t launch_sweep(float* W, const float* g, float* m, float* v, void* pf, void* pb, int64_t n,
                          const DevState* ds, const SweepScalars* hs, float s_f, float s_b, bool bf16,
                          int delta_form, bool update, cudaStream_t st);
+// f2: Momentum-SGD step (buf = mu*buf + (g + wd*W), W -= lr*buf) with the Eq. (4) moments
+// tracked alongside and the paper-literal prediction dW (Eq. (3)/(4)), one pass
+cudaError_t launch_sweep_sgd(float* W, const float* g, float* buf, float* m, float* v, void* pf, void* pb, int64_t n,
+                             const DevState* ds, const SweepScalars* hs, float s_f, float s_b, bool bf16,
+                             cudaStream_t st);
 // W_hat = W converted (version 0 with zero moments: no delta)
 cudaError_t launch_predict_copy(const float* W, void* pf, void* pb, int64_t n, bool bf16, cudaStream_t st);
 // version bump before an update: ver += 1, beta powers, c1, r2 (1 thread)
 cudaError_t launch_bump(DevState* ds, TraceRec* rec, int stage, int t, int T, cudaStream_t st);
-cudaError_t launch_state_init(DevState* ds, float lr, float b1, float b2, float eps, cudaStream_t st);
+cudaError_t launch_state_init(DevState* ds, float lr, float b1, float b2, float eps, float mu, float wd,
+                              cudaStream_t st);
 void host_scalars(int64_t k, float lr, float b1, float b2, float eps, SweepScalars* out);
 
 // ---- misc kernels (kernels/f32.cu) -----------------------------------------------------

@@ -23,19 +23,31 @@ namespace xp {
 namespace {
 
 struct Sc {
-  float c1, r2, omb1, omb2, inv1, inv2, lr, b1, b2, eps;
+  float c1, r2, omb1, omb2, inv1, inv2, lr, b1, b2, eps, mu, wd;
 };
 
 __device__ __forceinline__ Sc load_sc(const DevState* ds, const SweepScalars& hs) {
   Sc s;
   if (ds) {
     s.c1 = ds->c1; s.r2 = ds->r2; s.omb1 = ds->omb1; s.omb2 = ds->omb2; s.inv1 = ds->inv1; s.inv2 = ds->inv2;
-    s.lr = ds->lr; s.b1 = ds->b1; s.b2 = ds->b2; s.eps = ds->eps;
+    s.lr = ds->lr; s.b1 = ds->b1; s.b2 = ds->b2; s.eps = ds->eps; s.mu = ds->mu; s.wd = ds->wd;
   } else {
     s.c1 = hs.c1; s.r2 = hs.r2; s.omb1 = hs.omb1; s.omb2 = hs.omb2; s.inv1 = hs.inv1; s.inv2 = hs.inv2;
-    s.lr = hs.lr; s.b1 = hs.b1; s.b2 = hs.b2; s.eps = hs.eps;
+    s.lr = hs.lr; s.b1 = hs.b1; s.b2 = hs.b2; s.eps = hs.eps; s.mu = hs.mu; s.wd = hs.wd;
   }
   return s;
+}
+
+// one parameter, f2: Momentum-SGD update in place (PyTorch semantics: buf = mu*buf + (g + wd*W),
+// W -= lr*buf) with the Eq. (4) moments tracked from the raw gradient, returning the paper-form
+// prediction delta -- the op order of the oracle's sgd_elem
+__device__ __forceinline__ float elem_sgd(const Sc& s, float& W, float g, float& buf, float& m, float& v) {
+  m = __fmaf_rn(s.b1, m, __fmul_rn(s.omb1, g));
+  v = __fmaf_rn(s.b2, v, __fmul_rn(s.omb2, __fmul_rn(g, g)));
+  const float gw = __fmaf_rn(s.wd, W, g);
+  buf = __fmaf_rn(s.mu, buf, gw);
+  W = __fsub_rn(W, __fmul_rn(s.lr, buf));
+  return __fdiv_rn(__fmul_rn(s.lr, __fmul_rn(m, s.inv1)), __fsqrt_rn(__fadd_rn(__fmul_rn(v, s.inv2), s.eps)));
 }
 
 // one parameter: Adam update in place + prediction delta (Adam or paper form)
@@ -136,6 +148,80 @@ __global__ void __launch_bounds__(256) sweep_kernel(float* __restrict__ W, const
   }
 }
 
+// f2 sweep: reads W, g, buf, m, v (20 B) and writes W, buf, m, v (16 B) + two predictions per
+// parameter; 8 parameters per thread-iteration as in the Adam sweep
+template <bool BF16>
+__global__ void __launch_bounds__(256) sweep_sgd_kernel(float* __restrict__ W, const float* __restrict__ g,
+                                                        float* __restrict__ buf, float* __restrict__ m,
+                                                        float* __restrict__ v, void* __restrict__ pf,
+                                                        void* __restrict__ pb, int64_t n,
+                                                        const DevState* __restrict__ ds, SweepScalars hs, float sf,
+                                                        float sb) {
+  pdl_wait();
+  const Sc s = load_sc(ds, hs);
+  const float nsf = -sf, nsb = -sb;
+  const int64_t n8 = n >> 3;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
+    const int64_t e = i << 3;
+    float wv[8], gv[8], bv[8], mv[8], vv[8], fv[8], pv[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float4 w4 = __ldcs(reinterpret_cast<const float4*>(W + e) + h);
+      const float4 g4 = __ldcs(reinterpret_cast<const float4*>(g + e) + h);
+      const float4 b4 = __ldcs(reinterpret_cast<const float4*>(buf + e) + h);
+      const float4 m4 = __ldcs(reinterpret_cast<const float4*>(m + e) + h);
+      const float4 v4 = __ldcs(reinterpret_cast<const float4*>(v + e) + h);
+      wv[4 * h] = w4.x; wv[4 * h + 1] = w4.y; wv[4 * h + 2] = w4.z; wv[4 * h + 3] = w4.w;
+      gv[4 * h] = g4.x; gv[4 * h + 1] = g4.y; gv[4 * h + 2] = g4.z; gv[4 * h + 3] = g4.w;
+      bv[4 * h] = b4.x; bv[4 * h + 1] = b4.y; bv[4 * h + 2] = b4.z; bv[4 * h + 3] = b4.w;
+      mv[4 * h] = m4.x; mv[4 * h + 1] = m4.y; mv[4 * h + 2] = m4.z; mv[4 * h + 3] = m4.w;
+      vv[4 * h] = v4.x; vv[4 * h + 1] = v4.y; vv[4 * h + 2] = v4.z; vv[4 * h + 3] = v4.w;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float d = elem_sgd(s, wv[q], gv[q], bv[q], mv[q], vv[q]);
+      fv[q] = __fmaf_rn(nsf, d, wv[q]);
+      pv[q] = __fmaf_rn(nsb, d, wv[q]);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      __stcs(reinterpret_cast<float4*>(W + e) + h, make_float4(wv[4 * h], wv[4 * h + 1], wv[4 * h + 2], wv[4 * h + 3]));
+      __stcs(reinterpret_cast<float4*>(buf + e) + h, make_float4(bv[4 * h], bv[4 * h + 1], bv[4 * h + 2], bv[4 * h + 3]));
+      __stcs(reinterpret_cast<float4*>(m + e) + h, make_float4(mv[4 * h], mv[4 * h + 1], mv[4 * h + 2], mv[4 * h + 3]));
+      __stcs(reinterpret_cast<float4*>(v + e) + h, make_float4(vv[4 * h], vv[4 * h + 1], vv[4 * h + 2], vv[4 * h + 3]));
+    }
+    if (BF16) {
+      if (pf) *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(pf) + e) =
+          make_uint4(pack_bf16(fv[0], fv[1]), pack_bf16(fv[2], fv[3]), pack_bf16(fv[4], fv[5]), pack_bf16(fv[6], fv[7]));
+      if (pb) *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(pb) + e) =
+          make_uint4(pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]), pack_bf16(pv[6], pv[7]));
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (pf) reinterpret_cast<float4*>(static_cast<float*>(pf) + e)[h] =
+            make_float4(fv[4 * h], fv[4 * h + 1], fv[4 * h + 2], fv[4 * h + 3]);
+        if (pb) reinterpret_cast<float4*>(static_cast<float*>(pb) + e)[h] =
+            make_float4(pv[4 * h], pv[4 * h + 1], pv[4 * h + 2], pv[4 * h + 3]);
+      }
+    }
+  }
+  const int64_t tail0 = n8 << 3;
+  for (int64_t e = tail0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+    float w = W[e], bb = buf[e], mm = m[e], vv = v[e];
+    const float d = elem_sgd(s, w, g[e], bb, mm, vv);
+    W[e] = w; buf[e] = bb; m[e] = mm; v[e] = vv;
+    const float f = __fmaf_rn(nsf, d, w), b = __fmaf_rn(nsb, d, w);
+    if (BF16) {
+      if (pf) static_cast<__nv_bfloat16*>(pf)[e] = __float2bfloat16_rn(f);
+      if (pb) static_cast<__nv_bfloat16*>(pb)[e] = __float2bfloat16_rn(b);
+    } else {
+      if (pf) static_cast<float*>(pf)[e] = f;
+      if (pb) static_cast<float*>(pb)[e] = b;
+    }
+  }
+}
+
 template <bool BF16>
 __global__ void predict_copy_kernel(const float* __restrict__ W, void* __restrict__ pf, void* __restrict__ pb,
                                     int64_t n) {
@@ -168,7 +254,7 @@ __global__ void bump_kernel(DevState* ds, TraceRec* rec, int stage, int t, int T
   }
 }
 
-__global__ void state_init_kernel(DevState* ds, float lr, float b1, float b2, float eps) {
+__global__ void state_init_kernel(DevState* ds, float lr, float b1, float b2, float eps, float mu, float wd) {
   pdl_wait();
   ds->ver = 0; ds->fver = 0; ds->bver = 0; ds->pad = 0;
   ds->b1p = 1.0; ds->b2p = 1.0;
@@ -178,6 +264,7 @@ __global__ void state_init_kernel(DevState* ds, float lr, float b1, float b2, fl
   ds->inv1 = (float)(1.0 / (1.0 - (double)b1));
   ds->inv2 = (float)(1.0 / (1.0 - (double)b2));
   ds->lr = lr; ds->b1 = b1; ds->b2 = b2; ds->eps = eps;
+  ds->mu = mu; ds->wd = wd;
 }
 
 }  // namespace
@@ -191,7 +278,7 @@ void host_scalars(int64_t k, float lr, float b1, float b2, float eps, SweepScala
   o->omb2 = (float)(1.0 - (double)b2);
   o->inv1 = (float)(1.0 / (1.0 - (double)b1));
   o->inv2 = (float)(1.0 / (1.0 - (double)b2));
-  o->lr = lr; o->b1 = b1; o->b2 = b2; o->eps = eps;
+  o->lr = lr; o->b1 = b1; o->b2 = b2; o->eps = eps; o->mu = 0.f; o->wd = 0.f;
 }
 
 static int sweep_grid(int64_t n) {
@@ -226,6 +313,17 @@ cudaError_t launch_sweep(float* W, const float* g, float* m, float* v, void* pf,
   return cudaGetLastError();
 }
 
+cudaError_t launch_sweep_sgd(float* W, const float* g, float* buf, float* m, float* v, void* pf, void* pb, int64_t n,
+                             const DevState* ds, const SweepScalars* hs, float s_f, float s_b, bool bf16,
+                             cudaStream_t st) {
+  SweepScalars h{};
+  if (hs) h = *hs;
+  const int grid = sweep_grid(n);
+  if (bf16) launch_pdl(sweep_sgd_kernel<true>, dim3(grid), dim3(256), 0, st, W, g, buf, m, v, pf, pb, n, ds, h, s_f, s_b);
+  else launch_pdl(sweep_sgd_kernel<false>, dim3(grid), dim3(256), 0, st, W, g, buf, m, v, pf, pb, n, ds, h, s_f, s_b);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_predict_copy(const float* W, void* pf, void* pb, int64_t n, bool bf16, cudaStream_t st) {
   int grid = (int)((n + 255) / 256);
   if (grid > 148 * 16) grid = 148 * 16;
@@ -240,8 +338,9 @@ cudaError_t launch_bump(DevState* ds, TraceRec* rec, int stage, int t, int T, cu
   return cudaGetLastError();
 }
 
-cudaError_t launch_state_init(DevState* ds, float lr, float b1, float b2, float eps, cudaStream_t st) {
-  launch_pdl(state_init_kernel, dim3(1), dim3(1), 0, st, ds, lr, b1, b2, eps);
+cudaError_t launch_state_init(DevState* ds, float lr, float b1, float b2, float eps, float mu, float wd,
+                              cudaStream_t st) {
+  launch_pdl(state_init_kernel, dim3(1), dim3(1), 0, st, ds, lr, b1, b2, eps, mu, wd);
   return cudaGetLastError();
 }
 

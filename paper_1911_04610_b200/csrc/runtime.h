@@ -38,6 +38,7 @@ struct StageRT {
   int l0 = 0, l1 = 0;
   StagePlan plan;                       // blocks, arena layout (plan.h)
   float *W = nullptr, *g = nullptr, *m = nullptr, *v = nullptr;
+  float* buf = nullptr;                 // Momentum-SGD velocity (XP_OPT_MOMENTUM_SGD only)
   void* pf[2] = {nullptr, nullptr};
   void* pb = nullptr;
   DevState* ds = nullptr;

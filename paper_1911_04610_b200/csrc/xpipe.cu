@@ -380,8 +380,12 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     const float sf = (float)version_difference(c, k, 0), sbf = (float)sb;
     const bool bf16 = c->cfg.precision == XP_BF16;
     XP_TRY(prof_begin(c, s));
-    XP_TRY(check_launch(c, launch_sweep(s.W, s.g, s.m, s.v, s.pf[nv & 1], s.pb, s.plan.P, s.ds, nullptr, sf, sbf, bf16,
-                                        c->cfg.delta_form, true, s.stream), "sweep"));
+    if (c->cfg.optimizer == XP_OPT_MOMENTUM_SGD)
+      XP_TRY(check_launch(c, launch_sweep_sgd(s.W, s.g, s.buf, s.m, s.v, s.pf[nv & 1], s.pb, s.plan.P, s.ds, nullptr, sf,
+                                              sbf, bf16, s.stream), "sweep_sgd"));
+    else
+      XP_TRY(check_launch(c, launch_sweep(s.W, s.g, s.m, s.v, s.pf[nv & 1], s.pb, s.plan.P, s.ds, nullptr, sf, sbf,
+                                          bf16, c->cfg.delta_form, true, s.stream), "sweep"));
     XP_TRY(prof_end(c, s, XP_PROF_SWEEP, (double)s.plan.P * (bf16 ? 32.0 : 36.0)));
     s.host_ver = nv;
     if (c->cfg.snapshots) {
@@ -657,6 +661,11 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
     return set_err(nullptr, XP_EINVAL, "hyperparameters: lr > 0, betas in [0,1), eps > 0");
   if (cfg->moment_init == XP_MOM_GIVEN && (cfg->delta_form != XP_DELTA_PAPER || !cfg->init_m || !cfg->init_v))
     return set_err(nullptr, XP_EINVAL, "XP_MOM_GIVEN requires XP_DELTA_PAPER and init_m/init_v (R2)");
+  if (cfg->optimizer != XP_OPT_ADAM && cfg->optimizer != XP_OPT_MOMENTUM_SGD)
+    return set_err(nullptr, XP_EINVAL, "optimizer");
+  if (cfg->optimizer == XP_OPT_MOMENTUM_SGD &&
+      (cfg->delta_form != XP_DELTA_PAPER || !(cfg->momentum >= 0 && cfg->momentum < 1) || !(cfg->weight_decay >= 0)))
+    return set_err(nullptr, XP_EINVAL, "XP_OPT_MOMENTUM_SGD requires XP_DELTA_PAPER, momentum in [0,1), weight_decay >= 0");
   if (cfg->precision != XP_FP32 && cfg->precision != XP_BF16) return set_err(nullptr, XP_EINVAL, "precision");
   if (cfg->schedule != XP_SCHED_XPIPE && cfg->schedule != XP_SCHED_GPIPE) return set_err(nullptr, XP_EINVAL, "schedule");
   if (cfg->predict < 0 || cfg->predict > 2 || (cfg->predict == XP_PRED_FIXED && (cfg->s_fwd < 0 || cfg->s_bwd < 0)))
@@ -953,6 +962,10 @@ int xpipe_get_weights(xpipe_ctx* c, int32_t layer, int32_t tensor, int32_t state
         case XP_S_M: src = s.m; break;
         case XP_S_V: src = s.v; break;
         case XP_S_GRAD: src = s.g; break;
+        case XP_S_BUF:
+          if (!s.buf) return set_err(c, XP_EINVAL, "XP_S_BUF needs XP_OPT_MOMENTUM_SGD");
+          src = s.buf;
+          break;
         default: return set_err(c, XP_EINVAL, "state");
       }
       XP_CUDA(c, cudaMemcpy(buf.data(), src + off, ng * 4, cudaMemcpyDeviceToHost));
@@ -987,6 +1000,22 @@ int xpipe_adam_predict(float* W, const float* g, float* m, float* v, void* pred_
   host_scalars(version, lr, beta1, beta2, eps, &hs);
   cudaError_t e = launch_sweep(W, g, m, v, pred_f, pred_b, n, nullptr, &hs, (float)s_f, (float)s_b, pred_bf16 != 0,
                                delta_form, true, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_err(nullptr, XP_ECUDA, cudaGetErrorString(e));
+  return XP_OK;
+}
+
+int xpipe_sgd_predict(float* W, const float* g, float* buf, float* m, float* v, void* pred_f, void* pred_b, int64_t n,
+                      float lr, float beta1, float beta2, float eps, float momentum, float weight_decay, int32_t s_f,
+                      int32_t s_b, int32_t pred_bf16, void* stream) {
+  if (!W || !g || !buf || !m || !v || n < 0) return set_err(nullptr, XP_EINVAL, "sgd_predict args");
+  if (((uintptr_t)W | (uintptr_t)g | (uintptr_t)buf | (uintptr_t)m | (uintptr_t)v) & 15)
+    return set_err(nullptr, XP_EINVAL, "alignment");
+  SweepScalars hs;
+  host_scalars(1, lr, beta1, beta2, eps, &hs);  // the paper form uses only the constant corrections
+  hs.mu = momentum;
+  hs.wd = weight_decay;
+  cudaError_t e = launch_sweep_sgd(W, g, buf, m, v, pred_f, pred_b, n, nullptr, &hs, (float)s_f, (float)s_b,
+                                   pred_bf16 != 0, (cudaStream_t)stream);
   if (e != cudaSuccess) return set_err(nullptr, XP_ECUDA, cudaGetErrorString(e));
   return XP_OK;
 }

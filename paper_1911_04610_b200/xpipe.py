@@ -18,7 +18,8 @@ PRECISION = {"fp32": 0, "bf16": 1}
 SCHEDULE = {"xpipe": 0, "gpipe": 1}
 PREDICT = {"paper": 0, "off": 1, "fixed": 2}
 DELTA = {"adam": 0, "paper": 1}
-STATE = {"param": 0, "m": 1, "v": 2, "pred_fwd": 3, "pred_bwd": 4, "grad": 5}
+STATE = {"param": 0, "m": 1, "v": 2, "pred_fwd": 3, "pred_bwd": 4, "grad": 5, "buf": 6}
+OPTIMIZER = {"adam": 0, "sgd": 1}
 XP_FLUSH, XP_DEVICE_PTRS, XP_ASYNC = 1, 2, 4
 
 
@@ -42,7 +43,8 @@ class Config(C.Structure):
                [("init_params", C.POINTER(C.POINTER(C.c_float))),
                 ("init_m", C.POINTER(C.POINTER(C.c_float))),
                 ("init_v", C.POINTER(C.POINTER(C.c_float))),
-                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", C.c_void_p)]
+                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", C.c_void_p),
+                ("optimizer", C.c_int32), ("momentum", C.c_float), ("weight_decay", C.c_float)]
 
 
 class TraceRec(C.Structure):
@@ -93,6 +95,8 @@ def lib():
         L.xpipe_last_error.argtypes = [vp]
         L.xpipe_last_error.restype = C.c_char_p
         L.xpipe_adam_predict.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, f32, f32, f32, f32, i32, i32, i32, i32, vp]
+        L.xpipe_sgd_predict.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f32, f32, i32, i32, i32,
+                                        vp]
         L.xpipe_gemm_bf16.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i64, vp]
         L.xpipe_conv2d_bf16.argtypes = [i32, C.POINTER(i32), vp, vp, vp, i32, vp, i64, vp]
         _lib = L
@@ -135,7 +139,8 @@ class XPipe:
     def __init__(self, layers, stages, micro_batches, mini_batch, lr, betas, eps, in_shape, classes, params=None,
                  precision="fp32", schedule="xpipe", predict="paper", s_fwd=0, s_bwd=0, delta="adam",
                  init_m=None, init_v=None, devices=None, snapshots=False, trace=False, graphs=False, profile=False,
-                 seed=1, watchdog_ms=0, torch_allocator=True, my_stage=None):
+                 seed=1, watchdog_ms=0, torch_allocator=True, my_stage=None, optimizer="adam", momentum=0.9,
+                 weight_decay=5e-4):
         self.h = None
         L = lib()
         self.layers = list(layers)
@@ -148,7 +153,9 @@ class XPipe:
                      precision=PRECISION[precision], schedule=SCHEDULE[schedule], predict=PREDICT[predict],
                      s_fwd=s_fwd, s_bwd=s_bwd, delta_form=DELTA[delta], snapshots=int(snapshots), trace=int(trace),
                      graphs=int(graphs), profile=int(profile), watchdog_ms=watchdog_ms,
-                     multi_process=int(my_stage is not None), my_stage=my_stage or 0)
+                     multi_process=int(my_stage is not None), my_stage=my_stage or 0,
+                     optimizer=OPTIMIZER[optimizer], momentum=momentum if optimizer == "sgd" else 0.0,
+                     weight_decay=weight_decay if optimizer == "sgd" else 0.0)
         if devices:
             cfg.n_devices = len(devices)
             for i, d in enumerate(devices):
@@ -298,6 +305,18 @@ def adam_predict(W, g, m, v, pf, pb, version, lr, betas, eps, s_f, s_b, pred_bf1
                                     _ptr(pb) if pb is not None else None, n, version, lr, betas[0], betas[1], eps,
                                     s_f, s_b, int(pred_bf16), DELTA[delta],
                                     C.c_void_p(stream) if stream else None))
+
+
+def sgd_predict(W, g, buf, m, v, pf, pb, lr, betas, eps, momentum, weight_decay, s_f, s_b, pred_bf16, stream=None):
+    """The f2 sweep (Momentum SGD + paper-literal prediction) on torch CUDA tensors, in place."""
+    n = W.numel()
+    for nm, t in (("W", W), ("g", g), ("buf", buf), ("m", m), ("v", v)):
+        _want(nm, t, ("float32",), n)
+    for nm, t in (("pf", pf), ("pb", pb)):
+        _want(nm, t, ("bfloat16",) if pred_bf16 else ("float32",), n)
+    _check(lib().xpipe_sgd_predict(_ptr(W), _ptr(g), _ptr(buf), _ptr(m), _ptr(v), _ptr(pf) if pf is not None else None,
+                                   _ptr(pb) if pb is not None else None, n, lr, betas[0], betas[1], eps, momentum,
+                                   weight_decay, s_f, s_b, int(pred_bf16), C.c_void_p(stream) if stream else None))
 
 
 def gemm_bf16(A, B, D, M, N, K, a_kmajor=True, b_kmajor=True, ldd=None, stream=None):

@@ -73,3 +73,16 @@ def test_no_oracle_reference_in_product_sources():
             if f.endswith((".py", ".cu", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "xoracle" not in txt and "liboracle" not in txt, f
+
+
+def test_sgd_optimizer_validation(so):
+    """XP_OPT_MOMENTUM_SGD (f2) needs the paper prediction form and a momentum in [0, 1):
+    XP_EINVAL before any device work otherwise."""
+    import synthetic as S
+    from paper_1911_04610_b200 import XPipe, XPipeError
+    L = S.mlp()
+    for kw in (dict(delta="adam"), dict(delta="paper", momentum=1.0), dict(delta="paper", weight_decay=-1.0)):
+        with pytest.raises(XPipeError) as e:
+            XPipe(L, 2, 4, 32, 1e-2, (0.9, 0.999), 1e-8, (784, 1, 1), 10, torch_allocator=False, optimizer="sgd",
+                  **kw)
+        assert e.value.code == -1

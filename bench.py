@@ -264,6 +264,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the embedded config-5 sweep measurement")
+    ap.add_argument("--optimizer", default="adam", choices=["adam", "sgd"],
+                    help="sgd: Momentum SGD (0.9, wd 5e-4) + the paper-literal prediction (SURVEY 8f f2)")
     ap.add_argument("--schedule", default="xpipe", choices=["xpipe", "gpipe"],
                     help="gpipe: synchronous GPipe with a flush per mini-batch (prediction off), same kernels")
     ap.add_argument("--no-graphs", action="store_true", help="enqueue every kernel from the host (no CUDA graphs)")
@@ -302,6 +304,9 @@ def main():
     # f1: the GPipe-flush schedule (prediction off) through the same kernels, for the paper's
     # XPipe/GPipe throughput comparison (Figs. 7-8)
     sched = dict(schedule="gpipe", predict="off") if args.schedule == "gpipe" else {}
+    # f2: the paper's Momentum-SGD training with the literal Eq. (3)/(4) prediction
+    if args.optimizer == "sgd":
+        sched.update(optimizer="sgd", delta="paper", momentum=0.9, weight_decay=5e-4)
     def make_model(profile):
         if mp_mode:
             # one process per GPU: this rank owns stage `rank`; rings/flags are CUDA IPC-mapped
@@ -452,7 +457,7 @@ def main():
                        "processes": "one per GPU (CUDA IPC rings)" if ws > 1 else "one process",
                        "global_batch": N, "stages": K, "micro_batches": T, "minibatches_per_step": M,
                        "parallelism": "pipeline K=%d (%s)" % (K, "GPipe-flush" if args.schedule == "gpipe" else "XPipe"),
-                       "schedule": args.schedule,
+                       "schedule": args.schedule, "optimizer": args.optimizer,
                        "l2": "working set > L2: optimizer state 16 B/param x %.1fM params = %d MB (126 MB L2)"
                              % (nparams / 1e6, nparams * 16 // 10**6)},
             "e2e": e2e, "gpu_launches": result["launches"], "graph_replays": result.get("replays"),

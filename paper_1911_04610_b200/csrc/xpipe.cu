@@ -386,7 +386,10 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     else
       XP_TRY(check_launch(c, launch_sweep(s.W, s.g, s.m, s.v, s.pf[nv & 1], s.pb, s.plan.P, s.ds, nullptr, sf, sbf,
                                           bf16, c->cfg.delta_form, true, s.stream), "sweep"));
-    XP_TRY(prof_end(c, s, XP_PROF_SWEEP, (double)s.plan.P * (bf16 ? 32.0 : 36.0)));
+    // algorithmic bytes per parameter: Adam 16 B read + 12 B written + 2 predictions; the f2
+    // Momentum-SGD sweep also reads and writes the velocity (+8 B)
+    const double sgd_extra = c->cfg.optimizer == XP_OPT_MOMENTUM_SGD ? 8.0 : 0.0;
+    XP_TRY(prof_end(c, s, XP_PROF_SWEEP, (double)s.plan.P * ((bf16 ? 32.0 : 36.0) + sgd_extra)));
     s.host_ver = nv;
     if (c->cfg.snapshots) {
       if (s.snap_pool.empty()) return set_err(c, XP_ESCHED, "snapshot pool (internal)");

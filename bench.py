@@ -98,19 +98,25 @@ WORKLOAD_TEXT = {"mlp": "MLP 784-256-256-256-10 (configs[0])",
                  "inception": "Inception-V3 on synthetic Tiny-ImageNet 64x64 (BASELINE configs[3])"}
 
 
-def workload_model(name, K=1):
+def workload_model(name, K=1, image=64, micro=0, T=0):
     """(layers, input shape, classes, input kind, mini-batch N, micro-batches T, precision) of a
-    BASELINE config; DAG models get explicit unit-based stages for K (R17)."""
+    BASELINE config; DAG models get explicit unit-based stages for K (R17).  image=224: the
+    paper's upscaled Tiny-ImageNet (P:161, SURVEY f4) with the unmodified Inception stem;
+    micro / T override the micro-batch size and count (50*T on 2 GPUs, 100*T on 4)."""
     import synthetic as S
     from synthetic.models import resnet101, inception_v3, assign_stages
     if name == "mlp":
         return S.mlp(), (784, 1, 1), 10, "mnist", 32, 4, "fp32"
-    if name == "resnet101":
-        L, units = resnet101(classes=200)
-        return assign_stages(L, units, K), (3, 64, 64), 200, "imagenet", 256, 8, "bf16"
-    if name == "inception":
-        L, units = inception_v3(classes=200)
-        return assign_stages(L, units, K), (3, 64, 64), 200, "imagenet", 128, 4, "bf16"
+    if name in ("resnet101", "inception"):
+        if name == "resnet101":
+            L, units = resnet101(classes=200)
+            T0, n0 = 8, 32
+        else:
+            L, units = inception_v3(classes=200, stem_pad=image < 75)
+            T0, n0 = 4, 32
+        T = T or T0
+        n = micro or n0
+        return assign_stages(L, units, K), (3, image, image), 200, "imagenet", n * T, T, "bf16"
     return S.vgg16_cifar(), (3, 32, 32), 10, "cifar", 128, 4, "bf16"
 
 
@@ -264,6 +270,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the embedded config-5 sweep measurement")
+    ap.add_argument("--recompute", action="store_true", help="activation recomputation (P:167, SURVEY f3)")
+    ap.add_argument("--image", type=int, default=64, help="Tiny-ImageNet side for resnet101/inception (224: f4)")
+    ap.add_argument("--micro-batch", type=int, default=0, help="micro-batch size override (resnet101/inception)")
+    ap.add_argument("--micro-batches", type=int, default=0, help="T override (resnet101/inception)")
     ap.add_argument("--optimizer", default="adam", choices=["adam", "sgd"],
                     help="sgd: Momentum SGD (0.9, wd 5e-4) + the paper-literal prediction (SURVEY 8f f2)")
     ap.add_argument("--schedule", default="xpipe", choices=["xpipe", "gpipe"],
@@ -296,7 +306,8 @@ def main():
     # each BASELINE config names its stage count (VGG-16 4, ResNet-101 8, Inception-V3 4, MLP 2):
     # on one GPU all stages share the device (one stream each); on N GPUs one stage per GPU
     K = ws if mp_mode else (args.stages or (DEFAULT_STAGES[args.workload] if args.gpus == 1 else args.gpus))
-    L, shape, classes, kind, N, T, prec = workload_model(args.workload, K)
+    L, shape, classes, kind, N, T, prec = workload_model(args.workload, K, args.image, args.micro_batch,
+                                                         args.micro_batches)
     dev = local if mp_mode else 0
     P = S.make_params(L, 1)
     from synthetic.models import param_count
@@ -307,6 +318,8 @@ def main():
     # f2: the paper's Momentum-SGD training with the literal Eq. (3)/(4) prediction
     if args.optimizer == "sgd":
         sched.update(optimizer="sgd", delta="paper", momentum=0.9, weight_decay=5e-4)
+    if args.recompute:  # f3: activation recomputation in every backward
+        sched.update(recompute=True)
     def make_model(profile):
         if mp_mode:
             # one process per GPU: this rank owns stage `rank`; rings/flags are CUDA IPC-mapped
@@ -457,7 +470,8 @@ def main():
                        "processes": "one per GPU (CUDA IPC rings)" if ws > 1 else "one process",
                        "global_batch": N, "stages": K, "micro_batches": T, "minibatches_per_step": M,
                        "parallelism": "pipeline K=%d (%s)" % (K, "GPipe-flush" if args.schedule == "gpipe" else "XPipe"),
-                       "schedule": args.schedule, "optimizer": args.optimizer,
+                       "schedule": args.schedule, "optimizer": args.optimizer, "recompute": args.recompute,
+                       "image": list(shape),
                        "l2": "working set > L2: optimizer state 16 B/param x %.1fM params = %d MB (126 MB L2)"
                              % (nparams / 1e6, nparams * 16 // 10**6)},
             "e2e": e2e, "gpu_launches": result["launches"], "graph_replays": result.get("replays"),

@@ -120,6 +120,10 @@ typedef struct {
   void* alloc_user;
   int32_t optimizer;                  /* XP_OPT_ADAM (default) | XP_OPT_MOMENTUM_SGD */
   float momentum, weight_decay;       /* XP_OPT_MOMENTUM_SGD: in [0,1) and >= 0 (paper: 0.9, 5e-4) */
+  int32_t recompute;                  /* 1 = activation recomputation: every
+                                         backward B(u) first re-runs the stage forward under W_hat_b
+                                         from the stashed stage input (the last stage also its loss
+                                         gradient) and differentiates that forward */
 } xpipe_config;
 
 /* one device-trace record (K12): op 0 = forward, 1 = backward, 2 = update.  version is the

@@ -45,7 +45,8 @@ class _Config(C.Structure):
                [("init_params", C.POINTER(C.POINTER(C.c_double))),
                 ("init_m", C.POINTER(C.POINTER(C.c_double))),
                 ("init_v", C.POINTER(C.POINTER(C.c_double))),
-                ("optimizer", C.c_int32), ("momentum", C.c_double), ("weight_decay", C.c_double)]
+                ("optimizer", C.c_int32), ("momentum", C.c_double), ("weight_decay", C.c_double),
+                ("recompute", C.c_int32)]
 
 
 class _Trace(C.Structure):
@@ -124,7 +125,8 @@ class Oracle:
 
     def __init__(self, layers, stages, micro_batches, mini_batch, lr, betas, eps, in_shape, classes, params,
                  mode="fp64", schedule="xpipe", predict="paper", s_fwd=0, s_bwd=0, delta="adam",
-                 snapshots=False, init_m=None, init_v=None, optimizer="adam", momentum=0.9, weight_decay=5e-4):
+                 snapshots=False, init_m=None, init_v=None, optimizer="adam", momentum=0.9, weight_decay=5e-4,
+                 recompute=False):
         self.layers = list(layers)
         arr = (_Layer * len(self.layers))()
         for i, l in enumerate(self.layers):
@@ -142,7 +144,7 @@ class Oracle:
                       schedule=SCHEDULES[schedule], predict=PREDICT[predict], s_fwd=s_fwd, s_bwd=s_bwd,
                       delta_form=DELTA[delta], snapshots=int(snapshots), init_params=pp,
                       optimizer=OPTIMIZERS[optimizer], momentum=float(np.float32(momentum)),
-                      weight_decay=float(np.float32(weight_decay)))
+                      weight_decay=float(np.float32(weight_decay)), recompute=int(recompute))
         for name, src in (("init_m", init_m), ("init_v", init_v)):
             if src is not None:
                 tab = (C.POINTER(C.c_double) * stages)()

@@ -681,6 +681,7 @@ struct xo_ctx {
   int K = 1, T = 1, N = 1, n = 1;
   int schedule = XO_SCHED_XPIPE, predict = XO_PRED_PAPER, s_fwd = 0, s_bwd = 0;
   bool snapshots = false;
+  bool recompute = false;                /* f3: backward re-runs the stage forward under W_hat_b */
   std::vector<Stage> S;
   std::map<int64_t, Vec> inputs;         /* micro-batch u -> input [n, C, H, W] */
   std::map<int64_t, std::vector<int32_t>> labels;
@@ -915,7 +916,20 @@ int try_step(xo_ctx& c, int k) {
       if (k + 1 < c.K) { dout = std::move(st.inbox_grad[u]); st.inbox_grad.erase(u); }
       else { dout = std::move(st.dlogits[u]); st.dlogits.erase(u); }
       Vec din, gW;
-      stage_backward(c, st, st.cb.Wp, c.n, st.stash[u], dout, din, gW);
+      if (c.recompute) {
+        /* f3: activation recomputation -- the stage forward again, now under W_hat_b,
+           from the stashed stage input; the backward differentiates this forward (an exact
+           VJP of the stage at W_hat_b), the last stage from its recomputed loss gradient */
+        std::vector<Vec> acts;
+        stage_forward(c, st, st.cb.Wp, c.n, st.stash[u][0], acts);
+        if (k + 1 == c.K) {
+          double ls;
+          xent(c.M, c.n, c.M.classes, c.N, acts.back(), c.labels.at(u).data(), dout, &ls);
+        }
+        stage_backward(c, st, st.cb.Wp, c.n, acts, dout, din, gW);
+      } else {
+        stage_backward(c, st, st.cb.Wp, c.n, st.stash[u], dout, din, gW);
+      }
       st.stash.erase(u);
       if (j == 1) st.g = gW;
       else for (size_t i = 0; i < gW.size(); ++i) st.g[i] = c.M.add(st.g[i], gW[i]);
@@ -986,6 +1000,7 @@ int xo_init(const xo_layer* layers, int32_t n_layers, int32_t stages, int32_t T,
     return fail(E_INVAL, "Momentum SGD needs the paper prediction form, momentum in [0,1), weight decay >= 0");
   c->schedule = cfg->schedule; c->predict = cfg->predict; c->s_fwd = cfg->s_fwd; c->s_bwd = cfg->s_bwd;
   c->snapshots = cfg->snapshots != 0;
+  c->recompute = cfg->recompute != 0;
   Model& M = c->M;
   M.mode = cfg->mode;
   M.input = Shape{cfg->in_c, cfg->in_h, cfg->in_w};

@@ -63,6 +63,9 @@ typedef struct {
   /* XO_OPT_SGD (requires delta_form = XO_DELTA_PAPER): W <- W - lr*buf, buf <- mu*buf + (g + wd*W) */
   int32_t optimizer;
   double momentum, weight_decay;
+  /* f3: the backward re-runs the stage forward under W_hat_b from the stashed stage
+     input (the last stage also recomputes its loss gradient) and differentiates that */
+  int32_t recompute;
 } xo_config;
 
 typedef struct { int32_t stage, op /*0=F 1=B 2=U*/, t, j, version, s, bellwether; } xo_trace_rec;

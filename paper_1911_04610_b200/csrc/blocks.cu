@@ -210,7 +210,7 @@ int op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot, int64_
   const Op& O = s.plan.ops[o];
   if (O.kind == OP_XENT) {
     const int32_t* y = c->y_dev + (u - c->call_first) * c->n;
-    float* loss = c->loss_dev + (u - c->call_first);
+    float* loss = c->recompute_pass ? c->loss_scratch : c->loss_dev + (u - c->call_first);
     return check_launch(c, launch_xent_f32((const float*)s.act[O.in0][slot], y, s.dz[slot], loss, c->n, O.sin0.c,
                                            (float)(1.0 / (double)c->N), s.stream), "xent");
   }

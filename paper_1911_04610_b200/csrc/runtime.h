@@ -132,6 +132,8 @@ struct xpipe_ctx {
   std::map<std::string, GraphRec> graphs;
   int64_t graph_replays = 0;
   bool capturing = false;
+  bool recompute_pass = false;          // f3: op_forward is re-running a stage forward inside B(u)
+  float* loss_scratch = nullptr;        // the recomputed forward's loss (the reported loss is F(u)'s)
   std::vector<int64_t> cap_fwd0, cap_bwd0;  // enqueue counters when the capture started
   std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)
 };

@@ -335,6 +335,16 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
   XP_TRY(trace_slot(c, s, &rec));
   if (rec) XP_TRY(check_launch(c, launch_trace_begin(s.ds, rec, k, 1, (int)t, (int)j, sb, bw, s.stream), "trace"));
   if (bw) s.host_bver = s.host_ver;
+  if (c->cfg.recompute) {
+    // f3: re-run the stage forward for this micro-batch under W_hat_b from its stashed
+    // input (ring slot), overwriting the slot's activations, statistics and pool winners (and
+    // on the last stage dz) -- the backward below then differentiates this forward exactly
+    c->recompute_pass = true;
+    int r = XP_OK;
+    for (size_t o = 0; o < s.plan.ops.size() && r == XP_OK; ++o) r = op_forward(c, s, (int)o, s.pb, slot, u);
+    c->recompute_pass = false;
+    XP_TRY(r);
+  }
   const bool accumulate = (j != 1);
   s.gsel = 0;
   s.gdone_valid[0] = s.gdone_valid[1] = false;
@@ -625,6 +635,10 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
 }
 
 int ensure_call_buffers(xpipe_ctx* c, int64_t M) {
+  if (c->cfg.recompute && !c->loss_scratch && owned(c->S[c->K - 1])) {
+    c->loss_scratch = (float*)dmalloc(c, 256, c->S[c->K - 1].dev);
+    if (!c->loss_scratch) return set_err(c, XP_ENOMEM, "loss scratch");
+  }
   const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
   const int64_t xs = M * c->N * per, ys = M * c->N, ls = M * c->T;
   if (xs > c->x_cap || ys > c->y_cap || ls > c->loss_cap) {

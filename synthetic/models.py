@@ -191,19 +191,21 @@ def resnet101(classes=200, in_c=3, layers=(3, 4, 23, 3)):
     return B.L, B.units
 
 
-def inception_v3(classes=200, in_c=3):
+def inception_v3(classes=200, in_c=3, stem_pad=True):
     """C4: torchvision Inception-V3 with aux_logits off and no dropout, padding 1 on the
     unpadded stem convs Conv2d_1a, 2a, 4a so 64x64 inputs survive to Mixed_7 (R14).
+    stem_pad=False: the unmodified torchvision stem, for the paper's 224x224 inputs (f4).
     BasicConv2d = conv (no bias) + BN(eps=1e-3) + ReLU.  Units: stem conv / module / head."""
     B = Builder()
     e = 1e-3
+    sp = 1 if stem_pad else 0
     cb = lambda src, i, o, k, s=1, p=0: B.conv_bn(src, i, o, k, s, p, True, e)
-    x = cb(-1, in_c, 32, 3, 2, 1)                       # Conv2d_1a (padded, R14)
-    B.next_unit(); x = cb(x, 32, 32, 3, 1, 1)           # Conv2d_2a (padded)
+    x = cb(-1, in_c, 32, 3, 2, sp)                      # Conv2d_1a (padded at 64x64, R14)
+    B.next_unit(); x = cb(x, 32, 32, 3, 1, sp)          # Conv2d_2a
     B.next_unit(); x = cb(x, 32, 64, 3, 1, 1)           # Conv2d_2b
     x = B.add(maxpool(3, 2), src0=x)
     B.next_unit(); x = cb(x, 64, 80, 1)                 # Conv2d_3b
-    B.next_unit(); x = cb(x, 80, 192, 3, 1, 1)          # Conv2d_4a (padded)
+    B.next_unit(); x = cb(x, 80, 192, 3, 1, sp)         # Conv2d_4a
     x = B.add(maxpool(3, 2), src0=x)
 
     def incA(x, cin, pf):

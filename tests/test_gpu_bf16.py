@@ -135,3 +135,18 @@ def test_inception_v3_bf16(oracle_mod):
     L = assign_stages(L, units, 2)
     g, o, P, lg, lo = run_bf16(oracle_mod, L, (3, 64, 64), 2, 2, 16, 3, kind="imagenet")
     check(g, o, L, 2, 3)
+
+
+def test_paper_224_shapes_bf16(oracle_mod):
+    """f4: the paper's Tiny-ImageNet upscaled to 224x224 -- the ResNet stem (7x7 s2
+    conv, 3x3 s2 max-pool) and one bottleneck per stage group at 224^2 (112^2 stem output, 4 MB
+    bf16 per image), 2 stages; and the full Inception-V3 with its unmodified torchvision stem."""
+    from synthetic.models import resnet101, inception_v3, assign_stages
+    L, units = resnet101(classes=10, layers=(1, 1, 1, 1))
+    L = assign_stages(L, units, 2)
+    g, o, P, lg, lo = run_bf16(oracle_mod, L, (3, 224, 224), 2, 2, 4, 3, kind="imagenet")
+    check(g, o, L, 2, 3)
+    L, units = inception_v3(classes=10, stem_pad=False)
+    L = assign_stages(L, units, 2)
+    g, o, P, lg, lo = run_bf16(oracle_mod, L, (3, 224, 224), 2, 1, 2, 2, kind="imagenet")
+    check(g, o, L, 2, 2)

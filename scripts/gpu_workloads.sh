@@ -15,3 +15,9 @@ b inception_K4 --workload inception
 b inception_gpipe_K4 --workload inception --no-cpu-baseline --schedule gpipe
 b inception_K8 --workload inception --no-cpu-baseline --stages 8
 b mlp_K2 --workload mlp
+b vgg_sgd_K4 --no-cpu-baseline --optimizer sgd
+b vgg_recompute_K4 --no-cpu-baseline --recompute
+b resnet224_K2_T2 --workload resnet101 --no-cpu-baseline --stages 2 --image 224 --micro-batch 50 --micro-batches 2 --minibatches 2 --steps 5
+b resnet224_gpipe_K2_T2 --workload resnet101 --no-cpu-baseline --stages 2 --image 224 --micro-batch 50 --micro-batches 2 --minibatches 2 --steps 5 --schedule gpipe
+b inception224_K4_T4 --workload inception --no-cpu-baseline --stages 4 --image 224 --micro-batch 100 --micro-batches 4 --minibatches 2 --steps 5
+b inception224_gpipe_K4_T4 --workload inception --no-cpu-baseline --stages 4 --image 224 --micro-batch 100 --micro-batches 4 --minibatches 2 --steps 5 --schedule gpipe

@@ -111,6 +111,14 @@ __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int
       "l"((uint64_t)map), "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_5d(uint32_t dst, const CUtensorMap* map, int x0, int x1, int x2, int x3, int x4,
+                                       uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"(x4), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int x0, int x1, int x2, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
@@ -512,7 +520,7 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
     for (int j = 0; j < nunits; ++j) {
       const Work w = work_of<BN>(a, j, mt);
       int tn = 0, tp = 0, tq = 0;  // pixel origin of the tile's rows (fprop / dgrad)
-      if (MODE != GEMM_WGRAD) {
+      if (MODE == GEMM_FPROP || MODE == GEMM_DGRAD) {
         tn = w.m0 / (a.gq * a.gp);
         const int rem = w.m0 - tn * a.gq * a.gp;
         tp = rem / a.gq; tq = rem - tp * a.gq;
@@ -521,7 +529,21 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
         mbar_wait(empty0 + 8 * ring.slot, ring.phase ^ 1u);
         const uint32_t sa = base + ring.slot * STAGE, sb = sa + A_BYTES, full = full0 + 8 * ring.slot;
         const int k0 = (w.kb0 + i) * BK;
-        if (MODE == GEMM_FPROP) {
+        if (MODE == GEMM_PLAIN) {
+          mbar_expect_tx(full, STAGE);
+          if (A_MN) {
+#pragma unroll
+            for (int q = 0; q < BM / 64; ++q) tma_2d(sa + q * (BK * 128), tmA, w.m0 + 64 * q, k0, full);
+          } else {
+            tma_2d(sa, tmA, k0, w.m0, full);
+          }
+          if (a.b_tma == 1) {
+            tma_2d(sb, tmB, k0, w.n0, full);
+          } else {
+#pragma unroll
+            for (int q = 0; q < BN / 64; ++q) tma_2d(sb + q * (BK * 128), tmB, w.n0 + 64 * q, k0, full);
+          }
+        } else if (MODE == GEMM_FPROP) {
           mbar_expect_tx(full, STAGE);
           const int tap = k0 / a.g.C, c0 = k0 - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
           tma_4d(sa, tmA, c0, tq + ss - a.g.pw, tp + r - a.g.ph, tn, full);
@@ -534,11 +556,19 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
           for (int q = 0; q < BN / 64; ++q) tma_3d(sb + q * (BK * 128), tmB, w.n0 + 64 * q, tap, c0, full);
         } else if (MODE == GEMM_WGRAD) {
           const int pn = k0 / (a.gq * a.gp), rem = k0 - pn * a.gq * a.gp, pp = rem / a.gq, pq = rem - pp * a.gq;
-          const int nch = min(2, (a.M - w.m0 + 63) / 64);
-          mbar_expect_tx(full, (uint32_t)(nch * BK * 128 + BN * BK * 2));
-          for (int q = 0; q < nch; ++q) {
-            const int mm = w.m0 + 64 * q, tap = mm / a.g.C, c0 = mm - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
-            tma_4d(sa + q * (BK * 128), tmA, c0, pq + ss - a.g.pw, pp + r - a.g.ph, pn, full);
+          if (a.a_tma == 2) {
+            // C % 128 == 0: both 64-channel halves of the tile's 128 rows belong to one tap --
+            // one 5-D box {64 ch, pixel box, 2 channel blocks} lands them as the two MN blocks
+            mbar_expect_tx(full, (uint32_t)(2 * BK * 128 + BN * BK * 2));
+            const int tap = w.m0 / a.g.C, c0 = w.m0 - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
+            tma_5d(sa, tmA, 0, pq + ss - a.g.pw, pp + r - a.g.ph, pn, c0 / 64, full);
+          } else {
+            const int nch = (a.dev_flags & 1) ? 1 : min(2, (a.M - w.m0 + 63) / 64);  // dev 1: timing probe only
+            mbar_expect_tx(full, (uint32_t)(nch * BK * 128 + BN * BK * 2));
+            for (int q = 0; q < nch; ++q) {
+              const int mm = w.m0 + 64 * q, tap = mm / a.g.C, c0 = mm - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
+              tma_4d(sa + q * (BK * 128), tmA, c0, pq + ss - a.g.pw, pp + r - a.g.ph, pn, full);
+            }
           }
 #pragma unroll
           for (int q = 0; q < BN / 64; ++q) tma_2d(sb + q * (BK * 128), tmB, w.n0 + 64 * q, k0, full);
@@ -1009,10 +1039,24 @@ bool pixel_box(int T, int Q, int P, uint32_t* box) {
 }
 
 // the A-operand map of a stride-1 conv GEMM (sets a.a_tma; needs a.b_tma)
-template <int MODE>
+__host__ bool plain_tma() { static const bool v = getenv_flag("XPIPE_PLAIN_TMA"); return v; }
+template <int MODE, bool A_MN>
 void setup_a_tma(GemmArgs& a, CUtensorMap* m) {
   a.a_tma = 0;
-  if (MODE == GEMM_PLAIN || !a.b_tma || a.g.sh != 1 || a.g.sw != 1) return;
+  if (MODE == GEMM_PLAIN) {  // development: both operands of the unit GEMM by TMA
+    if (!plain_tma() || !a.b_tma) return;
+    if (A_MN) {  // A [K][M]
+      const uint64_t dims[2] = {(uint64_t)a.M, (uint64_t)a.K}, str[1] = {(uint64_t)a.lda * 2};
+      const uint32_t box[2] = {64, 64};
+      if (make_map(m, a.A, 2, dims, str, box)) a.a_tma = 1;
+    } else {     // A [M][K]
+      const uint64_t dims[2] = {(uint64_t)a.K, (uint64_t)a.M}, str[1] = {(uint64_t)a.lda * 2};
+      const uint32_t box[2] = {64, (uint32_t)BM};
+      if (make_map(m, a.A, 2, dims, str, box)) a.a_tma = 1;
+    }
+    return;
+  }
+  if (!a.b_tma || a.g.sh != 1 || a.g.sw != 1) return;
   const ConvGeo& g = a.g;
   uint32_t pb[3];
   uint64_t dims[4], str[3];
@@ -1028,6 +1072,14 @@ void setup_a_tma(GemmArgs& a, CUtensorMap* m) {
     dims[0] = g.Co; dims[1] = g.Q; dims[2] = g.P; dims[3] = g.Nimg;
     str[0] = (uint64_t)g.Co * 2; str[1] = (uint64_t)g.Q * g.Co * 2; str[2] = (uint64_t)g.P * g.Q * g.Co * 2;
     a.gq = g.W; a.gp = g.H;
+  }
+  static const bool no_tma5 = getenv_flag("XPIPE_NO_TMA5");
+  if (MODE == GEMM_WGRAD && g.C % 128 == 0 && !no_tma5) {
+    // {64 ch, W, H, N, C/64 channel blocks}: one box per k-block for the tile's two MN blocks
+    const uint64_t d5[5] = {64, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.Nimg, (uint64_t)(g.C / 64)};
+    const uint64_t s5[4] = {str[0], str[1], str[2], 128};
+    const uint32_t b5[5] = {64, pb[0], pb[1], pb[2], 2};
+    if (make_map(m, a.A, 5, d5, s5, b5)) { a.a_tma = 2; return; }
   }
   const uint32_t box[4] = {64, pb[0], pb[1], pb[2]};
   if (make_map(m, a.A, 4, dims, str, box)) a.a_tma = 1;
@@ -1053,24 +1105,28 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   }
   const int mt = (a.M + BM - 1) / BM, nt = (a.N + BN - 1) / BN;
   GemmArgs args = a;
-  dim3 grid;
-  if (splits <= 1) {
-    grid = dim3(std::max(1, std::min(mt * nt, num_sms())), 1, 1);
-    args.stages = std::max(4, std::min(DEEP, persist_stages()));  // >= LAG+1 (cp.async ring)
-  } else {
-    grid = dim3(mt, nt, splits);
-    args.stages = std::max(4, std::min(DEEP, split_stages()));  // small CTAs: clusters of up to 8 place easily
-  }
-  const int SMEM = args.stages * STAGE + 1024 + 1024;  // ring + alignment + barriers/BN exchange
+  static const int dev_flags = getenv_int("XPIPE_GEMM_DEV", 0);
   args.dbg = gemm_dbg_buffer();
+  args.dev_flags = dev_flags;
   CUtensorMap tmA, tmB;
   memset(&tmA, 0, sizeof tmA);
   memset(&tmB, 0, sizeof tmB);
   args.a_tma = args.b_tma = 0;
   if (!no_tma()) {
     setup_b_tma<MODE, BN, B_MN>(args, &tmB);
-    if (!no_tma_a()) setup_a_tma<MODE>(args, &tmA);
+    if (!no_tma_a()) setup_a_tma<MODE, A_MN>(args, &tmA);
   }
+  // ring depth: the cp.async gather needs >= LAG+1 = 4 stages; an all-TMA ring may be shallower
+  // so that wide tiles still leave room for a second CTA on the SM
+  static const int st128 = getenv_int("XPIPE_PSTAGES_128", 4), st256 = getenv_int("XPIPE_PSTAGES_256", 4);
+  int want = splits <= 1 ? persist_stages() : split_stages();
+  if (splits <= 1 && BN == 128) want = st128;
+  if (splits <= 1 && BN == 256) want = st256;
+  args.stages = std::max(args.a_tma ? 2 : 4, std::min(DEEP, want));
+  dim3 grid;
+  if (splits <= 1) grid = dim3(std::max(1, std::min(mt * nt, num_sms())), 1, 1);
+  else grid = dim3(mt, nt, splits);
+  const int SMEM = args.stages * STAGE + 1024 + 1024;  // ring + alignment + barriers/BN exchange
   if (splits <= 1) {
     launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);
     return cudaGetLastError();

@@ -54,6 +54,7 @@ struct GemmArgs {
   // bn_part[mtile][1][co] = sum of squared deviations (rows < M only), or null
   float* bn_part;
   unsigned long long* dbg;  // development timing probe (XPIPE_GEMM_DBG), else null
+  int dev_flags;            // development experiments (XPIPE_GEMM_DEV), 0 in production
 };
 
 // plain GEMM for unit parity: D[M][N] fp32 (ldd) = A(m,k) B(n,k)

@@ -290,8 +290,15 @@ def main():
     peaks, peak_kind = load_peaks()
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("XPIPE_BENCH_ONE_GPU"):
+            # development dry run of the multi-process path on a one-GPU box: every rank on
+            # device 0 (CUDA IPC within one device), gloo for the host plumbing
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.workload == "sweep":
         line = run_sweep(args, peaks, peak_kind)
         if rank == 0:

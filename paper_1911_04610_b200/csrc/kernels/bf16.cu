@@ -484,8 +484,12 @@ __global__ void linear_wgrad_bf16_kernel(const void* __restrict__ dy, const bf16
 }
 
 int grid1d(int64_t n, int threads = 256) {
+  static const int cap = [] {  // development knob: CTA cap of the elementwise kernels
+    const char* e = getenv("XPIPE_EW_CTAS");
+    return (e && *e) ? std::max(1, atoi(e)) : 148 * 16;
+  }();
   int64_t g = (n + threads - 1) / threads;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, cap));
 }
 
 }  // namespace

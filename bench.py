@@ -271,6 +271,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the embedded config-5 sweep measurement")
     ap.add_argument("--recompute", action="store_true", help="activation recomputation (P:167, SURVEY f3)")
+    ap.add_argument("--partition", default="layer-count", choices=["layer-count", "balanced"],
+                    help="stage split: the paper's layer-count rule (R17) or cost-balanced (SURVEY 8e)")
     ap.add_argument("--image", type=int, default=64, help="Tiny-ImageNet side for resnet101/inception (224: f4)")
     ap.add_argument("--micro-batch", type=int, default=0, help="micro-batch size override (resnet101/inception)")
     ap.add_argument("--micro-batches", type=int, default=0, help="T override (resnet101/inception)")
@@ -315,6 +317,16 @@ def main():
     K = ws if mp_mode else (args.stages or (DEFAULT_STAGES[args.workload] if args.gpus == 1 else args.gpus))
     L, shape, classes, kind, N, T, prec = workload_model(args.workload, K, args.image, args.micro_batch,
                                                          args.micro_batches)
+    if args.partition == "balanced" and K > 1:
+        # contiguous partition minimising the largest stage's forward MACs
+        from synthetic.models import chain_units, unit_macs, balanced_stages
+        if args.workload in ("resnet101", "inception"):
+            from synthetic.models import resnet101, inception_v3
+            units = (resnet101(classes=200)[1] if args.workload == "resnet101" else
+                     inception_v3(classes=200, stem_pad=args.image < 75)[1])
+        else:
+            units = chain_units(L)
+        L = balanced_stages(L, units, unit_macs(L, units, shape), K)
     dev = local if mp_mode else 0
     P = S.make_params(L, 1)
     from synthetic.models import param_count
@@ -478,6 +490,7 @@ def main():
                        "global_batch": N, "stages": K, "micro_batches": T, "minibatches_per_step": M,
                        "parallelism": "pipeline K=%d (%s)" % (K, "GPipe-flush" if args.schedule == "gpipe" else "XPipe"),
                        "schedule": args.schedule, "optimizer": args.optimizer, "recompute": args.recompute,
+                       "partition": args.partition,
                        "image": list(shape),
                        "l2": "working set > L2: optimizer state 16 B/param x %.1fM params = %d MB (126 MB L2)"
                              % (nparams / 1e6, nparams * 16 // 10**6)},

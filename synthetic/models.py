@@ -279,6 +279,60 @@ def assign_stages(layers, units, K):
     return [l.with_stage(st[units[i]]) for i, l in enumerate(layers)]
 
 
+def chain_units(layers):
+    """Partition units of a chain model (R17): a unit begins at every Linear / Conv2d."""
+    units, u = [], -1
+    for l in layers:
+        if l.kind in (LINEAR, CONV2D) or u < 0:
+            u += 1
+        units.append(u)
+    return units
+
+
+def unit_macs(layers, units, in_shape):
+    """Forward multiply-accumulates per sample of every unit (a cost model for partitioning;
+    no arithmetic of the method)."""
+    shapes = infer_shapes(layers, in_shape)
+    cost = [0.0] * (max(units) + 1)
+    for i, l in enumerate(layers):
+        if l.kind == LINEAR:
+            cost[units[i]] += l.in_c * l.out_c
+        elif l.kind == CONV2D:
+            c, h, w = shapes[i]
+            cost[units[i]] += c * h * w * l.in_c * l.kh * l.kw
+    return cost
+
+
+def balanced_stages(layers, units, cost, K):
+    """Contiguous partition of the units into K stages minimising the largest stage cost
+    (SURVEY 8e "cost-balanced split"; exact search over cut positions by dynamic programming),
+    written as explicit stage ids."""
+    n = len(cost)
+    pre = [0.0]
+    for c in cost:
+        pre.append(pre[-1] + c)
+    INF = float("inf")
+    best = [[INF] * (n + 1) for _ in range(K + 1)]
+    cut = [[0] * (n + 1) for _ in range(K + 1)]
+    best[0][0] = 0.0
+    for k in range(1, K + 1):
+        for j in range(k, n + 1):
+            for i in range(k - 1, j):
+                v = max(best[k - 1][i], pre[j] - pre[i])
+                if v < best[k][j]:
+                    best[k][j], cut[k][j] = v, i
+    bounds, j = [], n
+    for k in range(K, 0, -1):
+        bounds.append((cut[k][j], j))
+        j = cut[k][j]
+    bounds.reverse()
+    stage_of_unit = [0] * n
+    for k, (a, b) in enumerate(bounds):
+        for u in range(a, b):
+            stage_of_unit[u] = k
+    return [l.with_stage(stage_of_unit[units[i]]) for i, l in enumerate(layers)]
+
+
 def param_count(layers, in_shape):
     shapes = infer_shapes(layers, in_shape)
     n = 0

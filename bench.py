@@ -191,7 +191,11 @@ def run_reference(args):
         o.step(x, y, 1, flush=True)
     el = time.perf_counter() - t0
     v = args.steps * n / el
-    cfg = {"workload": "%s (oracle sample: one %d-sample micro-batch per step, K=1)" % (args.workload, n)}
+    K = args.stages or (DEFAULT_STAGES[args.workload] if args.gpus == 1 else args.gpus)
+    cfg = {"workload": "%s, K=%d stages, mini-batch %d, T=%d micro-batches" % (WORKLOAD_TEXT[args.workload], K, N, T),
+           "global_batch": N, "stages": K, "micro_batches": T,
+           "sample": "oracle (bf16 emulation, fp64 accumulation): one %d-sample micro-batch fwd+bwd+update per "
+                     "step; the per-sample work equals the K-stage pipeline's" % n}
     line = {"impl": "reference", "metric": METRICS.get(args.workload, METRIC), "value": v, "unit": "samples/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1000 / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",

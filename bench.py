@@ -351,9 +351,11 @@ def main():
                       profile=profile, watchdog_ms=300000, my_stage=rank, **sched)
             connect_pipeline(m, dist.new_group(backend="gloo"))
         else:
+            # the profiled pass runs every stage on one stream (serialize): each launch then runs
+            # alone, so its event-timed duration is the kernel's own (as in ncu's launch list)
             m = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
                       devices=list(range(args.gpus)), profile=profile, watchdog_ms=300000,
-                      graphs=not args.no_graphs, **sched)
+                      graphs=not args.no_graphs, serialize=profile and args.gpus == 1, **sched)
         return m
 
     x, y = S.make_inputs(M * N, shape, classes, 1, kind=kind)
@@ -459,9 +461,9 @@ def main():
     roof["launches_per_step"] = d["launches"] / args.steps
     roof["work_per_launch"] = d["work"] / d["launches"]
     roof["peak_source"] = peak_kind + (" (sustained)" if roof["bound"] == "tensor" else "")
-    roof["note"] = ("live launch durations with all K stage streams running concurrently on the GPU "
-                    "(each launch shares the SMs with the other stages' kernels); share_norm is comparable "
-                    "with the serialised ncu launch list")
+    roof["note"] = ("CUDA-event launch durations from a profiled pass of the same step with all K stages "
+                    "serialised on one stream (each launch runs alone, as in the ncu launch list); the timed "
+                    "run overlaps the stages' kernels, so its step is shorter than the sum of these")
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
@@ -500,7 +502,8 @@ def main():
                              % (nparams / 1e6, nparams * 16 // 10**6)},
             "e2e": e2e, "gpu_launches": result["launches"], "graph_replays": result.get("replays"),
             "clocks": result["clocks"],
-            "roofline": result["roof"], "kernel_shares": result["shares"], "bubble": bubble, "cpu_baseline": cpu,
+            "roofline": result["roof"], "kernel_shares": result["shares"],
+            "profiled_step_ms": prof_step_ms if not mp_mode else None, "bubble": bubble, "cpu_baseline": cpu,
             "adam_predict": sweep}
     print(json.dumps(line), flush=True)
     return 0

@@ -124,6 +124,9 @@ typedef struct {
                                          backward B(u) first re-runs the stage forward under W_hat_b
                                          from the stashed stage input (the last stage also its loss
                                          gradient) and differentiates that forward */
+  int32_t serialize;                  /* profiling aid (single process, one device): all stages and
+                                         their weight-gradient work on one stream in the dataflow
+                                         enqueue order, so every kernel runs alone */
 } xpipe_config;
 
 /* one device-trace record (K12): op 0 = forward, 1 = backward, 2 = update.  version is the

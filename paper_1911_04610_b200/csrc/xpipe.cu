@@ -110,7 +110,13 @@ void free_all(xpipe_ctx* c) {
     s.ev_pool.clear();
     for (auto& v : s.ev_flag) { for (auto e : v) cudaEventDestroy(e); v.clear(); }
     for (auto& e : s.tmark) if (e) { cudaEventDestroy(e); e = nullptr; }
-    if (s.side) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.side); cudaStreamDestroy(s.side); s.side = nullptr; }
+    // a serialised context shares stage 0's stream: destroy each stream once
+    const bool shared = c->cfg.serialize && !c->mp() && s.k > 0 && s.dev == c->S[0].dev;
+    if (s.side && s.side != s.stream && !shared) {
+      cudaSetDevice(s.dev); cudaStreamSynchronize(s.side); cudaStreamDestroy(s.side);
+    }
+    s.side = nullptr;
+    if (shared) s.stream = nullptr;
     for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1]})
       if (*e) { cudaEventDestroy(*e); *e = nullptr; }
     if (s.stream) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.stream); cudaStreamDestroy(s.stream); s.stream = nullptr; }
@@ -732,8 +738,17 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
     StageRT& s = c->S[k];
     if (c->mp() && k != c->cfg.my_stage) continue;
     cudaSetDevice(s.dev);
-    if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
-    if (cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
+    if (c->cfg.serialize && !c->mp() && k > 0 && s.dev == c->S[0].dev) {
+      // profiling aid: every stage (and its weight-gradient work) on stage 0's stream, in the
+      // host's dataflow enqueue order -- each kernel then runs alone, as in ncu's launch list
+      s.stream = c->S[0].stream;
+      s.side = c->S[0].stream;
+    } else {
+      if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
+      if (c->cfg.serialize && !c->mp()) s.side = s.stream;
+      else if (cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking) != cudaSuccess)
+        return fail_init(XP_ECUDA, "stream");
+    }
     for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1]})
       if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail_init(XP_ECUDA, "event");
     if (cudaMallocHost(&s.diag, 256) != cudaSuccess) return fail_init(XP_ENOMEM, "diag buffer");

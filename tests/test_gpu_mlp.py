@@ -118,3 +118,23 @@ def test_cuda_graph_replay_bit_exact(oracle_mod, K, T):
         assert g.version(k) == o.version(k) == sum(calls)
     assert np.array_equal(g.params_flat(), o.params_flat().astype(np.float32))
     np.testing.assert_allclose(lg[np.isfinite(lg)], lo[np.isfinite(lg)], rtol=1e-5)
+
+
+@pytest.mark.parametrize("K,T", [(2, 4), (3, 2)])
+def test_serialized_streams_bit_exact(oracle_mod, K, T):
+    """cfg.serialize (the bench's profiling mode: every stage on one stream in the dataflow
+    enqueue order) runs the same pipeline: weights and trace bit-exact with the oracle."""
+    from paper_1911_04610_b200 import XPipe
+    L = S.mlp()
+    P = S.make_params(L, 1)
+    N, M = 32, 5
+    x, y = S.make_inputs(M * N, (784, 1, 1), 10, 1, kind="mnist")
+    o = oracle_mod.Oracle(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, P, mode="fp32")
+    g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, params=P, precision="fp32", trace=True,
+              serialize=True, watchdog_ms=20000)
+    o.step(x, y, M, flush=True)
+    g.step(x, y, M, flush=True)
+    for k in range(K):
+        assert g.trace(k) == o.trace(k)
+    assert np.array_equal(g.params_flat(), o.params_flat().astype(np.float32))
+    g.close()

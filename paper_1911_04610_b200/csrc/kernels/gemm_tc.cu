@@ -1124,7 +1124,8 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   if (splits <= 1 && BN == 256) want = st256;
   args.stages = std::max(args.a_tma ? 2 : 4, std::min(DEEP, want));
   dim3 grid;
-  if (splits <= 1) grid = dim3(std::max(1, std::min(mt * nt, num_sms())), 1, 1);
+  static const int pmult = std::max(1, getenv_int("XPIPE_PERSIST_MULT", 1));  // dev: CTAs per SM in the grid
+  if (splits <= 1) grid = dim3(std::max(1, std::min(mt * nt, pmult * num_sms())), 1, 1);
   else grid = dim3(mt, nt, splits);
   const int SMEM = args.stages * STAGE + 1024 + 1024;  // ring + alignment + barriers/BN exchange
   if (splits <= 1) {

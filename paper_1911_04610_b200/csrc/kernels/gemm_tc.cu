@@ -1204,9 +1204,11 @@ int choose_bn(int M, int N) {
 // pipeline fill, epilogue -- is several k-blocks' worth); no split when the tile grid alone
 // fills half the SMs or K is short.
 struct SplitPlan { int bn, cs, nc, kbps; };
-SplitPlan plan_splits(int M, int N, int K) {
+__host__ int wgrad_min_bn() { static const int v = getenv_int("XPIPE_WGRAD_BN", 64); return v; }
+SplitPlan plan_splits(int M, int N, int K, int min_bn = 64) {
   SplitPlan p;
   p.bn = choose_bn(M, N);
+  if (min_bn > p.bn && N > 64) p.bn = N > 128 && min_bn >= 256 ? 256 : 128;
   const int tiles = ((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn);
   const int nkb = std::max(1, (K + BK - 1) / BK);
   int s = 1;
@@ -1222,7 +1224,7 @@ SplitPlan plan_splits(int M, int N, int K) {
 template <int MODE, bool A_MN, bool B_MN>
 cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_ldo, int accumulate, float* ws,
                       int64_t ws_elems, int* counters, cudaStream_t st) {
-  SplitPlan p = plan_splits(a.M, a.N, a.K);
+  SplitPlan p = plan_splits(a.M, a.N, a.K, MODE == GEMM_WGRAD ? wgrad_min_bn() : 64);
   a.kb_per_split = p.kbps;
   a.cs = p.cs; a.nc = p.nc; a.splits = p.cs * p.nc;
   a.ws = ws; a.ws_elems = ws ? ws_elems : 0; a.tile_counters = counters;
@@ -1275,14 +1277,14 @@ cudaError_t tc_conv_wgrad(const ConvGeo& g, const bf16* X, const bf16* dY, float
 
 int64_t tc_conv_ws_elems(const ConvGeo& g) {
   // split-K partial planes + cross-cluster slices of the largest of the three GEMMs
-  auto need = [](int M, int N, int K) -> int64_t {
-    const SplitPlan p = plan_splits(M, N, K);
+  auto need = [](int M, int N, int K, int min_bn = 64) -> int64_t {
+    const SplitPlan p = plan_splits(M, N, K, min_bn);
     if (p.cs * p.nc <= 1) return 0;
     const int64_t tiles = (int64_t)((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn);
     return tiles * (p.cs * p.nc + (p.nc > 1 ? p.nc : 0)) * BM * p.bn;
   };
   return std::max({need(g.Nimg * g.P * g.Q, g.Co, g.R * g.S * g.C), need(g.Nimg * g.H * g.W, g.C, g.R * g.S * g.Co),
-                   need(g.R * g.S * g.C, g.Co, g.Nimg * g.P * g.Q)});
+                   need(g.R * g.S * g.C, g.Co, g.Nimg * g.P * g.Q, wgrad_min_bn())});
 }
 
 }  // namespace xp

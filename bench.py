@@ -480,7 +480,8 @@ def main():
         bubble = measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank, sched)
     except Exception as e:  # the bubble is a report, not the metric
         bubble = {"error": repr(e)[:200]}
-    cpu = None if args.no_cpu_baseline else cpu_baseline(args.workload)
+    # the oracle baseline is timed on rank 0 at N=1 only (the contract); N>1 lines omit it
+    cpu = None if (args.no_cpu_baseline or mp_mode) else cpu_baseline(args.workload)
     sweep = None
     if not args.no_sweep and not mp_mode:
         # the BASELINE metric's second half: the fused Adam+prediction sweep alone (config 5)

@@ -191,6 +191,20 @@ int xpipe_sync(struct xpipe_ctx* h);
 int xpipe_get_weights(struct xpipe_ctx* h, int32_t layer, int32_t tensor, int32_t state,
                       int64_t version, float* dst, size_t count);
 
+/* Overwrite one parameter tensor's state (XP_S_PARAM, XP_S_M, XP_S_V or XP_S_BUF) with src,
+   fp32 in PyTorch layout, count = the tensor size (else XP_EINVAL).  Waits for the pipeline
+   first; the W_hat buffers are NOT updated -- call xpipe_refresh_predictions after the last
+   set.  Used for teacher-forced parity diagnostics: the oracle's state is
+   loaded before each step.  XP_EINVAL for a stage of another process. */
+int xpipe_set_weights(struct xpipe_ctx* h, int32_t layer, int32_t tensor, int32_t state, const float* src,
+                      size_t count);
+
+/* Recompute every owned stage's W_hat_f (buffer of the current version) and W_hat_b from its
+   current W, m, v and version, as the update sweep would have (Eq. (3) with the stage's
+   s_f / s_b).  Only between calls of a flushed pipeline (XP_ESTATE otherwise is not checked:
+   the caller flushes). */
+int xpipe_refresh_predictions(struct xpipe_ctx* h);
+
 /* Number of trace records of a stage (*n_out) and up to cap of them (dst may be NULL). */
 int xpipe_get_trace(struct xpipe_ctx* h, int32_t stage, xpipe_trace_rec* dst, size_t cap,
                     size_t* n_out);

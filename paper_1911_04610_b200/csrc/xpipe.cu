@@ -1007,6 +1007,56 @@ int xpipe_get_weights(xpipe_ctx* c, int32_t layer, int32_t tensor, int32_t state
   return XP_OK;
 }
 
+int xpipe_set_weights(xpipe_ctx* c, int32_t layer, int32_t tensor, int32_t state, const float* src, size_t count) {
+  if (!c || !src) return set_err(c, XP_EINVAL, "args");
+  if (c->poisoned) return XP_ESTATE;
+  if (layer < 0 || layer >= (int)c->net.layers.size()) return set_err(c, XP_EINVAL, "layer");
+  const LayerInfo& L = c->net.layers[layer];
+  if (tensor != XP_T_WEIGHT && tensor != XP_T_BIAS) return set_err(c, XP_EINVAL, "tensor");
+  const int64_t n = tensor == XP_T_WEIGHT ? L.nw_torch : L.nb;
+  if ((int64_t)count != n) return set_err(c, XP_EINVAL, "count is not the tensor size");
+  if (n == 0) return XP_OK;
+  XP_TRY(sync_all(c));
+  StageRT& s = c->S[L.stage];
+  if (!owned(s)) return set_err(c, XP_EINVAL, "layer belongs to a stage of another process");
+  float* dst = nullptr;
+  switch (state) {
+    case XP_S_PARAM: dst = s.W; break;
+    case XP_S_M: dst = s.m; break;
+    case XP_S_V: dst = s.v; break;
+    case XP_S_BUF: dst = s.buf; break;
+    default: return set_err(c, XP_EINVAL, "state");
+  }
+  if (!dst) return set_err(c, XP_EINVAL, "XP_S_BUF needs XP_OPT_MOMENTUM_SGD");
+  const int64_t off = tensor == XP_T_WEIGHT ? L.woff : L.boff;
+  const int64_t ng = tensor == XP_T_WEIGHT ? L.nw_gpu : L.nb;
+  std::vector<float> buf(ng, 0.f);  // channel padding stays zero
+  torch_to_gpu_layout(L, tensor, src, buf.data());
+  cudaSetDevice(s.dev);
+  XP_CUDA(c, cudaMemcpy(dst + off, buf.data(), ng * 4, cudaMemcpyHostToDevice));
+  return XP_OK;
+}
+
+int xpipe_refresh_predictions(xpipe_ctx* c) {
+  if (!c) return set_err(c, XP_EINVAL, "args");
+  if (c->poisoned) return XP_ESTATE;
+  XP_TRY(sync_all(c));
+  const bool bf = c->cfg.precision == XP_BF16;
+  for (auto& s : c->S) {
+    if (!owned(s)) continue;
+    cudaSetDevice(s.dev);
+    const float sf = (float)version_difference(c, s.k, 0), sb = (float)version_difference(c, s.k, 1);
+    void* pf = s.pf[s.host_ver & 1];
+    if (c->cfg.delta_form == XP_DELTA_ADAM && s.host_ver == 0)
+      XP_TRY(check_launch(c, launch_predict_copy(s.W, pf, s.pb, s.plan.P, bf, s.stream), "refresh"));
+    else
+      XP_TRY(check_launch(c, launch_sweep(s.W, s.g, s.m, s.v, pf, s.pb, s.plan.P, s.ds, nullptr, sf, sb, bf,
+                                          c->cfg.delta_form, false, s.stream), "refresh"));
+    XP_CUDA(c, cudaStreamSynchronize(s.stream));
+  }
+  return XP_OK;
+}
+
 int xpipe_get_trace(xpipe_ctx* c, int32_t stage, xpipe_trace_rec* dst, size_t cap, size_t* n_out) {
   if (!c || !n_out || stage < 0 || stage >= c->K) return set_err(c, XP_EINVAL, "args");
   if (c->poisoned) return XP_ESTATE;

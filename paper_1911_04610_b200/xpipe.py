@@ -98,6 +98,8 @@ def lib():
         L.xpipe_adam_predict.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, f32, f32, f32, f32, i32, i32, i32, i32, vp]
         L.xpipe_sgd_predict.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f32, f32, i32, i32, i32,
                                         vp]
+        L.xpipe_set_weights.argtypes = [vp, i32, i32, i32, vp, C.c_size_t]
+        L.xpipe_refresh_predictions.argtypes = [vp]
         L.xpipe_gemm_bf16.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i64, vp]
         L.xpipe_conv2d_bf16.argtypes = [i32, C.POINTER(i32), vp, vp, vp, i32, vp, i64, vp]
         _lib = L
@@ -246,6 +248,15 @@ class XPipe:
         out = np.empty(count, dtype=np.float32)
         _check(lib().xpipe_get_weights(self.h, layer, tensor, STATE[state], version, _ptr(out), count), self.h)
         return out
+
+    def set(self, layer, tensor, state, values):
+        """xpipe_set_weights: overwrite one tensor's W / m / v / buf (PyTorch layout)."""
+        a = np.ascontiguousarray(values, dtype=np.float32).ravel()
+        _check(lib().xpipe_set_weights(self.h, layer, tensor, STATE[state], _ptr(a), a.size), self.h)
+
+    def refresh_predictions(self):
+        """xpipe_refresh_predictions: rematerialise W_hat_f / W_hat_b from the current state."""
+        _check(lib().xpipe_refresh_predictions(self.h), self.h)
 
     def _count(self, layer, tensor):
         l = self.layers[layer]

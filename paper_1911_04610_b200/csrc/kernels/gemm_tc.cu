@@ -512,8 +512,35 @@ __device__ __forceinline__ Work work_of(const GemmArgs& a, int j, int mt) {
 template <int MODE, int BN, bool A_MN, bool B_MN>
 __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* tmA, const CUtensorMap* tmB, uint32_t base,
                                          uint32_t full0, uint32_t empty0, int nunits, int mt, int tid) {
-  constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
+  constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
   Ring ring(a.stages);
+  if (MODE == GEMM_FPROP && a.a_tma == 3) {
+    // paired k-blocks (C % 128 == 0, no split-K, even ring): one 5-D box lands the A tiles of
+    // k-blocks 2i and 2i+1 (two 64-channel blocks of one tap) in two consecutive A slots and
+    // one 3-D box the two B tiles in two consecutive B slots, all on slot 2i's full barrier;
+    // slot 2i+1's barrier is arrived at once (its bytes are counted by slot 2i's)
+    if (tid != 0) return;
+    for (int j = 0; j < nunits; ++j) {
+      const Work w = work_of<BN>(a, j, mt);
+      const int tn = w.m0 / (a.gq * a.gp), rem = w.m0 - tn * a.gq * a.gp, tp = rem / a.gq, tq = rem - tp * a.gq;
+      for (int i = 0; i < w.nkb; i += 2) {
+        const int s0 = ring.slot;
+        mbar_wait(empty0 + 8 * s0, ring.phase ^ 1u);
+        mbar_wait(empty0 + 8 * (s0 + 1), ring.phase ^ 1u);
+        const uint32_t sa = base + s0 * A_BYTES, sb = base + a.stages * A_BYTES + s0 * B_BYTES;
+        const uint32_t full = full0 + 8 * s0;
+        const int k0 = (w.kb0 + i) * BK;
+        const int tap = k0 / a.g.C, c0 = k0 - tap * a.g.C, r = tap / a.g.S, ss = tap - r * a.g.S;
+        mbar_expect_tx(full, 2 * STAGE);
+        tma_5d(sa, tmA, 0, tq + ss - a.g.pw, tp + r - a.g.ph, tn, c0 / 64, full);
+        tma_3d(sb, tmB, 0, w.n0, k0 / 64, full);
+        mbar_arrive(full0 + 8 * (s0 + 1));
+        ring.next();
+        ring.next();
+      }
+    }
+    return;
+  }
   if (a.a_tma) {
     // full-TMA pipeline: one elected thread streams both operands; the others are idle
     if (tid != 0) return;
@@ -527,7 +554,8 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
       }
       for (int i = 0; i < w.nkb; ++i, ring.next()) {
         mbar_wait(empty0 + 8 * ring.slot, ring.phase ^ 1u);
-        const uint32_t sa = base + ring.slot * STAGE, sb = sa + A_BYTES, full = full0 + 8 * ring.slot;
+        const uint32_t sa = base + ring.slot * A_BYTES, sb = base + a.stages * A_BYTES + ring.slot * B_BYTES;
+        const uint32_t full = full0 + 8 * ring.slot;
         const int k0 = (w.kb0 + i) * BK;
         if (MODE == GEMM_PLAIN) {
           mbar_expect_tx(full, STAGE);
@@ -602,7 +630,7 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
     for (int i = 0; i < w.nkb; ++i, ring.next()) {
       const int kb = w.kb0 + i;
       mbar_wait(empty0 + 8 * ring.slot, ring.phase ^ 1u);
-      const uint32_t sa = base + ring.slot * STAGE, sb = sa + A_BYTES;
+      const uint32_t sa = base + ring.slot * A_BYTES, sb = base + a.stages * A_BYTES + ring.slot * B_BYTES;
       const uint32_t full = full0 + 8 * ring.slot;
       if (a.b_tma && tid == 0) {  // one elected thread moves the whole B tile with the TMA engine
         mbar_expect_tx(full, BN * BK * 2);
@@ -651,7 +679,7 @@ template <int MODE, int BN, bool A_MN, bool B_MN>
 __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, const __grid_constant__ CUtensorMap tmA,
                                                                const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
-  constexpr uint32_t A_BYTES = BM * BK * 2, STAGE = A_BYTES + BN * BK * 2;
+  constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
   const int ST = a.stages;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023) & ~1023u;
@@ -714,7 +742,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
           mbar_wait(full0 + 8 * ring.slot, ring.phase);
           if (a.dbg && j == 0 && i == 0) a.dbg[cta * 16 + 1] = gtimer();
           tc_fence_after();
-          const uint32_t sa = base + ring.slot * STAGE, sb = sa + A_BYTES;
+          const uint32_t sa = base + ring.slot * A_BYTES, sb = base + ST * A_BYTES + ring.slot * B_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = A_MN ? sdesc(sa + kk * 2048, BK * 128, 1024) : sdesc(sa + kk * 32, 16, 1024);
@@ -1123,6 +1151,28 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   if (splits <= 1 && BN == 128) want = st128;
   if (splits <= 1 && BN == 256) want = st256;
   args.stages = std::max(args.a_tma ? 2 : 4, std::min(DEEP, want));
+  static const bool no_pair = getenv_flag("XPIPE_NO_KPAIR");
+  if (MODE == GEMM_FPROP && splits <= 1 && args.a_tma == 1 && args.b_tma == 1 && args.g.C % 128 == 0 &&
+      args.stages % 2 == 0 && !no_pair) {
+    // paired k-blocks (see the producer): A as a 5-D map with the channel block outermost, B as
+    // a 3-D map {64, Co, K/64}; both boxes cover two consecutive k-blocks
+    const ConvGeo& g = args.g;
+    uint32_t pb[3];
+    CUtensorMap pa, pbm;
+    if (pixel_box(BM, g.Q, g.P, pb)) {
+      const uint64_t d5[5] = {64, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)g.Nimg, (uint64_t)(g.C / 64)};
+      const uint64_t s5[4] = {(uint64_t)g.C * 2, (uint64_t)g.W * g.C * 2, (uint64_t)g.H * g.W * g.C * 2, 128};
+      const uint32_t b5[5] = {64, pb[0], pb[1], pb[2], 2};
+      const uint64_t d3[3] = {64, (uint64_t)args.N, (uint64_t)(args.K / 64)};
+      const uint64_t s3[2] = {(uint64_t)args.K * 2, 128};
+      const uint32_t b3[3] = {64, (uint32_t)BN, 2};
+      if (args.K % 128 == 0 && make_map(&pa, args.A, 5, d5, s5, b5) && make_map(&pbm, args.B, 3, d3, s3, b3)) {
+        tmA = pa;
+        tmB = pbm;
+        args.a_tma = 3;
+      }
+    }
+  }
   dim3 grid;
   static const int pmult = std::max(1, getenv_int("XPIPE_PERSIST_MULT", 1));  // dev: CTAs per SM in the grid
   if (splits <= 1) grid = dim3(std::max(1, std::min(mt * nt, pmult * num_sms())), 1, 1);

@@ -55,7 +55,6 @@ cudaError_t launch_trace_begin(DevState* ds, TraceRec* rec, int stage, int op, i
                                cudaStream_t st);
 cudaError_t launch_trace_end(TraceRec* rec, cudaStream_t st);
 cudaError_t launch_rebase_flags(uint32_t* flags, int n, uint32_t delta, cudaStream_t st);
-cudaError_t launch_copy_f32(const float* src, float* dst, int64_t n, cudaStream_t st);
 cudaError_t launch_fill_uniform(float* dst, int64_t n, float bound, uint64_t seed, uint64_t stream_id,
                                 cudaStream_t st);
 cudaError_t launch_fill_const(float* dst, int64_t n, float value, cudaStream_t st);

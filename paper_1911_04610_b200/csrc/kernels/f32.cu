@@ -43,12 +43,6 @@ __global__ void rebase_flags_kernel(uint32_t* f, int n, uint32_t delta) {
   if (threadIdx.x < n) f[threadIdx.x] -= delta;
 }
 
-__global__ void copy_kernel(const float* __restrict__ s, float* __restrict__ d, int64_t n) {
-  pdl_wait();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    d[i] = s[i];
-}
-
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ull;
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -212,11 +206,6 @@ cudaError_t launch_rebase_flags(uint32_t* flags, int n, uint32_t delta, cudaStre
 
 cudaError_t launch_trace_end(TraceRec* rec, cudaStream_t st) {
   launch_pdl(trace_end_kernel, dim3(1), dim3(1), 0, st, rec);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_copy_f32(const float* src, float* dst, int64_t n, cudaStream_t st) {
-  launch_pdl(copy_kernel, dim3(grid_for(n)), dim3(256), 0, st, src, dst, n);
   return cudaGetLastError();
 }
 

@@ -275,6 +275,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the embedded config-5 sweep measurement")
     ap.add_argument("--recompute", action="store_true", help="activation recomputation (P:167, SURVEY f3)")
+    ap.add_argument("--no-fb-overlap", action="store_true",
+                    help="one stream per stage (default: a forward stream per stage, F(u+S) overlaps B(u))")
     ap.add_argument("--partition", default="layer-count", choices=["layer-count", "balanced"],
                     help="stage split: the paper's layer-count rule (R17) or cost-balanced (SURVEY 8e)")
     ap.add_argument("--image", type=int, default=64, help="Tiny-ImageNet side for resnet101/inception (224: f4)")
@@ -343,6 +345,8 @@ def main():
         sched.update(optimizer="sgd", delta="paper", momentum=0.9, weight_decay=5e-4)
     if args.recompute:  # f3: activation recomputation in every backward
         sched.update(recompute=True)
+    if not args.no_fb_overlap:  # forwards on a second stream per stage (F(u+S) overlaps B(u))
+        sched.update(fb_overlap=True)
     def make_model(profile):
         if mp_mode:
             # one process per GPU: this rank owns stage `rank`; rings/flags are CUDA IPC-mapped
@@ -497,7 +501,7 @@ def main():
                        "global_batch": N, "stages": K, "micro_batches": T, "minibatches_per_step": M,
                        "parallelism": "pipeline K=%d (%s)" % (K, "GPipe-flush" if args.schedule == "gpipe" else "XPipe"),
                        "schedule": args.schedule, "optimizer": args.optimizer, "recompute": args.recompute,
-                       "partition": args.partition,
+                       "partition": args.partition, "fb_overlap": not args.no_fb_overlap,
                        "image": list(shape),
                        "l2": "working set > L2: optimizer state 16 B/param x %.1fM params = %d MB (126 MB L2)"
                              % (nparams / 1e6, nparams * 16 // 10**6)},

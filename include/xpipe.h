@@ -127,6 +127,10 @@ typedef struct {
   int32_t serialize;                  /* profiling aid (single process, one device): all stages and
                                          their weight-gradient work on one stream in the dataflow
                                          enqueue order, so every kernel runs alone */
+  int32_t fb_overlap;                 /* 1 = each stage runs its forwards on a second stream, so
+                                         F(u+S) overlaps B(u) (one more ring/stash slot per stage;
+                                         ordering by events: F(u) -> B(u), B(u) -> F(u+S+1),
+                                         update -> next bellwether forward); same results */
 } xpipe_config;
 
 /* one device-trace record (K12): op 0 = forward, 1 = backward, 2 = update.  version is the

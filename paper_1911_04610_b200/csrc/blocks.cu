@@ -102,6 +102,13 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
     s.ws_side = (float*)A((size_t)std::max<int64_t>(ws, 64) * 4);
     s.ctr_side = (int*)A((size_t)kTileCounters * sizeof(int));
     if (!s.ws || !s.bnws || !s.ctr || !s.ws_side || !s.ctr_side) return set_err(c, XP_ENOMEM, "workspace");
+    if (s.fstream != s.stream) {  // fb_overlap: the forward stream's own scratch
+      s.ws_f = (float*)A((size_t)std::max<int64_t>(ws, 64) * 4);
+      s.bnws_f = (float*)A(bnws * 4);
+      s.ctr_f = (int*)A((size_t)kTileCounters * sizeof(int));
+      if (!s.ws_f || !s.bnws_f || !s.ctr_f) return set_err(c, XP_ENOMEM, "workspace");
+      XP_CUDA(c, cudaMemsetAsync(s.ctr_f, 0, (size_t)kTileCounters * sizeof(int), s.stream));
+    }
     XP_CUDA(c, cudaMemsetAsync(s.ctr, 0, (size_t)kTileCounters * sizeof(int), s.stream));
     XP_CUDA(c, cudaMemsetAsync(s.ctr_side, 0, (size_t)kTileCounters * sizeof(int), s.stream));
   }

@@ -69,6 +69,15 @@ struct StageRT {
   float* ws_side = nullptr;
   int* ctr_side = nullptr;
   int64_t gbuf_elems = 0;
+  // fb_overlap: forwards on their own stream with their own scratch (swapped in by FwdScope)
+  cudaStream_t fstream = nullptr;
+  float* ws_f = nullptr;
+  int* ctr_f = nullptr;
+  float* bnws_f = nullptr;
+  std::vector<cudaEvent_t> ev_fdone, ev_bdone;  // per slot: F(u) done, B(u) done
+  std::vector<int64_t> fdone_epoch, bdone_epoch;
+  cudaEvent_t ev_upd = nullptr, ev_fmark = nullptr, ev_fjoin = nullptr;
+  int64_t upd_epoch = -1;
   float* ws = nullptr;                  // split-K workspace (fp32)
   int64_t ws_elems = 0;
   float* bnws = nullptr;                // BatchNorm partial-reduction workspace
@@ -133,6 +142,7 @@ struct xpipe_ctx {
   int64_t graph_replays = 0;
   bool capturing = false;
   bool recompute_pass = false;          // f3: op_forward is re-running a stage forward inside B(u)
+  int64_t call_epoch = 0;               // bumped per call: events recorded in earlier calls are complete
   float* loss_scratch = nullptr;        // the recomputed forward's loss (the reported loss is F(u)'s)
   std::vector<int64_t> cap_fwd0, cap_bwd0;  // enqueue counters when the capture started
   std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)

@@ -112,13 +112,19 @@ void free_all(xpipe_ctx* c) {
     for (auto& e : s.tmark) if (e) { cudaEventDestroy(e); e = nullptr; }
     // a serialised context shares stage 0's stream: destroy each stream once
     const bool shared = c->cfg.serialize && !c->mp() && s.k > 0 && s.dev == c->S[0].dev;
+    const bool own_fstream = s.fstream && s.fstream != s.stream;
     if (s.side && s.side != s.stream && !shared) {
       cudaSetDevice(s.dev); cudaStreamSynchronize(s.side); cudaStreamDestroy(s.side);
     }
     s.side = nullptr;
     if (shared) s.stream = nullptr;
-    for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1]})
+    for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1], &s.ev_upd, &s.ev_fmark, &s.ev_fjoin})
       if (*e) { cudaEventDestroy(*e); *e = nullptr; }
+    for (auto* v : {&s.ev_fdone, &s.ev_bdone}) { for (auto e : *v) if (e) cudaEventDestroy(e); v->clear(); }
+    if (own_fstream) {
+      cudaSetDevice(s.dev); cudaStreamSynchronize(s.fstream); cudaStreamDestroy(s.fstream);
+    }
+    s.fstream = nullptr;
     if (s.stream) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.stream); cudaStreamDestroy(s.stream); s.stream = nullptr; }
   }
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -296,9 +302,56 @@ int reserve_for_call(xpipe_ctx* c, int64_t M) {
   return XP_OK;
 }
 
+// ---- fb_overlap plumbing -------------------------------------------------------------------
+// A forward runs on the stage's forward stream with the forward scratch (split-K workspace,
+// counters, BN partials) swapped in, so every launcher below uses them unchanged.
+struct FwdScope {
+  StageRT& s;
+  bool on;
+  explicit FwdScope(StageRT& st) : s(st), on(st.fstream && st.fstream != st.stream) { if (on) swap(); }
+  ~FwdScope() { if (on) swap(); }
+  void swap() {
+    std::swap(s.stream, s.fstream);
+    std::swap(s.ws, s.ws_f);
+    std::swap(s.ctr, s.ctr_f);
+    std::swap(s.bnws, s.bnws_f);
+  }
+};
+// events between a stage's two streams; an event recorded in an earlier call is complete (every
+// call starts from a drained pipeline), so waiting on it is skipped -- which also keeps graph
+// captures free of edges to work outside the capture
+int ev_record(xpipe_ctx* c, cudaStream_t st, cudaEvent_t e, int64_t* epoch) {
+  XP_CUDA(c, cudaEventRecord(e, st));
+  *epoch = c->call_epoch;
+  return XP_OK;
+}
+int ev_wait(xpipe_ctx* c, cudaStream_t st, cudaEvent_t e, int64_t epoch) {
+  if (epoch != c->call_epoch) return XP_OK;
+  XP_CUDA(c, cudaStreamWaitEvent(st, e, 0));
+  return XP_OK;
+}
+// make the stage stream's completion imply the forward stream's (end of a drive)
+int join_fstreams(xpipe_ctx* c) {
+  for (auto& s : c->S) {
+    if (!owned(s) || !s.fstream || s.fstream == s.stream) continue;
+    cudaSetDevice(s.dev);
+    XP_CUDA(c, cudaEventRecord(s.ev_fjoin, s.fstream));
+    XP_CUDA(c, cudaStreamWaitEvent(s.stream, s.ev_fjoin, 0));
+  }
+  return XP_OK;
+}
+
 // ---- forward / backward of one stage on one micro-batch -----------------------------------
 int enqueue_forward(xpipe_ctx* c, int k, int64_t u) {
   StageRT& s = c->S[k];
+  cudaSetDevice(s.dev);
+  FwdScope fwd(s);  // fb_overlap: from here s.stream is the forward stream
+  if (fwd.on) {
+    const int slot0 = (int)((u - 1) % s.S);
+    XP_TRY(ev_wait(c, s.stream, s.ev_bdone[slot0], s.bdone_epoch[slot0]));  // B(u - S) freed the slot
+    const int64_t t0 = (u - 1) / c->T + 1;
+    if (u - (t0 - 1) * c->T == 1) XP_TRY(ev_wait(c, s.stream, s.ev_upd, s.upd_epoch));  // W_hat_f of the version
+  }
   const int64_t t = (u - 1) / c->T + 1, j = u - (t - 1) * c->T;
   const int slot = (int)((u - 1) % s.S);
   const int sf = version_difference(c, k, 0);
@@ -326,6 +379,7 @@ int enqueue_forward(xpipe_ctx* c, int k, int64_t u) {
     XP_TRY(flag_write(c, s, nx, 0, u));
   }
   if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
+  if (fwd.on) XP_TRY(ev_record(c, s.stream, s.ev_fdone[slot], &s.fdone_epoch[slot]));
   return XP_OK;
 }
 
@@ -336,6 +390,8 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
   const int sb = version_difference(c, k, 1);
   const bool bw = (j == 1);
   cudaSetDevice(s.dev);
+  const bool ov = s.fstream && s.fstream != s.stream;
+  if (ov) XP_TRY(ev_wait(c, s.stream, s.ev_fdone[slot], s.fdone_epoch[slot]));  // F(u) on the forward stream
   if (k + 1 < c->K) XP_TRY(flag_wait(c, s, 1, u));
   TraceRec* rec = nullptr;
   XP_TRY(trace_slot(c, s, &rec));
@@ -387,8 +443,14 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     s.side_used = false;
   }
   if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
+  if (ov) XP_TRY(ev_record(c, s.stream, s.ev_bdone[slot], &s.bdone_epoch[slot]));  // slot free for F(u + S)
   if (j == c->T) {
     // the T-th micro-batch's backward ends the mini-batch: update + prediction (K1)
+    if (ov) {  // forwards enqueued so far (still reading W_hat_f buffers) finish before the sweep
+      int64_t e = 0;
+      XP_TRY(ev_record(c, s.fstream, s.ev_fmark, &e));
+      XP_TRY(ev_wait(c, s.stream, s.ev_fmark, e));
+    }
     TraceRec* urec = nullptr;
     XP_TRY(trace_slot(c, s, &urec));
     XP_TRY(check_launch(c, launch_bump(s.ds, urec, k, (int)t, c->T, s.stream), "bump"));
@@ -407,6 +469,7 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     const double sgd_extra = c->cfg.optimizer == XP_OPT_MOMENTUM_SGD ? 8.0 : 0.0;
     XP_TRY(prof_end(c, s, XP_PROF_SWEEP, (double)s.plan.P * ((bf16 ? 32.0 : 36.0) + sgd_extra)));
     s.host_ver = nv;
+    if (ov) XP_TRY(ev_record(c, s.stream, s.ev_upd, &s.upd_epoch));  // the next bellwether forward waits
     if (c->cfg.snapshots) {
       if (s.snap_pool.empty()) return set_err(c, XP_ESCHED, "snapshot pool (internal)");
       Snapshot sn{nv, {}, s.snap_pool.back()};
@@ -460,7 +523,7 @@ int drive(xpipe_ctx* c, int64_t total) {
       }
     }
   }
-  return XP_OK;
+  return join_fstreams(c);
 }
 
 // on a watchdog timeout: read the ring flags and the trace tail through a side stream
@@ -506,6 +569,7 @@ int sync_all(xpipe_ctx* c) {
     cudaSetDevice(s.dev);
     for (;;) {
       cudaError_t e = cudaStreamQuery(s.stream);
+      if (e == cudaSuccess && s.fstream && s.fstream != s.stream) e = cudaStreamQuery(s.fstream);
       if (e == cudaSuccess) break;
       if (e != cudaErrorNotReady) return set_err(c, XP_ECUDA, std::string("stream: ") + cudaGetErrorString(e));
       if (std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count() > ms)
@@ -595,6 +659,8 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
   XP_CUDA(c, cudaStreamBeginCapture(o.stream, cudaStreamCaptureModeThreadLocal));
   XP_CUDA(c, cudaEventRecord(evs[0], o.stream));
   for (size_t k = 1; k < c->S.size(); ++k) XP_CUDA(c, cudaStreamWaitEvent(c->S[k].stream, evs[0], 0));
+  for (auto& s : c->S)
+    if (s.fstream && s.fstream != s.stream) XP_CUDA(c, cudaStreamWaitEvent(s.fstream, evs[0], 0));
   c->cap_fwd0.clear(); c->cap_bwd0.clear();
   for (auto& s : c->S) {
     c->cap_fwd0.push_back(s.fwd_enq);
@@ -716,6 +782,15 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
     if (s.dev < 0 || s.dev >= ndev) return set_err(nullptr, XP_EINVAL, "device id out of range");
     s.plan = c->net.stages[k];
     s.S = c->cfg.schedule == XP_SCHED_GPIPE ? T : (stages - k);
+    if (c->cfg.fb_overlap) {
+      // one more slot, so F(u+S) can overlap B(u); rounded to a divisor or a multiple of T so
+      // the slot phase of every stage repeats each call (a call feeds whole mini-batches) and
+      // steady-state calls keep replaying one CUDA graph
+      int want = s.S + 1;
+      if (want <= T) { while (T % want) ++want; }
+      else want = (want + T - 1) / T * T;
+      s.S = want;
+    }
   }
   // peer access between the devices of neighbouring stages (multi-process mode: lazily, by
   // cudaIpcOpenMemHandle)
@@ -749,6 +824,17 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
       else if (cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking) != cudaSuccess)
         return fail_init(XP_ECUDA, "stream");
     }
+    s.fstream = s.stream;
+    if (c->cfg.fb_overlap && !c->cfg.serialize &&
+        cudaStreamCreateWithFlags(&s.fstream, cudaStreamNonBlocking) != cudaSuccess)
+      return fail_init(XP_ECUDA, "stream");
+    s.ev_fdone.assign(s.S, nullptr); s.ev_bdone.assign(s.S, nullptr);
+    s.fdone_epoch.assign(s.S, -1); s.bdone_epoch.assign(s.S, -1);
+    for (auto* v : {&s.ev_fdone, &s.ev_bdone})
+      for (auto& e : *v)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail_init(XP_ECUDA, "event");
+    for (cudaEvent_t* e : {&s.ev_upd, &s.ev_fmark, &s.ev_fjoin})
+      if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail_init(XP_ECUDA, "event");
     for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1]})
       if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail_init(XP_ECUDA, "event");
     if (cudaMallocHost(&s.diag, 256) != cudaSuccess) return fail_init(XP_ENOMEM, "diag buffer");
@@ -785,6 +871,7 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
   const int64_t k0 = c->kernels, g0 = c->graph_replays;
   // previous call's work must be done before its call buffers are overwritten
   XP_TRY(sync_all(c));
+  ++c->call_epoch;  // every event recorded before this point is complete
   if (M > 0) {
     XP_TRY(ensure_call_buffers(c, M));
     const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
@@ -793,13 +880,13 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     if (owned(s0)) {
       cudaSetDevice(s0.dev);
       XP_CUDA(c, cudaMemcpyAsync(c->x_dev, x, (size_t)M * c->N * per * 4,
-                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.stream));
+                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.fstream));
     }
     if (owned(sl)) {
       cudaSetDevice(sl.dev);
       XP_CUDA(c, cudaMemcpyAsync(c->y_dev, y, (size_t)M * c->N * 4,
-                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sl.stream));
-      XP_CUDA(c, cudaMemsetAsync(c->loss_dev, 0xff, (size_t)M * c->T * 4, sl.stream));  // NaN = not computed
+                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sl.fstream));
+      XP_CUDA(c, cudaMemsetAsync(c->loss_dev, 0xff, (size_t)M * c->T * 4, sl.fstream));  // NaN = not computed
     }
     c->call_first = c->fed + 1;
     c->fed += (int64_t)M * c->T;

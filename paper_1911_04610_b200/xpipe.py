@@ -45,7 +45,7 @@ class Config(C.Structure):
                 ("init_v", C.POINTER(C.POINTER(C.c_float))),
                 ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", C.c_void_p),
                 ("optimizer", C.c_int32), ("momentum", C.c_float), ("weight_decay", C.c_float),
-                ("recompute", C.c_int32), ("serialize", C.c_int32)]
+                ("recompute", C.c_int32), ("serialize", C.c_int32), ("fb_overlap", C.c_int32)]
 
 
 class TraceRec(C.Structure):
@@ -143,7 +143,7 @@ class XPipe:
                  precision="fp32", schedule="xpipe", predict="paper", s_fwd=0, s_bwd=0, delta="adam",
                  init_m=None, init_v=None, devices=None, snapshots=False, trace=False, graphs=False, profile=False,
                  seed=1, watchdog_ms=0, torch_allocator=True, my_stage=None, optimizer="adam", momentum=0.9,
-                 weight_decay=5e-4, recompute=False, serialize=False):
+                 weight_decay=5e-4, recompute=False, serialize=False, fb_overlap=False):
         self.h = None
         L = lib()
         self.layers = list(layers)
@@ -159,7 +159,7 @@ class XPipe:
                      multi_process=int(my_stage is not None), my_stage=my_stage or 0,
                      optimizer=OPTIMIZER[optimizer], momentum=momentum if optimizer == "sgd" else 0.0,
                      weight_decay=weight_decay if optimizer == "sgd" else 0.0, recompute=int(recompute),
-                     serialize=int(serialize))
+                     serialize=int(serialize), fb_overlap=int(fb_overlap))
         if devices:
             cfg.n_devices = len(devices)
             for i, d in enumerate(devices):

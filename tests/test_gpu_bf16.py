@@ -150,3 +150,20 @@ def test_paper_224_shapes_bf16(oracle_mod):
     L = assign_stages(L, units, 2)
     g, o, P, lg, lo = run_bf16(oracle_mod, L, (3, 224, 224), 2, 1, 2, 2, kind="imagenet")
     check(g, o, L, 2, 2)
+
+
+@pytest.mark.parametrize("K,T", [(2, 2), (4, 1)])
+def test_vgg_small_bf16_fb_overlap(oracle_mod, K, T):
+    """The bf16 conv pipeline with forwards on their own stream per stage (cfg.fb_overlap):
+    same tolerance, traces and W_hat self-consistency as without."""
+    from paper_1911_04610_b200 import XPipe
+    L = vgg_small()
+    P = S.make_params(L, 1)
+    N, M = 16, 8
+    x, y = S.make_inputs(M * N, (3, 8, 8), 10, 1, kind="cifar")
+    g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (3, 8, 8), 10, params=P, precision="bf16", trace=True,
+              snapshots=True, fb_overlap=True, watchdog_ms=120000)
+    o = oracle_mod.Oracle(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (3, 8, 8), 10, P, mode="bf16", snapshots=True)
+    g.step(x, y, M, flush=True)
+    o.step(x, y, M, flush=True)
+    check(g, o, L, K, M)

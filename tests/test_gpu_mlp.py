@@ -138,3 +138,39 @@ def test_serialized_streams_bit_exact(oracle_mod, K, T):
         assert g.trace(k) == o.trace(k)
     assert np.array_equal(g.params_flat(), o.params_flat().astype(np.float32))
     g.close()
+
+
+@pytest.mark.parametrize("K,T,schedule", [(2, 4, "xpipe"), (3, 2, "xpipe"), (1, 4, "xpipe"), (2, 2, "gpipe")])
+def test_fb_overlap_bit_exact(oracle_mod, K, T, schedule):
+    """cfg.fb_overlap (forwards on a second stream per stage, one more ring slot, event
+    ordering F(u) -> B(u) -> F(u+S+1) and update -> bellwether forward): weights after every
+    version, trace and losses bit-exact with the oracle; split calls and CUDA graphs too."""
+    from paper_1911_04610_b200 import XPipe
+    L = S.mlp()
+    P = S.make_params(L, 1)
+    N, M = 32, 8
+    x, y = S.make_inputs(M * N, (784, 1, 1), 10, 1, kind="mnist")
+    o = oracle_mod.Oracle(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, P, mode="fp32", schedule=schedule,
+                          snapshots=True)
+    g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, params=P, precision="fp32", trace=True,
+              snapshots=True, schedule=schedule, fb_overlap=True, watchdog_ms=20000)
+    lo = o.step(x, y, M, flush=True)
+    lg = np.concatenate([g.step(x[:3 * N], y[:3 * N], 3), g.step(x[3 * N:], y[3 * N:], M - 3, flush=True)])
+    assert np.array_equal(lg, lo)
+    for k in range(K):
+        assert g.trace(k) == o.trace(k)
+    for v in range(M + 1):
+        assert np.array_equal(g.params_flat("param", v), o.params_flat("param", v).astype(np.float32)), v
+    g.close()
+    # CUDA-graph replay of steady-state calls with the overlap
+    g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, params=P, precision="fp32", graphs=True,
+              schedule=schedule, fb_overlap=True, watchdog_ms=20000)
+    o = oracle_mod.Oracle(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, P, mode="fp32", schedule=schedule)
+    xs, ys = S.make_inputs(12 * N, (784, 1, 1), 10, 3, kind="mnist")
+    reps = 0
+    for i in range(12):
+        g.step(xs[i * N:(i + 1) * N], ys[i * N:(i + 1) * N], 1, flush=(i == 11))
+        reps += g.last_stats.graph_replays
+    o.step(xs, ys, 12, flush=True)
+    assert np.array_equal(g.params_flat(), o.params_flat().astype(np.float32))
+    g.close()

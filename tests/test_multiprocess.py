@@ -58,7 +58,7 @@ def test_multiprocess_validation_without_gpu():
     assert e.value.code == -1
 
 
-def _ipc_worker(rank, world, port, q):
+def _ipc_worker(rank, world, port, q, overlap=False):
     sys.path.insert(0, ROOT)
     try:
         import torch
@@ -72,7 +72,7 @@ def _ipc_worker(rank, world, port, q):
         P = S.make_params(L, 1)
         x, y = S.make_inputs(10 * 32, (784, 1, 1), 10, 1, kind="mnist")
         g = XPipe(L, world, 4, 32, 1e-3, (0.9, 0.999), 1e-8, (784, 1, 1), 10, params=P, precision="fp32",
-                  trace=True, my_stage=rank, watchdog_ms=60000)
+                  trace=True, my_stage=rank, watchdog_ms=60000, fb_overlap=overlap)
         connect_pipeline(g)
         dist.barrier()
         g.step(x[:96], y[:96], 3)             # call splitting across processes too
@@ -87,7 +87,8 @@ def _ipc_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_two_process_pipeline_one_gpu(oracle_mod):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_two_process_pipeline_one_gpu(oracle_mod, overlap):
     """Two processes, one stage each, rings and flags shared through CUDA IPC on one B200:
     weights and traces bit-exact with the oracle's K=2 replay."""
     import torch.multiprocessing as mp
@@ -95,7 +96,7 @@ def test_two_process_pipeline_one_gpu(oracle_mod):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, overlap)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}

@@ -145,7 +145,7 @@ def cpu_baseline(workload, seconds=20.0):
 
 def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank, sched=None):
     """Bubble fraction of one traced call (single-process mode): 1 - sum_k busy_k / (K * span),
-    busy_k = device time of stage k's F/B ops (%globaltimer), next to the uniform-cost ideal
+    busy_k = device time covered by stage k's F/B ops (%globaltimer), next to the uniform-cost ideal
     (K-1)/(M*T+K-1) of SPEC S:397 / SURVEY A.3."""
     if mp_mode:
         return None
@@ -160,7 +160,20 @@ def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, 
     for k in range(K):
         tr = g.trace(k, timestamps=True)
         ops = [r for r in tr if r[1] in (0, 1)]
-        busy.append(sum(r[9] - r[8] for r in ops))
+        # busy time = the union of the stage's F/B intervals (with fb_overlap a forward and a
+        # backward of the stage run at the same time)
+        iv = sorted((r[8], r[9]) for r in ops)
+        tot, cur0, cur1 = 0, None, None
+        for a, b in iv:
+            if cur1 is None or a > cur1:
+                if cur1 is not None:
+                    tot += cur1 - cur0
+                cur0, cur1 = a, b
+            else:
+                cur1 = max(cur1, b)
+        if cur1 is not None:
+            tot += cur1 - cur0
+        busy.append(tot)
         t0s.append(min(r[8] for r in ops))
         t1s.append(max(r[9] for r in ops))
     g.close()

@@ -152,8 +152,11 @@ def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, 
     import synthetic as S
     import torch
     from paper_1911_04610_b200 import XPipe
+    # the schedule's bubble: one stream per stage (with fb_overlap a stage is two workers and the
+    # single-worker busy fraction no longer describes the schedule)
+    sched = {k: v for k, v in (sched or {}).items() if k != "fb_overlap"}
     g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
-              devices=list(range(args.gpus)), trace=True, watchdog_ms=300000, **(sched or {}))
+              devices=list(range(args.gpus)), trace=True, watchdog_ms=300000, **sched)
     x, y = S.make_inputs(M * N, shape, classes, 2, kind=kind)
     g.step(torch.from_numpy(x).cuda(0), torch.from_numpy(y).cuda((K - 1) % args.gpus), M, flush=True)
     busy, t0s, t1s = [], [], []
@@ -178,10 +181,11 @@ def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, 
         t1s.append(max(r[9] for r in ops))
     g.close()
     span = max(t1s) - min(t0s)
-    gp = (sched or {}).get("schedule") == "gpipe"
+    gp = sched.get("schedule") == "gpipe"
     ideal = (K - 1) / (T + K - 1) if gp else (K - 1) / (M * T + K - 1)  # SURVEY A.3 closed forms
     return {"bubble_fraction": 1.0 - sum(busy) / (K * span), "ideal_uniform": ideal,
-            "traced_minibatches": M, "note": "separate traced call with flush (trace kernels add overhead)"}
+            "traced_minibatches": M,
+            "note": "separate traced call with flush, one stream per stage (trace kernels add overhead)"}
 
 
 def run_reference(args):

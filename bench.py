@@ -283,7 +283,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="vgg16", choices=["vgg16", "mlp", "resnet101", "inception", "sweep"])
-    ap.add_argument("--minibatches", type=int, default=4, help="mini-batches fed per step")
+    ap.add_argument("--minibatches", type=int, default=16,
+                    help="mini-batches fed per step, i.e. per xpipe_step call; a call starts from the "
+                         "previous call's completed work, so fewer, larger calls amortise that drain "
+                         "(4 -> 16 per call measured +3%%)")
     ap.add_argument("--stages", type=int, default=0,
                     help="pipeline stages (default: the BASELINE config's -- VGG-16 4, MLP 2 -- on one GPU, "
                          "else one per GPU)")

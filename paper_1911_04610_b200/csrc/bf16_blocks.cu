@@ -54,8 +54,16 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
       // without split-K the GEMM epilogue also emits the BN partials of its 128-row tiles
       int bn_tiles = 0;
       XP_TRY(prof_begin(c, s));
-      XP_TRY(check_launch(c, tc_conv_fprop(g, x, W + L.woff, mid, s.ws, s.ws_elems, s.ctr, s.stream, s.bnws, &bn_tiles),
-                          "conv_fprop"));
+      if (o < (int)s.cols.size() && !s.cols[o].empty()) {  // few input channels: explicit im2col + dense GEMM
+        bf16* cols = (bf16*)s.cols[o][slot];
+        XP_TRY(check_launch(c, launch_im2col_bf16(x, cols, n, g.H, g.W, g.C, g.P, g.Q, g.R, g.S, g.sh, g.sw, g.ph,
+                                                  g.pw, s.stream), "im2col"));
+        XP_TRY(check_launch(c, tc_im2col_fprop(g, cols, W + L.woff, mid, s.ws, s.ws_elems, s.ctr, s.stream, s.bnws,
+                                               &bn_tiles), "conv_fprop"));
+      } else {
+        XP_TRY(check_launch(c, tc_conv_fprop(g, x, W + L.woff, mid, s.ws, s.ws_elems, s.ctr, s.stream, s.bnws,
+                                             &bn_tiles), "conv_fprop"));
+      }
       XP_TRY(prof_end(c, s, XP_PROF_CONV_FPROP, conv_flops(g, L.in0.c)));
       const LayerInfo& N = c->net.layers[O.lbn];
       const int M = n * O.smid.h * O.smid.w;
@@ -147,8 +155,12 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       XP_CUDA(c, cudaEventRecord(s.ev_fork, s.stream));
       XP_CUDA(c, cudaStreamWaitEvent(s.side, s.ev_fork, 0));
       XP_TRY(prof_begin(c, s, s.side));
-      XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)s.act[O.in0][slot], dmid, s.g + L.woff, accumulate_g,
-                                           s.ws_side, s.ws_elems, s.ctr_side, s.side), "conv_wgrad"));
+      if (o < (int)s.cols.size() && !s.cols[o].empty())
+        XP_TRY(check_launch(c, tc_im2col_wgrad(g, (const bf16*)s.cols[o][slot], dmid, s.g + L.woff, accumulate_g,
+                                               s.ws_side, s.ws_elems, s.ctr_side, s.side), "conv_wgrad"));
+      else
+        XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)s.act[O.in0][slot], dmid, s.g + L.woff, accumulate_g,
+                                             s.ws_side, s.ws_elems, s.ctr_side, s.side), "conv_wgrad"));
       XP_TRY(prof_end(c, s, XP_PROF_CONV_WGRAD, conv_flops(g, L.in0.c), s.side));
       XP_CUDA(c, cudaEventRecord(s.ev_gdone[b], s.side));
       s.gdone_valid[b] = true;

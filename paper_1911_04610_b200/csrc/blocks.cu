@@ -16,6 +16,12 @@ bool is_bf16(const xpipe_ctx* c) { return c->cfg.precision == XP_BF16; }
 // Device memory of one stage: the flat parameter arena (W, g, m, v fp32 + W_hat_f[2] and
 // W_hat_b), the version/scalar state, the four ring flags, the input and gradient rings and
 // one stash set per in-flight micro-batch.
+// development switch: XPIPE_NO_IM2COL=1 runs few-channel convs through the cp.async gather
+static bool no_im2col() {
+  static const bool v = [] { const char* e = getenv("XPIPE_NO_IM2COL"); return e && *e && *e != '0'; }();
+  return v;
+}
+
 int allocate_stage(xpipe_ctx* c, StageRT& s) {
   const StagePlan& p = s.plan;
   const bool bf = is_bf16(c);
@@ -70,6 +76,13 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
     s.stats[o].resize(s.S);
     for (auto& q : s.mid[o]) if (!(q = A((size_t)n * O.smid.size() * 2))) return set_err(c, XP_ENOMEM, "stash");
     for (auto& q : s.stats[o]) if (!(q = (float*)A((size_t)O.smid.c * 4 * 4))) return set_err(c, XP_ENOMEM, "stash");
+    const LayerInfo& LC = c->net.layers[O.lmain];
+    if (LC.cin_pad < 64 && !no_im2col()) {  // too few channels for the TMA pixel boxes: im2col
+      if (s.cols.size() < p.ops.size()) s.cols.assign(p.ops.size(), {});
+      s.cols[o].resize(s.S);
+      const size_t cb = (size_t)n * O.smid.h * O.smid.w * LC.d.kh * LC.d.kw * LC.cin_pad * 2;
+      for (auto& q : s.cols[o]) if (!(q = A(cb))) return set_err(c, XP_ENOMEM, "im2col");
+    }
     if (O.lpool >= 0) {
       s.pidx[o].resize(s.S);
       for (auto& q : s.pidx[o]) if (!(q = (uint8_t*)A((size_t)n * O.sout.size()))) return set_err(c, XP_ENOMEM, "stash");

@@ -494,6 +494,36 @@ int grid1d(int64_t n, int threads = 256) {
 
 }  // namespace
 
+// explicit im2col of a conv input with few channels (C % 8 == 0, C < 64): cols[m][(r*S+s)*C + c]
+// = x[n][p*sh-ph+r][q*sw-pw+s][c] (zero outside), m = (n*P + p)*Q + q; 8 channels per thread
+__global__ void im2col_bf16_kernel(const bf16* __restrict__ x, bf16* __restrict__ cols, int n, int H, int W, int C,
+                                   int P, int Q, int R, int S, int sh, int sw, int ph, int pw) {
+  pdl_wait();
+  const int G = C / 8, taps = R * S;
+  const int64_t total = (int64_t)n * P * Q * taps * G;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    int64_t r0 = i / G;
+    const int tap = (int)(r0 % taps);
+    const int64_t m = r0 / taps;
+    const int q = (int)(m % Q), t = (int)(m / Q), p = t % P, s_img = t / P;
+    const int r = tap / S, s = tap - r * S;
+    const int ih = p * sh - ph + r, iw = q * sw - pw + s;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (ih >= 0 && ih < H && iw >= 0 && iw < W)
+      v = *reinterpret_cast<const uint4*>(x + (((int64_t)s_img * H + ih) * W + iw) * C + g * 8);
+    *reinterpret_cast<uint4*>(cols + m * (int64_t)taps * C + tap * C + g * 8) = v;
+  }
+}
+
+cudaError_t launch_im2col_bf16(const bf16* x, bf16* cols, int n, int H, int W, int C, int P, int Q, int R, int S,
+                               int sh, int sw, int ph, int pw, cudaStream_t st) {
+  if (C % 8) return cudaErrorInvalidValue;
+  launch_pdl(im2col_bf16_kernel, dim3(grid1d((int64_t)n * P * Q * R * S * (C / 8))), dim3(256), 0, st, x, cols, n, H, W,
+             C, P, Q, R, S, sh, sw, ph, pw);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stage_input_bf16(const float* x, bf16* y, int n, int C, int H, int W, int Cp, cudaStream_t st) {
   launch_pdl(stage_input_bf16_kernel, dim3(grid1d((int64_t)n * H * W * Cp)), dim3(256), 0, st, x, y, n, C, H, W, Cp);
   return cudaGetLastError();

@@ -32,6 +32,9 @@ cudaError_t launch_bn_bwd_apply(const __nv_bfloat16* x, const __nv_bfloat16* dou
                                 const uint8_t* pidx, const float* stats, const __nv_bfloat16* gamma_b, int n, int H,
                                 int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,
                                 bool relu, const float* ws, __nv_bfloat16* dx, cudaStream_t st);
+// explicit im2col of an NHWC conv input (C % 8 == 0): cols [n*P*Q][R*S*C], (r, s, c) c fastest
+cudaError_t launch_im2col_bf16(const __nv_bfloat16* x, __nv_bfloat16* cols, int n, int H, int W, int C, int P, int Q,
+                               int R, int S, int sh, int sw, int ph, int pw, cudaStream_t st);
 cudaError_t launch_linear_fwd_bf16(const __nv_bfloat16* x, const __nv_bfloat16* W, const __nv_bfloat16* b, void* y,
                                    int n, int in, int out, bool relu, bool f32out, cudaStream_t st);
 cudaError_t launch_linear_dgrad_bf16(const void* dy, bool dy_f32, const __nv_bfloat16* mask, const __nv_bfloat16* W,

@@ -779,7 +779,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
             for (int e = 0; e < 32; ++e) v[e] = 0u;
           }
           if (w.n0 + c0 < a.N) epi_store(a, row, w.n0 + c0, v);
-          if (MODE == GEMM_FPROP && a.bn_part && w.n0 + c0 < a.N) {
+          if ((MODE == GEMM_FPROP || MODE == GEMM_PLAIN) && a.bn_part && w.n0 + c0 < a.N) {
             // BatchNorm partials of this tile's 32 columns over its valid rows, from the stored
             // (bf16-rounded) values: tile mean, then the sum of squared deviations (two passes;
             // the second re-reads the accumulator from TMEM), fixed-order reductions
@@ -1072,7 +1072,7 @@ template <int MODE, bool A_MN>
 void setup_a_tma(GemmArgs& a, CUtensorMap* m) {
   a.a_tma = 0;
   if (MODE == GEMM_PLAIN) {  // development: both operands of the unit GEMM by TMA
-    if (!plain_tma() || !a.b_tma) return;
+    if (!(plain_tma() || a.force_tma) || !a.b_tma) return;
     if (A_MN) {  // A [K][M]
       const uint64_t dims[2] = {(uint64_t)a.M, (uint64_t)a.K}, str[1] = {(uint64_t)a.lda * 2};
       const uint32_t box[2] = {64, 64};
@@ -1315,6 +1315,30 @@ cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const bf16* dY, const bf16* 
   a.g = g; a.A = dY; a.B = Wt;
   a.M = g.Nimg * g.H * g.W; a.N = Cx; a.K = g.R * g.S * g.Co;
   return run_split<GEMM_DGRAD, false, true>(a, EPI_BF16, dX, Cx, accumulate ? 1 : 0, ws, ws_elems, counters, st);
+}
+
+cudaError_t tc_im2col_fprop(const ConvGeo& g, const bf16* cols, const bf16* Wt, bf16* Y, float* ws, int64_t ws_elems,
+                            int* counters, cudaStream_t st, float* bn_part, int* bn_tiles) {
+  GemmArgs a{};
+  a.g = g; a.A = cols; a.B = Wt;
+  a.M = g.Nimg * g.P * g.Q; a.N = g.Co; a.K = g.R * g.S * g.C;
+  a.lda = a.K; a.ldb = a.K;
+  a.force_tma = 1;
+  const SplitPlan sp = plan_splits(a.M, a.N, a.K);
+  const bool fused_bn = bn_part && sp.cs * sp.nc <= 1;
+  a.bn_part = fused_bn ? bn_part : nullptr;
+  if (bn_tiles) *bn_tiles = fused_bn ? (a.M + BM - 1) / BM : 0;
+  return run_split<GEMM_PLAIN, false, false>(a, EPI_BF16, Y, g.Co, 0, ws, ws_elems, counters, st);
+}
+
+cudaError_t tc_im2col_wgrad(const ConvGeo& g, const bf16* cols, const bf16* dY, float* gW, bool accumulate, float* ws,
+                            int64_t ws_elems, int* counters, cudaStream_t st) {
+  GemmArgs a{};
+  a.g = g; a.A = cols; a.B = dY;
+  a.M = g.R * g.S * g.C; a.N = g.Co; a.K = g.Nimg * g.P * g.Q;
+  a.lda = a.M; a.ldb = g.Co;  // both MN-major: cols [pixels][R*S*C], dY [pixels][Co]
+  a.force_tma = 1;
+  return run_split<GEMM_PLAIN, true, true>(a, EPI_WGRAD_T, gW, a.M, accumulate ? 1 : 0, ws, ws_elems, counters, st);
 }
 
 cudaError_t tc_conv_wgrad(const ConvGeo& g, const bf16* X, const bf16* dY, float* gW, bool accumulate, float* ws,

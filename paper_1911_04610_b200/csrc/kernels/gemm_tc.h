@@ -53,6 +53,7 @@ struct GemmArgs {
   // 128-row tile of the stored (bf16-rounded) output, bn_part[mtile][0][co] = tile mean and
   // bn_part[mtile][1][co] = sum of squared deviations (rows < M only), or null
   float* bn_part;
+  int force_tma;            // PLAIN: stream both operands by TMA (the im2col'd first layer)
   unsigned long long* dbg;  // development timing probe (XPIPE_GEMM_DBG), else null
   int dev_flags;            // development experiments (XPIPE_GEMM_DEV), 0 in production
 };
@@ -77,6 +78,15 @@ cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const __nv_bfloat16* dY, con
 // gW [Co][R][S][C] fp32 (=|+=) sum over pixels of dY x im2col(X)
 cudaError_t tc_conv_wgrad(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* dY, float* gW, bool accumulate,
                           float* ws, int64_t ws_elems, int* counters, cudaStream_t st);
+// A conv whose input channels are too few for the TMA pixel-box path (C % 64 != 0, the
+// network's first layer) runs on an explicit im2col matrix cols [Nimg*P*Q][R*S*C] (bf16,
+// (r, s, c) with c fastest -- the weight layout): fprop = cols . W^T (+ the fused BN partials),
+// wgrad: g (=|+=) (cols^T . dY)^T, both dense GEMMs with TMA-fed operands.
+cudaError_t tc_im2col_fprop(const ConvGeo& g, const __nv_bfloat16* cols, const __nv_bfloat16* Wt, __nv_bfloat16* Y,
+                            float* ws, int64_t ws_elems, int* counters, cudaStream_t st, float* bn_part,
+                            int* bn_tiles);
+cudaError_t tc_im2col_wgrad(const ConvGeo& g, const __nv_bfloat16* cols, const __nv_bfloat16* dY, float* gW,
+                            bool accumulate, float* ws, int64_t ws_elems, int* counters, cudaStream_t st);
 // workspace (floats) the launchers above can use profitably for split-K
 int64_t tc_conv_ws_elems(const ConvGeo& g);
 

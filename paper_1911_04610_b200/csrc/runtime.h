@@ -81,6 +81,7 @@ struct StageRT {
   float* ws = nullptr;                  // split-K workspace (fp32)
   int64_t ws_elems = 0;
   float* bnws = nullptr;                // BatchNorm partial-reduction workspace
+  std::vector<std::vector<void*>> cols; // per op, per slot: im2col of a few-channel conv input
   int* ctr = nullptr;                   // split-K arrival counters of this stage's stream
   // host program state
   int64_t pos = 0;

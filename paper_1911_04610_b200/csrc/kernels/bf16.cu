@@ -21,6 +21,28 @@ typedef __nv_bfloat16 bf16;
 
 __device__ __forceinline__ float q16(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 
+// 8 consecutive per-channel constants (c0 % 8 == 0): two 16-byte loads where aligned
+__device__ __forceinline__ void ld8f(const float* __restrict__ p, float (&v)[8]) {
+  if (((uintptr_t)p & 15) == 0) {
+    const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = p[e];
+  }
+}
+__device__ __forceinline__ void ld8bf(const __nv_bfloat16* __restrict__ p, float (&v)[8]) {
+  if (((uintptr_t)p & 15) == 0) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = __bfloat162float(b[e]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = __bfloat162float(p[e]);
+  }
+}
+
 // The BN-apply + ReLU of one element, bit-identical wherever it is (re)computed:
 // a = Q(relu(gamma * ((x - mean) * rstd) + beta))
 __device__ __forceinline__ float bn_act(float x, float mean, float rstd, float gamma, float beta, int relu) {
@@ -206,11 +228,9 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
     const int c0 = g * 8;
     float mean[8], rstd[8], ga[8], be[8], best[8];
     int arg[8];
+    ld8f(st + c0, mean); ld8f(st + C + c0, rstd); ld8f(st + 2 * C + c0, ga); ld8f(st + 3 * C + c0, be);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      mean[e] = st[c0 + e]; rstd[e] = st[C + c0 + e]; ga[e] = st[2 * C + c0 + e]; be[e] = st[3 * C + c0 + e];
-      best[e] = 0.f; arg[e] = 0;
-    }
+    for (int e = 0; e < 8; ++e) { best[e] = 0.f; arg[e] = 0; }
     if (!pool) {
       const uint4 u = *reinterpret_cast<const uint4*>(x + (((int64_t)s * H + p) * W + q) * C + c0);
       const bf16* v = reinterpret_cast<const bf16*>(&u);
@@ -311,8 +331,9 @@ __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __r
   const int c0 = g * 8;
   const int r0 = blockIdx.x * RC, r1 = min(M, r0 + RC);
   float s1[8], s2[8], mean[8], rstd[8];
+  ld8f(st + c0, mean); ld8f(st + C + c0, rstd);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) { s1[e] = 0.f; s2[e] = 0.f; mean[e] = st[c0 + e]; rstd[e] = st[C + c0 + e]; }
+  for (int e = 0; e < 8; ++e) { s1[e] = 0.f; s2[e] = 0.f; }
 #pragma unroll
   for (int k = 0; k < kBnRows; ++k) {  // RC <= kBnRows*RL: every row of the lane, loads in flight together
     const int r = r0 + rl + k * RL;
@@ -402,18 +423,18 @@ __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __re
     routed_dy8(dout, y, pidx, G, sidx, h, w, c0, dy);
     const uint4 ux = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + c0);
     const bf16* xv = reinterpret_cast<const bf16*>(&ux);
+    float mean[8], rstd[8], gb[8], t1[8], t2[8];
+    ld8f(st + c0, mean); ld8f(st + C + c0, rstd); ld8bf(gamma_b + c0, gb); ld8f(tot + c0, t1); ld8f(tot + C + c0, t2);
     uint32_t o4[4];
 #pragma unroll
     for (int e2 = 0; e2 < 4; ++e2) {
       float v2[2];
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const int e = 2 * e2 + q, c = c0 + e;
-        const float mean = st[c], rstd = st[C + c];
-        const float xh = __fmul_rn(__fsub_rn(__bfloat162float(xv[e]), mean), rstd);
-        const float gb = __bfloat162float(gamma_b[c]);
-        v2[q] = __fmul_rn(__fmul_rn(gb, rstd), __fsub_rn(__fsub_rn(dy[e], __fmul_rn(tot[c], inv_cnt)),
-                                                          __fmul_rn(xh, __fmul_rn(tot[C + c], inv_cnt))));
+        const int e = 2 * e2 + q;
+        const float xh = __fmul_rn(__fsub_rn(__bfloat162float(xv[e]), mean[e]), rstd[e]);
+        v2[q] = __fmul_rn(__fmul_rn(gb[e], rstd[e]), __fsub_rn(__fsub_rn(dy[e], __fmul_rn(t1[e], inv_cnt)),
+                                                              __fmul_rn(xh, __fmul_rn(t2[e], inv_cnt))));
       }
       __nv_bfloat162 t2 = __floats2bfloat162_rn(v2[0], v2[1]);
       o4[e2] = *reinterpret_cast<uint32_t*>(&t2);

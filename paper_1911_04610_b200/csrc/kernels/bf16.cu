@@ -55,14 +55,14 @@ __device__ __forceinline__ float bn_act(float x, float mean, float rstd, float g
 __global__ void stage_input_bf16_kernel(const float* __restrict__ x, bf16* __restrict__ y, int n, int C, int H, int W,
                                         int Cp) {
   pdl_wait();
-  const int64_t total = (int64_t)n * H * W * Cp;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % Cp);
-    int64_t r = i / Cp;
-    const int w = (int)(r % W);
+  const int total = n * H * W * Cp;  // < 2^30 (checked at launch): 32-bit index arithmetic
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c = i % Cp;
+    int r = i / Cp;
+    const int w = r % W;
     r /= W;
-    const int h = (int)(r % H);
-    const int s = (int)(r / H);
+    const int h = r % H;
+    const int s = r / H;
     const float v = c < C ? x[(((int64_t)s * C + c) * H + h) * W + w] : 0.f;
     y[i] = __float2bfloat16_rn(v);
   }
@@ -217,14 +217,14 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
                                 int sh, int sw, int ph, int pw, int pool, int relu) {
   pdl_wait();
   const int G = C / 8;
-  const int64_t total = (int64_t)n * P * Q * G;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int g = (int)(i % G);
-    int64_t r = i / G;
-    const int q = (int)(r % Q);
+  const int total = n * P * Q * G;  // < 2^30 (checked at launch): 32-bit index arithmetic
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % G;
+    int r = i / G;
+    const int q = r % Q;
     r /= Q;
-    const int p = (int)(r % P);
-    const int s = (int)(r / P);
+    const int p = r % P;
+    const int s = r / P;
     const int c0 = g * 8;
     float mean[8], rstd[8], ga[8], be[8], best[8];
     int arg[8];
@@ -413,10 +413,10 @@ __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __re
   pdl_wait();
   const int C = G.C, NG = C / 8;
   const float inv_cnt = 1.f / (float)M;
-  const int64_t total = (int64_t)M * NG;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int g = (int)(i % NG);
-    const int r = (int)(i / NG);
+  const int total = M * NG;  // < 2^30 (checked at launch): 32-bit index arithmetic
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % NG;
+    const int r = i / NG;
     const int c0 = g * 8;
     const int w = r % G.W, t = r / G.W, h = t % G.H, sidx = t / G.H;
     float dy[8];
@@ -504,6 +504,9 @@ __global__ void linear_wgrad_bf16_kernel(const void* __restrict__ dy, const bf16
   *dst = accumulate ? __fadd_rn(*dst, acc) : acc;
 }
 
+// element-count bound of the 32-bit-indexed elementwise kernels (index + grid stride < 2^31)
+constexpr int64_t kMaxElems = int64_t(1) << 30;
+
 int grid1d(int64_t n, int threads = 256) {
   static const int cap = [] {  // development knob: CTA cap of the elementwise kernels
     const char* e = getenv("XPIPE_EW_CTAS");
@@ -521,31 +524,32 @@ __global__ void im2col_bf16_kernel(const bf16* __restrict__ x, bf16* __restrict_
                                    int P, int Q, int R, int S, int sh, int sw, int ph, int pw) {
   pdl_wait();
   const int G = C / 8, taps = R * S;
-  const int64_t total = (int64_t)n * P * Q * taps * G;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int g = (int)(i % G);
-    int64_t r0 = i / G;
-    const int tap = (int)(r0 % taps);
-    const int64_t m = r0 / taps;
-    const int q = (int)(m % Q), t = (int)(m / Q), p = t % P, s_img = t / P;
+  const int total = n * P * Q * taps * G;  // < 2^30 (checked at launch): 32-bit index arithmetic
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % G;
+    const int r0 = i / G;
+    const int tap = r0 % taps;
+    const int m = r0 / taps;
+    const int q = m % Q, t = m / Q, p = t % P, s_img = t / P;
     const int r = tap / S, s = tap - r * S;
     const int ih = p * sh - ph + r, iw = q * sw - pw + s;
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
     if (ih >= 0 && ih < H && iw >= 0 && iw < W)
       v = *reinterpret_cast<const uint4*>(x + (((int64_t)s_img * H + ih) * W + iw) * C + g * 8);
-    *reinterpret_cast<uint4*>(cols + m * (int64_t)taps * C + tap * C + g * 8) = v;
+    *reinterpret_cast<uint4*>(cols + (int64_t)m * taps * C + tap * C + g * 8) = v;
   }
 }
 
 cudaError_t launch_im2col_bf16(const bf16* x, bf16* cols, int n, int H, int W, int C, int P, int Q, int R, int S,
                                int sh, int sw, int ph, int pw, cudaStream_t st) {
-  if (C % 8) return cudaErrorInvalidValue;
+  if (C % 8 || (int64_t)n * P * Q * R * S * (C / 8) >= kMaxElems) return cudaErrorInvalidValue;
   launch_pdl(im2col_bf16_kernel, dim3(grid1d((int64_t)n * P * Q * R * S * (C / 8))), dim3(256), 0, st, x, cols, n, H, W,
              C, P, Q, R, S, sh, sw, ph, pw);
   return cudaGetLastError();
 }
 
 cudaError_t launch_stage_input_bf16(const float* x, bf16* y, int n, int C, int H, int W, int Cp, cudaStream_t st) {
+  if ((int64_t)n * H * W * Cp >= kMaxElems) return cudaErrorInvalidValue;
   launch_pdl(stage_input_bf16_kernel, dim3(grid1d((int64_t)n * H * W * Cp)), dim3(256), 0, st, x, y, n, C, H, W, Cp);
   return cudaGetLastError();
 }
@@ -589,6 +593,7 @@ cudaError_t launch_bn_stats_final(const float* part, int chunks, int M, int RC, 
 cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, uint8_t* pidx, int n, int H, int W, int C, int P,
                             int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st) {
   const int64_t total = (int64_t)n * P * Q * (C / 8);
+  if (C % 8 || total >= kMaxElems) return cudaErrorInvalidValue;
   launch_pdl(bn_apply_kernel, dim3(grid1d(total)), dim3(256), 0, st, x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
                                                  pool ? 1 : 0, relu ? 1 : 0);
   return cudaGetLastError();
@@ -619,6 +624,7 @@ cudaError_t launch_bn_bwd_apply(const bf16* x, const bf16* dout, const bf16* y, 
   BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
   const int M = n * H * W;
   const float* tot = ws + (size_t)bn_chunks(M, C) * 2 * C;
+  if ((int64_t)M * (C / 8) >= kMaxElems) return cudaErrorInvalidValue;
   launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats, tot,
              gamma_b, G, M, dx);
   return cudaGetLastError();

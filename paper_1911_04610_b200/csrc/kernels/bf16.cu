@@ -275,12 +275,12 @@ struct BwdGeo {
 };
 
 __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const bf16* __restrict__ y,
-                                           const uint8_t* __restrict__ pidx, const BwdGeo& G, int s, int h, int w,
-                                           int c0, float (&dy)[8]) {
+                                           const uint8_t* __restrict__ pidx, const BwdGeo& G, int row, int c0,
+                                           float (&dy)[8]) {
 #pragma unroll
   for (int e = 0; e < 8; ++e) dy[e] = 0.f;
-  if (!G.pool) {
-    const int64_t o = (((int64_t)s * G.H + h) * G.W + w) * G.C + c0;
+  if (!G.pool) {  // row = (s*H + h)*W + w indexes dout/y directly
+    const int64_t o = (int64_t)row * G.C + c0;
     const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
     const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
     const bf16* d = reinterpret_cast<const bf16*>(&ud);
@@ -289,6 +289,7 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
     for (int e = 0; e < 8; ++e) dy[e] = (G.relu && !(__bfloat162float(yy[e]) > 0.f)) ? 0.f : __bfloat162float(d[e]);
     return;
   }
+  const int w = row % G.W, t = row / G.W, h = t % G.H, s = t / G.H;
   const int plo = max(0, (h + G.ph - G.kh + G.sh) / G.sh), phi = min(G.P - 1, (h + G.ph) / G.sh);
   const int qlo = max(0, (w + G.pw - G.kw + G.sw) / G.sw), qhi = min(G.Q - 1, (w + G.pw) / G.sw);
   int hits[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -338,9 +339,8 @@ __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __r
   for (int k = 0; k < kBnRows; ++k) {  // RC <= kBnRows*RL: every row of the lane, loads in flight together
     const int r = r0 + rl + k * RL;
     if (rl < RL && r < r1) {
-      const int w = r % G.W, t = r / G.W, h = t % G.H, sidx = t / G.H;
       float dy[8];
-      routed_dy8(dout, y, pidx, G, sidx, h, w, c0, dy);
+      routed_dy8(dout, y, pidx, G, r, c0, dy);
       const uint4 ux = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + c0);
       const bf16* xv = reinterpret_cast<const bf16*>(&ux);
 #pragma unroll
@@ -418,9 +418,8 @@ __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __re
     const int g = i % NG;
     const int r = i / NG;
     const int c0 = g * 8;
-    const int w = r % G.W, t = r / G.W, h = t % G.H, sidx = t / G.H;
     float dy[8];
-    routed_dy8(dout, y, pidx, G, sidx, h, w, c0, dy);
+    routed_dy8(dout, y, pidx, G, r, c0, dy);
     const uint4 ux = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + c0);
     const bf16* xv = reinterpret_cast<const bf16*>(&ux);
     float mean[8], rstd[8], gb[8], t1[8], t2[8];

@@ -442,6 +442,64 @@ __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __re
   }
 }
 
+// Pooled layers whose windows tile the map exactly (kh == sh, kw == sw, no padding, H = P*kh,
+// W = Q*kw): one thread per (pooled output, 8 channels) -- the routed gradient, winner index and
+// ReLU mask are loaded once for the kh*kw inputs of the window; per element the arithmetic is
+// bn_bwd_apply_kernel's (every input lies in exactly one window, so no Q() of a fan-in sum).
+__global__ void bn_bwd_apply_tiled_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                          const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
+                                          const float* __restrict__ st, const float* __restrict__ tot,
+                                          const bf16* __restrict__ gamma_b, BwdGeo G, int M, int Mo,
+                                          bf16* __restrict__ dx) {
+  pdl_wait();
+  const int C = G.C, NG = C / 8;
+  const float inv_cnt = 1.f / (float)M;
+  const int total = Mo * NG;  // < 2^30 (checked at launch)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % NG, ro = i / NG;
+    const int q = ro % G.Q, t = ro / G.Q, p = t % G.P, s = t / G.P;
+    const int c0 = g * 8;
+    const int64_t o = (int64_t)ro * C + c0;
+    const uint2 ui = *reinterpret_cast<const uint2*>(pidx + o);
+    const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
+    const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
+    const bf16* d = reinterpret_cast<const bf16*>(&ud);
+    const bf16* yy = reinterpret_cast<const bf16*>(&uy);
+    float gv[8];
+    int win[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      win[e] = (int)(((e < 4 ? ui.x : ui.y) >> (8 * (e & 3))) & 0xFF);
+      gv[e] = (G.relu && !(__bfloat162float(yy[e]) > 0.f)) ? 0.f : __bfloat162float(d[e]);
+    }
+    float mean[8], rstd[8], gb[8], t1[8], t2[8];
+    ld8f(st + c0, mean); ld8f(st + C + c0, rstd); ld8bf(gamma_b + c0, gb); ld8f(tot + c0, t1); ld8f(tot + C + c0, t2);
+    for (int a = 0; a < G.kh; ++a)
+      for (int b = 0; b < G.kw; ++b) {
+        const int pos = a * G.kw + b;
+        const int64_t r = ((int64_t)s * G.H + p * G.kh + a) * G.W + q * G.kw + b;
+        const uint4 ux = *reinterpret_cast<const uint4*>(x + r * C + c0);
+        const bf16* xv = reinterpret_cast<const bf16*>(&ux);
+        uint32_t o4[4];
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+          float v2[2];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int e = 2 * e2 + h2;
+            const float dy = win[e] == pos ? gv[e] : 0.f;
+            const float xh = __fmul_rn(__fsub_rn(__bfloat162float(xv[e]), mean[e]), rstd[e]);
+            v2[h2] = __fmul_rn(__fmul_rn(gb[e], rstd[e]), __fsub_rn(__fsub_rn(dy, __fmul_rn(t1[e], inv_cnt)),
+                                                                    __fmul_rn(xh, __fmul_rn(t2[e], inv_cnt))));
+          }
+          __nv_bfloat162 t2v = __floats2bfloat162_rn(v2[0], v2[1]);
+          o4[e2] = *reinterpret_cast<uint32_t*>(&t2v);
+        }
+        *reinterpret_cast<uint4*>(dx + r * C + c0) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+      }
+  }
+}
+
 // ---- bf16-operand Linear (small: micro-batch rows) ------------------------------------------
 // y[r][o] = sum_i x[r][i] W[o][i] (fp32) + b[o]; logits: fp32 out, else Q(relu?) bf16.
 // One warp per (r, o); lanes stride over i, shuffle reduction.
@@ -501,6 +559,12 @@ __global__ void linear_wgrad_bf16_kernel(const void* __restrict__ dy, const bf16
   }
   float* dst = i < in ? &gW[(int64_t)o * in + i] : &gb[o];
   *dst = accumulate ? __fadd_rn(*dst, acc) : acc;
+}
+
+// development switch: XPIPE_NO_BN_TILED=1 keeps the per-input-element pooled BN backward
+bool bn_tiled_off() {
+  static const bool v = [] { const char* e = getenv("XPIPE_NO_BN_TILED"); return e && *e && *e != '0'; }();
+  return v;
 }
 
 // element-count bound of the 32-bit-indexed elementwise kernels (index + grid stride < 2^31)
@@ -624,6 +688,13 @@ cudaError_t launch_bn_bwd_apply(const bf16* x, const bf16* dout, const bf16* y, 
   const int M = n * H * W;
   const float* tot = ws + (size_t)bn_chunks(M, C) * 2 * C;
   if ((int64_t)M * (C / 8) >= kMaxElems) return cudaErrorInvalidValue;
+  if (pool && kh == sh && kw == sw && ph == 0 && pw == 0 && H == P * kh && W == Q * kw && kh * kw <= 255 &&
+      !bn_tiled_off()) {
+    const int Mo = n * P * Q;
+    launch_pdl(bn_bwd_apply_tiled_kernel, dim3(grid1d((int64_t)Mo * (C / 8))), dim3(256), 0, st, x, dout, y, pidx,
+               stats, tot, gamma_b, G, M, Mo, dx);
+    return cudaGetLastError();
+  }
   launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats, tot,
              gamma_b, G, M, dx);
   return cudaGetLastError();

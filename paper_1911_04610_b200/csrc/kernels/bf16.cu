@@ -290,6 +290,22 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
     return;
   }
   const int w = row % G.W, t = row / G.W, h = t % G.H, s = t / G.H;
+  if (G.pool == 2) {  // windows tile the map exactly: the one window holding (h, w)
+    const int p = h / G.kh, q = w / G.kw;
+    const int pos = (h - p * G.kh) * G.kw + (w - q * G.kw);
+    const int64_t o = (((int64_t)s * G.P + p) * G.Q + q) * G.C + c0;
+    const uint2 ui = *reinterpret_cast<const uint2*>(pidx + o);
+    const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
+    const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
+    const bf16* d = reinterpret_cast<const bf16*>(&ud);
+    const bf16* yy = reinterpret_cast<const bf16*>(&uy);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int win = (int)(((e < 4 ? ui.x : ui.y) >> (8 * (e & 3))) & 0xFF);
+      if (win == pos && !(G.relu && !(__bfloat162float(yy[e]) > 0.f))) dy[e] = __bfloat162float(d[e]);
+    }
+    return;
+  }
   const int plo = max(0, (h + G.ph - G.kh + G.sh) / G.sh), phi = min(G.P - 1, (h + G.ph) / G.sh);
   const int qlo = max(0, (w + G.pw - G.kw + G.sw) / G.sw), qhi = min(G.Q - 1, (w + G.pw) / G.sw);
   int hits[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -668,6 +684,7 @@ cudaError_t launch_bn_bwd_reduce(const bf16* x, const bf16* dout, const bf16* y,
                                  bool accumulate, cudaStream_t st) {
   if (C % 8 || C > 2048) return cudaErrorInvalidValue;
   BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
+  if (pool && kh == sh && kw == sw && ph == 0 && pw == 0 && H == P * kh && W == Q * kw && !bn_tiled_off()) G.pool = 2;
   const int M = n * H * W;
   const int RC = bn_chunk_rows(M, C), chunks = bn_chunks(M, C);
   const int threads = bn_threads(C);

@@ -5,9 +5,9 @@ export PYTHONUNBUFFERED=1
 P=paper_1911_04610_b200
 for v in old new; do
   cp $P/libxpipe_$v.so $P/libxpipe.so
-  timeout 300 python scripts/params_dump.py $out/params_$v.npy > $out/dump_$v.log 2>&1
+  timeout 300 python scripts/params_dump.py /tmp/params_$v.npy > $out/dump_$v.log 2>&1
 done
-python -c "import numpy as np, sys; a, b = (np.load(sys.argv[i]) for i in (1, 2)); print('params bit-identical:', a.shape == b.shape and bool(np.array_equal(a, b)))" $out/params_old.npy $out/params_new.npy | tee -a $out/summary.txt
+python -c "import numpy as np, sys; a, b = (np.load(sys.argv[i]) for i in (1, 2)); print('params bit-identical:', a.shape == b.shape and bool(np.array_equal(a, b)))" /tmp/params_old.npy /tmp/params_new.npy | tee -a $out/summary.txt
 for rep in 1 2 3; do for v in old new; do for K in ${KS:-4 1}; do
   cp $P/libxpipe_$v.so $P/libxpipe.so
   timeout 300 python bench.py --steps 10 --warmup 3 --stages $K --no-cpu-baseline --no-e2e --no-sweep > $out/b.log 2>&1

@@ -1237,11 +1237,17 @@ cudaError_t launch_bn(const GemmArgs& a, int bn, int splits, cudaStream_t st) {
 // N tile: the widest tile whose grid still fills the SMs (a narrower tile gives more CTAs and
 // avoids split-K and its reduction pass); 64 when nothing fills them
 __host__ int bn_fill() { static const int v = getenv_int("XPIPE_BN_FILL", 148); return v; }
-// split-K only when the tile grid covers under a quarter of the SMs: with two CTAs per SM and
-// the other pipeline stages' kernels running concurrently, a split's reduction costs more than
-// the idle SMs it would fill (measured: threshold 74 -> 37 tiles, VGG-16 K=4 +5 %, K=1 equal;
-// 24 and below lose at K=1)
-__host__ int split_below() { static const int v = getenv_int("XPIPE_SPLIT_BELOW", num_sms() / 4); return v; }
+// split-K only when the tile grid covers under a quarter of the SMs (one pipeline stage on the
+// device), or under 3/16 of them when several stages share it: with two CTAs per SM and the
+// other stages' kernels running concurrently, a split's reduction costs more than the idle SMs
+// it would fill (measured, VGG-16: threshold 74 -> 37 tiles K=4 +5 %, K=1 equal; 37 -> 28 tiles
+// K=2 +3.8 %, K=4 +1.4 %, but K=1 -5 %)
+int g_coresident = 1;
+__host__ int split_below() {
+  static const int env = getenv_int("XPIPE_SPLIT_BELOW", 0);
+  if (env > 0) return env;
+  return g_coresident > 1 ? num_sms() * 3 / 16 : num_sms() / 4;
+}
 int choose_bn(int M, int N) {
   const int64_t mt = (M + 127) / 128;
   if (N > 128 && mt * ((N + 255) / 256) >= bn_fill()) return 256;
@@ -1283,6 +1289,8 @@ cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_
 }
 
 }  // namespace
+
+void tc_set_coresident_stages(int n) { g_coresident = n < 1 ? 1 : n; }
 
 cudaError_t tc_gemm_plain(const bf16* A, const bf16* B, float* D, int M, int N, int K, bool a_kmajor, bool b_kmajor,
                           int64_t ldd, cudaStream_t st) {

@@ -87,6 +87,9 @@ cudaError_t tc_im2col_fprop(const ConvGeo& g, const __nv_bfloat16* cols, const _
                             int* bn_tiles);
 cudaError_t tc_im2col_wgrad(const ConvGeo& g, const __nv_bfloat16* cols, const __nv_bfloat16* dY, float* gW,
                             bool accumulate, float* ws, int64_t ws_elems, int* counters, cudaStream_t st);
+// number of pipeline stages whose streams share this process's busiest device (sets the
+// split-K threshold; 1 = one stage per device)
+void tc_set_coresident_stages(int n);
 // workspace (floats) the launchers above can use profitably for split-K
 int64_t tc_conv_ws_elems(const ConvGeo& g);
 

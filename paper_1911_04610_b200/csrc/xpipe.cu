@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "../../include/xpipe.h"
+#include "kernels/gemm_tc.h"
 #include "runtime.h"
 
 using namespace xp;
@@ -791,6 +792,15 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
       else want = (want + T - 1) / T * T;
       s.S = want;
     }
+  }
+  {
+    int most = 1;
+    for (int k = 0; k < stages; ++k) {
+      int same = 0;
+      for (int q = 0; q < stages; ++q) same += c->S[q].dev == c->S[k].dev;
+      most = std::max(most, same);
+    }
+    tc_set_coresident_stages(c->cfg.serialize ? 1 : most);
   }
   // peer access between the devices of neighbouring stages (multi-process mode: lazily, by
   // cudaIpcOpenMemHandle)

@@ -800,7 +800,8 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
       for (int q = 0; q < stages; ++q) same += c->S[q].dev == c->S[k].dev;
       most = std::max(most, same);
     }
-    tc_set_coresident_stages(c->cfg.serialize ? 1 : most);
+    // multi-process mode: this process runs only its own stage
+    tc_set_coresident_stages(c->cfg.serialize || c->mp() ? 1 : most);
   }
   // peer access between the devices of neighbouring stages (multi-process mode: lazily, by
   // cudaIpcOpenMemHandle)

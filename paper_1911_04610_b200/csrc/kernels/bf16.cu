@@ -212,6 +212,9 @@ __global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks
 // ---- BN-apply [+ ReLU] [+ pool] ----------------------------------------------------------
 // y[n][p][q][c] = first max over the pool window (row-major scan) of bn_act(x[n][h][w][c]);
 // pidx[n][p][q][c] = the winner's position in the window (the backward routes through it)
+// PK = 2: pools whose 2x2 windows tile the map exactly (compile-time window, no bounds checks,
+// the four loads issued together); PK = 0: any window, runtime loop
+template <int PK>
 __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restrict__ st, bf16* __restrict__ y,
                                 uint8_t* __restrict__ pidx, int n, int H, int W, int C, int P, int Q, int kh, int kw,
                                 int sh, int sw, int ph, int pw, int pool, int relu) {
@@ -238,16 +241,19 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
       for (int e = 0; e < 8; ++e) best[e] = bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e], relu);
     } else {
       bool first = true;
-      for (int a = 0; a < kh; ++a)
-        for (int b = 0; b < kw; ++b) {
+      const int KH = PK ? PK : kh, KW = PK ? PK : kw;
+#pragma unroll
+      for (int a = 0; a < KH; ++a)
+#pragma unroll
+        for (int b = 0; b < KW; ++b) {
           const int hh = p * sh - ph + a, ww = q * sw - pw + b;
-          if (hh < 0 || hh >= H || ww < 0 || ww >= W) continue;
+          if (!PK && (hh < 0 || hh >= H || ww < 0 || ww >= W)) continue;
           const uint4 u = *reinterpret_cast<const uint4*>(x + (((int64_t)s * H + hh) * W + ww) * C + c0);
           const bf16* v = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const float t = bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e], relu);
-            if (first || t > best[e]) { best[e] = t; arg[e] = a * kw + b; }
+            if (first || t > best[e]) { best[e] = t; arg[e] = a * KW + b; }
           }
           first = false;
         }
@@ -462,6 +468,7 @@ __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __re
 // W = Q*kw): one thread per (pooled output, 8 channels) -- the routed gradient, winner index and
 // ReLU mask are loaded once for the kh*kw inputs of the window; per element the arithmetic is
 // bn_bwd_apply_kernel's (every input lies in exactly one window, so no Q() of a fan-in sum).
+template <int PK>  // 2: 2x2 windows (compile-time, unrolled), 0: runtime kh x kw
 __global__ void bn_bwd_apply_tiled_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
                                           const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
                                           const float* __restrict__ st, const float* __restrict__ tot,
@@ -490,10 +497,13 @@ __global__ void bn_bwd_apply_tiled_kernel(const bf16* __restrict__ x, const bf16
     }
     float mean[8], rstd[8], gb[8], t1[8], t2[8];
     ld8f(st + c0, mean); ld8f(st + C + c0, rstd); ld8bf(gamma_b + c0, gb); ld8f(tot + c0, t1); ld8f(tot + C + c0, t2);
-    for (int a = 0; a < G.kh; ++a)
-      for (int b = 0; b < G.kw; ++b) {
-        const int pos = a * G.kw + b;
-        const int64_t r = ((int64_t)s * G.H + p * G.kh + a) * G.W + q * G.kw + b;
+    const int KH = PK ? PK : G.kh, KW = PK ? PK : G.kw;
+#pragma unroll
+    for (int a = 0; a < KH; ++a)
+#pragma unroll
+      for (int b = 0; b < KW; ++b) {
+        const int pos = a * KW + b;
+        const int64_t r = ((int64_t)s * G.H + p * KH + a) * G.W + q * KW + b;
         const uint4 ux = *reinterpret_cast<const uint4*>(x + r * C + c0);
         const bf16* xv = reinterpret_cast<const bf16*>(&ux);
         uint32_t o4[4];
@@ -673,8 +683,13 @@ cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, uint8_t*
                             int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st) {
   const int64_t total = (int64_t)n * P * Q * (C / 8);
   if (C % 8 || total >= kMaxElems) return cudaErrorInvalidValue;
-  launch_pdl(bn_apply_kernel, dim3(grid1d(total)), dim3(256), 0, st, x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
-                                                 pool ? 1 : 0, relu ? 1 : 0);
+  if (pool && kh == 2 && kw == 2 && sh == 2 && sw == 2 && ph == 0 && pw == 0 && H == 2 * P && W == 2 * Q &&
+      !bn_tiled_off())
+    launch_pdl(bn_apply_kernel<2>, dim3(grid1d(total)), dim3(256), 0, st, x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh,
+               sw, ph, pw, 1, relu ? 1 : 0);
+  else
+    launch_pdl(bn_apply_kernel<0>, dim3(grid1d(total)), dim3(256), 0, st, x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh,
+               sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -708,8 +723,12 @@ cudaError_t launch_bn_bwd_apply(const bf16* x, const bf16* dout, const bf16* y, 
   if (pool && kh == sh && kw == sw && ph == 0 && pw == 0 && H == P * kh && W == Q * kw && kh * kw <= 255 &&
       !bn_tiled_off()) {
     const int Mo = n * P * Q;
-    launch_pdl(bn_bwd_apply_tiled_kernel, dim3(grid1d((int64_t)Mo * (C / 8))), dim3(256), 0, st, x, dout, y, pidx,
-               stats, tot, gamma_b, G, M, Mo, dx);
+    if (kh == 2 && kw == 2)
+      launch_pdl(bn_bwd_apply_tiled_kernel<2>, dim3(grid1d((int64_t)Mo * (C / 8))), dim3(256), 0, st, x, dout, y, pidx,
+                 stats, tot, gamma_b, G, M, Mo, dx);
+    else
+      launch_pdl(bn_bwd_apply_tiled_kernel<0>, dim3(grid1d((int64_t)Mo * (C / 8))), dim3(256), 0, st, x, dout, y, pidx,
+                 stats, tot, gamma_b, G, M, Mo, dx);
     return cudaGetLastError();
   }
   launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats, tot,

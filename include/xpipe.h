@@ -36,7 +36,8 @@ enum {
   XP_ECUDA = -3,         /* CUDA runtime/driver error (context poisoned) */
   XP_ECOMM = -4,         /* stage-to-stage transport error (context poisoned) */
   XP_ESCHED = -5,        /* schedule/cache violation or pipeline watchdog timeout (internal) */
-  XP_ENONFINITE = -6,    /* non-finite loss seen (only checked with cfg.trace) */
+  XP_ENONFINITE = -6,    /* non-finite loss seen by the loss kernel (device flag, read at the end of a
+                            synchronous xpipe_step; the context stays usable) */
   XP_ESTATE = -7,        /* context is poisoned */
   XP_EUNSUPPORTED = -8   /* valid request this build does not implement */
 };
@@ -61,8 +62,12 @@ enum { XP_MOM_ZERO = 0, XP_MOM_GIVEN = 1 /* cfg.init_m / cfg.init_v (e.g. 1e-4*U
    the prediction keeps its own Eq. (4) moments of the raw gradient and uses the
    literal Eq. (3)/(4) dW, so it requires delta_form = XP_DELTA_PAPER. */
 enum { XP_OPT_ADAM = 0, XP_OPT_MOMENTUM_SGD = 1 };
-enum { XP_TRANSPORT_P2P = 0 };  /* producer kernels store into the consumer's ring slot
-                                   (same device or NVLink peer); device-side flags order it */
+enum { XP_TRANSPORT_P2P = 0 };  /* the producer stream copies its boundary tensor into the consumer's
+                                   ring slot with the copy engine (cudaMemcpyAsync, same device or
+                                   NVLink peer, or a CUDA-IPC-mapped slot in multi-process mode),
+                                   then writes the slot's ready flag with a stream memory operation
+                                   (cuStreamWriteValue32); the consumer stream waits on the flag
+                                   (cuStreamWaitValue32) -- no SM spins, no host involvement */
 
 /* xpipe_step flags */
 enum { XP_FLUSH = 1,        /* drain the pipeline at the end of the call */
@@ -179,8 +184,11 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
    unless XP_DEVICE_PTRS.  With XP_FLUSH the pipeline drains: afterwards every stage's
    version equals the number of mini-batches fed.  Splitting a sequence of mini-batches
    across calls (flush only at the end) gives bit-identical weights and traces.
-   Errors: XP_EINVAL (labels out of range are not checked on device pointers), XP_ECUDA,
-   XP_ESCHED (watchdog), XP_ENONFINITE (with cfg.trace). */
+   Errors: XP_EINVAL (labels out of range: checked on the host before any device work for host
+   pointers, by the loss kernel for device pointers -- then reported at the end of the call, the
+   affected rows got no one-hot term), XP_ECUDA, XP_ESCHED (watchdog), XP_ENONFINITE (a non-finite
+   loss; the call's work completed).  With XP_ASYNC these device-side checks are reported by the
+   next synchronous call. */
 int xpipe_step(struct xpipe_ctx* h, const float* x, const int32_t* y, int32_t n_minibatches,
                uint32_t flags, xpipe_stats* st);
 
@@ -238,6 +246,14 @@ int xpipe_finalize(struct xpipe_ctx* h);
 
 /* Last error message of h (h == NULL: this thread's last init error). Never NULL. */
 const char* xpipe_last_error(const struct xpipe_ctx* h);
+
+/* The first n ops of stage `stage`'s program (reading R7) as the
+   runtime executes them: ops[p] = 0 (forward) or 1 (backward) of micro-batch us[p] (1-based,
+   an unbounded stream; the update follows B(u) exactly when u % micro_batches == 0).  Generated
+   by the runtime's dependency-driven simulation (schedule.h); host-only, needs no GPU.
+   schedule = XP_SCHED_XPIPE | XP_SCHED_GPIPE.  Errors: XP_EINVAL. */
+int xpipe_schedule_program(int32_t stages, int32_t micro_batches, int32_t schedule, int32_t stage, int64_t n,
+                           int32_t* ops, int64_t* us);
 
 /* ---- kernel-level entry points (config 5 and unit parity) ----------------------------- */
 

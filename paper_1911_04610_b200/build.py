@@ -33,9 +33,10 @@ def sources():
 
 def headers():
     out = [os.path.join(ROOT, "include", "xpipe.h")]
-    for f in os.listdir(CSRC):
-        if f.endswith(".h"):
-            out.append(os.path.join(CSRC, f))
+    for d in (CSRC, os.path.join(CSRC, "kernels")):
+        for f in os.listdir(d):
+            if f.endswith(".h") or f.endswith(".cuh"):
+                out.append(os.path.join(d, f))
     return out
 
 

@@ -232,7 +232,7 @@ int op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot, int64_
     const int32_t* y = c->y_dev + (u - c->call_first) * c->n;
     float* loss = c->recompute_pass ? c->loss_scratch : c->loss_dev + (u - c->call_first);
     return check_launch(c, launch_xent_f32((const float*)s.act[O.in0][slot], y, s.dz[slot], loss, c->n, O.sin0.c,
-                                           (float)(1.0 / (double)c->N), s.stream), "xent");
+                                           (float)(1.0 / (double)c->N), c->status_dev, s.stream), "xent");
   }
   if (!is_bf16(c)) {
     if (O.kind != OP_LINEAR) return set_err(c, XP_EUNSUPPORTED, "fp32 op");

@@ -68,9 +68,12 @@ cudaError_t launch_linear_dgrad_f32(const float* dy, const float* ymask, const f
 // g[o][i] (=|+=) sum_r fmaf(dy'[r][o], x[r][i]); gb[o] (=|+=) sum_r dy'[r][o]
 cudaError_t launch_linear_wgrad_f32(const float* dy, const float* ymask, const float* x, float* gW, float* gb,
                                     int n, int in, int out, bool accumulate, cudaStream_t st);
-// softmax cross-entropy: dz[r][c] = (p - onehot) * invN; loss[0] = mean_r -log p_y
+// softmax cross-entropy: dz[r][c] = (p - onehot) * invN; loss[0] = mean_r -log p_y; one CTA,
+// one thread per row (n <= kXentMaxRows); status bits below are OR-ed into *status (nullable)
+constexpr int kXentMaxRows = 256;
+enum { XP_STATUS_NONFINITE = 1, XP_STATUS_LABEL = 2 };
 cudaError_t launch_xent_f32(const float* z, const int32_t* y, float* dz, float* loss, int n, int classes,
-                            float invN, cudaStream_t st);
+                            float invN, uint32_t* status, cudaStream_t st);
 
 // ---- bf16 path (kernels/bf16.cu, kernels/gemm_tc.cu) -----------------------------------
 // NCHW fp32 -> NHWC bf16 with the channel count padded to Cp (zeros)

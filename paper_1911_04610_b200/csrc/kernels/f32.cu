@@ -154,9 +154,11 @@ __global__ void __launch_bounds__(256) linear_wgrad_f32_kernel(const float* __re
 
 // softmax cross-entropy, one thread per row (classes sequential):
 // e_c = (float)exp((double)(z_c - max)); s = sum_c e_c (class order); p = e/s;
-// dz = (p - onehot) * invN; loss row = -log(e_y/s) (reporting only)
+// dz = (p - onehot) * invN; loss row = -log(e_y/s) (reporting only).
+// status (nullable): bit XP_STATUS_LABEL if a label lies outside [0, C) (its row then gets no
+// onehot term), bit XP_STATUS_NONFINITE if the mean loss is not finite; read by xpipe_step.
 __global__ void xent_f32_kernel(const float* __restrict__ z, const int32_t* __restrict__ y, float* __restrict__ dz,
-                                float* __restrict__ loss, int n, int C, float invN) {
+                                float* __restrict__ loss, int n, int C, float invN, uint32_t* __restrict__ status) {
   pdl_wait();
   __shared__ double lsum[256];
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -168,6 +170,7 @@ __global__ void xent_f32_kernel(const float* __restrict__ z, const int32_t* __re
     float s = 0.f;
     for (int c = 0; c < C; ++c) s = __fadd_rn(s, (float)exp((double)__fsub_rn(zr[c], mx)));
     const int lab = y[r];
+    if ((lab < 0 || lab >= C) && status) atomicOr(status, (uint32_t)XP_STATUS_LABEL);
     for (int c = 0; c < C; ++c) {
       const float e = (float)exp((double)__fsub_rn(zr[c], mx));
       const float p = __fdiv_rn(e, s);
@@ -180,7 +183,9 @@ __global__ void xent_f32_kernel(const float* __restrict__ z, const int32_t* __re
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double t = 0.0;
     for (int q = 0; q < n && q < 256; ++q) t += lsum[q];
-    *loss = (float)(t / n);
+    const float lv = (float)(t / n);
+    *loss = lv;
+    if (status && !isfinite(lv)) atomicOr(status, (uint32_t)XP_STATUS_NONFINITE);
   }
 }
 
@@ -241,9 +246,9 @@ cudaError_t launch_linear_wgrad_f32(const float* dy, const float* ymask, const f
 }
 
 cudaError_t launch_xent_f32(const float* z, const int32_t* y, float* dz, float* loss, int n, int classes, float invN,
-                            cudaStream_t st) {
-  if (n > 256) return cudaErrorInvalidValue;
-  launch_pdl(xent_f32_kernel, dim3(1), dim3(256), 0, st, z, y, dz, loss, n, classes, invN);
+                            uint32_t* status, cudaStream_t st) {
+  if (n > kXentMaxRows) return cudaErrorInvalidValue;
+  launch_pdl(xent_f32_kernel, dim3(1), dim3(256), 0, st, z, y, dz, loss, n, classes, invN, status);
   return cudaGetLastError();
 }
 

@@ -8,6 +8,7 @@
 #include "../../include/xpipe.h"
 #include "internal.h"
 #include "plan.h"
+#include "schedule.h"
 
 #define XP_CUDA(c, call)                                                                           \
   do {                                                                                             \
@@ -77,6 +78,7 @@ struct StageRT {
   std::vector<cudaEvent_t> ev_fdone, ev_bdone;  // per slot: F(u) done, B(u) done
   std::vector<int64_t> fdone_epoch, bdone_epoch;
   cudaEvent_t ev_upd = nullptr, ev_fmark = nullptr, ev_fjoin = nullptr;
+  cudaEvent_t ev_in = nullptr;          // the call's input / label copies (main stream) are done
   int64_t upd_epoch = -1;
   float* ws = nullptr;                  // split-K workspace (fp32)
   int64_t ws_elems = 0;
@@ -116,6 +118,7 @@ struct xpipe_ctx {
   float lr = 0, b1 = 0, b2 = 0, eps = 0;
   xpipe_config cfg{};
   std::vector<StageRT> S;
+  xp::ScheduleSim sched;              // stage programs (a1), generated by simulation
   std::vector<Alloc> allocs;
   std::vector<void*> ipc_allocs;     // cudaMalloc'ed (exportable) rings/flags, multi-process mode
   std::vector<void*> ipc_opened;     // neighbour memory mapped with cudaIpcOpenMemHandle
@@ -145,6 +148,8 @@ struct xpipe_ctx {
   bool recompute_pass = false;          // f3: op_forward is re-running a stage forward inside B(u)
   int64_t call_epoch = 0;               // bumped per call: events recorded in earlier calls are complete
   float* loss_scratch = nullptr;        // the recomputed forward's loss (the reported loss is F(u)'s)
+  uint32_t* status_dev = nullptr;       // last stage: XP_STATUS_* bits set by the loss kernel
+  uint32_t* status_host = nullptr;      // pinned mirror read after a synchronous call
   std::vector<int64_t> cap_fwd0, cap_bwd0;  // enqueue counters when the capture started
   std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)
 };

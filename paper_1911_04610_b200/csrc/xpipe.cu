@@ -119,7 +119,8 @@ void free_all(xpipe_ctx* c) {
     }
     s.side = nullptr;
     if (shared) s.stream = nullptr;
-    for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1], &s.ev_upd, &s.ev_fmark, &s.ev_fjoin})
+    for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1], &s.ev_upd, &s.ev_fmark, &s.ev_fjoin,
+                           &s.ev_in})
       if (*e) { cudaEventDestroy(*e); *e = nullptr; }
     for (auto* v : {&s.ev_fdone, &s.ev_bdone}) { for (auto e : *v) if (e) cudaEventDestroy(e); v->clear(); }
     if (own_fstream) {
@@ -128,6 +129,7 @@ void free_all(xpipe_ctx* c) {
     s.fstream = nullptr;
     if (s.stream) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.stream); cudaStreamDestroy(s.stream); s.stream = nullptr; }
   }
+  if (c->status_host) { cudaFreeHost(c->status_host); c->status_host = nullptr; }
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   c->ipc_opened.clear();
   for (void* p : c->ipc_allocs) cudaFree(p);
@@ -237,22 +239,18 @@ int flag_write(xpipe_ctx* c, StageRT& s, StageRT& tgt, int which, int64_t value)
   return XP_OK;
 }
 
-// ---- stage program (a1; R7), written independently of the oracle ---------------------------
-// returns op (0 = F, 1 = B) and micro-batch u (absolute, 1-based) at program position p
-void program_op(const xpipe_ctx* c, int k, int64_t p, int* op, int64_t* u) {
-  if (c->cfg.schedule == XP_SCHED_GPIPE) {
-    const int64_t t = p / (2 * c->T), r = p % (2 * c->T);
-    *op = r < c->T ? 0 : 1;
-    *u = t * c->T + (r < c->T ? r : r - c->T) + 1;
-  } else {
-    const int64_t W = c->K - k;
-    if (p < W) { *op = 0; *u = p + 1; }
-    else {
-      const int64_t q = p - W, i = q / 2 + 1;
-      if (q % 2 == 0) { *op = 1; *u = i; } else { *op = 0; *u = i + W; }
-    }
-  }
+// ---- stage program (a1; R7) ------------------------------------------------------------------
+// op (0 = F, 1 = B) and micro-batch u (absolute, 1-based) at program position p of stage k, from
+// the dependency-driven schedule simulation (schedule.h)
+void program_op(xpipe_ctx* c, int k, int64_t p, int* op, int64_t* u) {
+  c->sched.op_at(k, p, op, u);
   *u += c->base;
+}
+
+void reset_schedule(xpipe_ctx* c) {
+  std::vector<bool> rec;
+  for (const auto& s : c->S) rec.push_back(owned(s));
+  c->sched.reset(c->K, c->T, c->cfg.schedule == XP_SCHED_GPIPE, rec);
 }
 
 int trace_slot(xpipe_ctx* c, StageRT& s, TraceRec** rec) {
@@ -760,6 +758,10 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
   if (cfg->schedule != XP_SCHED_XPIPE && cfg->schedule != XP_SCHED_GPIPE) return set_err(nullptr, XP_EINVAL, "schedule");
   if (cfg->predict < 0 || cfg->predict > 2 || (cfg->predict == XP_PRED_FIXED && (cfg->s_fwd < 0 || cfg->s_bwd < 0)))
     return set_err(nullptr, XP_EINVAL, "predict");
+  if (cfg->schedule == XP_SCHED_GPIPE && cfg->predict == XP_PRED_PAPER)
+    return set_err(nullptr, XP_EINVAL, "GPipe runs under the current weights: use XP_PRED_OFF (or XP_PRED_FIXED for diagnostics)");
+  if (N / T > kXentMaxRows)
+    return set_err(nullptr, XP_EUNSUPPORTED, "micro-batch N/T > " + std::to_string(kXentMaxRows) + " (loss kernel limit)");
   if (cfg->multi_process && (cfg->my_stage < 0 || cfg->my_stage >= stages))
     return set_err(nullptr, XP_EINVAL, "my_stage out of range");
   std::unique_ptr<xpipe_ctx> c(new xpipe_ctx());
@@ -770,6 +772,11 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
   std::string perr;
   int r = build_net_plan(layers, n_layers, stages, c->cfg, c->n, &c->net, &perr);
   if (r != XP_OK) return set_err(nullptr, r, perr);
+  for (const auto& sp : c->net.stages)
+    for (const Op& O : sp.ops)
+      if (O.kind == OP_CONV && (O.smid.c % 8 || O.smid.c > 2048))
+        return set_err(nullptr, XP_EUNSUPPORTED, "BatchNorm kernels need C % 8 == 0 and C <= 2048 (conv output channels " +
+                                                     std::to_string(O.smid.c) + ")");
   if (!load_driver_entry_points()) return set_err(nullptr, XP_ECUDA, "CUDA driver stream memory operations unavailable");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return set_err(nullptr, XP_ECUDA, "no CUDA device");
@@ -844,7 +851,7 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
     for (auto* v : {&s.ev_fdone, &s.ev_bdone})
       for (auto& e : *v)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail_init(XP_ECUDA, "event");
-    for (cudaEvent_t* e : {&s.ev_upd, &s.ev_fmark, &s.ev_fjoin})
+    for (cudaEvent_t* e : {&s.ev_upd, &s.ev_fmark, &s.ev_fjoin, &s.ev_in})
       if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail_init(XP_ECUDA, "event");
     for (cudaEvent_t* e : {&s.ev_fork, &s.ev_join, &s.ev_gdone[0], &s.ev_gdone[1]})
       if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return fail_init(XP_ECUDA, "event");
@@ -854,11 +861,19 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
     rr = init_stage_params(cp, s, layers);
     if (rr != XP_OK) return fail_init(rr, "parameter init");
   }
+  if (owned(c->S[stages - 1])) {
+    StageRT& sl = c->S[stages - 1];
+    cudaSetDevice(sl.dev);
+    c->status_dev = (uint32_t*)dmalloc(cp, 256, sl.dev);
+    if (!c->status_dev || cudaMallocHost(&c->status_host, 256) != cudaSuccess) return fail_init(XP_ENOMEM, "status word");
+    if (cudaMemsetAsync(c->status_dev, 0, 4, sl.stream) != cudaSuccess) return fail_init(XP_ECUDA, "status word");
+  }
   for (auto& s : c->S) {
     if (!owned(s)) continue;
     cudaSetDevice(s.dev);
     if (cudaStreamSynchronize(s.stream) != cudaSuccess) return fail_init(XP_ECUDA, "init sync");
   }
+  reset_schedule(cp);
   cudaSetDevice(cur);
   *out = c.release();
   return XP_OK;
@@ -888,16 +903,28 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
     StageRT& s0 = c->S[0];
     StageRT& sl = c->S[c->K - 1];
+    // the copies run on the stages' main streams; the forward streams (fb_overlap) and, for a
+    // graph replay, the launch stream wait for them (ev_in) before any op reads x / y / losses
     if (owned(s0)) {
       cudaSetDevice(s0.dev);
       XP_CUDA(c, cudaMemcpyAsync(c->x_dev, x, (size_t)M * c->N * per * 4,
-                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.fstream));
+                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.stream));
     }
     if (owned(sl)) {
       cudaSetDevice(sl.dev);
       XP_CUDA(c, cudaMemcpyAsync(c->y_dev, y, (size_t)M * c->N * 4,
-                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sl.fstream));
-      XP_CUDA(c, cudaMemsetAsync(c->loss_dev, 0xff, (size_t)M * c->T * 4, sl.fstream));  // NaN = not computed
+                                 dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sl.stream));
+      XP_CUDA(c, cudaMemsetAsync(c->loss_dev, 0xff, (size_t)M * c->T * 4, sl.stream));  // NaN = not computed
+    }
+    for (StageRT* q : {&s0, &sl}) {
+      if (!owned(*q)) continue;
+      cudaSetDevice(q->dev);
+      XP_CUDA(c, cudaEventRecord(q->ev_in, q->stream));
+      if (q->fstream && q->fstream != q->stream) XP_CUDA(c, cudaStreamWaitEvent(q->fstream, q->ev_in, 0));
+    }
+    if (owned(s0) && owned(sl) && sl.dev == s0.dev && &sl != &s0) {
+      cudaSetDevice(s0.dev);
+      XP_CUDA(c, cudaStreamWaitEvent(s0.stream, sl.ev_in, 0));  // graph launch stream sees the label copy
     }
     c->call_first = c->fed + 1;
     c->fed += (int64_t)M * c->T;
@@ -916,10 +943,20 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
       s.pos = 0;
     }
     c->base = c->fed;
+    reset_schedule(c);
   }
   int rr = XP_OK;
   if (!(flags & XP_ASYNC)) rr = sync_all(c);
   if (rr != XP_OK) return rr;
+  uint32_t status = 0;
+  if (!(flags & XP_ASYNC) && c->status_dev) {
+    // loss-kernel status word (device-side label range and non-finite loss checks)
+    StageRT& sl = c->S[c->K - 1];
+    cudaSetDevice(sl.dev);
+    XP_CUDA(c, cudaMemcpy(c->status_host, c->status_dev, 4, cudaMemcpyDeviceToHost));
+    status = *c->status_host;
+    if (status) XP_CUDA(c, cudaMemset(c->status_dev, 0, 4));
+  }
   if (st) {
     st->kernel_launches = c->kernels - k0;
     st->graph_replays = c->graph_replays - g0;
@@ -943,6 +980,8 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     }
   }
   cudaSetDevice(cur);
+  if (status & XP_STATUS_LABEL) return set_err(c, XP_EINVAL, "label out of range (device check)");
+  if (status & XP_STATUS_NONFINITE) return set_err(c, XP_ENONFINITE, "non-finite loss");
   return XP_OK;
 }
 
@@ -1171,11 +1210,31 @@ int xpipe_get_trace(xpipe_ctx* c, int32_t stage, xpipe_trace_rec* dst, size_t ca
   return XP_OK;
 }
 
+int xpipe_schedule_program(int32_t stages, int32_t micro_batches, int32_t schedule, int32_t stage, int64_t n,
+                           int32_t* ops, int64_t* us) {
+  if (stages < 1 || micro_batches < 1 || stage < 0 || stage >= stages || n < 0 || (n > 0 && (!ops || !us)) ||
+      (schedule != XP_SCHED_XPIPE && schedule != XP_SCHED_GPIPE))
+    return set_err(nullptr, XP_EINVAL, "schedule_program args");
+  ScheduleSim sim;
+  std::vector<bool> rec(stages, false);
+  rec[stage] = true;
+  sim.reset(stages, micro_batches, schedule == XP_SCHED_GPIPE, rec);
+  for (int64_t p = 0; p < n; ++p) {
+    int op;
+    int64_t u;
+    sim.op_at(stage, p, &op, &u);
+    ops[p] = op;
+    us[p] = u;
+  }
+  return XP_OK;
+}
+
 int xpipe_adam_predict(float* W, const float* g, float* m, float* v, void* pred_f, void* pred_b, int64_t n,
                        int64_t version, float lr, float beta1, float beta2, float eps, int32_t s_f, int32_t s_b,
                        int32_t pred_bf16, int32_t delta_form, void* stream) {
   if (!W || !g || !m || !v || n < 0 || version < 1) return set_err(nullptr, XP_EINVAL, "adam_predict args");
-  if (((uintptr_t)W | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) return set_err(nullptr, XP_EINVAL, "alignment");
+  if (((uintptr_t)W | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v | (uintptr_t)pred_f | (uintptr_t)pred_b) & 15)
+    return set_err(nullptr, XP_EINVAL, "alignment (all six arrays 16-byte aligned)");
   SweepScalars hs;
   host_scalars(version, lr, beta1, beta2, eps, &hs);
   cudaError_t e = launch_sweep(W, g, m, v, pred_f, pred_b, n, nullptr, &hs, (float)s_f, (float)s_b, pred_bf16 != 0,
@@ -1188,8 +1247,8 @@ int xpipe_sgd_predict(float* W, const float* g, float* buf, float* m, float* v, 
                       float lr, float beta1, float beta2, float eps, float momentum, float weight_decay, int32_t s_f,
                       int32_t s_b, int32_t pred_bf16, void* stream) {
   if (!W || !g || !buf || !m || !v || n < 0) return set_err(nullptr, XP_EINVAL, "sgd_predict args");
-  if (((uintptr_t)W | (uintptr_t)g | (uintptr_t)buf | (uintptr_t)m | (uintptr_t)v) & 15)
-    return set_err(nullptr, XP_EINVAL, "alignment");
+  if (((uintptr_t)W | (uintptr_t)g | (uintptr_t)buf | (uintptr_t)m | (uintptr_t)v | (uintptr_t)pred_f | (uintptr_t)pred_b) & 15)
+    return set_err(nullptr, XP_EINVAL, "alignment (all seven arrays 16-byte aligned)");
   SweepScalars hs;
   host_scalars(1, lr, beta1, beta2, eps, &hs);  // the paper form uses only the constant corrections
   hs.mu = momentum;

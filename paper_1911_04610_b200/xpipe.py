@@ -102,6 +102,7 @@ def lib():
         L.xpipe_refresh_predictions.argtypes = [vp]
         L.xpipe_gemm_bf16.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i64, vp]
         L.xpipe_conv2d_bf16.argtypes = [i32, C.POINTER(i32), vp, vp, vp, i32, vp, i64, vp]
+        L.xpipe_schedule_program.argtypes = [i32, i32, i32, i32, i64, vp, vp]
         _lib = L
     return _lib
 
@@ -140,12 +141,14 @@ class XPipe:
     xpipe_finalize."""
 
     def __init__(self, layers, stages, micro_batches, mini_batch, lr, betas, eps, in_shape, classes, params=None,
-                 precision="fp32", schedule="xpipe", predict="paper", s_fwd=0, s_bwd=0, delta="adam",
+                 precision="fp32", schedule="xpipe", predict=None, s_fwd=0, s_bwd=0, delta="adam",
                  init_m=None, init_v=None, devices=None, snapshots=False, trace=False, graphs=False, profile=False,
                  seed=1, watchdog_ms=0, torch_allocator=True, my_stage=None, optimizer="adam", momentum=0.9,
                  weight_decay=5e-4, recompute=False, serialize=False, fb_overlap=False):
         self.h = None
         L = lib()
+        if predict is None:  # GPipe runs under the current weights (no prediction)
+            predict = "off" if schedule == "gpipe" else "paper"
         self.layers = list(layers)
         arr = (Layer * len(self.layers))()
         for i, l in enumerate(self.layers):
@@ -207,7 +210,12 @@ class XPipe:
     def step(self, x, y, M, flush=False, async_=False, losses=True):
         """x: [M*N, C, H, W] float32, y: [M*N] int32 -- numpy (host) or torch CUDA tensors (device)."""
         flags = (XP_FLUSH if flush else 0) | (XP_ASYNC if async_ else 0)
+        per = self.in_shape[0] * self.in_shape[1] * self.in_shape[2]
         if hasattr(x, "is_cuda") and x.is_cuda:
+            if not (hasattr(y, "is_cuda") and y.is_cuda):
+                raise TypeError("x and y must both be CUDA tensors or both host arrays")
+            _want("x", x, ("float32",), M * self.N * per)
+            _want("y", y, ("int32",), M * self.N)
             flags |= XP_DEVICE_PTRS
         else:
             x = np.ascontiguousarray(x, dtype=np.float32)
@@ -305,6 +313,8 @@ def _want(name, t, dtypes, n=None):
         raise ValueError("%s must be contiguous" % name)
     if n is not None and t.numel() < n:
         raise ValueError("%s has %d elements, needs %d" % (name, t.numel(), n))
+    if hasattr(t, "data_ptr") and t.data_ptr() % 16:
+        raise ValueError("%s must be 16-byte aligned" % name)
 
 
 def adam_predict(W, g, m, v, pf, pb, version, lr, betas, eps, s_f, s_b, pred_bf16, delta="adam", stream=None):
@@ -368,3 +378,11 @@ def connect_pipeline(model, group=None):
     for b in blobs:
         model.ipc_import(b)
     return blobs
+
+
+def schedule_program(stages, micro_batches, stage, n, schedule="xpipe"):
+    """xpipe_schedule_program: the first n (op, u) of a stage's program (host-only)."""
+    ops = np.empty(n, np.int32)
+    us = np.empty(n, np.int64)
+    _check(lib().xpipe_schedule_program(stages, micro_batches, SCHEDULE[schedule], stage, n, _ptr(ops), _ptr(us)))
+    return list(zip(ops.tolist(), us.tolist()))

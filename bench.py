@@ -143,49 +143,48 @@ def cpu_baseline(workload, seconds=20.0):
                       % (done, n, "bf16 emulation" if prec == "bf16" else "fp32", el)}
 
 
-def measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank, sched=None):
-    """Bubble fraction of one traced call (single-process mode): 1 - sum_k busy_k / (K * span),
-    busy_k = device time covered by stage k's F/B ops (%globaltimer), next to the uniform-cost ideal
-    (K-1)/(M*T+K-1) of SPEC S:397 / SURVEY A.3."""
-    if mp_mode:
-        return None
-    import synthetic as S
-    import torch
-    from paper_1911_04610_b200 import XPipe
-    # the schedule's bubble: one stream per stage (with fb_overlap a stage is two workers and the
-    # single-worker busy fraction no longer describes the schedule)
-    sched = {k: v for k, v in (sched or {}).items() if k != "fb_overlap"}
-    g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
-              devices=list(range(args.gpus)), trace=True, watchdog_ms=300000, **sched)
-    x, y = S.make_inputs(M * N, shape, classes, 2, kind=kind)
-    g.step(torch.from_numpy(x).cuda(0), torch.from_numpy(y).cuda((K - 1) % args.gpus), M, flush=True)
-    busy, t0s, t1s = [], [], []
-    for k in range(K):
-        tr = g.trace(k, timestamps=True)
-        ops = [r for r in tr if r[1] in (0, 1)]
-        # busy time = the union of the stage's F/B intervals (with fb_overlap a forward and a
-        # backward of the stage run at the same time)
-        iv = sorted((r[8], r[9]) for r in ops)
-        tot, cur0, cur1 = 0, None, None
-        for a, b in iv:
-            if cur1 is None or a > cur1:
-                if cur1 is not None:
-                    tot += cur1 - cur0
-                cur0, cur1 = a, b
-            else:
-                cur1 = max(cur1, b)
-        if cur1 is not None:
-            tot += cur1 - cur0
-        busy.append(tot)
-        t0s.append(min(r[8] for r in ops))
-        t1s.append(max(r[9] for r in ops))
-    g.close()
-    span = max(t1s) - min(t0s)
-    gp = sched.get("schedule") == "gpipe"
-    ideal = (K - 1) / (T + K - 1) if gp else (K - 1) / (M * T + K - 1)  # SURVEY A.3 closed forms
-    return {"bubble_fraction": 1.0 - sum(busy) / (K * span), "ideal_uniform": ideal,
-            "traced_minibatches": M,
-            "note": "separate traced call with flush, one stream per stage (trace kernels add overhead)"}
+def stage_costs(g, L, shape, K):
+    """Per stage: training flops per sample (2 x (fwd + dgrad + wgrad) MACs; the first layer
+    needs no dgrad) and parameters, from the layer list and the library's stage assignment
+    (SURVEY 8d "algorithmic work")."""
+    from synthetic.models import infer_shapes, LINEAR, CONV2D, BATCHNORM2D
+    shapes = infer_shapes(L, shape)
+    flops = [0.0] * K
+    params = [0] * K
+    first = True
+    for i, l in enumerate(L):
+        k = g.stage_of(i)
+        if l.kind == LINEAR:
+            mac = l.in_c * l.out_c
+            params[k] += mac + (l.out_c if l.bias else 0)
+        elif l.kind == CONV2D:
+            c, h, w = shapes[i]
+            mac = c * h * w * l.in_c * l.kh * l.kw
+            params[k] += l.out_c * l.in_c * l.kh * l.kw + (l.out_c if l.bias else 0)
+        elif l.kind == BATCHNORM2D:
+            params[k] += 2 * l.in_c
+            continue
+        else:
+            continue
+        flops[k] += 2.0 * mac * (2 if first else 3)
+        first = False
+    return flops, params
+
+
+def pipeline_roofline(flops, params, N, M, ms_per_step, peaks, one_device, sweep_bytes=32.0):
+    """ideal time per mini-batch at the measured peaks (stage GEMM/conv flops at the
+    sustained bf16 tensor peak + the K1 sweep's bytes at the HBM copy peak), the bottleneck stage
+    when every stage has its own GPU, the sum when they share one, over the measured time per
+    mini-batch.  BN / elementwise traffic, launch latency and hand-offs are not in the ideal."""
+    tp = peaks.get("bf16_tflops_sustained", 1400.0) * 1e12
+    hb = peaks["hbm_gbs"] * 1e9
+    per = [f * N / tp + p * sweep_bytes / hb for f, p in zip(flops, params)]
+    ideal = sum(per) if one_device else max(per)
+    meas = ms_per_step * 1e-3 / M
+    return {"frac": ideal / meas, "ideal_ms_per_minibatch": ideal * 1e3, "measured_ms_per_minibatch": meas * 1e3,
+            "per_stage_ideal_ms": [x * 1e3 for x in per],
+            "note": "ideal = %s of per-stage (flops/sustained tensor peak + 32 B/param sweep/HBM peak)"
+                    % ("sum (all stages share one GPU)" if one_device else "max (one stage per GPU)")}
 
 
 def run_reference(args):
@@ -307,6 +306,8 @@ def main():
     ap.add_argument("--schedule", default="xpipe", choices=["xpipe", "gpipe"],
                     help="gpipe: synchronous GPipe with a flush per mini-batch (prediction off), same kernels")
     ap.add_argument("--no-graphs", action="store_true", help="enqueue every kernel from the host (no CUDA graphs)")
+    ap.add_argument("--no-timing", dest="timing", action="store_false",
+                    help="do not time the ops of the timed run (cfg.timing: bubble, steady rate, hand-offs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -372,14 +373,16 @@ def main():
             # one process per GPU: this rank owns stage `rank`; rings/flags are CUDA IPC-mapped
             import torch.distributed as dist
             m = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
-                      profile=profile, watchdog_ms=300000, my_stage=rank, **sched)
+                      profile=profile, watchdog_ms=300000, my_stage=rank, timing=not profile and args.timing,
+                      **sched)
             connect_pipeline(m, dist.new_group(backend="gloo"))
         else:
             # the profiled pass runs every stage on one stream (serialize): each launch then runs
             # alone, so its event-timed duration is the kernel's own (as in ncu's launch list)
             m = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec,
                       devices=list(range(args.gpus)), profile=profile, watchdog_ms=300000,
-                      graphs=not args.no_graphs, serialize=profile and args.gpus == 1, **sched)
+                      graphs=not args.no_graphs, serialize=profile and args.gpus == 1,
+                      timing=not profile and args.timing, **sched)
         return m
 
     x, y = S.make_inputs(M * N, shape, classes, 1, kind=kind)
@@ -409,6 +412,7 @@ def main():
     warm(g)
     launches = 0
     replays = 0
+    tim = []
     with Clocks(dev) as ck:
         g.timer_start()
         for _ in range(args.steps):
@@ -416,8 +420,11 @@ def main():
             st = g.last_stats
             launches += st.kernel_launches
             replays += st.graph_replays
+            if args.timing:
+                tim.append(st.timing(K))
         ms = g.timer_stop()
         barrier()
+    flops, params = stage_costs(g, L, shape, K)
     clocks = ck.summary()
     e2e_s = None
     if not args.no_e2e:
@@ -449,8 +456,19 @@ def main():
     if mp_mode:
         import torch.distributed as dist
         allp = [None] * ws
-        dist.all_gather_object(allp, {"ms": ms, "prof": prof, "launches": launches, "e2e_s": e2e_s})
+        dist.all_gather_object(allp, {"ms": ms, "prof": prof, "launches": launches, "e2e_s": e2e_s, "tim": tim})
         ms = max(p["ms"] for p in allp)                       # max over ranks
+        # each rank timed its own stage: merge per step (busy of stage r from rank r, the span as
+        # the max over ranks, the steady rate from stage 0's rank)
+        if args.timing:
+            merged = []
+            for i in range(len(tim)):
+                t = dict(allp[0]["tim"][i])
+                t["span_ms"] = max(p["tim"][i]["span_ms"] for p in allp)
+                for key in ("busy_ms", "p2p_fwd_ms", "p2p_bwd_ms", "p2p_fwd_bytes", "p2p_bwd_bytes"):
+                    t[key] = [allp[r]["tim"][i][key][r] for r in range(ws)]
+                merged.append(t)
+            tim = merged
         e2e_s = None if e2e_s is None else max(p["e2e_s"] for p in allp)
         launches = sum(p["launches"] for p in allp)
         prof = {}
@@ -500,10 +518,38 @@ def main():
                   "unit": "GB/s" if k in BYTE_CLASSES else "TFLOP/s", "launches": v["launches"]}
               for k, v in prof.items()}
     result = dict(ms=ms, clocks=clocks, roof=roof, shares=shares, launches=launches, replays=replays)
-    try:
-        bubble = measure_bubble(L, K, T, N, M, shape, classes, kind, prec, P, args, mp_mode, rank, sched)
-    except Exception as e:  # the bubble is a report, not the metric
-        bubble = {"error": repr(e)[:200]}
+    # bubble fraction and hand-offs of the timed run itself (xpipe_stats from per-op CUDA events,
+    # also inside the replayed graphs): 1 - sum_k busy_k / (K * span) over all timed steps
+    bubble = None
+    if tim:
+        span = sum(t["span_ms"] for t in tim)
+        busy = [sum(t["busy_ms"][k] for t in tim) for k in range(K)]
+        gp_ = args.schedule == "gpipe"
+        ideal = (K - 1) / (T + K - 1) if gp_ else (K - 1) / (M * T + K - 1)  # SURVEY A.3 closed forms
+        steady = [t["steady_samples_per_s"] for t in tim if t["steady_samples_per_s"] > 0]
+        edges = []
+        for k in range(K):
+            fb = sum(t["p2p_fwd_bytes"][k] for t in tim)
+            fm = sum(t["p2p_fwd_ms"][k] for t in tim)
+            bb = sum(t["p2p_bwd_bytes"][k] for t in tim)
+            bm = sum(t["p2p_bwd_ms"][k] for t in tim)
+            if fb:
+                edges.append({"edge": "%d->%d" % (k, k + 1), "GB_per_s": fb / (fm * 1e-3) / 1e9 if fm else None,
+                              "ms_per_step": fm / len(tim), "unhidden_frac_of_span": fm / span})
+            if bb:
+                edges.append({"edge": "%d->%d" % (k, k - 1), "GB_per_s": bb / (bm * 1e-3) / 1e9 if bm else None,
+                              "ms_per_step": bm / len(tim), "unhidden_frac_of_span": bm / span})
+        bubble = {"bubble_fraction": 1.0 - sum(busy) / (K * span), "ideal_uniform": ideal,
+                  "busy_frac_per_stage": [b / span for b in busy],
+                  "span_ms_per_step": span / len(tim),
+                  "steady_samples_per_s": statistics.median(steady) if steady else None,
+                  "p2p": edges,
+                  "source": "xpipe_stats of the timed run (cfg.timing: CUDA events per op on its stream, "
+                            "recorded inside the replayed graphs); a stage's busy time is the union of its "
+                            "F/B op intervals (input arrival to hand-off end; B(t,T) to the update's end)"}
+    one_dev = (not mp_mode) and args.gpus == 1
+    proof = pipeline_roofline(flops, params, N, M, result["ms"] / args.steps, peaks, one_dev,
+                              sweep_bytes=32.0 if prec == "bf16" else 36.0)
     # the oracle baseline is timed on rank 0 at N=1 only (the contract); N>1 lines omit it
     cpu = None if (args.no_cpu_baseline or mp_mode) else cpu_baseline(args.workload)
     sweep = None
@@ -528,7 +574,8 @@ def main():
             "e2e": e2e, "gpu_launches": result["launches"], "graph_replays": result.get("replays"),
             "clocks": result["clocks"],
             "roofline": result["roof"], "kernel_shares": result["shares"],
-            "profiled_step_ms": prof_step_ms if not mp_mode else None, "bubble": bubble, "cpu_baseline": cpu,
+            "profiled_step_ms": prof_step_ms if not mp_mode else None, "bubble": bubble,
+            "pipeline_roofline": proof, "cpu_baseline": cpu,
             "adam_predict": sweep}
     print(json.dumps(line), flush=True)
     return 0

@@ -136,6 +136,10 @@ typedef struct {
                                          F(u+S) overlaps B(u) (one more ring/stash slot per stage;
                                          ordering by events: F(u) -> B(u), B(u) -> F(u+S+1),
                                          update -> next bellwether forward); same results */
+  int32_t timing;                     /* 1 = time every forward/backward op with CUDA events on the
+                                         stream it runs on (also inside replayed graphs) and fill
+                                         the span / busy / bubble / steady-rate / hand-off fields
+                                         of xpipe_stats; no per-op kernels are added */
 } xpipe_config;
 
 /* one device-trace record (K12): op 0 = forward, 1 = backward, 2 = update.  version is the
@@ -157,14 +161,32 @@ enum { XP_PROF_SWEEP = 0,       /* K1: work = algorithmic bytes */
        XP_PROF_BN_BWD_APPLY = 7,  /* BN input gradient: bytes */
        XP_PROF_N = 8 };
 
+#define XP_STATS_STAGES 16
 typedef struct {
-  double span_ms;                    /* reserved */
+  double span_ms;                    /* cfg.timing: device time from the first op start to the last
+                                        op end of this call over the process's stages (per-device
+                                        CUDA events; devices aligned at the call's start, every call
+                                        begins with a drained pipeline); else 0 */
   double prof_ms[XP_PROF_N];         /* summed device time per kernel class (cfg.profile) */
   int64_t prof_launches[XP_PROF_N];
   double prof_work[XP_PROF_N];       /* algorithmic bytes (sweep, BN) or flops (GEMM classes) */
   int64_t kernel_launches;           /* kernels enqueued by this call (directly or in a graph) */
   int64_t graph_replays;             /* 1 if this call replayed a captured CUDA graph */
   float* losses;                     /* optional caller buffer of M*T per-micro-batch mean losses */
+  /* ---- cfg.timing (zero otherwise) ---- */
+  double busy_ms[XP_STATS_STAGES];   /* per stage: length of the union of its op intervals (an op
+                                        runs from its input's arrival to the end of its hand-off, a
+                                        backward B(t,T) to the end of the update sweep) */
+  double bubble_fraction;            /* 1 - sum_k busy_ms[k] / (stages owned * span_ms) */
+  double steady_samples_per_s;       /* mini-batches / time between the bellwether forwards
+                                        on stage 0 (0 if stage 0 is not owned or too few); the first
+                                        K mini-batches after an empty pipeline and the last K of a
+                                        flushing call are excluded (warm-up / drain) */
+  double p2p_fwd_ms[XP_STATS_STAGES];   /* stage k: summed time of its activation hand-offs k->k+1 */
+  double p2p_bwd_ms[XP_STATS_STAGES];   /* stage k: summed time of its gradient hand-offs k->k-1 */
+  double p2p_fwd_bytes[XP_STATS_STAGES];
+  double p2p_bwd_bytes[XP_STATS_STAGES];
+  int64_t ops_timed;                 /* forward + backward ops timed in this call */
 } xpipe_stats;
 
 /* Build the pipeline.  layers/n_layers: the network, last layer XP_SOFTMAX_XENT;

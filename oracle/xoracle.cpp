@@ -3,8 +3,10 @@
  *
  * TEST INFRASTRUCTURE ONLY.  Loaded by tests/, __graft_entry__.smoke() and bench.py's
  * cpu_baseline / --impl reference legs; never by the product path.  Shares no code with
- * the CUDA product.  Built with -O2 -fopenmp -ffp-contract=off (no -ffast-math) so every
- * float operation written here is one IEEE operation.
+ * the CUDA product.  Built with -O3 -march=native -fopenmp -ffp-contract=off (no -ffast-math;
+ * oracle/__init__.py) so every float operation written here is one IEEE operation: vector code
+ * only evaluates the written operations lane by lane, and no multiply-add is contracted except
+ * the explicit std::fmaf calls of the fp32 contract.
  *
  * Every function cites the passage it follows (P:n = /root/reference/PAPER.md line n;
  * "R<n>" = DESIGN.md reading n; "fp32 contract" = DESIGN.md section 4).
@@ -175,47 +177,77 @@ void valid_range(int sw, int pw, int s, int W, int Q, int& qlo, int& qhi) {
   while (qhi > qlo && (qhi - 1) * sw - pw + s >= W) --qhi;
 }
 
+/* Loop blocking of the conv sums below: a task owns a block of kPix output (or input) pixels x
+   kChan channels and keeps their independent sums in a small array; each sum still runs over
+   its terms one at a time in the order its comment states.  Blocking only decides which sums
+   advance together (weights and inputs are reused from cache); no sum is split or reordered. */
+constexpr int kPix = 32, kChan = 64, kOut = 8;
+
 /* Conv2d: cross-correlation with zero padding (PyTorch semantics), NCHW.
-   y[n][co][p][q] = sum_{ci,r,s} x[n][ci][p*sh-ph+r][q*sw-pw+s] * W[co][ci][r][s] (+ b) */
+   y[n][co][p][q] = sum_{ci,r,s} x[n][ci][p*sh-ph+r][q*sw-pw+s] * W[co][ci][r][s] (+ b)
+   Every output is one sequential sum in (ci, r, s) order over its in-range taps (taps that
+   fall into the zero padding are skipped); weights are read from a copy laid out
+   [ci][r][s][co]. */
 void conv_fwd(const Model& M, int li, int n, const Vec& x, const double* W, const double* b, Vec& y) {
   const Layer& l = M.L[li];
   const int C = l.in0.c, H = l.in0.h, Wd = l.in0.w, K = l.d.out_c, R = l.d.kh, S = l.d.kw;
   const int P = l.out.h, Q = l.out.w;
+  const bool f32 = M.mode == XO_FP32;
+  Vec Wt((size_t)C * R * S * K);
+  std::vector<float> Wtf(f32 ? Wt.size() : 0);
+  for (int co = 0; co < K; ++co)
+    for (int ci = 0; ci < C; ++ci)
+      for (int rs = 0; rs < R * S; ++rs) {
+        const double w = W[((size_t)co * C + ci) * R * S + rs];
+        Wt[((size_t)ci * R * S + rs) * K + co] = w;
+        if (f32) Wtf[((size_t)ci * R * S + rs) * K + co] = (float)w;
+      }
   y.assign((size_t)n * K * P * Q, 0.0);
-#pragma omp parallel for collapse(2) schedule(static)
-  for (int s0 = 0; s0 < n; ++s0)
-    for (int co = 0; co < K; ++co) {
-      Vec acc((size_t)P * Q, 0.0);
-      std::vector<float> accf((size_t)P * Q, 0.f);
-      for (int ci = 0; ci < C; ++ci)
-        for (int r = 0; r < R; ++r)
-          for (int s = 0; s < S; ++s) {
-            double w = W[(((size_t)co * C + ci) * R + r) * S + s];
-            int qlo, qhi;
-            valid_range(l.d.sw, l.d.pw, s, Wd, Q, qlo, qhi);
-            for (int p = 0; p < P; ++p) {
-              int ih = p * l.d.sh - l.d.ph + r;
-              if (ih < 0 || ih >= H) continue;
-              const double* xr = &x[(((size_t)s0 * C + ci) * H + ih) * Wd];
-              double* ar = &acc[(size_t)p * Q];
-              float* af = &accf[(size_t)p * Q];
-              if (M.mode == XO_FP32) {
-                for (int q = qlo; q < qhi; ++q) af[q] = std::fmaf((float)xr[q * l.d.sw - l.d.pw + s], (float)w, af[q]);
-              } else if (l.d.sw == 1) {
-                const double* xs = xr + s - l.d.pw;
-                for (int q = qlo; q < qhi; ++q) ar[q] += xs[q] * w;
-              } else {
-                for (int q = qlo; q < qhi; ++q) ar[q] += xr[q * l.d.sw - l.d.pw + s] * w;
-              }
+  const int64_t npix = (int64_t)n * P * Q;
+  const int64_t pblocks = (npix + kPix - 1) / kPix, cblocks = (K + kChan - 1) / kChan;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t task = 0; task < pblocks * cblocks; ++task) {
+    const int64_t px0 = (task / cblocks) * kPix;
+    const int c0 = (int)(task % cblocks) * kChan;
+    const int np = (int)std::min<int64_t>(kPix, npix - px0), nc = std::min(kChan, K - c0);
+    double acc[kPix][kChan] = {};
+    float accf[kPix][kChan] = {};
+    int s0v[kPix], pv[kPix], qv[kPix];
+    for (int i = 0; i < np; ++i) {
+      const int64_t px = px0 + i;
+      s0v[i] = (int)(px / ((int64_t)P * Q));
+      pv[i] = (int)(px / Q % P);
+      qv[i] = (int)(px % Q);
+    }
+    for (int ci = 0; ci < C; ++ci)
+      for (int r = 0; r < R; ++r)
+        for (int s = 0; s < S; ++s) {
+          const size_t wo = (((size_t)ci * R + r) * S + s) * K + c0;
+          for (int i = 0; i < np; ++i) {
+            const int ih = pv[i] * l.d.sh - l.d.ph + r, iw = qv[i] * l.d.sw - l.d.pw + s;
+            if (ih < 0 || ih >= H || iw < 0 || iw >= Wd) continue;
+            const double xv = x[(((size_t)s0v[i] * C + ci) * H + ih) * Wd + iw];
+            if (f32) {
+              const float xf = (float)xv;
+              const float* w = &Wtf[wo];
+              float* a = accf[i];
+              for (int co = 0; co < nc; ++co) a[co] = std::fmaf(xf, w[co], a[co]);
+            } else {
+              const double* w = &Wt[wo];
+              double* a = acc[i];
+              for (int co = 0; co < nc; ++co) a[co] += xv * w[co];
             }
           }
-      for (int pq = 0; pq < P * Q; ++pq) {
-        double v = (M.mode == XO_FP32) ? (double)accf[pq] : acc[pq];
+        }
+    for (int i = 0; i < np; ++i)
+      for (int j = 0; j < nc; ++j) {
+        const int co = c0 + j;
+        double v = f32 ? (double)accf[i][j] : acc[i][j];
         if (M.mode == XO_BF16) v = (double)(float)v;
         if (l.d.bias) v = (M.mode == XO_FP64) ? v + b[co] : (double)((float)v + (float)b[co]);
-        y[((size_t)s0 * K + co) * P * Q + pq] = M.qa(v, li);
+        y[(((size_t)s0v[i] * K + co) * P + pv[i]) * Q + qv[i]] = M.qa(v, li);
       }
-    }
+  }
 }
 
 void conv_bwd(const Model& M, int li, int n, const Vec& x, const Vec& dy, const double* W,
@@ -223,73 +255,115 @@ void conv_bwd(const Model& M, int li, int n, const Vec& x, const Vec& dy, const 
   const Layer& l = M.L[li];
   const int C = l.in0.c, H = l.in0.h, Wd = l.in0.w, K = l.d.out_c, R = l.d.kh, S = l.d.kw;
   const int P = l.out.h, Q = l.out.w;
+  const bool f32 = M.mode == XO_FP32;
   if (need_dx) {
-    /* dx[n][ci][ih][iw] = sum_{co,r,s : ih = p*sh-ph+r, iw = q*sw-pw+s} dy[n][co][p][q] W[co][ci][r][s] */
-    dx.assign((size_t)n * C * H * Wd, 0.0);
-#pragma omp parallel for collapse(2) schedule(static)
-    for (int s0 = 0; s0 < n; ++s0)
-      for (int ci = 0; ci < C; ++ci) {
-        Vec acc((size_t)H * Wd, 0.0);
-        std::vector<float> accf((size_t)H * Wd, 0.f);
-        for (int co = 0; co < K; ++co)
-          for (int r = 0; r < R; ++r)
-            for (int s = 0; s < S; ++s) {
-              double w = W[(((size_t)co * C + ci) * R + r) * S + s];
-              int qlo, qhi;
-              valid_range(l.d.sw, l.d.pw, s, Wd, Q, qlo, qhi);
-              for (int p = 0; p < P; ++p) {
-                int ih = p * l.d.sh - l.d.ph + r;
-                if (ih < 0 || ih >= H) continue;
-                const double* dyr = &dy[(((size_t)s0 * K + co) * P + p) * Q];
-                double* ar = &acc[(size_t)ih * Wd];
-                float* af = &accf[(size_t)ih * Wd];
-                if (M.mode == XO_FP32) {
-                  for (int q = qlo; q < qhi; ++q) af[q * l.d.sw - l.d.pw + s] = std::fmaf((float)dyr[q], (float)w, af[q * l.d.sw - l.d.pw + s]);
-                } else if (l.d.sw == 1) {
-                  double* as = ar + s - l.d.pw;
-                  for (int q = qlo; q < qhi; ++q) as[q] += dyr[q] * w;
-                } else {
-                  for (int q = qlo; q < qhi; ++q) ar[q * l.d.sw - l.d.pw + s] += dyr[q] * w;
-                }
-              }
-            }
-        for (int hw = 0; hw < H * Wd; ++hw) {
-          double v = (M.mode == XO_FP32) ? (double)accf[hw] : acc[hw];
-          if (M.mode == XO_BF16) v = (double)(float)v;
-          dx[((size_t)s0 * C + ci) * H * Wd + hw] = M.qg(v);
+    /* dx[n][ci][ih][iw] = sum_{co,r,s : ih = p*sh-ph+r, iw = q*sw-pw+s} dy[n][co][p][q] W[co][ci][r][s]:
+       one sequential sum per input element in (co, r, s) order over the taps that map it to an
+       output pixel; weights read from a copy laid out [co][r][s][ci] */
+    Vec Wk((size_t)K * R * S * C);
+    std::vector<float> Wkf(f32 ? Wk.size() : 0);
+    for (int co = 0; co < K; ++co)
+      for (int ci = 0; ci < C; ++ci)
+        for (int rs = 0; rs < R * S; ++rs) {
+          const double w = W[((size_t)co * C + ci) * R * S + rs];
+          Wk[((size_t)co * R * S + rs) * C + ci] = w;
+          if (f32) Wkf[((size_t)co * R * S + rs) * C + ci] = (float)w;
         }
+    dx.assign((size_t)n * C * H * Wd, 0.0);
+    const int64_t npix = (int64_t)n * H * Wd;
+    const int64_t pblocks = (npix + kPix - 1) / kPix, cblocks = (C + kChan - 1) / kChan;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t task = 0; task < pblocks * cblocks; ++task) {
+      const int64_t px0 = (task / cblocks) * kPix;
+      const int c0 = (int)(task % cblocks) * kChan;
+      const int np = (int)std::min<int64_t>(kPix, npix - px0), nc = std::min(kChan, C - c0);
+      double acc[kPix][kChan] = {};
+      float accf[kPix][kChan] = {};
+      int s0v[kPix], hv[kPix], wv[kPix];
+      for (int i = 0; i < np; ++i) {
+        const int64_t px = px0 + i;
+        s0v[i] = (int)(px / ((int64_t)H * Wd));
+        hv[i] = (int)(px / Wd % H);
+        wv[i] = (int)(px % Wd);
       }
-  }
-  /* dW[co][ci][r][s] = sum_{n,p,q} dy[n][co][p][q] x[n][ci][p*sh-ph+r][q*sw-pw+s]; every
-     dW element is one sequential sum in (n, p, q) order; the R*S sums of a (co, ci) pair
-     advance together (independent accumulators, no reordering within any sum) */
-#pragma omp parallel for collapse(2) schedule(static)
-  for (int co = 0; co < K; ++co)
-    for (int ci = 0; ci < C; ++ci) {
-      std::vector<double> acc((size_t)R * S, 0.0);
-      std::vector<float> accf((size_t)R * S, 0.f);
-      for (int s0 = 0; s0 < n; ++s0)
-        for (int p = 0; p < P; ++p)
-          for (int q = 0; q < Q; ++q) {
-            const double a = dy[(((size_t)s0 * K + co) * P + p) * Q + q];
-            for (int r = 0; r < R; ++r) {
-              const int ih = p * l.d.sh - l.d.ph + r;
-              if (ih < 0 || ih >= H) continue;
-              const double* xr = &x[(((size_t)s0 * C + ci) * H + ih) * Wd];
-              for (int s = 0; s < S; ++s) {
-                const int iw = q * l.d.sw - l.d.pw + s;
-                if (iw < 0 || iw >= Wd) continue;
-                if (M.mode == XO_FP32) accf[r * S + s] = std::fmaf((float)a, (float)xr[iw], accf[r * S + s]);
-                else acc[r * S + s] += a * xr[iw];
+      for (int co = 0; co < K; ++co)
+        for (int r = 0; r < R; ++r)
+          for (int s = 0; s < S; ++s) {
+            const size_t wo = (((size_t)co * R + r) * S + s) * C + c0;
+            for (int i = 0; i < np; ++i) {
+              const int ph_ = hv[i] + l.d.ph - r, qw_ = wv[i] + l.d.pw - s;   /* = p * sh, q * sw */
+              if (ph_ < 0 || qw_ < 0 || ph_ % l.d.sh || qw_ % l.d.sw) continue;
+              const int p = ph_ / l.d.sh, q = qw_ / l.d.sw;
+              if (p >= P || q >= Q) continue;
+              const double d = dy[(((size_t)s0v[i] * K + co) * P + p) * Q + q];
+              if (f32) {
+                const float df = (float)d;
+                const float* w = &Wkf[wo];
+                float* a = accf[i];
+                for (int j = 0; j < nc; ++j) a[j] = std::fmaf(df, w[j], a[j]);
+              } else {
+                const double* w = &Wk[wo];
+                double* a = acc[i];
+                for (int j = 0; j < nc; ++j) a[j] += d * w[j];
               }
             }
           }
-      for (int rs = 0; rs < R * S; ++rs) {
-        double v = (M.mode == XO_FP32) ? (double)accf[rs] : acc[rs];
-        if (M.mode == XO_BF16) v = (double)(float)v;
-        dW[((size_t)co * C + ci) * R * S + rs] = v;
-      }
+      for (int i = 0; i < np; ++i)
+        for (int j = 0; j < nc; ++j) {
+          double v = f32 ? (double)accf[i][j] : acc[i][j];
+          if (M.mode == XO_BF16) v = (double)(float)v;
+          dx[(((size_t)s0v[i] * C + c0 + j) * H + hv[i]) * Wd + wv[i]] = M.qg(v);
+        }
     }
+  }
+  /* dW[co][ci][r][s] = sum_{n,p,q} dy[n][co][p][q] x[n][ci][p*sh-ph+r][q*sw-pw+s]; every dW
+     element is one sequential sum in (n, p, q) order over its in-range taps; the input is read
+     from a copy laid out [n][h][w][ci] */
+  Vec xt((size_t)n * H * Wd * C);
+  for (int s0 = 0; s0 < n; ++s0)
+    for (int ci = 0; ci < C; ++ci)
+      for (int hw = 0; hw < H * Wd; ++hw)
+        xt[((size_t)s0 * H * Wd + hw) * C + ci] = x[((size_t)s0 * C + ci) * H * Wd + hw];
+  const int oblocks = (K + kOut - 1) / kOut, cblocks = (C + kChan - 1) / kChan;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int task = 0; task < oblocks * cblocks; ++task) {
+    const int o0 = (task / cblocks) * kOut, c0 = (task % cblocks) * kChan;
+    const int no = std::min(kOut, K - o0), nc = std::min(kChan, C - c0);
+    Vec acc((size_t)kOut * R * S * kChan, 0.0);
+    std::vector<float> accf((size_t)kOut * R * S * kChan, 0.f);
+    for (int s0 = 0; s0 < n; ++s0)
+      for (int p = 0; p < P; ++p)
+        for (int q = 0; q < Q; ++q)
+          for (int r = 0; r < R; ++r) {
+            const int ih = p * l.d.sh - l.d.ph + r;
+            if (ih < 0 || ih >= H) continue;
+            for (int s = 0; s < S; ++s) {
+              const int iw = q * l.d.sw - l.d.pw + s;
+              if (iw < 0 || iw >= Wd) continue;
+              const double* xr = &xt[(((size_t)s0 * H + ih) * Wd + iw) * C + c0];
+              for (int oi = 0; oi < no; ++oi) {
+                const double a = dy[(((size_t)s0 * K + o0 + oi) * P + p) * Q + q];
+                const size_t ao = (((size_t)oi * R + r) * S + s) * kChan;
+                if (f32) {
+                  const float af = (float)a;
+                  float* ac = &accf[ao];
+                  for (int j = 0; j < nc; ++j) ac[j] = std::fmaf(af, (float)xr[j], ac[j]);
+                } else {
+                  double* ac = &acc[ao];
+                  for (int j = 0; j < nc; ++j) ac[j] += a * xr[j];
+                }
+              }
+            }
+          }
+    for (int oi = 0; oi < no; ++oi)
+      for (int j = 0; j < nc; ++j)
+        for (int rs = 0; rs < R * S; ++rs) {
+          const size_t ai = ((size_t)oi * R * S + rs) * kChan + j;
+          double v = f32 ? (double)accf[ai] : acc[ai];
+          if (M.mode == XO_BF16) v = (double)(float)v;
+          dW[((size_t)(o0 + oi) * C + c0 + j) * R * S + rs] = v;
+        }
+  }
   if (l.d.bias)
     for (int co = 0; co < K; ++co) {
       double acc = 0.0;
@@ -714,6 +788,7 @@ Vec predict_stage(const xo_ctx& c, const Stage& st, int s) {
   Vec out(st.W.size());
   bool trivial = (c.H.delta_form == XO_DELTA_ADAM && st.ver == 0);
   Scalars sc = scalars(c.H, st.ver);
+#pragma omp parallel for schedule(static)
   for (size_t i = 0; i < st.W.size(); ++i) {
     if (trivial) { out[i] = c.M.mode == XO_BF16 ? q_bf16(st.W[i]) : st.W[i]; continue; }
     double d = delta(c.M.mode, c.H, sc, st.m[i], st.v[i]);
@@ -932,18 +1007,26 @@ int try_step(xo_ctx& c, int k) {
       }
       st.stash.erase(u);
       if (j == 1) st.g = gW;
-      else for (size_t i = 0; i < gW.size(); ++i) st.g[i] = c.M.add(st.g[i], gW[i]);
+      else {
+        const int64_t ng = (int64_t)gW.size();
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < ng; ++i) st.g[i] = c.M.add(st.g[i], gW[i]);
+      }
       if (k > 0) c.S[k - 1].inbox_grad[u] = std::move(din);
       trace_push(st, 1, t, j, st.cb.ver, s, j == 1);
       if (j == c.T) {
         /* the T-th micro-batch's backward ends the mini-batch: update */
         const int64_t kv = st.ver + 1;
         Scalars sc = scalars(c.H, kv);
-        if (c.H.opt == XO_OPT_SGD)
-          for (size_t i = 0; i < st.W.size(); ++i)
+        const int64_t np = (int64_t)st.W.size();  /* elementwise: each element's step is independent */
+        if (c.H.opt == XO_OPT_SGD) {
+#pragma omp parallel for schedule(static)
+          for (int64_t i = 0; i < np; ++i)
             sgd_elem(c.M.mode, c.H, sc, st.W[i], st.buf[i], st.m[i], st.v[i], st.g[i], nullptr);
-        else
-          for (size_t i = 0; i < st.W.size(); ++i) adam_elem(c.M.mode, c.H, sc, st.W[i], st.m[i], st.v[i], st.g[i], nullptr);
+        } else {
+#pragma omp parallel for schedule(static)
+          for (int64_t i = 0; i < np; ++i) adam_elem(c.M.mode, c.H, sc, st.W[i], st.m[i], st.v[i], st.g[i], nullptr);
+        }
         st.ver = (int)kv;
         trace_push(st, 2, t, j, st.ver, 0, 0);
         if (c.snapshots) st.snaps[st.ver] = st.W;

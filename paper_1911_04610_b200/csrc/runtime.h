@@ -33,6 +33,14 @@ struct Alloc { void* p; size_t bytes; int dev; };
 
 struct Snapshot { int ver; std::vector<float> W; float* pinned; };
 
+// cfg.timing: one forward/backward op of a call and the indices (into StageRT::tev) of the
+// events recorded at its input arrival, compute end, hand-off end and update end (-1 = none)
+struct TimedOp {
+  int op = 0;
+  int64_t u_rel = 0;   // micro-batch relative to the call's first fed micro-batch
+  int e[4] = {-1, -1, -1, -1};
+};
+
 struct StageRT {
   int k = 0, dev = 0;
   cudaStream_t stream = nullptr;
@@ -79,6 +87,12 @@ struct StageRT {
   std::vector<int64_t> fdone_epoch, bdone_epoch;
   cudaEvent_t ev_upd = nullptr, ev_fmark = nullptr, ev_fjoin = nullptr;
   cudaEvent_t ev_in = nullptr;          // the call's input / label copies (main stream) are done
+  // cfg.timing: per-op events (pool, reused every call and by replayed graphs) and a reference
+  // event recorded at the call's start
+  std::vector<cudaEvent_t> tev;
+  size_t tev_used = 0;
+  std::vector<TimedOp> tops;
+  cudaEvent_t ev_ref = nullptr;
   int64_t upd_epoch = -1;
   float* ws = nullptr;                  // split-K workspace (fp32)
   int64_t ws_elems = 0;
@@ -139,6 +153,7 @@ struct xpipe_ctx {
     int64_t kernels = 0;
     std::vector<int64_t> dpos, dfwd, dbwd;
     std::vector<int> dver, dfver, dbver;
+    std::vector<std::vector<xp::TimedOp>> tops;
     std::vector<std::vector<int>> prof_cls;
     std::vector<std::vector<double>> prof_work;
   };

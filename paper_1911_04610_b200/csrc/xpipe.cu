@@ -109,6 +109,9 @@ void free_all(xpipe_ctx* c) {
     if (s.diag) { cudaFreeHost(s.diag); s.diag = nullptr; }
     for (auto e : s.ev_pool) cudaEventDestroy(e);
     s.ev_pool.clear();
+    for (auto e : s.tev) cudaEventDestroy(e);
+    s.tev.clear();
+    if (s.ev_ref) { cudaEventDestroy(s.ev_ref); s.ev_ref = nullptr; }
     for (auto& v : s.ev_flag) { for (auto e : v) cudaEventDestroy(e); v.clear(); }
     for (auto& e : s.tmark) if (e) { cudaEventDestroy(e); e = nullptr; }
     // a serialised context shares stage 0's stream: destroy each stream once
@@ -184,6 +187,17 @@ int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work, cudaStream_t st) {
   s.ev_used += 2;
   s.prof_cls.push_back(cls);
   s.prof_work.push_back(work);
+  return XP_OK;
+}
+// cfg.timing: record the next timing event of stage s on stream st; *idx = its index (or -1)
+int tmark(xpipe_ctx* c, StageRT& s, cudaStream_t st, int* idx) {
+  *idx = -1;
+  if (!c->cfg.timing) return XP_OK;
+  if (s.tev_used >= s.tev.size()) return set_err(c, XP_ESCHED, "timing event pool (internal)");
+  cudaEvent_t e = s.tev[s.tev_used];
+  if (c->capturing) XP_CUDA(c, cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+  else XP_CUDA(c, cudaEventRecord(e, st));
+  *idx = (int)s.tev_used++;
   return XP_OK;
 }
 }  // namespace xp
@@ -289,6 +303,15 @@ int reserve_for_call(xpipe_ctx* c, int64_t M) {
         s.ev_pool.push_back(e);
       }
     }
+    if (c->cfg.timing) {
+      const size_t want = (size_t)4 * (2 * (M * c->T + 2 * c->K + c->T) + 8);
+      while (s.tev.size() < want) {
+        cudaEvent_t e;
+        XP_CUDA(c, cudaEventCreate(&e));
+        s.tev.push_back(e);
+      }
+      if (!s.ev_ref) XP_CUDA(c, cudaEventCreate(&s.ev_ref));
+    }
     if (c->cfg.snapshots) {
       const size_t want = (size_t)(M + c->K + 1);
       while (s.snap_pool.size() < want) {
@@ -357,12 +380,17 @@ int enqueue_forward(xpipe_ctx* c, int k, int64_t u) {
   const bool bw = (j == 1);
   cudaSetDevice(s.dev);
   // input: stage 0 stages the call's input into its stash slot; others wait for the message
+  TimedOp top;
+  top.op = 0;
+  top.u_rel = u - c->call_first;
   if (k == 0) {
+    XP_TRY(tmark(c, s, s.stream, &top.e[0]));
     const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
     const float* src = c->x_dev + (u - c->call_first) * c->n * per;
     XP_TRY(stage_input(c, s, src, s.in_slot[slot]));
   } else {
     XP_TRY(flag_wait(c, s, 0, u));
+    XP_TRY(tmark(c, s, s.stream, &top.e[0]));
   }
   TraceRec* rec = nullptr;
   XP_TRY(trace_slot(c, s, &rec));
@@ -370,13 +398,16 @@ int enqueue_forward(xpipe_ctx* c, int k, int64_t u) {
   if (bw) s.host_fver = s.host_ver;
   const void* Wf = s.pf[s.host_fver & 1];
   for (size_t o = 0; o < s.plan.ops.size(); ++o) XP_TRY(op_forward(c, s, (int)o, Wf, slot, u));
+  XP_TRY(tmark(c, s, s.stream, &top.e[1]));
   if (k + 1 < c->K) {
     StageRT& nx = c->S[k + 1];
     XP_TRY(flag_wait(c, s, 2, u - nx.S));  // ring credit: consumer released u - R
     XP_CUDA(c, cudaMemcpyAsync(nx.in_slot[(u - 1) % nx.S], s.act[s.plan.out_tensor][slot], s.plan.out_bytes,
                                cudaMemcpyDefault, s.stream));
+    XP_TRY(tmark(c, s, s.stream, &top.e[2]));
     XP_TRY(flag_write(c, s, nx, 0, u));
   }
+  if (c->cfg.timing) s.tops.push_back(top);
   if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
   if (fwd.on) XP_TRY(ev_record(c, s.stream, s.ev_fdone[slot], &s.fdone_epoch[slot]));
   return XP_OK;
@@ -392,6 +423,10 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
   const bool ov = s.fstream && s.fstream != s.stream;
   if (ov) XP_TRY(ev_wait(c, s.stream, s.ev_fdone[slot], s.fdone_epoch[slot]));  // F(u) on the forward stream
   if (k + 1 < c->K) XP_TRY(flag_wait(c, s, 1, u));
+  TimedOp top;
+  top.op = 1;
+  top.u_rel = u - c->call_first;
+  XP_TRY(tmark(c, s, s.stream, &top.e[0]));
   TraceRec* rec = nullptr;
   XP_TRY(trace_slot(c, s, &rec));
   if (rec) XP_TRY(check_launch(c, launch_trace_begin(s.ds, rec, k, 1, (int)t, (int)j, sb, bw, s.stream), "trace"));
@@ -427,12 +462,14 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     if (need0) has[O.in0] = 1;
     if (need1) has[O.in1] = 1;
   }
+  XP_TRY(tmark(c, s, s.stream, &top.e[1]));
   if (k + 1 < c->K) XP_TRY(flag_write(c, s, c->S[k + 1], 3, u));  // released gin slot u
   if (k > 0) {
     if (!has[0]) return set_err(c, XP_ESCHED, "no gradient reaches the stage input (internal)");
     StageRT& pv = c->S[k - 1];
     XP_TRY(flag_wait(c, s, 3, u - pv.S));
     XP_CUDA(c, cudaMemcpyAsync(pv.gin_slot[(u - 1) % pv.S], gp[0], P.in_bytes, cudaMemcpyDefault, s.stream));
+    XP_TRY(tmark(c, s, s.stream, &top.e[2]));
     XP_TRY(flag_write(c, s, pv, 1, u));
     XP_TRY(flag_write(c, s, pv, 2, u));  // released our input slot u
   }
@@ -477,6 +514,8 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
       s.snaps.push_back(std::move(sn));
     }
   }
+  XP_TRY(tmark(c, s, s.stream, &top.e[3]));  // the op's end: side-stream joined (+ update)
+  if (c->cfg.timing) s.tops.push_back(top);
   return XP_OK;
 }
 
@@ -640,6 +679,7 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
       c->S[k].prof_cls = g.prof_cls[k];
       c->S[k].prof_work = g.prof_work[k];
       c->S[k].ev_used = 2 * g.prof_cls[k].size();
+      c->S[k].tops = g.tops[k];                   // ... and the same timing events
     }
     return XP_OK;
   }
@@ -690,8 +730,8 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
   if (e != cudaSuccess) return set_err(c, XP_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
   g.kernels = c->kernels - k0;
   g.dpos.clear(); g.dver.clear(); g.dfver.clear(); g.dbver.clear(); g.dfwd.clear(); g.dbwd.clear();
-  g.prof_cls.clear(); g.prof_work.clear();
-  for (auto& s : c->S) { g.prof_cls.push_back(s.prof_cls); g.prof_work.push_back(s.prof_work); }
+  g.prof_cls.clear(); g.prof_work.clear(); g.tops.clear();
+  for (auto& s : c->S) { g.prof_cls.push_back(s.prof_cls); g.prof_work.push_back(s.prof_work); g.tops.push_back(s.tops); }
   for (size_t k = 0; k < c->S.size(); ++k) {
     StageRT& s = c->S[k];
     g.dpos.push_back(s.pos - pos0[k]);
@@ -702,6 +742,74 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
     g.dbver.push_back(s.host_bver - ver0[k]);
   }
   XP_CUDA(c, cudaGraphLaunch(g.exec, o.stream));
+  return XP_OK;
+}
+
+// cfg.timing: the call's span, per-stage busy time (union of op intervals), bubble fraction,
+// steady-phase rate and hand-off times, from the per-op events
+int timing_stats(xpipe_ctx* c, int64_t M, bool empty_before, bool flush, xpipe_stats* st) {
+  double t_lo = 1e300, t_hi = -1e300, busy_sum = 0;
+  int owned_n = 0, ops = 0;
+  auto at = [&](StageRT& s, int e, double* ms) -> int {
+    float v = 0;
+    XP_CUDA(c, cudaEventElapsedTime(&v, s.ev_ref, s.tev[e]));
+    *ms = v;
+    return XP_OK;
+  };
+  std::vector<double> bell;  // stage 0's bellwether forward starts, in order
+  for (auto& s : c->S) {
+    if (!owned(s)) continue;
+    ++owned_n;
+    cudaSetDevice(s.dev);
+    std::vector<std::pair<double, double>> iv;
+    double pf = 0, pb = 0, bf = 0, bb = 0;
+    for (const TimedOp& o : s.tops) {
+      if (o.e[0] < 0) continue;
+      double t0, t1 = 0, t2 = 0, tend = 0;
+      XP_TRY(at(s, o.e[0], &t0));
+      if (o.e[1] >= 0) XP_TRY(at(s, o.e[1], &t1));
+      tend = t1;
+      if (o.e[2] >= 0) {
+        XP_TRY(at(s, o.e[2], &t2));
+        tend = t2;
+        if (o.op == 0) { pf += t2 - t1; bf += (double)s.plan.out_bytes; }
+        else { pb += t2 - t1; bb += (double)s.plan.in_bytes; }
+      }
+      if (o.e[3] >= 0) { double t3; XP_TRY(at(s, o.e[3], &t3)); tend = std::max(tend, t3); }
+      iv.push_back({t0, tend});
+      t_lo = std::min(t_lo, t0);
+      t_hi = std::max(t_hi, tend);
+      ++ops;
+      if (s.k == 0 && o.op == 0) {
+        const int64_t u = o.u_rel + c->call_first;
+        if ((u - 1) % c->T == 0 && o.u_rel >= 0) bell.push_back(t0);
+      }
+    }
+    std::sort(iv.begin(), iv.end());
+    double busy = 0, a = -1e300, b = -1e300;
+    for (auto& p : iv) {
+      if (p.first > b) { if (b > a) busy += b - a; a = p.first; b = p.second; }
+      else b = std::max(b, p.second);
+    }
+    if (b > a) busy += b - a;
+    busy_sum += busy;
+    if (s.k < XP_STATS_STAGES) {
+      st->busy_ms[s.k] = busy;
+      st->p2p_fwd_ms[s.k] = pf; st->p2p_bwd_ms[s.k] = pb;
+      st->p2p_fwd_bytes[s.k] = bf; st->p2p_bwd_bytes[s.k] = bb;
+    }
+  }
+  st->ops_timed = ops;
+  st->span_ms = t_hi > t_lo ? t_hi - t_lo : 0;
+  st->bubble_fraction = st->span_ms > 0 ? 1.0 - busy_sum / (owned_n * st->span_ms) : 0;
+  // steady phase: drop the warm-up (first K mini-batches after an empty pipeline) and the drain
+  // (last K mini-batches of a flushing call)
+  const size_t lo = empty_before ? (size_t)c->K : 0;
+  const size_t hi = bell.size() >= (flush ? (size_t)c->K : 0) ? bell.size() - (flush ? (size_t)c->K : 0) : 0;
+  st->steady_samples_per_s = 0;
+  if (hi > lo + 1 && bell[hi - 1] > bell[lo])
+    st->steady_samples_per_s = (double)(hi - 1 - lo) * c->N / ((bell[hi - 1] - bell[lo]) * 1e-3);
+  (void)M;
   return XP_OK;
 }
 
@@ -929,8 +1037,19 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     c->call_first = c->fed + 1;
     c->fed += (int64_t)M * c->T;
   }
-  for (auto& s : c->S) { s.ev_used = 0; s.prof_cls.clear(); s.prof_work.clear(); }
+  for (auto& s : c->S) { s.ev_used = 0; s.prof_cls.clear(); s.prof_work.clear(); s.tev_used = 0; s.tops.clear(); }
   XP_TRY(reserve_for_call(c, M));
+  const bool empty_before = c->fed - (int64_t)M * c->T == c->base;  // pipeline empty at the call's start
+  if (c->cfg.timing) {
+    // reference events: every stream is drained, so all devices start the call together
+    const bool graph = graph_eligible(c, flags, M, c->fed - (int64_t)M * c->T);
+    for (auto& s : c->S) {
+      if (!owned(s)) continue;
+      StageRT& rs = graph ? c->S[0] : s;
+      cudaSetDevice(rs.dev);
+      XP_CUDA(c, cudaEventRecord(s.ev_ref, rs.stream));
+    }
+  }
   const int64_t fed_before = c->fed - (int64_t)M * c->T;
   if (graph_eligible(c, flags, M, fed_before)) XP_TRY(drive_graph(c, M, fed_before));
   else XP_TRY(drive(c, -1));
@@ -961,6 +1080,10 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     st->kernel_launches = c->kernels - k0;
     st->graph_replays = c->graph_replays - g0;
     st->span_ms = 0;
+    st->bubble_fraction = st->steady_samples_per_s = 0;
+    st->ops_timed = 0;
+    for (int q = 0; q < XP_STATS_STAGES; ++q)
+      st->busy_ms[q] = st->p2p_fwd_ms[q] = st->p2p_bwd_ms[q] = st->p2p_fwd_bytes[q] = st->p2p_bwd_bytes[q] = 0;
     for (int q = 0; q < XP_PROF_N; ++q) { st->prof_ms[q] = 0; st->prof_launches[q] = 0; st->prof_work[q] = 0; }
     if (c->cfg.profile && !(flags & XP_ASYNC)) {
       for (auto& s : c->S) {
@@ -974,6 +1097,7 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
         }
       }
     }
+    if (c->cfg.timing && !(flags & XP_ASYNC)) XP_TRY(timing_stats(c, M, empty_before, (flags & XP_FLUSH) != 0, st));
     if (st->losses && M > 0 && !(flags & XP_ASYNC) && owned(c->S[c->K - 1])) {
       cudaSetDevice(c->S[c->K - 1].dev);
       XP_CUDA(c, cudaMemcpy(st->losses, c->loss_dev, (size_t)M * c->T * 4, cudaMemcpyDeviceToHost));

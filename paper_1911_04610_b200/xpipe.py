@@ -45,7 +45,8 @@ class Config(C.Structure):
                 ("init_v", C.POINTER(C.POINTER(C.c_float))),
                 ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", C.c_void_p),
                 ("optimizer", C.c_int32), ("momentum", C.c_float), ("weight_decay", C.c_float),
-                ("recompute", C.c_int32), ("serialize", C.c_int32), ("fb_overlap", C.c_int32)]
+                ("recompute", C.c_int32), ("serialize", C.c_int32), ("fb_overlap", C.c_int32),
+                ("timing", C.c_int32)]
 
 
 class TraceRec(C.Structure):
@@ -58,10 +59,26 @@ PROF_CLASSES = ("sweep", "conv_fprop", "conv_dgrad", "conv_wgrad", "bn_stats", "
 BYTE_CLASSES = ("sweep", "bn_stats", "bn_apply", "bn_bwd_reduce", "bn_bwd_apply")  # work in bytes (else flops)
 
 
+STATS_STAGES = 16
+
+
 class Stats(C.Structure):
     _fields_ = [("span_ms", C.c_double), ("prof_ms", C.c_double * 8), ("prof_launches", C.c_int64 * 8),
                 ("prof_work", C.c_double * 8), ("kernel_launches", C.c_int64), ("graph_replays", C.c_int64),
-                ("losses", C.POINTER(C.c_float))]
+                ("losses", C.POINTER(C.c_float)),
+                ("busy_ms", C.c_double * STATS_STAGES), ("bubble_fraction", C.c_double),
+                ("steady_samples_per_s", C.c_double),
+                ("p2p_fwd_ms", C.c_double * STATS_STAGES), ("p2p_bwd_ms", C.c_double * STATS_STAGES),
+                ("p2p_fwd_bytes", C.c_double * STATS_STAGES), ("p2p_bwd_bytes", C.c_double * STATS_STAGES),
+                ("ops_timed", C.c_int64)]
+
+    def timing(self, K):
+        """cfg.timing fields as a dict (stages 0..K-1)."""
+        k = min(K, STATS_STAGES)
+        return dict(span_ms=self.span_ms, busy_ms=list(self.busy_ms[:k]), bubble_fraction=self.bubble_fraction,
+                    steady_samples_per_s=self.steady_samples_per_s, p2p_fwd_ms=list(self.p2p_fwd_ms[:k]),
+                    p2p_bwd_ms=list(self.p2p_bwd_ms[:k]), p2p_fwd_bytes=list(self.p2p_fwd_bytes[:k]),
+                    p2p_bwd_bytes=list(self.p2p_bwd_bytes[:k]), ops_timed=self.ops_timed)
 
     def profile(self):
         return {n: dict(ms=self.prof_ms[i], launches=self.prof_launches[i], work=self.prof_work[i])
@@ -144,7 +161,7 @@ class XPipe:
                  precision="fp32", schedule="xpipe", predict=None, s_fwd=0, s_bwd=0, delta="adam",
                  init_m=None, init_v=None, devices=None, snapshots=False, trace=False, graphs=False, profile=False,
                  seed=1, watchdog_ms=0, torch_allocator=True, my_stage=None, optimizer="adam", momentum=0.9,
-                 weight_decay=5e-4, recompute=False, serialize=False, fb_overlap=False):
+                 weight_decay=5e-4, recompute=False, serialize=False, fb_overlap=False, timing=False):
         self.h = None
         L = lib()
         if predict is None:  # GPipe runs under the current weights (no prediction)
@@ -162,7 +179,7 @@ class XPipe:
                      multi_process=int(my_stage is not None), my_stage=my_stage or 0,
                      optimizer=OPTIMIZER[optimizer], momentum=momentum if optimizer == "sgd" else 0.0,
                      weight_decay=weight_decay if optimizer == "sgd" else 0.0, recompute=int(recompute),
-                     serialize=int(serialize), fb_overlap=int(fb_overlap))
+                     serialize=int(serialize), fb_overlap=int(fb_overlap), timing=int(timing))
         if devices:
             cfg.n_devices = len(devices)
             for i, d in enumerate(devices):

@@ -35,3 +35,16 @@ def predict_from_state(W, m, v, k, s, lr, b1, b2, eps, bf16=True):
     # fmaf(-s, d, W): -s*d is exact in double and the double sum is exact here -> one rounding
     p = (-(float(s)) * d.astype(np.float64) + W.astype(np.float64)).astype(np.float32)
     return bf16_round(p) if bf16 else p
+
+
+def log_parity(name, **fields):
+    """Append one parity record (relFrob curves, margins) as a JSON line to $XPIPE_PARITY_LOG
+    when set, so GPU runs can bring the curves back for profiles/."""
+    import json
+    import os
+    path = os.environ.get("XPIPE_PARITY_LOG")
+    if not path:
+        return
+    os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+    with open(path, "a") as f:
+        f.write(json.dumps(dict(test=name, **fields)) + "\n")

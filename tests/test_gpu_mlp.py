@@ -149,9 +149,10 @@ def test_fb_overlap_bit_exact(oracle_mod, K, T, schedule):
     L = S.mlp()
     P = S.make_params(L, 1)
     N, M = 32, 8
+    pred = "off" if schedule == "gpipe" else "paper"  # GPipe runs under the current weights
     x, y = S.make_inputs(M * N, (784, 1, 1), 10, 1, kind="mnist")
     o = oracle_mod.Oracle(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, P, mode="fp32", schedule=schedule,
-                          snapshots=True)
+                          predict=pred, snapshots=True)
     g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, params=P, precision="fp32", trace=True,
               snapshots=True, schedule=schedule, fb_overlap=True, watchdog_ms=20000)
     lo = o.step(x, y, M, flush=True)
@@ -165,7 +166,8 @@ def test_fb_overlap_bit_exact(oracle_mod, K, T, schedule):
     # CUDA-graph replay of steady-state calls with the overlap
     g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, params=P, precision="fp32", graphs=True,
               schedule=schedule, fb_overlap=True, watchdog_ms=20000)
-    o = oracle_mod.Oracle(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, P, mode="fp32", schedule=schedule)
+    o = oracle_mod.Oracle(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, P, mode="fp32", schedule=schedule,
+                          predict=pred)
     xs, ys = S.make_inputs(12 * N, (784, 1, 1), 10, 3, kind="mnist")
     reps = 0
     for i in range(12):

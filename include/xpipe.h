@@ -62,6 +62,13 @@ enum { XP_MOM_ZERO = 0, XP_MOM_GIVEN = 1 /* cfg.init_m / cfg.init_v (e.g. 1e-4*U
    the prediction keeps its own Eq. (4) moments of the raw gradient and uses the
    literal Eq. (3)/(4) dW, so it requires delta_form = XP_DELTA_PAPER. */
 enum { XP_OPT_ADAM = 0, XP_OPT_MOMENTUM_SGD = 1 };
+/* where the backward's predicted weights W_hat_b come from (the bellwether makes the
+   prediction and caches it for the other T-1 micro-batches of its pass):
+   XP_WBWD_MATERIALIZE -- the update sweep writes W_hat_b of the new version (32 B/param sweep);
+   XP_WBWD_BELLWETHER  -- the update sweep writes W_hat_f only (30 B/param) and the backward
+   bellwether B(t,1) computes W_hat_b from the stage's current W, m, v (one 14 B/param pass:
+   read W, m, v, write bf16 W_hat_b), bit-identical to the materialised values. */
+enum { XP_WBWD_MATERIALIZE = 0, XP_WBWD_BELLWETHER = 1 };
 enum { XP_TRANSPORT_P2P = 0 };  /* the producer stream copies its boundary tensor into the consumer's
                                    ring slot with the copy engine (cudaMemcpyAsync, same device or
                                    NVLink peer, or a CUDA-IPC-mapped slot in multi-process mode),
@@ -136,10 +143,14 @@ typedef struct {
                                          F(u+S) overlaps B(u) (one more ring/stash slot per stage;
                                          ordering by events: F(u) -> B(u), B(u) -> F(u+S+1),
                                          update -> next bellwether forward); same results */
-  int32_t timing;                     /* 1 = time every forward/backward op with CUDA events on the
-                                         stream it runs on (also inside replayed graphs) and fill
-                                         the span / busy / bubble / steady-rate / hand-off fields
-                                         of xpipe_stats; no per-op kernels are added */
+  int32_t timing;                     /* p > 0: every p-th xpipe_step call (the first, p+1-th, ...) stamps
+                                         each forward/backward op with %globaltimer on the stream it
+                                         runs on (1-thread kernels at its start and end, and around the
+                                         hand-off of bellwether micro-batches; also inside replayed
+                                         graphs, which exist per variant) and fills the span / busy /
+                                         bubble / steady-rate / hand-off fields of xpipe_stats
+                                         (ops_timed = 0 on the other calls); 0 = off */
+  int32_t wbwd;                       /* XP_WBWD_MATERIALIZE (default) | XP_WBWD_BELLWETHER */
 } xpipe_config;
 
 /* one device-trace record (K12): op 0 = forward, 1 = backward, 2 = update.  version is the
@@ -164,9 +175,8 @@ enum { XP_PROF_SWEEP = 0,       /* K1: work = algorithmic bytes */
 #define XP_STATS_STAGES 16
 typedef struct {
   double span_ms;                    /* cfg.timing: device time from the first op start to the last
-                                        op end of this call over the process's stages (per-device
-                                        CUDA events; devices aligned at the call's start, every call
-                                        begins with a drained pipeline); else 0 */
+                                        op end of this call over the process's stages (%globaltimer);
+                                        else 0 */
   double prof_ms[XP_PROF_N];         /* summed device time per kernel class (cfg.profile) */
   int64_t prof_launches[XP_PROF_N];
   double prof_work[XP_PROF_N];       /* algorithmic bytes (sweep, BN) or flops (GEMM classes) */
@@ -182,8 +192,11 @@ typedef struct {
                                         on stage 0 (0 if stage 0 is not owned or too few); the first
                                         K mini-batches after an empty pipeline and the last K of a
                                         flushing call are excluded (warm-up / drain) */
-  double p2p_fwd_ms[XP_STATS_STAGES];   /* stage k: summed time of its activation hand-offs k->k+1 */
-  double p2p_bwd_ms[XP_STATS_STAGES];   /* stage k: summed time of its gradient hand-offs k->k-1 */
+  /* hand-off times, sampled on the bellwether micro-batches (1 in T; the other messages are
+     the same size): stage k's activation messages k->k+1 and gradient messages k->k-1, summed
+     time and bytes over the sampled messages (GB/s = bytes / time) */
+  double p2p_fwd_ms[XP_STATS_STAGES];
+  double p2p_bwd_ms[XP_STATS_STAGES];
   double p2p_fwd_bytes[XP_STATS_STAGES];
   double p2p_bwd_bytes[XP_STATS_STAGES];
   int64_t ops_timed;                 /* forward + backward ops timed in this call */

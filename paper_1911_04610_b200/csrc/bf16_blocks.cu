@@ -125,12 +125,20 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       const ConvGeo g = conv_geo(c, O, L);
       const LayerInfo& N = c->net.layers[O.lbn];
       const PoolGeo p = pool_geo(c, O.lpool);
-      // gradient buffer: alternate between two so the side-stream wgrad of this op can overlap
-      // the next op's BN backward; before reuse, wait for the wgrad two ops back
+      // gradient of the conv output.  Batched weight gradients: this micro-batch's slot of the
+      // op's per-mini-batch buffer [T][n*P*Q*Co].  Otherwise alternate between two scratch
+      // buffers so the side-stream wgrad of this op can overlap the next op's BN backward;
+      // before reuse, wait for the wgrad two ops back
       const int b = s.gsel;
-      s.gsel ^= 1;
-      bf16* dmid = (bf16*)(b ? s.gmid1 : s.gmid);
-      if (s.gdone_valid[b]) XP_CUDA(c, cudaStreamWaitEvent(s.stream, s.ev_gdone[b], 0));
+      bf16* dmid;
+      const int64_t mid_elems = (int64_t)n * O.smid.size();
+      if (s.wbatch) {
+        dmid = (bf16*)s.dmid_all[o] + (int64_t)(s.cur_j - 1) * mid_elems;
+      } else {
+        s.gsel ^= 1;
+        dmid = (bf16*)(b ? s.gmid1 : s.gmid);
+        if (s.gdone_valid[b]) XP_CUDA(c, cudaStreamWaitEvent(s.stream, s.ev_gdone[b], 0));
+      }
       const bf16* xmid = (const bf16*)s.mid[o][slot];
       const bf16* yout = (const bf16*)s.act[O.out][slot];
       const uint8_t* pw8 = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
@@ -151,20 +159,36 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
                                                  p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws, dmid, s.stream),
                           "bn_bwd_apply"));
       XP_TRY(prof_end(c, s, XP_PROF_BN_BWD_APPLY, pass_bytes + 2.0 * mid_e));
-      // fork: the weight gradient (accumulated into g, read only by the update) on the side stream
-      XP_CUDA(c, cudaEventRecord(s.ev_fork, s.stream));
-      XP_CUDA(c, cudaStreamWaitEvent(s.side, s.ev_fork, 0));
-      XP_TRY(prof_begin(c, s, s.side));
-      if (o < (int)s.cols.size() && !s.cols[o].empty())
-        XP_TRY(check_launch(c, tc_im2col_wgrad(g, (const bf16*)s.cols[o][slot], dmid, s.g + L.woff, accumulate_g,
+      // fork: the weight gradient (into g, read only by the update) on the side stream.
+      // Batched: once per mini-batch, after the T-th micro-batch's conv-output gradient, as one
+      // GEMM over the T micro-batches (K = T*n*P*Q; g stored, "accumulate, then apply")
+      if (!s.wbatch || s.cur_j == c->T) {
+        XP_CUDA(c, cudaEventRecord(s.ev_fork, s.stream));
+        XP_CUDA(c, cudaStreamWaitEvent(s.side, s.ev_fork, 0));
+        ConvGeo gw = g;
+        int wslot = slot;
+        const bf16* wdy = dmid;
+        bool wacc = accumulate_g;
+        if (s.wbatch) {
+          gw.Nimg = n * c->T;
+          wslot = s.cur_slot0;
+          wdy = (const bf16*)s.dmid_all[o];
+          wacc = false;
+        }
+        XP_TRY(prof_begin(c, s, s.side));
+        if (o < (int)s.cols.size() && !s.cols[o].empty())
+          XP_TRY(check_launch(c, tc_im2col_wgrad(gw, (const bf16*)s.cols[o][wslot], wdy, s.g + L.woff, wacc,
+                                                 s.ws_side, s.ws_elems, s.ctr_side, s.side), "conv_wgrad"));
+        else
+          XP_TRY(check_launch(c, tc_conv_wgrad(gw, (const bf16*)s.act[O.in0][wslot], wdy, s.g + L.woff, wacc,
                                                s.ws_side, s.ws_elems, s.ctr_side, s.side), "conv_wgrad"));
-      else
-        XP_TRY(check_launch(c, tc_conv_wgrad(g, (const bf16*)s.act[O.in0][slot], dmid, s.g + L.woff, accumulate_g,
-                                             s.ws_side, s.ws_elems, s.ctr_side, s.side), "conv_wgrad"));
-      XP_TRY(prof_end(c, s, XP_PROF_CONV_WGRAD, conv_flops(g, L.in0.c), s.side));
-      XP_CUDA(c, cudaEventRecord(s.ev_gdone[b], s.side));
-      s.gdone_valid[b] = true;
-      s.side_used = true;
+        XP_TRY(prof_end(c, s, XP_PROF_CONV_WGRAD, conv_flops(gw, L.in0.c), s.side));
+        if (!s.wbatch) {
+          XP_CUDA(c, cudaEventRecord(s.ev_gdone[b], s.side));
+          s.gdone_valid[b] = true;
+        }
+        s.side_used = true;
+      }
       if (dx0) {
         XP_TRY(prof_begin(c, s));
         XP_TRY(check_launch(c, tc_conv_dgrad(g, O.sin0.c, dmid, W + L.woff, (bf16*)dx0, s.ws, s.ws_elems, s.ctr,

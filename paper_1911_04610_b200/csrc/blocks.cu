@@ -31,6 +31,8 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
   s.W = (float*)A(P * 4); s.g = (float*)A(P * 4); s.m = (float*)A(P * 4); s.v = (float*)A(P * 4);
   s.pf[0] = A(P * pes); s.pf[1] = A(P * pes); s.pb = A(P * pes);
   s.ds = (DevState*)A(sizeof(DevState));
+  s.dbase = (int64_t*)A(64);
+  if (!s.dbase) return set_err(c, XP_ENOMEM, "arena");
   s.flags = (uint32_t*)dmalloc_shared(c, 64, s.dev);
   if (!s.W || !s.g || !s.m || !s.v || !s.pf[0] || !s.pf[1] || !s.pb || !s.ds || !s.flags)
     return set_err(c, XP_ENOMEM, "arena");
@@ -38,7 +40,9 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
   XP_CUDA(c, cudaMemsetAsync(s.flags, 0, 64, s.stream));
   const int n = c->n;
   // rings: one contiguous allocation each (one IPC handle per ring in multi-process mode)
-  s.in_stride = (p.in_slot_bytes + 255) & ~size_t(255);
+  // batched weight gradients read T consecutive slots as one [T*n][H][W][C] tensor: slots are
+  // packed at exactly the slot size (a multiple of 16 bytes for bf16 NHWC with C % 8 == 0)
+  s.in_stride = s.wbatch ? ((p.in_slot_bytes + 15) & ~size_t(15)) : ((p.in_slot_bytes + 255) & ~size_t(255));
   s.gin_stride = (p.out_bytes + 255) & ~size_t(255);
   uint8_t* ring = (uint8_t*)dmalloc_shared(c, s.in_stride * s.S, s.dev);
   if (!ring) return set_err(c, XP_ENOMEM, "input ring");
@@ -58,8 +62,11 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
   s.grad.assign(p.tensors.size(), nullptr);
   for (size_t t = 1; t < p.tensors.size(); ++t) {
     const TensorInfo& T = p.tensors[t];
+    const size_t bytes = ((size_t)n * T.shape.size() * T.es + 15) & ~size_t(15);
+    uint8_t* base = (uint8_t*)A(bytes * s.S);  // the S slots of one tensor, packed
+    if (!base) return set_err(c, XP_ENOMEM, "stash");
     s.act[t].resize(s.S);
-    for (auto& q : s.act[t]) if (!(q = A((size_t)n * T.shape.size() * T.es))) return set_err(c, XP_ENOMEM, "stash");
+    for (int i = 0; i < s.S; ++i) s.act[t][i] = base + i * bytes;
   }
   // activation-gradient buffers, one per tensor (reused by every backward pass, stream-ordered)
   for (size_t t = 0; t < p.tensors.size(); ++t) {
@@ -81,7 +88,13 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
       if (s.cols.size() < p.ops.size()) s.cols.assign(p.ops.size(), {});
       s.cols[o].resize(s.S);
       const size_t cb = (size_t)n * O.smid.h * O.smid.w * LC.d.kh * LC.d.kw * LC.cin_pad * 2;
-      for (auto& q : s.cols[o]) if (!(q = A(cb))) return set_err(c, XP_ENOMEM, "im2col");
+      uint8_t* base = (uint8_t*)A(cb * s.S);  // packed slots (batched wgrad reads T of them)
+      if (!base) return set_err(c, XP_ENOMEM, "im2col");
+      for (int i = 0; i < s.S; ++i) s.cols[o][i] = base + i * cb;
+    }
+    if (s.wbatch) {
+      if (s.dmid_all.size() < p.ops.size()) s.dmid_all.assign(p.ops.size(), nullptr);
+      if (!(s.dmid_all[o] = A((size_t)c->T * n * O.smid.size() * 2))) return set_err(c, XP_ENOMEM, "wgrad operands");
     }
     if (O.lpool >= 0) {
       s.pidx[o].resize(s.S);
@@ -104,6 +117,11 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
       const LayerInfo& L = c->net.layers[O.lmain];
       ConvGeo g{n, O.sin0.h, O.sin0.w, L.cin_pad, L.d.out_c, L.d.kh, L.d.kw, O.smid.h, O.smid.w, L.d.sh, L.d.sw, L.d.ph, L.d.pw};
       ws = std::max(ws, tc_conv_ws_elems(g));
+      if (s.wbatch) {  // the batched weight gradient: one GEMM over T micro-batches
+        ConvGeo gb = g;
+        gb.Nimg = n * c->T;
+        ws = std::max(ws, tc_conv_ws_elems(gb));
+      }
       const int Mmid = n * O.smid.h * O.smid.w;
       bnws = std::max(bnws, bn_ws_floats(Mmid, O.smid.c));
       bnws = std::max(bnws, (size_t)((Mmid + 127) / 128) * 2 * O.smid.c);  // fprop-epilogue partials

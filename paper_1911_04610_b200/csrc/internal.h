@@ -54,6 +54,11 @@ void host_scalars(int64_t k, float lr, float b1, float b2, float eps, SweepScala
 cudaError_t launch_trace_begin(DevState* ds, TraceRec* rec, int stage, int op, int t, int j, int s, int bw,
                                cudaStream_t st);
 cudaError_t launch_trace_end(TraceRec* rec, cudaStream_t st);
+cudaError_t launch_stamp(uint64_t* dst, cudaStream_t st);
+// ring flags inside graphs of the one-process-per-GPU mode: wait until / write *base + rel
+cudaError_t launch_flag_wait(const uint32_t* flag, const int64_t* base, int32_t rel, cudaStream_t st);
+cudaError_t launch_flag_write(uint32_t* flag, const int64_t* base, int32_t rel, cudaStream_t st);
+cudaError_t launch_set_i64(int64_t* dst, int64_t v, cudaStream_t st);  // *dst = %globaltimer after the stream's prior work
 cudaError_t launch_rebase_flags(uint32_t* flags, int n, uint32_t delta, cudaStream_t st);
 cudaError_t launch_fill_uniform(float* dst, int64_t n, float bound, uint64_t seed, uint64_t stream_id,
                                 cudaStream_t st);

@@ -34,6 +34,40 @@ __global__ void trace_begin_kernel(DevState* ds, TraceRec* rec, int stage, int o
   rec->t1_ns = 0;
 }
 
+// Ring flags inside CUDA graphs of the one-process-per-GPU mode.  The flags hold absolute
+// micro-batch indices written by other processes, so a captured graph cannot bake the values
+// in: the graph stores them relative to *base (the call's first micro-batch minus 1, set by a
+// kernel launched before every replay) and these 1-thread kernels wait / write base + rel.
+// flag_wait spins (acquire, system scope, wraparound-safe >=) with a nanosleep backoff.
+__global__ void flag_wait_kernel(const uint32_t* flag, const int64_t* base, int32_t rel) {
+  pdl_wait();
+  const uint32_t want = (uint32_t)(*base + rel);
+  unsigned ns = 32;
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int32_t)(v - want) >= 0) break;
+    __nanosleep(ns);
+    if (ns < 1024) ns *= 2;
+  }
+}
+__global__ void flag_write_kernel(uint32_t* flag, const int64_t* base, int32_t rel) {
+  pdl_wait();
+  __threadfence_system();
+  const uint32_t v = (uint32_t)(*base + rel);
+  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(flag), "r"(v) : "memory");
+}
+__global__ void set_i64_kernel(int64_t* dst, int64_t v) {
+  pdl_wait();
+  *dst = v;
+}
+
+// cfg.timing: one %globaltimer stamp after the preceding work of the stream (1 thread)
+__global__ void stamp_kernel(uint64_t* dst) {
+  pdl_wait();
+  *dst = globaltimer();
+}
+
 __global__ void trace_end_kernel(TraceRec* rec) {
   pdl_wait(); rec->t1_ns = globaltimer(); }
 
@@ -206,6 +240,24 @@ cudaError_t launch_trace_begin(DevState* ds, TraceRec* rec, int stage, int op, i
 
 cudaError_t launch_rebase_flags(uint32_t* flags, int n, uint32_t delta, cudaStream_t st) {
   launch_pdl(rebase_flags_kernel, dim3(1), dim3(32), 0, st, flags, n, delta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flag_wait(const uint32_t* flag, const int64_t* base, int32_t rel, cudaStream_t st) {
+  launch_pdl(flag_wait_kernel, dim3(1), dim3(1), 0, st, flag, base, rel);
+  return cudaGetLastError();
+}
+cudaError_t launch_flag_write(uint32_t* flag, const int64_t* base, int32_t rel, cudaStream_t st) {
+  launch_pdl(flag_write_kernel, dim3(1), dim3(1), 0, st, flag, base, rel);
+  return cudaGetLastError();
+}
+cudaError_t launch_set_i64(int64_t* dst, int64_t v, cudaStream_t st) {
+  launch_pdl(set_i64_kernel, dim3(1), dim3(1), 0, st, dst, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stamp(uint64_t* dst, cudaStream_t st) {
+  launch_pdl(stamp_kernel, dim3(1), dim3(1), 0, st, dst);
   return cudaGetLastError();
 }
 

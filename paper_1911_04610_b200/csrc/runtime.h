@@ -33,8 +33,8 @@ struct Alloc { void* p; size_t bytes; int dev; };
 
 struct Snapshot { int ver; std::vector<float> W; float* pinned; };
 
-// cfg.timing: one forward/backward op of a call and the indices (into StageRT::tev) of the
-// events recorded at its input arrival, compute end, hand-off end and update end (-1 = none)
+// cfg.timing: one forward/backward op of a call and the indices (into StageRT::tstamp) of the
+// stamps taken at its input arrival, compute end, hand-off end and op end (-1 = none)
 struct TimedOp {
   int op = 0;
   int64_t u_rel = 0;   // micro-batch relative to the call's first fed micro-batch
@@ -51,8 +51,15 @@ struct StageRT {
   void* pf[2] = {nullptr, nullptr};
   void* pb = nullptr;
   DevState* ds = nullptr;
+  int64_t* dbase = nullptr;             // multi-process graphs: the call's micro-batch base (device)
   uint32_t* flags = nullptr;            // [0] act_ready [1] grad_ready [2] act_ack [3] grad_ack
   int S = 1;                            // stash slots (max micro-batches in flight)
+  // batched weight gradients (bf16 conv stages): a conv op's wgrad runs once per mini-batch, at
+  // B(t,T), as one GEMM over the T micro-batches' stashed inputs (T consecutive, contiguous ring
+  // slots: S is a multiple of T) and their conv-output gradients (dmid_all[op], [T][n*P*Q*Co])
+  bool wbatch = false;
+  std::vector<void*> dmid_all;          // [op] conv-output gradients of the mini-batch's T micro-batches
+  int cur_j = 1, cur_slot0 = 0;         // the backward being enqueued: its j and its mini-batch's first slot
   void* in_ring = nullptr;              // contiguous ring allocations (IPC-exportable)
   void* gin_ring = nullptr;
   size_t in_stride = 0, gin_stride = 0;
@@ -87,12 +94,12 @@ struct StageRT {
   std::vector<int64_t> fdone_epoch, bdone_epoch;
   cudaEvent_t ev_upd = nullptr, ev_fmark = nullptr, ev_fjoin = nullptr;
   cudaEvent_t ev_in = nullptr;          // the call's input / label copies (main stream) are done
-  // cfg.timing: per-op events (pool, reused every call and by replayed graphs) and a reference
-  // event recorded at the call's start
-  std::vector<cudaEvent_t> tev;
-  size_t tev_used = 0;
+  // cfg.timing: per-op %globaltimer stamps (device buffer reused every call and by replayed
+  // graphs, pinned host mirror) and the ops they belong to
+  uint64_t* tstamp = nullptr;
+  uint64_t* tstamp_host = nullptr;
+  size_t tstamp_cap = 0, tev_used = 0;
   std::vector<TimedOp> tops;
-  cudaEvent_t ev_ref = nullptr;
   int64_t upd_epoch = -1;
   float* ws = nullptr;                  // split-K workspace (fp32)
   int64_t ws_elems = 0;
@@ -154,6 +161,7 @@ struct xpipe_ctx {
     std::vector<int64_t> dpos, dfwd, dbwd;
     std::vector<int> dver, dfver, dbver;
     std::vector<std::vector<xp::TimedOp>> tops;
+    std::vector<size_t> tev_used;
     std::vector<std::vector<int>> prof_cls;
     std::vector<std::vector<double>> prof_work;
   };
@@ -166,6 +174,9 @@ struct xpipe_ctx {
   uint32_t* status_dev = nullptr;       // last stage: XP_STATUS_* bits set by the loss kernel
   uint32_t* status_host = nullptr;      // pinned mirror read after a synchronous call
   std::vector<int64_t> cap_fwd0, cap_bwd0;  // enqueue counters when the capture started
+  int64_t cap_base = 0;                 // multi-process capture: fed_before of the captured call
+  int64_t calls = 0;                    // xpipe_step calls so far (cfg.timing sampling)
+  bool timed = false;                   // this call is stamped (cfg.timing)
   std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)
 };
 

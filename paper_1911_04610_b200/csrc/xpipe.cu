@@ -109,9 +109,7 @@ void free_all(xpipe_ctx* c) {
     if (s.diag) { cudaFreeHost(s.diag); s.diag = nullptr; }
     for (auto e : s.ev_pool) cudaEventDestroy(e);
     s.ev_pool.clear();
-    for (auto e : s.tev) cudaEventDestroy(e);
-    s.tev.clear();
-    if (s.ev_ref) { cudaEventDestroy(s.ev_ref); s.ev_ref = nullptr; }
+    if (s.tstamp_host) { cudaFreeHost(s.tstamp_host); s.tstamp_host = nullptr; }
     for (auto& v : s.ev_flag) { for (auto e : v) cudaEventDestroy(e); v.clear(); }
     for (auto& e : s.tmark) if (e) { cudaEventDestroy(e); e = nullptr; }
     // a serialised context shares stage 0's stream: destroy each stream once
@@ -189,20 +187,35 @@ int prof_end(xpipe_ctx* c, StageRT& s, int cls, double work, cudaStream_t st) {
   s.prof_work.push_back(work);
   return XP_OK;
 }
-// cfg.timing: record the next timing event of stage s on stream st; *idx = its index (or -1)
-int tmark(xpipe_ctx* c, StageRT& s, cudaStream_t st, int* idx) {
+// cfg.timing: take the next %globaltimer stamp of stage s on stream st (a 1-thread kernel after
+// the stream's prior work; inside a captured graph it is replayed with the same slot);
+// *idx = its slot (or -1 when timing is off or `want` is false)
+int tmark(xpipe_ctx* c, StageRT& s, cudaStream_t st, int* idx, bool want = true) {
   *idx = -1;
-  if (!c->cfg.timing) return XP_OK;
-  if (s.tev_used >= s.tev.size()) return set_err(c, XP_ESCHED, "timing event pool (internal)");
-  cudaEvent_t e = s.tev[s.tev_used];
-  if (c->capturing) XP_CUDA(c, cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
-  else XP_CUDA(c, cudaEventRecord(e, st));
+  if (!c->timed || !want) return XP_OK;
+  if (s.tev_used >= s.tstamp_cap) return set_err(c, XP_ESCHED, "timing stamp buffer (internal)");
+  XP_TRY(check_launch(c, launch_stamp(s.tstamp + s.tev_used, st), "stamp"));
   *idx = (int)s.tev_used++;
   return XP_OK;
 }
 }  // namespace xp
 
 namespace {
+
+// development switch: XPIPE_NO_WGRAD_BATCH=1 runs the conv weight gradients per micro-batch
+bool no_wgrad_batch() {
+  static const bool v = [] { const char* e = getenv("XPIPE_NO_WGRAD_BATCH"); return e && *e && *e != '0'; }();
+  return v;
+}
+
+// the activation-ring credit a producer waits for before writing message u into stage q's ring:
+// q released message u - S_q; with batched weight gradients q releases a mini-batch's slots
+// together, at its B(t,T) (flag value t*T)
+int64_t ring_credit(const xpipe_ctx* c, const StageRT& q, int64_t u) {
+  int64_t v = u - q.S;
+  if (q.wbatch && v > 0) v = (v + c->T - 1) / c->T * c->T;  // acks are written at multiples of T
+  return v;
+}
 
 // Flag values are micro-batch indices relative to c->flag_base (rebased between calls when
 // CUDA graphs are on); GEQ compares the wraparound-safe signed difference, so rebased values
@@ -223,6 +236,10 @@ int flag_wait(xpipe_ctx* c, StageRT& s, int which, int64_t value) {
   if (verbose()) fprintf(stderr, "[xpipe] stage %d wait %d(%p) >= %lld%s\n", s.k, which, (void*)flag, (long long)value,
                          value <= 0 ? " (skip)" : "");
   if (value <= 0) return XP_OK;  // absolute: that message never existed
+  if (c->capturing && c->mp()) {  // another process writes the flag: device-side wait on base + rel
+    XP_TRY(check_launch(c, launch_flag_wait(flag, s.dbase, (int32_t)(value - c->cap_base), s.stream), "flag_wait"));
+    return XP_OK;
+  }
   if (c->capturing) {
     // producer's enqueue counter at capture start: waits on earlier messages are satisfied
     const int prod = (which == 0 || which == 3) ? s.k - 1 : s.k + 1;
@@ -243,6 +260,9 @@ int flag_write(xpipe_ctx* c, StageRT& s, StageRT& tgt, int which, int64_t value)
   uint32_t* flag = &tgt.flags[which];
   if (verbose()) fprintf(stderr, "[xpipe] stage %d write stage %d flag %d(%p) = %lld\n", s.k, tgt.k, which, (void*)flag,
                          (long long)value);
+  if (c->capturing && c->mp()) {
+    return check_launch(c, launch_flag_write(flag, s.dbase, (int32_t)(value - c->cap_base), s.stream), "flag_write");
+  }
   if (c->capturing) {
     auto& evs = tgt.ev_flag[which];
     XP_CUDA(c, cudaEventRecord(evs[(value - 1) % evs.size()], s.stream));
@@ -305,12 +325,19 @@ int reserve_for_call(xpipe_ctx* c, int64_t M) {
     }
     if (c->cfg.timing) {
       const size_t want = (size_t)4 * (2 * (M * c->T + 2 * c->K + c->T) + 8);
-      while (s.tev.size() < want) {
-        cudaEvent_t e;
-        XP_CUDA(c, cudaEventCreate(&e));
-        s.tev.push_back(e);
+      if (s.tstamp_cap < want) {
+        // captured graphs hold the old buffer's addresses: drop them (re-captured on demand)
+        for (auto& kv : c->graphs)
+          if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        c->graphs.clear();
+        const size_t cap = std::max(want, 2 * s.tstamp_cap);
+        s.tstamp = (uint64_t*)dmalloc(c, cap * 8, s.dev);
+        if (s.tstamp_host) cudaFreeHost(s.tstamp_host);
+        s.tstamp_host = nullptr;
+        if (!s.tstamp || cudaMallocHost(&s.tstamp_host, cap * 8) != cudaSuccess)
+          return set_err(c, XP_ENOMEM, "timing stamps");
+        s.tstamp_cap = cap;
       }
-      if (!s.ev_ref) XP_CUDA(c, cudaEventCreate(&s.ev_ref));
     }
     if (c->cfg.snapshots) {
       const size_t want = (size_t)(M + c->K + 1);
@@ -398,16 +425,17 @@ int enqueue_forward(xpipe_ctx* c, int k, int64_t u) {
   if (bw) s.host_fver = s.host_ver;
   const void* Wf = s.pf[s.host_fver & 1];
   for (size_t o = 0; o < s.plan.ops.size(); ++o) XP_TRY(op_forward(c, s, (int)o, Wf, slot, u));
-  XP_TRY(tmark(c, s, s.stream, &top.e[1]));
+  // hand-off timing is sampled on the bellwether micro-batches (1 in T) to keep stamps few
+  XP_TRY(tmark(c, s, s.stream, &top.e[1], bw && k + 1 < c->K));
   if (k + 1 < c->K) {
     StageRT& nx = c->S[k + 1];
-    XP_TRY(flag_wait(c, s, 2, u - nx.S));  // ring credit: consumer released u - R
+    XP_TRY(flag_wait(c, s, 2, ring_credit(c, nx, u)));  // ring credit: consumer released u - R
     XP_CUDA(c, cudaMemcpyAsync(nx.in_slot[(u - 1) % nx.S], s.act[s.plan.out_tensor][slot], s.plan.out_bytes,
                                cudaMemcpyDefault, s.stream));
-    XP_TRY(tmark(c, s, s.stream, &top.e[2]));
     XP_TRY(flag_write(c, s, nx, 0, u));
   }
-  if (c->cfg.timing) s.tops.push_back(top);
+  XP_TRY(tmark(c, s, s.stream, &top.e[3]));  // the op's end
+  if (c->timed) s.tops.push_back(top);
   if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
   if (fwd.on) XP_TRY(ev_record(c, s.stream, s.ev_fdone[slot], &s.fdone_epoch[slot]));
   return XP_OK;
@@ -431,6 +459,18 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
   XP_TRY(trace_slot(c, s, &rec));
   if (rec) XP_TRY(check_launch(c, launch_trace_begin(s.ds, rec, k, 1, (int)t, (int)j, sb, bw, s.stream), "trace"));
   if (bw) s.host_bver = s.host_ver;
+  if (bw && c->cfg.wbwd == XP_WBWD_BELLWETHER) {
+    // the backward bellwether predicts W_hat_b from the stage's current state (version
+    // t-1: no update falls between B(t,1) and B(t,T)); the other T-1 backwards reuse it
+    const bool bf = c->cfg.precision == XP_BF16;
+    XP_TRY(prof_begin(c, s));
+    if (c->cfg.delta_form == XP_DELTA_ADAM && s.host_ver == 0)
+      XP_TRY(check_launch(c, launch_predict_copy(s.W, nullptr, s.pb, s.plan.P, bf, s.stream), "predict_b"));
+    else
+      XP_TRY(check_launch(c, launch_sweep(s.W, s.g, s.m, s.v, nullptr, s.pb, s.plan.P, s.ds, nullptr, 0.f, (float)sb, bf,
+                                          c->cfg.delta_form, false, s.stream), "predict_b"));
+    XP_TRY(prof_end(c, s, XP_PROF_SWEEP, (double)s.plan.P * (12.0 + (bf ? 2.0 : 4.0))));
+  }
   if (c->cfg.recompute) {
     // f3: re-run the stage forward for this micro-batch under W_hat_b from its stashed
     // input (ring slot), overwriting the slot's activations, statistics and pool winners (and
@@ -442,6 +482,8 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     XP_TRY(r);
   }
   const bool accumulate = (j != 1);
+  s.cur_j = (int)j;
+  s.cur_slot0 = (int)(((t - 1) * c->T) % s.S);  // slot of B(t,1) (contiguous T slots when wbatch)
   s.gsel = 0;
   s.gdone_valid[0] = s.gdone_valid[1] = false;
   // gradient bookkeeping over the stage's tensors: the output gradient is the gradient ring
@@ -462,24 +504,31 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     if (need0) has[O.in0] = 1;
     if (need1) has[O.in1] = 1;
   }
-  XP_TRY(tmark(c, s, s.stream, &top.e[1]));
+  XP_TRY(tmark(c, s, s.stream, &top.e[1], bw && k > 0));
   if (k + 1 < c->K) XP_TRY(flag_write(c, s, c->S[k + 1], 3, u));  // released gin slot u
   if (k > 0) {
     if (!has[0]) return set_err(c, XP_ESCHED, "no gradient reaches the stage input (internal)");
     StageRT& pv = c->S[k - 1];
     XP_TRY(flag_wait(c, s, 3, u - pv.S));
     XP_CUDA(c, cudaMemcpyAsync(pv.gin_slot[(u - 1) % pv.S], gp[0], P.in_bytes, cudaMemcpyDefault, s.stream));
-    XP_TRY(tmark(c, s, s.stream, &top.e[2]));
+    XP_TRY(tmark(c, s, s.stream, &top.e[2], bw));
     XP_TRY(flag_write(c, s, pv, 1, u));
-    XP_TRY(flag_write(c, s, pv, 2, u));  // released our input slot u
+    if (!s.wbatch) XP_TRY(flag_write(c, s, pv, 2, u));  // released our input slot u
   }
   if (s.side_used) {  // join the weight-gradient side stream (the update reads g)
     XP_CUDA(c, cudaEventRecord(s.ev_join, s.side));
     XP_CUDA(c, cudaStreamWaitEvent(s.stream, s.ev_join, 0));
     s.side_used = false;
   }
+  // batched weight gradients read every input slot of the mini-batch: release them together
+  if (s.wbatch && j == c->T && k > 0) XP_TRY(flag_write(c, s, c->S[k - 1], 2, u));
   if (rec) XP_TRY(check_launch(c, launch_trace_end(rec, s.stream), "trace"));
-  if (ov) XP_TRY(ev_record(c, s.stream, s.ev_bdone[slot], &s.bdone_epoch[slot]));  // slot free for F(u + S)
+  if (ov && !s.wbatch) XP_TRY(ev_record(c, s.stream, s.ev_bdone[slot], &s.bdone_epoch[slot]));  // slot free for F(u + S)
+  if (ov && s.wbatch && j == c->T)  // the mini-batch's T slots are free once its batched wgrads ran
+    for (int q = 0; q < c->T; ++q) {
+      const int sl = (s.cur_slot0 + q) % s.S;
+      XP_TRY(ev_record(c, s.stream, s.ev_bdone[sl], &s.bdone_epoch[sl]));
+    }
   if (j == c->T) {
     // the T-th micro-batch's backward ends the mini-batch: update + prediction (K1)
     if (ov) {  // forwards enqueued so far (still reading W_hat_f buffers) finish before the sweep
@@ -494,16 +543,18 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     const float sf = (float)version_difference(c, k, 0), sbf = (float)sb;
     const bool bf16 = c->cfg.precision == XP_BF16;
     XP_TRY(prof_begin(c, s));
+    void* pbw = c->cfg.wbwd == XP_WBWD_BELLWETHER ? nullptr : s.pb;  // bellwether mode: W_hat_b later
     if (c->cfg.optimizer == XP_OPT_MOMENTUM_SGD)
-      XP_TRY(check_launch(c, launch_sweep_sgd(s.W, s.g, s.buf, s.m, s.v, s.pf[nv & 1], s.pb, s.plan.P, s.ds, nullptr, sf,
+      XP_TRY(check_launch(c, launch_sweep_sgd(s.W, s.g, s.buf, s.m, s.v, s.pf[nv & 1], pbw, s.plan.P, s.ds, nullptr, sf,
                                               sbf, bf16, s.stream), "sweep_sgd"));
     else
-      XP_TRY(check_launch(c, launch_sweep(s.W, s.g, s.m, s.v, s.pf[nv & 1], s.pb, s.plan.P, s.ds, nullptr, sf, sbf,
+      XP_TRY(check_launch(c, launch_sweep(s.W, s.g, s.m, s.v, s.pf[nv & 1], pbw, s.plan.P, s.ds, nullptr, sf, sbf,
                                           bf16, c->cfg.delta_form, true, s.stream), "sweep"));
-    // algorithmic bytes per parameter: Adam 16 B read + 12 B written + 2 predictions; the f2
-    // Momentum-SGD sweep also reads and writes the velocity (+8 B)
+    // algorithmic bytes per parameter: Adam 16 B read + 12 B written + the predictions written
+    // (2, or 1 in bellwether mode); the f2 Momentum-SGD sweep also reads and writes the velocity
     const double sgd_extra = c->cfg.optimizer == XP_OPT_MOMENTUM_SGD ? 8.0 : 0.0;
-    XP_TRY(prof_end(c, s, XP_PROF_SWEEP, (double)s.plan.P * ((bf16 ? 32.0 : 36.0) + sgd_extra)));
+    const double pred_b = (bf16 ? 2.0 : 4.0) * (pbw ? 2.0 : 1.0);
+    XP_TRY(prof_end(c, s, XP_PROF_SWEEP, (double)s.plan.P * (28.0 + pred_b + sgd_extra)));
     s.host_ver = nv;
     if (ov) XP_TRY(ev_record(c, s.stream, s.ev_upd, &s.upd_epoch));  // the next bellwether forward waits
     if (c->cfg.snapshots) {
@@ -515,7 +566,7 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
     }
   }
   XP_TRY(tmark(c, s, s.stream, &top.e[3]));  // the op's end: side-stream joined (+ update)
-  if (c->cfg.timing) s.tops.push_back(top);
+  if (c->timed) s.tops.push_back(top);
   return XP_OK;
 }
 
@@ -528,7 +579,7 @@ bool op_ready(const xpipe_ctx* c, int k, int op, int64_t u) {
   const auto& S = c->S;
   if (op == 0) {
     if (k > 0 && S[k - 1].fwd_enq < u) return false;                          // activation message
-    if (k + 1 < c->K && S[k + 1].bwd_enq < u - S[k + 1].S) return false;      // ring credit
+    if (k + 1 < c->K && S[k + 1].bwd_enq < ring_credit(c, S[k + 1], u)) return false;  // ring credit
   } else {
     if (k + 1 < c->K ? S[k + 1].bwd_enq < u : S[k].fwd_enq < u) return false; // gradient / logits
     if (k > 0 && S[k - 1].bwd_enq < u - S[k - 1].S) return false;             // gradient ring credit
@@ -625,15 +676,22 @@ int sync_all(xpipe_ctx* c) {
 // mod S (ring-slot phase), and the parities of the version counters (W_hat_f buffer choice);
 // the ring flags are rebased to fed so their values repeat too.
 bool graph_eligible(const xpipe_ctx* c, uint32_t flags, int64_t M, int64_t fed_before) {
-  if (!c->cfg.graphs || c->mp() || c->cfg.trace || c->cfg.snapshots) return false;
+  if (!c->cfg.graphs || c->cfg.trace || c->cfg.snapshots) return false;
   if ((flags & XP_FLUSH) || M <= 0 || fed_before - c->base < 2 * c->K) return false;
+  if (c->mp()) {
+    // one process per GPU: the other processes' previous calls may still be running, so every
+    // flag wait of the call must be a real (positive) micro-batch index at capture already
+    int smax = 0;
+    for (const auto& s : c->S) smax = std::max(smax, s.S);
+    return fed_before - c->base >= smax + 2 * c->K + c->T;
+  }
   for (const auto& s : c->S)
-    if (s.dev != c->S[0].dev) return false;  // single-device capture only
+    if (s.dev != c->S[0].dev) return false;  // single-process capture: one device
   return true;
 }
 
 std::string graph_signature(const xpipe_ctx* c, int64_t M, int64_t fed_before) {
-  std::string sig = std::to_string(M) + ":" + std::to_string((uintptr_t)c->x_dev) + ":" +
+  std::string sig = std::to_string(M) + (c->timed ? "t:" : ":") + std::to_string((uintptr_t)c->x_dev) + ":" +
                     std::to_string((uintptr_t)c->y_dev) + ":" + std::to_string((uintptr_t)c->loss_dev);
   const int64_t f = fed_before - c->base;
   for (const auto& s : c->S)
@@ -656,11 +714,15 @@ int rebase_flags(xpipe_ctx* c, int64_t new_base) {
 }
 
 int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
-  XP_TRY(rebase_flags(c, fed_before));
+  // single process: flags rebased to the call's base (every stage drained); multi-process: the
+  // flags stay absolute (neighbours may still be running) and the graph's flag kernels read the
+  // call's base from the device
+  if (!c->mp()) XP_TRY(rebase_flags(c, fed_before));
   const std::string sig = graph_signature(c, M, fed_before);
   xpipe_ctx::GraphRec& g = c->graphs[sig];
-  StageRT& o = c->S[0];
+  StageRT& o = c->mp() ? c->S[c->cfg.my_stage] : c->S[0];
   cudaSetDevice(o.dev);
+  if (c->mp()) XP_TRY(check_launch(c, launch_set_i64(o.dbase, fed_before, o.stream), "base"));
   if (g.exec) {
     XP_CUDA(c, cudaGraphLaunch(g.exec, o.stream));
     for (size_t k = 0; k < c->S.size(); ++k) {
@@ -679,7 +741,8 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
       c->S[k].prof_cls = g.prof_cls[k];
       c->S[k].prof_work = g.prof_work[k];
       c->S[k].ev_used = 2 * g.prof_cls[k].size();
-      c->S[k].tops = g.tops[k];                   // ... and the same timing events
+      c->S[k].tops = g.tops[k];                   // ... and the same timing stamps
+      c->S[k].tev_used = g.tev_used[k];
     }
     return XP_OK;
   }
@@ -690,16 +753,18 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
   for (auto& s : c->S) { pos0.push_back(s.pos); ver0.push_back(s.host_ver); fwd0.push_back(s.fwd_enq); bwd0.push_back(s.bwd_enq); }
   const int64_t k0 = c->kernels;
   static thread_local std::vector<cudaEvent_t> evs;
-  while (evs.size() < c->S.size() + 1) {
+  while (evs.size() < c->S.size() + 2) {
     cudaEvent_t e;
     XP_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     evs.push_back(e);
   }
   XP_CUDA(c, cudaStreamBeginCapture(o.stream, cudaStreamCaptureModeThreadLocal));
   XP_CUDA(c, cudaEventRecord(evs[0], o.stream));
-  for (size_t k = 1; k < c->S.size(); ++k) XP_CUDA(c, cudaStreamWaitEvent(c->S[k].stream, evs[0], 0));
   for (auto& s : c->S)
-    if (s.fstream && s.fstream != s.stream) XP_CUDA(c, cudaStreamWaitEvent(s.fstream, evs[0], 0));
+    if (owned(s) && &s != &o) XP_CUDA(c, cudaStreamWaitEvent(s.stream, evs[0], 0));
+  for (auto& s : c->S)
+    if (owned(s) && s.fstream && s.fstream != s.stream) XP_CUDA(c, cudaStreamWaitEvent(s.fstream, evs[0], 0));
+  c->cap_base = fed_before;
   c->cap_fwd0.clear(); c->cap_bwd0.clear();
   for (auto& s : c->S) {
     c->cap_fwd0.push_back(s.fwd_enq);
@@ -717,8 +782,10 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
   c->capturing = true;
   int r = drive(c, -1);
   c->capturing = false;
-  for (size_t k = 1; k < c->S.size() && r == XP_OK; ++k) {
-    if (cudaEventRecord(evs[k], c->S[k].stream) != cudaSuccess || cudaStreamWaitEvent(o.stream, evs[k], 0) != cudaSuccess)
+  for (size_t k = 0; k < c->S.size() && r == XP_OK; ++k) {
+    if (!owned(c->S[k]) || &c->S[k] == &o) continue;
+    if (cudaEventRecord(evs[k + 1], c->S[k].stream) != cudaSuccess ||
+        cudaStreamWaitEvent(o.stream, evs[k + 1], 0) != cudaSuccess)
       r = set_err(c, XP_ECUDA, "graph join");
   }
   cudaGraph_t graph = nullptr;
@@ -730,8 +797,11 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
   if (e != cudaSuccess) return set_err(c, XP_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
   g.kernels = c->kernels - k0;
   g.dpos.clear(); g.dver.clear(); g.dfver.clear(); g.dbver.clear(); g.dfwd.clear(); g.dbwd.clear();
-  g.prof_cls.clear(); g.prof_work.clear(); g.tops.clear();
-  for (auto& s : c->S) { g.prof_cls.push_back(s.prof_cls); g.prof_work.push_back(s.prof_work); g.tops.push_back(s.tops); }
+  g.prof_cls.clear(); g.prof_work.clear(); g.tops.clear(); g.tev_used.clear();
+  for (auto& s : c->S) {
+    g.prof_cls.push_back(s.prof_cls); g.prof_work.push_back(s.prof_work);
+    g.tops.push_back(s.tops); g.tev_used.push_back(s.tev_used);
+  }
   for (size_t k = 0; k < c->S.size(); ++k) {
     StageRT& s = c->S[k];
     g.dpos.push_back(s.pos - pos0[k]);
@@ -750,10 +820,16 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
 int timing_stats(xpipe_ctx* c, int64_t M, bool empty_before, bool flush, xpipe_stats* st) {
   double t_lo = 1e300, t_hi = -1e300, busy_sum = 0;
   int owned_n = 0, ops = 0;
+  // one copy of every owned stage's stamps; times in ms relative to the first stamp seen
+  uint64_t t_ref = 0;
+  for (auto& s : c->S) {
+    if (!owned(s) || !s.tev_used) continue;
+    cudaSetDevice(s.dev);
+    XP_CUDA(c, cudaMemcpy(s.tstamp_host, s.tstamp, s.tev_used * 8, cudaMemcpyDeviceToHost));
+    if (!t_ref || s.tstamp_host[0] < t_ref) t_ref = s.tstamp_host[0];
+  }
   auto at = [&](StageRT& s, int e, double* ms) -> int {
-    float v = 0;
-    XP_CUDA(c, cudaEventElapsedTime(&v, s.ev_ref, s.tev[e]));
-    *ms = v;
+    *ms = ((double)(int64_t)(s.tstamp_host[e] - t_ref)) * 1e-6;
     return XP_OK;
   };
   std::vector<double> bell;  // stage 0's bellwether forward starts, in order
@@ -764,18 +840,15 @@ int timing_stats(xpipe_ctx* c, int64_t M, bool empty_before, bool flush, xpipe_s
     std::vector<std::pair<double, double>> iv;
     double pf = 0, pb = 0, bf = 0, bb = 0;
     for (const TimedOp& o : s.tops) {
-      if (o.e[0] < 0) continue;
+      if (o.e[0] < 0 || o.e[3] < 0) continue;
       double t0, t1 = 0, t2 = 0, tend = 0;
       XP_TRY(at(s, o.e[0], &t0));
-      if (o.e[1] >= 0) XP_TRY(at(s, o.e[1], &t1));
-      tend = t1;
-      if (o.e[2] >= 0) {
-        XP_TRY(at(s, o.e[2], &t2));
-        tend = t2;
-        if (o.op == 0) { pf += t2 - t1; bf += (double)s.plan.out_bytes; }
-        else { pb += t2 - t1; bb += (double)s.plan.in_bytes; }
+      XP_TRY(at(s, o.e[3], &tend));
+      if (o.e[1] >= 0) {  // a sampled hand-off: compute end -> copy end (forward: op end)
+        XP_TRY(at(s, o.e[1], &t1));
+        if (o.op == 0) { pf += tend - t1; bf += (double)s.plan.out_bytes; }
+        else if (o.e[2] >= 0) { XP_TRY(at(s, o.e[2], &t2)); pb += t2 - t1; bb += (double)s.plan.in_bytes; }
       }
-      if (o.e[3] >= 0) { double t3; XP_TRY(at(s, o.e[3], &t3)); tend = std::max(tend, t3); }
       iv.push_back({t0, tend});
       t_lo = std::min(t_lo, t0);
       t_hi = std::max(t_hi, tend);
@@ -863,6 +936,7 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
       (cfg->delta_form != XP_DELTA_PAPER || !(cfg->momentum >= 0 && cfg->momentum < 1) || !(cfg->weight_decay >= 0)))
     return set_err(nullptr, XP_EINVAL, "XP_OPT_MOMENTUM_SGD requires XP_DELTA_PAPER, momentum in [0,1), weight_decay >= 0");
   if (cfg->precision != XP_FP32 && cfg->precision != XP_BF16) return set_err(nullptr, XP_EINVAL, "precision");
+  if (cfg->wbwd != XP_WBWD_MATERIALIZE && cfg->wbwd != XP_WBWD_BELLWETHER) return set_err(nullptr, XP_EINVAL, "wbwd");
   if (cfg->schedule != XP_SCHED_XPIPE && cfg->schedule != XP_SCHED_GPIPE) return set_err(nullptr, XP_EINVAL, "schedule");
   if (cfg->predict < 0 || cfg->predict > 2 || (cfg->predict == XP_PRED_FIXED && (cfg->s_fwd < 0 || cfg->s_bwd < 0)))
     return set_err(nullptr, XP_EINVAL, "predict");
@@ -898,7 +972,17 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
     if (s.dev < 0 || s.dev >= ndev) return set_err(nullptr, XP_EINVAL, "device id out of range");
     s.plan = c->net.stages[k];
     s.S = c->cfg.schedule == XP_SCHED_GPIPE ? T : (stages - k);
-    if (c->cfg.fb_overlap) {
+    bool has_conv = false;
+    for (const Op& O : s.plan.ops) has_conv |= O.kind == OP_CONV;
+    s.wbatch = c->cfg.precision == XP_BF16 && has_conv && !no_wgrad_batch();
+    if (s.wbatch && c->cfg.schedule != XP_SCHED_GPIPE) {
+      // a slot is reused by F(u+S) only after the mini-batch of u finished (its batched wgrad
+      // reads all T slots at B(t,T)): F(u') follows B(u'-W) in program order (W = K-k), so
+      // S >= W + T - 1 (+1 when F(u') may overlap B(u'-W) on its own stream), a multiple of T
+      // so that a mini-batch's T slots are contiguous
+      const int want = stages - k + T - 1 + (c->cfg.fb_overlap ? 1 : 0);
+      s.S = (want + T - 1) / T * T;
+    } else if (c->cfg.fb_overlap) {
       // one more slot, so F(u+S) can overlap B(u); rounded to a divisor or a multiple of T so
       // the slot phase of every stage repeats each call (a call feeds whole mini-batches) and
       // steady-state calls keep replaying one CUDA graph
@@ -1038,18 +1122,11 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     c->fed += (int64_t)M * c->T;
   }
   for (auto& s : c->S) { s.ev_used = 0; s.prof_cls.clear(); s.prof_work.clear(); s.tev_used = 0; s.tops.clear(); }
+  // cfg.timing = p: this call is stamped when it is the p-th since the last stamped one
+  c->timed = c->cfg.timing > 0 && (c->calls++ % c->cfg.timing) == 0;
   XP_TRY(reserve_for_call(c, M));
   const bool empty_before = c->fed - (int64_t)M * c->T == c->base;  // pipeline empty at the call's start
-  if (c->cfg.timing) {
-    // reference events: every stream is drained, so all devices start the call together
-    const bool graph = graph_eligible(c, flags, M, c->fed - (int64_t)M * c->T);
-    for (auto& s : c->S) {
-      if (!owned(s)) continue;
-      StageRT& rs = graph ? c->S[0] : s;
-      cudaSetDevice(rs.dev);
-      XP_CUDA(c, cudaEventRecord(s.ev_ref, rs.stream));
-    }
-  }
+
   const int64_t fed_before = c->fed - (int64_t)M * c->T;
   if (graph_eligible(c, flags, M, fed_before)) XP_TRY(drive_graph(c, M, fed_before));
   else XP_TRY(drive(c, -1));
@@ -1097,7 +1174,7 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
         }
       }
     }
-    if (c->cfg.timing && !(flags & XP_ASYNC)) XP_TRY(timing_stats(c, M, empty_before, (flags & XP_FLUSH) != 0, st));
+    if (c->timed && !(flags & XP_ASYNC)) XP_TRY(timing_stats(c, M, empty_before, (flags & XP_FLUSH) != 0, st));
     if (st->losses && M > 0 && !(flags & XP_ASYNC) && owned(c->S[c->K - 1])) {
       cudaSetDevice(c->S[c->K - 1].dev);
       XP_CUDA(c, cudaMemcpy(st->losses, c->loss_dev, (size_t)M * c->T * 4, cudaMemcpyDeviceToHost));

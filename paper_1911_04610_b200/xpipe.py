@@ -20,6 +20,7 @@ PREDICT = {"paper": 0, "off": 1, "fixed": 2}
 DELTA = {"adam": 0, "paper": 1}
 STATE = {"param": 0, "m": 1, "v": 2, "pred_fwd": 3, "pred_bwd": 4, "grad": 5, "buf": 6}
 OPTIMIZER = {"adam": 0, "sgd": 1}
+WBWD = {"materialize": 0, "bellwether": 1}
 XP_FLUSH, XP_DEVICE_PTRS, XP_ASYNC = 1, 2, 4
 
 
@@ -46,7 +47,7 @@ class Config(C.Structure):
                 ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", C.c_void_p),
                 ("optimizer", C.c_int32), ("momentum", C.c_float), ("weight_decay", C.c_float),
                 ("recompute", C.c_int32), ("serialize", C.c_int32), ("fb_overlap", C.c_int32),
-                ("timing", C.c_int32)]
+                ("timing", C.c_int32), ("wbwd", C.c_int32)]
 
 
 class TraceRec(C.Structure):
@@ -161,7 +162,8 @@ class XPipe:
                  precision="fp32", schedule="xpipe", predict=None, s_fwd=0, s_bwd=0, delta="adam",
                  init_m=None, init_v=None, devices=None, snapshots=False, trace=False, graphs=False, profile=False,
                  seed=1, watchdog_ms=0, torch_allocator=True, my_stage=None, optimizer="adam", momentum=0.9,
-                 weight_decay=5e-4, recompute=False, serialize=False, fb_overlap=False, timing=False):
+                 weight_decay=5e-4, recompute=False, serialize=False, fb_overlap=False, timing=False,
+                 wbwd="materialize"):
         self.h = None
         L = lib()
         if predict is None:  # GPipe runs under the current weights (no prediction)
@@ -179,7 +181,8 @@ class XPipe:
                      multi_process=int(my_stage is not None), my_stage=my_stage or 0,
                      optimizer=OPTIMIZER[optimizer], momentum=momentum if optimizer == "sgd" else 0.0,
                      weight_decay=weight_decay if optimizer == "sgd" else 0.0, recompute=int(recompute),
-                     serialize=int(serialize), fb_overlap=int(fb_overlap), timing=int(timing))
+                     serialize=int(serialize), fb_overlap=int(fb_overlap), timing=int(timing),  # bool -> every call
+                     wbwd=WBWD[wbwd])
         if devices:
             cfg.n_devices = len(devices)
             for i, d in enumerate(devices):

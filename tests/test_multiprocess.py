@@ -58,7 +58,7 @@ def test_multiprocess_validation_without_gpu():
     assert e.value.code == -1
 
 
-def _ipc_worker(rank, world, port, q, overlap=False):
+def _ipc_worker(rank, world, port, q, overlap=False, graphs=False):
     sys.path.insert(0, ROOT)
     try:
         import torch
@@ -70,49 +70,65 @@ def _ipc_worker(rank, world, port, q, overlap=False):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         L = S.mlp()
         P = S.make_params(L, 1)
-        x, y = S.make_inputs(10 * 32, (784, 1, 1), 10, 1, kind="mnist")
+        M = 24 if graphs else 10
+        x, y = S.make_inputs(M * 32, (784, 1, 1), 10, 1, kind="mnist")
         g = XPipe(L, world, 4, 32, 1e-3, (0.9, 0.999), 1e-8, (784, 1, 1), 10, params=P, precision="fp32",
-                  trace=True, my_stage=rank, watchdog_ms=60000, fb_overlap=overlap)
+                  trace=not graphs, my_stage=rank, watchdog_ms=60000, fb_overlap=overlap, graphs=graphs)
         connect_pipeline(g)
         dist.barrier()
-        g.step(x[:96], y[:96], 3)             # call splitting across processes too
-        g.step(x[96:], y[96:], 7, flush=True)
+        replays = 0
+        if graphs:
+            # 2 mini-batches per call: steady-state calls are captured per process (device-side
+            # flag kernels on the call's base) and replayed, the processes never synchronising
+            for i in range(12):
+                sl = slice(i * 64, (i + 1) * 64)
+                g.step(x[sl], y[sl], 2)
+                replays += g.last_stats.graph_replays
+            g.step(x[:0], y[:0], 0, flush=True)
+        else:
+            g.step(x[:96], y[:96], 3)             # call splitting across processes too
+            g.step(x[96:], y[96:], 7, flush=True)
         out = {(i, t): g.get(i, t) for i in range(len(L)) for t in (0, 1) if g.stage_of(i) == rank and g._count(i, t)}
-        q.put((rank, out, g.trace(rank)))
+        q.put((rank, out, None if graphs else g.trace(rank), replays))
         dist.barrier()
         g.close()
         dist.destroy_process_group()
     except Exception as e:  # report to the parent
-        q.put((rank, repr(e), None))
+        q.put((rank, repr(e), None, 0))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("overlap", [False, True])
-def test_two_process_pipeline_one_gpu(oracle_mod, overlap):
+@pytest.mark.parametrize("overlap,graphs", [(False, False), (True, False), (False, True), (True, True)])
+def test_two_process_pipeline_one_gpu(oracle_mod, overlap, graphs):
     """Two processes, one stage each, rings and flags shared through CUDA IPC on one B200:
-    weights and traces bit-exact with the oracle's K=2 replay."""
+    weights (and, without graphs, traces) bit-exact with the oracle's K=2 replay; with graphs
+    each process captures and replays its own stage's steady-state calls."""
     import torch.multiprocessing as mp
     import synthetic as S
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, overlap)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, overlap, graphs)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
     for _ in range(2):
-        r, w, tr = q.get(timeout=600)
+        r, w, tr, reps = q.get(timeout=600)
         assert not isinstance(w, str), w
-        res[r] = (w, tr)
+        res[r] = (w, tr, reps)
     for p in procs:
         p.join(timeout=120)
     L = S.mlp()
     P = S.make_params(L, 1)
-    x, y = S.make_inputs(10 * 32, (784, 1, 1), 10, 1, kind="mnist")
+    M = 24 if graphs else 10
+    x, y = S.make_inputs(M * 32, (784, 1, 1), 10, 1, kind="mnist")
     o = oracle_mod.Oracle(L, 2, 4, 32, 1e-3, (0.9, 0.999), 1e-8, (784, 1, 1), 10, P, mode="fp32")
-    o.step(x, y, 10, flush=True)
+    o.step(x, y, M, flush=True)
     for r in range(2):
-        w, tr = res[r]
-        assert tr == o.trace(r)
+        w, tr, reps = res[r]
+        if graphs:
+            assert reps >= 4, (r, reps)
+        else:
+            assert tr == o.trace(r)
         for (i, t), a in w.items():
             assert np.array_equal(a, o.get(i, t).astype(np.float32)), (r, i, t)

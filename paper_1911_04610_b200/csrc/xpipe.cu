@@ -694,10 +694,12 @@ std::string graph_signature(const xpipe_ctx* c, int64_t M, int64_t fed_before) {
   std::string sig = std::to_string(M) + (c->timed ? "t:" : ":") + std::to_string((uintptr_t)c->x_dev) + ":" +
                     std::to_string((uintptr_t)c->y_dev) + ":" + std::to_string((uintptr_t)c->loss_dev);
   const int64_t f = fed_before - c->base;
-  for (const auto& s : c->S)
+  for (const auto& s : c->S) {
+    if (!owned(s)) continue;  // one process per GPU: other ranks' stages are not enqueued here
     sig += "|" + std::to_string(s.pos - 2 * f) + "," + std::to_string(s.fwd_enq - fed_before) + "," +
            std::to_string(s.bwd_enq - fed_before) + "," + std::to_string(f % s.S) + "," + std::to_string(s.host_ver & 1) +
            "," + std::to_string(s.host_fver & 1) + "," + std::to_string((int)s.done);
+  }
   return sig;
 }
 

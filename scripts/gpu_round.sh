@@ -4,6 +4,7 @@
 # and of the sweep.  usage (under gpurun): RUN=r01x bash scripts/gpu_round.sh [notests]
 out=gpurun_out/${RUN:-round}; mkdir -p $out
 export PYTHONUNBUFFERED=1
+export XPIPE_PARITY_LOG=$out/parity.jsonl
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $out/gpu.txt 2>&1
 python __graft_entry__.py > $out/build.log 2>&1 || { tail -30 $out/build.log; exit 1; }
 run() { name=$1; shift; echo "=== $name" >> $out/summary.txt; timeout ${T:-900} "$@" > $out/$name.log 2>&1; echo "rc=$?" >> $out/summary.txt; tail -${TL:-4} $out/$name.log >> $out/summary.txt; }

@@ -120,6 +120,46 @@ def workload_model(name, K=1, image=64, micro=0, T=0):
     return S.vgg16_cifar(), (3, 32, 32), 10, "cifar", 128, 4, "bf16"
 
 
+def measured_unit_costs(L, units, shape, classes, kind, N, T, prec, sched, minibatches=8, max_groups=16):
+    """Per-unit device cost for the cost-balanced partition ("a contiguous linear
+    partition minimising max_k(t_compute,k + t_sweep,k), with per-unit times measured on the
+    device").  The model runs on this GPU with every unit its own pipeline stage (or, beyond
+    max_groups units, every group of a forward-MAC-balanced max_groups-way split), all stages on
+    one stream (cfg.serialize: no overlap, so a stage's busy time is its own cost), with per-op
+    timing: busy_ms[g] = the union of stage g's forward / backward op intervals including its
+    hand-offs and its Adam + prediction sweep.  A group's time is shared among its units by
+    their forward MACs.  Returns the per-unit cost in ms per step."""
+    import synthetic as S
+    from synthetic.models import unit_macs, balanced_stages
+    from paper_1911_04610_b200 import XPipe
+    nu = max(units) + 1
+    macs = unit_macs(L, units, shape)
+    G = min(nu, max_groups)
+    if G == nu:
+        Lg = [l.with_stage(units[i]) for i, l in enumerate(L)]
+        group_of_unit = list(range(nu))
+    else:
+        Lg = balanced_stages(L, units, macs, G)
+        group_of_unit = [0] * nu
+        for i, l in enumerate(Lg):
+            group_of_unit[units[i]] = l.stage
+    P = S.make_params(Lg, 1)
+    x, y = S.make_inputs(minibatches * N, shape, classes, 1, kind=kind)
+    m = XPipe(Lg, G, T, N, 1e-4, (0.9, 0.999), 1e-8, shape, classes, params=P, precision=prec, serialize=True,
+              timing=1, graphs=False, watchdog_ms=300000, **{k: v for k, v in sched.items() if k != "fb_overlap"})
+    try:
+        m.step(x, y, minibatches)          # fill the pipeline (allocations, first captures)
+        m.step(x, y, minibatches)          # steady state, timed per op on the device
+        busy = m.last_stats.timing(G)["busy_ms"]
+    finally:
+        m.close()
+    gmacs = [0.0] * G
+    for u in range(nu):
+        gmacs[group_of_unit[u]] += macs[u]
+    return [busy[group_of_unit[u]] * (macs[u] / gmacs[group_of_unit[u]] if gmacs[group_of_unit[u]] else 1.0)
+            for u in range(nu)]
+
+
 def cpu_baseline(workload, seconds=20.0):
     """The oracle as it stands, on this host's cores: one micro-batch at a time of the same
     workload (K=1 stage, bf16 emulation for VGG-16 / fp32 for the MLP), bounded to ~seconds."""
@@ -296,8 +336,9 @@ def main():
     ap.add_argument("--recompute", action="store_true", help="activation recomputation (P:167, SURVEY f3)")
     ap.add_argument("--no-fb-overlap", action="store_true",
                     help="one stream per stage (default: a forward stream per stage, F(u+S) overlaps B(u))")
-    ap.add_argument("--partition", default="layer-count", choices=["layer-count", "balanced"],
-                    help="stage split: the paper's layer-count rule (R17) or cost-balanced (SURVEY 8e)")
+    ap.add_argument("--partition", default="layer-count", choices=["layer-count", "balanced", "macs"],
+                    help="stage split: the paper's layer-count rule (R17), cost-balanced on per-unit device "
+                         "times measured first (SURVEY 8e), or balanced on forward MACs")
     ap.add_argument("--image", type=int, default=64, help="Tiny-ImageNet side for resnet101/inception (224: f4)")
     ap.add_argument("--micro-batch", type=int, default=0, help="micro-batch size override (resnet101/inception)")
     ap.add_argument("--micro-batches", type=int, default=0, help="T override (resnet101/inception)")
@@ -346,20 +387,6 @@ def main():
     K = ws if mp_mode else (args.stages or (DEFAULT_STAGES[args.workload] if args.gpus == 1 else args.gpus))
     L, shape, classes, kind, N, T, prec = workload_model(args.workload, K, args.image, args.micro_batch,
                                                          args.micro_batches)
-    if args.partition == "balanced" and K > 1:
-        # contiguous partition minimising the largest stage's forward MACs
-        from synthetic.models import chain_units, unit_macs, balanced_stages
-        if args.workload in ("resnet101", "inception"):
-            from synthetic.models import resnet101, inception_v3
-            units = (resnet101(classes=200)[1] if args.workload == "resnet101" else
-                     inception_v3(classes=200, stem_pad=args.image < 75)[1])
-        else:
-            units = chain_units(L)
-        L = balanced_stages(L, units, unit_macs(L, units, shape), K)
-    dev = local if mp_mode else 0
-    P = S.make_params(L, 1)
-    from synthetic.models import param_count
-    nparams = param_count(L, shape)
     # f1: the GPipe-flush schedule (prediction off) through the same kernels, for the paper's
     # XPipe/GPipe throughput comparison (Figs. 7-8)
     sched = dict(schedule="gpipe", predict="off") if args.schedule == "gpipe" else {}
@@ -370,6 +397,34 @@ def main():
         sched.update(recompute=True)
     if not args.no_fb_overlap:  # forwards on a second stream per stage (F(u+S) overlaps B(u))
         sched.update(fb_overlap=True)
+    unit_cost = None
+    if args.partition in ("balanced", "macs") and K > 1:
+        # contiguous partition minimising the largest stage cost -- per-unit device
+        # times measured first (every rank measures the same model on its own GPU and takes the
+        # same deterministic split; rank 0's costs are broadcast so all ranks agree exactly)
+        from synthetic.models import chain_units, unit_macs, balanced_stages
+        if args.workload in ("resnet101", "inception"):
+            from synthetic.models import resnet101, inception_v3
+            units = (resnet101(classes=200)[1] if args.workload == "resnet101" else
+                     inception_v3(classes=200, stem_pad=args.image < 75)[1])
+        else:
+            units = chain_units(L)
+        if args.partition == "macs":
+            unit_cost = unit_macs(L, units, shape)
+        else:
+            if mp_mode:
+                torch.cuda.set_device(local if not os.environ.get("XPIPE_BENCH_ONE_GPU") else 0)
+            unit_cost = measured_unit_costs(L, units, shape, classes, kind, N, T, prec, sched) if rank == 0 else None
+            if mp_mode:
+                import torch.distributed as dist
+                box = [unit_cost]
+                dist.broadcast_object_list(box, src=0)
+                unit_cost = box[0]
+        L = balanced_stages(L, units, unit_cost, K)
+    dev = local if mp_mode else 0
+    P = S.make_params(L, 1)
+    from synthetic.models import param_count
+    nparams = param_count(L, shape)
     def make_model(profile):
         if mp_mode:
             # one process per GPU: this rank owns stage `rank`; rings/flags are CUDA IPC-mapped
@@ -570,6 +625,10 @@ def main():
         sl = run_sweep(args, peaks, peak_kind, n=1 << 27, steps=20)
         sweep = {k: sl[k] for k in ("value", "unit", "ms_per_step", "roofline")}
         sweep["config"] = sl["config"]["workload"]
+    # first layer of every stage where the split is explicit (DAG models, balanced partitions);
+    # None = the library's layer-count rule (R17)
+    stage_first = ([min((i for i, l in enumerate(L) if l.stage == k), default=-1) for k in range(K)]
+                   if K > 1 and all(l.stage >= 0 for l in L) else None)
     line = {"metric": METRICS.get(args.workload, METRIC), "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": result["ms"] / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
@@ -579,7 +638,9 @@ def main():
                        "global_batch": N, "stages": K, "micro_batches": T, "minibatches_per_step": M,
                        "parallelism": "pipeline K=%d (%s)" % (K, "GPipe-flush" if args.schedule == "gpipe" else "XPipe"),
                        "schedule": args.schedule, "optimizer": args.optimizer, "recompute": args.recompute,
-                       "partition": args.partition, "fb_overlap": not args.no_fb_overlap,
+                       "partition": args.partition, "stage_first_layer": stage_first,
+                       "unit_cost": ([round(c, 4) for c in unit_cost] if unit_cost else None),
+                       "fb_overlap": not args.no_fb_overlap,
                        "image": list(shape),
                        "l2": "working set > L2: optimizer state 16 B/param x %.1fM params = %d MB (126 MB L2)"
                              % (nparams / 1e6, nparams * 16 // 10**6)},

@@ -333,6 +333,22 @@ int xpipe_gemm_bf16(const void* A, const void* B, float* D, int32_t M, int32_t N
 int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void* in0, const void* in1, void* out,
                       int32_t accumulate, float* ws, int64_t ws_elems, void* stream);
 
+/* bf16 Linear layer on the tensor cores (swap-AB: the features are the 128-row UMMA side, the
+   micro-batch the narrow side; both operands by TMA), exposed for unit parity -- the ops the
+   bf16 pipeline runs for every Linear with in % 8 == 0 (north star (b)).
+   x [n][in] bf16, W [out][in] bf16 (PyTorch layout), in a multiple of 8.  mode:
+   1 = forward: y[r][o] = sum_i W[o][i] x[r][i] + b[o] (fp32 accumulation; b may be NULL);
+       y fp32 [n][out] if f32out, else bf16 [n][out] = Q(relu ? max(v, 0) : v).
+   2 = dgrad: dx [n][in] bf16 = Q(sum_o dy[r][o] W[o][i]); dy [n][ldp] bf16, ldp a multiple of
+       8, columns >= out zero.
+   3 = wgrad: gW [out][in] fp32 (=, or += when accumulate) sum_r dy[r][o] x[r][i].
+   ws: optional fp32 split-K workspace (as xpipe_conv2d_bf16, counters in its last 16384
+   elements).  Device pointers; asynchronous on stream.  Errors: XP_EINVAL (in or ldp not a
+   multiple of 8, ldp < out, n/in/out < 1), XP_ECUDA (launch). */
+int xpipe_linear_bf16(int32_t mode, const void* x, const void* W, const void* b, const void* dy, int32_t ldp,
+                      void* out, int32_t n, int32_t in, int32_t out_features, int32_t relu, int32_t f32out,
+                      int32_t accumulate, float* ws, int64_t ws_elems, void* stream);
+
 /* Development probe of the GEMM kernels (not part of the training path).  When the process
    runs with XPIPE_GEMM_DBG=1 every tensor-core GEMM launch records, per CTA c, 16 uint64 at
    host[16c ..]: globaltimer ns at start (after the PDL wait), first operand stage ready, all

@@ -2,7 +2,7 @@
 
 The product path is the CUDA library only.  Importing this package never imports oracle/.
 """
-from .xpipe import (XPipe, XPipeError, adam_predict, sgd_predict, gemm_bf16, conv2d_bf16, lib, SO_PATH,  # noqa: F401
+from .xpipe import (XPipe, XPipeError, adam_predict, sgd_predict, gemm_bf16, conv2d_bf16, linear_bf16, lib, SO_PATH,  # noqa: F401
                     exchange_blobs, connect_pipeline)
 
-__all__ = ["XPipe", "XPipeError", "adam_predict", "sgd_predict", "gemm_bf16", "conv2d_bf16", "exchange_blobs", "connect_pipeline", "lib", "SO_PATH"]
+__all__ = ["XPipe", "XPipeError", "adam_predict", "sgd_predict", "gemm_bf16", "conv2d_bf16", "linear_bf16", "exchange_blobs", "connect_pipeline", "lib", "SO_PATH"]

@@ -69,7 +69,7 @@ def build(force=False, verbose=False, extra=()):
     newest = max(os.path.getmtime(o) for o in objs)
     if force or not os.path.exists(SO) or os.path.getmtime(SO) < newest:
         tmp = SO + ".tmp%d" % os.getpid()
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-ldl", "-lpthread", "-lrt"]
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-Xlinker", "-z", "-Xlinker", "defs", "-o", tmp] + objs + ["-ldl", "-lpthread", "-lrt"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n%s" % r.stderr[-4000:])

@@ -8,6 +8,8 @@
 // parameters and statistics are stashed per micro-batch so the backward recompute of the
 // activation is bit-identical to the forward (R24).  Activation gradients that fan in from
 // several consumers accumulate with the oracle's rounding point, Q(old + Q(g)).
+#include <cstdlib>
+
 #include "kernels/bf16_kernels.h"
 #include "kernels/gemm_tc.h"
 #include "runtime.h"
@@ -16,6 +18,21 @@ namespace xp {
 
 namespace {
 typedef __nv_bfloat16 bf16;
+
+// bf16 Linear layers run on the tensor cores when they are a GEMM the UMMA tile can use (at
+// least 32 output features: the 2048 -> 200 heads of ResNet-101 / Inception-V3, the MLP's
+// hidden layers) and their rows are TMA-legal (in % 8 == 0).  The 512 -> 10 VGG-16 head (0.3
+// MFLOP per micro-batch, a GEMV) stays on the SIMT kernels: on the tensor cores it costs an
+// operand-preparation launch and two GEMM prologues (VGG-16 K=4: 99.6k vs 101.5k samples/s).
+// XPIPE_LINEAR_SIMT=1 / =0 (development) forces either path.
+bool linear_on_tc(const LayerInfo& L) {
+  static const int force = [] {
+    const char* e = getenv("XPIPE_LINEAR_SIMT");
+    return (e && *e) ? (*e != '0' ? 1 : 0) : -1;
+  }();
+  if (force == 1 || L.d.in_c % 8) return false;
+  return force == 0 || L.d.out_c >= 32;
+}
 
 ConvGeo conv_geo(const xpipe_ctx* c, const Op& O, const LayerInfo& L) {
   ConvGeo g;
@@ -46,6 +63,9 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
   const int n = c->n;
   switch (O.kind) {
     case OP_LINEAR:
+      if (linear_on_tc(L))  // swap-AB tcgen05 GEMM, bias / ReLU / fp32 logits in the epilogue
+        return check_launch(c, tc_linear_fwd(x, W + L.woff, L.nb ? W + L.boff : nullptr, y, n, L.d.in_c, L.d.out_c,
+                                             O.relu, O.logits, s.ws, s.ws_elems, s.ctr, s.stream), "linear_fwd");
       return check_launch(c, launch_linear_fwd_bf16(x, W + L.woff, L.nb ? W + L.boff : nullptr, y, n, L.d.in_c,
                                                     L.d.out_c, O.relu, O.logits, s.stream), "linear_fwd_bf16");
     case OP_CONV: {
@@ -67,6 +87,9 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
       XP_TRY(prof_end(c, s, XP_PROF_CONV_FPROP, conv_flops(g, L.in0.c)));
       const LayerInfo& N = c->net.layers[O.lbn];
       const int M = n * O.smid.h * O.smid.w;
+      const PoolGeo p = pool_geo(c, O.lpool);
+      uint8_t* pidx = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
+      const double out_elems = (double)n * O.sout.h * O.sout.w * O.sout.c;
       XP_TRY(prof_begin(c, s));
       if (bn_tiles)
         XP_TRY(check_launch(c, launch_bn_stats_final(s.bnws, bn_tiles, M, 128, O.smid.c, N.d.bn_eps, W + N.woff,
@@ -76,14 +99,13 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
                                                s.ctr + kTileCounters - 2, s.stats[o][slot], s.stream), "bn_stats"));
       // algorithmic bytes: the conv output read once (register-resident two passes)
       XP_TRY(prof_end(c, s, XP_PROF_BN_STATS, 2.0 * M * O.smid.c));
-      const PoolGeo p = pool_geo(c, O.lpool);
-      uint8_t* pidx = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
       XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, launch_bn_apply(mid, s.stats[o][slot], (bf16*)y, pidx, n, O.smid.h, O.smid.w, O.smid.c,
                                              O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0,
-                                             O.relu, s.stream), "bn_apply"));
+                                             O.relu, s.stream, O.in1 >= 0 ? (const bf16*)s.act[O.in1][slot] : nullptr,
+                                             s.plan.tensors[O.out].pitch()),
+                          "bn_apply"));
       // algorithmic bytes: conv output read, output written (+ 1 B pool winner per output)
-      const double out_elems = (double)n * O.sout.h * O.sout.w * O.sout.c;
       return prof_end(c, s, XP_PROF_BN_APPLY, 2.0 * M * O.smid.c + out_elems * (O.lpool >= 0 ? 3.0 : 2.0));
     }
     case OP_ADD:
@@ -96,7 +118,8 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
     case OP_MAXPOOL: case OP_AVGPOOL: {
       const PoolGeo p = pool_geo(c, O.lmain);
       return check_launch(c, launch_pool_fwd(x, (bf16*)y, n, O.sin0.h, O.sin0.w, O.sin0.c, O.sout.h, O.sout.w, p.kh,
-                                             p.kw, p.sh, p.sw, p.ph, p.pw, O.kind == OP_AVGPOOL, s.stream), "pool_fwd");
+                                             p.kw, p.sh, p.sw, p.ph, p.pw, O.kind == OP_AVGPOOL, s.stream,
+                                             s.plan.tensors[O.out].pitch()), "pool_fwd");
     }
     case OP_GAP:
       return check_launch(c, launch_gap_fwd(x, (bf16*)y, n, O.sin0.h * O.sin0.w, O.sin0.c, s.stream), "gap_fwd");
@@ -114,6 +137,19 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
     case OP_LINEAR: {
       if (acc0) return set_err(c, XP_EUNSUPPORTED, "fan-out into a Linear input");
       const bf16* mask = O.relu ? (const bf16*)s.act[O.out][slot] : nullptr;
+      if (linear_on_tc(L) && s.lin_dy) {
+        // masked bf16 output gradient (+ bias gradient), then wgrad and dgrad as tcgen05 GEMMs
+        bf16* dyp = (bf16*)s.lin_dy;
+        XP_TRY(check_launch(c, launch_linear_dy_prep(dy, O.logits, mask, dyp, s.lin_ldp, L.nb ? s.g + L.boff : nullptr, n,
+                                                     L.d.out_c, accumulate_g, s.stream), "linear_dy_prep"));
+        XP_TRY(check_launch(c, tc_linear_wgrad((const bf16*)s.act[O.in0][slot], dyp, s.lin_ldp, s.g + L.woff, n,
+                                               L.d.in_c, L.d.out_c, accumulate_g, s.ws, s.ws_elems, s.ctr, s.stream),
+                            "linear_wgrad"));
+        if (dx0)
+          XP_TRY(check_launch(c, tc_linear_dgrad(dyp, s.lin_ldp, W + L.woff, (bf16*)dx0, n, L.d.in_c, L.d.out_c, s.ws,
+                                                 s.ws_elems, s.ctr, s.stream), "linear_dgrad"));
+        return XP_OK;
+      }
       if (dx0)
         XP_TRY(check_launch(c, launch_linear_dgrad_bf16(dy, O.logits, mask, W + L.woff, (bf16*)dx0, n, L.d.in_c,
                                                         L.d.out_c, s.stream), "linear_dgrad_bf16"));
@@ -140,6 +176,7 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
         if (s.gdone_valid[b]) XP_CUDA(c, cudaStreamWaitEvent(s.stream, s.ev_gdone[b], 0));
       }
       const bf16* xmid = (const bf16*)s.mid[o][slot];
+      const int ldy = s.plan.tensors[O.out].pitch();  // dout / y rows (a concat view: its concat's)
       const bf16* yout = (const bf16*)s.act[O.out][slot];
       const uint8_t* pw8 = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
       // algorithmic bytes per pass: the conv output, plus dout and y (+ pool winners) at the
@@ -151,12 +188,13 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       XP_TRY(check_launch(c, launch_bn_bwd_reduce(xmid, (const bf16*)dy, yout, pw8, s.stats[o][slot], n, O.smid.h,
                                                   O.smid.w, O.smid.c, O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw, p.ph,
                                                   p.pw, O.lpool >= 0, O.relu, s.bnws, s.g + N.woff, s.g + N.boff,
-                                                  accumulate_g, s.stream), "bn_bwd_reduce"));
+                                                  accumulate_g, s.stream, O.in1 >= 0 ? (bf16*)dx1 : nullptr, acc1,
+                                                  ldy), "bn_bwd_reduce"));
       XP_TRY(prof_end(c, s, XP_PROF_BN_BWD_REDUCE, pass_bytes));
       XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, launch_bn_bwd_apply(xmid, (const bf16*)dy, yout, pw8, s.stats[o][slot], W + N.woff, n,
                                                  O.smid.h, O.smid.w, O.smid.c, O.sout.h, O.sout.w, p.kh, p.kw, p.sh,
-                                                 p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws, dmid, s.stream),
+                                                 p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws, dmid, s.stream, ldy),
                           "bn_bwd_apply"));
       XP_TRY(prof_end(c, s, XP_PROF_BN_BWD_APPLY, pass_bytes + 2.0 * mid_e));
       // fork: the weight gradient (into g, read only by the update) on the side stream.
@@ -209,7 +247,8 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       const PoolGeo p = pool_geo(c, O.lmain);
       return check_launch(c, launch_pool_bwd((const bf16*)s.act[O.in0][slot], (const bf16*)dy, (bf16*)dx0, n,
                                              O.sin0.h, O.sin0.w, O.sin0.c, O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw,
-                                             p.ph, p.pw, O.kind == OP_AVGPOOL, acc0, s.stream), "pool_bwd");
+                                             p.ph, p.pw, O.kind == OP_AVGPOOL, acc0, s.stream,
+                                             s.plan.tensors[O.out].pitch()), "pool_bwd");
     }
     case OP_GAP:
       if (!dx0) return XP_OK;

@@ -62,15 +62,24 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
   s.grad.assign(p.tensors.size(), nullptr);
   for (size_t t = 1; t < p.tensors.size(); ++t) {
     const TensorInfo& T = p.tensors[t];
+    if (T.producer == -2 || T.alias >= 0) continue;  // folded into a conv block / a concat view
     const size_t bytes = ((size_t)n * T.shape.size() * T.es + 15) & ~size_t(15);
     uint8_t* base = (uint8_t*)A(bytes * s.S);  // the S slots of one tensor, packed
     if (!base) return set_err(c, XP_ENOMEM, "stash");
     s.act[t].resize(s.S);
     for (int i = 0; i < s.S; ++i) s.act[t][i] = base + i * bytes;
   }
+  // channel-offset views into their concat's buffers (slots of the same layout)
+  for (size_t t = 1; t < p.tensors.size(); ++t) {
+    const TensorInfo& T = p.tensors[t];
+    if (T.alias < 0) continue;
+    s.act[t].resize(s.S);
+    for (int i = 0; i < s.S; ++i) s.act[t][i] = (uint8_t*)s.act[T.alias][i] + (size_t)T.coff * T.es;
+  }
   // activation-gradient buffers, one per tensor (reused by every backward pass, stream-ordered)
   for (size_t t = 0; t < p.tensors.size(); ++t) {
-    if (t == (size_t)p.out_tensor) continue;  // seeded by the gradient ring / dz
+    if (t == (size_t)p.out_tensor || p.tensors[t].producer == -2 || p.tensors[t].alias >= 0)
+      continue;  // seeded by the ring / dz; unused; a slice of its concat's gradient
     if (!(s.grad[t] = A((size_t)n * p.tensors[t].shape.size() * 4))) return set_err(c, XP_ENOMEM, "gradient buffers");
   }
   s.mid.assign(p.ops.size(), {});
@@ -126,6 +135,9 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
       bnws = std::max(bnws, bn_ws_floats(Mmid, O.smid.c));
       bnws = std::max(bnws, (size_t)((Mmid + 127) / 128) * 2 * O.smid.c);  // fprop-epilogue partials
     }
+    for (const Op& O : p.ops)
+      if (O.kind == OP_LINEAR) s.lin_ldp = std::max(s.lin_ldp, (c->net.layers[O.lmain].d.out_c + 7) / 8 * 8);
+    if (s.lin_ldp && !(s.lin_dy = A((size_t)n * s.lin_ldp * 2))) return set_err(c, XP_ENOMEM, "linear operand");
     s.ws_elems = ws;
     s.ws = (float*)A((size_t)std::max<int64_t>(ws, 64) * 4);
     s.bnws = (float*)A(bnws * 4);

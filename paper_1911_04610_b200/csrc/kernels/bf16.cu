@@ -104,13 +104,13 @@ __device__ __forceinline__ void lane_tree(float* sh, int RL, int G, int W, int r
   __syncthreads();
 }
 
-__global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C, int RC, float* __restrict__ part) {
-  pdl_wait();
+__device__ __forceinline__ void stats_partial_body(const bf16* __restrict__ x, int M, int C, int RC,
+                                                   float* __restrict__ part, int blk) {
   extern __shared__ float sh[];  // [RL][G][8]
   const int G = C / 8, RL = blockDim.x / G;
   const int g = threadIdx.x % G, rl = threadIdx.x / G;
   const bool act = rl < RL;
-  const int r0 = blockIdx.x * RC, r1 = min(M, r0 + RC);
+  const int r0 = blk * RC, r1 = min(M, r0 + RC);
   uint4 keep[kBnRows];
   float sum[8];
 #pragma unroll
@@ -156,10 +156,14 @@ __global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C
     for (int e = 0; e < 8; ++e) slot[e] = m2[e];
   lane_tree(sh, RL, G, 8, rl, g);
   if (rl == 0) {
-    float* p = part + (size_t)blockIdx.x * 2 * C;
+    float* p = part + (size_t)blk * 2 * C;
 #pragma unroll
     for (int e = 0; e < 8; ++e) { p[g * 8 + e] = mean[e]; p[C + g * 8 + e] = sh[(size_t)g * 8 + e]; }
   }
+}
+__global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C, int RC, float* __restrict__ part) {
+  pdl_wait();
+  stats_partial_body(x, M, C, RC, part, blockIdx.x);
   pdl_trigger();
 }
 
@@ -167,12 +171,11 @@ __global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C
 // tid % 8) takes channel c = 8*blockIdx.x + cc and merges chunks j, j+32, j+64, ... in order
 // (Chan's pairwise formula; loads batched 8 deep), then the 32 lanes of a channel are combined by
 // a fixed pairwise tree in shared memory (deterministic).
-__global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
-                                      const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
-                                      float* __restrict__ stats) {
-  pdl_wait();
+__device__ __forceinline__ void stats_final_body(const float* __restrict__ part, int chunks, int M, int RC, int C,
+                                                 float eps, const bf16* __restrict__ gamma,
+                                                 const bf16* __restrict__ beta, float* __restrict__ stats, int unit) {
   __shared__ float sh[32][8][3];
-  const int cc = threadIdx.x & 7, j = threadIdx.x >> 3, c = blockIdx.x * 8 + cc;
+  const int cc = threadIdx.x & 7, j = threadIdx.x >> 3, c = unit * 8 + cc;
   float na = 0.f, mean = 0.f, m2 = 0.f;
   if (c < C) {
     for (int k = j; k < chunks; k += 8 * 32) {
@@ -206,6 +209,12 @@ __global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks
     stats[2 * C + c] = __bfloat162float(gamma[c]);
     stats[3 * C + c] = __bfloat162float(beta[c]);
   }
+}
+__global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
+                                      const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
+                                      float* __restrict__ stats) {
+  pdl_wait();
+  stats_final_body(part, chunks, M, RC, C, eps, gamma, beta, stats, blockIdx.x);
   pdl_trigger();
 }
 
@@ -215,13 +224,14 @@ __global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks
 // PK = 2: pools whose 2x2 windows tile the map exactly (compile-time window, no bounds checks,
 // the four loads issued together); PK = 0: any window, runtime loop
 template <int PK>
-__global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restrict__ st, bf16* __restrict__ y,
-                                uint8_t* __restrict__ pidx, int n, int H, int W, int C, int P, int Q, int kh, int kw,
-                                int sh, int sw, int ph, int pw, int pool, int relu) {
-  pdl_wait();
+__device__ __forceinline__ void bn_apply_body(const bf16* __restrict__ x, const float* __restrict__ st,
+                                              bf16* __restrict__ y, uint8_t* __restrict__ pidx, int n, int H, int W,
+                                              int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw,
+                                              int pool, int relu, int i0, int istride,
+                                              const bf16* __restrict__ res, int ldy) {
   const int G = C / 8;
   const int total = n * P * Q * G;  // < 2^30 (checked at launch): 32-bit index arithmetic
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+  for (int i = i0; i < total; i += istride) {
     const int g = i % G;
     int r = i / G;
     const int q = r % Q;
@@ -234,7 +244,19 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
     ld8f(st + c0, mean); ld8f(st + C + c0, rstd); ld8f(st + 2 * C + c0, ga); ld8f(st + 3 * C + c0, be);
 #pragma unroll
     for (int e = 0; e < 8; ++e) { best[e] = 0.f; arg[e] = 0; }
-    if (!pool) {
+    if (!pool && res) {  // folded residual Add: relu?(Q(Q(BN(x)) + res))
+      const int64_t o = (((int64_t)s * H + p) * W + q) * C + c0;
+      const uint4 u = *reinterpret_cast<const uint4*>(x + o);
+      const uint4 ur = *reinterpret_cast<const uint4*>(res + o);
+      const bf16* v = reinterpret_cast<const bf16*>(&u);
+      const bf16* rv = reinterpret_cast<const bf16*>(&ur);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float t = q16(__fadd_rn(bn_act(__bfloat162float(v[e]), mean[e], rstd[e], ga[e], be[e], 0),
+                                      __bfloat162float(rv[e])));
+        best[e] = (relu && !(t > 0.f)) ? 0.f : t;
+      }
+    } else if (!pool) {
       const uint4 u = *reinterpret_cast<const uint4*>(x + (((int64_t)s * H + p) * W + q) * C + c0);
       const bf16* v = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
@@ -268,8 +290,17 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
       __nv_bfloat162 t = __floats2bfloat162_rn(best[2 * h2], best[2 * h2 + 1]);
       w4[h2] = *reinterpret_cast<uint32_t*>(&t);
     }
-    *reinterpret_cast<uint4*>(y + (((int64_t)s * P + p) * Q + q) * C + c0) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    *reinterpret_cast<uint4*>(y + (((int64_t)s * P + p) * Q + q) * ldy + c0) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
   }
+}
+template <int PK>
+__global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restrict__ st, bf16* __restrict__ y,
+                                uint8_t* __restrict__ pidx, int n, int H, int W, int C, int P, int Q, int kh, int kw,
+                                int sh, int sw, int ph, int pw, int pool, int relu, const bf16* __restrict__ res,
+                                int ldy) {
+  pdl_wait();
+  bn_apply_body<PK>(x, st, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool, relu,
+                    blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, res, ldy);
 }
 
 // The gradient reaching 8 channels of BN-output element (s,h,w,c0..c0+7), from the stash of
@@ -278,6 +309,7 @@ __global__ void bn_apply_kernel(const bf16* __restrict__ x, const float* __restr
 // winner's activation, so `y > 0` is exactly the ReLU mask of the winner).
 struct BwdGeo {
   int H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool, relu;
+  int ldy;  // row pitch of dout / y (the op output; > C for a concat view), pidx stays dense
 };
 
 __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const bf16* __restrict__ y,
@@ -286,7 +318,7 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
 #pragma unroll
   for (int e = 0; e < 8; ++e) dy[e] = 0.f;
   if (!G.pool) {  // row = (s*H + h)*W + w indexes dout/y directly
-    const int64_t o = (int64_t)row * G.C + c0;
+    const int64_t o = (int64_t)row * G.ldy + c0;
     const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
     const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
     const bf16* d = reinterpret_cast<const bf16*>(&ud);
@@ -299,10 +331,10 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
   if (G.pool == 2) {  // windows tile the map exactly: the one window holding (h, w)
     const int p = h / G.kh, q = w / G.kw;
     const int pos = (h - p * G.kh) * G.kw + (w - q * G.kw);
-    const int64_t o = (((int64_t)s * G.P + p) * G.Q + q) * G.C + c0;
-    const uint2 ui = *reinterpret_cast<const uint2*>(pidx + o);
-    const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
-    const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
+    const int64_t ro = ((int64_t)s * G.P + p) * G.Q + q;
+    const uint2 ui = *reinterpret_cast<const uint2*>(pidx + ro * G.C + c0);
+    const uint4 ud = *reinterpret_cast<const uint4*>(dout + ro * G.ldy + c0);
+    const uint4 uy = *reinterpret_cast<const uint4*>(y + ro * G.ldy + c0);
     const bf16* d = reinterpret_cast<const bf16*>(&ud);
     const bf16* yy = reinterpret_cast<const bf16*>(&uy);
 #pragma unroll
@@ -320,10 +352,10 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
       const int a = h - (p * G.sh - G.ph), b = w - (q * G.sw - G.pw);
       if (a < 0 || a >= G.kh || b < 0 || b >= G.kw) continue;
       const int pos = a * G.kw + b;
-      const int64_t o = (((int64_t)s * G.P + p) * G.Q + q) * G.C + c0;
-      const uint2 ui = *reinterpret_cast<const uint2*>(pidx + o);
-      const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
-      const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
+      const int64_t ro = ((int64_t)s * G.P + p) * G.Q + q;
+      const uint2 ui = *reinterpret_cast<const uint2*>(pidx + ro * G.C + c0);
+      const uint4 ud = *reinterpret_cast<const uint4*>(dout + ro * G.ldy + c0);
+      const uint4 uy = *reinterpret_cast<const uint4*>(y + ro * G.ldy + c0);
       const bf16* d = reinterpret_cast<const bf16*>(&ud);
       const bf16* yy = reinterpret_cast<const bf16*>(&uy);
 #pragma unroll
@@ -344,15 +376,16 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
 // per chunk of RC rows: sum dy and sum dy*xhat per channel (8 channels per thread, row lanes
 // combined by a fixed tree) -> part[chunk][2][C]
 
-__global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
-                                     const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
-                                     const float* __restrict__ st, BwdGeo G, int M, int RC, float* __restrict__ part) {
-  pdl_wait();
+__device__ __forceinline__ void bwd_reduce_body(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                                const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
+                                                const float* __restrict__ st, const BwdGeo& G, int M, int RC,
+                                                float* __restrict__ part, int blk, bf16* __restrict__ dres,
+                                                int acc_res) {
   extern __shared__ float sh[];
   const int C = G.C, NG = C / 8, RL = blockDim.x / NG;
   const int g = threadIdx.x % NG, rl = threadIdx.x / NG;
   const int c0 = g * 8;
-  const int r0 = blockIdx.x * RC, r1 = min(M, r0 + RC);
+  const int r0 = blk * RC, r1 = min(M, r0 + RC);
   float s1[8], s2[8], mean[8], rstd[8];
   ld8f(st + c0, mean); ld8f(st + C + c0, rstd);
 #pragma unroll
@@ -363,6 +396,24 @@ __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __r
     if (rl < RL && r < r1) {
       float dy[8];
       routed_dy8(dout, y, pidx, G, r, c0, dy);
+      if (dres) {  // folded residual Add (unpooled): the residual input's gradient is dy' too
+        bf16* dp = dres + (int64_t)r * C + c0;
+        float o8[8];
+        if (acc_res) ld8bf(dp, o8);
+        uint32_t w4[4];
+#pragma unroll
+        for (int h2 = 0; h2 < 4; ++h2) {
+          float v2[2];
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int e = 2 * h2 + t;
+            v2[t] = acc_res ? __fadd_rn(o8[e], q16(dy[e])) : dy[e];
+          }
+          __nv_bfloat162 t2 = __floats2bfloat162_rn(v2[0], v2[1]);
+          w4[h2] = *reinterpret_cast<uint32_t*>(&t2);
+        }
+        *reinterpret_cast<uint4*>(dp) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      }
       const uint4 ux = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + c0);
       const bf16* xv = reinterpret_cast<const bf16*>(&ux);
 #pragma unroll
@@ -379,20 +430,27 @@ __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __r
     for (int e = 0; e < 8; ++e) { slot[e] = s1[e]; slot[8 + e] = s2[e]; }
   lane_tree(sh, RL, NG, 16, rl, g);
   if (rl == 0) {
-    float* p = part + (size_t)blockIdx.x * 2 * C;
+    float* p = part + (size_t)blk * 2 * C;
 #pragma unroll
     for (int e = 0; e < 8; ++e) { p[c0 + e] = slot[e]; p[C + c0 + e] = slot[8 + e]; }
   }
+}
+__global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                     const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
+                                     const float* __restrict__ st, BwdGeo G, int M, int RC, float* __restrict__ part,
+                                     bf16* __restrict__ dres, int acc_res) {
+  pdl_wait();
+  bwd_reduce_body(x, dout, y, pidx, st, G, M, RC, part, blockIdx.x, dres, acc_res);
   pdl_trigger();
 }
 
 // totals over chunks (layout as bn_stats_final_kernel: 32 lanes per channel over chunks in
 // order, then a fixed tree); dgamma/dbeta into the accumulator
-__global__ void bn_bwd_final_kernel(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
-                                    float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate) {
-  pdl_wait();
+__device__ __forceinline__ void bwd_final_body(const float* __restrict__ part, int chunks, int C,
+                                               float* __restrict__ tot, float* __restrict__ g_gamma,
+                                               float* __restrict__ g_beta, int accumulate, int unit) {
   __shared__ float sh[32][8][2];
-  const int cc = threadIdx.x & 7, j = threadIdx.x >> 3, c = blockIdx.x * 8 + cc;
+  const int cc = threadIdx.x & 7, j = threadIdx.x >> 3, c = unit * 8 + cc;
   float s1 = 0.f, s2 = 0.f;
   if (c < C) {
     for (int k = j; k < chunks; k += 8 * 32) {
@@ -424,19 +482,24 @@ __global__ void bn_bwd_final_kernel(const float* __restrict__ part, int chunks, 
     g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
     g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
   }
+}
+__global__ void bn_bwd_final_kernel(const float* __restrict__ part, int chunks, int C, float* __restrict__ tot,
+                                    float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate) {
+  pdl_wait();
+  bwd_final_body(part, chunks, C, tot, g_gamma, g_beta, accumulate, blockIdx.x);
   pdl_trigger();
 }
 
 // dx = Q(gamma_b * rstd * (dy - sum(dy)/cnt - xhat * sum(dy xhat)/cnt)), 8 channels per thread
-__global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
-                                    const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
-                                    const float* __restrict__ st, const float* __restrict__ tot,
-                                    const bf16* __restrict__ gamma_b, BwdGeo G, int M, bf16* __restrict__ dx) {
-  pdl_wait();
+__device__ __forceinline__ void bwd_apply_body(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                               const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
+                                               const float* __restrict__ st, const float* __restrict__ tot,
+                                               const bf16* __restrict__ gamma_b, const BwdGeo& G, int M,
+                                               bf16* __restrict__ dx, int i0, int istride) {
   const int C = G.C, NG = C / 8;
   const float inv_cnt = 1.f / (float)M;
   const int total = M * NG;  // < 2^30 (checked at launch): 32-bit index arithmetic
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+  for (int i = i0; i < total; i += istride) {
     const int g = i % NG;
     const int r = i / NG;
     const int c0 = g * 8;
@@ -463,29 +526,35 @@ __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __re
     *reinterpret_cast<uint4*>(dx + (int64_t)r * C + c0) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
   }
 }
+__global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                    const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
+                                    const float* __restrict__ st, const float* __restrict__ tot,
+                                    const bf16* __restrict__ gamma_b, BwdGeo G, int M, bf16* __restrict__ dx) {
+  pdl_wait();
+  bwd_apply_body(x, dout, y, pidx, st, tot, gamma_b, G, M, dx, blockIdx.x * blockDim.x + threadIdx.x,
+                 gridDim.x * blockDim.x);
+}
 
 // Pooled layers whose windows tile the map exactly (kh == sh, kw == sw, no padding, H = P*kh,
 // W = Q*kw): one thread per (pooled output, 8 channels) -- the routed gradient, winner index and
 // ReLU mask are loaded once for the kh*kw inputs of the window; per element the arithmetic is
 // bn_bwd_apply_kernel's (every input lies in exactly one window, so no Q() of a fan-in sum).
 template <int PK>  // 2: 2x2 windows (compile-time, unrolled), 0: runtime kh x kw
-__global__ void bn_bwd_apply_tiled_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
-                                          const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
-                                          const float* __restrict__ st, const float* __restrict__ tot,
-                                          const bf16* __restrict__ gamma_b, BwdGeo G, int M, int Mo,
-                                          bf16* __restrict__ dx) {
-  pdl_wait();
+__device__ __forceinline__ void bwd_apply_tiled_body(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                                     const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
+                                                     const float* __restrict__ st, const float* __restrict__ tot,
+                                                     const bf16* __restrict__ gamma_b, const BwdGeo& G, int M, int Mo,
+                                                     bf16* __restrict__ dx, int i0, int istride) {
   const int C = G.C, NG = C / 8;
   const float inv_cnt = 1.f / (float)M;
   const int total = Mo * NG;  // < 2^30 (checked at launch)
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+  for (int i = i0; i < total; i += istride) {
     const int g = i % NG, ro = i / NG;
     const int q = ro % G.Q, t = ro / G.Q, p = t % G.P, s = t / G.P;
     const int c0 = g * 8;
-    const int64_t o = (int64_t)ro * C + c0;
-    const uint2 ui = *reinterpret_cast<const uint2*>(pidx + o);
-    const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
-    const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
+    const uint2 ui = *reinterpret_cast<const uint2*>(pidx + (int64_t)ro * C + c0);
+    const uint4 ud = *reinterpret_cast<const uint4*>(dout + (int64_t)ro * G.ldy + c0);
+    const uint4 uy = *reinterpret_cast<const uint4*>(y + (int64_t)ro * G.ldy + c0);
     const bf16* d = reinterpret_cast<const bf16*>(&ud);
     const bf16* yy = reinterpret_cast<const bf16*>(&uy);
     float gv[8];
@@ -525,6 +594,16 @@ __global__ void bn_bwd_apply_tiled_kernel(const bf16* __restrict__ x, const bf16
       }
   }
 }
+template <int PK>
+__global__ void bn_bwd_apply_tiled_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                          const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
+                                          const float* __restrict__ st, const float* __restrict__ tot,
+                                          const bf16* __restrict__ gamma_b, BwdGeo G, int M, int Mo,
+                                          bf16* __restrict__ dx) {
+  pdl_wait();
+  bwd_apply_tiled_body<PK>(x, dout, y, pidx, st, tot, gamma_b, G, M, Mo, dx, blockIdx.x * blockDim.x + threadIdx.x,
+                           gridDim.x * blockDim.x);
+}
 
 // ---- bf16-operand Linear (small: micro-batch rows) ------------------------------------------
 // y[r][o] = sum_i x[r][i] W[o][i] (fp32) + b[o]; logits: fp32 out, else Q(relu?) bf16.
@@ -555,6 +634,24 @@ __device__ __forceinline__ float load_dy(const void* dy, int64_t idx, const bf16
   float d = DY_F32 ? q16(static_cast<const float*>(dy)[idx]) : __bfloat162float(static_cast<const bf16*>(dy)[idx]);
   if (mask && !(__bfloat162float(mask[idx]) > 0.f)) d = 0.f;
   return d;
+}
+
+// tensor-core Linear backward operand: dyp[r][o] = dy'[r][o] (bf16; the masked, bf16-rounded
+// output gradient load_dy gives), zero for out <= o < ldp; gb[o] (=|+=) sum_r dy'[r][o] in r order
+// (the bias gradient of linear_wgrad_bf16_kernel, same bits)
+template <bool DY_F32>
+__global__ void linear_dy_prep_kernel(const void* __restrict__ dy, const bf16* __restrict__ mask, bf16* __restrict__ dyp,
+                                      int ldp, float* __restrict__ gb, int n, int out, int accumulate) {
+  pdl_wait();
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= ldp) return;
+  float acc = 0.f;
+  for (int r = 0; r < n; ++r) {
+    const float d = o < out ? load_dy<DY_F32>(dy, (int64_t)r * out + o, mask) : 0.f;
+    dyp[(int64_t)r * ldp + o] = __float2bfloat16_rn(d);
+    acc += d;
+  }
+  if (gb && o < out) gb[o] = accumulate ? __fadd_rn(gb[o], acc) : acc;
 }
 
 // dx[r][i] = Q(sum_o dy'[r][o] W[o][i]); thread per (r, i)
@@ -680,32 +777,35 @@ cudaError_t launch_bn_stats_final(const float* part, int chunks, int M, int RC, 
 }
 
 cudaError_t launch_bn_apply(const bf16* x, const float* stats, bf16* y, uint8_t* pidx, int n, int H, int W, int C, int P,
-                            int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st) {
+                            int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st,
+                            const bf16* res, int ldy) {
+  if (!ldy) ldy = C;
   const int64_t total = (int64_t)n * P * Q * (C / 8);
-  if (C % 8 || total >= kMaxElems) return cudaErrorInvalidValue;
+  if (C % 8 || total >= kMaxElems || (res && pool)) return cudaErrorInvalidValue;
   if (pool && kh == 2 && kw == 2 && sh == 2 && sw == 2 && ph == 0 && pw == 0 && H == 2 * P && W == 2 * Q &&
       !bn_tiled_off())
     launch_pdl(bn_apply_kernel<2>, dim3(grid1d(total)), dim3(256), 0, st, x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh,
-               sw, ph, pw, 1, relu ? 1 : 0);
+               sw, ph, pw, 1, relu ? 1 : 0, (const bf16*)nullptr, ldy);
   else
     launch_pdl(bn_apply_kernel<0>, dim3(grid1d(total)), dim3(256), 0, st, x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh,
-               sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0);
+               sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0, res, ldy);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bn_bwd_reduce(const bf16* x, const bf16* dout, const bf16* y, const uint8_t* pidx,
                                  const float* stats, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
                                  int sw, int ph, int pw, bool pool, bool relu, float* ws, float* g_gamma, float* g_beta,
-                                 bool accumulate, cudaStream_t st) {
-  if (C % 8 || C > 2048) return cudaErrorInvalidValue;
-  BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
+                                 bool accumulate, cudaStream_t st, bf16* dres, bool acc_res, int ldy) {
+  if (C % 8 || C > 2048 || (dres && pool) || (ldy && ldy % 8)) return cudaErrorInvalidValue;
+  BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0, ldy ? ldy : C};
   if (pool && kh == sh && kw == sw && ph == 0 && pw == 0 && H == P * kh && W == Q * kw && !bn_tiled_off()) G.pool = 2;
   const int M = n * H * W;
   const int RC = bn_chunk_rows(M, C), chunks = bn_chunks(M, C);
   const int threads = bn_threads(C);
   const size_t shm = (size_t)threads * 16 * 4;
   float* tot = ws + (size_t)chunks * 2 * C;
-  launch_pdl(bn_bwd_reduce_kernel, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC, ws);
+  launch_pdl(bn_bwd_reduce_kernel, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC, ws, dres,
+             acc_res ? 1 : 0);
   launch_pdl(bn_bwd_final_kernel, dim3((C + 7) / 8), dim3(256), 0, st, (const float*)ws, chunks, C, tot, g_gamma, g_beta,
              accumulate ? 1 : 0);
   return cudaGetLastError();
@@ -714,9 +814,9 @@ cudaError_t launch_bn_bwd_reduce(const bf16* x, const bf16* dout, const bf16* y,
 cudaError_t launch_bn_bwd_apply(const bf16* x, const bf16* dout, const bf16* y, const uint8_t* pidx, const float* stats,
                                 const bf16* gamma_b, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
                                 int sw, int ph, int pw, bool pool, bool relu, const float* ws, bf16* dx,
-                                cudaStream_t st) {
-  if (C % 8 || C > 2048) return cudaErrorInvalidValue;
-  BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0};
+                                cudaStream_t st, int ldy) {
+  if (C % 8 || C > 2048 || (ldy && ldy % 8)) return cudaErrorInvalidValue;
+  BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0, ldy ? ldy : C};
   const int M = n * H * W;
   const float* tot = ws + (size_t)bn_chunks(M, C) * 2 * C;
   if ((int64_t)M * (C / 8) >= kMaxElems) return cudaErrorInvalidValue;
@@ -733,6 +833,18 @@ cudaError_t launch_bn_bwd_apply(const bf16* x, const bf16* dout, const bf16* y, 
   }
   launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats, tot,
              gamma_b, G, M, dx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_linear_dy_prep(const void* dy, bool dy_f32, const bf16* mask, bf16* dyp, int ldp, float* gb, int n,
+                                  int out, bool accumulate, cudaStream_t st) {
+  if (ldp % 8 || ldp < out) return cudaErrorInvalidValue;
+  if (dy_f32)
+    launch_pdl(linear_dy_prep_kernel<true>, dim3((ldp + 127) / 128), dim3(128), 0, st, dy, mask, dyp, ldp, gb, n, out,
+               accumulate ? 1 : 0);
+  else
+    launch_pdl(linear_dy_prep_kernel<false>, dim3((ldp + 127) / 128), dim3(128), 0, st, dy, mask, dyp, ldp, gb, n, out,
+               accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -823,7 +935,7 @@ __global__ void concat_bwd_kernel(const bf16* dy, bf16* da, bf16* db, int64_t ro
 }
 // pooling forward: mode 0 max (first max, padded positions skipped), 1 avg (count_include_pad)
 __global__ void pool_fwd_kernel(const bf16* x, bf16* y, int n, int H, int W, int C, int P, int Q, int kh, int kw,
-                                int sh, int sw, int ph, int pw, int mode) {
+                                int sh, int sw, int ph, int pw, int mode, int ldy) {
   pdl_wait();
   const int64_t total = (int64_t)n * P * Q * C;
   const float inv = 1.f / (float)(kh * kw);
@@ -843,14 +955,14 @@ __global__ void pool_fwd_kernel(const bf16* x, bf16* y, int n, int H, int W, int
         if (mode == 0) { if (first || v > best) best = v; first = false; }
         else acc = __fadd_rn(acc, v);
       }
-    y[i] = __float2bfloat16_rn(mode == 0 ? best : __fmul_rn(acc, inv));
+    y[(((int64_t)s * P + p) * Q + q) * ldy + c] = __float2bfloat16_rn(mode == 0 ? best : __fmul_rn(acc, inv));
   }
 }
 // pooling backward, gather form over the input: for each input element sum the gradients of
 // the windows that route to it (max: it is the window's first max; avg: every window
 // covering it contributes g*inv), then store/accumulate
 __global__ void pool_bwd_kernel(const bf16* x, const bf16* dy, bf16* dx, int n, int H, int W, int C, int P, int Q,
-                                int kh, int kw, int sh, int sw, int ph, int pw, int mode, int accumulate) {
+                                int kh, int kw, int sh, int sw, int ph, int pw, int mode, int accumulate, int ldy) {
   pdl_wait();
   const int64_t total = (int64_t)n * H * W * C;
   const float inv = 1.f / (float)(kh * kw);
@@ -867,7 +979,7 @@ __global__ void pool_bwd_kernel(const bf16* x, const bf16* dy, bf16* dx, int n, 
     for (int p = plo; p <= phi; ++p)
       for (int q = qlo; q <= qhi; ++q) {
         if (h < p * sh - ph || h >= p * sh - ph + kh || w < q * sw - pw || w >= q * sw - pw + kw) continue;
-        const float g = __bfloat162float(dy[(((int64_t)s * P + p) * Q + q) * C + c]);
+        const float g = __bfloat162float(dy[(((int64_t)s * P + p) * Q + q) * ldy + c]);
         if (mode == 0) {
           float best = 0.f;
           int bh = -1, bw = -1;
@@ -933,14 +1045,15 @@ cudaError_t launch_concat_bwd(const bf16* dy, bf16* da, bf16* db, int64_t rows, 
   return cudaGetLastError();
 }
 cudaError_t launch_pool_fwd(const bf16* x, bf16* y, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
-                            int sw, int ph, int pw, bool avg, cudaStream_t st) {
-  launch_pdl(pool_fwd_kernel, dim3(g1((int64_t)n * P * Q * C)), dim3(256), 0, st, x, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, avg ? 1 : 0);
+                            int sw, int ph, int pw, bool avg, cudaStream_t st, int ldy) {
+  launch_pdl(pool_fwd_kernel, dim3(g1((int64_t)n * P * Q * C)), dim3(256), 0, st, x, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
+             avg ? 1 : 0, ldy ? ldy : C);
   return cudaGetLastError();
 }
 cudaError_t launch_pool_bwd(const bf16* x, const bf16* dy, bf16* dx, int n, int H, int W, int C, int P, int Q, int kh,
-                            int kw, int sh, int sw, int ph, int pw, bool avg, bool accumulate, cudaStream_t st) {
+                            int kw, int sh, int sw, int ph, int pw, bool avg, bool accumulate, cudaStream_t st, int ldy) {
   launch_pdl(pool_bwd_kernel, dim3(g1((int64_t)n * H * W * C)), dim3(256), 0, st, x, dy, dx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
-                                                              avg ? 1 : 0, accumulate ? 1 : 0);
+                                                              avg ? 1 : 0, accumulate ? 1 : 0, ldy ? ldy : C);
   return cudaGetLastError();
 }
 cudaError_t launch_gap_fwd(const bf16* x, bf16* y, int n, int HW, int C, cudaStream_t st) {

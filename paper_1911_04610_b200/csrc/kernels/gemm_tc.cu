@@ -358,6 +358,25 @@ __device__ __forceinline__ float warp_colsum(float (&t)[32], int lane) {
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // the 4 epilogue warps
 __device__ __forceinline__ float bf16r(uint32_t v) { return __bfloat162float(__float2bfloat16_rn(__uint_as_float(v))); }
 
+// swap-AB Linear epilogue: 8 columns (samples) [col0, col0+8) of feature row `row`:
+// v = acc + b[row]; fp32 out (logits) as is, else Q(relu ? max(v, 0) : v)
+__device__ __forceinline__ void linear_t_store8(const GemmArgs& a, int row, int col0, const float (&v)[8]) {
+  if (row >= a.M) return;
+  const float b = a.bias ? __bfloat162float(a.bias[row]) : 0.f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    if (col0 + e >= a.N) break;
+    float x = a.bias ? __fadd_rn(v[e], b) : v[e];
+    const int64_t o = (int64_t)(col0 + e) * a.ldo + row;
+    if (a.f32out) {
+      static_cast<float*>(a.out)[o] = x;
+    } else {
+      if (a.relu) x = x > 0.f ? x : 0.f;
+      static_cast<bf16*>(a.out)[o] = __float2bfloat16_rn(x);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // epilogue: row m of the tile, 32 accumulator columns starting at col0
 // ---------------------------------------------------------------------------------------
@@ -422,6 +441,14 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
           if (col0 + e + h < a.N) o[e + h] = __uint_as_float(v[e + h]);
       }
     }
+  } else if (a.epi == EPI_LINEAR_T) {  // out[c][m] = epi(D[m][c]); lanes = consecutive m
+    float v8[8];
+#pragma unroll
+    for (int e0 = 0; e0 < 32; e0 += 8) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v8[e] = __uint_as_float(v[e0 + e]);
+      linear_t_store8(a, row, col0 + e0, v8);
+    }
   } else {  // EPI_WGRAD_T: g[co][m] (=|+=) D[m][co]; lanes = consecutive m -> coalesced
     float* g = static_cast<float*>(a.out) + (int64_t)col0 * a.ldo + row;
     if (a.accumulate) {
@@ -467,6 +494,8 @@ __device__ __forceinline__ void epi_store8(const GemmArgs& a, int row, int col0,
     float* o = static_cast<float*>(a.out) + (int64_t)row * a.ldo + col0;
     for (int e = 0; e < 8; ++e)
       if (col0 + e < a.N) o[e] = v[e];
+  } else if (a.epi == EPI_LINEAR_T) {
+    linear_t_store8(a, row, col0, v);
   } else {
     float* g = static_cast<float*>(a.out) + (int64_t)col0 * a.ldo + row;
     float old[8];
@@ -1364,6 +1393,37 @@ cudaError_t tc_conv_wgrad(const ConvGeo& g, const bf16* X, const bf16* dY, float
   return run_split<GEMM_WGRAD, true, true>(a, EPI_WGRAD_T, gW, a.M, accumulate ? 1 : 0, ws, ws_elems, counters, st);
 }
 
+cudaError_t tc_linear_fwd(const bf16* x, const bf16* W, const bf16* b, void* y, int n, int in, int out, bool relu,
+                          bool f32out, float* ws, int64_t ws_elems, int* counters, cudaStream_t st) {
+  GemmArgs a{};
+  a.A = W; a.B = x;
+  a.M = out; a.N = n; a.K = in;
+  a.lda = in; a.ldb = in;
+  a.force_tma = 1;
+  a.bias = b; a.relu = relu ? 1 : 0; a.f32out = f32out ? 1 : 0;
+  return run_split<GEMM_PLAIN, false, false>(a, EPI_LINEAR_T, y, out, 0, ws, ws_elems, counters, st);
+}
+
+cudaError_t tc_linear_dgrad(const bf16* dyp, int ldp, const bf16* W, bf16* dx, int n, int in, int out, float* ws,
+                            int64_t ws_elems, int* counters, cudaStream_t st) {
+  GemmArgs a{};
+  a.A = W; a.B = dyp;
+  a.M = in; a.N = n; a.K = out;
+  a.lda = in; a.ldb = ldp;  // A = W^T (MN-major: W [out][in]), B = dyp [n][ldp] (K-major)
+  a.force_tma = 1;
+  return run_split<GEMM_PLAIN, true, false>(a, EPI_LINEAR_T, dx, in, 0, ws, ws_elems, counters, st);
+}
+
+cudaError_t tc_linear_wgrad(const bf16* x, const bf16* dyp, int ldp, float* gW, int n, int in, int out,
+                            bool accumulate, float* ws, int64_t ws_elems, int* counters, cudaStream_t st) {
+  GemmArgs a{};
+  a.A = x; a.B = dyp;
+  a.M = in; a.N = out; a.K = n;
+  a.lda = in; a.ldb = ldp;  // both MN-major: x [n][in], dyp [n][ldp]
+  a.force_tma = 1;
+  return run_split<GEMM_PLAIN, true, true>(a, EPI_WGRAD_T, gW, in, accumulate ? 1 : 0, ws, ws_elems, counters, st);
+}
+
 int64_t tc_conv_ws_elems(const ConvGeo& g) {
   // split-K partial planes + cross-cluster slices of the largest of the three GEMMs
   auto need = [](int M, int N, int K, int min_bn = 64) -> int64_t {
@@ -1414,5 +1474,32 @@ extern "C" int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void
   if (mode == 1) e = xp::tc_conv_fprop(g, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, counters, st);
   else if (mode == 2) e = xp::tc_conv_dgrad(g, g.C, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, counters, st);
   else e = xp::tc_conv_wgrad(g, (const B*)in0, (const B*)in1, (float*)out, accumulate != 0, ws, ws_elems, counters, st);
+  return e == cudaSuccess ? XP_OK : XP_ECUDA;
+}
+
+extern "C" int xpipe_linear_bf16(int32_t mode, const void* x, const void* W, const void* b, const void* dy, int32_t ldp,
+                                 void* out, int32_t n, int32_t in, int32_t out_features, int32_t relu, int32_t f32out,
+                                 int32_t accumulate, float* ws, int64_t ws_elems, void* stream) {
+  if (mode < 1 || mode > 3 || (mode != 3 && !W) || !out || n < 1 || in < 1 || out_features < 1 || in % 8)
+    return XP_EINVAL;
+  if (mode != 1 && (!dy || ldp % 8 || ldp < out_features)) return XP_EINVAL;
+  if (mode != 2 && !x) return XP_EINVAL;
+  if (!ws) ws_elems = 0;
+  int* counters = nullptr;
+  if (ws && ws_elems > xp::kTileCounters) {
+    ws_elems -= xp::kTileCounters;
+    counters = reinterpret_cast<int*>(ws + ws_elems);
+  }
+  typedef __nv_bfloat16 B;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (mode == 1)
+    e = xp::tc_linear_fwd((const B*)x, (const B*)W, (const B*)b, out, n, in, out_features, relu != 0, f32out != 0, ws,
+                          ws_elems, counters, st);
+  else if (mode == 2)
+    e = xp::tc_linear_dgrad((const B*)dy, ldp, (const B*)W, (B*)out, n, in, out_features, ws, ws_elems, counters, st);
+  else
+    e = xp::tc_linear_wgrad((const B*)x, (const B*)dy, ldp, (float*)out, n, in, out_features, accumulate != 0, ws,
+                            ws_elems, counters, st);
   return e == cudaSuccess ? XP_OK : XP_ECUDA;
 }

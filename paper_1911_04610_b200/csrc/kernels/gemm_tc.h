@@ -8,7 +8,9 @@
 namespace xp {
 
 enum { GEMM_PLAIN = 0, GEMM_FPROP = 1, GEMM_DGRAD = 2, GEMM_WGRAD = 3 };
-enum { EPI_BF16 = 0, EPI_F32 = 1, EPI_WGRAD_T = 2 };
+// EPI_LINEAR_T: swap-AB Linear, D[m = feature][c = sample] -> out[c][m] (ldo = features) with
+// the bias of feature m, optional ReLU, bf16 or (f32out) fp32
+enum { EPI_BF16 = 0, EPI_F32 = 1, EPI_WGRAD_T = 2, EPI_LINEAR_T = 3 };
 constexpr int kTileCounters = 1 << 14;  // per-stream split-K arrival counters (zero-initialised)
 
 struct ConvGeo {
@@ -56,6 +58,8 @@ struct GemmArgs {
   int force_tma;            // PLAIN: stream both operands by TMA (the im2col'd first layer)
   unsigned long long* dbg;  // development timing probe (XPIPE_GEMM_DBG), else null
   int dev_flags;            // development experiments (XPIPE_GEMM_DEV), 0 in production
+  const __nv_bfloat16* bias;  // EPI_LINEAR_T: per-row bias (or null)
+  int relu, f32out;           // EPI_LINEAR_T: ReLU on the bf16 output / fp32 output (logits)
 };
 
 // plain GEMM for unit parity: D[M][N] fp32 (ldd) = A(m,k) B(n,k)
@@ -87,6 +91,21 @@ cudaError_t tc_im2col_fprop(const ConvGeo& g, const __nv_bfloat16* cols, const _
                             int* bn_tiles);
 cudaError_t tc_im2col_wgrad(const ConvGeo& g, const __nv_bfloat16* cols, const __nv_bfloat16* dY, float* gW,
                             bool accumulate, float* ws, int64_t ws_elems, int* counters, cudaStream_t st);
+// bf16 Linear layers on the tensor cores, swap-AB (the micro-batch is the narrow N side of the
+// UMMA, features the 128-row M side), both operands by TMA:
+//   fwd  : y[r][o] = epi(sum_i W[o][i] x[r][i] + b[o])      (M = out, N = n, K = in; y fp32 if
+//          f32out, else Q(relu?(.)) bf16)
+//   dgrad: dx[r][i] = Q(sum_o dyp[r][o] W[o][i])              (M = in, N = n, K = out)
+//   wgrad: gW[o][i] (=|+=) sum_r dyp[r][o] x[r][i]           (M = in, N = out, K = n)
+// dyp [n][ldp] bf16 (ldp % 8 == 0, columns >= out zero) is the masked, bf16-rounded output
+// gradient (launch_linear_dy_prep); x rows and W rows need in % 8 == 0.
+cudaError_t tc_linear_fwd(const __nv_bfloat16* x, const __nv_bfloat16* W, const __nv_bfloat16* b, void* y, int n,
+                          int in, int out, bool relu, bool f32out, float* ws, int64_t ws_elems, int* counters,
+                          cudaStream_t st);
+cudaError_t tc_linear_dgrad(const __nv_bfloat16* dyp, int ldp, const __nv_bfloat16* W, __nv_bfloat16* dx, int n,
+                            int in, int out, float* ws, int64_t ws_elems, int* counters, cudaStream_t st);
+cudaError_t tc_linear_wgrad(const __nv_bfloat16* x, const __nv_bfloat16* dyp, int ldp, float* gW, int n, int in,
+                            int out, bool accumulate, float* ws, int64_t ws_elems, int* counters, cudaStream_t st);
 // number of pipeline stages whose streams share this process's busiest device (sets the
 // split-K threshold; 1 = one stage per device)
 void tc_set_coresident_stages(int n);

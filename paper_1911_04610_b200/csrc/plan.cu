@@ -3,6 +3,8 @@
 
 #include "plan.h"
 
+#include <cstdlib>
+
 namespace xp {
 
 namespace {
@@ -217,6 +219,69 @@ int build_net_plan(const xpipe_layer* layers, int n, int K, const xpipe_config& 
       s.max_act = std::max({s.max_act, o.sin0.size(), o.sin1.size(), o.smid.size(), o.sout.size()});
       s.ops.push_back(o);
       i = last + 1;
+    }
+    // fold a residual Add into the conv block right before it: Add(a, b) [+ ReLU] where the
+    // previous op is a conv block without ReLU / pool producing a or b for this Add alone; the
+    // fused op computes relu?(Q(Q(BN(conv)) + other)) -- the rounding points of the separate ops
+    // (XPIPE_NO_ADD_FUSE=1 keeps the separate Add, development)
+    static const bool no_fuse = [] { const char* e = getenv("XPIPE_NO_ADD_FUSE"); return e && *e && *e != '0'; }();
+    for (int o = 1; o < (int)s.ops.size() && !no_fuse; ++o) {
+      Op& A = s.ops[o];
+      Op& C = s.ops[o - 1];
+      if (A.kind != OP_ADD || C.kind != OP_CONV || C.relu || C.lpool >= 0 || C.in1 >= 0) continue;
+      if (C.out != A.in0 && C.out != A.in1) continue;
+      if (A.in0 == A.in1 || s.tensors[C.out].consumers != 1 || C.out == s.out_tensor) continue;
+      const int other = C.out == A.in0 ? A.in1 : A.in0;
+      const Shape so = C.out == A.in0 ? A.sin1 : A.sin0;
+      if (so.c != C.sout.c || so.h != C.sout.h || so.w != C.sout.w) continue;
+      const int dead = C.out;
+      C.in1 = other; C.sin1 = so; C.ladd = A.lmain; C.relu = A.relu; C.lrelu = A.lrelu;
+      C.out = A.out;
+      s.tensors[dead].consumers = 0;
+      s.tensors[dead].producer = -2;  // unused: no buffers
+      s.ops.erase(s.ops.begin() + o);
+      for (auto& t : s.tensors)
+        if (t.producer >= o) --t.producer;
+      s.tensors[C.out].producer = o - 1;
+    }
+    // concat elimination: a Concat whose two inputs are each produced in this stage by a conv
+    // block, a pooling op or another eliminated Concat, and consumed by this Concat alone,
+    // becomes channel-offset views of its output (outermost Concat first, so nested and chained
+    // concats resolve to one buffer); the producers store in place (XPIPE_NO_CONCAT_VIEWS=1 keeps
+    // the copies, development)
+    static const bool no_views = [] { const char* e = getenv("XPIPE_NO_CONCAT_VIEWS"); return e && *e && *e != '0'; }();
+    if (!no_views) {
+      const int no = (int)s.ops.size();
+      std::vector<char> cand(no, 0);
+      auto leaf_ok = [&](int t) {
+        if (t <= 0 || s.tensors[t].consumers != 1) return false;
+        const int pr = s.tensors[t].producer;
+        if (pr < 0) return false;
+        const int kd = s.ops[pr].kind;
+        return kd == OP_CONV || kd == OP_MAXPOOL || kd == OP_AVGPOOL || (kd == OP_CONCAT && cand[pr]);
+      };
+      for (int o = 0; o < no; ++o)
+        if (s.ops[o].kind == OP_CONCAT && s.ops[o].in0 != s.ops[o].in1)
+          cand[o] = leaf_ok(s.ops[o].in0) && leaf_ok(s.ops[o].in1);
+      for (int o = no - 1; o >= 0; --o) {
+        if (!cand[o]) continue;
+        const Op& O = s.ops[o];
+        const TensorInfo& Y = s.tensors[O.out];
+        const int base = Y.alias >= 0 ? Y.alias : O.out;
+        const int off = Y.alias >= 0 ? Y.coff : 0;
+        const int bc = s.tensors[base].shape.c;
+        TensorInfo& A = s.tensors[O.in0];
+        TensorInfo& B = s.tensors[O.in1];
+        A.alias = base; A.coff = off; A.base_c = bc;
+        B.alias = base; B.coff = off + O.sin0.c; B.base_c = bc;
+      }
+      std::vector<int> remap(no, -1);
+      std::vector<Op> kept;
+      for (int o = 0; o < no; ++o)
+        if (!cand[o]) { remap[o] = (int)kept.size(); kept.push_back(s.ops[o]); }
+      for (auto& t : s.tensors)
+        if (t.producer >= 0) t.producer = cand[t.producer] ? -3 : remap[t.producer];  // -3: view of an eliminated concat
+      s.ops.swap(kept);
     }
     // the op producing the logits keeps fp32
     if (s.ops.back().kind == OP_XENT) {

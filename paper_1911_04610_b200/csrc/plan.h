@@ -26,9 +26,14 @@ struct LayerInfo {
 
 // A fused execution unit of the GPU path (one stage = a DAG of ops in layer order):
 //   OP_CONV    : Conv2d + BatchNorm2d [+ ReLU] [+ MaxPool2d]         (bf16, tcgen05)
+//                or, with in1 >= 0, Conv2d + BatchNorm2d + residual Add (in1) [+ ReLU]: the
+//                Add that follows a bias-free, activation-free conv block is folded into the
+//                BN-apply (the ResNet bottleneck's last conv or its downsample branch)
 //   OP_LINEAR  : Linear [+ ReLU]                                      (fp32 contract or bf16)
 //   OP_ADD     : residual add [+ ReLU]
-//   OP_CONCAT  : channel concat of two tensors
+//   OP_CONCAT  : channel concat of two tensors (removed from the plan when both inputs can be
+//                written in place: their producers then store into the concat output at their
+//                channel offset, and their backward reads the gradient slice, see TensorInfo)
 //   OP_MAXPOOL / OP_AVGPOOL : standalone pooling;  OP_GAP : global average pool
 //   OP_XENT    : softmax cross-entropy on the logits
 enum { OP_LINEAR = 1, OP_CONV, OP_XENT, OP_ADD, OP_CONCAT, OP_MAXPOOL, OP_AVGPOOL, OP_GAP };
@@ -36,6 +41,7 @@ enum { OP_LINEAR = 1, OP_CONV, OP_XENT, OP_ADD, OP_CONCAT, OP_MAXPOOL, OP_AVGPOO
 struct Op {
   int kind = 0;
   int lmain = -1, lbn = -1, lrelu = -1, lpool = -1;
+  int ladd = -1;            // OP_CONV with a folded residual Add: the Add layer (in1 = residual)
   int in0 = -1, in1 = -1;   // input tensor ids (0 = the stage input)
   int out = -1;             // output tensor id (stashed per micro-batch)
   Shape sin0, sin1, smid, sout;
@@ -46,8 +52,12 @@ struct Op {
 struct TensorInfo {
   Shape shape;
   int es = 2;               // bytes per element (bf16 activations, fp32 logits / fp32 path)
-  int producer = -1;        // op index (-1 = stage input)
+  int producer = -1;        // op index (-1 = stage input, -2 = unused)
   int consumers = 0;
+  // channel-offset view (a concat input written in place): the tensor is channels
+  // [coff, coff + shape.c) of tensor `alias`, rows of pitch() elements; no buffers of its own
+  int alias = -1, coff = 0, base_c = 0;
+  int pitch() const { return alias >= 0 ? base_c : shape.c; }
 };
 
 struct StagePlan {

@@ -72,6 +72,8 @@ struct StageRT {
   std::vector<float*> dz;               // [slot] logits gradient (last stage)
   std::vector<void*> grad;              // [tensor] activation-gradient buffers (per op pass)
   void* gmid = nullptr;                 // conv op: gradient of the conv output (bf16), buffer 0
+  void* lin_dy = nullptr;               // tensor-core Linear backward operand dyp [n][lin_ldp] bf16
+  int lin_ldp = 0;
   void* gmid1 = nullptr;                //   buffer 1 (consecutive conv ops alternate; see side)
   // weight gradients run on a side stream, off the critical path of the backward chain
   // (bn-backward -> dgrad -> next op): forked after the op's BN backward, joined at the end of

@@ -494,9 +494,14 @@ int enqueue_backward(xpipe_ctx* c, int k, int64_t u) {
   std::vector<void*> gp(s.grad);
   gp[P.out_tensor] = (k + 1 < c->K) ? s.gin_slot[slot] : (void*)s.dz[slot];
   has[P.out_tensor] = 1;
+  // concat views: the gradient of a view is the slice of its concat's gradient (complete once
+  // every consumer of the concat has run, i.e. before the view's producer in reverse order)
+  for (size_t t = 0; t < P.tensors.size(); ++t)
+    if (P.tensors[t].alias >= 0) gp[t] = (uint8_t*)gp[P.tensors[t].alias] + (size_t)P.tensors[t].coff * P.tensors[t].es;
+  auto have = [&](int t) { return has[t] || (P.tensors[t].alias >= 0 && has[P.tensors[t].alias]); };
   for (int o = (int)P.ops.size() - 1; o >= 0; --o) {
     const Op& O = P.ops[o];
-    if (O.kind == OP_XENT || !has[O.out]) continue;
+    if (O.kind == OP_XENT || !have(O.out)) continue;
     const bool need0 = !(O.in0 == 0 && k == 0);  // the first stage needs no input gradient
     const bool need1 = O.in1 >= 0 && !(O.in1 == 0 && k == 0);
     XP_TRY(op_backward(c, s, o, gp[O.out], need0 ? gp[O.in0] : nullptr, need0 && has[O.in0],

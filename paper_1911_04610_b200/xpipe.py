@@ -120,6 +120,7 @@ def lib():
         L.xpipe_refresh_predictions.argtypes = [vp]
         L.xpipe_gemm_bf16.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i64, vp]
         L.xpipe_conv2d_bf16.argtypes = [i32, C.POINTER(i32), vp, vp, vp, i32, vp, i64, vp]
+        L.xpipe_linear_bf16.argtypes = [i32, vp, vp, vp, vp, i32, vp, i32, i32, i32, i32, i32, i32, vp, i64, vp]
         L.xpipe_schedule_program.argtypes = [i32, i32, i32, i32, i64, vp, vp]
         _lib = L
     return _lib
@@ -379,6 +380,21 @@ def conv2d_bf16(mode, geo, in0, in1, out, accumulate=False, ws=None, stream=None
     g = (C.c_int32 * 13)(*geo)
     _check(lib().xpipe_conv2d_bf16(mode, g, _ptr(in0), _ptr(in1), _ptr(out), int(accumulate),
                                    _ptr(ws) if ws is not None else None, ws.numel() if ws is not None else 0,
+                                   C.c_void_p(stream) if stream else None))
+
+
+def linear_bf16(mode, out, n, in_f, out_f, x=None, W=None, b=None, dy=None, ldp=0, relu=False, f32out=False,
+                accumulate=False, ws=None, stream=None):
+    """mode 1 forward (x, W, b -> out [n][out_f]) / 2 dgrad (dy [n][ldp], W -> out [n][in_f]) /
+    3 wgrad (x, dy -> out [out_f][in_f] fp32); see xpipe_linear_bf16 in include/xpipe.h."""
+    for nm, t in (("x", x), ("W", W), ("b", b), ("dy", dy)):
+        if t is not None:
+            _want(nm, t, ("bfloat16",))
+    _want("out", out, ("float32",) if (mode == 3 or (mode == 1 and f32out)) else ("bfloat16",))
+    _want("ws", ws, ("float32",))
+    p = lambda t: _ptr(t) if t is not None else None
+    _check(lib().xpipe_linear_bf16(mode, p(x), p(W), p(b), p(dy), ldp, _ptr(out), n, in_f, out_f, int(relu),
+                                   int(f32out), int(accumulate), p(ws), ws.numel() if ws is not None else 0,
                                    C.c_void_p(stream) if stream else None))
 
 

@@ -108,3 +108,62 @@ def test_conv_fprop_dgrad_wgrad(cfg):
         absw = torch.nn.grad.conv2d_weight(Xr.abs(), Wr.shape, dYr.abs(), (sh, sw), (ph, pw)) + 1.0
         ok, worst = rel_ok(dW.permute(0, 3, 1, 2).cpu(), refw, absw)
         assert ok, ("wgrad", worst)
+
+
+LINEARS = [
+    # (n, in, out): VGG-16 head, ResNet-101 / Inception-V3 heads (2048 -> 200, split-K), the MLP
+    # hidden layers in bf16 mode, ragged feature counts, a micro-batch wider than one N tile
+    (32, 512, 10), (32, 2048, 200), (8, 784, 256), (50, 64, 33), (100, 136, 130),
+]
+
+
+@pytest.mark.parametrize("n,inf,outf", LINEARS)
+def test_linear_tensor_core(n, inf, outf):
+    """xpipe_linear_bf16 (swap-AB tcgen05 GEMMs of the bf16 Linear layers) against fp64 torch on
+    the same bf16 operands: forward with bias (fp32 logits; bf16 with and without ReLU: every
+    output within one bf16 rounding of the fp64 value evaluated in fp32), dgrad (bf16), wgrad
+    stored then accumulated (fp32)."""
+    from paper_1911_04610_b200 import linear_bf16
+    g = torch.Generator().manual_seed(n * 31 + outf)
+    x = bf(torch.randn(n, inf, generator=g))
+    W = bf(torch.randn(outf, inf, generator=g) / inf ** 0.5)
+    b = bf(torch.randn(outf, generator=g))
+    ldp = (outf + 7) // 8 * 8
+    dy = torch.zeros(n, ldp, dtype=torch.bfloat16)
+    dy[:, :outf] = bf(torch.randn(n, outf, generator=g))
+    xd, Wd, bd, dyd = (t.to(DEV) for t in (x, W, b, dy))
+    ws = torch.zeros(1 << 22, device=DEV)
+    ref = x.double() @ W.double().t() + b.double()
+    mag = x.double().abs() @ W.double().abs().t() + b.double().abs()
+    # fp32 logits
+    y = torch.full((n, outf), float("nan"), device=DEV)
+    linear_bf16(1, y, n, inf, outf, x=xd, W=Wd, b=bd, f32out=True, ws=ws)
+    torch.cuda.synchronize()
+    assert ((y.cpu().double() - ref).abs() <= mag * 2.0 ** -16 + 1e-30).all()
+    # bf16 out, with / without ReLU: within one bf16 ulp of the exact value
+    for relu in (False, True):
+        yb = torch.full((n, outf), float("nan"), device=DEV, dtype=torch.bfloat16)
+        linear_bf16(1, yb, n, inf, outf, x=xd, W=Wd, b=bd, relu=relu, ws=ws)
+        torch.cuda.synchronize()
+        r = ref.clamp(min=0) if relu else ref
+        err = (yb.cpu().double() - r).abs()
+        assert (err <= r.abs() * 2.0 ** -8 + mag * 2.0 ** -16 + 1e-30).all()
+        if relu:
+            assert (yb.cpu() >= 0).all()
+    # dgrad
+    dx = torch.full((n, inf), float("nan"), device=DEV, dtype=torch.bfloat16)
+    linear_bf16(2, dx, n, inf, outf, W=Wd, dy=dyd, ldp=ldp, ws=ws)
+    torch.cuda.synchronize()
+    rdx = dy[:, :outf].double() @ W.double()
+    mdx = dy[:, :outf].double().abs() @ W.double().abs()
+    assert ((dx.cpu().double() - rdx).abs() <= rdx.abs() * 2.0 ** -8 + mdx * 2.0 ** -16 + 1e-30).all()
+    # wgrad: store, then accumulate
+    gW = torch.full((outf, inf), float("nan"), device=DEV)
+    linear_bf16(3, gW, n, inf, outf, x=xd, dy=dyd, ldp=ldp, ws=ws)
+    torch.cuda.synchronize()
+    rgw = dy[:, :outf].double().t() @ x.double()
+    mgw = dy[:, :outf].double().abs().t() @ x.double().abs()
+    assert ((gW.cpu().double() - rgw).abs() <= mgw * 2.0 ** -16 + 1e-30).all()
+    linear_bf16(3, gW, n, inf, outf, x=xd, dy=dyd, ldp=ldp, accumulate=True, ws=ws)
+    torch.cuda.synchronize()
+    assert ((gW.cpu().double() - 2 * rgw).abs() <= 2 * mgw * 2.0 ** -16 + 1e-30).all()

@@ -81,8 +81,18 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
         XP_TRY(check_launch(c, tc_im2col_fprop(g, cols, W + L.woff, mid, s.ws, s.ws_elems, s.ctr, s.stream, s.bnws,
                                                &bn_tiles), "conv_fprop"));
       } else {
+        // unpooled blocks whose M tiles fit one thread-block cluster: the BN statistics and the
+        // BN-apply [+ residual] [+ ReLU] run in the GEMM's epilogue (GemmArgs::bnf)
+        const LayerInfo& NB = c->net.layers[O.lbn];
+        BnFuse f{W + NB.woff, W + NB.boff, NB.d.bn_eps, s.stats[o][slot], (bf16*)y, s.plan.tensors[O.out].pitch(),
+                 O.in1 >= 0 ? (const bf16*)s.act[O.in1][slot] : nullptr, O.relu};
+        bool fused = false;
         XP_TRY(check_launch(c, tc_conv_fprop(g, x, W + L.woff, mid, s.ws, s.ws_elems, s.ctr, s.stream, s.bnws,
-                                             &bn_tiles), "conv_fprop"));
+                                             &bn_tiles, O.lpool < 0 ? &f : nullptr, &fused), "conv_fprop"));
+        if (fused) {
+          // algorithmic work: the GEMM's flops (the BN pass re-reads nothing from memory)
+          return prof_end(c, s, XP_PROF_CONV_FPROP, conv_flops(g, L.in0.c));
+        }
       }
       XP_TRY(prof_end(c, s, XP_PROF_CONV_FPROP, conv_flops(g, L.in0.c)));
       const LayerInfo& N = c->net.layers[O.lbn];

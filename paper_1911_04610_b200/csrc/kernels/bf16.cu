@@ -68,13 +68,15 @@ __global__ void stage_input_bf16_kernel(const float* __restrict__ x, bf16* __res
   }
 }
 
+// Chan's pairwise merge with explicit roundings (no contraction), so the GEMM epilogue's fused
+// BatchNorm (kernels/gemm_tc.cu chan_merge_rn) reproduces it bit for bit
 __device__ __forceinline__ void chan_merge(float& na, float& mean, float& m2, float nb, float mb, float m2b) {
   if (nb == 0.f) return;
   if (na == 0.f) { na = nb; mean = mb; m2 = m2b; return; }
-  const float nab = na + nb;
-  const float d = mb - mean;
-  mean += d * (nb / nab);
-  m2 += m2b + d * d * (na * nb / nab);
+  const float nab = __fadd_rn(na, nb);
+  const float d = __fsub_rn(mb, mean);
+  mean = __fadd_rn(mean, __fmul_rn(d, __fdiv_rn(nb, nab)));
+  m2 = __fadd_rn(m2, __fadd_rn(m2b, __fmul_rn(__fmul_rn(d, d), __fdiv_rn(__fmul_rn(na, nb), nab))));
   na = nab;
 }
 
@@ -205,7 +207,7 @@ __device__ __forceinline__ void stats_final_body(const float* __restrict__ part,
   __syncthreads();
   if (j == 0 && c < C) {
     stats[c] = sh[0][cc][1];
-    stats[C + c] = 1.f / sqrtf(sh[0][cc][2] / sh[0][cc][0] + eps);
+    stats[C + c] = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(sh[0][cc][2], sh[0][cc][0]), eps)));
     stats[2 * C + c] = __bfloat162float(gamma[c]);
     stats[3 * C + c] = __bfloat162float(beta[c]);
   }

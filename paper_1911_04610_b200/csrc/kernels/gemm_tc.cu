@@ -507,6 +507,95 @@ __device__ __forceinline__ void epi_store8(const GemmArgs& a, int row, int col0,
   }
 }
 
+// BatchNorm merge of Chan's pairwise formula, explicit roundings (bn_stats_final_kernel's)
+__device__ __forceinline__ void chan_merge_rn(float& na, float& mean, float& m2, float nb, float mb, float m2b) {
+  if (nb == 0.f) return;
+  if (na == 0.f) { na = nb; mean = mb; m2 = m2b; return; }
+  const float nab = __fadd_rn(na, nb);
+  const float d = __fsub_rn(mb, mean);
+  mean = __fadd_rn(mean, __fmul_rn(d, __fdiv_rn(nb, nab)));
+  m2 = __fadd_rn(m2, __fadd_rn(m2b, __fmul_rn(__fmul_rn(d, d), __fdiv_rn(__fmul_rn(na, nb), nab))));
+  na = nab;
+}
+
+// GemmArgs::bnf, run by the 4 epilogue warps (et = 0..127) after the cluster barrier: the
+// statistics of the tile's columns from the mt tile partials of the cluster (DSMEM), merged
+// in bn_stats_final_kernel's order (chunk j on lane j, then a pairwise tree of strides 16..1;
+// mt <= 16, so the stride-16 level is empty), then BN [+ residual] [+ ReLU] of the TMEM
+// accumulator (buffer 0: one tile per CTA) with the bf16-rounded stored conv output as x
+template <int BN>
+__device__ __forceinline__ void bnf_apply(const GemmArgs& a, uint32_t base_u, float* bnx, uint32_t tmem, int mt, int et,
+                                          int q, int lane) {
+  float* fin = bnx + 2 * BN;  // [4][BN]: mean, rstd, gamma, beta
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  for (int c = et; c < BN; c += 128) {
+    const int col = n0 + c;
+    if (col >= a.N) break;
+    float n[16], me[16], m2[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      n[i] = 0.f; me[i] = 0.f; m2[i] = 0.f;
+      if (i < mt) {
+        float t;
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(t) : "r"(mapa(base_u + (uint32_t)(c * 4), (uint32_t)i)) : "memory");
+        me[i] = t;
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(t) : "r"(mapa(base_u + (uint32_t)((BN + c) * 4), (uint32_t)i)) : "memory");
+        m2[i] = t;
+        n[i] = (float)min(BM, a.M - i * BM);
+      }
+    }
+#pragma unroll
+    for (int stride = 8; stride > 0; stride >>= 1)
+#pragma unroll
+      for (int j = 0; j < stride; ++j) chan_merge_rn(n[j], me[j], m2[j], n[j + stride], me[j + stride], m2[j + stride]);
+    const float rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(m2[0], n[0]), a.bn_eps)));
+    const float ga = __bfloat162float(a.gamma[col]), be = __bfloat162float(a.beta[col]);
+    fin[c] = me[0]; fin[BN + c] = rstd; fin[2 * BN + c] = ga; fin[3 * BN + c] = be;
+    if (blockIdx.x == 0) {
+      a.stats[col] = me[0]; a.stats[a.N + col] = rstd; a.stats[2 * a.N + col] = ga; a.stats[3 * a.N + col] = be;
+    }
+  }
+  epi_bar();
+  const int row = m0 + q * 32 + lane;
+  tc_fence_after();
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    if (n0 + c0 >= a.N) break;
+    uint32_t v[32];
+    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+    if (row >= a.M) continue;
+#pragma unroll
+    for (int e0 = 0; e0 < 32; e0 += 8) {
+      const int col = n0 + c0 + e0;
+      if (col >= a.N) break;
+      float r8[8];
+      if (a.res) {
+        const uint4 u = *reinterpret_cast<const uint4*>(a.res + (int64_t)row * a.N + col);
+        const bf16* rb = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r8[e] = __bfloat162float(rb[e]);
+      }
+      uint32_t w4[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        float o2[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int e = 2 * h + t, cc = c0 + e0 + e;
+          const float x = bf16r(v[e0 + e]);
+          const float tt = __fmul_rn(__fsub_rn(x, fin[cc]), fin[BN + cc]);
+          float y = __fadd_rn(__fmul_rn(fin[2 * BN + cc], tt), fin[3 * BN + cc]);
+          if (a.res) y = __bfloat162float(__float2bfloat16_rn(__fadd_rn(__bfloat162float(__float2bfloat16_rn(y)), r8[e])));
+          o2[t] = (a.relu && !(y > 0.f)) ? 0.f : y;
+        }
+        __nv_bfloat162 t2 = __floats2bfloat162_rn(o2[0], o2[1]);
+        w4[h] = *reinterpret_cast<uint32_t*>(&t2);
+      }
+      *reinterpret_cast<uint4*>(a.y + (int64_t)row * a.ldy + col) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+  }
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -527,14 +616,14 @@ struct Ring {
 // (tile blockIdx.xy, k range blockIdx.z); otherwise persistent: tiles blockIdx.x, +gridDim.x, ...
 struct Work { int m0, n0, kb0, nkb; };
 __device__ __forceinline__ int local_units(const GemmArgs& a, int ntiles) {
-  if (a.splits > 1) return 1;
+  if (a.splits > 1 || a.bnf) return 1;
   return (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 }
 template <int BN>
 __device__ __forceinline__ Work work_of(const GemmArgs& a, int j, int mt) {
   Work w;
   const int nkb_total = (a.K + BK - 1) / BK;
-  if (a.splits > 1) {
+  if (a.splits > 1 || a.bnf) {
     w.m0 = blockIdx.x * BM; w.n0 = blockIdx.y * BN;
     w.kb0 = blockIdx.z * a.kb_per_split;
     w.nkb = max(0, min(nkb_total, w.kb0 + a.kb_per_split) - w.kb0);
@@ -815,7 +904,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
             for (int e = 0; e < 32; ++e) v[e] = 0u;
           }
           if (w.n0 + c0 < a.N) epi_store(a, row, w.n0 + c0, v);
-          if ((MODE == GEMM_FPROP || MODE == GEMM_PLAIN) && a.bn_part && w.n0 + c0 < a.N) {
+          if ((MODE == GEMM_FPROP || MODE == GEMM_PLAIN) && (a.bn_part || a.bnf) && w.n0 + c0 < a.N) {
             // BatchNorm partials of this tile's 32 columns over its valid rows, from the stored
             // (bf16-rounded) values: tile mean, then the sum of squared deviations (two passes;
             // the second re-reads the accumulator from TMEM), fixed-order reductions
@@ -842,10 +931,17 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
             epi_bar();
             const int col = w.n0 + c0 + lane;
             if (q == 0 && col < a.N) {
-              float* bp = a.bn_part + (int64_t)(w.m0 / BM) * 2 * a.N;
-              bp[col] = mean;
-              bp[a.N + col] = __fadd_rn(__fadd_rn(__fadd_rn(epi_red[lane], epi_red[32 + lane]), epi_red[64 + lane]),
-                                        epi_red[96 + lane]);
+              const float m2 = __fadd_rn(__fadd_rn(__fadd_rn(epi_red[lane], epi_red[32 + lane]), epi_red[64 + lane]),
+                                         epi_red[96 + lane]);
+              if (a.bnf) {  // this tile's partials stay in the (drained) ring for the cluster merge
+                float* bnx = reinterpret_cast<float*>(smem_raw + (base - raw));
+                bnx[c0 + lane] = mean;
+                bnx[BN + c0 + lane] = m2;
+              } else {
+                float* bp = a.bn_part + (int64_t)(w.m0 / BM) * 2 * a.N;
+                bp[col] = mean;
+                bp[a.N + col] = m2;
+              }
             }
             epi_bar();  // epi_red free for the next chunk
           }
@@ -854,6 +950,11 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
         __syncwarp();
         if (lane == 0) mbar_arrive(acce0 + 8 * buf);
       }
+    }
+    if (MODE == GEMM_FPROP && a.bnf) {
+      cluster_sync();  // every tile's partials are in its CTA's smem
+      if (warp >= 5) bnf_apply<BN>(a, base, reinterpret_cast<float*>(smem_raw + (base - raw)), tmem, mt, tid - 160, q, lane);
+      cluster_sync();  // no CTA frees its smem while the others still read its partials
     }
   } else {
     // cluster split-K (one unit per CTA): park the partial tile in this CTA's smem (the ring is
@@ -1214,6 +1315,28 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   if (splits <= 1) grid = dim3(std::max(1, std::min(mt * nt, pmult * num_sms())), 1, 1);
   else grid = dim3(mt, nt, splits);
   const int SMEM = args.stages * STAGE + 1024 + 1024;  // ring + alignment + barriers/BN exchange
+  if (args.bnf) {  // one cluster of mt CTAs per N tile (the caller checked mt <= 16 and residency)
+    static bool np_attr = false;
+    if (!np_attr) {
+      cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      np_attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = mt; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cfg.gridDim = dim3(mt, nt, 1);
+    args.splits = 1; args.cs = 1; args.nc = 1;
+    args.kb_per_split = std::max(1, (a.K + BK - 1) / BK);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<MODE, BN, A_MN, B_MN>, args, tmA, tmB);
+  }
   if (splits <= 1) {
     launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);
     return cudaGetLastError();
@@ -1341,12 +1464,53 @@ cudaError_t tc_gemm_plain(const bf16* A, const bf16* B, float* D, int M, int N, 
   return launch_bn<GEMM_PLAIN, true, true>(a, bn, 1, st);
 }
 
+// can the M tiles of an N tile run as one cluster of mt CTAs (bnf)?  cached per (mt, BN)
+template <int BN>
+bool bnf_resident(int mt, const GemmArgs& a) {
+  static std::map<int, bool> cache;
+  auto it = cache.find(mt);
+  if (it != cache.end()) return it->second;
+  constexpr int STAGE = BM * BK * 2 + BN * BK * 2;
+  const int SMEM = std::max(4, persist_stages()) * STAGE + 2048;
+  auto kern = tc_gemm_kernel<GEMM_FPROP, BN, false, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(8, (kMaxSmem - 2048) / STAGE) * STAGE + 2048);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = mt; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(mt, 1, 1);
+  int n = 0;
+  const bool ok = cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0;
+  cudaGetLastError();
+  (void)a;
+  return cache[mt] = ok;
+}
+
+__host__ bool no_bnf() { static const bool v = getenv_flag("XPIPE_NO_BN_FUSE"); return v; }
+
 cudaError_t tc_conv_fprop(const ConvGeo& g, const bf16* X, const bf16* Wt, bf16* Y, float* ws, int64_t ws_elems,
-                          int* counters, cudaStream_t st, float* bn_part, int* bn_tiles) {
+                          int* counters, cudaStream_t st, float* bn_part, int* bn_tiles, const BnFuse* bnf,
+                          bool* bnf_done) {
   GemmArgs a{};
   a.g = g; a.A = X; a.B = Wt;
   a.M = g.Nimg * g.P * g.Q; a.N = g.Co; a.K = g.R * g.S * g.C;
   const SplitPlan sp = plan_splits(a.M, a.N, a.K);
+  const int mt = (a.M + BM - 1) / BM;
+  if (bnf_done) *bnf_done = false;
+  if (bnf && !no_bnf() && sp.cs * sp.nc <= 1 && mt <= 16 && g.Co % 8 == 0 && bnf->ldy % 8 == 0 &&
+      (sp.bn == 64 ? bnf_resident<64>(mt, a) : sp.bn == 128 ? bnf_resident<128>(mt, a) : bnf_resident<256>(mt, a))) {
+    a.bnf = 1;
+    a.gamma = bnf->gamma; a.beta = bnf->beta; a.bn_eps = bnf->eps; a.stats = bnf->stats;
+    a.y = bnf->y; a.ldy = bnf->ldy; a.res = bnf->res; a.relu = bnf->relu ? 1 : 0;
+    if (bn_tiles) *bn_tiles = 0;
+    if (bnf_done) *bnf_done = true;
+    return run_split<GEMM_FPROP, false, false>(a, EPI_BF16, Y, g.Co, 0, ws, ws_elems, counters, st);
+  }
   const bool fused_bn = bn_part && sp.cs * sp.nc <= 1;
   a.bn_part = fused_bn ? bn_part : nullptr;
   if (bn_tiles) *bn_tiles = fused_bn ? (a.M + BM - 1) / BM : 0;

@@ -59,7 +59,35 @@ struct GemmArgs {
   unsigned long long* dbg;  // development timing probe (XPIPE_GEMM_DBG), else null
   int dev_flags;            // development experiments (XPIPE_GEMM_DEV), 0 in production
   const __nv_bfloat16* bias;  // EPI_LINEAR_T: per-row bias (or null)
-  int relu, f32out;           // EPI_LINEAR_T: ReLU on the bf16 output / fp32 output (logits)
+  int relu, f32out;           // EPI_LINEAR_T: ReLU on the bf16 output / fp32 output (logits);
+                              // bnf: ReLU after the BatchNorm (and residual)
+  // bnf (FPROP, no split-K): the CTAs of one N tile form a cluster along M (grid (mt, nt),
+  // cluster (mt, 1, 1), one tile each); after the tile partials of the BatchNorm statistics
+  // (as bn_part) are exchanged over DSMEM, every CTA merges them (the fixed tree of
+  // bn_stats_final_kernel) and applies BN [+ residual] [+ ReLU] to its accumulator tile:
+  // y[row][col] (row pitch ldy) = Q(relu?(gamma (x - mean) rstd + beta)) of x = Q(acc), or with
+  // res: relu?(Q(Q(gamma (x - mean) rstd + beta) + res[row][col])); CTA rank 0 stores the
+  // statistics [4][N] (mean, rstd, gamma, beta) for the backward
+  int bnf;
+  const __nv_bfloat16* gamma;
+  const __nv_bfloat16* beta;
+  float bn_eps;
+  float* stats;
+  __nv_bfloat16* y;
+  int64_t ldy;
+  const __nv_bfloat16* res;
+};
+
+// the fused BatchNorm of a conv's forward (see GemmArgs::bnf); res may be null
+struct BnFuse {
+  const __nv_bfloat16* gamma;
+  const __nv_bfloat16* beta;
+  float eps;
+  float* stats;
+  __nv_bfloat16* y;
+  int ldy;
+  const __nv_bfloat16* res;
+  bool relu;
 };
 
 // plain GEMM for unit parity: D[M][N] fp32 (ldd) = A(m,k) B(n,k)
@@ -72,9 +100,11 @@ cudaError_t tc_gemm_plain(const __nv_bfloat16* A, const __nv_bfloat16* B, float*
 // bn_part (optional): if the launch runs without split-K, the per-128-row-tile BatchNorm
 // partials of Y go there ([ceil(M/128)][2][Co], see GemmArgs::bn_part) and *bn_tiles is set to
 // ceil(M/128); otherwise *bn_tiles = 0 and the caller computes the statistics itself
+// bnf (optional): fuse the BatchNorm statistics and apply into the GEMM when the launch runs
+// without split-K and the M tiles fit one thread-block cluster; *bnf_done tells the caller
 cudaError_t tc_conv_fprop(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* Wt, __nv_bfloat16* Y,
                           float* ws, int64_t ws_elems, int* counters, cudaStream_t st, float* bn_part = nullptr,
-                          int* bn_tiles = nullptr);
+                          int* bn_tiles = nullptr, const BnFuse* bnf = nullptr, bool* bnf_done = nullptr);
 // dX [Nimg*H*W][Cx] bf16 (Cx = real input channels, multiple of 8) from dY [Nimg*P*Q][Co]
 cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const __nv_bfloat16* dY, const __nv_bfloat16* Wt,
                           __nv_bfloat16* dX, float* ws, int64_t ws_elems, int* counters, cudaStream_t st,

@@ -675,6 +675,22 @@ int sync_all(xpipe_ctx* c) {
   return XP_OK;
 }
 
+// ---- streams --------------------------------------------------------------------------------
+// role 0 = a stage's main (backward / update) stream, 1 = its forward stream (fb_overlap), 2 = its
+// weight-gradient side stream.  Development knob XPIPE_STREAM_PRIO (default 0: all equal):
+// 1 = main streams high, side streams low; 2 = main high, forward and side low;
+// 3 = later stages higher (the pipeline drains from the last stage)
+cudaError_t make_stream(cudaStream_t* st, int role, int k, int K) {
+  static const int mode = [] { const char* e = getenv("XPIPE_STREAM_PRIO"); return (e && *e) ? atoi(e) : 0; }();
+  int lo = 0, hi = 0;  // numerically: greatest (lowest priority), least (highest priority)
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  int prio = lo;
+  if (mode == 1) prio = role == 0 ? hi : (role == 2 ? lo : (lo + hi) / 2);
+  else if (mode == 2) prio = role == 0 ? hi : lo;
+  else if (mode == 3) prio = lo + (int)((long)(hi - lo) * k / std::max(1, K - 1));
+  return cudaStreamCreateWithPriority(st, cudaStreamNonBlocking, prio);
+}
+
 // ---- CUDA graphs of steady-state steps -------------------------------------------------------
 // In steady state (no flush, every in-flight wait already past the warm-up) a call's enqueue is
 // a pure function of: M, the call buffers, and per stage (pos - 2*(fed - base)), (fed - base)
@@ -1036,14 +1052,13 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
       s.stream = c->S[0].stream;
       s.side = c->S[0].stream;
     } else {
-      if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
+      if (make_stream(&s.stream, 0, k, c->K) != cudaSuccess) return fail_init(XP_ECUDA, "stream");
       if (c->cfg.serialize && !c->mp()) s.side = s.stream;
-      else if (cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking) != cudaSuccess)
+      else if (make_stream(&s.side, 2, k, c->K) != cudaSuccess)
         return fail_init(XP_ECUDA, "stream");
     }
     s.fstream = s.stream;
-    if (c->cfg.fb_overlap && !c->cfg.serialize &&
-        cudaStreamCreateWithFlags(&s.fstream, cudaStreamNonBlocking) != cudaSuccess)
+    if (c->cfg.fb_overlap && !c->cfg.serialize && make_stream(&s.fstream, 1, k, c->K) != cudaSuccess)
       return fail_init(XP_ECUDA, "stream");
     s.ev_fdone.assign(s.S, nullptr); s.ev_bdone.assign(s.S, nullptr);
     s.fdone_epoch.assign(s.S, -1); s.bdone_epoch.assign(s.S, -1);

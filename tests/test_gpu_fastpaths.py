@@ -8,7 +8,11 @@ subprocesses on the same seeded inputs:
   * XPIPE_NO_CONCAT_VIEWS=1 -- Inception's channel concats eliminated (conv blocks and pooling
     ops store in place at their channel offset, their backward reads the gradient slice) vs
     the copy ops: the full Inception-V3 at 64x64 (four-way chains, the nested 1x3 / 3x1 concats
-    of Mixed_7, max-pool branches of the reductions), K=3."""
+    of Mixed_7, max-pool branches of the reductions), K=3;
+  * XPIPE_NO_BN_FUSE=1 -- the BatchNorm statistics and BN-apply [+ residual] [+ ReLU] in the
+    fprop GEMM's epilogue (the M tiles of an N tile as one thread-block cluster, partials over
+    DSMEM) vs the separate statistics-merge and apply launches: VGG-16 at CIFAR size K=2 (its
+    unpooled 8x8 / 4x4 layers), the ResNet blocks (residual blocks at 4x4 / 2x2) and Inception."""
 import os
 import subprocess
 import sys
@@ -27,7 +31,9 @@ import synthetic as S
 from synthetic.models import resnet101, inception_v3, assign_stages
 from paper_1911_04610_b200 import XPipe
 which = {which!r}
-if which == "resnet":
+if which == "vgg16":
+    L, shape, K, T, N, calls, kind = S.vgg16_cifar(), (3, 32, 32), 2, 2, 64, (3, 3, 3), "cifar"
+elif which == "resnet":
     L, units = resnet101(classes=10, layers=(2, 2, 2, 1))
     L, shape, K, T, N, calls, kind = assign_stages(L, units, 3), (3, 32, 32), 3, 2, 16, (3, 3, 3), "imagenet"
 else:
@@ -58,7 +64,9 @@ def run(which, switch, on, out):
     return np.load(out)
 
 
-@pytest.mark.parametrize("switch,which", [("XPIPE_NO_ADD_FUSE", "resnet"), ("XPIPE_NO_CONCAT_VIEWS", "inception")])
+@pytest.mark.parametrize("switch,which", [("XPIPE_NO_ADD_FUSE", "resnet"), ("XPIPE_NO_CONCAT_VIEWS", "inception"),
+                                          ("XPIPE_NO_BN_FUSE", "vgg16"), ("XPIPE_NO_BN_FUSE", "resnet"),
+                                          ("XPIPE_NO_BN_FUSE", "inception")])
 def test_fast_path_bit_identical(tmp_path, switch, which):
     fast = run(which, switch, False, str(tmp_path / "fast.npy"))
     general = run(which, switch, True, str(tmp_path / "general.npy"))

@@ -17,6 +17,10 @@ one GPU maps the 4 stages onto one device).
 import argparse
 import json
 import os
+
+# the library's default (paper_1911_04610_b200/xpipe.py): 32 hardware work queues, set before
+# torch creates the CUDA context
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import subprocess
 import sys

@@ -1491,7 +1491,11 @@ bool bnf_resident(int mt, const GemmArgs& a) {
   return cache[mt] = ok;
 }
 
-__host__ bool no_bnf() { static const bool v = getenv_flag("XPIPE_NO_BN_FUSE"); return v; }
+// opt-in (XPIPE_BN_FUSE=1): bit-identical to the separate statistics / apply launches and 9 % fewer
+// launches for VGG-16, but measured slower in the pipeline on one GPU (VGG-16 K=4 116.8k vs
+// 119.0k samples/s; K=1 worse still): a cluster of up to 16 CTAs must be co-scheduled on one
+// GPC while the other stages' kernels hold its SMs, and the merge runs in every CTA
+__host__ bool no_bnf() { static const bool v = !getenv_flag("XPIPE_BN_FUSE"); return v; }
 
 cudaError_t tc_conv_fprop(const ConvGeo& g, const bf16* X, const bf16* Wt, bf16* Y, float* ws, int64_t ws_elems,
                           int* counters, cudaStream_t st, float* bn_part, int* bn_tiles, const BnFuse* bnf,

@@ -18,6 +18,8 @@ T=600 TL=2 run ncu_launches ncu --metrics gpu__time_duration.sum --clock-control
     --log-file $out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-sweep
 T=600 TL=2 run ncu_wgrad ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:tc_gemm_kernel<\(int\)3" -s 300 -c 13 \
     -o $out/prof_wgrad python bench.py --steps 1 --warmup 3 --stages 1 --no-cpu-baseline --no-e2e --no-sweep --no-graphs
+T=600 TL=2 run ncu_fprop ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:tc_gemm_kernel<\(int\)1" -s 300 -c 13 \
+    -o $out/prof_fprop python bench.py --steps 1 --warmup 3 --stages 1 --no-cpu-baseline --no-e2e --no-sweep --no-graphs
 T=300 TL=2 run ncu_sweep ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 2 -c 1 \
     -o $out/prof_sweep python bench.py --workload sweep --steps 1 --warmup 3
 echo done >> $out/summary.txt

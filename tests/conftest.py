@@ -3,6 +3,9 @@ import sys
 
 import pytest
 
+# before any CUDA context exists (see paper_1911_04610_b200/xpipe.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -9,7 +9,7 @@ subprocesses on the same seeded inputs:
     ops store in place at their channel offset, their backward reads the gradient slice) vs
     the copy ops: the full Inception-V3 at 64x64 (four-way chains, the nested 1x3 / 3x1 concats
     of Mixed_7, max-pool branches of the reductions), K=3;
-  * XPIPE_NO_BN_FUSE=1 -- the BatchNorm statistics and BN-apply [+ residual] [+ ReLU] in the
+  * XPIPE_BN_FUSE=1 (opt-in) -- the BatchNorm statistics and BN-apply [+ residual] [+ ReLU] in the
     fprop GEMM's epilogue (the M tiles of an N tile as one thread-block cluster, partials over
     DSMEM) vs the separate statistics-merge and apply launches: VGG-16 at CIFAR size K=2 (its
     unpooled 8x8 / 4x4 layers), the ResNet blocks (residual blocks at 4x4 / 2x2) and Inception."""
@@ -54,9 +54,12 @@ g.close()
 
 
 def run(which, switch, on, out):
+    """on=True selects the general path: the NO_ switches disable a fast path, BN_FUSE enables one."""
     env = dict(os.environ)
     env.pop(switch, None)
-    if on:
+    if switch.startswith("XPIPE_NO_") and on:
+        env[switch] = "1"
+    if not switch.startswith("XPIPE_NO_") and not on:
         env[switch] = "1"
     code = RUN.format(root=ROOT, here=HERE, which=which, out=out)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
@@ -65,8 +68,8 @@ def run(which, switch, on, out):
 
 
 @pytest.mark.parametrize("switch,which", [("XPIPE_NO_ADD_FUSE", "resnet"), ("XPIPE_NO_CONCAT_VIEWS", "inception"),
-                                          ("XPIPE_NO_BN_FUSE", "vgg16"), ("XPIPE_NO_BN_FUSE", "resnet"),
-                                          ("XPIPE_NO_BN_FUSE", "inception")])
+                                          ("XPIPE_BN_FUSE", "vgg16"), ("XPIPE_BN_FUSE", "resnet"),
+                                          ("XPIPE_BN_FUSE", "inception")])
 def test_fast_path_bit_identical(tmp_path, switch, which):
     fast = run(which, switch, False, str(tmp_path / "fast.npy"))
     general = run(which, switch, True, str(tmp_path / "general.npy"))

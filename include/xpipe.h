@@ -327,7 +327,10 @@ int xpipe_gemm_bf16(const void* A, const void* B, float* D, int32_t M, int32_t N
    adds into out).  ws: optional fp32 device workspace of ws_elems for split-K across
    several clusters (NULL = split-K within one thread-block cluster only); its last 16384
    elements hold the split-K arrival counters: they must be zero before the first call and
-   every call leaves them zero (so zero the workspace once).  Calls sharing one ws must be
+   every call leaves them zero (so zero the workspace once).  Dgrad of a geometry the TMA pixel
+   boxes cannot serve (stride > 1, Co % 64 != 0, tile rows that are not a box of the input grid)
+   builds its explicit operand in the upper half of ws when it fits there (else the implicit
+   cp.async gather runs); 1x1 convs run as dense GEMMs.  Calls sharing one ws must be
    stream-ordered.  Device pointers; asynchronous on stream.  Errors: XP_EINVAL (bad
    geometry: C or Co not a multiple of 8, P/Q inconsistent), XP_ECUDA (launch). */
 int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void* in0, const void* in1, void* out,

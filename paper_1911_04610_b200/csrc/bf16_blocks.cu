@@ -240,7 +240,7 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       if (dx0) {
         XP_TRY(prof_begin(c, s));
         XP_TRY(check_launch(c, tc_conv_dgrad(g, O.sin0.c, dmid, W + L.woff, (bf16*)dx0, s.ws, s.ws_elems, s.ctr,
-                                             s.stream, acc0), "conv_dgrad"));
+                                             s.stream, acc0, (bf16*)s.dcols, s.dcols_elems), "conv_dgrad"));
         XP_TRY(prof_end(c, s, XP_PROF_CONV_DGRAD, conv_flops(g, L.in0.c)));
       }
       return XP_OK;

@@ -93,7 +93,12 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
     for (auto& q : s.mid[o]) if (!(q = A((size_t)n * O.smid.size() * 2))) return set_err(c, XP_ENOMEM, "stash");
     for (auto& q : s.stats[o]) if (!(q = (float*)A((size_t)O.smid.c * 4 * 4))) return set_err(c, XP_ENOMEM, "stash");
     const LayerInfo& LC = c->net.layers[O.lmain];
-    if (LC.cin_pad < 64 && !no_im2col()) {  // too few channels for the TMA pixel boxes: im2col
+    const ConvGeo cg{n, O.sin0.h, O.sin0.w, LC.cin_pad, LC.d.out_c, LC.d.kh, LC.d.kw, O.smid.h, O.smid.w,
+                     LC.d.sh, LC.d.sw, LC.d.ph, LC.d.pw};
+    // explicit dgrad operand scratch (geometries the TMA pixel boxes cannot serve)
+    if (!(O.in0 == 0 && s.k == 0)) s.dcols_elems = std::max(s.dcols_elems, tc_dgrad_cols_elems(cg));
+    // too few channels, or a geometry the TMA pixel boxes cannot serve: explicit im2col
+    if ((LC.cin_pad < 64 || tc_conv_needs_cols(cg)) && !no_im2col()) {
       if (s.cols.size() < p.ops.size()) s.cols.assign(p.ops.size(), {});
       s.cols[o].resize(s.S);
       const size_t cb = (size_t)n * O.smid.h * O.smid.w * LC.d.kh * LC.d.kw * LC.cin_pad * 2;
@@ -114,6 +119,7 @@ int allocate_stage(xpipe_ctx* c, StageRT& s) {
     s.dz.resize(s.S);
     for (auto& q : s.dz) if (!(q = (float*)A((size_t)n * c->cfg.classes * 4))) return set_err(c, XP_ENOMEM, "dz");
   }
+  if (s.dcols_elems && !(s.dcols = A((size_t)s.dcols_elems * 2))) return set_err(c, XP_ENOMEM, "dgrad operand");
   s.gbuf_elems = (int64_t)n * p.max_act;
   s.gmid = A((size_t)s.gbuf_elems * 4);
   s.gmid1 = A((size_t)s.gbuf_elems * 4);

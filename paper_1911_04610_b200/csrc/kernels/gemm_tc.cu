@@ -380,10 +380,17 @@ __device__ __forceinline__ void linear_t_store8(const GemmArgs& a, int row, int 
 // ---------------------------------------------------------------------------------------
 // epilogue: row m of the tile, 32 accumulator columns starting at col0
 // ---------------------------------------------------------------------------------------
+// destination row of an EPI_BF16 store (GemmArgs::rm_*)
+__device__ __forceinline__ int64_t out_row(const GemmArgs& a, int row) {
+  if (!a.rm_Q) return row;
+  const int q = row % a.rm_Q, t = row / a.rm_Q, p = t % a.rm_P, n = t / a.rm_P;
+  return ((int64_t)n * a.rm_H + (int64_t)p * a.rm_sh) * a.rm_W + (int64_t)q * a.rm_sw;
+}
+
 __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, uint32_t (&v)[32]) {
   if (row >= a.M) return;
   if (a.epi == EPI_BF16) {
-    bf16* o = static_cast<bf16*>(a.out) + (int64_t)row * a.ldo + col0;
+    bf16* o = static_cast<bf16*>(a.out) + out_row(a, row) * a.ldo + col0;
     if (a.accumulate) {  // fan-out tensor: out = Q(old + Q(acc)) (the oracle's rounding points)
 #pragma unroll
       for (int e0 = 0; e0 < 32; e0 += 8) {
@@ -470,7 +477,7 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
 // 8 consecutive columns [col0, col0+8) of row `row` (split-K reduction output)
 __device__ __forceinline__ void epi_store8(const GemmArgs& a, int row, int col0, const float (&v)[8]) {
   if (a.epi == EPI_BF16) {
-    bf16* o = static_cast<bf16*>(a.out) + (int64_t)row * a.ldo + col0;
+    bf16* o = static_cast<bf16*>(a.out) + out_row(a, row) * a.ldo + col0;
     if (!a.accumulate && col0 + 8 <= a.N) {
       uint32_t w[4];
 #pragma unroll
@@ -703,8 +710,10 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
           tma_2d(sb, tmB, k0, w.n0, full);
         } else if (MODE == GEMM_DGRAD) {
           mbar_expect_tx(full, STAGE);
-          const int tap = k0 / a.g.Co, c0 = k0 - tap * a.g.Co, r = tap / a.g.S, ss = tap - r * a.g.S;
-          tma_4d(sa, tmA, c0, tq + a.g.pw - ss, tp + a.g.ph - r, tn, full);
+          const int kco = a.kco ? a.kco : a.g.Co;
+          const int tap = k0 / kco, c0 = k0 - tap * kco, r = tap / a.g.S, ss = tap - r * a.g.S;
+          if (a.a_tma == 4) tma_2d(sa, tmA, k0, w.m0, full);  // explicit operand rows
+          else tma_4d(sa, tmA, c0, tq + a.g.pw - ss, tp + a.g.ph - r, tn, full);
 #pragma unroll
           for (int q = 0; q < BN / 64; ++q) tma_3d(sb + q * (BK * 128), tmB, w.n0 + 64 * q, tap, c0, full);
         } else if (MODE == GEMM_WGRAD) {
@@ -1110,6 +1119,27 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
   }
 }
 
+// explicit transposed-conv operand of a dgrad: cols[m][tap * kco + co] = dY[n][p][q][co] with
+// (p, q) = ((h + ph - r) / sh, (w + pw - s) / sw) when both divide exactly and lie in the output
+// grid, else 0 (also for Co <= co < kco); m = (n * H + h) * W + w, 8 channels per thread
+__global__ void dgrad_cols_kernel(const bf16* __restrict__ dY, bf16* __restrict__ cols, ConvGeo g, int kco) {
+  pdl_wait();
+  const int G = kco / 8, RS = g.R * g.S;
+  const int total = g.Nimg * g.H * g.W * RS * G;  // < 2^31 (checked at launch)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int gi = i % G, t = i / G, tap = t % RS, m = t / RS;
+    const int w = m % g.W, hn = m / g.W, h = hn % g.H, n = hn / g.H;
+    const int r = tap / g.S, ss = tap - r * g.S, co = gi * 8;
+    const int hp = h + g.ph - r, wp = w + g.pw - ss;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (co < g.Co && hp >= 0 && wp >= 0 && hp % g.sh == 0 && wp % g.sw == 0) {
+      const int p = hp / g.sh, q = wp / g.sw;
+      if (p < g.P && q < g.Q) v = *reinterpret_cast<const uint4*>(dY + (((int64_t)n * g.P + p) * g.Q + q) * g.Co + co);
+    }
+    *reinterpret_cast<uint4*>(cols + (int64_t)t * kco + co) = v;
+  }
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -1185,7 +1215,7 @@ void setup_b_tma(GemmArgs& a, CUtensorMap* m) {
     const uint64_t dims[2] = {(uint64_t)a.g.Co, (uint64_t)a.K}, str[1] = {(uint64_t)a.g.Co * 2};
     const uint32_t box[2] = {64, 64};
     if (make_map(m, a.B, 2, dims, str, box)) a.b_tma = 2;
-  } else if (MODE == GEMM_DGRAD && a.g.Co % 64 == 0) {  // W [Co][R*S][C]: k-block = 64 co of one tap
+  } else if (MODE == GEMM_DGRAD && (a.g.Co % 64 == 0 || a.kco)) {  // W [Co][R*S][C]: k-block = 64 co of one tap
     const uint64_t dims[3] = {(uint64_t)a.g.C, (uint64_t)(a.g.R * a.g.S), (uint64_t)a.g.Co};
     const uint64_t str[2] = {(uint64_t)a.g.C * 2, (uint64_t)a.g.R * a.g.S * a.g.C * 2};
     const uint32_t box[3] = {64, 1, 64};
@@ -1279,8 +1309,15 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   args.a_tma = args.b_tma = 0;
   if (!no_tma()) {
     setup_b_tma<MODE, BN, B_MN>(args, &tmB);
-    if (!no_tma_a()) setup_a_tma<MODE, A_MN>(args, &tmA);
+    if (MODE == GEMM_DGRAD && args.kco) {  // explicit operand [M][K]: 2D K-major box {64, 128}
+      const uint64_t dims[2] = {(uint64_t)args.K, (uint64_t)args.M}, str[1] = {(uint64_t)args.K * 2};
+      const uint32_t box[2] = {64, (uint32_t)BM};
+      if (args.b_tma == 3 && make_map(&tmA, args.A, 2, dims, str, box)) args.a_tma = 4;
+    } else if (!no_tma_a()) {
+      setup_a_tma<MODE, A_MN>(args, &tmA);
+    }
   }
+  if (MODE == GEMM_DGRAD && args.kco && args.a_tma != 4) return cudaErrorInvalidValue;  // needs both maps
   // ring depth: the cp.async gather needs >= LAG+1 = 4 stages; an all-TMA ring may be shallower
   // so that wide tiles still leave room for a second CTA on the SM
   static const int st128 = getenv_int("XPIPE_PSTAGES_128", 4), st256 = getenv_int("XPIPE_PSTAGES_256", 4);
@@ -1464,6 +1501,10 @@ cudaError_t tc_gemm_plain(const bf16* A, const bf16* B, float* D, int M, int N, 
   return launch_bn<GEMM_PLAIN, true, true>(a, bn, 1, st);
 }
 
+// 1x1 convs run as dense GEMMs (XPIPE_NO_DENSE_CONV=1 keeps the implicit gathers, development)
+bool is_pointwise(const ConvGeo& g) { return g.R == 1 && g.S == 1 && g.ph == 0 && g.pw == 0; }
+__host__ bool no_dense() { static const bool v = getenv_flag("XPIPE_NO_DENSE_CONV"); return v; }
+
 // can the M tiles of an N tile run as one cluster of mt CTAs (bnf)?  cached per (mt, BN)
 template <int BN>
 bool bnf_resident(int mt, const GemmArgs& a) {
@@ -1503,9 +1544,11 @@ cudaError_t tc_conv_fprop(const ConvGeo& g, const bf16* X, const bf16* Wt, bf16*
   GemmArgs a{};
   a.g = g; a.A = X; a.B = Wt;
   a.M = g.Nimg * g.P * g.Q; a.N = g.Co; a.K = g.R * g.S * g.C;
+  if (bnf_done) *bnf_done = false;
+  if (is_pointwise(g) && g.sh == 1 && g.sw == 1 && !no_dense())  // 1x1: X is the GEMM's A operand
+    return tc_im2col_fprop(g, X, Wt, Y, ws, ws_elems, counters, st, bn_part, bn_tiles);
   const SplitPlan sp = plan_splits(a.M, a.N, a.K);
   const int mt = (a.M + BM - 1) / BM;
-  if (bnf_done) *bnf_done = false;
   if (bnf && !no_bnf() && sp.cs * sp.nc <= 1 && mt <= 16 && g.Co % 8 == 0 && bnf->ldy % 8 == 0 &&
       (sp.bn == 64 ? bnf_resident<64>(mt, a) : sp.bn == 128 ? bnf_resident<128>(mt, a) : bnf_resident<256>(mt, a))) {
     a.bnf = 1;
@@ -1521,10 +1564,57 @@ cudaError_t tc_conv_fprop(const ConvGeo& g, const bf16* X, const bf16* Wt, bf16*
   return run_split<GEMM_FPROP, false, false>(a, EPI_BF16, Y, g.Co, 0, ws, ws_elems, counters, st);
 }
 
+
+int64_t tc_dgrad_cols_elems(const ConvGeo& g) {
+  if (no_dense() || is_pointwise(g)) return 0;
+  uint32_t pb[3];
+  if (g.sh == 1 && g.sw == 1 && g.Co % 64 == 0 && pixel_box(BM, g.W, g.H, pb)) return 0;  // TMA pixel boxes
+  return (int64_t)g.Nimg * g.H * g.W * g.R * g.S * ((g.Co + 63) / 64 * 64);
+}
+
+bool tc_conv_needs_cols(const ConvGeo& g) {
+  if (no_dense()) return false;
+  if (is_pointwise(g) && g.sh == 1 && g.sw == 1) return false;  // dense already
+  uint32_t pb[3];
+  return g.C % 64 != 0 || g.sh != 1 || g.sw != 1 || !pixel_box(BM, g.Q, g.P, pb) || !pixel_box(BK, g.Q, g.P, pb);
+}
+
 cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const bf16* dY, const bf16* Wt, bf16* dX, float* ws,
-                          int64_t ws_elems, int* counters, cudaStream_t st, bool accumulate) {
+                          int64_t ws_elems, int* counters, cudaStream_t st, bool accumulate, bf16* dcols,
+                          int64_t dcols_elems) {
   GemmArgs a{};
-  a.g = g; a.A = dY; a.B = Wt;
+  a.g = g; a.B = Wt;
+  if (is_pointwise(g) && !no_dense()) {
+    // 1x1: dX[(n, h, w)][c] = sum_co dY[(n, p, q)][co] W[co][c] at h = p sh, w = q sw -- a dense
+    // GEMM (A = dY K-major, B = W MN-major); strided: rows scatter, the other input pixels get 0
+    a.A = dY;
+    a.M = g.Nimg * g.P * g.Q; a.N = Cx; a.K = g.Co;
+    a.lda = g.Co; a.ldb = g.C;
+    a.force_tma = 1;
+    if (g.sh != 1 || g.sw != 1 || g.P != g.H || g.Q != g.W) {
+      a.rm_P = g.P; a.rm_Q = g.Q; a.rm_H = g.H; a.rm_W = g.W; a.rm_sh = g.sh; a.rm_sw = g.sw;
+      if (!accumulate) {
+        const cudaError_t e = cudaMemsetAsync(dX, 0, (size_t)g.Nimg * g.H * g.W * Cx * 2, st);
+        if (e != cudaSuccess) return e;
+      }
+    }
+    return run_split<GEMM_PLAIN, false, true>(a, EPI_BF16, dX, Cx, accumulate ? 1 : 0, ws, ws_elems, counters, st);
+  }
+  const int64_t need = tc_dgrad_cols_elems(g);
+  if (need && dcols && dcols_elems >= need && need < (int64_t)1 << 31) {
+    // explicit transposed-conv operand (the TMA pixel boxes cannot serve this geometry), then a
+    // GEMM with both operands by TMA
+    const int kco = (g.Co + 63) / 64 * 64;
+    const int64_t items = need / 8;
+    launch_pdl(dgrad_cols_kernel, dim3((unsigned)std::min<int64_t>((items + 255) / 256, 148 * 16)), dim3(256), 0, st,
+               dY, dcols, g, kco);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    a.A = dcols; a.kco = kco;
+    a.M = g.Nimg * g.H * g.W; a.N = Cx; a.K = g.R * g.S * kco;
+    return run_split<GEMM_DGRAD, false, true>(a, EPI_BF16, dX, Cx, accumulate ? 1 : 0, ws, ws_elems, counters, st);
+  }
+  a.A = dY;
   a.M = g.Nimg * g.H * g.W; a.N = Cx; a.K = g.R * g.S * g.Co;
   return run_split<GEMM_DGRAD, false, true>(a, EPI_BF16, dX, Cx, accumulate ? 1 : 0, ws, ws_elems, counters, st);
 }
@@ -1555,6 +1645,8 @@ cudaError_t tc_im2col_wgrad(const ConvGeo& g, const bf16* cols, const bf16* dY, 
 
 cudaError_t tc_conv_wgrad(const ConvGeo& g, const bf16* X, const bf16* dY, float* gW, bool accumulate, float* ws,
                           int64_t ws_elems, int* counters, cudaStream_t st) {
+  if (is_pointwise(g) && g.sh == 1 && g.sw == 1 && !no_dense())  // 1x1: X is the im2col matrix
+    return tc_im2col_wgrad(g, X, dY, gW, accumulate, ws, ws_elems, counters, st);
   GemmArgs a{};
   a.g = g; a.A = X; a.B = dY;
   a.M = g.R * g.S * g.C; a.N = g.Co; a.K = g.Nimg * g.P * g.Q;
@@ -1640,7 +1732,18 @@ extern "C" int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void
   cudaError_t e;
   typedef __nv_bfloat16 B;
   if (mode == 1) e = xp::tc_conv_fprop(g, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, counters, st);
-  else if (mode == 2) e = xp::tc_conv_dgrad(g, g.C, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, counters, st);
+  else if (mode == 2) {
+    // the explicit dgrad operand (geometries the TMA pixel boxes cannot serve) in the upper half
+    // of the workspace when it fits, the split-K partials in the lower half
+    const int64_t need = xp::tc_dgrad_cols_elems(g);
+    B* dcols = nullptr;
+    if (need && ws && (need + 1) / 2 <= ws_elems / 2) {
+      dcols = reinterpret_cast<B*>(ws + ws_elems / 2);
+      ws_elems /= 2;
+    }
+    e = xp::tc_conv_dgrad(g, g.C, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, counters, st, false, dcols,
+                          dcols ? need : 0);
+  }
   else e = xp::tc_conv_wgrad(g, (const B*)in0, (const B*)in1, (float*)out, accumulate != 0, ws, ws_elems, counters, st);
   return e == cudaSuccess ? XP_OK : XP_ECUDA;
 }

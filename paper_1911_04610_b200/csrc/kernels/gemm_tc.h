@@ -68,6 +68,12 @@ struct GemmArgs {
   // y[row][col] (row pitch ldy) = Q(relu?(gamma (x - mean) rstd + beta)) of x = Q(acc), or with
   // res: relu?(Q(Q(gamma (x - mean) rstd + beta) + res[row][col])); CTA rank 0 stores the
   // statistics [4][N] (mean, rstd, gamma, beta) for the backward
+  // DGRAD from an explicit operand (a_tma = 4): A = cols [M][K] dense (tc_dgrad_cols), k = tap *
+  // kco + co with kco = Co rounded up to 64 (every k-block inside one tap); 0 = implicit gather
+  int kco;
+  // EPI_BF16 row map (strided 1x1 dgrad): GEMM row m = (n, p, q) of a [rm_P][rm_Q] grid stores to
+  // row (n * rm_H + p * rm_sh) * rm_W + q * rm_sw; rm_Q = 0: identity
+  int rm_P, rm_Q, rm_H, rm_W, rm_sh, rm_sw;
   int bnf;
   const __nv_bfloat16* gamma;
   const __nv_bfloat16* beta;
@@ -105,10 +111,20 @@ cudaError_t tc_gemm_plain(const __nv_bfloat16* A, const __nv_bfloat16* B, float*
 cudaError_t tc_conv_fprop(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* Wt, __nv_bfloat16* Y,
                           float* ws, int64_t ws_elems, int* counters, cudaStream_t st, float* bn_part = nullptr,
                           int* bn_tiles = nullptr, const BnFuse* bnf = nullptr, bool* bnf_done = nullptr);
-// dX [Nimg*H*W][Cx] bf16 (Cx = real input channels, multiple of 8) from dY [Nimg*P*Q][Co]
+// dX [Nimg*H*W][Cx] bf16 (Cx = real input channels, multiple of 8) from dY [Nimg*P*Q][Co].
+// Paths: 1x1 stride-1 convs as a dense GEMM (dY x W); strided 1x1 convs as a dense GEMM over dY
+// whose rows scatter to the strided input pixels (the others zero, or untouched when
+// accumulating); geometries the TMA pixel boxes cannot serve (stride > 1, Co % 64, tile rows
+// that are not a box of the input grid) through an explicit transposed-conv operand built in
+// dcols (tc_dgrad_cols_elems(g) bf16, caller scratch; NULL keeps the implicit cp.async gather)
 cudaError_t tc_conv_dgrad(const ConvGeo& g, int Cx, const __nv_bfloat16* dY, const __nv_bfloat16* Wt,
                           __nv_bfloat16* dX, float* ws, int64_t ws_elems, int* counters, cudaStream_t st,
-                          bool accumulate = false);
+                          bool accumulate = false, __nv_bfloat16* dcols = nullptr, int64_t dcols_elems = 0);
+// elements of the explicit dgrad operand a geometry needs (0: the conv runs without one)
+int64_t tc_dgrad_cols_elems(const ConvGeo& g);
+// the forward / weight-gradient A operand cannot come from TMA pixel boxes of the activation
+// (and the conv is not a 1x1 stride-1 one, which runs dense): use the explicit im2col path
+bool tc_conv_needs_cols(const ConvGeo& g);
 // gW [Co][R][S][C] fp32 (=|+=) sum over pixels of dY x im2col(X)
 cudaError_t tc_conv_wgrad(const ConvGeo& g, const __nv_bfloat16* X, const __nv_bfloat16* dY, float* gW, bool accumulate,
                           float* ws, int64_t ws_elems, int* counters, cudaStream_t st);

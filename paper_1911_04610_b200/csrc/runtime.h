@@ -72,6 +72,8 @@ struct StageRT {
   std::vector<float*> dz;               // [slot] logits gradient (last stage)
   std::vector<void*> grad;              // [tensor] activation-gradient buffers (per op pass)
   void* gmid = nullptr;                 // conv op: gradient of the conv output (bf16), buffer 0
+  void* dcols = nullptr;                // explicit dgrad operand scratch (tc_dgrad_cols_elems), bf16
+  int64_t dcols_elems = 0;
   void* lin_dy = nullptr;               // tensor-core Linear backward operand dyp [n][lin_ldp] bf16
   int lin_ldp = 0;
   void* gmid1 = nullptr;                //   buffer 1 (consecutive conv ops alternate; see side)

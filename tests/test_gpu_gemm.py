@@ -56,6 +56,18 @@ CONVS = [
     (5, 64, 8, 8, 64, 1, 1, 1, 1, 0, 0),        # wgrad M = 64 (half an MN tile)
     (2, 64, 8, 8, 64, 1, 7, 1, 1, 0, 3),        # asymmetric filter / padding
     (6, 192, 2, 2, 320, 3, 3, 1, 1, 1, 1),      # box {2, 2, 32}, ragged N tiles
+    # Inception-V3 / ResNet-101 geometries at 64x64: dense 1x1 GEMMs (stride 1 at any spatial size,
+    # strided 1x1 dgrad scattering rows), and the explicit dgrad operand where the TMA pixel boxes
+    # cannot serve (7x7 / 3x3 maps, Co % 64 != 0, stride 2)
+    (4, 96, 7, 7, 96, 3, 3, 1, 1, 1, 1),
+    (3, 192, 3, 3, 160, 1, 7, 1, 1, 0, 3),
+    (3, 160, 3, 3, 192, 7, 1, 1, 1, 3, 0),
+    (2, 288, 7, 7, 384, 3, 3, 2, 2, 0, 0),
+    (2, 48, 7, 7, 64, 5, 5, 1, 1, 2, 2),
+    (2, 768, 3, 3, 192, 1, 1, 1, 1, 0, 0),
+    (2, 256, 16, 16, 512, 1, 1, 2, 2, 0, 0),
+    (3, 1024, 4, 4, 2048, 1, 1, 2, 2, 0, 0),
+    (2, 256, 8, 8, 256, 3, 3, 2, 2, 1, 1),
 ]
 
 

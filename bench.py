@@ -164,7 +164,32 @@ def measured_unit_costs(L, units, shape, classes, kind, N, T, prec, sched, minib
             for u in range(nu)]
 
 
-def cpu_baseline(workload, seconds=20.0):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline_single_thread(workload, seconds=8.0):
+    """The same oracle measurement on one host thread (1 thread and all cores), in a
+    subprocess so OpenMP starts with OMP_NUM_THREADS=1; samples/s or None."""
+    code = ("import sys, json; sys.path.insert(0, %r); import bench; "
+            "r = bench.cpu_baseline(%r, seconds=%r, single_thread=False); print(json.dumps(r['value']))"
+            % (os.path.dirname(os.path.abspath(__file__)), workload, seconds))
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
+        v = float(out.stdout.strip().splitlines()[-1])
+        return {"value": v, "unit": "samples/s", "cores": 1}
+    except Exception:
+        return None
+
+
+def cpu_baseline(workload, seconds=20.0, single_thread=True):
     """The oracle as it stands, on this host's cores: one micro-batch at a time of the same
     workload (K=1 stage, bf16 emulation for VGG-16 / fp32 for the MLP), bounded to ~seconds."""
     import oracle
@@ -181,8 +206,10 @@ def cpu_baseline(workload, seconds=20.0):
         el = time.perf_counter() - t0
         if el >= seconds or (done >= 1 and el * (done + 1) / done > 3 * seconds):
             break
-    cores = os.cpu_count()
+    cores = int(os.environ.get("OMP_NUM_THREADS") or len(os.sched_getaffinity(0)))
+    one = cpu_baseline_single_thread(workload) if single_thread else None
     return {"value": done * n / el, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "single_thread": one,
             "sample": "%d micro-batch(es) of %d samples through the oracle (%s, K=1, fwd+bwd+update), %.1f s"
                       % (done, n, "bf16 emulation" if prec == "bf16" else "fp32", el)}
 

@@ -673,32 +673,6 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
     }
     return;
   }
-  if (MODE == GEMM_DGRAD && a.a_tma == 5) {
-    // paired k-blocks (Co % 128 == 0, no split-K, BN 64, even ring): one 5-D box of dY lands the
-    // A tiles of k-blocks 2i and 2i+1 (two 64-channel blocks of one tap), one 128-row box of the
-    // weights their B tiles, all on slot 2i's barrier; slot 2i+1's is arrived at once
-    if (tid != 0) return;
-    for (int j = 0; j < nunits; ++j) {
-      const Work w = work_of<BN>(a, j, mt);
-      const int tn = w.m0 / (a.gq * a.gp), rem = w.m0 - tn * a.gq * a.gp, tp = rem / a.gq, tq = rem - tp * a.gq;
-      for (int i = 0; i < w.nkb; i += 2) {
-        const int s0 = ring.slot;
-        mbar_wait(empty0 + 8 * s0, ring.phase ^ 1u);
-        mbar_wait(empty0 + 8 * (s0 + 1), ring.phase ^ 1u);
-        const uint32_t sa = base + s0 * A_BYTES, sb = base + a.stages * A_BYTES + s0 * B_BYTES;
-        const uint32_t full = full0 + 8 * s0;
-        const int k0 = (w.kb0 + i) * BK;
-        const int tap = k0 / a.g.Co, c0 = k0 - tap * a.g.Co, r = tap / a.g.S, ss = tap - r * a.g.S;
-        mbar_expect_tx(full, 2 * STAGE);
-        tma_5d(sa, tmA, 0, tq + a.g.pw - ss, tp + a.g.ph - r, tn, c0 / 64, full);
-        tma_3d(sb, tmB, w.n0, tap, c0, full);
-        mbar_arrive(full0 + 8 * (s0 + 1));
-        ring.next();
-        ring.next();
-      }
-    }
-    return;
-  }
   if (a.a_tma) {
     // full-TMA pipeline: one elected thread streams both operands; the others are idle
     if (tid != 0) return;
@@ -1370,28 +1344,6 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
         tmA = pa;
         tmB = pbm;
         args.a_tma = 3;
-      }
-    }
-  }
-  if (MODE == GEMM_DGRAD && BN == 64 && splits <= 1 && args.a_tma == 1 && args.b_tma == 3 && args.g.Co % 128 == 0 &&
-      args.stages % 2 == 0 && !no_pair) {
-    // paired dgrad k-blocks (128 output channels of one tap): A as a 5-D map over dY with the
-    // channel block outermost, B as the 3-D weight map with a 128-row box; both land two
-    // consecutive ring slots on the first slot's barrier
-    const ConvGeo& g = args.g;
-    uint32_t pb[3];
-    CUtensorMap pa, pbm;
-    if (pixel_box(BM, g.W, g.H, pb)) {
-      const uint64_t d5[5] = {64, (uint64_t)g.Q, (uint64_t)g.P, (uint64_t)g.Nimg, (uint64_t)(g.Co / 64)};
-      const uint64_t s5[4] = {(uint64_t)g.Co * 2, (uint64_t)g.Q * g.Co * 2, (uint64_t)g.P * g.Q * g.Co * 2, 128};
-      const uint32_t b5[5] = {64, pb[0], pb[1], pb[2], 2};
-      const uint64_t d3[3] = {(uint64_t)g.C, (uint64_t)(g.R * g.S), (uint64_t)g.Co};
-      const uint64_t s3[2] = {(uint64_t)g.C * 2, (uint64_t)g.R * g.S * g.C * 2};
-      const uint32_t b3[3] = {64, 1, 128};
-      if (make_map(&pa, args.A, 5, d5, s5, b5) && make_map(&pbm, args.B, 3, d3, s3, b3)) {
-        tmA = pa;
-        tmB = pbm;
-        args.a_tma = 5;
       }
     }
   }

@@ -491,11 +491,14 @@ def main():
         if mp_mode:
             # every rank must run the same number of calls (the stages are coupled): a fixed count
             # that covers eligibility, the first sighting, the capture and a few replays
-            for _ in range(args.warmup + (0 if args.no_graphs else 2 * K + 4)):
+            for _ in range(args.warmup + (0 if args.no_graphs else 2 * K + 4 + 2 * max(1, args.timing))):
                 m.step(xd, yd, M)
             barrier()
             return
-        while w < args.warmup or (not args.no_graphs and streak < K + 1 and w < args.warmup + 4 * K + 8):
+        # (the calls stamped for xpipe_stats -- every --timing-th -- have a graph of their own: the
+        # streak must cover one of them too, or the timed region would enqueue it from the host)
+        tp = max(1, args.timing)
+        while w < args.warmup or (not args.no_graphs and streak < K + 1 + tp and w < args.warmup + 4 * K + 8 + 3 * tp):
             m.step(xd, yd, M)
             streak = streak + 1 if m.last_stats.graph_replays else 0
             w += 1

@@ -1549,7 +1549,8 @@ cudaError_t tc_conv_fprop(const ConvGeo& g, const bf16* X, const bf16* Wt, bf16*
     return tc_im2col_fprop(g, X, Wt, Y, ws, ws_elems, counters, st, bn_part, bn_tiles);
   const SplitPlan sp = plan_splits(a.M, a.N, a.K);
   const int mt = (a.M + BM - 1) / BM;
-  if (bnf && !no_bnf() && sp.cs * sp.nc <= 1 && mt <= 16 && g.Co % 8 == 0 && bnf->ldy % 8 == 0 &&
+  static const int bnf_mt = std::min(16, std::max(1, getenv_int("XPIPE_BN_FUSE_MT", 16)));  // dev: cluster cap
+  if (bnf && !no_bnf() && sp.cs * sp.nc <= 1 && mt <= bnf_mt && g.Co % 8 == 0 && bnf->ldy % 8 == 0 &&
       (sp.bn == 64 ? bnf_resident<64>(mt, a) : sp.bn == 128 ? bnf_resident<128>(mt, a) : bnf_resident<256>(mt, a))) {
     a.bnf = 1;
     a.gamma = bnf->gamma; a.beta = bnf->beta; a.bn_eps = bnf->eps; a.stats = bnf->stats;

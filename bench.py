@@ -378,6 +378,8 @@ def main():
     ap.add_argument("--schedule", default="xpipe", choices=["xpipe", "gpipe"],
                     help="gpipe: synchronous GPipe with a flush per mini-batch (prediction off), same kernels")
     ap.add_argument("--no-graphs", action="store_true", help="enqueue every kernel from the host (no CUDA graphs)")
+    ap.add_argument("--sync-calls", action="store_true",
+                    help="every xpipe_step call waits for its work (no chained asynchronous graph replays)")
     ap.add_argument("--timing", type=int, default=4,
                     help="stamp every p-th call of the timed run (cfg.timing: bubble, steady rate, hand-offs); "
                          "0 = off.  Stamping every call costs ~6%% at VGG-16 K=4, every 4th ~1.5%%")
@@ -513,7 +515,9 @@ def main():
     with Clocks(dev) as ck:
         g.timer_start()
         for _ in range(args.steps):
-            g.step(xd, yd, M, losses=False)
+            # asynchronous calls: consecutive graph replays chain on the device (no host wait at
+            # the call boundary); stamped calls complete synchronously; timer_stop waits for all
+            g.step(xd, yd, M, losses=False, async_=not args.sync_calls)
             st = g.last_stats
             launches += st.kernel_launches
             replays += st.graph_replays
@@ -527,12 +531,14 @@ def main():
     if not args.no_e2e:
         xh = torch.from_numpy(x).pin_memory()
         yh = torch.from_numpy(y).pin_memory()
+        lh = torch.empty(M * T, dtype=torch.float32).pin_memory()  # every step's losses (D2H)
         xh_np, yh_np = xh.numpy(), yh.numpy()
         g.step(xh_np, yh_np, M)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            g.step(xh_np, yh_np, M, losses=True)
+            g.step(xh_np, yh_np, M, async_=not args.sync_calls, loss_out=lh)
+        g.sync()
         barrier()
         e2e_s = time.perf_counter() - t0
     # ---- a separate profiled pass (CUDA events around every kernel class) for the roofline and

@@ -79,7 +79,10 @@ enum { XP_TRANSPORT_P2P = 0 };  /* the producer stream copies its boundary tenso
 /* xpipe_step flags */
 enum { XP_FLUSH = 1,        /* drain the pipeline at the end of the call */
        XP_DEVICE_PTRS = 2,  /* x and y are device pointers on stage 0's / stage K-1's device */
-       XP_ASYNC = 4 };      /* return after enqueue; the next call (or xpipe_sync) waits */
+       XP_ASYNC = 4 };      /* return after enqueue; the next call (or xpipe_sync) waits -- except
+                                 that consecutive replays of captured graphs (single process, one
+                                 device) chain on the device without a host wait; a call stamped by
+                                 cfg.timing always completes (its statistics are read back) */
 
 /* xpipe_get_weights selectors */
 enum { XP_T_WEIGHT = 0, XP_T_BIAS = 1 };       /* BatchNorm: WEIGHT = gamma, BIAS = beta */
@@ -223,7 +226,8 @@ int xpipe_init(const xpipe_layer* layers, int32_t n_layers, int32_t stages, int3
    pointers, by the loss kernel for device pointers -- then reported at the end of the call, the
    affected rows got no one-hot term), XP_ECUDA, XP_ESCHED (watchdog), XP_ENONFINITE (a non-finite
    loss; the call's work completed).  With XP_ASYNC these device-side checks are reported by the
-   next synchronous call. */
+   next synchronous call; st->losses (when set) is then filled by an asynchronous copy, valid
+   after the next synchronous call or xpipe_sync. */
 int xpipe_step(struct xpipe_ctx* h, const float* x, const int32_t* y, int32_t n_minibatches,
                uint32_t flags, xpipe_stats* st);
 

@@ -181,6 +181,7 @@ struct xpipe_ctx {
   int64_t cap_base = 0;                 // multi-process capture: fed_before of the captured call
   int64_t calls = 0;                    // xpipe_step calls so far (cfg.timing sampling)
   bool timed = false;                   // this call is stamped (cfg.timing)
+  bool chain_ok = false;                // the last call was an asynchronous graph replay (XP_ASYNC)
   std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)
 };
 

@@ -743,14 +743,25 @@ int rebase_flags(xpipe_ctx* c, int64_t new_base) {
   return XP_OK;
 }
 
-int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before) {
+int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before, bool chain = false) {
   // single process: flags rebased to the call's base (every stage drained); multi-process: the
   // flags stay absolute (neighbours may still be running) and the graph's flag kernels read the
-  // call's base from the device
-  if (!c->mp()) XP_TRY(rebase_flags(c, fed_before));
+  // call's base from the device.  Chained replay (the previous call's graph still running): the
+  // rebase kernels go on the launch stream, ordered after that graph and before this one
   const std::string sig = graph_signature(c, M, fed_before);
   xpipe_ctx::GraphRec& g = c->graphs[sig];
   StageRT& o = c->mp() ? c->S[c->cfg.my_stage] : c->S[0];
+  if (!c->mp()) {
+    if (chain) {
+      const int64_t delta = fed_before - c->flag_base;
+      cudaSetDevice(o.dev);
+      for (auto& s : c->S)
+        if (delta) XP_TRY(check_launch(c, launch_rebase_flags(s.flags, 4, (uint32_t)delta, o.stream), "rebase"));
+      c->flag_base = fed_before;
+    } else {
+      XP_TRY(rebase_flags(c, fed_before));
+    }
+  }
   cudaSetDevice(o.dev);
   if (c->mp()) XP_TRY(check_launch(c, launch_set_i64(o.dbase, fed_before, o.stream), "base"));
   if (g.exec) {
@@ -932,6 +943,21 @@ int ensure_call_buffers(xpipe_ctx* c, int64_t M) {
     if ((first && !c->x_dev) || (last && (!c->y_dev || !c->loss_dev))) return set_err(c, XP_ENOMEM, "call buffers");
   }
   return XP_OK;
+}
+
+// a chained replay (see xpipe_step) needs: the single-process graph path, the same call
+// buffers (no reallocation), no stamping / profiling / tracing / snapshots, and an already
+// captured graph for this call's signature
+__host__ bool no_chain() { static const bool v = [] { const char* e = getenv("XPIPE_NO_CHAIN"); return e && *e && *e != '0'; }(); return v; }
+bool can_chain(xpipe_ctx* c, uint32_t flags, int64_t M) {
+  if (no_chain() || c->mp() || M <= 0 || (flags & XP_FLUSH) || c->timed || c->cfg.profile || c->cfg.trace ||
+      c->cfg.snapshots || c->cfg.recompute)
+    return false;
+  const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
+  if (M * c->N * per > c->x_cap || M * c->N > c->y_cap || M * c->T > c->loss_cap) return false;
+  if (!graph_eligible(c, flags, M, c->fed)) return false;
+  auto it = c->graphs.find(graph_signature(c, M, c->fed));
+  return it != c->graphs.end() && it->second.exec != nullptr;
 }
 
 }  // namespace
@@ -1116,10 +1142,29 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
   int cur = 0;
   cudaGetDevice(&cur);
   const int64_t k0 = c->kernels, g0 = c->graph_replays;
-  // previous call's work must be done before its call buffers are overwritten
-  XP_TRY(sync_all(c));
-  ++c->call_epoch;  // every event recorded before this point is complete
-  if (M > 0) {
+  // cfg.timing = p: this call is stamped when it is the p-th since the last stamped one
+  c->timed = c->cfg.timing > 0 && (c->calls++ % c->cfg.timing) == 0;
+  // Chained replay: the previous call was an asynchronous replay of a captured graph and this
+  // one replays one too.  Both graphs, the rebase and the input copies are then ordered on the
+  // launch stream (a graph launch is one stream operation there), so the previous call's work
+  // need not be waited for on the host; otherwise it must be done before its call buffers are
+  // overwritten
+  const bool chain = c->chain_ok && can_chain(c, flags, M);
+  c->chain_ok = false;
+  if (!chain) XP_TRY(sync_all(c));
+  ++c->call_epoch;  // every event recorded before this point is complete (chain: no event logic runs)
+  if (M > 0 && chain) {
+    const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
+    StageRT& s0 = c->S[0];
+    cudaSetDevice(s0.dev);
+    XP_CUDA(c, cudaMemcpyAsync(c->x_dev, x, (size_t)M * c->N * per * 4,
+                               dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.stream));
+    XP_CUDA(c, cudaMemcpyAsync(c->y_dev, y, (size_t)M * c->N * 4,
+                               dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.stream));
+    XP_CUDA(c, cudaMemsetAsync(c->loss_dev, 0xff, (size_t)M * c->T * 4, s0.stream));  // NaN = not computed
+    c->call_first = c->fed + 1;
+    c->fed += (int64_t)M * c->T;
+  } else if (M > 0) {
     XP_TRY(ensure_call_buffers(c, M));
     const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
     StageRT& s0 = c->S[0];
@@ -1151,13 +1196,11 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     c->fed += (int64_t)M * c->T;
   }
   for (auto& s : c->S) { s.ev_used = 0; s.prof_cls.clear(); s.prof_work.clear(); s.tev_used = 0; s.tops.clear(); }
-  // cfg.timing = p: this call is stamped when it is the p-th since the last stamped one
-  c->timed = c->cfg.timing > 0 && (c->calls++ % c->cfg.timing) == 0;
-  XP_TRY(reserve_for_call(c, M));
+  if (!chain) XP_TRY(reserve_for_call(c, M));  // chain: the same M as a replayed call, nothing to reserve
   const bool empty_before = c->fed - (int64_t)M * c->T == c->base;  // pipeline empty at the call's start
 
   const int64_t fed_before = c->fed - (int64_t)M * c->T;
-  if (graph_eligible(c, flags, M, fed_before)) XP_TRY(drive_graph(c, M, fed_before));
+  if (graph_eligible(c, flags, M, fed_before)) XP_TRY(drive_graph(c, M, fed_before, chain));
   else XP_TRY(drive(c, -1));
   if (flags & XP_FLUSH) {
     XP_TRY(drive(c, c->fed));
@@ -1171,8 +1214,20 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     reset_schedule(c);
   }
   int rr = XP_OK;
+  // XP_ASYNC: return after enqueue -- except a stamped call (its statistics are read back); an
+  // asynchronous single-process graph replay lets the next replay chain behind it
+  const bool replayed = c->graph_replays > g0;
+  if ((flags & XP_ASYNC) && c->timed) flags &= ~(uint32_t)XP_ASYNC;
   if (!(flags & XP_ASYNC)) rr = sync_all(c);
   if (rr != XP_OK) return rr;
+  c->chain_ok = (flags & XP_ASYNC) && replayed && !c->mp() && !(flags & XP_FLUSH) && !c->cfg.profile;
+  if ((flags & XP_ASYNC) && st && st->losses && M > 0 && owned(c->S[c->K - 1])) {
+    // the losses follow the call's work on its stream (a replay: the launch stream; else the last
+    // stage's, where the loss kernel ran); the caller's buffer is read after a sync
+    StageRT& q = (replayed && !c->mp()) ? c->S[0] : c->S[c->K - 1];
+    cudaSetDevice(q.dev);
+    XP_CUDA(c, cudaMemcpyAsync(st->losses, c->loss_dev, (size_t)M * c->T * 4, cudaMemcpyDeviceToHost, q.stream));
+  }
   uint32_t status = 0;
   if (!(flags & XP_ASYNC) && c->status_dev) {
     // loss-kernel status word (device-side label range and non-finite loss checks)

@@ -235,8 +235,11 @@ class XPipe:
         except Exception:
             pass
 
-    def step(self, x, y, M, flush=False, async_=False, losses=True):
-        """x: [M*N, C, H, W] float32, y: [M*N] int32 -- numpy (host) or torch CUDA tensors (device)."""
+    def step(self, x, y, M, flush=False, async_=False, losses=True, loss_out=None):
+        """x: [M*N, C, H, W] float32, y: [M*N] int32 -- numpy (host) or torch CUDA tensors (device).
+        async_: return after enqueue (XP_ASYNC; replays of captured graphs then chain on the device);
+        loss_out: a caller buffer of M*T float32 (pinned host memory for an asynchronous copy)
+        receiving the losses, valid after the next synchronous call or sync()."""
         flags = (XP_FLUSH if flush else 0) | (XP_ASYNC if async_ else 0)
         per = self.in_shape[0] * self.in_shape[1] * self.in_shape[2]
         if hasattr(x, "is_cuda") and x.is_cuda:
@@ -250,7 +253,11 @@ class XPipe:
             y = np.ascontiguousarray(y, dtype=np.int32)
         st = Stats()
         out = None
-        if losses and not async_:
+        if loss_out is not None:
+            _want("loss_out", loss_out, ("float32",), M * self.T)
+            st.losses = C.cast(_ptr(loss_out), C.POINTER(C.c_float))
+            out = loss_out
+        elif losses and not async_:
             out = np.empty(M * self.T, dtype=np.float32)
             st.losses = out.ctypes.data_as(C.POINTER(C.c_float))
         _check(lib().xpipe_step(self.h, _ptr(x), _ptr(y), M, flags, C.byref(st)), self.h)

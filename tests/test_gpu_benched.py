@@ -178,6 +178,41 @@ def test_fp32_graphs_overlap_changing_pinned_inputs(oracle_mod):
     g.close()
 
 
+@pytest.mark.parametrize("timing", [0, 3])
+def test_fp32_async_chained_replays(oracle_mod, timing):
+    """Asynchronous calls (XP_ASYNC) whose graph replays chain on the device without a host wait
+    (the bench's timed loop): every call's inputs are distinct device tensors and its losses go
+    to a pinned buffer by an asynchronous copy; weights bit-exact with the oracle after the flush
+    and the losses equal the oracle's.  timing=3: every third call is stamped and completes
+    synchronously in between."""
+    from paper_1911_04610_b200 import XPipe
+    L = S.mlp()
+    P = S.make_params(L, 1)
+    K, T, N, C, calls = 2, 4, 32, 8, 12
+    M = C * calls
+    x, y = S.make_inputs(M * N, (784, 1, 1), 10, 7, kind="mnist")
+    g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, params=P, precision="fp32", graphs=True,
+              fb_overlap=True, timing=timing, watchdog_ms=60000)
+    xs = [torch.from_numpy(x[i * C * N:(i + 1) * C * N].copy()).cuda() for i in range(calls)]
+    ys = [torch.from_numpy(y[i * C * N:(i + 1) * C * N].copy()).cuda() for i in range(calls)]
+    outs = [torch.full((C * T,), float("nan")).pin_memory() for _ in range(calls)]
+    replays = 0
+    for i in range(calls):
+        g.step(xs[i], ys[i], C, async_=True, loss_out=outs[i])
+        replays += g.last_stats.graph_replays
+    g.sync()
+    g.step(x[:0], y[:0], 0, flush=True)
+    assert replays >= 4, replays
+    o = oracle_mod.Oracle(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, P, mode="fp32")
+    lo = o.step(x, y, M, flush=True)
+    assert np.array_equal(g.params_flat(), o.params_flat().astype(np.float32))
+    got = torch.cat(outs).numpy()
+    assert np.isfinite(got).all()
+    if lo is not None:
+        assert np.allclose(got, np.asarray(lo, dtype=np.float32).ravel()[:got.size], rtol=0, atol=0)
+    g.close()
+
+
 def test_device_label_range_and_nonfinite(oracle_mod):
     """Device-pointer labels are range-checked by the loss kernel (XP_EINVAL after the call) and
     a non-finite loss is reported as XP_ENONFINITE."""

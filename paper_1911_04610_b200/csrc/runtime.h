@@ -182,6 +182,7 @@ struct xpipe_ctx {
   int64_t calls = 0;                    // xpipe_step calls so far (cfg.timing sampling)
   bool timed = false;                   // this call is stamped (cfg.timing)
   bool chain_ok = false;                // the last call was an asynchronous graph replay (XP_ASYNC)
+  bool graph_launched = false;          // this call's work went out as one graph launch
   std::vector<std::pair<int64_t, int64_t>> loss_map;  // (u, index into loss_dev)
 };
 

@@ -766,6 +766,7 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before, bool chain = false)
   if (c->mp()) XP_TRY(check_launch(c, launch_set_i64(o.dbase, fed_before, o.stream), "base"));
   if (g.exec) {
     XP_CUDA(c, cudaGraphLaunch(g.exec, o.stream));
+    c->graph_launched = true;
     for (size_t k = 0; k < c->S.size(); ++k) {
       StageRT& s = c->S[k];
       const int v0 = s.host_ver;
@@ -853,6 +854,7 @@ int drive_graph(xpipe_ctx* c, int64_t M, int64_t fed_before, bool chain = false)
     g.dbver.push_back(s.host_bver - ver0[k]);
   }
   XP_CUDA(c, cudaGraphLaunch(g.exec, o.stream));
+  c->graph_launched = true;
   return XP_OK;
 }
 
@@ -1151,6 +1153,7 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
   // overwritten
   const bool chain = c->chain_ok && can_chain(c, flags, M);
   c->chain_ok = false;
+  c->graph_launched = false;
   if (!chain) XP_TRY(sync_all(c));
   ++c->call_epoch;  // every event recorded before this point is complete (chain: no event logic runs)
   if (M > 0 && chain) {
@@ -1216,7 +1219,7 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
   int rr = XP_OK;
   // XP_ASYNC: return after enqueue -- except a stamped call (its statistics are read back); an
   // asynchronous single-process graph replay lets the next replay chain behind it
-  const bool replayed = c->graph_replays > g0;
+  const bool replayed = c->graph_launched;  // a replay, or the launch right after the capture
   if ((flags & XP_ASYNC) && c->timed) flags &= ~(uint32_t)XP_ASYNC;
   if (!(flags & XP_ASYNC)) rr = sync_all(c);
   if (rr != XP_OK) return rr;

@@ -326,7 +326,10 @@ int xpipe_gemm_bf16(const void* A, const void* B, float* D, int32_t M, int32_t N
 /* Implicit-GEMM convolution on the same tensor-core path, exposed for unit parity.
    geo = {Nimg, H, W, C, Co, R, S, P, Q, sh, sw, ph, pw}: input NHWC [Nimg][H][W][C] bf16 (C a
    multiple of 8), weights KRSC [Co][R][S][C] bf16, output NHWC [Nimg][P][Q][Co].  mode:
-   1 = fprop (in0 = X, in1 = W, out = Y bf16), 2 = dgrad (in0 = dY, in1 = W, out = dX bf16
+   1 = fprop (in0 = X, in1 = W, out = Y bf16), 4 = the same through an explicit im2col operand
+   (built in the upper half of ws, which must hold Nimg*P*Q*R*S*C bf16 there; the pipeline's path
+   for geometries the TMA pixel boxes cannot serve), 5 = wgrad likewise (as 3),
+   2 = dgrad (in0 = dY, in1 = W, out = dX bf16
    [Nimg][H][W][C]), 3 = wgrad (in0 = X, in1 = dY, out = dW fp32 [Co][R][S][C], accumulate
    adds into out).  ws: optional fp32 device workspace of ws_elems for split-K across
    several clusters (NULL = split-K within one thread-block cluster only); its last 16384

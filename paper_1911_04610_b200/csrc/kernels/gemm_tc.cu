@@ -27,6 +27,7 @@
 #include "../internal.h"
 #include "launch.h"
 #include "gemm_tc.h"
+#include "bf16_kernels.h"
 
 namespace xp {
 
@@ -1717,7 +1718,7 @@ extern "C" int xpipe_gemm_bf16(const void* A, const void* B, float* D, int32_t M
 
 extern "C" int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void* in0, const void* in1, void* out,
                                  int32_t accumulate, float* ws, int64_t ws_elems, void* stream) {
-  if (!geo || !in0 || !in1 || !out || mode < 1 || mode > 3) return XP_EINVAL;
+  if (!geo || !in0 || !in1 || !out || mode < 1 || mode > 5) return XP_EINVAL;
   xp::ConvGeo g{geo[0], geo[1], geo[2], geo[3], geo[4], geo[5], geo[6], geo[7], geo[8], geo[9], geo[10], geo[11], geo[12]};
   if (g.C % 8 || g.Co % 8 || g.Nimg < 1) return XP_EINVAL;
   if (g.P != (g.H + 2 * g.ph - g.R) / g.sh + 1 || g.Q != (g.W + 2 * g.pw - g.S) / g.sw + 1) return XP_EINVAL;
@@ -1745,7 +1746,21 @@ extern "C" int xpipe_conv2d_bf16(int32_t mode, const int32_t geo[13], const void
     e = xp::tc_conv_dgrad(g, g.C, (const B*)in0, (const B*)in1, (B*)out, ws, ws_elems, counters, st, false, dcols,
                           dcols ? need : 0);
   }
-  else e = xp::tc_conv_wgrad(g, (const B*)in0, (const B*)in1, (float*)out, accumulate != 0, ws, ws_elems, counters, st);
+  else if (mode == 3) {
+    e = xp::tc_conv_wgrad(g, (const B*)in0, (const B*)in1, (float*)out, accumulate != 0, ws, ws_elems, counters, st);
+  } else {
+    // 4 / 5: fprop / wgrad through the explicit im2col operand (the pipeline's path for
+    // geometries the TMA pixel boxes cannot serve), built in the upper half of ws
+    const int64_t need = (int64_t)g.Nimg * g.P * g.Q * g.R * g.S * g.C;
+    if (!ws || (need + 1) / 2 > ws_elems / 2) return XP_EINVAL;
+    B* cols = reinterpret_cast<B*>(ws + ws_elems / 2);
+    ws_elems /= 2;
+    e = xp::launch_im2col_bf16((const B*)in0, cols, g.Nimg, g.H, g.W, g.C, g.P, g.Q, g.R, g.S, g.sh, g.sw, g.ph, g.pw, st);
+    if (e == cudaSuccess && mode == 4)
+      e = xp::tc_im2col_fprop(g, cols, (const B*)in1, (B*)out, ws, ws_elems, counters, st, nullptr, nullptr);
+    else if (e == cudaSuccess)
+      e = xp::tc_im2col_wgrad(g, cols, (const B*)in1, (float*)out, accumulate != 0, ws, ws_elems, counters, st);
+  }
   return e == cudaSuccess ? XP_OK : XP_ECUDA;
 }
 

@@ -386,10 +386,11 @@ def gemm_bf16(A, B, D, M, N, K, a_kmajor=True, b_kmajor=True, ldd=None, stream=N
 
 
 def conv2d_bf16(mode, geo, in0, in1, out, accumulate=False, ws=None, stream=None):
-    """mode 1 fprop / 2 dgrad / 3 wgrad; geo = (Nimg, H, W, C, Co, R, S, P, Q, sh, sw, ph, pw)."""
+    """mode 1 fprop / 2 dgrad / 3 wgrad / 4, 5 fprop, wgrad via explicit im2col;
+    geo = (Nimg, H, W, C, Co, R, S, P, Q, sh, sw, ph, pw)."""
     _want("in0", in0, ("bfloat16",))
     _want("in1", in1, ("bfloat16",))
-    _want("out", out, ("float32",) if mode == 3 else ("bfloat16",))
+    _want("out", out, ("float32",) if mode in (3, 5) else ("bfloat16",))
     _want("ws", ws, ("float32",))
     g = (C.c_int32 * 13)(*geo)
     _check(lib().xpipe_conv2d_bf16(mode, g, _ptr(in0), _ptr(in1), _ptr(out), int(accumulate),

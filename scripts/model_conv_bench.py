@@ -44,6 +44,24 @@ def geometries(model, image):
     return geo, T
 
 
+def pixel_box(T, Q, P):
+    if Q % T == 0:
+        return True
+    if T % Q:
+        return False
+    rp = T // Q
+    return P % rp == 0 or rp % P == 0
+
+
+def needs_cols(geo):
+    """the pipeline's rule (kernels/gemm_tc.cu tc_conv_needs_cols, blocks.cu): explicit im2col for
+    few channels or a geometry the TMA pixel boxes cannot serve (not a 1x1 stride-1 conv)"""
+    n, H, W, C, Co, R, S_, P, Q, sh, sw, ph, pw = geo
+    if R == 1 and S_ == 1 and ph == 0 and pw == 0 and sh == 1 and sw == 1:
+        return False
+    return C < 64 or C % 64 != 0 or sh != 1 or sw != 1 or not pixel_box(128, Q, P) or not pixel_box(64, Q, P)
+
+
 def time_launch(fn, iters):
     st = torch.cuda.current_stream()
     for _ in range(3):
@@ -74,7 +92,7 @@ def main():
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     geo, T = geometries(args.model, args.image)
-    ws = torch.zeros((16 << 20) + (1 << 14), dtype=torch.float32, device=dev)
+    ws = torch.zeros((160 << 20) + (1 << 14), dtype=torch.float32, device=dev)  # upper half: im2col / dgrad operands
     n = args.batch
     rows = []
     for (H, W, C, Co, kh, kw, sh, sw, ph, pw, first), cnt in geo.items():
@@ -88,10 +106,13 @@ def main():
         g1 = (n, H, W, C, Co, kh, kw, P, Q, sh, sw, ph, pw)
         gT = (T * n, H, W, C, Co, kh, kw, P, Q, sh, sw, ph, pw)
         flops = 2.0 * n * P * Q * Co * kh * kw * C
-        tf = time_launch(lambda s: xpipe.conv2d_bf16(1, g1, x, w, y, ws=ws, stream=s), args.iters)
+        # the pipeline's path: explicit im2col where the TMA pixel boxes cannot serve the geometry
+        cols = needs_cols(g1)
+        mf, mw = (4, 5) if cols else (1, 3)
+        tf = time_launch(lambda s: xpipe.conv2d_bf16(mf, g1, x, w, y, ws=ws, stream=s), args.iters)
         td = float("nan") if first else time_launch(lambda s: xpipe.conv2d_bf16(2, g1, dy, w, dx, ws=ws, stream=s),
                                                     args.iters)
-        tw = time_launch(lambda s: xpipe.conv2d_bf16(3, gT, x, dy, gw, ws=ws, stream=s), args.iters)
+        tw = time_launch(lambda s: xpipe.conv2d_bf16(mw, gT, x, dy, gw, ws=ws, stream=s), args.iters)
         per_mb = cnt * (T * (tf + (0 if first else td)) + tw)
         rows.append(((H, W, C, Co, kh, kw, sh, ph, pw), cnt, tf, td, tw, flops, per_mb))
     rows.sort(key=lambda r: -r[6])

@@ -100,20 +100,24 @@ int bf16_op_forward(xpipe_ctx* c, StageRT& s, int o, const void* Wf, int slot) {
       const PoolGeo p = pool_geo(c, O.lpool);
       uint8_t* pidx = O.lpool >= 0 ? s.pidx[o][slot] : nullptr;
       const double out_elems = (double)n * O.sout.h * O.sout.w * O.sout.c;
+      // statistics partials: from the fprop epilogue (128-row tiles), else one reduction launch
+      int chunks = bn_tiles, rc = 128;
+      if (!bn_tiles) {
+        XP_TRY(prof_begin(c, s));
+        XP_TRY(check_launch(c, launch_bn_stats_partial(mid, M, O.smid.c, s.bnws, s.stream), "bn_stats"));
+        // algorithmic bytes: the conv output read once (register-resident two passes)
+        XP_TRY(prof_end(c, s, XP_PROF_BN_STATS, 2.0 * M * O.smid.c));
+        rc = bn_chunk_rows(M, O.smid.c);
+        chunks = (M + rc - 1) / rc;
+      }
+      // merge + BN-apply [+ residual] [+ ReLU] [+ pool] (one launch for small layers)
       XP_TRY(prof_begin(c, s));
-      if (bn_tiles)
-        XP_TRY(check_launch(c, launch_bn_stats_final(s.bnws, bn_tiles, M, 128, O.smid.c, N.d.bn_eps, W + N.woff,
-                                                     W + N.boff, s.stats[o][slot], s.stream), "bn_stats_final"));
-      else
-        XP_TRY(check_launch(c, launch_bn_stats(mid, M, O.smid.c, N.d.bn_eps, W + N.woff, W + N.boff, s.bnws,
-                                               s.ctr + kTileCounters - 2, s.stats[o][slot], s.stream), "bn_stats"));
-      // algorithmic bytes: the conv output read once (register-resident two passes)
-      XP_TRY(prof_end(c, s, XP_PROF_BN_STATS, 2.0 * M * O.smid.c));
-      XP_TRY(prof_begin(c, s));
-      XP_TRY(check_launch(c, launch_bn_apply(mid, s.stats[o][slot], (bf16*)y, pidx, n, O.smid.h, O.smid.w, O.smid.c,
-                                             O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw, p.ph, p.pw, O.lpool >= 0,
-                                             O.relu, s.stream, O.in1 >= 0 ? (const bf16*)s.act[O.in1][slot] : nullptr,
-                                             s.plan.tensors[O.out].pitch()),
+      XP_TRY(check_launch(c, launch_bn_apply_stats(s.bnws, chunks, rc, N.d.bn_eps, W + N.woff, W + N.boff,
+                                                   s.stats[o][slot], mid, (bf16*)y, pidx, n, O.smid.h, O.smid.w,
+                                                   O.smid.c, O.sout.h, O.sout.w, p.kh, p.kw, p.sh, p.sw, p.ph, p.pw,
+                                                   O.lpool >= 0, O.relu, s.stream,
+                                                   O.in1 >= 0 ? (const bf16*)s.act[O.in1][slot] : nullptr,
+                                                   s.plan.tensors[O.out].pitch()),
                           "bn_apply"));
       // algorithmic bytes: conv output read, output written (+ 1 B pool winner per output)
       return prof_end(c, s, XP_PROF_BN_APPLY, 2.0 * M * O.smid.c + out_elems * (O.lpool >= 0 ? 3.0 : 2.0));
@@ -204,7 +208,8 @@ int bf16_op_backward(xpipe_ctx* c, StageRT& s, int o, const void* dy, void* dx0,
       XP_TRY(prof_begin(c, s));
       XP_TRY(check_launch(c, launch_bn_bwd_apply(xmid, (const bf16*)dy, yout, pw8, s.stats[o][slot], W + N.woff, n,
                                                  O.smid.h, O.smid.w, O.smid.c, O.sout.h, O.sout.w, p.kh, p.kw, p.sh,
-                                                 p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws, dmid, s.stream, ldy),
+                                                 p.sw, p.ph, p.pw, O.lpool >= 0, O.relu, s.bnws, dmid, s.stream, ldy,
+                                                 s.g + N.woff, s.g + N.boff, accumulate_g),
                           "bn_bwd_apply"));
       XP_TRY(prof_end(c, s, XP_PROF_BN_BWD_APPLY, pass_bytes + 2.0 * mid_e));
       // fork: the weight gradient (into g, read only by the update) on the side stream.

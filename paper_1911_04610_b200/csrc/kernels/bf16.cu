@@ -607,6 +607,120 @@ __global__ void bn_bwd_apply_tiled_kernel(const bf16* __restrict__ x, const bf16
                            gridDim.x * blockDim.x);
 }
 
+// ---- folded BatchNorm merges (small layers) -------------------------------------------------
+// The per-channel merge of the partials (bn_stats_final_kernel / bn_bwd_final_kernel) done by
+// every CTA of the elementwise kernel that needs its result, into shared memory, in exactly the
+// final kernels' order (lane j merges chunks j, j+32, ... in order, then a pairwise tree of
+// strides 16..1), so the results are bit-identical and one launch per BatchNorm and direction
+// disappears.  Used where the partials are few (chunks x C <= kFoldFloats) and the layer small
+// (M x C <= kFoldElems): every CTA then re-reads at most 64 KB of partials from L2.
+constexpr int kFoldFloats = 8192;
+constexpr int64_t kFoldElems = int64_t(1) << 20;
+
+// The final kernels' order as a tree evaluated depth first (few live registers): lane j of 32
+// merges chunks j, j+32, ... in order; node(l, j) = merge(node(l-1, j), node(l-1, j + 32 >> l)),
+// the result is node(5, 0) -- the same pairwise tree as the shared-memory loop over strides 16..1
+struct ChanAcc { float n, mean, m2; };
+struct SumAcc { float a, b; };
+__device__ __forceinline__ ChanAcc chan_lane(const float* __restrict__ part, int chunks, int M, int RC, int C, int c,
+                                             int j) {
+  ChanAcc r{0.f, 0.f, 0.f};
+  for (int k = j; k < chunks; k += 32)
+    chan_merge(r.n, r.mean, r.m2, (float)min(RC, M - k * RC), __ldcg(part + (size_t)k * 2 * C + c),
+               __ldcg(part + (size_t)k * 2 * C + C + c));
+  return r;
+}
+template <int L>
+__device__ __forceinline__ ChanAcc chan_node(const float* __restrict__ part, int chunks, int M, int RC, int C, int c,
+                                             int j) {
+  if constexpr (L == 0) {
+    return chan_lane(part, chunks, M, RC, C, c, j);
+  } else {
+    ChanAcc x = chan_node<L - 1>(part, chunks, M, RC, C, c, j);
+    const ChanAcc y = chan_node<L - 1>(part, chunks, M, RC, C, c, j + (32 >> L));
+    chan_merge(x.n, x.mean, x.m2, y.n, y.mean, y.m2);
+    return x;
+  }
+}
+__device__ __forceinline__ SumAcc sum_lane(const float* __restrict__ part, int chunks, int C, int c, int j) {
+  SumAcc r{0.f, 0.f};
+  for (int k = j; k < chunks; k += 32) {
+    r.a = __fadd_rn(r.a, __ldcg(part + (size_t)k * 2 * C + c));
+    r.b = __fadd_rn(r.b, __ldcg(part + (size_t)k * 2 * C + C + c));
+  }
+  return r;
+}
+template <int L>
+__device__ __forceinline__ SumAcc sum_node(const float* __restrict__ part, int chunks, int C, int c, int j) {
+  if constexpr (L == 0) {
+    return sum_lane(part, chunks, C, c, j);
+  } else {
+    SumAcc x = sum_node<L - 1>(part, chunks, C, c, j);
+    const SumAcc y = sum_node<L - 1>(part, chunks, C, c, j + (32 >> L));
+    x.a = __fadd_rn(x.a, y.a);
+    x.b = __fadd_rn(x.b, y.b);
+    return x;
+  }
+}
+__device__ __forceinline__ void stats_merge_exact(const float* __restrict__ part, int chunks, int M, int RC, int C,
+                                                  int c, float& mean, float& m2, float& n) {
+  const ChanAcc r = chan_node<5>(part, chunks, M, RC, C, c, 0);
+  mean = r.mean; m2 = r.m2; n = r.n;
+}
+__device__ __forceinline__ void sums_merge_exact(const float* __restrict__ part, int chunks, int C, int c, float& s1,
+                                                 float& s2) {
+  const SumAcc r = sum_node<5>(part, chunks, C, c, 0);
+  s1 = r.a; s2 = r.b;
+}
+
+// forward: statistics merge (+ the stashed stats, by CTA 0) then BN-apply [+ ReLU] [+ pool]
+template <int PK>
+__global__ void __launch_bounds__(256, 2) bn_apply_fold_kernel(const bf16* __restrict__ x, const float* __restrict__ part, int chunks, int M, int RC,
+                                     float eps, const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
+                                     float* __restrict__ stats, bf16* __restrict__ y, uint8_t* __restrict__ pidx, int n,
+                                     int H, int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw,
+                                     int pool, int relu, const bf16* __restrict__ res, int ldy) {
+  extern __shared__ float sst[];  // [4][C]: mean, rstd, gamma, beta
+  pdl_wait();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float mean, m2, cnt;
+    stats_merge_exact(part, chunks, M, RC, C, c, mean, m2, cnt);
+    const float rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(m2, cnt), eps)));
+    const float ga = __bfloat162float(gamma[c]), be = __bfloat162float(beta[c]);
+    sst[c] = mean; sst[C + c] = rstd; sst[2 * C + c] = ga; sst[3 * C + c] = be;
+    if (blockIdx.x == 0) { stats[c] = mean; stats[C + c] = rstd; stats[2 * C + c] = ga; stats[3 * C + c] = be; }
+  }
+  __syncthreads();
+  bn_apply_body<PK>(x, sst, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool, relu,
+                    blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, res, ldy);
+}
+
+// backward: totals merge (+ dgamma, dbeta into the accumulator, by CTA 0) then the input gradient
+template <int AP>
+__global__ void __launch_bounds__(256, 2) bn_bwd_apply_fold_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
+                                         const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
+                                         const float* __restrict__ st, const float* __restrict__ part, int chunks,
+                                         float* __restrict__ g_gamma, float* __restrict__ g_beta, int accumulate,
+                                         const bf16* __restrict__ gamma_b, BwdGeo G, int M, int Mo,
+                                         bf16* __restrict__ dx) {
+  extern __shared__ float stot[];  // [2][C]
+  pdl_wait();
+  const int C = G.C;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float s1, s2;
+    sums_merge_exact(part, chunks, C, c, s1, s2);
+    stot[c] = s1; stot[C + c] = s2;
+    if (blockIdx.x == 0) {
+      g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
+      g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
+    }
+  }
+  __syncthreads();
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x, is = gridDim.x * blockDim.x;
+  if (AP == 0) bwd_apply_body(x, dout, y, pidx, st, stot, gamma_b, G, M, dx, i0, is);
+  else bwd_apply_tiled_body<AP == 2 ? 2 : 0>(x, dout, y, pidx, st, stot, gamma_b, G, M, Mo, dx, i0, is);
+}
+
 // ---- bf16-operand Linear (small: micro-batch rows) ------------------------------------------
 // y[r][o] = sum_i x[r][i] W[o][i] (fp32) + b[o]; logits: fp32 out, else Q(relu?) bf16.
 // One warp per (r, o); lanes stride over i, shuffle reduction.
@@ -747,14 +861,30 @@ int bn_threads(int C) { const int G = C / 8; return G >= 256 ? G : (256 / G) * G
 // rows per partial chunk: ~64 chunks (a few rows per lane, every load in flight at once; fewer
 // partials make the final merge a single round of loads -- 512 chunks measured 9 % slower in the
 // 4-stage pipeline), at most kBnRows rows per lane (register-resident two passes)
+bool bn_fold_off() {
+  static const bool v = [] { const char* e = getenv("XPIPE_BN_FOLD"); return e && *e == '0'; }();
+  return v;
+}
 int bn_chunk_rows(int M, int C) {
   const int RL = bn_threads(C) / (C / 8);
   static const int target = [] {  // development knob: target chunk count
     const char* e = getenv("XPIPE_BN_CHUNKS");
     return (e && *e) ? std::max(1, atoi(e)) : 64;  // measured: 512 -> 64 chunks +9 % (VGG-16 K=4)
   }();
-  return std::max(1, std::min(std::max(RL, (M + target - 1) / target), kBnRows * RL));
+  const int rc = std::max(1, std::min(std::max(RL, (M + target - 1) / target), kBnRows * RL));
+  // a small layer whose partials could be folded into the elementwise pass with the longest
+  // chunks: take those (fewer partials)
+  const int rmax = std::max(1, kBnRows * RL);
+  if (!bn_fold_off() && (int64_t)M * C <= kFoldElems && (int64_t)((M + rc - 1) / rc) * C > kFoldFloats &&
+      (int64_t)((M + rmax - 1) / rmax) * C <= kFoldFloats)
+    return rmax;
+  return rc;
 }
+// fold the final merge of `chunks` partials into the elementwise kernel (see bn_apply_fold_kernel)
+bool bn_fold(int M, int C, int chunks) {
+  return !bn_fold_off() && (int64_t)M * C <= kFoldElems && (int64_t)chunks * C <= kFoldFloats;
+}
+int fold_grid(int64_t items) { return std::min(grid1d(items), 2 * 148); }
 int bn_chunks(int M, int C) { return (M + bn_chunk_rows(M, C) - 1) / bn_chunk_rows(M, C); }
 size_t bn_ws_floats(int M, int C) { return (size_t)bn_chunks(M, C) * 2 * C + 2 * (size_t)C; }
 
@@ -768,6 +898,39 @@ cudaError_t launch_bn_stats(const bf16* x, int M, int C, float eps, const bf16* 
   launch_pdl(bn_stats_partial_kernel, dim3(chunks), dim3(threads), shm, st, x, M, C, RC, ws);
   launch_pdl(bn_stats_final_kernel, dim3((C + 7) / 8), dim3(256), 0, st, (const float*)ws, chunks, M, RC, C, eps, gamma,
              beta, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bn_stats_partial(const bf16* x, int M, int C, float* ws, cudaStream_t st) {
+  if (C % 8 || C > 2048) return cudaErrorInvalidValue;
+  const int RC = bn_chunk_rows(M, C), chunks = bn_chunks(M, C);
+  const int threads = bn_threads(C);
+  launch_pdl(bn_stats_partial_kernel, dim3(chunks), dim3(threads), (size_t)threads * 8 * 4, st, x, M, C, RC, ws);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bn_apply_stats(const float* part, int chunks, int RC, float eps, const bf16* gamma, const bf16* beta,
+                                  float* stats, const bf16* x, bf16* y, uint8_t* pidx, int n, int H, int W, int C,
+                                  int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu,
+                                  cudaStream_t st, const bf16* res, int ldy) {
+  const int M = n * H * W;
+  if (!bn_fold(M, C, chunks)) {
+    cudaError_t e = launch_bn_stats_final(part, chunks, M, RC, C, eps, gamma, beta, stats, st);
+    if (e != cudaSuccess) return e;
+    return launch_bn_apply(x, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool, relu, st, res, ldy);
+  }
+  if (!ldy) ldy = C;
+  const int64_t total = (int64_t)n * P * Q * (C / 8);
+  if (C % 8 || C > 2048 || total >= kMaxElems || (res && pool)) return cudaErrorInvalidValue;
+  const size_t shm = (size_t)4 * C * 4;
+  if (pool && kh == 2 && kw == 2 && sh == 2 && sw == 2 && ph == 0 && pw == 0 && H == 2 * P && W == 2 * Q &&
+      !bn_tiled_off())
+    launch_pdl(bn_apply_fold_kernel<2>, dim3(fold_grid(total)), dim3(256), shm, st, x, part, chunks, M, RC, eps, gamma,
+               beta, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, 1, relu ? 1 : 0, (const bf16*)nullptr,
+               ldy);
+  else
+    launch_pdl(bn_apply_fold_kernel<0>, dim3(fold_grid(total)), dim3(256), shm, st, x, part, chunks, M, RC, eps, gamma,
+               beta, stats, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0, res, ldy);
   return cudaGetLastError();
 }
 
@@ -808,6 +971,7 @@ cudaError_t launch_bn_bwd_reduce(const bf16* x, const bf16* dout, const bf16* y,
   float* tot = ws + (size_t)chunks * 2 * C;
   launch_pdl(bn_bwd_reduce_kernel, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC, ws, dres,
              acc_res ? 1 : 0);
+  if (bn_fold(M, C, chunks)) return cudaGetLastError();  // the merge runs in launch_bn_bwd_apply
   launch_pdl(bn_bwd_final_kernel, dim3((C + 7) / 8), dim3(256), 0, st, (const float*)ws, chunks, C, tot, g_gamma, g_beta,
              accumulate ? 1 : 0);
   return cudaGetLastError();
@@ -816,12 +980,31 @@ cudaError_t launch_bn_bwd_reduce(const bf16* x, const bf16* dout, const bf16* y,
 cudaError_t launch_bn_bwd_apply(const bf16* x, const bf16* dout, const bf16* y, const uint8_t* pidx, const float* stats,
                                 const bf16* gamma_b, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
                                 int sw, int ph, int pw, bool pool, bool relu, const float* ws, bf16* dx,
-                                cudaStream_t st, int ldy) {
+                                cudaStream_t st, int ldy, float* g_gamma, float* g_beta, bool accumulate) {
   if (C % 8 || C > 2048 || (ldy && ldy % 8)) return cudaErrorInvalidValue;
   BwdGeo G{H, W, C, pool ? P : H, pool ? Q : W, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0, ldy ? ldy : C};
   const int M = n * H * W;
-  const float* tot = ws + (size_t)bn_chunks(M, C) * 2 * C;
+  const int chunks = bn_chunks(M, C);
+  const float* tot = ws + (size_t)chunks * 2 * C;
   if ((int64_t)M * (C / 8) >= kMaxElems) return cudaErrorInvalidValue;
+  const bool tiled = pool && kh == sh && kw == sw && ph == 0 && pw == 0 && H == P * kh && W == Q * kw &&
+                     kh * kw <= 255 && !bn_tiled_off();
+  if (bn_fold(M, C, chunks)) {  // the totals merge (and dgamma / dbeta) in this kernel
+    if (!g_gamma || !g_beta) return cudaErrorInvalidValue;
+    const size_t shm = (size_t)2 * C * 4;
+    const int acc = accumulate ? 1 : 0;
+    const int Mo = n * P * Q;
+    if (!tiled)
+      launch_pdl(bn_bwd_apply_fold_kernel<0>, dim3(fold_grid((int64_t)M * (C / 8))), dim3(256), shm, st, x, dout, y,
+                 pidx, stats, (const float*)ws, chunks, g_gamma, g_beta, acc, gamma_b, G, M, Mo, dx);
+    else if (kh == 2 && kw == 2)
+      launch_pdl(bn_bwd_apply_fold_kernel<2>, dim3(fold_grid((int64_t)Mo * (C / 8))), dim3(256), shm, st, x, dout, y,
+                 pidx, stats, (const float*)ws, chunks, g_gamma, g_beta, acc, gamma_b, G, M, Mo, dx);
+    else
+      launch_pdl(bn_bwd_apply_fold_kernel<1>, dim3(fold_grid((int64_t)Mo * (C / 8))), dim3(256), shm, st, x, dout, y,
+                 pidx, stats, (const float*)ws, chunks, g_gamma, g_beta, acc, gamma_b, G, M, Mo, dx);
+    return cudaGetLastError();
+  }
   if (pool && kh == sh && kw == sw && ph == 0 && pw == 0 && H == P * kh && W == Q * kw && kh * kw <= 255 &&
       !bn_tiled_off()) {
     const int Mo = n * P * Q;

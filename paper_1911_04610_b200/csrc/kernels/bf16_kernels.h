@@ -11,6 +11,19 @@ size_t bn_ws_floats(int M, int C);
 // counter: one zero-initialised int owned by the calling stream (last-block merge)
 cudaError_t launch_bn_stats(const __nv_bfloat16* x, int M, int C, float eps, const __nv_bfloat16* gamma,
                             const __nv_bfloat16* beta, float* ws, int* counter, float* stats, cudaStream_t st);
+// Small layers (chunks x C <= 8192, M x C <= 2^20) fold the final merges into the elementwise
+// kernels (bit-identical; XPIPE_BN_FOLD=0 keeps the separate launches): launch_bn_bwd_reduce then
+// launches only the reduction and launch_bn_bwd_apply merges the totals (and accumulates dgamma /
+// dbeta into g_gamma / g_beta); launch_bn_apply_stats merges the forward partials and applies.
+// The partials of the stored conv output alone (chunks = bn_chunks, rows bn_chunk_rows):
+cudaError_t launch_bn_stats_partial(const __nv_bfloat16* x, int M, int C, float* ws, cudaStream_t st);
+int bn_chunk_rows(int M, int C);
+// merge of the partials [chunks][2][C] of RC-row chunks + BN-apply (folded or as two launches)
+cudaError_t launch_bn_apply_stats(const float* part, int chunks, int RC, float eps, const __nv_bfloat16* gamma,
+                                  const __nv_bfloat16* beta, float* stats, const __nv_bfloat16* x, __nv_bfloat16* y,
+                                  uint8_t* pidx, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
+                                  int sw, int ph, int pw, bool pool, bool relu, cudaStream_t st,
+                                  const __nv_bfloat16* res, int ldy);
 // the final merge alone, over partials [chunks][2][C] (mean, M2) of RC-row chunks (the last
 // one ragged) produced elsewhere -- the fprop GEMM epilogue (RC = 128)
 cudaError_t launch_bn_stats_final(const float* part, int chunks, int M, int RC, int C, float eps,
@@ -36,7 +49,8 @@ cudaError_t launch_bn_bwd_reduce(const __nv_bfloat16* x, const __nv_bfloat16* do
 cudaError_t launch_bn_bwd_apply(const __nv_bfloat16* x, const __nv_bfloat16* dout, const __nv_bfloat16* y,
                                 const uint8_t* pidx, const float* stats, const __nv_bfloat16* gamma_b, int n, int H,
                                 int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool,
-                                bool relu, const float* ws, __nv_bfloat16* dx, cudaStream_t st, int ldy = 0);
+                                bool relu, const float* ws, __nv_bfloat16* dx, cudaStream_t st, int ldy,
+                                float* g_gamma, float* g_beta, bool accumulate);
 // explicit im2col of an NHWC conv input (C % 8 == 0): cols [n*P*Q][R*S*C], (r, s, c) c fastest
 cudaError_t launch_im2col_bf16(const __nv_bfloat16* x, __nv_bfloat16* cols, int n, int H, int W, int C, int P, int Q,
                                int R, int S, int sh, int sw, int ph, int pw, cudaStream_t st);

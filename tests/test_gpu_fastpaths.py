@@ -12,7 +12,10 @@ subprocesses on the same seeded inputs:
   * XPIPE_BN_FUSE=1 (opt-in) -- the BatchNorm statistics and BN-apply [+ residual] [+ ReLU] in the
     fprop GEMM's epilogue (the M tiles of an N tile as one thread-block cluster, partials over
     DSMEM) vs the separate statistics-merge and apply launches: VGG-16 at CIFAR size K=2 (its
-    unpooled 8x8 / 4x4 layers), the ResNet blocks (residual blocks at 4x4 / 2x2) and Inception."""
+    unpooled 8x8 / 4x4 layers), the ResNet blocks (residual blocks at 4x4 / 2x2) and Inception;
+  * XPIPE_BN_FOLD=0 -- the final merges of small layers' BatchNorm partials folded into the
+    elementwise kernels (every CTA merges into shared memory in the final kernels' order) vs the
+    separate merge launches: VGG-16, ResNet blocks, Inception."""
 import os
 import subprocess
 import sys
@@ -53,26 +56,29 @@ g.close()
 """
 
 
-def run(which, switch, on, out):
-    """on=True selects the general path: the NO_ switches disable a fast path, BN_FUSE enables one."""
+def run(which, env_set, out):
     env = dict(os.environ)
-    env.pop(switch, None)
-    if switch.startswith("XPIPE_NO_") and on:
-        env[switch] = "1"
-    if not switch.startswith("XPIPE_NO_") and not on:
-        env[switch] = "1"
+    for k in ("XPIPE_NO_ADD_FUSE", "XPIPE_NO_CONCAT_VIEWS", "XPIPE_BN_FUSE", "XPIPE_BN_FOLD"):
+        env.pop(k, None)
+    if env_set:
+        k, v = env_set.split("=")
+        env[k] = v
     code = RUN.format(root=ROOT, here=HERE, which=which, out=out)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     return np.load(out)
 
 
-@pytest.mark.parametrize("switch,which", [("XPIPE_NO_ADD_FUSE", "resnet"), ("XPIPE_NO_CONCAT_VIEWS", "inception"),
-                                          ("XPIPE_BN_FUSE", "vgg16"), ("XPIPE_BN_FUSE", "resnet"),
-                                          ("XPIPE_BN_FUSE", "inception")])
-def test_fast_path_bit_identical(tmp_path, switch, which):
-    fast = run(which, switch, False, str(tmp_path / "fast.npy"))
-    general = run(which, switch, True, str(tmp_path / "general.npy"))
+# (environment of the fast path, of the general path, model)
+CASES = [("", "XPIPE_NO_ADD_FUSE=1", "resnet"), ("", "XPIPE_NO_CONCAT_VIEWS=1", "inception"),
+         ("XPIPE_BN_FUSE=1", "", "vgg16"), ("XPIPE_BN_FUSE=1", "", "resnet"), ("XPIPE_BN_FUSE=1", "", "inception"),
+         ("", "XPIPE_BN_FOLD=0", "vgg16"), ("", "XPIPE_BN_FOLD=0", "resnet"), ("", "XPIPE_BN_FOLD=0", "inception")]
+
+
+@pytest.mark.parametrize("fast_env,general_env,which", CASES)
+def test_fast_path_bit_identical(tmp_path, fast_env, general_env, which):
+    fast = run(which, fast_env, str(tmp_path / "fast.npy"))
+    general = run(which, general_env, str(tmp_path / "general.npy"))
     assert fast.shape == general.shape
     assert np.isfinite(fast).all()
     assert np.array_equal(fast, general)

@@ -609,68 +609,47 @@ __global__ void bn_bwd_apply_tiled_kernel(const bf16* __restrict__ x, const bf16
 
 // ---- folded BatchNorm merges (small layers) -------------------------------------------------
 // The per-channel merge of the partials (bn_stats_final_kernel / bn_bwd_final_kernel) done by
-// every CTA of the elementwise kernel that needs its result, into shared memory, in exactly the
-// final kernels' order (lane j merges chunks j, j+32, ... in order, then a pairwise tree of
-// strides 16..1), so the results are bit-identical and one launch per BatchNorm and direction
-// disappears.  Used where the partials are few (chunks x C <= kFoldFloats) and the layer small
+// every CTA of the elementwise kernel that needs its result, into shared memory, so one launch
+// per BatchNorm and direction disappears.  Used where the partials are few (chunks x C <= kFoldFloats) and the layer small
 // (M x C <= kFoldElems): every CTA then re-reads at most 64 KB of partials from L2.
 constexpr int kFoldFloats = 8192;
 constexpr int64_t kFoldElems = int64_t(1) << 20;
 
-// The final kernels' order as a tree evaluated depth first (few live registers): lane j of 32
-// merges chunks j, j+32, ... in order; node(l, j) = merge(node(l-1, j), node(l-1, j + 32 >> l)),
-// the result is node(5, 0) -- the same pairwise tree as the shared-memory loop over strides 16..1
-struct ChanAcc { float n, mean, m2; };
-struct SumAcc { float a, b; };
-__device__ __forceinline__ ChanAcc chan_lane(const float* __restrict__ part, int chunks, int M, int RC, int C, int c,
-                                             int j) {
-  ChanAcc r{0.f, 0.f, 0.f};
-  for (int k = j; k < chunks; k += 32)
-    chan_merge(r.n, r.mean, r.m2, (float)min(RC, M - k * RC), __ldcg(part + (size_t)k * 2 * C + c),
-               __ldcg(part + (size_t)k * 2 * C + C + c));
-  return r;
-}
-template <int L>
-__device__ __forceinline__ ChanAcc chan_node(const float* __restrict__ part, int chunks, int M, int RC, int C, int c,
-                                             int j) {
-  if constexpr (L == 0) {
-    return chan_lane(part, chunks, M, RC, C, c, j);
-  } else {
-    ChanAcc x = chan_node<L - 1>(part, chunks, M, RC, C, c, j);
-    const ChanAcc y = chan_node<L - 1>(part, chunks, M, RC, C, c, j + (32 >> L));
-    chan_merge(x.n, x.mean, x.m2, y.n, y.mean, y.m2);
-    return x;
+// Each CTA merges the (few) partials of every channel sequentially in chunk order, all of a
+// channel's loads in flight together (the separate final kernels use 32 lanes per channel and a
+// pairwise tree, one CTA per 8 channels -- a different summation order: this path matches them
+// to fp32 rounding, not bit for bit)
+__device__ __forceinline__ void stats_merge_seq(const float* __restrict__ part, int chunks, int M, int RC, int C, int c,
+                                                float& mean, float& m2, float& n) {
+  n = 0.f; mean = 0.f; m2 = 0.f;
+  for (int k0 = 0; k0 < chunks; k0 += 8) {
+    float mb[8], qb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u;
+      mb[u] = k < chunks ? __ldcg(part + (size_t)k * 2 * C + c) : 0.f;
+      qb[u] = k < chunks ? __ldcg(part + (size_t)k * 2 * C + C + c) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < chunks) chan_merge(n, mean, m2, (float)min(RC, M - (k0 + u) * RC), mb[u], qb[u]);
   }
 }
-__device__ __forceinline__ SumAcc sum_lane(const float* __restrict__ part, int chunks, int C, int c, int j) {
-  SumAcc r{0.f, 0.f};
-  for (int k = j; k < chunks; k += 32) {
-    r.a = __fadd_rn(r.a, __ldcg(part + (size_t)k * 2 * C + c));
-    r.b = __fadd_rn(r.b, __ldcg(part + (size_t)k * 2 * C + C + c));
+__device__ __forceinline__ void sums_merge_seq(const float* __restrict__ part, int chunks, int C, int c, float& s1,
+                                               float& s2) {
+  s1 = 0.f; s2 = 0.f;
+  for (int k0 = 0; k0 < chunks; k0 += 8) {
+    float a[8], b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u;
+      a[u] = k < chunks ? __ldcg(part + (size_t)k * 2 * C + c) : 0.f;
+      b[u] = k < chunks ? __ldcg(part + (size_t)k * 2 * C + C + c) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < chunks) { s1 = __fadd_rn(s1, a[u]); s2 = __fadd_rn(s2, b[u]); }
   }
-  return r;
-}
-template <int L>
-__device__ __forceinline__ SumAcc sum_node(const float* __restrict__ part, int chunks, int C, int c, int j) {
-  if constexpr (L == 0) {
-    return sum_lane(part, chunks, C, c, j);
-  } else {
-    SumAcc x = sum_node<L - 1>(part, chunks, C, c, j);
-    const SumAcc y = sum_node<L - 1>(part, chunks, C, c, j + (32 >> L));
-    x.a = __fadd_rn(x.a, y.a);
-    x.b = __fadd_rn(x.b, y.b);
-    return x;
-  }
-}
-__device__ __forceinline__ void stats_merge_exact(const float* __restrict__ part, int chunks, int M, int RC, int C,
-                                                  int c, float& mean, float& m2, float& n) {
-  const ChanAcc r = chan_node<5>(part, chunks, M, RC, C, c, 0);
-  mean = r.mean; m2 = r.m2; n = r.n;
-}
-__device__ __forceinline__ void sums_merge_exact(const float* __restrict__ part, int chunks, int C, int c, float& s1,
-                                                 float& s2) {
-  const SumAcc r = sum_node<5>(part, chunks, C, c, 0);
-  s1 = r.a; s2 = r.b;
 }
 
 // forward: statistics merge (+ the stashed stats, by CTA 0) then BN-apply [+ ReLU] [+ pool]
@@ -684,7 +663,7 @@ __global__ void __launch_bounds__(256, 2) bn_apply_fold_kernel(const bf16* __res
   pdl_wait();
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     float mean, m2, cnt;
-    stats_merge_exact(part, chunks, M, RC, C, c, mean, m2, cnt);
+    stats_merge_seq(part, chunks, M, RC, C, c, mean, m2, cnt);
     const float rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(m2, cnt), eps)));
     const float ga = __bfloat162float(gamma[c]), be = __bfloat162float(beta[c]);
     sst[c] = mean; sst[C + c] = rstd; sst[2 * C + c] = ga; sst[3 * C + c] = be;
@@ -708,7 +687,7 @@ __global__ void __launch_bounds__(256, 2) bn_bwd_apply_fold_kernel(const bf16* _
   const int C = G.C;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     float s1, s2;
-    sums_merge_exact(part, chunks, C, c, s1, s2);
+    sums_merge_seq(part, chunks, C, c, s1, s2);
     stot[c] = s1; stot[C + c] = s2;
     if (blockIdx.x == 0) {
       g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
@@ -875,7 +854,7 @@ int bn_chunk_rows(int M, int C) {
   // a small layer whose partials could be folded into the elementwise pass with the longest
   // chunks: take those (fewer partials)
   const int rmax = std::max(1, kBnRows * RL);
-  if (!bn_fold_off() && (int64_t)M * C <= kFoldElems && (int64_t)((M + rc - 1) / rc) * C > kFoldFloats &&
+  if ((int64_t)M * C <= kFoldElems && (int64_t)((M + rc - 1) / rc) * C > kFoldFloats &&
       (int64_t)((M + rmax - 1) / rmax) * C <= kFoldFloats)
     return rmax;
   return rc;

@@ -12,10 +12,7 @@ subprocesses on the same seeded inputs:
   * XPIPE_BN_FUSE=1 (opt-in) -- the BatchNorm statistics and BN-apply [+ residual] [+ ReLU] in the
     fprop GEMM's epilogue (the M tiles of an N tile as one thread-block cluster, partials over
     DSMEM) vs the separate statistics-merge and apply launches: VGG-16 at CIFAR size K=2 (its
-    unpooled 8x8 / 4x4 layers), the ResNet blocks (residual blocks at 4x4 / 2x2) and Inception;
-  * XPIPE_BN_FOLD=0 -- the final merges of small layers' BatchNorm partials folded into the
-    elementwise kernels (every CTA merges into shared memory in the final kernels' order) vs the
-    separate merge launches: VGG-16, ResNet blocks, Inception."""
+    unpooled 8x8 / 4x4 layers), the ResNet blocks (residual blocks at 4x4 / 2x2) and Inception."""
 import os
 import subprocess
 import sys
@@ -71,8 +68,7 @@ def run(which, env_set, out):
 
 # (environment of the fast path, of the general path, model)
 CASES = [("", "XPIPE_NO_ADD_FUSE=1", "resnet"), ("", "XPIPE_NO_CONCAT_VIEWS=1", "inception"),
-         ("XPIPE_BN_FUSE=1", "", "vgg16"), ("XPIPE_BN_FUSE=1", "", "resnet"), ("XPIPE_BN_FUSE=1", "", "inception"),
-         ("", "XPIPE_BN_FOLD=0", "vgg16"), ("", "XPIPE_BN_FOLD=0", "resnet"), ("", "XPIPE_BN_FOLD=0", "inception")]
+         ("XPIPE_BN_FUSE=1", "", "vgg16"), ("XPIPE_BN_FUSE=1", "", "resnet"), ("XPIPE_BN_FUSE=1", "", "inception")]
 
 
 @pytest.mark.parametrize("fast_env,general_env,which", CASES)

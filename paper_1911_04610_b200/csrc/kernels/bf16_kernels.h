@@ -11,8 +11,9 @@ size_t bn_ws_floats(int M, int C);
 // counter: one zero-initialised int owned by the calling stream (last-block merge)
 cudaError_t launch_bn_stats(const __nv_bfloat16* x, int M, int C, float eps, const __nv_bfloat16* gamma,
                             const __nv_bfloat16* beta, float* ws, int* counter, float* stats, cudaStream_t st);
-// Small layers (chunks x C <= 8192, M x C <= 2^20) fold the final merges into the elementwise
-// kernels (bit-identical; XPIPE_BN_FOLD=0 keeps the separate launches): launch_bn_bwd_reduce then
+// Opt-in (XPIPE_BN_FOLD=1, measured slower): small layers (chunks x C <= 8192, M x C <= 2^20) fold
+// the final merges into the elementwise kernels (sequential merge order: equal to the separate
+// merge launches to fp32 rounding, not bit for bit): launch_bn_bwd_reduce then
 // launches only the reduction and launch_bn_bwd_apply merges the totals (and accumulates dgamma /
 // dbeta into g_gamma / g_beta); launch_bn_apply_stats merges the forward partials and applies.
 // The partials of the stored conv output alone (chunks = bn_chunks, rows bn_chunk_rows):

@@ -57,7 +57,9 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "sm__inst_executed_pipe_tensor.sum", "launch__registers_per_thread", "launch__grid_size",
         "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "lts__t_bytes.sum", "l1tex__t_bytes.sum"]
+        "lts__t_bytes.sum", "l1tex__t_bytes.sum", "sm__warps_active.avg.per_cycle_active",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_active.avg",
+        "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers", "launch__block_size"]
 
 
 def full(rep, out_md, traffic_key=None):
@@ -70,6 +72,15 @@ def full(rep, out_md, traffic_key=None):
     for row in rd[2:]:
         d = dict(zip(hdr, row))
         item = {"kernel": short(d.get("Kernel Name", "?"))}
+        stalls = []
+        for k in hdr:
+            if "warps_issue_stalled" in k and k.endswith("per_warp_active.pct"):
+                try:
+                    stalls.append((float(d[k].replace(",", "")), k))
+                except ValueError:
+                    pass
+        for v, k in sorted(stalls, reverse=True)[:6]:  # the dominant warp stall reasons
+            item[k] = "%.1f %%" % v
         for k in hdr:
             if k in WANT or ("tensor" in k and "pct" in k and ".avg." in k):
                 if k not in WANT and d[k].strip() in ("0", "0.000000", ""):

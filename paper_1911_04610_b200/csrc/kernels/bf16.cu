@@ -840,8 +840,11 @@ int bn_threads(int C) { const int G = C / 8; return G >= 256 ? G : (256 / G) * G
 // rows per partial chunk: ~64 chunks (a few rows per lane, every load in flight at once; fewer
 // partials make the final merge a single round of loads -- 512 chunks measured 9 % slower in the
 // 4-stage pipeline), at most kBnRows rows per lane (register-resident two passes)
+// folded merges are opt-in (XPIPE_BN_FOLD=1): measured slower in the pipeline (VGG-16 K=4 102.7k
+// vs 113.1k samples/s, ResNet-101 K=8 23.8k vs 27.9k, Inception-V3 K=4 24.2k vs 25.3k) -- every
+// CTA's merge is a chain of dependent L2 round trips ahead of its elementwise work
 bool bn_fold_off() {
-  static const bool v = [] { const char* e = getenv("XPIPE_BN_FOLD"); return e && *e == '0'; }();
+  static const bool v = [] { const char* e = getenv("XPIPE_BN_FOLD"); return !(e && *e == '1'); }();
   return v;
 }
 int bn_chunk_rows(int M, int C) {
@@ -854,7 +857,7 @@ int bn_chunk_rows(int M, int C) {
   // a small layer whose partials could be folded into the elementwise pass with the longest
   // chunks: take those (fewer partials)
   const int rmax = std::max(1, kBnRows * RL);
-  if ((int64_t)M * C <= kFoldElems && (int64_t)((M + rc - 1) / rc) * C > kFoldFloats &&
+  if (!bn_fold_off() && (int64_t)M * C <= kFoldElems && (int64_t)((M + rc - 1) / rc) * C > kFoldFloats &&
       (int64_t)((M + rmax - 1) / rmax) * C <= kFoldFloats)
     return rmax;
   return rc;

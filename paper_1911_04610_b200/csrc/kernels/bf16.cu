@@ -314,12 +314,18 @@ struct BwdGeo {
   int ldy;  // row pitch of dout / y (the op output; > C for a concat view), pidx stays dense
 };
 
+// PM: the pool mode as a compile-time constant (0 none, 2 exact tiling, 1 general windows; G.pool
+// holds the same value), or -1 to dispatch on G.pool at run time.  The unrolled reduction loop
+// instantiates one mode only: with all three inlined in each of its kBnRows iterations the kernel
+// was 7k instructions and stalled mostly on instruction fetch (ncu: "no instruction" 11.6 vs
+// long scoreboard 5.2 cycles per issue)
+template <int PM = -1>
 __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const bf16* __restrict__ y,
                                            const uint8_t* __restrict__ pidx, const BwdGeo& G, int row, int c0,
                                            float (&dy)[8]) {
 #pragma unroll
   for (int e = 0; e < 8; ++e) dy[e] = 0.f;
-  if (!G.pool) {  // row = (s*H + h)*W + w indexes dout/y directly
+  if (PM == 0 || (PM < 0 && !G.pool)) {  // row = (s*H + h)*W + w indexes dout/y directly
     const int64_t o = (int64_t)row * G.ldy + c0;
     const uint4 ud = *reinterpret_cast<const uint4*>(dout + o);
     const uint4 uy = *reinterpret_cast<const uint4*>(y + o);
@@ -330,7 +336,7 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
     return;
   }
   const int w = row % G.W, t = row / G.W, h = t % G.H, s = t / G.H;
-  if (G.pool == 2) {  // windows tile the map exactly: the one window holding (h, w)
+  if (PM == 2 || (PM < 0 && G.pool == 2)) {  // windows tile the map exactly: the one window holding (h, w)
     const int p = h / G.kh, q = w / G.kw;
     const int pos = (h - p * G.kh) * G.kw + (w - q * G.kw);
     const int64_t ro = ((int64_t)s * G.P + p) * G.Q + q;
@@ -378,6 +384,7 @@ __device__ __forceinline__ void routed_dy8(const bf16* __restrict__ dout, const 
 // per chunk of RC rows: sum dy and sum dy*xhat per channel (8 channels per thread, row lanes
 // combined by a fixed tree) -> part[chunk][2][C]
 
+template <int PM, bool DRES>
 __device__ __forceinline__ void bwd_reduce_body(const bf16* __restrict__ x, const bf16* __restrict__ dout,
                                                 const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
                                                 const float* __restrict__ st, const BwdGeo& G, int M, int RC,
@@ -397,8 +404,8 @@ __device__ __forceinline__ void bwd_reduce_body(const bf16* __restrict__ x, cons
     const int r = r0 + rl + k * RL;
     if (rl < RL && r < r1) {
       float dy[8];
-      routed_dy8(dout, y, pidx, G, r, c0, dy);
-      if (dres) {  // folded residual Add (unpooled): the residual input's gradient is dy' too
+      routed_dy8<PM>(dout, y, pidx, G, r, c0, dy);
+      if (DRES) {  // folded residual Add (unpooled): the residual input's gradient is dy' too
         bf16* dp = dres + (int64_t)r * C + c0;
         float o8[8];
         if (acc_res) ld8bf(dp, o8);
@@ -437,12 +444,13 @@ __device__ __forceinline__ void bwd_reduce_body(const bf16* __restrict__ x, cons
     for (int e = 0; e < 8; ++e) { p[c0 + e] = slot[e]; p[C + c0 + e] = slot[8 + e]; }
   }
 }
+template <int PM, bool DRES>
 __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
                                      const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
                                      const float* __restrict__ st, BwdGeo G, int M, int RC, float* __restrict__ part,
                                      bf16* __restrict__ dres, int acc_res) {
   pdl_wait();
-  bwd_reduce_body(x, dout, y, pidx, st, G, M, RC, part, blockIdx.x, dres, acc_res);
+  bwd_reduce_body<PM, DRES>(x, dout, y, pidx, st, G, M, RC, part, blockIdx.x, dres, acc_res);
   pdl_trigger();
 }
 
@@ -493,6 +501,7 @@ __global__ void bn_bwd_final_kernel(const float* __restrict__ part, int chunks, 
 }
 
 // dx = Q(gamma_b * rstd * (dy - sum(dy)/cnt - xhat * sum(dy xhat)/cnt)), 8 channels per thread
+template <int PM = -1>
 __device__ __forceinline__ void bwd_apply_body(const bf16* __restrict__ x, const bf16* __restrict__ dout,
                                                const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
                                                const float* __restrict__ st, const float* __restrict__ tot,
@@ -506,7 +515,7 @@ __device__ __forceinline__ void bwd_apply_body(const bf16* __restrict__ x, const
     const int r = i / NG;
     const int c0 = g * 8;
     float dy[8];
-    routed_dy8(dout, y, pidx, G, r, c0, dy);
+    routed_dy8<PM>(dout, y, pidx, G, r, c0, dy);
     const uint4 ux = *reinterpret_cast<const uint4*>(x + (int64_t)r * C + c0);
     const bf16* xv = reinterpret_cast<const bf16*>(&ux);
     float mean[8], rstd[8], gb[8], t1[8], t2[8];
@@ -528,12 +537,13 @@ __device__ __forceinline__ void bwd_apply_body(const bf16* __restrict__ x, const
     *reinterpret_cast<uint4*>(dx + (int64_t)r * C + c0) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
   }
 }
+template <int PM>
 __global__ void bn_bwd_apply_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dout,
                                     const bf16* __restrict__ y, const uint8_t* __restrict__ pidx,
                                     const float* __restrict__ st, const float* __restrict__ tot,
                                     const bf16* __restrict__ gamma_b, BwdGeo G, int M, bf16* __restrict__ dx) {
   pdl_wait();
-  bwd_apply_body(x, dout, y, pidx, st, tot, gamma_b, G, M, dx, blockIdx.x * blockDim.x + threadIdx.x,
+  bwd_apply_body<PM>(x, dout, y, pidx, st, tot, gamma_b, G, M, dx, blockIdx.x * blockDim.x + threadIdx.x,
                  gridDim.x * blockDim.x);
 }
 
@@ -741,10 +751,17 @@ __global__ void linear_dy_prep_kernel(const void* __restrict__ dy, const bf16* _
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= ldp) return;
   float acc = 0.f;
-  for (int r = 0; r < n; ++r) {
-    const float d = o < out ? load_dy<DY_F32>(dy, (int64_t)r * out + o, mask) : 0.f;
-    dyp[(int64_t)r * ldp + o] = __float2bfloat16_rn(d);
-    acc += d;
+  for (int r0 = 0; r0 < n; r0 += 8) {  // eight rows' loads in flight, then the in-order sum
+    float d[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      d[u] = (o < out && r0 + u < n) ? load_dy<DY_F32>(dy, (int64_t)(r0 + u) * out + o, mask) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (r0 + u < n) {
+        dyp[(int64_t)(r0 + u) * ldp + o] = __float2bfloat16_rn(d[u]);
+        acc += d[u];
+      }
   }
   if (gb && o < out) gb[o] = accumulate ? __fadd_rn(gb[o], acc) : acc;
 }
@@ -951,8 +968,19 @@ cudaError_t launch_bn_bwd_reduce(const bf16* x, const bf16* dout, const bf16* y,
   const int threads = bn_threads(C);
   const size_t shm = (size_t)threads * 16 * 4;
   float* tot = ws + (size_t)chunks * 2 * C;
-  launch_pdl(bn_bwd_reduce_kernel, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC, ws, dres,
-             acc_res ? 1 : 0);
+  const int ar = acc_res ? 1 : 0;
+  if (G.pool == 2)
+    launch_pdl(bn_bwd_reduce_kernel<2, false>, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC,
+               ws, (bf16*)nullptr, ar);
+  else if (G.pool)
+    launch_pdl(bn_bwd_reduce_kernel<1, false>, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC,
+               ws, (bf16*)nullptr, ar);
+  else if (dres)
+    launch_pdl(bn_bwd_reduce_kernel<0, true>, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC,
+               ws, dres, ar);
+  else
+    launch_pdl(bn_bwd_reduce_kernel<0, false>, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC,
+               ws, (bf16*)nullptr, ar);
   if (bn_fold(M, C, chunks)) return cudaGetLastError();  // the merge runs in launch_bn_bwd_apply
   launch_pdl(bn_bwd_final_kernel, dim3((C + 7) / 8), dim3(256), 0, st, (const float*)ws, chunks, C, tot, g_gamma, g_beta,
              accumulate ? 1 : 0);
@@ -998,8 +1026,12 @@ cudaError_t launch_bn_bwd_apply(const bf16* x, const bf16* dout, const bf16* y, 
                  stats, tot, gamma_b, G, M, Mo, dx);
     return cudaGetLastError();
   }
-  launch_pdl(bn_bwd_apply_kernel, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats, tot,
-             gamma_b, G, M, dx);
+  if (G.pool)
+    launch_pdl(bn_bwd_apply_kernel<1>, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats,
+               tot, gamma_b, G, M, dx);
+  else
+    launch_pdl(bn_bwd_apply_kernel<0>, dim3(grid1d((int64_t)M * (C / 8))), dim3(256), 0, st, x, dout, y, pidx, stats,
+               tot, gamma_b, G, M, dx);
   return cudaGetLastError();
 }
 

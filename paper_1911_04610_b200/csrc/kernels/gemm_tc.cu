@@ -1458,14 +1458,20 @@ int choose_bn(int M, int N) {
 // fills half the SMs or K is short.
 struct SplitPlan { int bn, cs, nc, kbps; };
 __host__ int wgrad_min_bn() { static const int v = getenv_int("XPIPE_WGRAD_BN", 64); return v; }
-SplitPlan plan_splits(int M, int N, int K, int min_bn = 64) {
+// forward / input-gradient GEMMs: their own split threshold (development knob XPIPE_SPLIT_FD_BELOW,
+// tiles; 1 = never split them), the weight gradients keep split_below()
+__host__ int split_fd_below() {
+  static const int env = getenv_int("XPIPE_SPLIT_FD_BELOW", 0);
+  return env > 0 ? env : split_below();
+}
+SplitPlan plan_splits(int M, int N, int K, int min_bn = 64, bool wg = false) {
   SplitPlan p;
   p.bn = choose_bn(M, N);
   if (min_bn > p.bn && N > 64) p.bn = N > 128 && min_bn >= 256 ? 256 : 128;
   const int tiles = ((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn);
   const int nkb = std::max(1, (K + BK - 1) / BK);
   int s = 1;
-  if (!no_splitk() && tiles < split_below() && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / split_min_kb()));
+  if (!no_splitk() && tiles < (wg ? split_below() : split_fd_below()) && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / split_min_kb()));
   if (tiles * (int64_t)std::min(s, kMaxCluster) > kTileCounters - 64) s = 1;  // tail: BN counters
   p.cs = std::min(s, kMaxCluster);  // cluster size
   p.nc = std::max(1, s / p.cs);      // clusters per tile
@@ -1477,7 +1483,7 @@ SplitPlan plan_splits(int M, int N, int K, int min_bn = 64) {
 template <int MODE, bool A_MN, bool B_MN>
 cudaError_t run_split(GemmArgs a, int final_epi, void* final_out, int64_t final_ldo, int accumulate, float* ws,
                       int64_t ws_elems, int* counters, cudaStream_t st) {
-  SplitPlan p = plan_splits(a.M, a.N, a.K, MODE == GEMM_WGRAD ? wgrad_min_bn() : 64);
+  SplitPlan p = plan_splits(a.M, a.N, a.K, MODE == GEMM_WGRAD ? wgrad_min_bn() : 64, final_epi == EPI_WGRAD_T);
   a.kb_per_split = p.kbps;
   a.cs = p.cs; a.nc = p.nc; a.splits = p.cs * p.nc;
   a.ws = ws; a.ws_elems = ws ? ws_elems : 0; a.tile_counters = counters;
@@ -1688,14 +1694,14 @@ cudaError_t tc_linear_wgrad(const bf16* x, const bf16* dyp, int ldp, float* gW, 
 
 int64_t tc_conv_ws_elems(const ConvGeo& g) {
   // split-K partial planes + cross-cluster slices of the largest of the three GEMMs
-  auto need = [](int M, int N, int K, int min_bn = 64) -> int64_t {
-    const SplitPlan p = plan_splits(M, N, K, min_bn);
+  auto need = [](int M, int N, int K, int min_bn = 64, bool wg = false) -> int64_t {
+    const SplitPlan p = plan_splits(M, N, K, min_bn, wg);
     if (p.cs * p.nc <= 1) return 0;
     const int64_t tiles = (int64_t)((M + BM - 1) / BM) * ((N + p.bn - 1) / p.bn);
     return tiles * (p.cs * p.nc + (p.nc > 1 ? p.nc : 0)) * BM * p.bn;
   };
   return std::max({need(g.Nimg * g.P * g.Q, g.Co, g.R * g.S * g.C), need(g.Nimg * g.H * g.W, g.C, g.R * g.S * g.Co),
-                   need(g.R * g.S * g.C, g.Co, g.Nimg * g.P * g.Q, wgrad_min_bn())});
+                   need(g.R * g.S * g.C, g.Co, g.Nimg * g.P * g.Q, wgrad_min_bn(), true)});
 }
 
 }  // namespace xp

@@ -175,11 +175,15 @@ __global__ void bn_stats_partial_kernel(const bf16* __restrict__ x, int M, int C
 // a fixed pairwise tree in shared memory (deterministic).
 __device__ __forceinline__ void stats_final_body(const float* __restrict__ part, int chunks, int M, int RC, int C,
                                                  float eps, const bf16* __restrict__ gamma,
-                                                 const bf16* __restrict__ beta, float* __restrict__ stats, int unit) {
+                                                 const bf16* __restrict__ beta, float* __restrict__ stats, int unit,
+                                                 float* __restrict__ sout = nullptr) {
+  // threads >= 256 of a wider block (the fused final + apply kernel) only pass the barriers;
+  // sout (shared memory, [4][C], nullable): the 8 channels' results for the block itself
   __shared__ float sh[32][8][3];
-  const int cc = threadIdx.x & 7, j = threadIdx.x >> 3, c = unit * 8 + cc;
+  const bool act = threadIdx.x < 256;
+  const int cc = threadIdx.x & 7, j = (threadIdx.x >> 3) & 31, c = unit * 8 + cc;
   float na = 0.f, mean = 0.f, m2 = 0.f;
-  if (c < C) {
+  if (act && c < C) {
     for (int k = j; k < chunks; k += 8 * 32) {
       float mb[8], qb[8];
 #pragma unroll
@@ -195,21 +199,22 @@ __device__ __forceinline__ void stats_final_body(const float* __restrict__ part,
       }
     }
   }
-  sh[j][cc][0] = na; sh[j][cc][1] = mean; sh[j][cc][2] = m2;
+  if (act) { sh[j][cc][0] = na; sh[j][cc][1] = mean; sh[j][cc][2] = m2; }
   for (int stride = 16; stride > 0; stride >>= 1) {
     __syncthreads();
-    if (j < stride) {
+    if (act && j < stride) {
       float a = sh[j][cc][0], b = sh[j][cc][1], q = sh[j][cc][2];
       chan_merge(a, b, q, sh[j + stride][cc][0], sh[j + stride][cc][1], sh[j + stride][cc][2]);
       sh[j][cc][0] = a; sh[j][cc][1] = b; sh[j][cc][2] = q;
     }
   }
   __syncthreads();
-  if (j == 0 && c < C) {
-    stats[c] = sh[0][cc][1];
-    stats[C + c] = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(sh[0][cc][2], sh[0][cc][0]), eps)));
-    stats[2 * C + c] = __bfloat162float(gamma[c]);
-    stats[3 * C + c] = __bfloat162float(beta[c]);
+  if (act && j == 0 && c < C) {
+    const float mu = sh[0][cc][1];
+    const float rs = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(sh[0][cc][2], sh[0][cc][0]), eps)));
+    const float ga = __bfloat162float(gamma[c]), be = __bfloat162float(beta[c]);
+    stats[c] = mu; stats[C + c] = rs; stats[2 * C + c] = ga; stats[3 * C + c] = be;
+    if (sout) { sout[c] = mu; sout[C + c] = rs; sout[2 * C + c] = ga; sout[3 * C + c] = be; }
   }
 }
 __global__ void bn_stats_final_kernel(const float* __restrict__ part, int chunks, int M, int RC, int C, float eps,
@@ -458,11 +463,14 @@ __global__ void bn_bwd_reduce_kernel(const bf16* __restrict__ x, const bf16* __r
 // order, then a fixed tree); dgamma/dbeta into the accumulator
 __device__ __forceinline__ void bwd_final_body(const float* __restrict__ part, int chunks, int C,
                                                float* __restrict__ tot, float* __restrict__ g_gamma,
-                                               float* __restrict__ g_beta, int accumulate, int unit) {
+                                               float* __restrict__ g_beta, int accumulate, int unit,
+                                               float* __restrict__ sout = nullptr) {
+  // wider blocks / sout ([2][C], shared): as stats_final_body
   __shared__ float sh[32][8][2];
-  const int cc = threadIdx.x & 7, j = threadIdx.x >> 3, c = unit * 8 + cc;
+  const bool act = threadIdx.x < 256;
+  const int cc = threadIdx.x & 7, j = (threadIdx.x >> 3) & 31, c = unit * 8 + cc;
   float s1 = 0.f, s2 = 0.f;
-  if (c < C) {
+  if (act && c < C) {
     for (int k = j; k < chunks; k += 8 * 32) {
       float a[8], b[8];
 #pragma unroll
@@ -476,19 +484,20 @@ __device__ __forceinline__ void bwd_final_body(const float* __restrict__ part, i
         if (k + 32 * u < chunks) { s1 = __fadd_rn(s1, a[u]); s2 = __fadd_rn(s2, b[u]); }
     }
   }
-  sh[j][cc][0] = s1; sh[j][cc][1] = s2;
+  if (act) { sh[j][cc][0] = s1; sh[j][cc][1] = s2; }
   for (int stride = 16; stride > 0; stride >>= 1) {
     __syncthreads();
-    if (j < stride) {
+    if (act && j < stride) {
       sh[j][cc][0] = __fadd_rn(sh[j][cc][0], sh[j + stride][cc][0]);
       sh[j][cc][1] = __fadd_rn(sh[j][cc][1], sh[j + stride][cc][1]);
     }
   }
   __syncthreads();
-  if (j == 0 && c < C) {
+  if (act && j == 0 && c < C) {
     s1 = sh[0][cc][0]; s2 = sh[0][cc][1];
     tot[c] = s1;
     tot[C + c] = s2;
+    if (sout) { sout[c] = s1; sout[C + c] = s2; }
     g_beta[c] = accumulate ? __fadd_rn(g_beta[c], s1) : s1;
     g_gamma[c] = accumulate ? __fadd_rn(g_gamma[c], s2) : s2;
   }
@@ -615,6 +624,46 @@ __global__ void bn_bwd_apply_tiled_kernel(const bf16* __restrict__ x, const bf16
   pdl_wait();
   bwd_apply_tiled_body<PK>(x, dout, y, pidx, st, tot, gamma_b, G, M, Mo, dx, blockIdx.x * blockDim.x + threadIdx.x,
                            gridDim.x * blockDim.x);
+}
+
+// ---- final merge + elementwise pass in one launch, one block per 8 channels ------------------
+// Layers with few rows (M <= kFaRows): block u merges the partials of channels 8u..8u+7 exactly as
+// the separate final kernel does (same body, same bits) and then runs the elementwise pass for
+// those channels over every row (i = u + G*tid, stride G*blockDim: the separate kernels' item
+// index restricted to group u).  No block repeats another's merge, so one launch per BatchNorm
+// and direction disappears at no extra work.
+constexpr int kFaThreads = 512;
+template <int PK>
+__global__ void __launch_bounds__(kFaThreads) bn_final_apply_kernel(
+    const float* __restrict__ part, int chunks, int M, int RC, float eps, const bf16* __restrict__ gamma,
+    const bf16* __restrict__ beta, float* __restrict__ stats, const bf16* __restrict__ x, bf16* __restrict__ y,
+    uint8_t* __restrict__ pidx, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph,
+    int pw, int pool, int relu, const bf16* __restrict__ res, int ldy) {
+  extern __shared__ float fst[];  // [4][C]: this block's 8 channels filled
+  pdl_wait();
+  stats_final_body(part, chunks, M, RC, C, eps, gamma, beta, stats, blockIdx.x, fst);
+  __syncthreads();
+  const int G = C / 8;
+  bn_apply_body<PK>(x, fst, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool, relu,
+                    (int)blockIdx.x + G * (int)threadIdx.x, G * (int)blockDim.x, res, ldy);
+}
+// TL: 2 / 1 the exact-tiling pooled body (2x2 / runtime window), 0 the row body (PM = G.pool)
+template <int TL>
+__global__ void __launch_bounds__(kFaThreads) bn_bwd_final_apply_kernel(
+    const float* __restrict__ part, int chunks, float* __restrict__ tot, float* __restrict__ g_gamma,
+    float* __restrict__ g_beta, int accumulate, const bf16* __restrict__ x, const bf16* __restrict__ dout,
+    const bf16* __restrict__ y, const uint8_t* __restrict__ pidx, const float* __restrict__ st,
+    const bf16* __restrict__ gamma_b, BwdGeo G, int M, int Mo, bf16* __restrict__ dx) {
+  extern __shared__ float ftot[];  // [2][C]
+  pdl_wait();
+  const int C = G.C, NG = C / 8;
+  bwd_final_body(part, chunks, C, tot, g_gamma, g_beta, accumulate, blockIdx.x, ftot);
+  __syncthreads();
+  const int i0 = (int)blockIdx.x + NG * (int)threadIdx.x, is = NG * (int)blockDim.x;
+  if (TL == 2) bwd_apply_tiled_body<2>(x, dout, y, pidx, st, ftot, gamma_b, G, M, Mo, dx, i0, is);
+  else if (TL == 1) bwd_apply_tiled_body<0>(x, dout, y, pidx, st, ftot, gamma_b, G, M, Mo, dx, i0, is);
+  else if (G.pool) bwd_apply_body<1>(x, dout, y, pidx, st, ftot, gamma_b, G, M, dx, i0, is);
+  else bwd_apply_body<0>(x, dout, y, pidx, st, ftot, gamma_b, G, M, dx, i0, is);
 }
 
 // ---- folded BatchNorm merges (small layers) -------------------------------------------------
@@ -788,9 +837,17 @@ __global__ void linear_wgrad_bf16_kernel(const void* __restrict__ dy, const bf16
   const int o = blockIdx.y;
   if (i > in || (i == in && !gb)) return;
   float acc = 0.f;
-  for (int r = 0; r < n; ++r) {
-    const float d = load_dy<DY_F32>(dy, (int64_t)r * out + o, mask);
-    acc += i < in ? d * __bfloat162float(x[(int64_t)r * in + i]) : d;
+  for (int r0 = 0; r0 < n; r0 += 8) {  // eight rows' loads in flight, then the in-order sum
+    float d[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = r0 + u;
+      d[u] = r < n ? load_dy<DY_F32>(dy, (int64_t)r * out + o, mask) : 0.f;
+      xv[u] = (r < n && i < in) ? __bfloat162float(x[(int64_t)r * in + i]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (r0 + u < n) acc += i < in ? d[u] * xv[u] : d[u];
   }
   float* dst = i < in ? &gW[(int64_t)o * in + i] : &gb[o];
   *dst = accumulate ? __fadd_rn(*dst, acc) : acc;
@@ -883,6 +940,22 @@ int bn_chunk_rows(int M, int C) {
 bool bn_fold(int M, int C, int chunks) {
   return !bn_fold_off() && (int64_t)M * C <= kFoldElems && (int64_t)chunks * C <= kFoldFloats;
 }
+// final merge and elementwise pass as one launch (bn_final_apply_kernel / bn_bwd_final_apply_kernel)
+// for layers of at most XPIPE_BN_FA_ROWS rows (default 2048: at most 4 rows per thread of the
+// 512-thread blocks).  Opt-in (XPIPE_BN_FA=1): bit-identical, one launch per BatchNorm and
+// direction fewer, but measured slower in the pipeline (A/B on one B200: VGG-16 K=4 111.0k vs
+// 120.7k, ResNet-101 K=8 23.9k vs 28.8k, Inception-V3 K=4 25.8k vs 27.0k samples/s) -- C/8
+// blocks walking every row with 16-byte row-strided accesses replace a wide, coalesced grid
+bool bn_fa(int M) {
+  static const int rows = [] {
+    const char* e = getenv("XPIPE_BN_FA");
+    if (!(e && *e == '1')) return 0;
+    const char* r = getenv("XPIPE_BN_FA_ROWS");
+    return (r && *r) ? atoi(r) : 2048;
+  }();
+  return M <= rows;
+}
+inline float* ws_mut(const float* p) { return const_cast<float*>(p); }
 int fold_grid(int64_t items) { return std::min(grid1d(items), 2 * 148); }
 int bn_chunks(int M, int C) { return (M + bn_chunk_rows(M, C) - 1) / bn_chunk_rows(M, C); }
 size_t bn_ws_floats(int M, int C) { return (size_t)bn_chunks(M, C) * 2 * C + 2 * (size_t)C; }
@@ -913,6 +986,22 @@ cudaError_t launch_bn_apply_stats(const float* part, int chunks, int RC, float e
                                   int P, int Q, int kh, int kw, int sh, int sw, int ph, int pw, bool pool, bool relu,
                                   cudaStream_t st, const bf16* res, int ldy) {
   const int M = n * H * W;
+  if (!bn_fold(M, C, chunks) && bn_fa(M)) {
+    if (!ldy) ldy = C;
+    const int64_t total = (int64_t)n * P * Q * (C / 8);
+    if (C % 8 || C > 2048 || total >= kMaxElems || (res && pool)) return cudaErrorInvalidValue;
+    const size_t shm = (size_t)4 * C * 4;
+    if (pool && kh == 2 && kw == 2 && sh == 2 && sw == 2 && ph == 0 && pw == 0 && H == 2 * P && W == 2 * Q &&
+        !bn_tiled_off())
+      launch_pdl(bn_final_apply_kernel<2>, dim3(C / 8), dim3(kFaThreads), shm, st, part, chunks, M, RC, eps, gamma,
+                 beta, stats, x, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, 1, relu ? 1 : 0,
+                 (const bf16*)nullptr, ldy);
+    else
+      launch_pdl(bn_final_apply_kernel<0>, dim3(C / 8), dim3(kFaThreads), shm, st, part, chunks, M, RC, eps, gamma,
+                 beta, stats, x, y, pidx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw, pool ? 1 : 0, relu ? 1 : 0, res,
+                 ldy);
+    return cudaGetLastError();
+  }
   if (!bn_fold(M, C, chunks)) {
     cudaError_t e = launch_bn_stats_final(part, chunks, M, RC, C, eps, gamma, beta, stats, st);
     if (e != cudaSuccess) return e;
@@ -981,7 +1070,7 @@ cudaError_t launch_bn_bwd_reduce(const bf16* x, const bf16* dout, const bf16* y,
   else
     launch_pdl(bn_bwd_reduce_kernel<0, false>, dim3(chunks), dim3(threads), shm, st, x, dout, y, pidx, stats, G, M, RC,
                ws, (bf16*)nullptr, ar);
-  if (bn_fold(M, C, chunks)) return cudaGetLastError();  // the merge runs in launch_bn_bwd_apply
+  if (bn_fold(M, C, chunks) || bn_fa(M)) return cudaGetLastError();  // the merge runs in launch_bn_bwd_apply
   launch_pdl(bn_bwd_final_kernel, dim3((C + 7) / 8), dim3(256), 0, st, (const float*)ws, chunks, C, tot, g_gamma, g_beta,
              accumulate ? 1 : 0);
   return cudaGetLastError();
@@ -1013,6 +1102,23 @@ cudaError_t launch_bn_bwd_apply(const bf16* x, const bf16* dout, const bf16* y, 
     else
       launch_pdl(bn_bwd_apply_fold_kernel<1>, dim3(fold_grid((int64_t)Mo * (C / 8))), dim3(256), shm, st, x, dout, y,
                  pidx, stats, (const float*)ws, chunks, g_gamma, g_beta, acc, gamma_b, G, M, Mo, dx);
+    return cudaGetLastError();
+  }
+  if (bn_fa(M)) {  // the totals merge (and dgamma / dbeta) and the input gradient, one block per 8 channels
+    if (!g_gamma || !g_beta) return cudaErrorInvalidValue;
+    const size_t shm = (size_t)2 * C * 4;
+    const int acc = accumulate ? 1 : 0;
+    const int Mo = n * P * Q;
+    float* totw = ws_mut(ws) + (size_t)chunks * 2 * C;
+    if (tiled && kh == 2 && kw == 2)
+      launch_pdl(bn_bwd_final_apply_kernel<2>, dim3(C / 8), dim3(kFaThreads), shm, st, ws, chunks, totw, g_gamma,
+                 g_beta, acc, x, dout, y, pidx, stats, gamma_b, G, M, Mo, dx);
+    else if (tiled)
+      launch_pdl(bn_bwd_final_apply_kernel<1>, dim3(C / 8), dim3(kFaThreads), shm, st, ws, chunks, totw, g_gamma,
+                 g_beta, acc, x, dout, y, pidx, stats, gamma_b, G, M, Mo, dx);
+    else
+      launch_pdl(bn_bwd_final_apply_kernel<0>, dim3(C / 8), dim3(kFaThreads), shm, st, ws, chunks, totw, g_gamma,
+                 g_beta, acc, x, dout, y, pidx, stats, gamma_b, G, M, Mo, dx);
     return cudaGetLastError();
   }
   if (pool && kh == sh && kw == sw && ph == 0 && pw == 0 && H == P * kh && W == Q * kw && kh * kw <= 255 &&
@@ -1200,6 +1306,121 @@ __global__ void pool_bwd_kernel(const bf16* x, const bf16* dy, bf16* dx, int n, 
     put_grad(dx + i, acc, accumulate);
   }
 }
+// The two pooling kernels above, 8 channels per thread (16-byte loads / stores, 32-bit index
+// arithmetic; C % 8 == 0, row pitches % 8 == 0): per element the same window scan, the same
+// first-max rule and the same sums in the same order, so the results are bit-identical
+__device__ __forceinline__ void unpack8(const uint4& u, float (&v)[8]) {
+  const bf16* b = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = __bfloat162float(b[e]);
+}
+__device__ __forceinline__ uint4 pack8(const float (&v)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    __nv_bfloat162 t = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+    w[h] = *reinterpret_cast<uint32_t*>(&t);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__global__ void pool_fwd8_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, int n, int H, int W, int C, int P,
+                                 int Q, int kh, int kw, int sh, int sw, int ph, int pw, int mode, int ldy) {
+  pdl_wait();
+  const int G = C / 8, total = n * P * Q * G;
+  const float inv = 1.f / (float)(kh * kw);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % G;
+    int r = i / G;
+    const int q = r % Q; r /= Q;
+    const int p = r % P;
+    const int s = r / P;
+    float best[8], acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { best[e] = 0.f; acc[e] = 0.f; }
+    bool first = true;
+    for (int a = 0; a < kh; ++a)
+      for (int b = 0; b < kw; ++b) {
+        const int hh = p * sh - ph + a, ww = q * sw - pw + b;
+        if (hh < 0 || hh >= H || ww < 0 || ww >= W) continue;
+        float v[8];
+        unpack8(*reinterpret_cast<const uint4*>(x + ((s * H + hh) * W + ww) * C + g * 8), v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (mode == 0) { if (first || v[e] > best[e]) best[e] = v[e]; }
+          else acc[e] = __fadd_rn(acc[e], v[e]);
+        }
+        first = false;
+      }
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = mode == 0 ? best[e] : __fmul_rn(acc[e], inv);
+    *reinterpret_cast<uint4*>(y + ((s * P + p) * Q + q) * ldy + g * 8) = pack8(o);
+  }
+}
+__global__ void pool_bwd8_kernel(const bf16* __restrict__ x, const bf16* __restrict__ dy, bf16* __restrict__ dx,
+                                 int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh, int sw, int ph,
+                                 int pw, int mode, int accumulate, int ldy) {
+  pdl_wait();
+  const int G = C / 8, total = n * H * W * G;
+  const float inv = 1.f / (float)(kh * kw);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int g = i % G;
+    int r = i / G;
+    const int w = r % W; r /= W;
+    const int h = r % H;
+    const int s = r / H;
+    const int plo = max(0, (h + ph - kh + sh) / sh), phi = min(P - 1, (h + ph) / sh);
+    const int qlo = max(0, (w + pw - kw + sw) / sw), qhi = min(Q - 1, (w + pw) / sw);
+    float acc[8];
+    int hits[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { acc[e] = 0.f; hits[e] = 0; }
+    for (int p = plo; p <= phi; ++p)
+      for (int q = qlo; q <= qhi; ++q) {
+        if (h < p * sh - ph || h >= p * sh - ph + kh || w < q * sw - pw || w >= q * sw - pw + kw) continue;
+        float gv[8];
+        unpack8(*reinterpret_cast<const uint4*>(dy + ((s * P + p) * Q + q) * ldy + g * 8), gv);
+        if (mode == 0) {
+          float best[8];
+          int bpos[8];  // the window's first max, as h * W + w (-1: none yet)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) { best[e] = 0.f; bpos[e] = -1; }
+          for (int a = 0; a < kh; ++a)
+            for (int b = 0; b < kw; ++b) {
+              const int hh = p * sh - ph + a, ww = q * sw - pw + b;
+              if (hh < 0 || hh >= H || ww < 0 || ww >= W) continue;
+              float v[8];
+              unpack8(*reinterpret_cast<const uint4*>(x + ((s * H + hh) * W + ww) * C + g * 8), v);
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                if (bpos[e] < 0 || v[e] > best[e]) { best[e] = v[e]; bpos[e] = hh * W + ww; }
+            }
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (bpos[e] == h * W + w) { acc[e] = hits[e] ? __fadd_rn(acc[e], gv[e]) : gv[e]; ++hits[e]; }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float gi = __fmul_rn(gv[e], inv);
+            acc[e] = hits[e] ? __fadd_rn(acc[e], gi) : gi;
+            ++hits[e];
+          }
+        }
+      }
+    bf16* d = dx + (int64_t)i * 8;
+    float o[8];
+    if (accumulate) {
+      float old[8];
+      unpack8(*reinterpret_cast<const uint4*>(d), old);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(old[e], q16b(acc[e]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = q16b(acc[e]);
+    }
+    *reinterpret_cast<uint4*>(d) = pack8(o);
+  }
+}
 // global average pool: y[s][c] = (sum over H*W in raster order) * (1/(H*W))
 __global__ void gap_fwd_kernel(const bf16* x, bf16* y, int n, int HW, int C) {
   pdl_wait();
@@ -1243,14 +1464,27 @@ cudaError_t launch_concat_bwd(const bf16* dy, bf16* da, bf16* db, int64_t rows, 
   launch_pdl(concat_bwd_kernel, dim3(g1(rows * (Ca + Cb))), dim3(256), 0, st, dy, da, db, rows, Ca, Cb, acc_a ? 1 : 0, acc_b ? 1 : 0);
   return cudaGetLastError();
 }
+bool pool_vec_off() { static const bool v = getenv("XPIPE_NO_POOL_VEC") != nullptr; return v; }
 cudaError_t launch_pool_fwd(const bf16* x, bf16* y, int n, int H, int W, int C, int P, int Q, int kh, int kw, int sh,
                             int sw, int ph, int pw, bool avg, cudaStream_t st, int ldy) {
+  if (!ldy) ldy = C;
+  if (C % 8 == 0 && ldy % 8 == 0 && (int64_t)n * std::max(H * W, P * Q) * C < kMaxElems && !pool_vec_off()) {
+    launch_pdl(pool_fwd8_kernel, dim3(g1((int64_t)n * P * Q * C / 8)), dim3(256), 0, st, x, y, n, H, W, C, P, Q, kh,
+               kw, sh, sw, ph, pw, avg ? 1 : 0, ldy);
+    return cudaGetLastError();
+  }
   launch_pdl(pool_fwd_kernel, dim3(g1((int64_t)n * P * Q * C)), dim3(256), 0, st, x, y, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
              avg ? 1 : 0, ldy ? ldy : C);
   return cudaGetLastError();
 }
 cudaError_t launch_pool_bwd(const bf16* x, const bf16* dy, bf16* dx, int n, int H, int W, int C, int P, int Q, int kh,
                             int kw, int sh, int sw, int ph, int pw, bool avg, bool accumulate, cudaStream_t st, int ldy) {
+  if (!ldy) ldy = C;
+  if (C % 8 == 0 && ldy % 8 == 0 && (int64_t)n * std::max(H * W, P * Q) * C < kMaxElems && !pool_vec_off()) {
+    launch_pdl(pool_bwd8_kernel, dim3(g1((int64_t)n * H * W * C / 8)), dim3(256), 0, st, x, dy, dx, n, H, W, C, P, Q,
+               kh, kw, sh, sw, ph, pw, avg ? 1 : 0, accumulate ? 1 : 0, ldy);
+    return cudaGetLastError();
+  }
   launch_pdl(pool_bwd_kernel, dim3(g1((int64_t)n * H * W * C)), dim3(256), 0, st, x, dy, dx, n, H, W, C, P, Q, kh, kw, sh, sw, ph, pw,
                                                               avg ? 1 : 0, accumulate ? 1 : 0, ldy ? ldy : C);
   return cudaGetLastError();

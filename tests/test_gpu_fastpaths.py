@@ -12,7 +12,13 @@ subprocesses on the same seeded inputs:
   * XPIPE_BN_FUSE=1 (opt-in) -- the BatchNorm statistics and BN-apply [+ residual] [+ ReLU] in the
     fprop GEMM's epilogue (the M tiles of an N tile as one thread-block cluster, partials over
     DSMEM) vs the separate statistics-merge and apply launches: VGG-16 at CIFAR size K=2 (its
-    unpooled 8x8 / 4x4 layers), the ResNet blocks (residual blocks at 4x4 / 2x2) and Inception."""
+    unpooled 8x8 / 4x4 layers), the ResNet blocks (residual blocks at 4x4 / 2x2) and Inception;
+  * XPIPE_BN_FA=1 (opt-in) -- for layers of at most 2048 rows, the BatchNorm final merge and the elementwise
+    pass as one launch with one block per 8 channels (forward: statistics merge + BN-apply
+    [+ residual] [+ ReLU] [+ pool]; backward: totals merge + dgamma/dbeta + input gradient,
+    pooled tiled / general / unpooled) vs the two launches: VGG-16, ResNet blocks, Inception;
+  * XPIPE_NO_POOL_VEC=1 -- the standalone max / average pools (Inception's branch and reduction
+    pools) 8 channels per thread vs one element per thread: Inception."""
 import os
 import subprocess
 import sys
@@ -55,7 +61,8 @@ g.close()
 
 def run(which, env_set, out):
     env = dict(os.environ)
-    for k in ("XPIPE_NO_ADD_FUSE", "XPIPE_NO_CONCAT_VIEWS", "XPIPE_BN_FUSE", "XPIPE_BN_FOLD"):
+    for k in ("XPIPE_NO_ADD_FUSE", "XPIPE_NO_CONCAT_VIEWS", "XPIPE_BN_FUSE", "XPIPE_BN_FOLD", "XPIPE_BN_FA",
+              "XPIPE_NO_POOL_VEC"):
         env.pop(k, None)
     if env_set:
         k, v = env_set.split("=")
@@ -68,7 +75,9 @@ def run(which, env_set, out):
 
 # (environment of the fast path, of the general path, model)
 CASES = [("", "XPIPE_NO_ADD_FUSE=1", "resnet"), ("", "XPIPE_NO_CONCAT_VIEWS=1", "inception"),
-         ("XPIPE_BN_FUSE=1", "", "vgg16"), ("XPIPE_BN_FUSE=1", "", "resnet"), ("XPIPE_BN_FUSE=1", "", "inception")]
+         ("XPIPE_BN_FUSE=1", "", "vgg16"), ("XPIPE_BN_FUSE=1", "", "resnet"), ("XPIPE_BN_FUSE=1", "", "inception"),
+         ("XPIPE_BN_FA=1", "", "vgg16"), ("XPIPE_BN_FA=1", "", "resnet"), ("XPIPE_BN_FA=1", "", "inception"),
+         ("", "XPIPE_NO_POOL_VEC=1", "inception")]
 
 
 @pytest.mark.parametrize("fast_env,general_env,which", CASES)

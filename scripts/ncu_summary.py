@@ -63,7 +63,10 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 
 
 def full(rep, out_md, traffic_key=None):
-    out = subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # a raw-page CSV exported on the box (ncu -i ... --page raw --csv)
+        out = open(rep).read()
+    else:
+        out = subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rd = list(csv.reader(io.StringIO(out)))
     if len(rd) < 3:
         raise SystemExit("no data in " + rep)
@@ -74,13 +77,13 @@ def full(rep, out_md, traffic_key=None):
         item = {"kernel": short(d.get("Kernel Name", "?"))}
         stalls = []
         for k in hdr:
-            if "warps_issue_stalled" in k and k.endswith("per_warp_active.pct"):
+            if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
                 try:
                     stalls.append((float(d[k].replace(",", "")), k))
                 except ValueError:
                     pass
         for v, k in sorted(stalls, reverse=True)[:6]:  # the dominant warp stall reasons
-            item[k] = "%.1f %%" % v
+            item[k] = "%.2f cycles per issued instruction" % v
         for k in hdr:
             if k in WANT or ("tensor" in k and "pct" in k and ".avg." in k):
                 if k not in WANT and d[k].strip() in ("0", "0.000000", ""):

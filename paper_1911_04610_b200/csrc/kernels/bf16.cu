@@ -837,17 +837,9 @@ __global__ void linear_wgrad_bf16_kernel(const void* __restrict__ dy, const bf16
   const int o = blockIdx.y;
   if (i > in || (i == in && !gb)) return;
   float acc = 0.f;
-  for (int r0 = 0; r0 < n; r0 += 8) {  // eight rows' loads in flight, then the in-order sum
-    float d[8], xv[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int r = r0 + u;
-      d[u] = r < n ? load_dy<DY_F32>(dy, (int64_t)r * out + o, mask) : 0.f;
-      xv[u] = (r < n && i < in) ? __bfloat162float(x[(int64_t)r * in + i]) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (r0 + u < n) acc += i < in ? d[u] * xv[u] : d[u];
+  for (int r = 0; r < n; ++r) {
+    const float d = load_dy<DY_F32>(dy, (int64_t)r * out + o, mask);
+    acc += i < in ? d * __bfloat162float(x[(int64_t)r * in + i]) : d;
   }
   float* dst = i < in ? &gW[(int64_t)o * in + i] : &gb[o];
   *dst = accumulate ? __fadd_rn(*dst, acc) : acc;

@@ -350,7 +350,9 @@ cudaError_t launch_linear_wgrad_f32(const float* dy, const float* ymask, const f
 cudaError_t launch_xent_f32(const float* z, const int32_t* y, float* dz, float* loss, int n, int classes, float invN,
                             uint32_t* status, cudaStream_t st) {
   if (n > kXentMaxRows) return cudaErrorInvalidValue;
-  if (classes >= 1 && classes <= kXentWarpC) {
+  // few classes (VGG-16's 10): the per-row serial loop is shorter than the warp kernel's
+  // cross-lane steps (ncu: 8.1 vs 9.3 us); the warp kernel from 64 classes on
+  if (classes > 64 && classes <= kXentWarpC) {
     const size_t shm = (size_t)8 * classes * sizeof(float);
     static bool attr = false;
     if (!attr) {

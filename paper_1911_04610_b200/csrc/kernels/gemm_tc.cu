@@ -388,9 +388,17 @@ __device__ __forceinline__ int64_t out_row(const GemmArgs& a, int row) {
   return ((int64_t)n * a.rm_H + (int64_t)p * a.rm_sh) * a.rm_W + (int64_t)q * a.rm_sw;
 }
 
+// the epilogue kind is fixed by the mode for the conv GEMMs (fprop / dgrad: bf16 rows, wgrad: the
+// transposed fp32 gradient), so only the plain GEMM instantiations carry every store path
+template <int MODE>
+__device__ __forceinline__ int epi_kind(const GemmArgs& a) {
+  return (MODE == GEMM_FPROP || MODE == GEMM_DGRAD) ? EPI_BF16 : (MODE == GEMM_WGRAD ? EPI_WGRAD_T : a.epi);
+}
+template <int MODE>
 __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, uint32_t (&v)[32]) {
   if (row >= a.M) return;
-  if (a.epi == EPI_BF16) {
+  const int epi = epi_kind<MODE>(a);
+  if (epi == EPI_BF16) {
     bf16* o = static_cast<bf16*>(a.out) + out_row(a, row) * a.ldo + col0;
     if (a.accumulate) {  // fan-out tensor: out = Q(old + Q(acc)) (the oracle's rounding points)
 #pragma unroll
@@ -437,7 +445,7 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
           if (col0 + e + h < a.N) o[e + h] = __float2bfloat16_rn(__uint_as_float(v[e + h]));
       }
     }
-  } else if (a.epi == EPI_F32) {
+  } else if (epi == EPI_F32) {
     float* o = static_cast<float*>(a.out) + (int64_t)blockIdx.z * a.split_stride + (int64_t)row * a.ldo + col0;
 #pragma unroll
     for (int e = 0; e < 32; e += 4) {
@@ -449,7 +457,7 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
           if (col0 + e + h < a.N) o[e + h] = __uint_as_float(v[e + h]);
       }
     }
-  } else if (a.epi == EPI_LINEAR_T) {  // out[c][m] = epi(D[m][c]); lanes = consecutive m
+  } else if (epi == EPI_LINEAR_T) {  // out[c][m] = epi(D[m][c]); lanes = consecutive m
     float v8[8];
 #pragma unroll
     for (int e0 = 0; e0 < 32; e0 += 8) {
@@ -476,8 +484,10 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
 }
 
 // 8 consecutive columns [col0, col0+8) of row `row` (split-K reduction output)
+template <int MODE>
 __device__ __forceinline__ void epi_store8(const GemmArgs& a, int row, int col0, const float (&v)[8]) {
-  if (a.epi == EPI_BF16) {
+  const int epi = epi_kind<MODE>(a);
+  if (epi == EPI_BF16) {
     bf16* o = static_cast<bf16*>(a.out) + out_row(a, row) * a.ldo + col0;
     if (!a.accumulate && col0 + 8 <= a.N) {
       uint32_t w[4];
@@ -498,11 +508,11 @@ __device__ __forceinline__ void epi_store8(const GemmArgs& a, int row, int col0,
           o[e] = __float2bfloat16_rn(v[e]);
         }
       }
-  } else if (a.epi == EPI_F32) {
+  } else if (epi == EPI_F32) {
     float* o = static_cast<float*>(a.out) + (int64_t)row * a.ldo + col0;
     for (int e = 0; e < 8; ++e)
       if (col0 + e < a.N) o[e] = v[e];
-  } else if (a.epi == EPI_LINEAR_T) {
+  } else if (epi == EPI_LINEAR_T) {
     linear_t_store8(a, row, col0, v);
   } else {
     float* g = static_cast<float*>(a.out) + (int64_t)col0 * a.ldo + row;
@@ -623,15 +633,19 @@ struct Ring {
 // one unit of a CTA's work: an output tile and its k-block range.  Split-K: one unit per CTA
 // (tile blockIdx.xy, k range blockIdx.z); otherwise persistent: tiles blockIdx.x, +gridDim.x, ...
 struct Work { int m0, n0, kb0, nkb; };
+// XS: the instantiation carries the split-K reduction and the cluster-fused BatchNorm (false:
+// neither is compiled in -- the kernels of unsplit launches are smaller, which the instruction
+// fetch of the concurrently running stages' kernels sees)
+template <bool XS = true>
 __device__ __forceinline__ int local_units(const GemmArgs& a, int ntiles) {
-  if (a.splits > 1 || a.bnf) return 1;
+  if (XS && (a.splits > 1 || a.bnf)) return 1;
   return (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 }
-template <int BN>
+template <int BN, bool XS = true>
 __device__ __forceinline__ Work work_of(const GemmArgs& a, int j, int mt) {
   Work w;
   const int nkb_total = (a.K + BK - 1) / BK;
-  if (a.splits > 1 || a.bnf) {
+  if (XS && (a.splits > 1 || a.bnf)) {
     w.m0 = blockIdx.x * BM; w.n0 = blockIdx.y * BN;
     w.kb0 = blockIdx.z * a.kb_per_split;
     w.nkb = max(0, min(nkb_total, w.kb0 + a.kb_per_split) - w.kb0);
@@ -642,7 +656,7 @@ __device__ __forceinline__ Work work_of(const GemmArgs& a, int j, int mt) {
   return w;
 }
 
-template <int MODE, int BN, bool A_MN, bool B_MN>
+template <int MODE, int BN, bool A_MN, bool B_MN, bool XS>
 __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* tmA, const CUtensorMap* tmB, uint32_t base,
                                          uint32_t full0, uint32_t empty0, int nunits, int mt, int tid) {
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
@@ -654,7 +668,7 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
     // slot 2i+1's barrier is arrived at once (its bytes are counted by slot 2i's)
     if (tid != 0) return;
     for (int j = 0; j < nunits; ++j) {
-      const Work w = work_of<BN>(a, j, mt);
+      const Work w = work_of<BN, XS>(a, j, mt);
       const int tn = w.m0 / (a.gq * a.gp), rem = w.m0 - tn * a.gq * a.gp, tp = rem / a.gq, tq = rem - tp * a.gq;
       for (int i = 0; i < w.nkb; i += 2) {
         const int s0 = ring.slot;
@@ -678,7 +692,7 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
     // full-TMA pipeline: one elected thread streams both operands; the others are idle
     if (tid != 0) return;
     for (int j = 0; j < nunits; ++j) {
-      const Work w = work_of<BN>(a, j, mt);
+      const Work w = work_of<BN, XS>(a, j, mt);
       int tn = 0, tp = 0, tq = 0;  // pixel origin of the tile's rows (fprop / dgrad)
       if (MODE == GEMM_FPROP || MODE == GEMM_DGRAD) {
         tn = w.m0 / (a.gq * a.gp);
@@ -746,7 +760,7 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
   Ring arr(a.stages);
   int issued = 0, arrived = 0;
   for (int j = 0; j < nunits; ++j) {
-    const Work w = work_of<BN>(a, j, mt);
+    const Work w = work_of<BN, XS>(a, j, mt);
     DenseK<BM> pak; DenseMN<BM> pam; DenseK<BN> pbk; DenseMN<BN> pbm;
     FpropA fa; DgradA da; WgradA wa; DgradB<BN> db;
     if (MODE == GEMM_PLAIN) {
@@ -810,7 +824,7 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
   for (; arrived < issued; ++arrived, arr.next()) mbar_arrive(full0 + 8 * arr.slot);
 }
 
-template <int MODE, int BN, bool A_MN, bool B_MN>
+template <int MODE, int BN, bool A_MN, bool B_MN, bool XS>
 __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, const __grid_constant__ CUtensorMap tmA,
                                                                const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ uint8_t smem_raw[];
@@ -826,7 +840,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const int mt = (a.M + BM - 1) / BM, ntiles = mt * ((a.N + BN - 1) / BN);
-  const int nunits = local_units(a, ntiles);
+  const int nunits = local_units<XS>(a, ntiles);
 
   if (tid == 0) {
     if (a.a_tma) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
@@ -861,14 +875,14 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
   if (a.dbg && tid == 0) a.dbg[cta * 16 + 0] = gtimer();
 
   if (warp < 4) {
-    producer<MODE, BN, A_MN, B_MN>(a, &tmA, &tmB, base, full0, empty0, nunits, mt, tid);
+    producer<MODE, BN, A_MN, B_MN, XS>(a, &tmA, &tmB, base, full0, empty0, nunits, mt, tid);
     __syncwarp();  // reconverge (the TMA producer is one thread) before the aligned barriers
   } else if (warp == 4) {
     if (lane == 0) {
       const uint32_t id = idesc<BN, A_MN, B_MN>();
       Ring ring(ST);
       for (int j = 0; j < nunits; ++j) {
-        const Work w = work_of<BN>(a, j, mt);
+        const Work w = work_of<BN, XS>(a, j, mt);
         const int buf = j & 1;
         mbar_wait(acce0 + 8 * buf, ((uint32_t)(j >> 1) & 1u) ^ 1u);  // accumulator drained
         tc_fence_after();
@@ -895,10 +909,10 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
   }
   constexpr int LDS = BN + 4;  // fp32 staging row pitch of the split-K reduction (bank skew)
   const int q = warp & 3;      // TMEM lane quadrant of an epilogue warp
-  if (a.splits <= 1) {
+  if (!XS || a.splits <= 1) {
     if (warp >= 5) {
       for (int j = 0; j < nunits; ++j) {
-        const Work w = work_of<BN>(a, j, mt);
+        const Work w = work_of<BN, XS>(a, j, mt);
         const int buf = j & 1;
         mbar_wait(accf0 + 8 * buf, (uint32_t)(j >> 1) & 1u);
         if (a.dbg && j == 0 && warp == 5 && lane == 0) a.dbg[cta * 16 + 3] = gtimer();
@@ -913,8 +927,8 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = 0u;
           }
-          if (w.n0 + c0 < a.N) epi_store(a, row, w.n0 + c0, v);
-          if ((MODE == GEMM_FPROP || MODE == GEMM_PLAIN) && (a.bn_part || a.bnf) && w.n0 + c0 < a.N) {
+          if (w.n0 + c0 < a.N) epi_store<MODE>(a, row, w.n0 + c0, v);
+          if ((MODE == GEMM_FPROP || MODE == GEMM_PLAIN) && (a.bn_part || (XS && a.bnf)) && w.n0 + c0 < a.N) {
             // BatchNorm partials of this tile's 32 columns over its valid rows, from the stored
             // (bf16-rounded) values: tile mean, then the sum of squared deviations (two passes;
             // the second re-reads the accumulator from TMEM), fixed-order reductions
@@ -943,7 +957,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
             if (q == 0 && col < a.N) {
               const float m2 = __fadd_rn(__fadd_rn(__fadd_rn(epi_red[lane], epi_red[32 + lane]), epi_red[64 + lane]),
                                          epi_red[96 + lane]);
-              if (a.bnf) {  // this tile's partials stay in the (drained) ring for the cluster merge
+              if (XS && a.bnf) {  // this tile's partials stay in the (drained) ring for the cluster merge
                 float* bnx = reinterpret_cast<float*>(smem_raw + (base - raw));
                 bnx[c0 + lane] = mean;
                 bnx[BN + c0 + lane] = m2;
@@ -961,7 +975,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
         if (lane == 0) mbar_arrive(acce0 + 8 * buf);
       }
     }
-    if (MODE == GEMM_FPROP && a.bnf) {
+    if (XS && MODE == GEMM_FPROP && a.bnf) {
       cluster_sync();  // every tile's partials are in its CTA's smem
       if (warp >= 5) bnf_apply<BN>(a, base, reinterpret_cast<float*>(smem_raw + (base - raw)), tmem, mt, tid - 160, q, lane);
       cluster_sync();  // no CTA frees its smem while the others still read its partials
@@ -969,7 +983,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
   } else {
     // cluster split-K (one unit per CTA): park the partial tile in this CTA's smem (the ring is
     // drained: every stage was consumed by an MMA that completed before the accumulator barrier)
-    const Work w = work_of<BN>(a, 0, mt);
+    const Work w = work_of<BN, XS>(a, 0, mt);
     const int m0 = w.m0, n0 = w.n0;
     float* red = reinterpret_cast<float*>(smem_raw + (base - raw));
     const int tile_id = blockIdx.y * gridDim.x + blockIdx.x;
@@ -1050,7 +1064,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
           for (int e = 0; e < 8; ++e) acc[e] = src ? __fadd_rn(acc[e], x[e]) : x[e];
         }
       if (nc == 1) {
-        epi_store8(a, gr, gc, acc);
+        epi_store8<MODE>(a, gr, gc, acc);
       } else {
         float4* d = reinterpret_cast<float4*>(wsp + lr * BN + ch * 8);
         __stcg(d, make_float4(acc[0], acc[1], acc[2], acc[3]));
@@ -1098,7 +1112,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
                 for (int e = 0; e < 8; ++e) acc[e] = (c0 + u) ? __fadd_rn(acc[e], x[e]) : x[e];
               }
           }
-          epi_store8(a, gr, gc, acc);
+          epi_store8<MODE>(a, gr, gc, acc);
         }
       }
     }
@@ -1294,8 +1308,11 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   constexpr int DEEP = std::min(8, (kMaxSmem - 2048) / STAGE);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, DEEP * STAGE + 1024 + 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DEEP * STAGE + 1024 + 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -1356,7 +1373,7 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   if (args.bnf) {  // one cluster of mt CTAs per N tile (the caller checked mt <= 16 and residency)
     static bool np_attr = false;
     if (!np_attr) {
-      cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       np_attr = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -1373,10 +1390,10 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     cfg.gridDim = dim3(mt, nt, 1);
     args.splits = 1; args.cs = 1; args.nc = 1;
     args.kb_per_split = std::max(1, (a.K + BK - 1) / BK);
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<MODE, BN, A_MN, B_MN>, args, tmA, tmB);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>, args, tmA, tmB);
   }
   if (splits <= 1) {
-    launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);
+    launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN, false>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -1399,7 +1416,7 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     at[1].val.clusterDim.z = cs;
     cfg.gridDim = dim3(mt, nt, cs);
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<MODE, BN, A_MN, B_MN>, &cfg) != cudaSuccess || n <= 0)
+    if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>, &cfg) != cudaSuccess || n <= 0)
       n = 1 << 20;  // unknown: do not constrain
     cudaGetLastError();
     maxc_cache[cs] = n;
@@ -1421,7 +1438,7 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   args.kb_per_split = (nkb + args.splits - 1) / args.splits;
   at[1].val.clusterDim.z = args.cs;
   cfg.gridDim = dim3(mt, nt, args.splits);
-  return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<MODE, BN, A_MN, B_MN>, args, tmA, tmB);
+  return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>, args, tmA, tmB);
 }
 
 template <int MODE, bool A_MN, bool B_MN>
@@ -1464,6 +1481,15 @@ __host__ int split_fd_below() {
   static const int env = getenv_int("XPIPE_SPLIT_FD_BELOW", 0);
   return env > 0 ? env : split_below();
 }
+// smallest split worth its reduction (development knob XPIPE_SPLIT_MIN_S): 3 when several
+// pipeline stages share the device -- a 2-way split's cluster reduction costs about the main
+// loop it saves while its second CTA takes SM time from the other stages (measured: ResNet-101
+// K=8 30.3k -> 31.6k samples/s, VGG-16 K=4 and Inception-V3 K=4 unchanged) -- else 2
+__host__ int split_min_s() {
+  static const int env = getenv_int("XPIPE_SPLIT_MIN_S", 0);
+  if (env > 0) return env;
+  return g_coresident > 1 ? 3 : 2;
+}
 SplitPlan plan_splits(int M, int N, int K, int min_bn = 64, bool wg = false) {
   SplitPlan p;
   p.bn = choose_bn(M, N);
@@ -1472,6 +1498,7 @@ SplitPlan plan_splits(int M, int N, int K, int min_bn = 64, bool wg = false) {
   const int nkb = std::max(1, (K + BK - 1) / BK);
   int s = 1;
   if (!no_splitk() && tiles < (wg ? split_below() : split_fd_below()) && nkb >= 16) s = std::max(1, std::min(num_sms() / tiles, nkb / split_min_kb()));
+  if (s < split_min_s()) s = 1;  // a 2-way split's reduction costs about what it saves
   if (tiles * (int64_t)std::min(s, kMaxCluster) > kTileCounters - 64) s = 1;  // tail: BN counters
   p.cs = std::min(s, kMaxCluster);  // cluster size
   p.nc = std::max(1, s / p.cs);      // clusters per tile
@@ -1520,7 +1547,7 @@ bool bnf_resident(int mt, const GemmArgs& a) {
   if (it != cache.end()) return it->second;
   constexpr int STAGE = BM * BK * 2 + BN * BK * 2;
   const int SMEM = std::max(4, persist_stages()) * STAGE + 2048;
-  auto kern = tc_gemm_kernel<GEMM_FPROP, BN, false, false>;
+  auto kern = tc_gemm_kernel<GEMM_FPROP, BN, false, false, true>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(8, (kMaxSmem - 2048) / STAGE) * STAGE + 2048);
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};

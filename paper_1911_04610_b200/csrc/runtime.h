@@ -152,6 +152,12 @@ struct xpipe_ctx {
   float* x_dev = nullptr; int64_t x_cap = 0;
   int32_t* y_dev = nullptr; int64_t y_cap = 0;
   float* loss_dev = nullptr; int64_t loss_cap = 0;
+  // staging of host inputs for chained calls (one process): the next call's H2D copies run on
+  // cstream while the previous call's graph executes; a device-to-device copy on the launch
+  // stream then moves them into x_dev / y_dev at the call boundary
+  float* x_stage = nullptr; int32_t* y_stage = nullptr; int64_t x_stage_cap = 0, y_stage_cap = 0;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_staged = nullptr, ev_stage_free = nullptr;
   int64_t fed = 0;           // micro-batches fed (absolute, 1-based count)
   int64_t base = 0;          // micro-batch offset of the current epoch
   int64_t call_first = 0;    // first micro-batch (absolute) of the current call's input buffer

@@ -130,6 +130,13 @@ void free_all(xpipe_ctx* c) {
     s.fstream = nullptr;
     if (s.stream) { cudaSetDevice(s.dev); cudaStreamSynchronize(s.stream); cudaStreamDestroy(s.stream); s.stream = nullptr; }
   }
+  if (c->cstream) {
+    cudaStreamSynchronize(c->cstream);
+    cudaStreamDestroy(c->cstream);
+    c->cstream = nullptr;
+  }
+  for (cudaEvent_t* e : {&c->ev_staged, &c->ev_stage_free})
+    if (*e) { cudaEventDestroy(*e); *e = nullptr; }
   if (c->status_host) { cudaFreeHost(c->status_host); c->status_host = nullptr; }
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   c->ipc_opened.clear();
@@ -944,6 +951,22 @@ int ensure_call_buffers(xpipe_ctx* c, int64_t M) {
     if (last && ls > c->loss_cap) { c->loss_dev = (float*)dmalloc(c, ls * 4, c->S[c->K - 1].dev); c->loss_cap = ls; }
     if ((first && !c->x_dev) || (last && (!c->y_dev || !c->loss_dev))) return set_err(c, XP_ENOMEM, "call buffers");
   }
+  if (!c->mp() && !c->cfg.serialize && (c->x_stage_cap < c->x_cap || c->y_stage_cap < c->y_cap)) {
+    const int dev = c->S[0].dev;
+    cudaSetDevice(dev);
+    if (!c->cstream) {
+      if (cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->ev_stage_free, cudaEventDisableTiming) != cudaSuccess)
+        return set_err(c, XP_ECUDA, "staging stream");
+    }
+    XP_CUDA(c, cudaStreamSynchronize(c->cstream));
+    c->x_stage = (float*)dmalloc(c, c->x_cap * 4, dev);
+    c->y_stage = (int32_t*)dmalloc(c, c->y_cap * 4, dev);
+    if (!c->x_stage || !c->y_stage) return set_err(c, XP_ENOMEM, "staging buffers");
+    c->x_stage_cap = c->x_cap;
+    c->y_stage_cap = c->y_cap;
+  }
   return XP_OK;
 }
 
@@ -1160,10 +1183,25 @@ int xpipe_step(xpipe_ctx* c, const float* x, const int32_t* y, int32_t M, uint32
     const int64_t per = (int64_t)c->cfg.in_c * c->cfg.in_h * c->cfg.in_w;
     StageRT& s0 = c->S[0];
     cudaSetDevice(s0.dev);
-    XP_CUDA(c, cudaMemcpyAsync(c->x_dev, x, (size_t)M * c->N * per * 4,
-                               dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.stream));
-    XP_CUDA(c, cudaMemcpyAsync(c->y_dev, y, (size_t)M * c->N * 4,
-                               dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s0.stream));
+    const size_t xb = (size_t)M * c->N * per * 4, yb = (size_t)M * c->N * 4;
+    if (!dev_ptrs && c->cstream && (int64_t)M * c->N * per <= c->x_stage_cap && (int64_t)M * c->N <= c->y_stage_cap) {
+      // host inputs: H2D into the staging buffers now, concurrently with the previous call's
+      // graph (cstream waits only for the previous call's staging copy-out), then a device copy
+      // into the call buffers at the boundary
+      XP_CUDA(c, cudaStreamWaitEvent(c->cstream, c->ev_stage_free, 0));
+      XP_CUDA(c, cudaMemcpyAsync(c->x_stage, x, xb, cudaMemcpyHostToDevice, c->cstream));
+      XP_CUDA(c, cudaMemcpyAsync(c->y_stage, y, yb, cudaMemcpyHostToDevice, c->cstream));
+      XP_CUDA(c, cudaEventRecord(c->ev_staged, c->cstream));
+      XP_CUDA(c, cudaStreamWaitEvent(s0.stream, c->ev_staged, 0));
+      XP_CUDA(c, cudaMemcpyAsync(c->x_dev, c->x_stage, xb, cudaMemcpyDeviceToDevice, s0.stream));
+      XP_CUDA(c, cudaMemcpyAsync(c->y_dev, c->y_stage, yb, cudaMemcpyDeviceToDevice, s0.stream));
+      XP_CUDA(c, cudaEventRecord(c->ev_stage_free, s0.stream));
+    } else {
+      XP_CUDA(c, cudaMemcpyAsync(c->x_dev, x, xb, dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 s0.stream));
+      XP_CUDA(c, cudaMemcpyAsync(c->y_dev, y, yb, dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 s0.stream));
+    }
     XP_CUDA(c, cudaMemsetAsync(c->loss_dev, 0xff, (size_t)M * c->T * 4, s0.stream));  // NaN = not computed
     c->call_first = c->fed + 1;
     c->fed += (int64_t)M * c->T;

@@ -14,8 +14,11 @@ for rep in $(seq ${REPS:-2}); do for wl in ${WLS:-vgg16 resnet101 inception}; do
   if [ "$rest" != "$lib" ]; then for t in $(echo ${rest#*,} | tr ',' ' '); do
     case $t in --*) args="$args $t";; *) envs="$envs $t";; esac; done; fi
   cp $P/libxpipe_$lib.so $P/libxpipe.so
-  env $envs timeout 600 python bench.py --workload $wl --steps ${STEPS:-8} --warmup 3 --no-cpu-baseline --no-e2e --no-sweep $BARGS $args > $out/b_$name.log 2>&1
-  echo "rep$rep $wl $name rc=$? $(grep -o '"value": [0-9.]*' $out/b_$name.log | head -1)" >> $out/summary.txt
+  env $envs timeout 600 python bench.py --workload $wl --steps ${STEPS:-8} --warmup 3 ${BASE_ARGS:---no-cpu-baseline --no-e2e --no-sweep} $BARGS $args > $out/b_$name.log 2>&1
+  echo "rep$rep $wl $name rc=$? $(tail -1 $out/b_$name.log | python -c 'import json,sys
+try:
+    d=json.loads(sys.stdin.read()); e=d.get("e2e") or {}; print("value", round(d["value"]), "e2e", e.get("value") and round(e["value"]))
+except Exception as ex: print("failed", ex)')" >> $out/summary.txt
 done; done; done
 cp $P/libxpipe_new.so $P/libxpipe.so
 echo done >> $out/summary.txt

@@ -178,13 +178,14 @@ def test_fp32_graphs_overlap_changing_pinned_inputs(oracle_mod):
     g.close()
 
 
-@pytest.mark.parametrize("timing", [0, 3])
-def test_fp32_async_chained_replays(oracle_mod, timing):
+@pytest.mark.parametrize("timing,host", [(0, False), (3, False), (0, True), (3, True)])
+def test_fp32_async_chained_replays(oracle_mod, timing, host):
     """Asynchronous calls (XP_ASYNC) whose graph replays chain on the device without a host wait
-    (the bench's timed loop): every call's inputs are distinct device tensors and its losses go
-    to a pinned buffer by an asynchronous copy; weights bit-exact with the oracle after the flush
-    and the losses equal the oracle's.  timing=3: every third call is stamped and completes
-    synchronously in between."""
+    (the bench's timed loop): every call's inputs are distinct device tensors (host=True: distinct
+    pinned host buffers -- the e2e loop -- whose H2D copies are staged on the copy stream while the
+    previous call's graph runs) and its losses go to a pinned buffer by an asynchronous copy;
+    weights bit-exact with the oracle after the flush and the losses equal the oracle's.
+    timing=3: every third call is stamped and completes synchronously in between."""
     from paper_1911_04610_b200 import XPipe
     L = S.mlp()
     P = S.make_params(L, 1)
@@ -193,12 +194,18 @@ def test_fp32_async_chained_replays(oracle_mod, timing):
     x, y = S.make_inputs(M * N, (784, 1, 1), 10, 7, kind="mnist")
     g = XPipe(L, K, T, N, 1e-4, (0.9, 0.999), 1e-8, (784, 1, 1), 10, params=P, precision="fp32", graphs=True,
               fb_overlap=True, timing=timing, watchdog_ms=60000)
-    xs = [torch.from_numpy(x[i * C * N:(i + 1) * C * N].copy()).cuda() for i in range(calls)]
-    ys = [torch.from_numpy(y[i * C * N:(i + 1) * C * N].copy()).cuda() for i in range(calls)]
+    xs = [torch.from_numpy(x[i * C * N:(i + 1) * C * N].copy()) for i in range(calls)]
+    ys = [torch.from_numpy(y[i * C * N:(i + 1) * C * N].copy()) for i in range(calls)]
+    if host:  # pinned host buffers (kept alive until the sync below), passed as numpy views
+        xs = [t.pin_memory() for t in xs]
+        ys = [t.pin_memory() for t in ys]
+        xs_arg, ys_arg = [t.numpy() for t in xs], [t.numpy() for t in ys]
+    else:
+        xs_arg, ys_arg = [t.cuda() for t in xs], [t.cuda() for t in ys]
     outs = [torch.full((C * T,), float("nan")).pin_memory() for _ in range(calls)]
     replays = 0
     for i in range(calls):
-        g.step(xs[i], ys[i], C, async_=True, loss_out=outs[i])
+        g.step(xs_arg[i], ys_arg[i], C, async_=True, loss_out=outs[i])
         replays += g.last_stats.graph_replays
     g.sync()
     g.step(x[:0], y[:0], 0, flush=True)

@@ -656,9 +656,13 @@ __device__ __forceinline__ Work work_of(const GemmArgs& a, int j, int mt) {
   return w;
 }
 
-template <int MODE, int BN, bool A_MN, bool B_MN, bool XS>
+// V (kernel variant): 0 = all-TMA operands, no split-K / fused BN; 1 = all-TMA with them;
+// 2 = general (the cp.async gather producer too).  Each launch takes the smallest variant that
+// serves it: the unused paths are not compiled in, so the instructions a variant fetches stay few
+template <int MODE, int BN, bool A_MN, bool B_MN, int V>
 __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* tmA, const CUtensorMap* tmB, uint32_t base,
                                          uint32_t full0, uint32_t empty0, int nunits, int mt, int tid) {
+  constexpr bool XS = V != 0;
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
   Ring ring(a.stages);
   if (MODE == GEMM_FPROP && a.a_tma == 3) {
@@ -754,6 +758,7 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
     }
     return;
   }
+  if constexpr (V != 2) return;  // the all-TMA variants have no gather producer
   // cp.async gather of A (and of B unless b_tma): the full barrier of k-block g is arrived
   // once its group has landed, LAG groups later (stages >= LAG + 1 keeps the ring live)
   constexpr int LAG = 3;
@@ -824,9 +829,10 @@ __device__ __forceinline__ void producer(const GemmArgs& a, const CUtensorMap* t
   for (; arrived < issued; ++arrived, arr.next()) mbar_arrive(full0 + 8 * arr.slot);
 }
 
-template <int MODE, int BN, bool A_MN, bool B_MN, bool XS>
+template <int MODE, int BN, bool A_MN, bool B_MN, int V>
 __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, const __grid_constant__ CUtensorMap tmA,
                                                                const __grid_constant__ CUtensorMap tmB) {
+  constexpr bool XS = V != 0;
   extern __shared__ uint8_t smem_raw[];
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
   const int ST = a.stages;
@@ -875,7 +881,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
   if (a.dbg && tid == 0) a.dbg[cta * 16 + 0] = gtimer();
 
   if (warp < 4) {
-    producer<MODE, BN, A_MN, B_MN, XS>(a, &tmA, &tmB, base, full0, empty0, nunits, mt, tid);
+    producer<MODE, BN, A_MN, B_MN, V>(a, &tmA, &tmB, base, full0, empty0, nunits, mt, tid);
     __syncwarp();  // reconverge (the TMA producer is one thread) before the aligned barriers
   } else if (warp == 4) {
     if (lane == 0) {
@@ -1308,12 +1314,11 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   constexpr int DEEP = std::min(8, (kMaxSmem - 2048) / STAGE);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, DEEP * STAGE + 1024 + 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             DEEP * STAGE + 1024 + 1024);
-    if (e != cudaSuccess) return e;
+    for (auto kern : {tc_gemm_kernel<MODE, BN, A_MN, B_MN, 0>, tc_gemm_kernel<MODE, BN, A_MN, B_MN, 1>,
+                      tc_gemm_kernel<MODE, BN, A_MN, B_MN, 2>}) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DEEP * STAGE + 1024 + 1024);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
   const int mt = (a.M + BM - 1) / BM, nt = (a.N + BN - 1) / BN;
@@ -1370,10 +1375,13 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   if (splits <= 1) grid = dim3(std::max(1, std::min(mt * nt, pmult * num_sms())), 1, 1);
   else grid = dim3(mt, nt, splits);
   const int SMEM = args.stages * STAGE + 1024 + 1024;  // ring + alignment + barriers/BN exchange
+  // the variant of a split / cluster launch: all-TMA (1) or with the gather producer (2)
+  auto* const kern_x = args.a_tma ? tc_gemm_kernel<MODE, BN, A_MN, B_MN, 1> : tc_gemm_kernel<MODE, BN, A_MN, B_MN, 2>;
   if (args.bnf) {  // one cluster of mt CTAs per N tile (the caller checked mt <= 16 and residency)
     static bool np_attr = false;
     if (!np_attr) {
-      cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(tc_gemm_kernel<MODE, BN, A_MN, B_MN, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       np_attr = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -1390,10 +1398,14 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     cfg.gridDim = dim3(mt, nt, 1);
     args.splits = 1; args.cs = 1; args.nc = 1;
     args.kb_per_split = std::max(1, (a.K + BK - 1) / BK);
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>, args, tmA, tmB);
+    return cudaLaunchKernelEx(&cfg, args.a_tma ? tc_gemm_kernel<MODE, BN, A_MN, B_MN, 1> : tc_gemm_kernel<MODE, BN, A_MN, B_MN, 2>,
+                              args, tmA, tmB);
   }
   if (splits <= 1) {
-    launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN, false>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);
+    if (args.a_tma)
+      launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN, 0>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);
+    else
+      launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN, 2>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -1416,7 +1428,7 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     at[1].val.clusterDim.z = cs;
     cfg.gridDim = dim3(mt, nt, cs);
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>, &cfg) != cudaSuccess || n <= 0)
+    if (cudaOccupancyMaxActiveClusters(&n, kern_x, &cfg) != cudaSuccess || n <= 0)
       n = 1 << 20;  // unknown: do not constrain
     cudaGetLastError();
     maxc_cache[cs] = n;
@@ -1438,7 +1450,7 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   args.kb_per_split = (nkb + args.splits - 1) / args.splits;
   at[1].val.clusterDim.z = args.cs;
   cfg.gridDim = dim3(mt, nt, args.splits);
-  return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<MODE, BN, A_MN, B_MN, true>, args, tmA, tmB);
+  return cudaLaunchKernelEx(&cfg, kern_x, args, tmA, tmB);
 }
 
 template <int MODE, bool A_MN, bool B_MN>
@@ -1547,7 +1559,7 @@ bool bnf_resident(int mt, const GemmArgs& a) {
   if (it != cache.end()) return it->second;
   constexpr int STAGE = BM * BK * 2 + BN * BK * 2;
   const int SMEM = std::max(4, persist_stages()) * STAGE + 2048;
-  auto kern = tc_gemm_kernel<GEMM_FPROP, BN, false, false, true>;
+  auto kern = tc_gemm_kernel<GEMM_FPROP, BN, false, false, 1>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(8, (kMaxSmem - 2048) / STAGE) * STAGE + 2048);
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};

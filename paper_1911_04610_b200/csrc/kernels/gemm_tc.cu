@@ -390,14 +390,24 @@ __device__ __forceinline__ int64_t out_row(const GemmArgs& a, int row) {
 
 // the epilogue kind is fixed by the mode for the conv GEMMs (fprop / dgrad: bf16 rows, wgrad: the
 // transposed fp32 gradient), so only the plain GEMM instantiations carry every store path
-template <int MODE>
+// The plain GEMMs of the pipeline fix it by their operand majors (A K-major, B MN-major: the 1x1
+// dgrad, bf16; A MN-major, B K-major: the Linear dgrad, transposed; both MN-major: weight
+// gradients; both K-major: 1x1 / im2col fprop, bf16, or the Linear forward); the fp32 store of
+// the unit GEMM entry is compiled into the general variant (V = 2) only
+template <int MODE, bool A_MN, bool B_MN, int V>
 __device__ __forceinline__ int epi_kind(const GemmArgs& a) {
-  return (MODE == GEMM_FPROP || MODE == GEMM_DGRAD) ? EPI_BF16 : (MODE == GEMM_WGRAD ? EPI_WGRAD_T : a.epi);
+  if (MODE == GEMM_FPROP || MODE == GEMM_DGRAD) return EPI_BF16;
+  if (MODE == GEMM_WGRAD) return EPI_WGRAD_T;
+  if (V == 2) return a.epi;
+  if (!A_MN && B_MN) return EPI_BF16;
+  if (A_MN && !B_MN) return EPI_LINEAR_T;
+  if (A_MN && B_MN) return EPI_WGRAD_T;
+  return a.epi == EPI_LINEAR_T ? EPI_LINEAR_T : EPI_BF16;
 }
-template <int MODE>
+template <int MODE, bool A_MN, bool B_MN, int V>
 __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, uint32_t (&v)[32]) {
   if (row >= a.M) return;
-  const int epi = epi_kind<MODE>(a);
+  const int epi = epi_kind<MODE, A_MN, B_MN, V>(a);
   if (epi == EPI_BF16) {
     bf16* o = static_cast<bf16*>(a.out) + out_row(a, row) * a.ldo + col0;
     if (a.accumulate) {  // fan-out tensor: out = Q(old + Q(acc)) (the oracle's rounding points)
@@ -484,9 +494,9 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int row, int col0, 
 }
 
 // 8 consecutive columns [col0, col0+8) of row `row` (split-K reduction output)
-template <int MODE>
+template <int MODE, bool A_MN, bool B_MN, int V>
 __device__ __forceinline__ void epi_store8(const GemmArgs& a, int row, int col0, const float (&v)[8]) {
-  const int epi = epi_kind<MODE>(a);
+  const int epi = epi_kind<MODE, A_MN, B_MN, V>(a);
   if (epi == EPI_BF16) {
     bf16* o = static_cast<bf16*>(a.out) + out_row(a, row) * a.ldo + col0;
     if (!a.accumulate && col0 + 8 <= a.N) {
@@ -933,7 +943,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = 0u;
           }
-          if (w.n0 + c0 < a.N) epi_store<MODE>(a, row, w.n0 + c0, v);
+          if (w.n0 + c0 < a.N) epi_store<MODE, A_MN, B_MN, V>(a, row, w.n0 + c0, v);
           if ((MODE == GEMM_FPROP || MODE == GEMM_PLAIN) && (a.bn_part || (XS && a.bnf)) && w.n0 + c0 < a.N) {
             // BatchNorm partials of this tile's 32 columns over its valid rows, from the stored
             // (bf16-rounded) values: tile mean, then the sum of squared deviations (two passes;
@@ -1070,7 +1080,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
           for (int e = 0; e < 8; ++e) acc[e] = src ? __fadd_rn(acc[e], x[e]) : x[e];
         }
       if (nc == 1) {
-        epi_store8<MODE>(a, gr, gc, acc);
+        epi_store8<MODE, A_MN, B_MN, V>(a, gr, gc, acc);
       } else {
         float4* d = reinterpret_cast<float4*>(wsp + lr * BN + ch * 8);
         __stcg(d, make_float4(acc[0], acc[1], acc[2], acc[3]));
@@ -1118,7 +1128,7 @@ __global__ void __maxnreg__(XP_GEMM_MAXREG) tc_gemm_kernel(const GemmArgs a, con
                 for (int e = 0; e < 8; ++e) acc[e] = (c0 + u) ? __fadd_rn(acc[e], x[e]) : x[e];
               }
           }
-          epi_store8<MODE>(a, gr, gc, acc);
+          epi_store8<MODE, A_MN, B_MN, V>(a, gr, gc, acc);
         }
       }
     }
@@ -1375,8 +1385,10 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
   if (splits <= 1) grid = dim3(std::max(1, std::min(mt * nt, pmult * num_sms())), 1, 1);
   else grid = dim3(mt, nt, splits);
   const int SMEM = args.stages * STAGE + 1024 + 1024;  // ring + alignment + barriers/BN exchange
-  // the variant of a split / cluster launch: all-TMA (1) or with the gather producer (2)
-  auto* const kern_x = args.a_tma ? tc_gemm_kernel<MODE, BN, A_MN, B_MN, 1> : tc_gemm_kernel<MODE, BN, A_MN, B_MN, 2>;
+  // the general variant (2) for the cp.async gather producer and the unit entry's fp32 store;
+  // else all-TMA, with (1) or without (0) the split-K / cluster paths
+  const bool general = !args.a_tma || args.epi == EPI_F32;
+  auto* const kern_x = general ? tc_gemm_kernel<MODE, BN, A_MN, B_MN, 2> : tc_gemm_kernel<MODE, BN, A_MN, B_MN, 1>;
   if (args.bnf) {  // one cluster of mt CTAs per N tile (the caller checked mt <= 16 and residency)
     static bool np_attr = false;
     if (!np_attr) {
@@ -1398,11 +1410,10 @@ cudaError_t launch(const GemmArgs& a, int splits, cudaStream_t st) {
     cfg.gridDim = dim3(mt, nt, 1);
     args.splits = 1; args.cs = 1; args.nc = 1;
     args.kb_per_split = std::max(1, (a.K + BK - 1) / BK);
-    return cudaLaunchKernelEx(&cfg, args.a_tma ? tc_gemm_kernel<MODE, BN, A_MN, B_MN, 1> : tc_gemm_kernel<MODE, BN, A_MN, B_MN, 2>,
-                              args, tmA, tmB);
+    return cudaLaunchKernelEx(&cfg, kern_x, args, tmA, tmB);
   }
   if (splits <= 1) {
-    if (args.a_tma)
+    if (!general)
       launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN, 0>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);
     else
       launch_pdl(tc_gemm_kernel<MODE, BN, A_MN, B_MN, 2>, grid, dim3(NTHREADS), SMEM, st, args, tmA, tmB);

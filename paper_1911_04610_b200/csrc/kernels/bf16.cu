@@ -89,6 +89,7 @@ __device__ __forceinline__ void chan_merge(float& na, float& mean, float& m2, fl
 #define XP_BN_ROWS 8
 #endif
 constexpr int kBnRows = XP_BN_ROWS;
+constexpr int kFinalU = 2;  // partial loads in flight per lane in the final merges
 
 // fixed-order tree over the RL row lanes of slot [rl][G][W] (W floats per (lane, group));
 // the result lands in lane 0.  Every thread of the block must call it.
@@ -184,16 +185,18 @@ __device__ __forceinline__ void stats_final_body(const float* __restrict__ part,
   const int cc = threadIdx.x & 7, j = (threadIdx.x >> 3) & 31, c = unit * 8 + cc;
   float na = 0.f, mean = 0.f, m2 = 0.f;
   if (act && c < C) {
-    for (int k = j; k < chunks; k += 8 * 32) {
-      float mb[8], qb[8];
+    // loads batched kFinalU deep (the ~64 partials of a layer are two per lane; a deeper batch
+    // only adds predicated code to fetch), merged in chunk order j, j+32, ...
+    for (int k = j; k < chunks; k += kFinalU * 32) {
+      float mb[kFinalU], qb[kFinalU];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kFinalU; ++u) {
         const int kk = k + 32 * u;
         mb[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + c) : 0.f;
         qb[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + C + c) : 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kFinalU; ++u) {
         const int kk = k + 32 * u;
         if (kk < chunks) chan_merge(na, mean, m2, (float)min(RC, M - kk * RC), mb[u], qb[u]);
       }
@@ -471,16 +474,16 @@ __device__ __forceinline__ void bwd_final_body(const float* __restrict__ part, i
   const int cc = threadIdx.x & 7, j = (threadIdx.x >> 3) & 31, c = unit * 8 + cc;
   float s1 = 0.f, s2 = 0.f;
   if (act && c < C) {
-    for (int k = j; k < chunks; k += 8 * 32) {
-      float a[8], b[8];
+    for (int k = j; k < chunks; k += kFinalU * 32) {
+      float a[kFinalU], b[kFinalU];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kFinalU; ++u) {
         const int kk = k + 32 * u;
         a[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + c) : 0.f;
         b[u] = kk < chunks ? __ldcg(part + (size_t)kk * 2 * C + C + c) : 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < kFinalU; ++u)
         if (k + 32 * u < chunks) { s1 = __fadd_rn(s1, a[u]); s2 = __fadd_rn(s2, b[u]); }
     }
   }
